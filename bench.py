@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark: stereo pairs/s of the full per-frame stereo chain on B200.
+
+Metric (BASELINE.json): stereo pairs/sec at 960x540 D=64, 1/2/4/8 B200.
+Workload (BASELINE.json configs[3], "C4"): every rank processes a batch of
+256 synthetic textured 960x540 pairs per step, d in [0, 63], the whole
+run_stereo_only chain: luma -> ZNCC WTA -> 3 rounds of
+outlier removal + hole filling -> 10 refinement iterations -> oriented point
+cloud (points, normals, colours). Frames shard across ranks with no collective
+(weak scaling); NCCL only carries the barrier and the max-over-ranks time.
+
+  value  device-resident throughput: inputs already in HBM, results written to
+         device output tensors; CUDA events on the ctx stream, max over ranks.
+  e2e    the same through the public host API (ss_stereo_batch): pinned host
+         RGB in, H2D + chain + D2H of disparity/validity/cloud inside the timed
+         region.
+  roofline  dominant kernel = the ZNCC cost sweep (k_wta11): algorithmic
+         lane-ops per launch (SURVEY.md §8d census: 12 N (D+10) + 3 N D per
+         frame) / its CUDA-event duration vs the ALU issue peak
+         (148 SM x 128 lanes x sm_max_mhz).
+  cpu_baseline  the reference itself (oracle/_ref, compiled from
+         /root/reference by oracle/Makefile) on the host cores, bounded sample.
+
+`--impl reference` runs only that reference CPU path (rank 0) on the same
+metric and config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+W, H, D = 960, 540, 64
+CENSUS = {"textured": 2.16e9, "lowtex": 2.25e9, "fhd": 10.6e9}  # lane-ops/pair, BASELINE.md
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--frames", type=int, default=256, help="pairs per rank per step")
+    ap.add_argument("--batch", type=int, default=16, help="frames per device launch")
+    ap.add_argument("--unique", type=int, default=32, help="distinct seeded frames (tiled)")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-pairs", type=int, default=2)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-i", str(self.device), "-lms", "100"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, p in zip(names, parts[2:]):
+                if p.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_frames(rank, frames, unique):
+    from paper_2007_12623_b200.synth import as_rgb, stereo_pair
+    u = max(1, min(unique, frames))
+    Ls, Rs = [], []
+    for i in range(u):
+        L, R, _ = stereo_pair("textured", W, H, D, seed=rank * frames + i)
+        Ls.append(as_rgb(L))
+        Rs.append(as_rgb(R))
+    Ls, Rs = np.stack(Ls), np.stack(Rs)
+    reps = (frames + u - 1) // u
+    return np.tile(Ls, (reps, 1, 1, 1))[:frames], np.tile(Rs, (reps, 1, 1, 1))[:frames]
+
+
+def reference_chain(pairs):
+    """The reference's own CPU path (oracle/_ref) on host pairs; cloud stage from
+    the restatement (the reference's needs Eigen, absent). Returns seconds."""
+    from oracle.oracle import Oracle
+    from paper_2007_12623_b200.synth import default_rig, params_for
+    kind = "reference" if Oracle.available("ref") else "port"
+    ref = Oracle("ref" if kind == "reference" else "orc")
+    orc = Oracle("orc")
+    p = params_for(D)
+    rig = default_rig(W, H)
+    t0 = time.perf_counter()
+    for L, R in pairs:
+        lg, rg = ref.to_gray(L), ref.to_gray(R)
+        d, v = ref.compute_disparity(lg, rg, p)
+        d, v = ref.cleanup_pass(d, v, p)
+        d, v = ref.refine_disparities(d, v, lg, rg, p)
+        orc.disparity_to_cloud(d, v, L, rig)
+    return time.perf_counter() - t0, kind
+
+
+def cpu_pairs(n):
+    from paper_2007_12623_b200.synth import as_rgb, stereo_pair
+    out = []
+    for i in range(n):
+        L, R, _ = stereo_pair("textured", W, H, D, seed=i)
+        out.append((as_rgb(L), as_rgb(R)))
+    return out
+
+
+def config_dict(args, world):
+    return {"workload": "C4: 256 synthetic textured 960x540 stereo pairs per rank per step, "
+                        "D=64 (d 0..63), full chain luma+WTA+cleanup+refine+cloud(normals)",
+            "width": W, "height": H, "disparities": D, "pairs_per_step_per_gpu": args.frames,
+            "frames_per_launch": args.batch, "unique_seeded_frames": min(args.unique, args.frames),
+            "cache": "inputs > L2 (per-step input 796 MB RGB per GPU; 153 MB/frame cost volume)",
+            "parallelism": f"frame-shard x{world}, no collective"}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    pairs = cpu_pairs(1)
+    times = []
+    kind = "reference"
+    for i in range(args.warmup + args.steps):
+        t, kind = reference_chain(pairs)
+        if i >= args.warmup:
+            times.append(t)
+    total = sum(times)
+    value = len(times) / total
+    cores = os.cpu_count()
+    line = {
+        "metric": "stereo pairs/sec at 960x540 D=64", "value": value, "unit": "pairs/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8/int64/f64", "data": "synthetic",
+        "config": config_dict(args, world), "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores, "kind": kind,
+                         "sample": "1 C1 pair per step through oracle/_ref (unmodified reference "
+                                   "matcher/cleanup/smoothing, OpenMP all cores) + restated cloud"},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2007_12623_b200 as ss
+    from paper_2007_12623_b200.synth import default_rig, params_for
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    F, B = args.frames, args.batch
+    N = W * H
+    Lh_np, Rh_np = make_frames(rank, F, args.unique)
+    # pinned host inputs (e2e) and HBM-resident copies (device value)
+    Lh = torch.from_numpy(Lh_np).pin_memory()
+    Rh = torch.from_numpy(Rh_np).pin_memory()
+    Ld, Rd = Lh.to(dev), Rh.to(dev)
+    del Lh_np, Rh_np
+    flags = ss.SS_OUT_DISPARITY | ss.SS_OUT_CLOUD | ss.SS_OUT_NORMALS
+    od = {"disparity": torch.empty((F, H, W), dtype=torch.float32, device=dev),
+          "valid": torch.empty((F, H, W), dtype=torch.uint8, device=dev),
+          "index": torch.empty((F, H, W), dtype=torch.int32, device=dev),
+          "points": torch.empty((F, N, 3), dtype=torch.float32, device=dev),
+          "normals": torch.empty((F, N, 3), dtype=torch.float32, device=dev),
+          "colors": torch.empty((F, N, 3), dtype=torch.uint8, device=dev),
+          "n_points": torch.empty((F,), dtype=torch.int32, device=dev)}
+    p = params_for(D)
+    ctx = ss.StereoContext(local, W, H, B, ss.StereoParams(**p), ss.StereoRig(**default_rig(W, H)))
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+
+    def step_device():
+        for f0 in range(0, F, B):
+            m = min(B, F - f0)
+            d_out = {k: t[f0:f0 + m].data_ptr() for k, t in od.items()}
+            ctx.run_device(m, W, H, Ld[f0].data_ptr(), Rd[f0].data_ptr(), flags, d_out=d_out)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        ctx.sync()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step_device()
+    barrier()
+    ctx.reset_stats()
+    ctx.enable_timing(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_device()
+        e1.record(stream)
+        e1.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    stages = ctx.stage_times()
+    stats = ctx.stats()
+    ctx.enable_timing(False)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    pairs = world * F * args.steps
+    value = pairs / (ms_max / 1000.0)
+
+    # ---- e2e through the public host API (pinned host buffers) ----
+    ho = ss.StereoContext.alloc_outputs(F, H, W, flags,
+                                        alloc=lambda s, dt: ss.pinned_empty(s, dt))
+    ctx.run(Lh.numpy()[:B], Rh.numpy()[:B], flags,
+            out={k: v[:B] for k, v in ho.items()})  # warm the host path
+    barrier()
+    f0e, f1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0e.record(stream)
+    for _ in range(args.e2e_steps):
+        ctx.run(Lh.numpy(), Rh.numpy(), flags, out=ho)
+    f1e.record(stream)
+    f1e.synchronize()
+    barrier()
+    ems = f0e.elapsed_time(f1e)
+    te = torch.tensor([ems], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * F * args.e2e_steps / (float(te.item()) / 1000.0)
+    npts = int(ho["n_points"].sum())
+    h2d = 2 * F * N * 3
+    d2h = F * N * (4 + 1 + 4) + 4 * F + npts * (12 + 12 + 3)
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        ctx.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {}
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    alu_peak = n_sm * 128 * sm_max * 1e6  # lane-ops/s
+    wta_ms, wta_launches = stages["wta_sweep"]
+    per_frame_ops = N * (12 * (D + 10) + 3 * D)
+    launches = max(wta_launches, 1)
+    frames_timed = F * args.steps
+    ops_per_launch = per_frame_ops * frames_timed / launches
+    achieved = ops_per_launch / (wta_ms / launches / 1000.0) if wta_ms > 0 else 0.0
+    hbm_peak = float(peaks.get("hbm_gbs", 6446.9))
+    roofline = {
+        "bound": "alu", "kernel": "k_wta11 (ZNCC cost sweep + WTA)",
+        "achieved": achieved / 1e12, "peak": alu_peak / 1e12, "unit": "Tlane-op/s",
+        "frac": achieved / alu_peak if alu_peak else None, "traffic": None,
+        "peak_source": f"{n_sm} SM x 128 lanes x sm_max_mhz {sm_max:.0f} (MEASURED_PEAKS.json); "
+                       "ALU issue, not a bf16/HBM figure: the path is integer/FP64 ALU work",
+        "ops_per_launch": ops_per_launch, "avg_launch_ms": wta_ms / launches,
+        "pipeline_census_frac": CENSUS["textured"] * value / world / alu_peak,
+        "hbm_frac_pipeline": 21.8e6 * value / world / (hbm_peak * 1e9),
+    }
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        pairs_cpu = cpu_pairs(args.cpu_pairs)
+        tcpu, kind = reference_chain(pairs_cpu)
+        cpu = {"value": len(pairs_cpu) / tcpu, "unit": "pairs/s", "cores": os.cpu_count(),
+               "kind": kind,
+               "sample": f"{len(pairs_cpu)} C1 pairs (960x540 D=64) through oracle/_ref "
+                         "(unmodified reference, OpenMP all cores) + restated cloud"}
+    stage_ms_per_pair = {k: v[0] / frames_timed for k, v in stages.items()}
+    line = {
+        "metric": "stereo pairs/sec at 960x540 D=64", "value": value, "unit": "pairs/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8/int32/f32-filter/f64", "data": "synthetic",
+        "config": config_dict(args, world),
+        "ms_per_pair": ms_max / args.steps / F,
+        "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(stats["kernel_launches"]),
+        "roofline": roofline, "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "stage_ms_per_pair": stage_ms_per_pair,
+        "exact_resolves": {"wta_pixels": stats["wta_resolved"],
+                           "refine_repicks": stats["refine_resolved"],
+                           "frames": stats["frames"]},
+    }
+    print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

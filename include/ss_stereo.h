@@ -1,0 +1,199 @@
+/*
+ * ss_stereo.h — C-ABI of the B200-native per-frame dense stereo path.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/include/stereoscan/stereo/*.hpp). Every entry point
+ * takes plain pointers and sizes; no C++ or torch types cross it. The C++
+ * header tree include/stereoscan/ re-declares the reference's functions on top
+ * of these calls (INTEGRATION.md shows the reference-side binding).
+ *
+ *   ss_to_gray              replaces to_gray             image.hpp:44, matcher.cpp:21-30
+ *   ss_compute_disparity    replaces compute_disparity   matcher.hpp:35-36, matcher.cpp:166-211
+ *   ss_remove_outliers      replaces remove_outliers     cleanup.hpp:12, cleanup.cpp:12-42
+ *   ss_fill_holes           replaces fill_holes          cleanup.hpp:21-22, cleanup.cpp:44-92
+ *   ss_cleanup_pass         replaces cleanup_pass        cleanup.hpp:32, cleanup.cpp:111-123
+ *   ss_refine_disparities   replaces refine_disparities  smoothing.hpp:22-24, smoothing.cpp:68-159
+ *   ss_disparity_to_cloud   replaces disparity_to_cloud  cloud.hpp:34-35, cloud.cpp:14-94
+ *   ss_params_validate      replaces StereoParams::validate  params.hpp:23, matcher.cpp:9-19
+ *   ss_rig_validate         replaces StereoRig::validate     types.hpp:39, geometry.cpp:7-19
+ *
+ * Throughput entry (no reference analogue): ss_ctx_* run the
+ * whole run_stereo_only chain for a batch of frames on one
+ * GPU, device-resident between stages.
+ *
+ * Errors: functions return ss_status; on failure ss_last_error() holds the
+ * message for the calling thread. SS_EINVAL maps to std::invalid_argument and
+ * SS_EPARAM to stereoscan::Error in the C++ layer (same messages as the
+ * reference). There is no CPU fallback: without a CUDA device every compute
+ * entry point returns SS_ENODEV.
+ */
+#ifndef SS_STEREO_H
+#define SS_STEREO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t ss_status;
+#define SS_OK 0
+#define SS_EINVAL 1   /* contract violation   -> std::invalid_argument */
+#define SS_EPARAM 2   /* parameter/geometry   -> stereoscan::Error      */
+#define SS_ECUDA 3    /* CUDA runtime failure                           */
+#define SS_ENOMEM 4   /* device allocation failure                      */
+#define SS_ENODEV 5   /* no CUDA device: the path refuses to run on CPU */
+
+/* Field-for-field stereoscan::StereoParams (params.hpp:7-24). */
+typedef struct ss_stereo_params {
+  int32_t window;                  /* 11 */
+  int32_t d_min;                   /* -20 */
+  int32_t d_max;                   /* 80 */
+  double neighbor_jump_threshold;  /* 2.5 */
+  int32_t outlier_radius_start;    /* 10 */
+  int32_t outlier_radius_step;     /* 10 */
+  int32_t cleanup_iterations;      /* 3 */
+  int32_t fill_radius_radial;      /* 50 */
+  int32_t fill_radius_disc;        /* 20 */
+  int32_t smoothing_radius;        /* 15 */
+  double alpha;                    /* 0.1 */
+  double eta_smooth;               /* 0.01 */
+  int32_t refine_iterations;       /* 10 */
+  double min_zncc;                 /* 0.5 */
+} ss_stereo_params;
+
+/* CameraIntrinsics + StereoRig (types.hpp:23-40). */
+typedef struct ss_stereo_rig {
+  double fx, fy, cx, cy;
+  int32_t width, height;
+  double baseline_mm;
+} ss_stereo_rig;
+
+/* fill_holes modes (cleanup.hpp:14). */
+#define SS_FILL_RADIAL 0
+#define SS_FILL_DISC 1
+
+const char* ss_last_error(void);
+const char* ss_version(void);
+void ss_params_default(ss_stereo_params* p);
+ss_status ss_params_validate(const ss_stereo_params* p);
+ss_status ss_rig_validate(const ss_stereo_rig* rig);
+int32_t ss_disc_neighbor_count(int32_t radius);    /* cleanup.cpp:94-104 */
+int32_t ss_disc_fill_min_support(int32_t radius);  /* cleanup.cpp:106-109 */
+int32_t ss_device_count(void);
+
+/* ---- per-stage drop-ins: host buffers in, host buffers out (synchronous) ---- */
+
+ss_status ss_to_gray(const uint8_t* rgb, int32_t w, int32_t h, uint8_t* gray);
+
+ss_status ss_compute_disparity(const ss_stereo_params* p, const uint8_t* left, int32_t lw,
+                               int32_t lh, const uint8_t* right, int32_t rw, int32_t rh,
+                               float* disparity, uint8_t* valid);
+
+ss_status ss_remove_outliers(const float* disparity, const uint8_t* valid, int32_t w,
+                             int32_t h, int32_t radius, double threshold, float* out_disparity,
+                             uint8_t* out_valid);
+
+ss_status ss_fill_holes(const float* disparity, const uint8_t* valid, int32_t w, int32_t h,
+                        int32_t mode, int32_t radius, int32_t min_support,
+                        float* out_disparity, uint8_t* out_valid);
+
+ss_status ss_cleanup_pass(const ss_stereo_params* p, const float* disparity,
+                          const uint8_t* valid, int32_t w, int32_t h, float* out_disparity,
+                          uint8_t* out_valid);
+
+/* trace_discrete / trace_smooth: NULL or refine_iterations * w * h doubles,
+ * the RefineTrace snapshots of smoothing.hpp:10-13 (smoothing.cpp:148-151). */
+ss_status ss_refine_disparities(const ss_stereo_params* p, const float* disparity,
+                                const uint8_t* valid, int32_t w, int32_t h,
+                                const uint8_t* left, int32_t lw, int32_t lh,
+                                const uint8_t* right, int32_t rw, int32_t rh,
+                                float* out_disparity, uint8_t* out_valid,
+                                double* trace_discrete, double* trace_smooth);
+
+/* StereoCloud (cloud.hpp:14-29): index[w*h]; per point (capacity w*h):
+ * points xyz, normals xyz (double), colors rgb, pixels (u,v). */
+ss_status ss_disparity_to_cloud(const float* disparity, const uint8_t* valid, int32_t w,
+                                int32_t h, const uint8_t* rgb, int32_t cw, int32_t ch,
+                                const ss_stereo_rig* rig, int32_t* index, double* points,
+                                double* normals, uint8_t* colors, int32_t* pixels,
+                                int32_t* n_points);
+
+/* ---- throughput API: a batch of frames through the whole chain on one GPU ---- */
+
+typedef struct ss_ctx ss_ctx;
+
+#define SS_IN_RGB 0   /* interleaved 8-bit RGB, luma by to_gray */
+#define SS_IN_GRAY 1  /* 8-bit gray */
+
+#define SS_OUT_DISPARITY 1u  /* disparity (f32) + valid (u8) per pixel */
+#define SS_OUT_CLOUD 2u      /* packed cloud: index, points f32x3, colors */
+#define SS_OUT_NORMALS 4u    /* normals f32x3 (needs SS_OUT_CLOUD) */
+
+/* Per-batch outputs. Host pointers for ss_stereo_batch, device pointers for
+ * ss_stereo_batch_device. Arrays are frame-major: frame f of n starts at
+ * f*w*h (index, disparity, valid) or f*w*h*3 (points, normals, colors).
+ * Points of a frame are packed in raster order (cloud.cpp:23-39). */
+typedef struct ss_batch_out {
+  float* disparity;
+  uint8_t* valid;
+  int32_t* index;
+  float* points;
+  float* normals;
+  uint8_t* colors;
+  int32_t* n_points; /* n entries */
+} ss_batch_out;
+
+typedef struct ss_ctx_stats {
+  int64_t frames;            /* frames processed */
+  int64_t wta_resolved;      /* pixels whose WTA pick went through the exact FP64 resolve */
+  int64_t refine_resolved;   /* (pixel, iteration) re-picks resolved in exact FP64 */
+  int64_t refine_fallback;   /* (pixel, iteration) re-picks recomputed without the cost volume */
+  int64_t kernel_launches;   /* kernels launched by this ctx */
+} ss_ctx_stats;
+
+ss_status ss_ctx_create(int32_t device, int32_t max_w, int32_t max_h, int32_t max_batch,
+                        const ss_stereo_params* p, const ss_stereo_rig* rig, ss_ctx** out);
+ss_status ss_ctx_destroy(ss_ctx* ctx);
+/* cudaStream_t the ctx launches on (as void*). */
+void* ss_ctx_stream(ss_ctx* ctx);
+ss_status ss_ctx_sync(ss_ctx* ctx);
+ss_status ss_ctx_get_stats(ss_ctx* ctx, ss_ctx_stats* st);
+ss_status ss_ctx_reset_stats(ss_ctx* ctx);
+
+/* Per-stage device time (CUDA events on the ctx stream), the Table III-style
+ * RuntimeReport of SPEC.md:566-569 for the stereo stage. Stages:
+ * 0 luma, 1 stats+planes, 2 cost sweep/WTA (k_wta11), 3 FP64 resolve,
+ * 4 cleanup, 5 refine, 6 cloud. Timing is off by default. */
+#define SS_N_STAGES 7
+ss_status ss_ctx_enable_timing(ss_ctx* ctx, int32_t on);
+/* Sums (ms) and launch counts per stage since the last reset; synchronizes. */
+ss_status ss_ctx_stage_times(ss_ctx* ctx, double* ms, int64_t* launches);
+
+/* Whole chain for n frames of w x h from HOST memory (pinned for full speed):
+ * H2D, kernels, D2H on the ctx stream; returns after the outputs landed. */
+ss_status ss_stereo_batch(ss_ctx* ctx, int32_t n, int32_t w, int32_t h, int32_t in_format,
+                          const uint8_t* left, const uint8_t* right, uint32_t out_flags,
+                          const ss_batch_out* out);
+
+/* Same with DEVICE inputs/outputs; asynchronous on `stream` (NULL = ctx
+ * stream). Output device pointers may be NULL to keep results in the ctx's
+ * own buffers (see ss_ctx_device_outputs). */
+ss_status ss_stereo_batch_device(ss_ctx* ctx, int32_t n, int32_t w, int32_t h,
+                                 int32_t in_format, const uint8_t* d_left,
+                                 const uint8_t* d_right, uint32_t out_flags,
+                                 const ss_batch_out* d_out, void* stream);
+
+/* Device pointers of the ctx-owned result buffers of the last batch. */
+ss_status ss_ctx_device_outputs(ss_ctx* ctx, ss_batch_out* d_out);
+
+/* Pinned host memory helpers (cudaHostAlloc / cudaFreeHost). */
+void* ss_host_alloc(size_t bytes);
+void ss_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SS_STEREO_H */

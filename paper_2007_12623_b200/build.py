@@ -1,0 +1,98 @@
+"""Build the sm_100a shared library in-tree (no JIT cache, no pip install).
+
+    python -m paper_2007_12623_b200.build        # or __graft_entry__.build()
+
+Compiles every csrc/*.cu and csrc/*.cpp with nvcc for
+``-gencode arch=compute_100a,code=sm_100a`` into
+``paper_2007_12623_b200/lib/libstereoscan_b200.so`` and the C++ API test
+driver ``tests/cpp/build/test_api``. Objects are rebuilt only when a source or
+header is newer. ``--fmad=false`` is load-bearing: the reference's double
+arithmetic is uncontracted, and so must ours be.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import glob
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INC = os.path.join(ROOT, "include")
+OBJ = os.path.join(PKG, "build")
+LIB_DIR = os.path.join(PKG, "lib")
+LIB = os.path.join(LIB_DIR, "libstereoscan_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CUDA_LIB = "/usr/local/cuda/lib64"
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
+                 "-Xcompiler", "-ffp-contract=off", f"-I{INC}", f"-I{CSRC}",
+                 "-Xptxas", "-warn-spills"]
+
+
+def _deps():
+    return [p for p in glob.glob(os.path.join(CSRC, "*")) if p.endswith((".cuh", ".h"))] + \
+        glob.glob(os.path.join(INC, "**", "*.h*"), recursive=True)
+
+
+def _newer(target, sources):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def _compile(src):
+    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+    if _newer(obj, [src] + _deps()):
+        cmd = [NVCC] + COMMON + ["-c", src, "-o", obj]
+        if src.endswith(".cpp"):
+            cmd = [NVCC] + COMMON + ["-x", "cu", "-c", src, "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+        if r.stderr.strip():
+            sys.stderr.write(r.stderr)
+    return obj
+
+
+def build(verbose: bool = True) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(LIB_DIR, exist_ok=True)
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(_compile, srcs))
+    if _newer(LIB, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "shared", "-o", LIB] + objs + \
+            ["-Xlinker", f"-rpath,{CUDA_LIB}"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+        if verbose:
+            print(f"built {LIB}")
+    _build_cpp_test(verbose)
+    return LIB
+
+
+def _build_cpp_test(verbose):
+    src = os.path.join(ROOT, "tests", "cpp", "test_api.cpp")
+    if not os.path.exists(src):
+        return
+    out_dir = os.path.join(ROOT, "tests", "cpp", "build")
+    os.makedirs(out_dir, exist_ok=True)
+    exe = os.path.join(out_dir, "test_api")
+    if _newer(exe, [src, LIB] + _deps()):
+        cmd = ["g++", "-std=c++17", "-O1", f"-I{INC}", src, "-o", exe, f"-L{LIB_DIR}",
+               "-lstereoscan_b200", f"-Wl,-rpath,{LIB_DIR}", f"-Wl,-rpath,{CUDA_LIB}"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"C++ test build failed:\n{r.stdout}\n{r.stderr}")
+        if verbose:
+            print(f"built {exe}")
+
+
+if __name__ == "__main__":
+    build()

@@ -1,0 +1,53 @@
+// Exact (reference-identical) chessboard ZNCC on the device.
+//
+// zncc_chessboard, matcher.cpp:38-64: int64 statistics over the taps with
+// (du + dv) even, score = double(num) / sqrt(double(var_l * var_r)), IEEE
+// round-to-nearest (CUDA's double sqrt and division are correctly rounded).
+// `wta_semantics` reproduces compute_disparity's patch_stats, which stores
+// sum and var as int32 (matcher.cpp:132-133): identical for window <= 19.
+#pragma once
+
+#include <stdint.h>
+
+namespace ssb {
+
+struct ExactScore {
+  double score;
+  bool defined;
+};
+
+__device__ __forceinline__ ExactScore zncc_exact(const uint8_t* __restrict__ L,
+                                                 const uint8_t* __restrict__ R, int W, int lu,
+                                                 int lv, int ru, int half,
+                                                 bool wta_semantics) {
+  int64_t n = 0, sl = 0, sr = 0, sll = 0, srr = 0, slr = 0;
+  for (int dv = -half; dv <= half; ++dv) {
+    const uint8_t* lr = L + (long)(lv + dv) * W + lu;
+    const uint8_t* rr = R + (long)(lv + dv) * W + ru;
+    for (int du = -half + ((dv + half) & 1); du <= half; du += 2) {
+      const int64_t a = __ldg(lr + du), b = __ldg(rr + du);
+      n += 1;
+      sl += a;
+      sr += b;
+      sll += a * a;
+      srr += b * b;
+      slr += a * b;
+    }
+  }
+  int64_t var_l = n * sll - sl * sl;
+  int64_t var_r = n * srr - sr * sr;
+  int64_t num;
+  if (wta_semantics) {
+    var_l = (int32_t)var_l;
+    var_r = (int32_t)var_r;
+    num = n * slr - (int64_t)(int32_t)sl * (int64_t)(int32_t)sr;
+  } else {
+    num = n * slr - sl * sr;
+  }
+  ExactScore r;
+  r.defined = !(var_l == 0 || var_r == 0);
+  r.score = r.defined ? __ddiv_rn((double)num, __dsqrt_rn((double)(var_l * var_r))) : 0.0;
+  return r;
+}
+
+}  // namespace ssb

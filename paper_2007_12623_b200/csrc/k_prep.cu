@@ -1,0 +1,120 @@
+// Frame preparation kernels: luma, parity planes, chessboard window stats.
+//
+//   k_to_gray   to_gray, matcher.cpp:21-30 (FP64, no FMA, lround)
+//   k_planes    parity-split rows for the dp4a cross-correlation (layout in
+//               ss_internal.cuh)
+//   k_stats     patch_stats, matcher.cpp:112-137, plus the float reciprocal
+//               sqrt of the variance used by the FP32 filter of the WTA sweep
+//
+// All three are HBM/latency-trivial next to the WTA sweep (a few bytes and a
+// few dozen integer ops per pixel); they are written for coalescing only.
+#include "ss_internal.cuh"
+
+namespace ssb {
+
+__global__ void k_to_gray(const uint8_t* __restrict__ rgb, uint8_t* __restrict__ gray,
+                          long n, long in_stride, long out_stride) {
+  const long f = blockIdx.y;
+  rgb += f * in_stride;
+  gray += f * out_stride;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
+       i += (long)gridDim.x * blockDim.x) {
+    // (0.299 R + 0.587 G) + 0.114 B, each product rounded, no contraction.
+    const double r = __dmul_rn(0.299, (double)rgb[3 * i + 0]);
+    const double g = __dmul_rn(0.587, (double)rgb[3 * i + 1]);
+    const double b = __dmul_rn(0.114, (double)rgb[3 * i + 2]);
+    gray[i] = (uint8_t)round(__dadd_rn(__dadd_rn(r, g), b));  // lround: half away from 0
+  }
+}
+
+void launch_to_gray(const uint8_t* rgb, uint8_t* gray, long n, int frames, long in_stride,
+                    long out_stride, cudaStream_t s) {
+  if (n <= 0 || frames <= 0) return;
+  const int threads = 256;
+  long blocks = (n + threads - 1) / threads;
+  if (blocks > 4096) blocks = 4096;
+  k_to_gray<<<dim3((unsigned)blocks, frames), threads, 0, s>>>(rgb, gray, n, in_stride,
+                                                              out_stride);
+}
+
+// One thread per 32-bit word of a plane row; padding words are written as 0.
+__global__ void k_planes(const uint8_t* __restrict__ gray, uint8_t* __restrict__ plane,
+                         int W, int H, int PB, int PP, long gray_stride, long plane_stride) {
+  const long f = blockIdx.z;
+  gray += f * gray_stride;
+  plane += f * plane_stride;
+  const int words = PP / 4;
+  const int wi = blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = blockIdx.y;  // y * 2 + parity
+  if (wi >= words) return;
+  const int y = row >> 1, par = row & 1;
+  const int half_w = (W + 1) / 2;
+  const uint8_t* src = gray + (long)y * W;
+  uint32_t word = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int j = wi * 4 + b - PB;  // plane index
+    const int x = 2 * j + par;
+    uint32_t val = 0;
+    if (j >= 0 && j < half_w && x < W) val = src[x];
+    word |= val << (8 * b);
+  }
+  reinterpret_cast<uint32_t*>(plane + (long)row * PP)[wi] = word;
+}
+
+void launch_planes(const uint8_t* gray, uint8_t* plane, const Geom& g, int frames,
+                   long gray_stride, long plane_stride, cudaStream_t s) {
+  if (g.W <= 0 || g.H <= 0 || frames <= 0) return;
+  const int words = g.PP / 4;
+  const int threads = 128;
+  dim3 grid((words + threads - 1) / threads, 2 * g.H, frames);
+  k_planes<<<grid, threads, 0, s>>>(gray, plane, g.W, g.H, g.PB, g.PP, gray_stride,
+                                    plane_stride);
+}
+
+// Chessboard window statistics of one image. out[i] = {sum, bits(1/sqrt(var))}
+// with NaN when the window leaves the image or var == 0 (undefined ZNCC).
+// Right-image rows are padded by SPAD entries each side ({0, NaN}).
+__global__ void k_stats(const uint8_t* __restrict__ gray, int2* __restrict__ out, int W,
+                        int H, int half, int pitch, int pad, long gray_stride,
+                        long stat_stride) {
+  const long f = blockIdx.z;
+  gray += f * gray_stride;
+  out += f * stat_stride;
+  const int v = blockIdx.y;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < pitch;
+       x += gridDim.x * blockDim.x) {
+    const int u = x - pad;
+    int2 r = make_int2(0, __float_as_int(__int_as_float(0x7fc00000)));
+    if (u >= half && u < W - half && v >= half && v < H - half) {
+      int64_t n = 0, s = 0, sq = 0;
+      for (int dv = -half; dv <= half; ++dv) {
+        const uint8_t* row = gray + (long)(v + dv) * W + u;
+        for (int du = -half + ((dv + half) & 1); du <= half; du += 2) {
+          const int64_t a = row[du];
+          n += 1;
+          s += a;
+          sq += a * a;
+        }
+      }
+      // patch_stats stores int32 (matcher.cpp:132-133); windows >= 27 wrap.
+      const int32_t var = (int32_t)(n * sq - s * s);
+      r.x = (int32_t)s;
+      if (var != 0) r.y = __float_as_int((float)(1.0 / sqrt((double)var)));
+    }
+    out[(long)v * pitch + x] = r;
+  }
+}
+
+void launch_stats(const uint8_t* gray, int2* lstat, int2* rstat, int is_right, const Geom& g,
+                  int frames, long gray_stride, long stat_stride, cudaStream_t s) {
+  if (g.W <= 0 || g.H <= 0 || frames <= 0) return;
+  const int pitch = is_right ? g.SP : g.W;
+  const int pad = is_right ? g.SPAD : 0;
+  const int threads = 128;
+  dim3 grid((pitch + threads - 1) / threads, g.H, frames);
+  k_stats<<<grid, threads, 0, s>>>(gray, is_right ? rstat : lstat, g.W, g.H, g.half, pitch,
+                                   pad, gray_stride, stat_stride);
+}
+
+}  // namespace ssb

@@ -1,0 +1,941 @@
+// Runtime + C-ABI (include/ss_stereo.h): device context, buffer arena,
+// stage orchestration on one CUDA stream, and the per-stage drop-ins.
+//
+// One ss_ctx per (host thread, GPU). All per-frame buffers are byte arenas that
+// grow on demand; strides are recomputed from each call's geometry, so one
+// context serves every frame size. Per-stage C calls use a lazily created,
+// thread-local context on the current device (SURVEY.md §8b threading row).
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ss_internal.cuh"
+#include "ss_stereo.h"
+
+using namespace ssb;
+
+namespace {
+
+thread_local std::string tl_err;
+
+struct SsError {
+  ss_status code;
+  std::string msg;
+};
+
+[[noreturn]] void raise(ss_status code, const std::string& msg) { throw SsError{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    if (e == cudaErrorMemoryAllocation)
+      raise(SS_ENOMEM, std::string(what) + ": " + cudaGetErrorString(e));
+    raise(SS_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <class F>
+ss_status guarded(F&& f) {
+  try {
+    f();
+    return SS_OK;
+  } catch (const SsError& e) {
+    tl_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    tl_err = "host allocation failed";
+    return SS_ENOMEM;
+  } catch (const std::exception& e) {
+    tl_err = e.what();
+    return SS_ECUDA;
+  }
+}
+
+void require_device() {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    raise(SS_ENODEV,
+          "no CUDA device: the B200 stereo path has no CPU fallback (cudaGetDeviceCount: " +
+              std::string(cudaGetErrorString(e)) + ")");
+}
+
+// Growable device arena.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t need) {
+    if (need <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    need = std::max<size_t>(need, 256);
+    ck(cudaMalloc(&p, need), "cudaMalloc");
+    bytes = need;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+long round_up(long x, long m) { return (x + m - 1) / m * m; }
+
+void validate_params(const ss_stereo_params* p) {
+  // StereoParams::validate, matcher.cpp:9-19 — same checks, order, messages.
+  if (p->window < 3 || p->window % 2 == 0) raise(SS_EPARAM, "stereo: window must be odd and >= 3");
+  if (p->d_min >= p->d_max) raise(SS_EPARAM, "stereo: d_min must be < d_max");
+  if (p->outlier_radius_start <= 0 || p->outlier_radius_step <= 0 ||
+      p->fill_radius_radial <= 0 || p->fill_radius_disc <= 0 || p->smoothing_radius <= 0)
+    raise(SS_EPARAM, "stereo: radii must be > 0");
+  if (!(p->alpha >= 0.0 && p->alpha <= 1.0)) raise(SS_EPARAM, "stereo: alpha must be in [0,1]");
+  if (p->cleanup_iterations < 0) raise(SS_EPARAM, "stereo: cleanup_iterations must be >= 0");
+  if (p->refine_iterations < 0) raise(SS_EPARAM, "stereo: refine_iterations must be >= 0");
+}
+
+void validate_rig(const ss_stereo_rig* r) {
+  // CameraIntrinsics / StereoRig::validate, geometry.cpp:7-19.
+  if (!(r->fx > 0.0)) raise(SS_EPARAM, "intrinsics: fx must be > 0");
+  if (!(r->fy > 0.0)) raise(SS_EPARAM, "intrinsics: fy must be > 0");
+  if (r->width <= 0) raise(SS_EPARAM, "intrinsics: width must be > 0");
+  if (r->height <= 0) raise(SS_EPARAM, "intrinsics: height must be > 0");
+  if (!(r->cx >= 0.0 && r->cx < r->width)) raise(SS_EPARAM, "intrinsics: cx out of image bounds");
+  if (!(r->cy >= 0.0 && r->cy < r->height)) raise(SS_EPARAM, "intrinsics: cy out of image bounds");
+  if (!(r->baseline_mm > 0.0)) raise(SS_EPARAM, "rig: baseline_mm must be > 0");
+}
+
+int32_t disc_neighbor_count(int32_t radius) {
+  int32_t n = 0;
+  for (int dv = -radius; dv <= radius; ++dv)
+    for (int du = -radius; du <= radius; ++du) {
+      const int dd = du * du + dv * dv;
+      if (dd != 0 && dd <= radius * radius) ++n;
+    }
+  return n;
+}
+
+int32_t disc_fill_min_support(int32_t radius) {
+  return (int32_t)std::ceil(0.25 * disc_neighbor_count(radius));
+}
+
+Geom make_geom(int W, int H, const ss_stereo_params* p) {
+  Geom g{};
+  g.W = W;
+  g.H = H;
+  g.half = p->window / 2;
+  g.dmin = p->d_min;
+  g.dmax = p->d_max;
+  g.cmin = p->d_min - kRefineR;
+  g.NC = p->d_max - p->d_min + 1 + 2 * kRefineR;
+  const int span = std::max(std::abs(g.cmin), std::abs(g.cmin + std::max(g.NC, 1) - 1)) + 2 * kDB;
+  g.PB = (int)round_up(span / 2 + 24, 4);
+  g.PP = (int)round_up((long)(W + 1) / 2 + 2L * g.PB, 16);
+  g.SPAD = span + 24;
+  g.SP = W + 2 * g.SPAD;
+  return g;
+}
+
+bool fast_path(const Geom& g, const ss_stereo_params* p) {
+  return p->window == 11 && g.NC >= 1 && (g.NC + kDB - 1) / kDB <= 16;
+}
+
+}  // namespace
+
+struct ss_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  ss_stereo_params params{};
+  ss_stereo_rig rig{};
+  bool has_rig = false;
+  int max_w = 0, max_h = 0, max_batch = 1;
+
+  DevBuf in_l, in_r, gray_l, gray_r, plane_l, plane_r, lstat, rstat, vol;
+  DevBuf disp_a, disp_b, valid_a, valid_b, flags, flag_count;
+  DevBuf o, d, avg, b, psum, pcnt, cnt, span, wtab;
+  DevBuf index, block_sums, npoints, pts_f, nrm_f, colors, pts_d, nrm_d, pixels;
+  DevBuf counters, trace_o, trace_d;
+  int wtab_radius = -1;
+
+  ss_ctx_stats stats{};
+  // per-stage event timing (ss_ctx_enable_timing)
+  bool timing = false;
+  struct StageRec {
+    int stage;
+    cudaEvent_t a, b;
+    int64_t launches;
+  };
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<StageRec> pending;
+  double stage_ms[SS_N_STAGES] = {};
+  int64_t stage_launches[SS_N_STAGES] = {};
+  // which buffer holds the final map of the last run
+  float* last_disp = nullptr;
+  uint8_t* last_valid = nullptr;
+  long last_N = 0;
+  int last_frames = 0;
+
+  ~ss_ctx() {
+    for (DevBuf* b : {&in_l, &in_r, &gray_l, &gray_r, &plane_l, &plane_r, &lstat, &rstat, &vol,
+                      &disp_a, &disp_b, &valid_a, &valid_b, &flags, &flag_count, &o, &d, &avg,
+                      &b, &psum, &pcnt, &cnt, &span, &wtab, &index, &block_sums, &npoints,
+                      &pts_f, &nrm_f, &colors, &pts_d, &nrm_d, &pixels, &counters, &trace_o,
+                      &trace_d})
+      b->release();
+    for (auto& r : pending) {
+      ev_pool.push_back(r.a);
+      ev_pool.push_back(r.b);
+    }
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  cudaEvent_t take_event() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+  }
+
+  // RAII stage marker: events on the ctx stream around one stage.
+  struct Stage {
+    ss_ctx* c;
+    int id;
+    cudaEvent_t a = nullptr;
+    int64_t l0;
+    Stage(ss_ctx* ctx, int stage) : c(ctx), id(stage), l0(ctx->stats.kernel_launches) {
+      if (c->timing) {
+        a = c->take_event();
+        ck(cudaEventRecord(a, c->stream), "cudaEventRecord");
+      }
+    }
+    ~Stage() {
+      if (!a) return;
+      cudaEvent_t b = c->take_event();
+      cudaEventRecord(b, c->stream);
+      c->pending.push_back({id, a, b, c->stats.kernel_launches - l0});
+    }
+  };
+
+  void collect_times() {
+    if (pending.empty()) return;
+    ck(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    for (auto& r : pending) {
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, r.a, r.b), "cudaEventElapsedTime");
+      stage_ms[r.stage] += ms;
+      stage_launches[r.stage] += r.launches;
+      ev_pool.push_back(r.a);
+      ev_pool.push_back(r.b);
+    }
+    pending.clear();
+  }
+
+  void activate() { ck(cudaSetDevice(device), "cudaSetDevice"); }
+
+  void init(int dev) {
+    device = dev;
+    activate();
+    ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    counters.ensure(4 * sizeof(unsigned long long));
+    ck(cudaMemsetAsync(counters.p, 0, 4 * sizeof(unsigned long long), stream), "memset");
+  }
+
+  unsigned long long* ctr() { return counters.as<unsigned long long>(); }
+
+  // ---- stage runners (device-resident, frames packed with stride N) ----
+
+  void prepare_gray(int n, int W, int H, int in_format, const uint8_t* dl, const uint8_t* dr) {
+    Stage st(this, 0);
+    const long N = (long)W * H;
+    gray_l.ensure(N * n);
+    gray_r.ensure(N * n);
+    if (in_format == SS_IN_RGB) {
+      launch_to_gray(dl, gray_l.as<uint8_t>(), N, n, 3 * N, N, stream);
+      launch_to_gray(dr, gray_r.as<uint8_t>(), N, n, 3 * N, N, stream);
+      stats.kernel_launches += 2;
+    } else {
+      if (dl != gray_l.p) ck(cudaMemcpyAsync(gray_l.p, dl, N * n, cudaMemcpyDeviceToDevice, stream), "copy");
+      if (dr != gray_r.p) ck(cudaMemcpyAsync(gray_r.p, dr, N * n, cudaMemcpyDeviceToDevice, stream), "copy");
+    }
+  }
+
+  // Stats, planes and the cost volume for the fast path (window 11).
+  void build_volume(int n, const Geom& g, bool do_argmax) {
+    const long N = g.N();
+    const long plane_stride = (long)g.H * 2 * g.PP;
+    const long rstride = (long)g.H * g.SP;
+    plane_l.ensure(plane_stride * n);
+    plane_r.ensure(plane_stride * n);
+    lstat.ensure(sizeof(int2) * N * n);
+    rstat.ensure(sizeof(int2) * rstride * n);
+    vol.ensure(sizeof(float) * (size_t)g.NC * N * n);
+    flags.ensure(sizeof(int) * N * n);
+    flag_count.ensure(sizeof(unsigned) * n);
+    {
+    Stage st(this, 1);
+    launch_planes(gray_l.as<uint8_t>(), plane_l.as<uint8_t>(), g, n, N, plane_stride, stream);
+    launch_planes(gray_r.as<uint8_t>(), plane_r.as<uint8_t>(), g, n, N, plane_stride, stream);
+    launch_stats(gray_l.as<uint8_t>(), lstat.as<int2>(), nullptr, 0, g, n, N, N, stream);
+    launch_stats(gray_r.as<uint8_t>(), nullptr, rstat.as<int2>(), 1, g, n, N, rstride, stream);
+    stats.kernel_launches += 4;
+    }
+    ck(cudaMemsetAsync(flag_count.p, 0, sizeof(unsigned) * n, stream), "memset");
+    if (do_argmax) {
+      ck(cudaMemsetAsync(disp_a.p, 0, sizeof(float) * N * n, stream), "memset");
+      ck(cudaMemsetAsync(valid_a.p, 0, N * n, stream), "memset");
+    }
+    Stage st(this, 2);
+    launch_wta11(plane_l.as<uint8_t>(), plane_r.as<uint8_t>(), lstat.as<int2>(), rstat.as<int2>(),
+                 vol.as<float>(), disp_a.as<float>(), valid_a.as<uint8_t>(), flags.as<int>(),
+                 flag_count.as<unsigned>(), g, params.min_zncc, n, plane_stride, N, rstride,
+                 (long)g.NC * N, N, do_argmax ? 1 : 0, stream);
+    stats.kernel_launches += 1;
+  }
+
+  void ensure_maps(long N, int n) {
+    disp_a.ensure(sizeof(float) * N * n);
+    disp_b.ensure(sizeof(float) * N * n);
+    valid_a.ensure(N * n);
+    valid_b.ensure(N * n);
+  }
+
+  // compute_disparity on gray_l/gray_r -> disp_a/valid_a.
+  bool run_wta(int n, const Geom& g) {
+    const long N = g.N();
+    ensure_maps(N, n);
+    if (fast_path(g, &params)) {
+      build_volume(n, g, true);
+      Stage st(this, 3);
+      launch_wta_resolve(gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), flags.as<int>(),
+                         flag_count.as<unsigned>(), disp_a.as<float>(), valid_a.as<uint8_t>(),
+                         g, params.min_zncc, n, N, N, N, ctr() + 0, stream);
+      stats.kernel_launches += 1;
+      return true;
+    }
+    Stage st(this, 2);
+    ck(cudaMemsetAsync(disp_a.p, 0, sizeof(float) * N * n, stream), "memset");
+    ck(cudaMemsetAsync(valid_a.p, 0, N * n, stream), "memset");
+    launch_wta_generic(gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), disp_a.as<float>(),
+                       valid_a.as<uint8_t>(), g, params.min_zncc, n, N, N, stream);
+    stats.kernel_launches += 1;
+    return false;
+  }
+
+  void ensure_wtab(int radius) {
+    if (radius == wtab_radius) return;
+    const int r2 = std::max(radius, 0) * std::max(radius, 0);
+    std::vector<double> w(r2 + 1, 0.0);
+    for (int dd = 1; dd <= r2; ++dd) w[dd] = 1.0 / std::sqrt(static_cast<double>(dd));
+    wtab.ensure(sizeof(double) * (r2 + 1));
+    ck(cudaMemcpy(wtab.p, w.data(), sizeof(double) * (r2 + 1), cudaMemcpyHostToDevice), "wtab");
+    wtab_radius = radius;
+  }
+
+  // cleanup_pass on disp_a/valid_a -> disp_a/valid_a (cleanup.cpp:111-123).
+  void run_cleanup(int n, int W, int H) {
+    Stage st(this, 4);
+    const long N = (long)W * H;
+    const int disc_support = disc_fill_min_support(params.fill_radius_disc);
+    ensure_wtab(params.fill_radius_disc);
+    for (int k = 0; k < params.cleanup_iterations; ++k) {
+      const int r = params.outlier_radius_start + k * params.outlier_radius_step;
+      launch_remove_outliers(disp_a.as<float>(), valid_a.as<uint8_t>(), disp_b.as<float>(),
+                             valid_b.as<uint8_t>(), W, H, r, params.neighbor_jump_threshold, n, N,
+                             stream);
+      launch_fill_radial(disp_b.as<float>(), valid_b.as<uint8_t>(), disp_a.as<float>(),
+                         valid_a.as<uint8_t>(), W, H, params.fill_radius_radial, 4, n, N, stream);
+      launch_fill_disc(disp_a.as<float>(), valid_a.as<uint8_t>(), disp_b.as<float>(),
+                       valid_b.as<uint8_t>(), W, H, params.fill_radius_disc, disc_support,
+                       wtab.as<double>(), n, N, stream);
+      ck(cudaMemcpyAsync(disp_a.p, disp_b.p, sizeof(float) * N * n, cudaMemcpyDeviceToDevice,
+                         stream), "copy");
+      ck(cudaMemcpyAsync(valid_a.p, valid_b.p, N * n, cudaMemcpyDeviceToDevice, stream), "copy");
+      stats.kernel_launches += 3;
+    }
+  }
+
+  // refine_disparities: disp_a/valid_a (+ gray, volume) -> disp_b/valid_a.
+  void run_refine(int n, const Geom& g, bool have_volume, double* h_trace_o, double* h_trace_d) {
+    Stage st(this, 5);
+    const int W = g.W, H = g.H;
+    const long N = g.N();
+    const long pstride = (long)H * (W + 1);
+    o.ensure(sizeof(double) * N * n);
+    d.ensure(sizeof(double) * N * n);
+    avg.ensure(sizeof(double) * N * n);
+    b.ensure(sizeof(double) * N * n);
+    psum.ensure(sizeof(double) * pstride * n);
+    pcnt.ensure(sizeof(int) * pstride * n);
+    cnt.ensure(sizeof(int) * N * n);
+    const int r = params.smoothing_radius;
+    std::vector<int> sp(std::max(r, 0) + 1);
+    for (int dy = 0; dy <= r; ++dy)
+      sp[dy] = (int)std::floor(std::sqrt((double)r * r - (double)dy * dy));
+    span.ensure(sizeof(int) * sp.size());
+    ck(cudaMemcpyAsync(span.p, sp.data(), sizeof(int) * sp.size(), cudaMemcpyHostToDevice, stream),
+       "span");
+    RefineArgs a{};
+    a.g = g;
+    a.alpha = params.alpha;
+    a.one_minus_alpha = 1.0 - params.alpha;
+    a.eta = params.eta_smooth;
+    a.eta_f = (float)params.eta_smooth;
+    a.lo = params.d_min - kRefineR;
+    a.hi = params.d_max + kRefineR;
+    a.radius = r;
+    a.span = span.as<int>();
+    const int iters = params.refine_iterations;
+    if (h_trace_o || h_trace_d) {
+      trace_o.ensure(sizeof(double) * N * std::max(iters, 1));
+      trace_d.ensure(sizeof(double) * N * std::max(iters, 1));
+    }
+    launch_refine_init(disp_a.as<float>(), valid_a.as<uint8_t>(), o.as<double>(), d.as<double>(),
+                       W, H, n, N, stream);
+    launch_row_count(valid_a.as<uint8_t>(), pcnt.as<int>(), W, H, n, N, pstride, stream);
+    launch_disc_count(valid_a.as<uint8_t>(), pcnt.as<int>(), cnt.as<int>(), a, n, N, pstride,
+                      stream);
+    stats.kernel_launches += 3;
+    for (int it = 0; it < iters; ++it) {
+      launch_row_scan(o.as<double>(), valid_a.as<uint8_t>(), psum.as<double>(), W, H, n, N,
+                      pstride, stream);
+      launch_avg_b(psum.as<double>(), valid_a.as<uint8_t>(), cnt.as<int>(), o.as<double>(),
+                   d.as<double>(), avg.as<double>(), b.as<double>(), a, n, N, pstride, stream);
+      launch_row_scan(b.as<double>(), valid_a.as<uint8_t>(), psum.as<double>(), W, H, n, N,
+                      pstride, stream);
+      launch_d_repick(psum.as<double>(), valid_a.as<uint8_t>(), cnt.as<int>(), avg.as<double>(),
+                      d.as<double>(), o.as<double>(), gray_l.as<uint8_t>(), gray_r.as<uint8_t>(),
+                      lstat.as<int2>(), have_volume ? vol.as<float>() : nullptr, a, n, N,
+                      pstride, N, N, (long)g.NC * N, ctr() + (have_volume ? 1 : 2), stream);
+      stats.kernel_launches += 4;
+      if (h_trace_o)
+        ck(cudaMemcpyAsync(trace_o.as<double>() + (long)it * N, o.p, sizeof(double) * N,
+                           cudaMemcpyDeviceToDevice, stream), "trace");
+      if (h_trace_d)
+        ck(cudaMemcpyAsync(trace_d.as<double>() + (long)it * N, d.p, sizeof(double) * N,
+                           cudaMemcpyDeviceToDevice, stream), "trace");
+    }
+    launch_refine_out(d.as<double>(), valid_a.as<uint8_t>(), disp_a.as<float>(),
+                      disp_b.as<float>(), W, H, n, N, stream);
+    stats.kernel_launches += 1;
+    if (h_trace_o && iters > 0)
+      ck(cudaMemcpyAsync(h_trace_o, trace_o.p, sizeof(double) * N * iters,
+                         cudaMemcpyDeviceToHost, stream), "trace D2H");
+    if (h_trace_d && iters > 0)
+      ck(cudaMemcpyAsync(h_trace_d, trace_d.p, sizeof(double) * N * iters,
+                         cudaMemcpyDeviceToHost, stream), "trace D2H");
+  }
+
+  // disparity_to_cloud of (disp, valid) -> index/points/normals/colors.
+  void run_cloud(int n, int W, int H, const float* dsp, const uint8_t* vld, const uint8_t* rgb,
+                 int cw, int ch, long rgb_stride, bool want_double, bool want_normals,
+                 bool want_pixels) {
+    Stage st(this, 6);
+    const long N = (long)W * H;
+    index.ensure(sizeof(int) * N * n);
+    const long nblocks = (N + 1023) / 1024;
+    block_sums.ensure(sizeof(int) * std::max<long>(nblocks, 1) * n);
+    npoints.ensure(sizeof(int) * n);
+    colors.ensure(3 * N * n);
+    CloudArgs c{rig.fx, rig.fy, rig.cx, rig.cy, rig.baseline_mm};
+    launch_cloud_index(dsp, vld, index.as<int>(), block_sums.as<int>(), npoints.as<int>(), W, H,
+                       n, N, stream);
+    stats.kernel_launches += 3;
+    if (want_double) {
+      pts_d.ensure(sizeof(double) * 3 * N * n);
+      if (want_normals) nrm_d.ensure(sizeof(double) * 3 * N * n);
+    } else {
+      pts_f.ensure(sizeof(float) * 3 * N * n);
+      if (want_normals) nrm_f.ensure(sizeof(float) * 3 * N * n);
+    }
+    if (want_pixels) pixels.ensure(sizeof(int) * 2 * N * n);
+    launch_cloud_points(dsp, index.as<int>(), rgb, cw, ch, W, H, c,
+                        want_double ? pts_d.as<double>() : nullptr,
+                        want_double ? nullptr : pts_f.as<float>(), colors.as<uint8_t>(),
+                        want_pixels ? pixels.as<int>() : nullptr, n, N, rgb_stride, stream);
+    stats.kernel_launches += 1;
+    if (want_normals) {
+      launch_cloud_normals(dsp, index.as<int>(), c, want_double ? nrm_d.as<double>() : nullptr,
+                           want_double ? nullptr : nrm_f.as<float>(), W, H, n, N, stream);
+      stats.kernel_launches += 1;
+    }
+  }
+
+  // Whole run_stereo_only chain on device inputs (in_l/in_r hold the frames).
+  void run_chain(int n, int W, int H, int in_format, const uint8_t* dl, const uint8_t* dr,
+                 uint32_t flags_out) {
+    const Geom g = make_geom(W, H, &params);
+    prepare_gray(n, W, H, in_format, dl, dr);
+    const bool vol_ok = run_wta(n, g);
+    run_cleanup(n, W, H);
+    run_refine(n, g, vol_ok, nullptr, nullptr);
+    last_disp = disp_b.as<float>();
+    last_valid = valid_a.as<uint8_t>();
+    last_N = g.N();
+    last_frames = n;
+    if (flags_out & (SS_OUT_CLOUD | SS_OUT_NORMALS)) {
+      if (!has_rig) raise(SS_EINVAL, "stereo batch: cloud output requested but ctx has no rig");
+      run_cloud(n, W, H, last_disp, last_valid, in_format == SS_IN_RGB ? dl : nullptr, W, H,
+                3L * g.N(), false, (flags_out & SS_OUT_NORMALS) != 0, false);
+    }
+    stats.frames += n;
+  }
+};
+
+namespace {
+
+ss_ctx* thread_ctx() {
+  thread_local std::unique_ptr<ss_ctx> ctx;
+  require_device();
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
+  if (!ctx || ctx->device != dev) {
+    ctx.reset(new ss_ctx());
+    ctx->init(dev);
+  }
+  ctx->activate();
+  return ctx.get();
+}
+
+void h2d(DevBuf& b, const void* src, size_t bytes, cudaStream_t s) {
+  b.ensure(bytes);
+  if (bytes) ck(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, s), "H2D");
+}
+
+void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes) ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+}
+
+void sync(ss_ctx* c) { ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize"); }
+
+void check_dims(int32_t w, int32_t h, const char* who) {
+  if (w < 0 || h < 0) raise(SS_EINVAL, std::string(who) + ": negative image size");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ss_last_error(void) { return tl_err.c_str(); }
+const char* ss_version(void) { return "stereoscan-b200 0.1 (sm_100a)"; }
+
+void ss_params_default(ss_stereo_params* p) {
+  p->window = 11;
+  p->d_min = -20;
+  p->d_max = 80;
+  p->neighbor_jump_threshold = 2.5;
+  p->outlier_radius_start = 10;
+  p->outlier_radius_step = 10;
+  p->cleanup_iterations = 3;
+  p->fill_radius_radial = 50;
+  p->fill_radius_disc = 20;
+  p->smoothing_radius = 15;
+  p->alpha = 0.1;
+  p->eta_smooth = 0.01;
+  p->refine_iterations = 10;
+  p->min_zncc = 0.5;
+}
+
+ss_status ss_params_validate(const ss_stereo_params* p) {
+  return guarded([&] { validate_params(p); });
+}
+
+ss_status ss_rig_validate(const ss_stereo_rig* r) {
+  return guarded([&] { validate_rig(r); });
+}
+
+int32_t ss_disc_neighbor_count(int32_t radius) { return disc_neighbor_count(radius); }
+int32_t ss_disc_fill_min_support(int32_t radius) { return disc_fill_min_support(radius); }
+
+int32_t ss_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+ss_status ss_to_gray(const uint8_t* rgb, int32_t w, int32_t h, uint8_t* gray) {
+  return guarded([&] {
+    check_dims(w, h, "to_gray");
+    ss_ctx* c = thread_ctx();
+    const long N = (long)w * h;
+    if (N == 0) return;
+    h2d(c->in_l, rgb, 3 * N, c->stream);
+    c->gray_l.ensure(N);
+    launch_to_gray(c->in_l.as<uint8_t>(), c->gray_l.as<uint8_t>(), N, 1, 3 * N, N, c->stream);
+    c->stats.kernel_launches += 1;
+    d2h(gray, c->gray_l.p, N, c->stream);
+    sync(c);
+  });
+}
+
+ss_status ss_compute_disparity(const ss_stereo_params* p, const uint8_t* left, int32_t lw,
+                               int32_t lh, const uint8_t* right, int32_t rw, int32_t rh,
+                               float* disparity, uint8_t* valid) {
+  return guarded([&] {
+    if (lw != rw || lh != rh) raise(SS_EINVAL, "compute_disparity: image sizes differ");
+    validate_params(p);
+    check_dims(lw, lh, "compute_disparity");
+    const long N = (long)lw * lh;
+    if (N == 0) return;
+    ss_ctx* c = thread_ctx();
+    c->params = *p;
+    h2d(c->gray_l, left, N, c->stream);
+    h2d(c->gray_r, right, N, c->stream);
+    const Geom g = make_geom(lw, lh, p);
+    c->run_wta(1, g);
+    d2h(disparity, c->disp_a.p, sizeof(float) * N, c->stream);
+    d2h(valid, c->valid_a.p, N, c->stream);
+    sync(c);
+  });
+}
+
+ss_status ss_remove_outliers(const float* disparity, const uint8_t* valid, int32_t w, int32_t h,
+                             int32_t radius, double threshold, float* out_disparity,
+                             uint8_t* out_valid) {
+  return guarded([&] {
+    check_dims(w, h, "remove_outliers");
+    const long N = (long)w * h;
+    if (N == 0) return;
+    ss_ctx* c = thread_ctx();
+    c->ensure_maps(N, 1);
+    ck(cudaMemcpyAsync(c->disp_a.p, disparity, sizeof(float) * N, cudaMemcpyHostToDevice,
+                       c->stream), "H2D");
+    ck(cudaMemcpyAsync(c->valid_a.p, valid, N, cudaMemcpyHostToDevice, c->stream), "H2D");
+    launch_remove_outliers(c->disp_a.as<float>(), c->valid_a.as<uint8_t>(), c->disp_b.as<float>(),
+                           c->valid_b.as<uint8_t>(), w, h, radius, threshold, 1, N, c->stream);
+    c->stats.kernel_launches += 1;
+    d2h(out_disparity, c->disp_b.p, sizeof(float) * N, c->stream);
+    d2h(out_valid, c->valid_b.p, N, c->stream);
+    sync(c);
+  });
+}
+
+ss_status ss_fill_holes(const float* disparity, const uint8_t* valid, int32_t w, int32_t h,
+                        int32_t mode, int32_t radius, int32_t min_support, float* out_disparity,
+                        uint8_t* out_valid) {
+  return guarded([&] {
+    check_dims(w, h, "fill_holes");
+    if (mode != SS_FILL_RADIAL && mode != SS_FILL_DISC)
+      raise(SS_EINVAL, "fill_holes: unknown FillMode");
+    const long N = (long)w * h;
+    if (N == 0) return;
+    ss_ctx* c = thread_ctx();
+    c->ensure_maps(N, 1);
+    ck(cudaMemcpyAsync(c->disp_a.p, disparity, sizeof(float) * N, cudaMemcpyHostToDevice,
+                       c->stream), "H2D");
+    ck(cudaMemcpyAsync(c->valid_a.p, valid, N, cudaMemcpyHostToDevice, c->stream), "H2D");
+    if (mode == SS_FILL_RADIAL) {
+      launch_fill_radial(c->disp_a.as<float>(), c->valid_a.as<uint8_t>(), c->disp_b.as<float>(),
+                         c->valid_b.as<uint8_t>(), w, h, radius, min_support, 1, N, c->stream);
+    } else {
+      c->ensure_wtab(radius);
+      launch_fill_disc(c->disp_a.as<float>(), c->valid_a.as<uint8_t>(), c->disp_b.as<float>(),
+                       c->valid_b.as<uint8_t>(), w, h, radius, min_support,
+                       c->wtab.as<double>(), 1, N, c->stream);
+    }
+    c->stats.kernel_launches += 1;
+    d2h(out_disparity, c->disp_b.p, sizeof(float) * N, c->stream);
+    d2h(out_valid, c->valid_b.p, N, c->stream);
+    sync(c);
+  });
+}
+
+ss_status ss_cleanup_pass(const ss_stereo_params* p, const float* disparity,
+                          const uint8_t* valid, int32_t w, int32_t h, float* out_disparity,
+                          uint8_t* out_valid) {
+  return guarded([&] {
+    check_dims(w, h, "cleanup_pass");
+    const long N = (long)w * h;
+    if (N == 0) return;
+    ss_ctx* c = thread_ctx();
+    c->params = *p;
+    c->ensure_maps(N, 1);
+    ck(cudaMemcpyAsync(c->disp_a.p, disparity, sizeof(float) * N, cudaMemcpyHostToDevice,
+                       c->stream), "H2D");
+    ck(cudaMemcpyAsync(c->valid_a.p, valid, N, cudaMemcpyHostToDevice, c->stream), "H2D");
+    c->run_cleanup(1, w, h);
+    d2h(out_disparity, c->disp_a.p, sizeof(float) * N, c->stream);
+    d2h(out_valid, c->valid_a.p, N, c->stream);
+    sync(c);
+  });
+}
+
+ss_status ss_refine_disparities(const ss_stereo_params* p, const float* disparity,
+                                const uint8_t* valid, int32_t w, int32_t h,
+                                const uint8_t* left, int32_t lw, int32_t lh,
+                                const uint8_t* right, int32_t rw, int32_t rh,
+                                float* out_disparity, uint8_t* out_valid,
+                                double* trace_discrete, double* trace_smooth) {
+  return guarded([&] {
+    check_dims(w, h, "refine_disparities");
+    // The reference indexes the images with the map's geometry (UB on a
+    // mismatch); the drop-in rejects it instead (documented divergence).
+    if (lw != w || lh != h || rw != w || rh != h)
+      raise(SS_EINVAL, "refine_disparities: map and image sizes differ");
+    const long N = (long)w * h;
+    if (N == 0) return;
+    ss_ctx* c = thread_ctx();
+    c->params = *p;
+    const Geom g = make_geom(w, h, p);
+    c->ensure_maps(N, 1);
+    h2d(c->gray_l, left, N, c->stream);
+    h2d(c->gray_r, right, N, c->stream);
+    const bool vol_ok = fast_path(g, p);
+    if (vol_ok) c->build_volume(1, g, false);
+    ck(cudaMemcpyAsync(c->disp_a.p, disparity, sizeof(float) * N, cudaMemcpyHostToDevice,
+                       c->stream), "H2D");
+    ck(cudaMemcpyAsync(c->valid_a.p, valid, N, cudaMemcpyHostToDevice, c->stream), "H2D");
+    c->run_refine(1, g, vol_ok, trace_discrete, trace_smooth);
+    d2h(out_disparity, c->disp_b.p, sizeof(float) * N, c->stream);
+    d2h(out_valid, c->valid_a.p, N, c->stream);
+    sync(c);
+  });
+}
+
+ss_status ss_disparity_to_cloud(const float* disparity, const uint8_t* valid, int32_t w,
+                                int32_t h, const uint8_t* rgb, int32_t cw, int32_t ch,
+                                const ss_stereo_rig* rig, int32_t* index, double* points,
+                                double* normals, uint8_t* colors, int32_t* pixels,
+                                int32_t* n_points) {
+  return guarded([&] {
+    validate_rig(rig);
+    check_dims(w, h, "disparity_to_cloud");
+    const long N = (long)w * h;
+    *n_points = 0;
+    if (N == 0) return;
+    ss_ctx* c = thread_ctx();
+    c->rig = *rig;
+    c->has_rig = true;
+    c->ensure_maps(N, 1);
+    ck(cudaMemcpyAsync(c->disp_a.p, disparity, sizeof(float) * N, cudaMemcpyHostToDevice,
+                       c->stream), "H2D");
+    ck(cudaMemcpyAsync(c->valid_a.p, valid, N, cudaMemcpyHostToDevice, c->stream), "H2D");
+    const long CN = (long)std::max(cw, 0) * std::max(ch, 0);
+    const uint8_t* drgb = nullptr;
+    if (rgb && CN > 0) {
+      h2d(c->in_l, rgb, 3 * CN, c->stream);
+      drgb = c->in_l.as<uint8_t>();
+    }
+    c->run_cloud(1, w, h, c->disp_a.as<float>(), c->valid_a.as<uint8_t>(), drgb, cw, ch, 0,
+                 true, true, true);
+    int np = 0;
+    d2h(&np, c->npoints.p, sizeof(int), c->stream);
+    sync(c);
+    *n_points = np;
+    d2h(index, c->index.p, sizeof(int) * N, c->stream);
+    d2h(points, c->pts_d.p, sizeof(double) * 3 * np, c->stream);
+    d2h(normals, c->nrm_d.p, sizeof(double) * 3 * np, c->stream);
+    d2h(colors, c->colors.p, 3L * np, c->stream);
+    d2h(pixels, c->pixels.p, sizeof(int) * 2 * np, c->stream);
+    sync(c);
+  });
+}
+
+// ---- throughput API ----
+
+ss_status ss_ctx_create(int32_t device, int32_t max_w, int32_t max_h, int32_t max_batch,
+                        const ss_stereo_params* p, const ss_stereo_rig* rig, ss_ctx** out) {
+  return guarded([&] {
+    *out = nullptr;
+    require_device();
+    validate_params(p);
+    if (rig) validate_rig(rig);
+    if (max_w <= 0 || max_h <= 0 || max_batch <= 0)
+      raise(SS_EINVAL, "ss_ctx_create: max_w, max_h and max_batch must be > 0");
+    std::unique_ptr<ss_ctx> c(new ss_ctx());
+    c->init(device);
+    c->params = *p;
+    if (rig) {
+      c->rig = *rig;
+      c->has_rig = true;
+    }
+    c->max_w = max_w;
+    c->max_h = max_h;
+    c->max_batch = max_batch;
+    *out = c.release();
+  });
+}
+
+ss_status ss_ctx_destroy(ss_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    ctx->activate();
+    cudaStreamSynchronize(ctx->stream);
+    delete ctx;
+  });
+}
+
+ss_status ss_ctx_enable_timing(ss_ctx* ctx, int32_t on) {
+  return guarded([&] {
+    ctx->activate();
+    ctx->collect_times();
+    ctx->timing = on != 0;
+  });
+}
+
+ss_status ss_ctx_stage_times(ss_ctx* ctx, double* ms, int64_t* launches) {
+  return guarded([&] {
+    ctx->activate();
+    ctx->collect_times();
+    for (int i = 0; i < SS_N_STAGES; ++i) {
+      if (ms) ms[i] = ctx->stage_ms[i];
+      if (launches) launches[i] = ctx->stage_launches[i];
+    }
+  });
+}
+
+void* ss_ctx_stream(ss_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+ss_status ss_ctx_sync(ss_ctx* ctx) {
+  return guarded([&] {
+    ctx->activate();
+    sync(ctx);
+  });
+}
+
+ss_status ss_ctx_get_stats(ss_ctx* ctx, ss_ctx_stats* st) {
+  return guarded([&] {
+    ctx->activate();
+    unsigned long long c[4];
+    ck(cudaMemcpyAsync(c, ctx->counters.p, sizeof c, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    sync(ctx);
+    *st = ctx->stats;
+    st->wta_resolved = (int64_t)c[0];
+    st->refine_resolved = (int64_t)c[1];
+    st->refine_fallback = (int64_t)c[2];
+  });
+}
+
+ss_status ss_ctx_reset_stats(ss_ctx* ctx) {
+  return guarded([&] {
+    ctx->activate();
+    ck(cudaMemsetAsync(ctx->counters.p, 0, 4 * sizeof(unsigned long long), ctx->stream), "memset");
+    sync(ctx);
+    ctx->collect_times();
+    ctx->stats = ss_ctx_stats{};
+    for (int i = 0; i < SS_N_STAGES; ++i) {
+      ctx->stage_ms[i] = 0.0;
+      ctx->stage_launches[i] = 0;
+    }
+  });
+}
+
+ss_status ss_stereo_batch_device(ss_ctx* ctx, int32_t n, int32_t w, int32_t h,
+                                 int32_t in_format, const uint8_t* d_left,
+                                 const uint8_t* d_right, uint32_t out_flags,
+                                 const ss_batch_out* d_out, void* stream) {
+  return guarded([&] {
+    if (!ctx) raise(SS_EINVAL, "ss_stereo_batch_device: null ctx");
+    if (n < 0 || w <= 0 || h <= 0) raise(SS_EINVAL, "ss_stereo_batch_device: bad shape");
+    if (n > ctx->max_batch) raise(SS_EINVAL, "ss_stereo_batch_device: n exceeds max_batch");
+    if (in_format != SS_IN_RGB && in_format != SS_IN_GRAY)
+      raise(SS_EINVAL, "ss_stereo_batch_device: unknown input format");
+    ctx->activate();
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    cudaEvent_t ev = nullptr;
+    if (user && user != ctx->stream) {
+      ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+      ck(cudaEventRecord(ev, user), "event");
+      ck(cudaStreamWaitEvent(ctx->stream, ev, 0), "wait");
+    }
+    if (n > 0) ctx->run_chain(n, w, h, in_format, d_left, d_right, out_flags);
+    const long N = (long)w * h;
+    if (d_out && n > 0) {
+      auto cp = [&](void* dst, const void* src, size_t bytes) {
+        if (dst && bytes)
+          ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream), "D2D");
+      };
+      cp(d_out->disparity, ctx->last_disp, sizeof(float) * N * n);
+      cp(d_out->valid, ctx->last_valid, N * n);
+      if (out_flags & SS_OUT_CLOUD) {
+        cp(d_out->index, ctx->index.p, sizeof(int) * N * n);
+        cp(d_out->n_points, ctx->npoints.p, sizeof(int) * n);
+        cp(d_out->points, ctx->pts_f.p, sizeof(float) * 3 * N * n);
+        cp(d_out->colors, ctx->colors.p, 3 * N * n);
+      }
+      if (out_flags & SS_OUT_NORMALS) cp(d_out->normals, ctx->nrm_f.p, sizeof(float) * 3 * N * n);
+    }
+    if (ev) {
+      ck(cudaEventRecord(ev, ctx->stream), "event");
+      ck(cudaStreamWaitEvent(user, ev, 0), "wait");
+      cudaEventDestroy(ev);
+    }
+  });
+}
+
+ss_status ss_ctx_device_outputs(ss_ctx* ctx, ss_batch_out* o) {
+  return guarded([&] {
+    o->disparity = ctx->last_disp;
+    o->valid = ctx->last_valid;
+    o->index = ctx->index.as<int32_t>();
+    o->points = ctx->pts_f.as<float>();
+    o->normals = ctx->nrm_f.as<float>();
+    o->colors = ctx->colors.as<uint8_t>();
+    o->n_points = ctx->npoints.as<int32_t>();
+  });
+}
+
+ss_status ss_stereo_batch(ss_ctx* ctx, int32_t n, int32_t w, int32_t h, int32_t in_format,
+                          const uint8_t* left, const uint8_t* right, uint32_t out_flags,
+                          const ss_batch_out* out) {
+  return guarded([&] {
+    if (!ctx) raise(SS_EINVAL, "ss_stereo_batch: null ctx");
+    if (n < 0 || w <= 0 || h <= 0) raise(SS_EINVAL, "ss_stereo_batch: bad shape");
+    if (in_format != SS_IN_RGB && in_format != SS_IN_GRAY)
+      raise(SS_EINVAL, "ss_stereo_batch: unknown input format");
+    ctx->activate();
+    const long N = (long)w * h;
+    const long in_bytes = (in_format == SS_IN_RGB ? 3 : 1) * N;
+    std::vector<int> np(ctx->max_batch);
+    for (int f0 = 0; f0 < n; f0 += ctx->max_batch) {
+      const int m = std::min(ctx->max_batch, n - f0);
+      h2d(ctx->in_l, left + f0 * in_bytes, in_bytes * m, ctx->stream);
+      h2d(ctx->in_r, right + f0 * in_bytes, in_bytes * m, ctx->stream);
+      ctx->run_chain(m, w, h, in_format, ctx->in_l.as<uint8_t>(), ctx->in_r.as<uint8_t>(),
+                     out_flags);
+      if (out->disparity) d2h(out->disparity + f0 * N, ctx->last_disp, sizeof(float) * N * m, ctx->stream);
+      if (out->valid) d2h(out->valid + f0 * N, ctx->last_valid, N * m, ctx->stream);
+      if (out_flags & (SS_OUT_CLOUD | SS_OUT_NORMALS)) {
+        d2h(np.data(), ctx->npoints.p, sizeof(int) * m, ctx->stream);
+        if (out->index) d2h(out->index + f0 * N, ctx->index.p, sizeof(int) * N * m, ctx->stream);
+        sync(ctx);
+        for (int f = 0; f < m; ++f) {
+          const long k = np[f];
+          if (out->n_points) out->n_points[f0 + f] = (int32_t)k;
+          const long po = (long)(f0 + f) * N * 3, so = (long)f * N * 3;
+          if (out->points)
+            d2h(out->points + po, ctx->pts_f.as<float>() + so, sizeof(float) * 3 * k, ctx->stream);
+          if (out->colors) d2h(out->colors + po, ctx->colors.as<uint8_t>() + so, 3 * k, ctx->stream);
+          if (out->normals && (out_flags & SS_OUT_NORMALS))
+            d2h(out->normals + po, ctx->nrm_f.as<float>() + so, sizeof(float) * 3 * k, ctx->stream);
+        }
+      }
+      sync(ctx);
+    }
+  });
+}
+
+void* ss_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void ss_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

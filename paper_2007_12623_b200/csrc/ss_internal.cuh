@@ -1,0 +1,108 @@
+// Internal declarations shared by the sm_100a kernels and the runtime.
+//
+// HBM layout of one frame (all frame-major; frame f of a batch at f * stride):
+//   gray[N]                  u8  row-major luma (exact path, cloud colours)
+//   plane[H][2][PP]          u8  parity-split rows: [.][0] even columns,
+//                                [.][1] odd columns, PB bytes of zero padding
+//                                each side -> any 4-byte window of a chessboard
+//                                row is two aligned loads + one funnel shift
+//   lstat[N]                 int2 {chessboard sum, float bits of 1/sqrt(var)}
+//   rstat[H][SP]             int2 same for the right image, SPAD padded
+//                                columns each side hold {0, NaN}
+//   vol[NC][H][W]            f32 g(c) = num(c) / sqrt(var_r) for c in
+//                                [d_min-5, d_max+5] (the refine range)
+//   disp/valid               f32/u8 DisparityMap (image.hpp:46-67)
+//   refine state             f64 o, d, avg, b; psum[H][W+1]; cnt[N] (int)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ssb {
+
+constexpr int kDB = 16;        // disparities per thread in the WTA sweep
+constexpr int kRefineR = 5;    // kRefineSearchRadius (params.hpp:38)
+constexpr double kZnccEps = 1e-3;  // kZnccCostEpsilon (params.hpp:34)
+
+struct Geom {
+  int W, H;        // frame size
+  int half;        // window / 2
+  int dmin, dmax;  // candidate range of the WTA
+  int cmin, NC;    // volume range [cmin, cmin + NC)
+  int PB, PP;      // plane padding (bytes) and row pitch (bytes)
+  int SPAD, SP;    // right-stat padding (elements) and row pitch
+  long N() const { return (long)W * H; }
+};
+
+// ---- launchers (stream-ordered, frame index in blockIdx.z / y) ----
+void launch_to_gray(const uint8_t* rgb, uint8_t* gray, long n_pixels, int frames,
+                    long in_stride, long out_stride, cudaStream_t s);
+void launch_planes(const uint8_t* gray, uint8_t* plane, const Geom& g, int frames,
+                   long gray_stride, long plane_stride, cudaStream_t s);
+void launch_stats(const uint8_t* gray, int2* lstat, int2* rstat, int is_right, const Geom& g,
+                  int frames, long gray_stride, long stat_stride, cudaStream_t s);
+void launch_wta11(const uint8_t* lplane, const uint8_t* rplane, const int2* lstat,
+                  const int2* rstat, float* vol, float* disp, uint8_t* valid, int* flag_list,
+                  unsigned int* flag_count, const Geom& g, double min_zncc, int frames,
+                  long plane_stride, long lstat_stride, long rstat_stride, long vol_stride,
+                  long map_stride, int do_argmax, cudaStream_t s);
+void launch_wta_resolve(const uint8_t* lgray, const uint8_t* rgray, const int* flag_list,
+                        const unsigned int* flag_count, float* disp, uint8_t* valid,
+                        const Geom& g, double min_zncc, int frames, long gray_stride,
+                        long map_stride, long flag_stride, unsigned long long* counters,
+                        cudaStream_t s);
+void launch_wta_generic(const uint8_t* lgray, const uint8_t* rgray, float* disp,
+                        uint8_t* valid, const Geom& g, double min_zncc, int frames,
+                        long gray_stride, long map_stride, cudaStream_t s);
+
+void launch_remove_outliers(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
+                            int W, int H, int radius, double thr, int frames, long stride,
+                            cudaStream_t s);
+void launch_fill_radial(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
+                        int W, int H, int radius, int min_support, int frames, long stride,
+                        cudaStream_t s);
+void launch_fill_disc(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
+                      int W, int H, int radius, int min_support, const double* wtab,
+                      int frames, long stride, cudaStream_t s);
+
+struct RefineArgs {
+  Geom g;
+  double alpha, one_minus_alpha, eta, lo, hi;
+  float eta_f;
+  int radius;       // smoothing_radius
+  const int* span;  // [radius + 1]
+};
+void launch_refine_init(const float* disp, const uint8_t* valid, double* o, double* d,
+                        int W, int H, int frames, long stride, cudaStream_t s);
+void launch_row_count(const uint8_t* valid, int* pcnt, int W, int H, int frames, long stride,
+                      long pstride, cudaStream_t s);
+void launch_disc_count(const uint8_t* valid, const int* pcnt, int* cnt, const RefineArgs& a,
+                       int frames, long stride, long pstride, cudaStream_t s);
+void launch_row_scan(const double* val, const uint8_t* valid, double* psum, int W, int H,
+                     int frames, long stride, long pstride, cudaStream_t s);
+void launch_avg_b(const double* psum, const uint8_t* valid, const int* cnt, const double* o,
+                  const double* d, double* avg, double* b, const RefineArgs& a, int frames,
+                  long stride, long pstride, cudaStream_t s);
+void launch_d_repick(const double* psum, const uint8_t* valid, const int* cnt,
+                     const double* avg, double* d, double* o, const uint8_t* lgray,
+                     const uint8_t* rgray, const int2* lstat, const float* vol,
+                     const RefineArgs& a, int frames, long stride, long pstride,
+                     long gray_stride, long lstat_stride, long vol_stride,
+                     unsigned long long* counters, cudaStream_t s);
+void launch_refine_out(const double* d, const uint8_t* valid, const float* din, float* dout,
+                       int W, int H, int frames, long stride, cudaStream_t s);
+
+struct CloudArgs {
+  double fx, fy, cx, cy, baseline;
+};
+void launch_cloud_index(const float* disp, const uint8_t* valid, int* index, int* block_sums,
+                        int* n_points, int W, int H, int frames, long stride, cudaStream_t s);
+void launch_cloud_points(const float* disp, const int* index, const uint8_t* rgb, int cw,
+                         int ch, int W, int H, const CloudArgs& c, double* pts_d,
+                         float* pts_f, uint8_t* colors, int* pixels, int frames, long stride,
+                         long rgb_stride, cudaStream_t s);
+void launch_cloud_normals(const float* disp, const int* index, const CloudArgs& c,
+                          double* nrm_d, float* nrm_f, int W, int H, int frames, long stride,
+                          cudaStream_t s);
+
+}  // namespace ssb
