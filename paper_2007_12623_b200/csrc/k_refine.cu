@@ -12,7 +12,7 @@
 //                 (smoothing.cpp:114-146): argmin over integer candidates of
 //                 1/max(zncc, 1e-3) + (eta diff) diff, strict < (first min).
 //                 Candidate costs come from the WTA cost volume in FP32 with a
-//                 rigorous 1.6e-5 relative margin; when more than one
+//                 rigorous 4e-6 relative margin (error <= 7 ulp = 4.2e-7); when more than one
 //                 candidate lies within the margin of the minimum, those
 //                 candidates are re-scored in exact FP64 (zncc_exact), so the
 //                 pick equals the reference's. Without a volume (window != 11)
@@ -233,6 +233,23 @@ __global__ void k_d_repick(const double* __restrict__ psum, const uint8_t* __res
 
   float rl = __int_as_float(0x7fc00000);
   if (fits) rl = __int_as_float(__ldg(&lstat[f * lstat_stride + pix].y));
+  if (isnan(rl)) {
+    // Window does not fit or var_l == 0: every match cost is exactly
+    // 1/kZnccCostEpsilon, so the reference's double costs are computed as is.
+    const double m = __ddiv_rn(1.0, kZnccEps);
+    double best_cost = 0.0;
+    int best = c_lo;
+    for (int c = c_lo; c <= c_hi; ++c) {
+      const double diff = __dsub_rn((double)c, dv);
+      const double cost = __dadd_rn(m, __dmul_rn(__dmul_rn(a.eta, diff), diff));
+      if (c == c_lo || cost < best_cost) {
+        best_cost = cost;
+        best = c;
+      }
+    }
+    o[i] = best;
+    return;
+  }
   const float* vp = vol + f * vol_stride + pix;
   const long HW = (long)H * W;
   float cf[kMaxCand];
@@ -258,7 +275,7 @@ __global__ void k_d_repick(const double* __restrict__ psum, const uint8_t* __res
     }
   }
   // Any candidate whose exact cost could undercut the float minimum.
-  const float thr = best_f * (1.0f + 1.6e-5f);
+  const float thr = best_f * (1.0f + 4e-6f);
   int near = 0;
 #pragma unroll
   for (int k = 0; k < kMaxCand; ++k) near += (cf[k] <= thr) ? 1 : 0;

@@ -22,6 +22,7 @@
 // k_wta_exact — one warp per pixel, lanes over d, reference arithmetic
 //   (zncc_chessboard int64 statistics, double score, first maximum). Used for
 //   the flagged pixels and, over all pixels, for windows other than 11.
+#include <limits.h>
 #include <math.h>
 
 #include <utility>
@@ -34,6 +35,7 @@ namespace ssb {
 namespace {
 
 constexpr int kRB = 4;  // output rows per shared-memory reduction chunk
+constexpr int kNoArg = INT_MIN;  // "no defined candidate" (disparities may be negative)
 
 __device__ __forceinline__ uint32_t ld_win(const uint8_t* row, int start) {
   const uint32_t* w = reinterpret_cast<const uint32_t*>(row);
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(512) k_wta11(
       }
     }
     float best = -INFINITY, second = -INFINITY;
-    int arg = -1;
+    int arg = kNoArg;
     if (active) {
       const int sl = __ldg(&lstat[(long)v * W + u].x);
       const int2* rrow = rstat + (long)v * g.SP + g.SPAD + ru0;
@@ -232,11 +234,11 @@ __global__ void __launch_bounds__(512) k_wta11(
       __syncthreads();
       for (int r = j; r <= slot; r += NB) {
         float B = -INFINITY, S = -INFINITY;
-        int A = -1;
+        int A = kNoArg;
         for (int jj = 0; jj < NB; ++jj) {
           const int o = (r * NB + jj) * 32 + lane;
           const int a = s_arg[o];
-          if (a < 0) continue;
+          if (a == kNoArg) continue;
           const float b = s_best[o], s2 = s_sec[o];
           if (b > B) {
             S = fmaxf(B, s2);
@@ -252,7 +254,7 @@ __global__ void __launch_bounds__(512) k_wta11(
           const float rl = __int_as_float(__ldg(&lstat[idx].y));
           float dout = 0.f;
           uint8_t vout = 0;
-          if (A >= 0 && !isnan(rl)) {
+          if (A != kNoArg && !isnan(rl)) {
             const bool near_tie = S >= B - 4e-6f * fabsf(B);
             const float sc = B * rl;
             const bool amb = fabsf(sc - min_zncc_f) <= thr_tol;
