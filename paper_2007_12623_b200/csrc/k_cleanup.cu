@@ -9,11 +9,12 @@
 //   k_fill_radial      cleanup.cpp:54-68 — nearest valid hit per ray <= R,
 //                      IDW w = 1/(step * {1, sqrt2}), double sums in direction
 //                      order 0..7 (the reference's order, so bit-exact).
-//   k_fill_disc        cleanup.cpp:69-84 — all valid pixels of the radius-R
-//                      disc in raster order, w = 1/sqrt(dd) from a table built
-//                      with the same IEEE double ops on the host. The support
-//                      count (integer) is taken first; the FP64 sums run only
-//                      for pixels that will be filled.
+//   k_disc_select /    cleanup.cpp:69-84 — support of every invalid pixel from
+//   k_disc_sum         per-row prefix counts (exact integers); only pixels that
+//                      will be filled enter a compacted list, and one thread
+//                      per listed pixel accumulates all valid pixels of the
+//                      radius-R disc in raster order in FP64, w = 1/sqrt(dd)
+//                      from a table built with the same IEEE ops on the host.
 // All maps of a frame stay L2-resident (5 B/pixel); these passes are a few
 // percent of the frame and latency-, not bandwidth-bound.
 #include <math.h>
@@ -111,56 +112,71 @@ __global__ void k_fill_radial(const float* __restrict__ din, const uint8_t* __re
   vout[i] = ov;
 }
 
-__global__ void k_fill_disc(const float* __restrict__ din, const uint8_t* __restrict__ vin,
-                            float* __restrict__ dout, uint8_t* __restrict__ vout, int W, int H,
-                            int radius, int min_support, const double* __restrict__ wtab,
-                            long stride) {
+// Disc fill, pass 1: copy the map through and, for invalid pixels, count the
+// valid disc neighbours from per-row prefix counts (exact integers, 2 loads
+// per disc row). Pixels that will be filled go to a per-frame list.
+__global__ void k_disc_select(const float* __restrict__ din, const uint8_t* __restrict__ vin,
+                              float* __restrict__ dout, uint8_t* __restrict__ vout,
+                              const int* __restrict__ pcnt, const int* __restrict__ span,
+                              int* __restrict__ list, unsigned* __restrict__ count, int W, int H,
+                              int radius, int min_support, long stride, long pstride) {
   const long f = blockIdx.z;
-  din += f * stride;
-  vin += f * stride;
-  dout += f * stride;
-  vout += f * stride;
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = blockIdx.y * blockDim.y + threadIdx.y;
   if (u >= W || v >= H) return;
-  const long i = (long)v * W + u;
-  float od = din[i];
-  uint8_t ov = vin[i];
-  if (!ov) {
-    const int r2 = radius * radius;
-    const int v0 = max(-radius, -v), v1 = min(radius, H - 1 - v);
-    // Pass 1: integer support count (decides whether a fill happens).
-    int support = 0;
-    for (int dv = v0; dv <= v1; ++dv) {
-      const int span = (int)floor(sqrt((double)(r2 - dv * dv)));
-      const int a = max(-span, -u), b = min(span, W - 1 - u);
-      const uint8_t* row = vin + (long)(v + dv) * W + u;
-      for (int du = a; du <= b; ++du) support += __ldg(row + du);
-    }
-    support -= 0;  // the centre is invalid, so it never counted
-    if (support >= min_support && support > 0) {
-      // Pass 2: reference-order double sums (raster dv, du).
-      double wsum = 0.0, vsum = 0.0;
-      for (int dv = v0; dv <= v1; ++dv) {
-        const int span = (int)floor(sqrt((double)(r2 - dv * dv)));
-        const int a = max(-span, -u), b = min(span, W - 1 - u);
-        const uint8_t* row = vin + (long)(v + dv) * W + u;
-        const float* drow = din + (long)(v + dv) * W + u;
-        for (int du = a; du <= b; ++du) {
-          if (!__ldg(row + du)) continue;
-          const double w = wtab[du * du + dv * dv];
-          wsum = __dadd_rn(wsum, w);
-          vsum = __dadd_rn(vsum, __dmul_rn(w, (double)__ldg(drow + du)));
-        }
-      }
-      if (wsum > 0.0) {
-        od = (float)__ddiv_rn(vsum, wsum);
-        ov = 1;
-      }
-    }
-  }
+  const long i = f * stride + (long)v * W + u;
+  const float od = din[i];
+  const uint8_t ov = vin[i];
   dout[i] = od;
   vout[i] = ov;
+  if (ov || radius <= 0) return;
+  const int* pc = pcnt + f * pstride;
+  const int v0 = max(-radius, -v), v1 = min(radius, H - 1 - v);
+  int support = 0;
+  for (int dv = v0; dv <= v1; ++dv) {
+    const int sx = __ldg(span + (dv < 0 ? -dv : dv));
+    const int* row = pc + (long)(v + dv) * (W + 1);
+    support += __ldg(row + min(W - 1, u + sx) + 1) - __ldg(row + max(0, u - sx));
+  }
+  // The centre is invalid, so it never contributes (cleanup.cpp:74 skips dd == 0).
+  if (support >= min_support && support > 0)
+    list[f * stride + atomicAdd(count + f, 1u)] = (int)((long)v * W + u);
+}
+
+// Disc fill, pass 2: one thread per listed pixel, the reference's raster-order
+// double accumulation (cleanup.cpp:71-83), w = 1/sqrt(dd) from a host table.
+__global__ void k_disc_sum(const float* __restrict__ din, const uint8_t* __restrict__ vin,
+                           float* __restrict__ dout, uint8_t* __restrict__ vout,
+                           const int* __restrict__ list, const unsigned* __restrict__ count,
+                           const int* __restrict__ span, const double* __restrict__ wtab, int W,
+                           int H, int radius, long stride) {
+  const long f = blockIdx.y;
+  const unsigned n = count[f];
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int idx = list[f * stride + t];
+    const int v = idx / W, u = idx % W;
+    const uint8_t* vf = vin + f * stride;
+    const float* df = din + f * stride;
+    const int v0 = max(-radius, -v), v1 = min(radius, H - 1 - v);
+    double wsum = 0.0, vsum = 0.0;
+    for (int dv = v0; dv <= v1; ++dv) {
+      const int sx = __ldg(span + (dv < 0 ? -dv : dv));
+      const int a = max(-sx, -u), b = min(sx, W - 1 - u);
+      const uint8_t* row = vf + (long)(v + dv) * W + u;
+      const float* drow = df + (long)(v + dv) * W + u;
+      const int dv2 = dv * dv;
+      for (int du = a; du <= b; ++du) {
+        if (!__ldg(row + du)) continue;
+        const double w = __ldg(wtab + du * du + dv2);
+        wsum = __dadd_rn(wsum, w);
+        vsum = __dadd_rn(vsum, __dmul_rn(w, (double)__ldg(drow + du)));
+      }
+    }
+    if (wsum > 0.0) {
+      dout[f * stride + idx] = (float)__ddiv_rn(vsum, wsum);
+      vout[f * stride + idx] = 1;
+    }
+  }
 }
 
 static dim3 map_grid(int W, int H, int frames, dim3 b) {
@@ -187,11 +203,18 @@ void launch_fill_radial(const float* din, const uint8_t* vin, float* dout, uint8
 
 void launch_fill_disc(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
                       int W, int H, int radius, int min_support, const double* wtab,
-                      int frames, long stride, cudaStream_t s) {
+                      const int* span, int* pcnt, int* list, unsigned* count, int frames,
+                      long stride, cudaStream_t s) {
   if (W <= 0 || H <= 0 || frames <= 0) return;
+  const long pstride = (long)H * (W + 1);
+  launch_row_count(vin, pcnt, W, H, frames, stride, pstride, s);
+  cudaMemsetAsync(count, 0, sizeof(unsigned) * frames, s);
   dim3 b(32, 8);
-  k_fill_disc<<<map_grid(W, H, frames, b), b, 0, s>>>(din, vin, dout, vout, W, H, radius,
-                                                      min_support, wtab, stride);
+  k_disc_select<<<map_grid(W, H, frames, b), b, 0, s>>>(din, vin, dout, vout, pcnt, span, list,
+                                                        count, W, H, radius, min_support, stride,
+                                                        pstride);
+  k_disc_sum<<<dim3(96, frames), 256, 0, s>>>(din, vin, dout, vout, list, count, span, wtab, W,
+                                             H, radius, stride);
 }
 
 }  // namespace ssb

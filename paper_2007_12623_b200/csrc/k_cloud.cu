@@ -144,17 +144,22 @@ __device__ __forceinline__ void point_of(const CloudArgs& c, int u, int v, doubl
 __global__ void k_cloud_points(const float* __restrict__ disp, const int* __restrict__ index,
                                const uint8_t* __restrict__ rgb, int cw, int ch, int W, int H,
                                CloudArgs c, double* __restrict__ pts_d, float* __restrict__ pts_f,
-                               uint8_t* __restrict__ colors, int* __restrict__ pixels,
-                               long stride, long rgb_stride) {
+                               float4* __restrict__ pts4, uint8_t* __restrict__ colors,
+                               int* __restrict__ pixels, long stride, long rgb_stride) {
   const long f = blockIdx.z;
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = blockIdx.y * blockDim.y + threadIdx.y;
   if (u >= W || v >= H) return;
   const long i = (long)v * W + u;
   const int k = index[f * stride + i];
-  if (k < 0) return;
+  if (k < 0) {
+    pts4[f * stride + i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
   double p[3];
   point_of(c, u, v, (double)disp[f * stride + i], p);
+  // pixel-indexed copy for the normal fit (w = 1 marks a point)
+  pts4[f * stride + i] = make_float4((float)p[0], (float)p[1], (float)p[2], 1.f);
   const long o = f * stride * 3 + 3l * k;
   if (pts_d) {
     pts_d[o + 0] = p[0];
@@ -186,22 +191,25 @@ __global__ void k_cloud_points(const float* __restrict__ disp, const int* __rest
 
 void launch_cloud_points(const float* disp, const int* index, const uint8_t* rgb, int cw,
                          int ch, int W, int H, const CloudArgs& c, double* pts_d,
-                         float* pts_f, uint8_t* colors, int* pixels, int frames, long stride,
-                         long rgb_stride, cudaStream_t s) {
+                         float* pts_f, float4* pts4, uint8_t* colors, int* pixels, int frames,
+                         long stride, long rgb_stride, cudaStream_t s) {
   if (W <= 0 || H <= 0 || frames <= 0) return;
   dim3 b(32, 8);
   dim3 grid((W + 31) / 32, (H + 7) / 8, frames);
-  k_cloud_points<<<grid, b, 0, s>>>(disp, index, rgb, cw, ch, W, H, c, pts_d, pts_f, colors,
-                                    pixels, stride, rgb_stride);
+  k_cloud_points<<<grid, b, 0, s>>>(disp, index, rgb, cw, ch, W, H, c, pts_d, pts_f, pts4,
+                                    colors, pixels, stride, rgb_stride);
 }
 
-// Smallest-eigenvalue eigenvector of a symmetric 3x3 (a00 a01 a02 a11 a12 a22).
-__device__ void sym3_smallest(const double a[6], double ev[3], double n[3]) {
-  const double a00 = a[0], a01 = a[1], a02 = a[2], a11 = a[3], a12 = a[4], a22 = a[5];
-  const double p1 = a01 * a01 + a02 * a02 + a12 * a12;
-  if (p1 == 0.0) {
-    // Diagonal: eigenvalues are the diagonal entries, eigenvectors the axes.
-    double d[3] = {a00, a11, a22};
+// Smallest eigenpair of a symmetric 3x3 (a00 a01 a02 a11 a12 a22):
+// trigonometric eigenvalues, eigenvector from the best-conditioned cross
+// product of two rows of (A - l0 I). T = float on the fast path, double for
+// the near-degenerate re-check.
+template <typename T>
+__device__ void sym3_smallest(const T a[6], T ev[3], T n[3]) {
+  const T a00 = a[0], a01 = a[1], a02 = a[2], a11 = a[3], a12 = a[4], a22 = a[5];
+  const T p1 = a01 * a01 + a02 * a02 + a12 * a12;
+  if (p1 == T(0)) {
+    T d[3] = {a00, a11, a22};
     int id[3] = {0, 1, 2};
     for (int x = 0; x < 3; ++x)
       for (int y = x + 1; y < 3; ++y)
@@ -211,153 +219,199 @@ __device__ void sym3_smallest(const double a[6], double ev[3], double n[3]) {
           id[y] = t;
         }
     for (int x = 0; x < 3; ++x) ev[x] = d[id[x]];
-    n[0] = id[0] == 0 ? 1.0 : 0.0;
-    n[1] = id[0] == 1 ? 1.0 : 0.0;
-    n[2] = id[0] == 2 ? 1.0 : 0.0;
+    n[0] = id[0] == 0 ? T(1) : T(0);
+    n[1] = id[0] == 1 ? T(1) : T(0);
+    n[2] = id[0] == 2 ? T(1) : T(0);
     return;
   }
-  const double q = (a00 + a11 + a22) / 3.0;
-  const double b00 = a00 - q, b11 = a11 - q, b22 = a22 - q;
-  const double p2 = b00 * b00 + b11 * b11 + b22 * b22 + 2.0 * p1;
-  const double p = sqrt(p2 / 6.0);
-  const double det = b00 * (b11 * b22 - a12 * a12) - a01 * (a01 * b22 - a12 * a02) +
-                     a02 * (a01 * a12 - b11 * a02);
-  double r = det / (2.0 * p * p * p);
-  r = r < -1.0 ? -1.0 : (r > 1.0 ? 1.0 : r);
-  const double phi = acos(r) / 3.0;
-  const double e2 = q + 2.0 * p * cos(phi);
-  const double e0 = q + 2.0 * p * cos(phi + 2.0943951023931954923);  // + 2 pi / 3
-  const double e1 = 3.0 * q - e0 - e2;
+  const T q = (a00 + a11 + a22) / T(3);
+  const T b00 = a00 - q, b11 = a11 - q, b22 = a22 - q;
+  const T p2 = b00 * b00 + b11 * b11 + b22 * b22 + T(2) * p1;
+  const T p = sqrt(p2 / T(6));
+  const T det = b00 * (b11 * b22 - a12 * a12) - a01 * (a01 * b22 - a12 * a02) +
+                a02 * (a01 * a12 - b11 * a02);
+  T r = det / (T(2) * p * p * p);
+  r = r < T(-1) ? T(-1) : (r > T(1) ? T(1) : r);
+  const T phi = acos(r) / T(3);
+  const T e2 = q + T(2) * p * cos(phi);
+  const T e0 = q + T(2) * p * cos(phi + T(2.0943951023931954923));  // + 2 pi / 3
+  const T e1 = T(3) * q - e0 - e2;
   ev[0] = e0;
   ev[1] = e1;
   ev[2] = e2;
-  const double r0[3] = {a00 - e0, a01, a02};
-  const double r1[3] = {a01, a11 - e0, a12};
-  const double r2[3] = {a02, a12, a22 - e0};
-  double c[3][3];
-  c[0][0] = r0[1] * r1[2] - r0[2] * r1[1];
-  c[0][1] = r0[2] * r1[0] - r0[0] * r1[2];
-  c[0][2] = r0[0] * r1[1] - r0[1] * r1[0];
-  c[1][0] = r0[1] * r2[2] - r0[2] * r2[1];
-  c[1][1] = r0[2] * r2[0] - r0[0] * r2[2];
-  c[1][2] = r0[0] * r2[1] - r0[1] * r2[0];
-  c[2][0] = r1[1] * r2[2] - r1[2] * r2[1];
-  c[2][1] = r1[2] * r2[0] - r1[0] * r2[2];
-  c[2][2] = r1[0] * r2[1] - r1[1] * r2[0];
+  const T r0[3] = {a00 - e0, a01, a02};
+  const T r1[3] = {a01, a11 - e0, a12};
+  const T r2[3] = {a02, a12, a22 - e0};
+  T cr[3][3];
+  cr[0][0] = r0[1] * r1[2] - r0[2] * r1[1];
+  cr[0][1] = r0[2] * r1[0] - r0[0] * r1[2];
+  cr[0][2] = r0[0] * r1[1] - r0[1] * r1[0];
+  cr[1][0] = r0[1] * r2[2] - r0[2] * r2[1];
+  cr[1][1] = r0[2] * r2[0] - r0[0] * r2[2];
+  cr[1][2] = r0[0] * r2[1] - r0[1] * r2[0];
+  cr[2][0] = r1[1] * r2[2] - r1[2] * r2[1];
+  cr[2][1] = r1[2] * r2[0] - r1[0] * r2[2];
+  cr[2][2] = r1[0] * r2[1] - r1[1] * r2[0];
   int bi = 0;
-  double bn = -1.0;
+  T bn = T(-1);
   for (int k = 0; k < 3; ++k) {
-    const double m = c[k][0] * c[k][0] + c[k][1] * c[k][1] + c[k][2] * c[k][2];
+    const T m = cr[k][0] * cr[k][0] + cr[k][1] * cr[k][1] + cr[k][2] * cr[k][2];
     if (m > bn) {
       bn = m;
       bi = k;
     }
   }
-  const double inv = 1.0 / sqrt(bn);
-  n[0] = c[bi][0] * inv;
-  n[1] = c[bi][1] * inv;
-  n[2] = c[bi][2] * inv;
+  const T inv = T(1) / sqrt(bn);
+  n[0] = cr[bi][0] * inv;
+  n[1] = cr[bi][1] * inv;
+  n[2] = cr[bi][2] * inv;
 }
 
-__global__ void k_cloud_normals(const float* __restrict__ disp, const int* __restrict__ index,
-                                int W, int H, CloudArgs c, double* __restrict__ nrm_d,
-                                float* __restrict__ nrm_f, long stride) {
+constexpr int kNW = 3;            // kNormalWindowHalf (cloud.cpp:10)
+constexpr int kNTX = 32, kNTY = 8;  // output tile
+
+// Normals from a shared-memory tile of pixel-indexed float points. Neighbour
+// coordinates are taken relative to the centre point (local frame, no
+// cancellation at 100 mm depth), mean and covariance in two passes. Windows
+// whose middle eigenvalue is within 1e-4 of degenerate are re-fitted in FP64
+// so the reference's 1e-9 acceptance test (cloud.cpp:81) decides them.
+__global__ void __launch_bounds__(kNTX * kNTY)
+    k_cloud_normals(const float4* __restrict__ pts4, const float* __restrict__ disp, int W,
+                    int H, CloudArgs cargs, double* __restrict__ nrm_d,
+                    float* __restrict__ nrm_f, const int* __restrict__ index, long stride) {
+  __shared__ float4 tile[kNTY + 2 * kNW][kNTX + 2 * kNW];
   const long f = blockIdx.z;
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  const int v = blockIdx.y * blockDim.y + threadIdx.y;
-  if (u >= W || v >= H) return;
-  disp += f * stride;
-  index += f * stride;
-  const int k = index[(long)v * W + u];
-  if (k < 0) return;
-  double p[3];
-  point_of(c, u, v, (double)disp[(long)v * W + u], p);
-  double mean[3] = {0.0, 0.0, 0.0};
-  int count = 0;
-  for (int dv = -3; dv <= 3; ++dv) {
-    const int nv = v + dv;
-    if (nv < 0 || nv >= H) continue;
-    for (int du = -3; du <= 3; ++du) {
-      const int nu = u + du;
-      if (nu < 0 || nu >= W) continue;
-      const long ni = (long)nv * W + nu;
-      if (__ldg(index + ni) < 0) continue;
-      double q[3];
-      point_of(c, nu, nv, (double)__ldg(disp + ni), q);
-      mean[0] += q[0];
-      mean[1] += q[1];
-      mean[2] += q[2];
-      ++count;
-    }
+  pts4 += f * stride;
+  const int bx = blockIdx.x * kNTX, by = blockIdx.y * kNTY;
+  for (int t = threadIdx.y * kNTX + threadIdx.x; t < (kNTY + 2 * kNW) * (kNTX + 2 * kNW);
+       t += kNTX * kNTY) {
+    const int ty = t / (kNTX + 2 * kNW), tx = t % (kNTX + 2 * kNW);
+    const int gx = bx + tx - kNW, gy = by + ty - kNW;
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (gx >= 0 && gx < W && gy >= 0 && gy < H) q = pts4[(long)gy * W + gx];
+    tile[ty][tx] = q;
   }
-  double n[3] = {0.0, 0.0, -1.0};
-  bool fitted = false;
-  if (count >= 3) {
-    mean[0] /= count;
-    mean[1] /= count;
-    mean[2] /= count;
-    double a[6] = {0, 0, 0, 0, 0, 0};
-    for (int dv = -3; dv <= 3; ++dv) {
-      const int nv = v + dv;
-      if (nv < 0 || nv >= H) continue;
-      for (int du = -3; du <= 3; ++du) {
-        const int nu = u + du;
-        if (nu < 0 || nu >= W) continue;
-        const long ni = (long)nv * W + nu;
-        if (__ldg(index + ni) < 0) continue;
-        double q[3];
-        point_of(c, nu, nv, (double)__ldg(disp + ni), q);
-        q[0] -= mean[0];
-        q[1] -= mean[1];
-        q[2] -= mean[2];
-        a[0] += q[0] * q[0];
-        a[1] += q[0] * q[1];
-        a[2] += q[0] * q[2];
-        a[3] += q[1] * q[1];
-        a[4] += q[1] * q[2];
-        a[5] += q[2] * q[2];
+  __syncthreads();
+  const int u = bx + threadIdx.x, v = by + threadIdx.y;
+  if (u >= W || v >= H) return;
+  const float4 c = tile[threadIdx.y + kNW][threadIdx.x + kNW];
+  if (c.w == 0.f) return;
+  const int k = index[f * stride + (long)v * W + u];
+  float sx = 0.f, sy = 0.f, sz = 0.f;
+  int count = 0;
+#pragma unroll
+  for (int dv = 0; dv <= 2 * kNW; ++dv)
+#pragma unroll
+    for (int du = 0; du <= 2 * kNW; ++du) {
+      const float4 q = tile[threadIdx.y + dv][threadIdx.x + du];
+      if (q.w != 0.f) {
+        sx += q.x - c.x;
+        sy += q.y - c.y;
+        sz += q.z - c.z;
+        ++count;
       }
     }
-    double ev[3], e[3];
-    sym3_smallest(a, ev, e);
-    if (ev[1] > 1e-9 * fmax(1.0, ev[2])) {
+  float n[3] = {0.f, 0.f, -1.f};
+  bool fitted = false;
+  if (count >= 3) {
+    const float inv = 1.f / (float)count;
+    const float mx = sx * inv, my = sy * inv, mz = sz * inv;
+    float a[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int dv = 0; dv <= 2 * kNW; ++dv)
+#pragma unroll
+      for (int du = 0; du <= 2 * kNW; ++du) {
+        const float4 q = tile[threadIdx.y + dv][threadIdx.x + du];
+        if (q.w != 0.f) {
+          const float x = (q.x - c.x) - mx, y = (q.y - c.y) - my, z = (q.z - c.z) - mz;
+          a[0] += x * x;
+          a[1] += x * y;
+          a[2] += x * z;
+          a[3] += y * y;
+          a[4] += y * z;
+          a[5] += z * z;
+        }
+      }
+    float ev[3], e[3];
+    sym3_smallest<float>(a, ev, e);
+    const float scale = fmaxf(1.f, ev[2]);
+    if (ev[1] > 1e-4f * scale) {
       n[0] = e[0];
       n[1] = e[1];
       n[2] = e[2];
       fitted = true;
+    } else {
+      // Near-degenerate neighbourhood: refit in FP64 from FP64 points.
+      double pd[3];
+      double mean[3] = {0.0, 0.0, 0.0};
+      for (int dv = -kNW; dv <= kNW; ++dv)
+        for (int du = -kNW; du <= kNW; ++du) {
+          if (tile[threadIdx.y + kNW + dv][threadIdx.x + kNW + du].w == 0.f) continue;
+          point_of(cargs, u + du, v + dv, (double)disp[f * stride + (long)(v + dv) * W + u + du], pd);
+          mean[0] += pd[0];
+          mean[1] += pd[1];
+          mean[2] += pd[2];
+        }
+      mean[0] /= count;
+      mean[1] /= count;
+      mean[2] /= count;
+      double ad[6] = {0, 0, 0, 0, 0, 0};
+      for (int dv = -kNW; dv <= kNW; ++dv)
+        for (int du = -kNW; du <= kNW; ++du) {
+          if (tile[threadIdx.y + kNW + dv][threadIdx.x + kNW + du].w == 0.f) continue;
+          point_of(cargs, u + du, v + dv, (double)disp[f * stride + (long)(v + dv) * W + u + du], pd);
+          const double x = pd[0] - mean[0], y = pd[1] - mean[1], z = pd[2] - mean[2];
+          ad[0] += x * x;
+          ad[1] += x * y;
+          ad[2] += x * z;
+          ad[3] += y * y;
+          ad[4] += y * z;
+          ad[5] += z * z;
+        }
+      double evd[3], ed[3];
+      sym3_smallest<double>(ad, evd, ed);
+      if (evd[1] > 1e-9 * fmax(1.0, evd[2])) {
+        n[0] = (float)ed[0];
+        n[1] = (float)ed[1];
+        n[2] = (float)ed[2];
+        fitted = true;
+      }
     }
   }
+  double nd[3] = {n[0], n[1], n[2]};
+  double pc[3];
+  point_of(cargs, u, v, (double)disp[f * stride + (long)v * W + u], pc);
   if (!fitted) {
-    const double len = sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
-    n[0] = -p[0] / len;
-    n[1] = -p[1] / len;
-    n[2] = -p[2] / len;
+    const double len = sqrt(pc[0] * pc[0] + pc[1] * pc[1] + pc[2] * pc[2]);
+    nd[0] = -pc[0] / len;
+    nd[1] = -pc[1] / len;
+    nd[2] = -pc[2] / len;
   }
-  if (n[0] * p[0] + n[1] * p[1] + n[2] * p[2] > 0.0) {
-    n[0] = -n[0];
-    n[1] = -n[1];
-    n[2] = -n[2];
+  if (nd[0] * pc[0] + nd[1] * pc[1] + nd[2] * pc[2] > 0.0) {
+    nd[0] = -nd[0];
+    nd[1] = -nd[1];
+    nd[2] = -nd[2];
   }
   const long o = f * stride * 3 + 3l * k;
   if (nrm_d) {
-    nrm_d[o + 0] = n[0];
-    nrm_d[o + 1] = n[1];
-    nrm_d[o + 2] = n[2];
+    nrm_d[o + 0] = nd[0];
+    nrm_d[o + 1] = nd[1];
+    nrm_d[o + 2] = nd[2];
   }
   if (nrm_f) {
-    nrm_f[o + 0] = (float)n[0];
-    nrm_f[o + 1] = (float)n[1];
-    nrm_f[o + 2] = (float)n[2];
+    nrm_f[o + 0] = (float)nd[0];
+    nrm_f[o + 1] = (float)nd[1];
+    nrm_f[o + 2] = (float)nd[2];
   }
 }
 
-void launch_cloud_normals(const float* disp, const int* index, const CloudArgs& c,
-                          double* nrm_d, float* nrm_f, int W, int H, int frames, long stride,
-                          cudaStream_t s) {
+void launch_cloud_normals(const float4* pts4, const float* disp, const int* index,
+                          const CloudArgs& c, double* nrm_d, float* nrm_f, int W, int H,
+                          int frames, long stride, cudaStream_t s) {
   if (W <= 0 || H <= 0 || frames <= 0) return;
-  dim3 b(32, 8);
-  dim3 grid((W + 31) / 32, (H + 7) / 8, frames);
-  k_cloud_normals<<<grid, b, 0, s>>>(disp, index, W, H, c, nrm_d, nrm_f, stride);
+  dim3 b(kNTX, kNTY);
+  dim3 grid((W + kNTX - 1) / kNTX, (H + kNTY - 1) / kNTY, frames);
+  k_cloud_normals<<<grid, b, 0, s>>>(pts4, disp, W, H, c, nrm_d, nrm_f, index, stride);
 }
 
 }  // namespace ssb

@@ -18,6 +18,7 @@
 //                 pick equals the reference's. Without a volume (window != 11)
 //                 every candidate is scored exactly.
 // The mask is fixed, so the per-pixel disc count is computed once (k_disc_count).
+#include <limits.h>
 #include <math.h>
 
 #include "exact.cuh"
@@ -48,27 +49,6 @@ void launch_refine_init(const float* disp, const uint8_t* valid, double* o, doub
   long blocks = (n + 255) / 256;
   if (blocks > 2048) blocks = 2048;
   k_refine_init<<<dim3((unsigned)blocks, frames), 256, 0, s>>>(disp, valid, o, d, n, stride);
-}
-
-__global__ void k_row_count(const uint8_t* __restrict__ valid, int* __restrict__ pcnt, int W,
-                            int H, long stride, long pstride) {
-  const long f = blockIdx.y;
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= H) return;
-  const uint8_t* m = valid + f * stride + (long)v * W;
-  int* p = pcnt + f * pstride + (long)v * (W + 1);
-  int c = 0;
-  p[0] = 0;
-  for (int u = 0; u < W; ++u) {
-    c += m[u] ? 1 : 0;
-    p[u + 1] = c;
-  }
-}
-
-void launch_row_count(const uint8_t* valid, int* pcnt, int W, int H, int frames, long stride,
-                      long pstride, cudaStream_t s) {
-  if (W <= 0 || H <= 0 || frames <= 0) return;
-  k_row_count<<<dim3((H + 63) / 64, frames), 64, 0, s>>>(valid, pcnt, W, H, stride, pstride);
 }
 
 __global__ void k_disc_count(const uint8_t* __restrict__ valid, const int* __restrict__ pcnt,
@@ -105,69 +85,98 @@ void launch_disc_count(const uint8_t* valid, const int* pcnt, int* cnt, const Re
   k_disc_count<<<grid, b, 0, s>>>(valid, pcnt, cnt, a, stride, pstride);
 }
 
-// Serial masked row prefix in double: the reference's exact summation order.
-__global__ void k_row_scan(const double* __restrict__ val, const uint8_t* __restrict__ valid,
-                           double* __restrict__ psum, int W, int H, long stride, long pstride) {
-  const long f = blockIdx.y;
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= H) return;
-  const double* x = val + f * stride + (long)v * W;
-  const uint8_t* m = valid + f * stride + (long)v * W;
-  double* p = psum + f * pstride + (long)v * (W + 1);
-  double s = 0.0;
-  p[0] = 0.0;
-  for (int u = 0; u < W; ++u) {
-    if (m[u]) s = __dadd_rn(s, x[u]);
-    p[u + 1] = s;
+// ---- disc sums of a masked field from its row prefixes (smoothing.cpp:43-63) ----
+//
+// The reference sums, for dy ascending, the span difference
+// psum[row][u1+1] - psum[row][u0] of each disc row. Both gathers run on a
+// 32 x 16 pixel tile whose psum rows/columns (plus the radius halo) are staged
+// in shared memory once, so the 2 (2R+1) reads per pixel are LDS, not L2
+// round trips. Summation order and operands are the reference's: bit-exact.
+
+constexpr int kTX = 32, kTY = 16, kBY = 8;  // tile = 32 x 16 pixels, block = 32 x 8
+
+struct PsumTile {
+  const double* t;  // smem [(kTY + 2R)][(kTX + 2R + 1)]
+  int pitch, u0, v0;  // psum column of t[.][0] is u0 - R; row of t[0] is v0 - R
+};
+
+__host__ __device__ inline int tile_pitch(int R) { return kTX + 2 * R + 1; }
+__host__ __device__ inline size_t tile_bytes(int R) {
+  return sizeof(double) * (size_t)(kTY + 2 * R) * tile_pitch(R) + sizeof(int) * (R + 1);
+}
+
+__device__ __forceinline__ PsumTile load_tile(const double* __restrict__ psum, int W, int H,
+                                             int R, const int* __restrict__ span_g,
+                                             int*& span) {
+  extern __shared__ double tile_mem[];
+  const int pitch = tile_pitch(R);
+  const int rows = kTY + 2 * R;
+  const int u0 = blockIdx.x * kTX, v0 = blockIdx.y * kTY;
+  span = reinterpret_cast<int*>(tile_mem + (size_t)rows * pitch);
+  const int tid = threadIdx.y * kTX + threadIdx.x;
+  for (int k = tid; k <= R; k += kTX * kBY) span[k] = __ldg(span_g + k);
+  for (int k = tid; k < rows * pitch; k += kTX * kBY) {
+    const int r = k / pitch, c = k % pitch;
+    const int pr = v0 - R + r, pc = u0 - R + c;
+    double x = 0.0;
+    if (pr >= 0 && pr < H && pc >= 0 && pc <= W) x = __ldg(psum + (long)pr * (W + 1) + pc);
+    tile_mem[k] = x;
   }
+  __syncthreads();
+  return PsumTile{tile_mem, pitch, u0, v0};
 }
 
-void launch_row_scan(const double* val, const uint8_t* valid, double* psum, int W, int H,
-                     int frames, long stride, long pstride, cudaStream_t s) {
-  if (W <= 0 || H <= 0 || frames <= 0) return;
-  k_row_scan<<<dim3((H + 31) / 32, frames), 32, 0, s>>>(val, valid, psum, W, H, stride,
-                                                        pstride);
-}
-
-// Disc sum of a masked field from its row prefixes, dy ascending.
-__device__ __forceinline__ double disc_sum(const double* __restrict__ psum, int W, int H,
-                                           int u, int v, int r, const int* __restrict__ span) {
-  const int lo = max(-r, -v), hi = min(r, H - 1 - v);
+__device__ __forceinline__ double disc_sum_tile(const PsumTile& T, const int* span, int W,
+                                                int H, int u, int v, int R) {
+  const int lo = max(-R, -v), hi = min(R, H - 1 - v);
   double s = 0.0;
   for (int dy = lo; dy <= hi; ++dy) {
-    const int sx = __ldg(span + (dy < 0 ? -dy : dy));
-    const int u0 = max(0, u - sx), u1 = min(W - 1, u + sx);
-    const double* row = psum + (long)(v + dy) * (W + 1);
-    s = __dadd_rn(s, __dsub_rn(__ldg(row + u1 + 1), __ldg(row + u0)));
+    const int sx = span[dy < 0 ? -dy : dy];
+    const int c0 = max(0, u - sx) - (T.u0 - R);
+    const int c1 = min(W - 1, u + sx) + 1 - (T.u0 - R);
+    const double* row = T.t + (v + dy - (T.v0 - R)) * T.pitch;
+    s = __dadd_rn(s, __dsub_rn(row[c1], row[c0]));
   }
   return s;
 }
 
-__global__ void k_avg_b(const double* __restrict__ psum, const uint8_t* __restrict__ valid,
-                        const int* __restrict__ cnt, const double* __restrict__ o,
-                        const double* __restrict__ d, double* __restrict__ avg,
-                        double* __restrict__ b, RefineArgs a, long stride, long pstride) {
+__global__ void __launch_bounds__(kTX * kBY)
+    k_avg_b(const double* __restrict__ psum, const uint8_t* __restrict__ valid,
+            const int* __restrict__ cnt, const double* __restrict__ o,
+            const double* __restrict__ d, double* __restrict__ avg, double* __restrict__ b,
+            RefineArgs a, long stride, long pstride) {
   const long f = blockIdx.z;
-  const int W = a.g.W, H = a.g.H;
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  const int v = blockIdx.y * blockDim.y + threadIdx.y;
-  if (u >= W || v >= H) return;
-  const long i = f * stride + (long)v * W + u;
-  if (!valid[i]) return;
-  const double s = disc_sum(psum + f * pstride, W, H, u, v, a.radius, a.span);
-  const double av = __ddiv_rn(s, (double)cnt[i]);
-  avg[i] = av;
-  // averaged - alpha * discrete - (1 - alpha) * smooth, left to right.
-  b[i] = __dsub_rn(__dsub_rn(av, __dmul_rn(a.alpha, o[i])), __dmul_rn(a.one_minus_alpha, d[i]));
+  const int W = a.g.W, H = a.g.H, R = a.radius;
+  int* span;
+  const PsumTile T = load_tile(psum + f * pstride, W, H, R, a.span, span);
+  const int u = blockIdx.x * kTX + threadIdx.x;
+#pragma unroll
+  for (int rr = 0; rr < kTY / kBY; ++rr) {
+    const int v = blockIdx.y * kTY + threadIdx.y + rr * kBY;
+    if (u >= W || v >= H) continue;
+    const long i = f * stride + (long)v * W + u;
+    if (!valid[i]) continue;
+    const double s = disc_sum_tile(T, span, W, H, u, v, R);
+    const double av = __ddiv_rn(s, (double)cnt[i]);
+    avg[i] = av;
+    // averaged - alpha * discrete - (1 - alpha) * smooth, left to right.
+    b[i] = __dsub_rn(__dsub_rn(av, __dmul_rn(a.alpha, o[i])), __dmul_rn(a.one_minus_alpha, d[i]));
+  }
 }
 
 void launch_avg_b(const double* psum, const uint8_t* valid, const int* cnt, const double* o,
                   const double* d, double* avg, double* b, const RefineArgs& a, int frames,
                   long stride, long pstride, cudaStream_t s) {
   if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
-  dim3 bl(32, 8);
-  dim3 grid((a.g.W + 31) / 32, (a.g.H + 7) / 8, frames);
-  k_avg_b<<<grid, bl, 0, s>>>(psum, valid, cnt, o, d, avg, b, a, stride, pstride);
+  const size_t smem = tile_bytes(a.radius);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaFuncSetAttribute(k_avg_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = smem;
+  }
+  dim3 bl(kTX, kBY);
+  dim3 grid((a.g.W + kTX - 1) / kTX, (a.g.H + kTY - 1) / kTY, frames);
+  k_avg_b<<<grid, bl, smem, s>>>(psum, valid, cnt, o, d, avg, b, a, stride, pstride);
 }
 
 __device__ __forceinline__ double exact_cost(const uint8_t* L, const uint8_t* R, int W,
@@ -185,36 +194,18 @@ __device__ __forceinline__ double exact_cost(const uint8_t* L, const uint8_t* R,
 
 constexpr int kMaxCand = 2 * kRefineR + 1;
 
-__global__ void k_d_repick(const double* __restrict__ psum, const uint8_t* __restrict__ valid,
-                           const int* __restrict__ cnt, const double* __restrict__ avg,
-                           double* __restrict__ d, double* __restrict__ o,
-                           const uint8_t* __restrict__ lgray, const uint8_t* __restrict__ rgray,
-                           const int2* __restrict__ lstat, const float* __restrict__ vol,
-                           RefineArgs a, long stride, long pstride, long gray_stride,
-                           long lstat_stride, long vol_stride,
-                           unsigned long long* __restrict__ counters) {
-  const long f = blockIdx.z;
+// Re-pick of one pixel (smoothing.cpp:119-144) given its smoothed d.
+__device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double dv,
+                                      const uint8_t* L, const uint8_t* R, const int2* lstat_f,
+                                      const float* vol_f, long pix,
+                                      unsigned long long* counters) {
   const int W = a.g.W, H = a.g.H, half = a.g.half;
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  const int v = blockIdx.y * blockDim.y + threadIdx.y;
-  if (u >= W || v >= H) return;
-  const long pix = (long)v * W + u;
-  const long i = f * stride + pix;
-  if (!valid[i]) return;
-  const double s = disc_sum(psum + f * pstride, W, H, u, v, a.radius, a.span);
-  const double bav = __ddiv_rn(s, (double)cnt[i]);
-  const double x = __dsub_rn(avg[i], bav);
-  const double dv = x < a.lo ? a.lo : (a.hi < x ? a.hi : x);  // std::clamp
-  d[i] = dv;
-
-  const uint8_t* L = lgray + f * gray_stride;
-  const uint8_t* R = rgray + f * gray_stride;
   const int c_lo = max((int)ceil(__dsub_rn(dv, (double)kRefineR)), (int)ceil(a.lo));
   const int c_hi = min((int)floor(__dadd_rn(dv, (double)kRefineR)), (int)floor(a.hi));
-  if (c_lo > c_hi) return;  // unreachable for a clamped d; mirrors `found`
+  if (c_lo > c_hi) return INT_MIN;  // unreachable for a clamped d; mirrors `found`
   const bool fits = u >= half && u < W - half && v >= half && v < H - half;
 
-  if (vol == nullptr) {
+  if (vol_f == nullptr) {
     // Generic window: every candidate in exact FP64.
     double best_cost = 0.0;
     int best = c_lo;
@@ -225,14 +216,11 @@ __global__ void k_d_repick(const double* __restrict__ psum, const uint8_t* __res
         best = c;
       }
     }
-    o[i] = best;
-    const unsigned act = __activemask();
-    if ((threadIdx.x & 31) == __ffs(act) - 1) atomicAdd(counters, (unsigned long long)__popc(act));
-    return;
+    return best;
   }
 
   float rl = __int_as_float(0x7fc00000);
-  if (fits) rl = __int_as_float(__ldg(&lstat[f * lstat_stride + pix].y));
+  if (fits) rl = __int_as_float(__ldg(&lstat_f[pix].y));
   if (isnan(rl)) {
     // Window does not fit or var_l == 0: every match cost is exactly
     // 1/kZnccCostEpsilon, so the reference's double costs are computed as is.
@@ -247,10 +235,9 @@ __global__ void k_d_repick(const double* __restrict__ psum, const uint8_t* __res
         best = c;
       }
     }
-    o[i] = best;
-    return;
+    return best;
   }
-  const float* vp = vol + f * vol_stride + pix;
+  const float* vp = vol_f + pix;
   const long HW = (long)H * W;
   float cf[kMaxCand];
   float best_f = INFINITY;
@@ -262,7 +249,7 @@ __global__ void k_d_repick(const double* __restrict__ psum, const uint8_t* __res
     if (c <= c_hi) {
       const int ru = u - c;
       float m = 1000.f;  // 1 / kZnccCostEpsilon, exact
-      if (fits && ru >= half && ru < W - half) {
+      if (ru >= half && ru < W - half) {
         const float sc = __ldg(vp + (long)(c - a.g.cmin) * HW) * rl;
         if (!isnan(sc)) m = 1.f / fmaxf(sc, 1e-3f);
       }
@@ -274,7 +261,8 @@ __global__ void k_d_repick(const double* __restrict__ psum, const uint8_t* __res
       }
     }
   }
-  // Any candidate whose exact cost could undercut the float minimum.
+  // Any candidate whose exact cost could undercut the float minimum
+  // (|cost_f - cost| <= 7 ulp = 4.2e-7 relative; margin 4e-6).
   const float thr = best_f * (1.0f + 4e-6f);
   int near = 0;
 #pragma unroll
@@ -282,7 +270,7 @@ __global__ void k_d_repick(const double* __restrict__ psum, const uint8_t* __res
   if (near > 1) {
     double best_cost = 0.0;
     bool found = false;
-#pragma unroll 1
+#pragma unroll
     for (int k = 0; k < kMaxCand; ++k) {
       if (!(cf[k] <= thr)) continue;
       const int c = c_lo + k;
@@ -295,7 +283,41 @@ __global__ void k_d_repick(const double* __restrict__ psum, const uint8_t* __res
     }
     atomicAdd(counters, 1ull);
   }
-  o[i] = best;
+  return best;
+}
+
+__global__ void __launch_bounds__(kTX * kBY)
+    k_d_repick(const double* __restrict__ psum, const uint8_t* __restrict__ valid,
+               const int* __restrict__ cnt, const double* __restrict__ avg,
+               double* __restrict__ d, double* __restrict__ o,
+               const uint8_t* __restrict__ lgray, const uint8_t* __restrict__ rgray,
+               const int2* __restrict__ lstat, const float* __restrict__ vol, RefineArgs a,
+               long stride, long pstride, long gray_stride, long lstat_stride, long vol_stride,
+               unsigned long long* __restrict__ counters) {
+  const long f = blockIdx.z;
+  const int W = a.g.W, H = a.g.H, R = a.radius;
+  int* span;
+  const PsumTile T = load_tile(psum + f * pstride, W, H, R, a.span, span);
+  const int u = blockIdx.x * kTX + threadIdx.x;
+  const uint8_t* L = lgray + f * gray_stride;
+  const uint8_t* Rg = rgray + f * gray_stride;
+  const int2* ls = lstat + f * lstat_stride;
+  const float* vf = vol ? vol + f * vol_stride : nullptr;
+#pragma unroll 1
+  for (int rr = 0; rr < kTY / kBY; ++rr) {
+    const int v = blockIdx.y * kTY + threadIdx.y + rr * kBY;
+    if (u >= W || v >= H) continue;
+    const long pix = (long)v * W + u;
+    const long i = f * stride + pix;
+    if (!valid[i]) continue;
+    const double s = disc_sum_tile(T, span, W, H, u, v, R);
+    const double bav = __ddiv_rn(s, (double)cnt[i]);
+    const double x = __dsub_rn(avg[i], bav);
+    const double dv = x < a.lo ? a.lo : (a.hi < x ? a.hi : x);  // std::clamp
+    d[i] = dv;
+    const int best = repick(a, u, v, dv, L, Rg, ls, vf, pix, counters);
+    if (best != INT_MIN) o[i] = best;
+  }
 }
 
 void launch_d_repick(const double* psum, const uint8_t* valid, const int* cnt,
@@ -305,11 +327,17 @@ void launch_d_repick(const double* psum, const uint8_t* valid, const int* cnt,
                      long gray_stride, long lstat_stride, long vol_stride,
                      unsigned long long* counters, cudaStream_t s) {
   if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
-  dim3 bl(32, 8);
-  dim3 grid((a.g.W + 31) / 32, (a.g.H + 7) / 8, frames);
-  k_d_repick<<<grid, bl, 0, s>>>(psum, valid, cnt, avg, d, o, lgray, rgray, lstat, vol, a,
-                                 stride, pstride, gray_stride, lstat_stride, vol_stride,
-                                 counters);
+  const size_t smem = tile_bytes(a.radius);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaFuncSetAttribute(k_d_repick, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = smem;
+  }
+  dim3 bl(kTX, kBY);
+  dim3 grid((a.g.W + kTX - 1) / kTX, (a.g.H + kTY - 1) / kTY, frames);
+  k_d_repick<<<grid, bl, smem, s>>>(psum, valid, cnt, avg, d, o, lgray, rgray, lstat, vol, a,
+                                    stride, pstride, gray_stride, lstat_stride, vol_stride,
+                                    counters);
 }
 
 __global__ void k_refine_out(const double* __restrict__ d, const uint8_t* __restrict__ valid,

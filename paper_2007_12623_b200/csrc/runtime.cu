@@ -161,8 +161,8 @@ struct ss_ctx {
 
   DevBuf in_l, in_r, gray_l, gray_r, plane_l, plane_r, lstat, rstat, vol;
   DevBuf disp_a, disp_b, valid_a, valid_b, flags, flag_count;
-  DevBuf o, d, avg, b, psum, pcnt, cnt, span, wtab;
-  DevBuf index, block_sums, npoints, pts_f, nrm_f, colors, pts_d, nrm_d, pixels;
+  DevBuf o, d, avg, b, psum, pcnt, cnt, span, wtab, fspan;
+  DevBuf index, block_sums, npoints, pts_f, nrm_f, colors, pts_d, nrm_d, pixels, pts4;
   DevBuf counters, trace_o, trace_d;
   int wtab_radius = -1;
 
@@ -187,8 +187,8 @@ struct ss_ctx {
   ~ss_ctx() {
     for (DevBuf* b : {&in_l, &in_r, &gray_l, &gray_r, &plane_l, &plane_r, &lstat, &rstat, &vol,
                       &disp_a, &disp_b, &valid_a, &valid_b, &flags, &flag_count, &o, &d, &avg,
-                      &b, &psum, &pcnt, &cnt, &span, &wtab, &index, &block_sums, &npoints,
-                      &pts_f, &nrm_f, &colors, &pts_d, &nrm_d, &pixels, &counters, &trace_o,
+                      &b, &psum, &pcnt, &cnt, &span, &wtab, &fspan, &index, &block_sums, &npoints,
+                      &pts_f, &nrm_f, &colors, &pts_d, &nrm_d, &pixels, &pts4, &counters, &trace_o,
                       &trace_d})
       b->release();
     for (auto& r : pending) {
@@ -342,7 +342,26 @@ struct ss_ctx {
     for (int dd = 1; dd <= r2; ++dd) w[dd] = 1.0 / std::sqrt(static_cast<double>(dd));
     wtab.ensure(sizeof(double) * (r2 + 1));
     ck(cudaMemcpy(wtab.p, w.data(), sizeof(double) * (r2 + 1), cudaMemcpyHostToDevice), "wtab");
+    // disc rows: |du| <= floor(sqrt(r^2 - dv^2))  <=>  du^2 + dv^2 <= r^2
+    std::vector<int> sp(std::max(radius, 0) + 1);
+    for (int dv = 0; dv <= radius; ++dv)
+      sp[dv] = (int)std::floor(std::sqrt((double)(r2 - dv * dv)));
+    fspan.ensure(sizeof(int) * sp.size());
+    ck(cudaMemcpy(fspan.p, sp.data(), sizeof(int) * sp.size(), cudaMemcpyHostToDevice), "fspan");
     wtab_radius = radius;
+  }
+
+  void fill_disc(int n, int W, int H, const float* din, const uint8_t* vin, float* dout,
+                 uint8_t* vout, int radius, int min_support) {
+    const long N = (long)W * H;
+    ensure_wtab(radius);
+    pcnt.ensure(sizeof(int) * (long)H * (W + 1) * n);
+    flags.ensure(sizeof(int) * N * n);
+    flag_count.ensure(sizeof(unsigned) * n);
+    launch_fill_disc(din, vin, dout, vout, W, H, radius, min_support, wtab.as<double>(),
+                     fspan.as<int>(), pcnt.as<int>(), flags.as<int>(), flag_count.as<unsigned>(),
+                     n, N, stream);
+    stats.kernel_launches += 3;
   }
 
   // cleanup_pass on disp_a/valid_a -> disp_a/valid_a (cleanup.cpp:111-123).
@@ -358,13 +377,12 @@ struct ss_ctx {
                              stream);
       launch_fill_radial(disp_b.as<float>(), valid_b.as<uint8_t>(), disp_a.as<float>(),
                          valid_a.as<uint8_t>(), W, H, params.fill_radius_radial, 4, n, N, stream);
-      launch_fill_disc(disp_a.as<float>(), valid_a.as<uint8_t>(), disp_b.as<float>(),
-                       valid_b.as<uint8_t>(), W, H, params.fill_radius_disc, disc_support,
-                       wtab.as<double>(), n, N, stream);
+      fill_disc(n, W, H, disp_a.as<float>(), valid_a.as<uint8_t>(), disp_b.as<float>(),
+                valid_b.as<uint8_t>(), params.fill_radius_disc, disc_support);
       ck(cudaMemcpyAsync(disp_a.p, disp_b.p, sizeof(float) * N * n, cudaMemcpyDeviceToDevice,
                          stream), "copy");
       ck(cudaMemcpyAsync(valid_a.p, valid_b.p, N * n, cudaMemcpyDeviceToDevice, stream), "copy");
-      stats.kernel_launches += 3;
+      stats.kernel_launches += 2;
     }
   }
 
@@ -462,13 +480,16 @@ struct ss_ctx {
       if (want_normals) nrm_f.ensure(sizeof(float) * 3 * N * n);
     }
     if (want_pixels) pixels.ensure(sizeof(int) * 2 * N * n);
+    pts4.ensure(sizeof(float4) * N * n);
     launch_cloud_points(dsp, index.as<int>(), rgb, cw, ch, W, H, c,
                         want_double ? pts_d.as<double>() : nullptr,
-                        want_double ? nullptr : pts_f.as<float>(), colors.as<uint8_t>(),
-                        want_pixels ? pixels.as<int>() : nullptr, n, N, rgb_stride, stream);
+                        want_double ? nullptr : pts_f.as<float>(), pts4.as<float4>(),
+                        colors.as<uint8_t>(), want_pixels ? pixels.as<int>() : nullptr, n, N,
+                        rgb_stride, stream);
     stats.kernel_launches += 1;
     if (want_normals) {
-      launch_cloud_normals(dsp, index.as<int>(), c, want_double ? nrm_d.as<double>() : nullptr,
+      launch_cloud_normals(pts4.as<float4>(), dsp, index.as<int>(), c,
+                           want_double ? nrm_d.as<double>() : nullptr,
                            want_double ? nullptr : nrm_f.as<float>(), W, H, n, N, stream);
       stats.kernel_launches += 1;
     }
@@ -640,13 +661,11 @@ ss_status ss_fill_holes(const float* disparity, const uint8_t* valid, int32_t w,
     if (mode == SS_FILL_RADIAL) {
       launch_fill_radial(c->disp_a.as<float>(), c->valid_a.as<uint8_t>(), c->disp_b.as<float>(),
                          c->valid_b.as<uint8_t>(), w, h, radius, min_support, 1, N, c->stream);
+      c->stats.kernel_launches += 1;
     } else {
-      c->ensure_wtab(radius);
-      launch_fill_disc(c->disp_a.as<float>(), c->valid_a.as<uint8_t>(), c->disp_b.as<float>(),
-                       c->valid_b.as<uint8_t>(), w, h, radius, min_support,
-                       c->wtab.as<double>(), 1, N, c->stream);
+      c->fill_disc(1, w, h, c->disp_a.as<float>(), c->valid_a.as<uint8_t>(),
+                   c->disp_b.as<float>(), c->valid_b.as<uint8_t>(), radius, min_support);
     }
-    c->stats.kernel_launches += 1;
     d2h(out_disparity, c->disp_b.p, sizeof(float) * N, c->stream);
     d2h(out_valid, c->valid_b.p, N, c->stream);
     sync(c);

@@ -61,9 +61,11 @@ void launch_remove_outliers(const float* din, const uint8_t* vin, float* dout, u
 void launch_fill_radial(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
                         int W, int H, int radius, int min_support, int frames, long stride,
                         cudaStream_t s);
+// pcnt: scratch [frames][H][W+1] ints; list: scratch [frames][W*H]; count: [frames]
 void launch_fill_disc(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
                       int W, int H, int radius, int min_support, const double* wtab,
-                      int frames, long stride, cudaStream_t s);
+                      const int* span, int* pcnt, int* list, unsigned* count, int frames,
+                      long stride, cudaStream_t s);
 
 struct RefineArgs {
   Geom g;
@@ -99,10 +101,10 @@ void launch_cloud_index(const float* disp, const uint8_t* valid, int* index, int
                         int* n_points, int W, int H, int frames, long stride, cudaStream_t s);
 void launch_cloud_points(const float* disp, const int* index, const uint8_t* rgb, int cw,
                          int ch, int W, int H, const CloudArgs& c, double* pts_d,
-                         float* pts_f, uint8_t* colors, int* pixels, int frames, long stride,
-                         long rgb_stride, cudaStream_t s);
-void launch_cloud_normals(const float* disp, const int* index, const CloudArgs& c,
-                          double* nrm_d, float* nrm_f, int W, int H, int frames, long stride,
-                          cudaStream_t s);
+                         float* pts_f, float4* pts4, uint8_t* colors, int* pixels, int frames,
+                         long stride, long rgb_stride, cudaStream_t s);
+void launch_cloud_normals(const float4* pts4, const float* disp, const int* index,
+                          const CloudArgs& c, double* nrm_d, float* nrm_f, int W, int H,
+                          int frames, long stride, cudaStream_t s);
 
 }  // namespace ssb
