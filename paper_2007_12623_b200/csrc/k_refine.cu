@@ -1,9 +1,13 @@
 // Anti-shrink Laplacian refinement (refine_disparities, smoothing.cpp:68-159).
 //
-// One iteration = 2 scans + 2 gathers, all FP64 in the reference's order:
-//   k_row_scan    serial left-to-right masked row prefix (smoothing.cpp:25-41);
-//                 one thread per (frame, row) — latency-bound, hidden by the
-//                 frame batch.
+// Iteration 0 (o = the cleanup output, fractional where filled) follows the
+// reference literally: FP64 row prefix of o (k_scan.cu), k_avg_b, FP64 row
+// prefix of b, k_d_repick. After it, o is integer-valued, so its disc sum is an
+// exact integer S_o (and the reference's double sum of it is exact too):
+// S_o is built once (int prefix + k_disc_count) and then maintained by
+// k_so_update from the few pixels whose o changed (hundreds to thousands per
+// frame), and b is formed inside the b prefix scan (SrcB). Iterations >= 1 are
+// therefore one serial FP64 scan + one tiled gather + a small scatter.
 //   k_avg_b       disc mean of o (31 row-span differences, dy ascending,
 //                 smoothing.cpp:43-63) fused with the correction
 //                 b = (avg - a o) - (1-a) d_prev (smoothing.cpp:91-99).
@@ -20,6 +24,8 @@
 // The mask is fixed, so the per-pixel disc count is computed once (k_disc_count).
 #include <limits.h>
 #include <math.h>
+
+#include <utility>
 
 #include "exact.cuh"
 #include "ss_internal.cuh"
@@ -140,6 +146,42 @@ __device__ __forceinline__ double disc_sum_tile(const PsumTile& T, const int* sp
   return s;
 }
 
+// Compile-time radius: interior pixels (no clamping) read the tile at
+// immediate offsets from one base pointer — no index arithmetic per disc row.
+__host__ __device__ constexpr int isqrt_floor(int x) {
+  int r = 0;
+  while ((r + 1) * (r + 1) <= x) ++r;
+  return r;
+}
+
+template <int R, int DY>
+__device__ __forceinline__ double span_diff(const double* q) {
+  constexpr int P = kTX + 2 * R + 1;
+  constexpr int SX = isqrt_floor(R * R - DY * DY);
+  return __dsub_rn(q[DY * P + SX + 1], q[DY * P - SX]);
+}
+
+template <int R, int... I>
+__device__ __forceinline__ double disc_sum_fixed(const double* q,
+                                                 std::integer_sequence<int, I...>) {
+  double s = 0.0;
+  ((s = __dadd_rn(s, span_diff<R, I - R>(q))), ...);  // dy ascending, left to right
+  return s;
+}
+
+template <int R>
+__device__ __forceinline__ double disc_sum_any(const PsumTile& T, const int* span, int W, int H,
+                                               int u, int v, int Rr) {
+  if constexpr (R > 0) {
+    if (u >= R && u + R <= W - 1 && v >= R && v + R <= H - 1) {
+      const double* q = T.t + (v - T.v0 + R) * T.pitch + (u - T.u0 + R);
+      return disc_sum_fixed<R>(q, std::make_integer_sequence<int, 2 * R + 1>{});
+    }
+  }
+  return disc_sum_tile(T, span, W, H, u, v, Rr);
+}
+
+template <int RF>
 __global__ void __launch_bounds__(kTX * kBY)
     k_avg_b(const double* __restrict__ psum, const uint8_t* __restrict__ valid,
             const int* __restrict__ cnt, const double* __restrict__ o,
@@ -156,7 +198,7 @@ __global__ void __launch_bounds__(kTX * kBY)
     if (u >= W || v >= H) continue;
     const long i = f * stride + (long)v * W + u;
     if (!valid[i]) continue;
-    const double s = disc_sum_tile(T, span, W, H, u, v, R);
+    const double s = disc_sum_any<RF>(T, span, W, H, u, v, R);
     const double av = __ddiv_rn(s, (double)cnt[i]);
     avg[i] = av;
     // averaged - alpha * discrete - (1 - alpha) * smooth, left to right.
@@ -169,14 +211,18 @@ void launch_avg_b(const double* psum, const uint8_t* valid, const int* cnt, cons
                   long stride, long pstride, cudaStream_t s) {
   if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
   const size_t smem = tile_bytes(a.radius);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaFuncSetAttribute(k_avg_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = smem;
-  }
   dim3 bl(kTX, kBY);
   dim3 grid((a.g.W + kTX - 1) / kTX, (a.g.H + kTY - 1) / kTY, frames);
-  k_avg_b<<<grid, bl, smem, s>>>(psum, valid, cnt, o, d, avg, b, a, stride, pstride);
+  if (a.radius == 15) {
+    k_avg_b<15><<<grid, bl, smem, s>>>(psum, valid, cnt, o, d, avg, b, a, stride, pstride);
+  } else {
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+      cudaFuncSetAttribute(k_avg_b<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      configured = smem;
+    }
+    k_avg_b<0><<<grid, bl, smem, s>>>(psum, valid, cnt, o, d, avg, b, a, stride, pstride);
+  }
 }
 
 __device__ __forceinline__ double exact_cost(const uint8_t* L, const uint8_t* R, int W,
@@ -286,12 +332,14 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
   return best;
 }
 
+template <int RF, bool USE_SO>
 __global__ void __launch_bounds__(kTX * kBY)
     k_d_repick(const double* __restrict__ psum, const uint8_t* __restrict__ valid,
                const int* __restrict__ cnt, const double* __restrict__ avg,
-               double* __restrict__ d, double* __restrict__ o,
+               const int* __restrict__ so, double* __restrict__ d, double* __restrict__ o,
                const uint8_t* __restrict__ lgray, const uint8_t* __restrict__ rgray,
-               const int2* __restrict__ lstat, const float* __restrict__ vol, RefineArgs a,
+               const int2* __restrict__ lstat, const float* __restrict__ vol,
+               int2* __restrict__ chg, unsigned* __restrict__ chg_count, RefineArgs a,
                long stride, long pstride, long gray_stride, long lstat_stride, long vol_stride,
                unsigned long long* __restrict__ counters) {
   const long f = blockIdx.z;
@@ -310,34 +358,86 @@ __global__ void __launch_bounds__(kTX * kBY)
     const long pix = (long)v * W + u;
     const long i = f * stride + pix;
     if (!valid[i]) continue;
-    const double s = disc_sum_tile(T, span, W, H, u, v, R);
-    const double bav = __ddiv_rn(s, (double)cnt[i]);
-    const double x = __dsub_rn(avg[i], bav);
+    const double s = disc_sum_any<RF>(T, span, W, H, u, v, R);
+    const double c = (double)cnt[i];
+    const double bav = __ddiv_rn(s, c);
+    // avg = s_o / c: with integer o the reference's double disc sum is exact,
+    // so the integer sum reproduces it bit for bit.
+    const double av = USE_SO ? __ddiv_rn((double)so[i], c) : avg[i];
+    const double x = __dsub_rn(av, bav);
     const double dv = x < a.lo ? a.lo : (a.hi < x ? a.hi : x);  // std::clamp
     d[i] = dv;
     const int best = repick(a, u, v, dv, L, Rg, ls, vf, pix, counters);
-    if (best != INT_MIN) o[i] = best;
+    if (best != INT_MIN) {
+      if (USE_SO) {
+        const int old = (int)o[i];
+        if (best != old) chg[f * stride + atomicAdd(chg_count + f, 1u)] = make_int2((int)pix, best - old);
+      }
+      o[i] = best;
+    }
   }
 }
 
 void launch_d_repick(const double* psum, const uint8_t* valid, const int* cnt,
-                     const double* avg, double* d, double* o, const uint8_t* lgray,
-                     const uint8_t* rgray, const int2* lstat, const float* vol,
-                     const RefineArgs& a, int frames, long stride, long pstride,
-                     long gray_stride, long lstat_stride, long vol_stride,
-                     unsigned long long* counters, cudaStream_t s) {
+                     const double* avg, const int* so, double* d, double* o,
+                     const uint8_t* lgray, const uint8_t* rgray, const int2* lstat,
+                     const float* vol, int2* chg, unsigned* chg_count, const RefineArgs& a,
+                     int frames, long stride, long pstride, long gray_stride,
+                     long lstat_stride, long vol_stride, unsigned long long* counters,
+                     cudaStream_t s) {
   if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
   const size_t smem = tile_bytes(a.radius);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaFuncSetAttribute(k_d_repick, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = smem;
-  }
   dim3 bl(kTX, kBY);
   dim3 grid((a.g.W + kTX - 1) / kTX, (a.g.H + kTY - 1) / kTY, frames);
-  k_d_repick<<<grid, bl, smem, s>>>(psum, valid, cnt, avg, d, o, lgray, rgray, lstat, vol, a,
-                                    stride, pstride, gray_stride, lstat_stride, vol_stride,
-                                    counters);
+#define SS_REPICK_ARGS                                                                       \
+  psum, valid, cnt, avg, so, d, o, lgray, rgray, lstat, vol, chg, chg_count, a, stride,      \
+      pstride, gray_stride, lstat_stride, vol_stride, counters
+  if (a.radius == 15) {
+    if (avg) k_d_repick<15, false><<<grid, bl, smem, s>>>(SS_REPICK_ARGS);
+    else k_d_repick<15, true><<<grid, bl, smem, s>>>(SS_REPICK_ARGS);
+  } else {
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+      cudaFuncSetAttribute(k_d_repick<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      cudaFuncSetAttribute(k_d_repick<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      configured = smem;
+    }
+    if (avg) k_d_repick<0, false><<<grid, bl, smem, s>>>(SS_REPICK_ARGS);
+    else k_d_repick<0, true><<<grid, bl, smem, s>>>(SS_REPICK_ARGS);
+  }
+#undef SS_REPICK_ARGS
+}
+
+// One warp per changed pixel j: S_o(i) += delta_j for every valid i whose disc
+// contains j (the disc relation is symmetric, clipped to the image exactly as
+// the reference's row spans are).
+__global__ void k_so_update(const int2* __restrict__ chg, const unsigned* __restrict__ chg_count,
+                            const uint8_t* __restrict__ valid, int* __restrict__ so,
+                            RefineArgs a, long stride) {
+  const long f = blockIdx.y;
+  const int W = a.g.W, H = a.g.H, R = a.radius;
+  const unsigned n = chg_count[f];
+  const int lane = threadIdx.x & 31;
+  const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
+  for (unsigned t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n; t += nwarps) {
+    const int2 e = chg[f * stride + t];
+    const int v = e.x / W, u = e.x % W;
+    for (int dy = max(-R, -v); dy <= min(R, H - 1 - v); ++dy) {
+      const int sx = __ldg(a.span + (dy < 0 ? -dy : dy));
+      const int u0 = max(0, u - sx), u1 = min(W - 1, u + sx);
+      const long row = f * stride + (long)(v + dy) * W;
+      for (int x = u0 + lane; x <= u1; x += 32)
+        if (__ldg(valid + row + x)) atomicAdd(so + row + x, e.y);
+    }
+  }
+}
+
+void launch_so_update(const int2* chg, const unsigned* chg_count, const uint8_t* valid,
+                      int* so, const RefineArgs& a, int frames, long stride, cudaStream_t s) {
+  if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
+  k_so_update<<<dim3(148, frames), 256, 0, s>>>(chg, chg_count, valid, so, a, stride);
 }
 
 __global__ void k_refine_out(const double* __restrict__ d, const uint8_t* __restrict__ valid,

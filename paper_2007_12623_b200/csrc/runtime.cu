@@ -163,7 +163,7 @@ struct ss_ctx {
   DevBuf disp_a, disp_b, valid_a, valid_b, flags, flag_count;
   DevBuf o, d, avg, b, psum, pcnt, cnt, span, wtab, fspan;
   DevBuf index, block_sums, npoints, pts_f, nrm_f, colors, pts_d, nrm_d, pixels, pts4;
-  DevBuf counters, trace_o, trace_d;
+  DevBuf counters, trace_o, trace_d, so, chg, chg_count;
   int wtab_radius = -1;
 
   ss_ctx_stats stats{};
@@ -189,7 +189,7 @@ struct ss_ctx {
                       &disp_a, &disp_b, &valid_a, &valid_b, &flags, &flag_count, &o, &d, &avg,
                       &b, &psum, &pcnt, &cnt, &span, &wtab, &fspan, &index, &block_sums, &npoints,
                       &pts_f, &nrm_f, &colors, &pts_d, &nrm_d, &pixels, &pts4, &counters, &trace_o,
-                      &trace_d})
+                      &trace_d, &so, &chg, &chg_count})
       b->release();
     for (auto& r : pending) {
       ev_pool.push_back(r.a);
@@ -427,18 +427,45 @@ struct ss_ctx {
     launch_disc_count(valid_a.as<uint8_t>(), pcnt.as<int>(), cnt.as<int>(), a, n, N, pstride,
                       stream);
     stats.kernel_launches += 3;
+    so.ensure(sizeof(int) * N * n);
+    chg.ensure(sizeof(int2) * N * n);
+    chg_count.ensure(sizeof(unsigned) * n);
+    const uint8_t* vm = valid_a.as<uint8_t>();
+    const float* volp = have_volume ? vol.as<float>() : nullptr;
     for (int it = 0; it < iters; ++it) {
-      launch_row_scan(o.as<double>(), valid_a.as<uint8_t>(), psum.as<double>(), W, H, n, N,
-                      pstride, stream);
-      launch_avg_b(psum.as<double>(), valid_a.as<uint8_t>(), cnt.as<int>(), o.as<double>(),
-                   d.as<double>(), avg.as<double>(), b.as<double>(), a, n, N, pstride, stream);
-      launch_row_scan(b.as<double>(), valid_a.as<uint8_t>(), psum.as<double>(), W, H, n, N,
-                      pstride, stream);
-      launch_d_repick(psum.as<double>(), valid_a.as<uint8_t>(), cnt.as<int>(), avg.as<double>(),
-                      d.as<double>(), o.as<double>(), gray_l.as<uint8_t>(), gray_r.as<uint8_t>(),
-                      lstat.as<int2>(), have_volume ? vol.as<float>() : nullptr, a, n, N,
-                      pstride, N, N, (long)g.NC * N, ctr() + (have_volume ? 1 : 2), stream);
-      stats.kernel_launches += 4;
+      if (it == 0) {
+        // o is the cleanup output (fractional fills): the reference's FP64 path.
+        launch_row_scan(o.as<double>(), vm, psum.as<double>(), W, H, n, N, pstride, stream);
+        launch_avg_b(psum.as<double>(), vm, cnt.as<int>(), o.as<double>(), d.as<double>(),
+                     avg.as<double>(), b.as<double>(), a, n, N, pstride, stream);
+        launch_row_scan(b.as<double>(), vm, psum.as<double>(), W, H, n, N, pstride, stream);
+        launch_d_repick(psum.as<double>(), vm, cnt.as<int>(), avg.as<double>(), nullptr,
+                        d.as<double>(), o.as<double>(), gray_l.as<uint8_t>(),
+                        gray_r.as<uint8_t>(), lstat.as<int2>(), volp, nullptr, nullptr, a, n, N,
+                        pstride, N, N, (long)g.NC * N, ctr() + 1, stream);
+        stats.kernel_launches += 4;
+        if (iters > 1) {
+          // o is integer-valued from here on: exact integer disc sums S_o.
+          launch_int_scan(o.as<double>(), vm, pcnt.as<int>(), W, H, n, N, pstride, stream);
+          launch_disc_count(vm, pcnt.as<int>(), so.as<int>(), a, n, N, pstride, stream);
+          stats.kernel_launches += 2;
+        }
+      } else {
+        ck(cudaMemsetAsync(chg_count.p, 0, sizeof(unsigned) * n, stream), "memset");
+        launch_b_scan(so.as<int>(), cnt.as<int>(), o.as<double>(), d.as<double>(), a.alpha,
+                      a.one_minus_alpha, vm, psum.as<double>(), W, H, n, N, pstride, stream);
+        launch_d_repick(psum.as<double>(), vm, cnt.as<int>(), nullptr, so.as<int>(),
+                        d.as<double>(), o.as<double>(), gray_l.as<uint8_t>(),
+                        gray_r.as<uint8_t>(), lstat.as<int2>(), volp, chg.as<int2>(),
+                        chg_count.as<unsigned>(), a, n, N, pstride, N, N, (long)g.NC * N,
+                        ctr() + 1, stream);
+        stats.kernel_launches += 2;
+        if (it + 1 < iters) {
+          launch_so_update(chg.as<int2>(), chg_count.as<unsigned>(), vm, so.as<int>(), a, n, N,
+                           stream);
+          stats.kernel_launches += 1;
+        }
+      }
       if (h_trace_o)
         ck(cudaMemcpyAsync(trace_o.as<double>() + (long)it * N, o.p, sizeof(double) * N,
                            cudaMemcpyDeviceToDevice, stream), "trace");

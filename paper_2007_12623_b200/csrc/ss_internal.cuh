@@ -82,15 +82,26 @@ void launch_disc_count(const uint8_t* valid, const int* pcnt, int* cnt, const Re
                        int frames, long stride, long pstride, cudaStream_t s);
 void launch_row_scan(const double* val, const uint8_t* valid, double* psum, int W, int H,
                      int frames, long stride, long pstride, cudaStream_t s);
+void launch_int_scan(const double* val, const uint8_t* valid, int* ipsum, int W, int H,
+                     int frames, long stride, long pstride, cudaStream_t s);
+void launch_b_scan(const int* so, const int* cnt, const double* o, const double* d,
+                   double alpha, double one_minus_alpha, const uint8_t* valid, double* psum,
+                   int W, int H, int frames, long stride, long pstride, cudaStream_t s);
 void launch_avg_b(const double* psum, const uint8_t* valid, const int* cnt, const double* o,
                   const double* d, double* avg, double* b, const RefineArgs& a, int frames,
                   long stride, long pstride, cudaStream_t s);
+// avg: the double disc mean of o (iteration 0) or nullptr to use the exact
+// integer disc sum `so` (iterations >= 1); o changes are appended to chg.
 void launch_d_repick(const double* psum, const uint8_t* valid, const int* cnt,
-                     const double* avg, double* d, double* o, const uint8_t* lgray,
-                     const uint8_t* rgray, const int2* lstat, const float* vol,
-                     const RefineArgs& a, int frames, long stride, long pstride,
-                     long gray_stride, long lstat_stride, long vol_stride,
-                     unsigned long long* counters, cudaStream_t s);
+                     const double* avg, const int* so, double* d, double* o,
+                     const uint8_t* lgray, const uint8_t* rgray, const int2* lstat,
+                     const float* vol, int2* chg, unsigned* chg_count, const RefineArgs& a,
+                     int frames, long stride, long pstride, long gray_stride,
+                     long lstat_stride, long vol_stride, unsigned long long* counters,
+                     cudaStream_t s);
+// S_o += delta over the disc of every changed pixel (exact integers).
+void launch_so_update(const int2* chg, const unsigned* chg_count, const uint8_t* valid,
+                      int* so, const RefineArgs& a, int frames, long stride, cudaStream_t s);
 void launch_refine_out(const double* d, const uint8_t* valid, const float* din, float* dout,
                        int W, int H, int frames, long stride, cudaStream_t s);
 
