@@ -25,6 +25,7 @@
 #include <limits.h>
 #include <math.h>
 
+#include <type_traits>
 #include <utility>
 
 #include "exact.cuh"
@@ -57,40 +58,6 @@ void launch_refine_init(const float* disp, const uint8_t* valid, double* o, doub
   k_refine_init<<<dim3((unsigned)blocks, frames), 256, 0, s>>>(disp, valid, o, d, n, stride);
 }
 
-__global__ void k_disc_count(const uint8_t* __restrict__ valid, const int* __restrict__ pcnt,
-                             int* __restrict__ cnt, RefineArgs a, long stride, long pstride) {
-  const long f = blockIdx.z;
-  const int W = a.g.W, H = a.g.H;
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  const int v = blockIdx.y * blockDim.y + threadIdx.y;
-  if (u >= W || v >= H) return;
-  const long i = (long)v * W + u;
-  valid += f * stride;
-  pcnt += f * pstride;
-  if (!valid[i]) {
-    cnt[f * stride + i] = 0;
-    return;
-  }
-  const int r = a.radius;
-  const int lo = max(-r, -v), hi = min(r, H - 1 - v);
-  int c = 0;
-  for (int dy = lo; dy <= hi; ++dy) {
-    const int sx = a.span[dy < 0 ? -dy : dy];
-    const int u0 = max(0, u - sx), u1 = min(W - 1, u + sx);
-    const int* row = pcnt + (long)(v + dy) * (W + 1);
-    c += row[u1 + 1] - row[u0];
-  }
-  cnt[f * stride + i] = c;
-}
-
-void launch_disc_count(const uint8_t* valid, const int* pcnt, int* cnt, const RefineArgs& a,
-                       int frames, long stride, long pstride, cudaStream_t s) {
-  if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
-  dim3 b(32, 8);
-  dim3 grid((a.g.W + 31) / 32, (a.g.H + 7) / 8, frames);
-  k_disc_count<<<grid, b, 0, s>>>(valid, pcnt, cnt, a, stride, pstride);
-}
-
 // ---- disc sums of a masked field from its row prefixes (smoothing.cpp:43-63) ----
 //
 // The reference sums, for dy ascending, the span difference
@@ -101,20 +68,26 @@ void launch_disc_count(const uint8_t* valid, const int* pcnt, int* cnt, const Re
 
 constexpr int kTX = 32, kTY = 16, kBY = 8;  // tile = 32 x 16 pixels, block = 32 x 8
 
+template <typename T>
 struct PsumTile {
-  const double* t;  // smem [(kTY + 2R)][(kTX + 2R + 1)]
+  const T* t;         // smem [(kTY + 2R)][(kTX + 2R + 1)]
   int pitch, u0, v0;  // psum column of t[.][0] is u0 - R; row of t[0] is v0 - R
 };
 
 __host__ __device__ inline int tile_pitch(int R) { return kTX + 2 * R + 1; }
+template <typename T>
 __host__ __device__ inline size_t tile_bytes(int R) {
-  return sizeof(double) * (size_t)(kTY + 2 * R) * tile_pitch(R) + sizeof(int) * (R + 1);
+  return sizeof(T) * (size_t)(kTY + 2 * R) * tile_pitch(R) + sizeof(int) * (R + 1);
 }
 
-__device__ __forceinline__ PsumTile load_tile(const double* __restrict__ psum, int W, int H,
-                                             int R, const int* __restrict__ span_g,
-                                             int*& span) {
-  extern __shared__ double tile_mem[];
+// Stage the BT-layout prefix rows [v0-R, v0+kTY+R) x columns [u0-R, u0+kTX+R]
+// of one frame. Consecutive threads walk rows first: within a 32-row block
+// of the BT layout those are consecutive addresses.
+template <typename T>
+__device__ __forceinline__ PsumTile<T> load_tile(const T* __restrict__ psumT, int W, int H, int R,
+                                                 const int* __restrict__ span_g, int*& span) {
+  extern __shared__ double tile_raw[];
+  T* tile_mem = reinterpret_cast<T*>(tile_raw);
   const int pitch = tile_pitch(R);
   const int rows = kTY + 2 * R;
   const int u0 = blockIdx.x * kTX, v0 = blockIdx.y * kTY;
@@ -122,26 +95,39 @@ __device__ __forceinline__ PsumTile load_tile(const double* __restrict__ psum, i
   const int tid = threadIdx.y * kTX + threadIdx.x;
   for (int k = tid; k <= R; k += kTX * kBY) span[k] = __ldg(span_g + k);
   for (int k = tid; k < rows * pitch; k += kTX * kBY) {
-    const int r = k / pitch, c = k % pitch;
+    const int r = k % rows, c = k / rows;
     const int pr = v0 - R + r, pc = u0 - R + c;
-    double x = 0.0;
-    if (pr >= 0 && pr < H && pc >= 0 && pc <= W) x = __ldg(psum + (long)pr * (W + 1) + pc);
-    tile_mem[k] = x;
+    T x = T(0);
+    if (pr >= 0 && pr < H && pc >= 0 && pc <= W)
+      x = __ldg(psumT + ((long)(pr >> 5) * (W + 1) + pc) * 32 + (pr & 31));
+    tile_mem[r * pitch + c] = x;
   }
   __syncthreads();
-  return PsumTile{tile_mem, pitch, u0, v0};
+  return PsumTile<T>{tile_mem, pitch, u0, v0};
 }
 
-__device__ __forceinline__ double disc_sum_tile(const PsumTile& T, const int* span, int W,
-                                                int H, int u, int v, int R) {
+template <typename T>
+__device__ __forceinline__ T tsub(T a, T b) {
+  if constexpr (std::is_same<T, double>::value) return __dsub_rn(a, b);
+  else return a - b;
+}
+template <typename T>
+__device__ __forceinline__ T tadd(T a, T b) {
+  if constexpr (std::is_same<T, double>::value) return __dadd_rn(a, b);
+  else return a + b;
+}
+
+template <typename T>
+__device__ __forceinline__ T disc_sum_tile(const PsumTile<T>& P, const int* span, int W, int H,
+                                           int u, int v, int R) {
   const int lo = max(-R, -v), hi = min(R, H - 1 - v);
-  double s = 0.0;
+  T s = T(0);
   for (int dy = lo; dy <= hi; ++dy) {
     const int sx = span[dy < 0 ? -dy : dy];
-    const int c0 = max(0, u - sx) - (T.u0 - R);
-    const int c1 = min(W - 1, u + sx) + 1 - (T.u0 - R);
-    const double* row = T.t + (v + dy - (T.v0 - R)) * T.pitch;
-    s = __dadd_rn(s, __dsub_rn(row[c1], row[c0]));
+    const int c0 = max(0, u - sx) - (P.u0 - R);
+    const int c1 = min(W - 1, u + sx) + 1 - (P.u0 - R);
+    const T* row = P.t + (v + dy - (P.v0 - R)) * P.pitch;
+    s = tadd(s, tsub(row[c1], row[c0]));
   }
   return s;
 }
@@ -154,43 +140,80 @@ __host__ __device__ constexpr int isqrt_floor(int x) {
   return r;
 }
 
-template <int R, int DY>
-__device__ __forceinline__ double span_diff(const double* q) {
+template <typename T, int R, int DY>
+__device__ __forceinline__ T span_diff(const T* q) {
   constexpr int P = kTX + 2 * R + 1;
   constexpr int SX = isqrt_floor(R * R - DY * DY);
-  return __dsub_rn(q[DY * P + SX + 1], q[DY * P - SX]);
+  return tsub(q[DY * P + SX + 1], q[DY * P - SX]);
 }
 
-template <int R, int... I>
-__device__ __forceinline__ double disc_sum_fixed(const double* q,
-                                                 std::integer_sequence<int, I...>) {
-  double s = 0.0;
-  ((s = __dadd_rn(s, span_diff<R, I - R>(q))), ...);  // dy ascending, left to right
+template <typename T, int R, int... I>
+__device__ __forceinline__ T disc_sum_fixed(const T* q, std::integer_sequence<int, I...>) {
+  T s = T(0);
+  ((s = tadd(s, span_diff<T, R, I - R>(q))), ...);  // dy ascending, left to right
   return s;
 }
 
-template <int R>
-__device__ __forceinline__ double disc_sum_any(const PsumTile& T, const int* span, int W, int H,
-                                               int u, int v, int Rr) {
+template <int R, typename T>
+__device__ __forceinline__ T disc_sum_any(const PsumTile<T>& P, const int* span, int W, int H,
+                                          int u, int v, int Rr) {
   if constexpr (R > 0) {
     if (u >= R && u + R <= W - 1 && v >= R && v + R <= H - 1) {
-      const double* q = T.t + (v - T.v0 + R) * T.pitch + (u - T.u0 + R);
-      return disc_sum_fixed<R>(q, std::make_integer_sequence<int, 2 * R + 1>{});
+      const T* q = P.t + (v - P.v0 + R) * P.pitch + (u - P.u0 + R);
+      return disc_sum_fixed<T, R>(q, std::make_integer_sequence<int, 2 * R + 1>{});
     }
   }
-  return disc_sum_tile(T, span, W, H, u, v, Rr);
+  return disc_sum_tile(P, span, W, H, u, v, Rr);
+}
+
+// Exact integer disc sums (disc counts, S_o) from an int BT prefix.
+template <int RF>
+__global__ void __launch_bounds__(kTX * kBY)
+    k_disc_isum(const uint8_t* __restrict__ valid, const int* __restrict__ ipsumT,
+                int* __restrict__ out, RefineArgs a, long stride) {
+  const long f = blockIdx.z;
+  const int W = a.g.W, H = a.g.H, R = a.radius;
+  int* span;
+  const PsumTile<int> P = load_tile(ipsumT + f * bt_frame(W, H, 1), W, H, R, a.span, span);
+  const int u = blockIdx.x * kTX + threadIdx.x;
+#pragma unroll
+  for (int rr = 0; rr < kTY / kBY; ++rr) {
+    const int v = blockIdx.y * kTY + threadIdx.y + rr * kBY;
+    if (u >= W || v >= H) continue;
+    const long i = f * stride + (long)v * W + u;
+    out[i] = valid[i] ? disc_sum_any<RF>(P, span, W, H, u, v, R) : 0;
+  }
+}
+
+void launch_disc_isum(const uint8_t* valid, const int* ipsumT, int* out, const RefineArgs& a,
+                      int frames, long stride, cudaStream_t s) {
+  if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
+  const size_t smem = tile_bytes<int>(a.radius);
+  dim3 bl(kTX, kBY);
+  dim3 grid((a.g.W + kTX - 1) / kTX, (a.g.H + kTY - 1) / kTY, frames);
+  if (a.radius == 15) {
+    k_disc_isum<15><<<grid, bl, smem, s>>>(valid, ipsumT, out, a, stride);
+  } else {
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+      cudaFuncSetAttribute(k_disc_isum<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      configured = smem;
+    }
+    k_disc_isum<0><<<grid, bl, smem, s>>>(valid, ipsumT, out, a, stride);
+  }
 }
 
 template <int RF>
 __global__ void __launch_bounds__(kTX * kBY)
-    k_avg_b(const double* __restrict__ psum, const uint8_t* __restrict__ valid,
+    k_avg_b(const double* __restrict__ psumT, const uint8_t* __restrict__ valid,
             const int* __restrict__ cnt, const double* __restrict__ o,
             const double* __restrict__ d, double* __restrict__ avg, double* __restrict__ b,
-            RefineArgs a, long stride, long pstride) {
+            RefineArgs a, long stride) {
   const long f = blockIdx.z;
   const int W = a.g.W, H = a.g.H, R = a.radius;
   int* span;
-  const PsumTile T = load_tile(psum + f * pstride, W, H, R, a.span, span);
+  const PsumTile<double> T = load_tile(psumT + f * bt_frame(W, H, 1), W, H, R, a.span, span);
   const int u = blockIdx.x * kTX + threadIdx.x;
 #pragma unroll
   for (int rr = 0; rr < kTY / kBY; ++rr) {
@@ -206,22 +229,22 @@ __global__ void __launch_bounds__(kTX * kBY)
   }
 }
 
-void launch_avg_b(const double* psum, const uint8_t* valid, const int* cnt, const double* o,
+void launch_avg_b(const double* psumT, const uint8_t* valid, const int* cnt, const double* o,
                   const double* d, double* avg, double* b, const RefineArgs& a, int frames,
-                  long stride, long pstride, cudaStream_t s) {
+                  long stride, cudaStream_t s) {
   if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
-  const size_t smem = tile_bytes(a.radius);
+  const size_t smem = tile_bytes<double>(a.radius);
   dim3 bl(kTX, kBY);
   dim3 grid((a.g.W + kTX - 1) / kTX, (a.g.H + kTY - 1) / kTY, frames);
   if (a.radius == 15) {
-    k_avg_b<15><<<grid, bl, smem, s>>>(psum, valid, cnt, o, d, avg, b, a, stride, pstride);
+    k_avg_b<15><<<grid, bl, smem, s>>>(psumT, valid, cnt, o, d, avg, b, a, stride);
   } else {
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
       cudaFuncSetAttribute(k_avg_b<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       configured = smem;
     }
-    k_avg_b<0><<<grid, bl, smem, s>>>(psum, valid, cnt, o, d, avg, b, a, stride, pstride);
+    k_avg_b<0><<<grid, bl, smem, s>>>(psumT, valid, cnt, o, d, avg, b, a, stride);
   }
 }
 
@@ -283,8 +306,7 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
     }
     return best;
   }
-  const float* vp = vol_f + pix;
-  const long HW = (long)H * W;
+  const float* vp = vol_f + pix * a.g.NCP - a.g.cmin;  // vp[c]: candidate c of this pixel
   float cf[kMaxCand];
   float best_f = INFINITY;
   int best = c_lo;
@@ -296,7 +318,7 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
       const int ru = u - c;
       float m = 1000.f;  // 1 / kZnccCostEpsilon, exact
       if (ru >= half && ru < W - half) {
-        const float sc = __ldg(vp + (long)(c - a.g.cmin) * HW) * rl;
+        const float sc = __ldg(vp + c) * rl;
         if (!isnan(sc)) m = 1.f / fmaxf(sc, 1e-3f);
       }
       const float df = (float)__dsub_rn((double)c, dv);
@@ -334,18 +356,18 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
 
 template <int RF, bool USE_SO>
 __global__ void __launch_bounds__(kTX * kBY)
-    k_d_repick(const double* __restrict__ psum, const uint8_t* __restrict__ valid,
+    k_d_repick(const double* __restrict__ psumT, const uint8_t* __restrict__ valid,
                const int* __restrict__ cnt, const double* __restrict__ avg,
                const int* __restrict__ so, double* __restrict__ d, double* __restrict__ o,
                const uint8_t* __restrict__ lgray, const uint8_t* __restrict__ rgray,
                const int2* __restrict__ lstat, const float* __restrict__ vol,
                int2* __restrict__ chg, unsigned* __restrict__ chg_count, RefineArgs a,
-               long stride, long pstride, long gray_stride, long lstat_stride, long vol_stride,
+               long stride, long gray_stride, long lstat_stride, long vol_stride,
                unsigned long long* __restrict__ counters) {
   const long f = blockIdx.z;
   const int W = a.g.W, H = a.g.H, R = a.radius;
   int* span;
-  const PsumTile T = load_tile(psum + f * pstride, W, H, R, a.span, span);
+  const PsumTile<double> T = load_tile(psumT + f * bt_frame(W, H, 1), W, H, R, a.span, span);
   const int u = blockIdx.x * kTX + threadIdx.x;
   const uint8_t* L = lgray + f * gray_stride;
   const uint8_t* Rg = rgray + f * gray_stride;
@@ -378,20 +400,19 @@ __global__ void __launch_bounds__(kTX * kBY)
   }
 }
 
-void launch_d_repick(const double* psum, const uint8_t* valid, const int* cnt,
+void launch_d_repick(const double* psumT, const uint8_t* valid, const int* cnt,
                      const double* avg, const int* so, double* d, double* o,
                      const uint8_t* lgray, const uint8_t* rgray, const int2* lstat,
                      const float* vol, int2* chg, unsigned* chg_count, const RefineArgs& a,
-                     int frames, long stride, long pstride, long gray_stride,
-                     long lstat_stride, long vol_stride, unsigned long long* counters,
-                     cudaStream_t s) {
+                     int frames, long stride, long gray_stride, long lstat_stride,
+                     long vol_stride, unsigned long long* counters, cudaStream_t s) {
   if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
-  const size_t smem = tile_bytes(a.radius);
+  const size_t smem = tile_bytes<double>(a.radius);
   dim3 bl(kTX, kBY);
   dim3 grid((a.g.W + kTX - 1) / kTX, (a.g.H + kTY - 1) / kTY, frames);
 #define SS_REPICK_ARGS                                                                       \
-  psum, valid, cnt, avg, so, d, o, lgray, rgray, lstat, vol, chg, chg_count, a, stride,      \
-      pstride, gray_stride, lstat_stride, vol_stride, counters
+  psumT, valid, cnt, avg, so, d, o, lgray, rgray, lstat, vol, chg, chg_count, a, stride,     \
+      gray_stride, lstat_stride, vol_stride, counters
   if (a.radius == 15) {
     if (avg) k_d_repick<15, false><<<grid, bl, smem, s>>>(SS_REPICK_ARGS);
     else k_d_repick<15, true><<<grid, bl, smem, s>>>(SS_REPICK_ARGS);

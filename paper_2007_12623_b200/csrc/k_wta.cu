@@ -148,7 +148,6 @@ __global__ void __launch_bounds__(512) k_wta11(
   const int c0 = g.cmin + j * kDB;
   const int nact = min(kDB, g.NC - j * kDB);
   const bool active = (u < W - h) && (nact > 0);
-  const long HW = (long)H * W;
 
   ThreadGeom tg;
   tg.lplane = lplane;
@@ -203,14 +202,17 @@ __global__ void __launch_bounds__(512) k_wta11(
     if (active) {
       const int sl = __ldg(&lstat[(long)v * W + u].x);
       const int2* rrow = rstat + (long)v * g.SP + g.SPAD + ru0;
-      float* vrow = vol + (long)(j * kDB) * HW + (long)v * W + u;
+      // pixel-major volume: this thread's kDB candidates are 64 contiguous bytes
+      float4* vrow = reinterpret_cast<float4*>(vol + ((long)v * W + u) * g.NCP + j * kDB);
+      float gvs[kDB];
 #pragma unroll
       for (int i = 0; i < kDB; ++i) {
+        gvs[i] = 0.f;
         if (i < nact) {
           const int2 rs = __ldg(rrow - i);
           const int num = 61 * X[i] - sl * rs.x;
           const float gv = __int2float_rn(num) * __int_as_float(rs.y);
-          __stcs(vrow + (long)i * HW, gv);
+          gvs[i] = gv;
           const int c = c0 + i;
           if (c >= g.dmin && c <= g.dmax) {
             if (gv > best) {
@@ -223,6 +225,10 @@ __global__ void __launch_bounds__(512) k_wta11(
           }
         }
       }
+#pragma unroll
+      for (int q = 0; q < kDB / 4; ++q)
+        if (4 * q < nact)  // NCP is a multiple of 4: the tail vector stays in this pixel
+          __stcs(vrow + q, make_float4(gvs[4 * q], gvs[4 * q + 1], gvs[4 * q + 2], gvs[4 * q + 3]));
     }
     if (!do_argmax) continue;
     const int slot = (v - v_begin) & (kRB - 1);

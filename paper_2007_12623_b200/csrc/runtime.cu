@@ -137,6 +137,7 @@ Geom make_geom(int W, int H, const ss_stereo_params* p) {
   g.dmax = p->d_max;
   g.cmin = p->d_min - kRefineR;
   g.NC = p->d_max - p->d_min + 1 + 2 * kRefineR;
+  g.NCP = (int)round_up(std::max(g.NC, 1), 4);
   const int span = std::max(std::abs(g.cmin), std::abs(g.cmin + std::max(g.NC, 1) - 1)) + 2 * kDB;
   g.PB = (int)round_up(span / 2 + 24, 4);
   g.PP = (int)round_up((long)(W + 1) / 2 + 2L * g.PB, 16);
@@ -163,7 +164,7 @@ struct ss_ctx {
   DevBuf disp_a, disp_b, valid_a, valid_b, flags, flag_count;
   DevBuf o, d, avg, b, psum, pcnt, cnt, span, wtab, fspan;
   DevBuf index, block_sums, npoints, pts_f, nrm_f, colors, pts_d, nrm_d, pixels, pts4;
-  DevBuf counters, trace_o, trace_d, so, chg, chg_count;
+  DevBuf counters, trace_o, trace_d, so, chg, chg_count, xbt, mbt;
   int wtab_radius = -1;
 
   ss_ctx_stats stats{};
@@ -189,7 +190,7 @@ struct ss_ctx {
                       &disp_a, &disp_b, &valid_a, &valid_b, &flags, &flag_count, &o, &d, &avg,
                       &b, &psum, &pcnt, &cnt, &span, &wtab, &fspan, &index, &block_sums, &npoints,
                       &pts_f, &nrm_f, &colors, &pts_d, &nrm_d, &pixels, &pts4, &counters, &trace_o,
-                      &trace_d, &so, &chg, &chg_count})
+                      &trace_d, &so, &chg, &chg_count, &xbt, &mbt})
       b->release();
     for (auto& r : pending) {
       ev_pool.push_back(r.a);
@@ -282,7 +283,7 @@ struct ss_ctx {
     plane_r.ensure(plane_stride * n);
     lstat.ensure(sizeof(int2) * N * n);
     rstat.ensure(sizeof(int2) * rstride * n);
-    vol.ensure(sizeof(float) * (size_t)g.NC * N * n);
+    vol.ensure(sizeof(float) * (size_t)g.NCP * N * n);
     flags.ensure(sizeof(int) * N * n);
     flag_count.ensure(sizeof(unsigned) * n);
     {
@@ -302,7 +303,7 @@ struct ss_ctx {
     launch_wta11(plane_l.as<uint8_t>(), plane_r.as<uint8_t>(), lstat.as<int2>(), rstat.as<int2>(),
                  vol.as<float>(), disp_a.as<float>(), valid_a.as<uint8_t>(), flags.as<int>(),
                  flag_count.as<unsigned>(), g, params.min_zncc, n, plane_stride, N, rstride,
-                 (long)g.NC * N, N, do_argmax ? 1 : 0, stream);
+                 (long)g.NCP * N, N, do_argmax ? 1 : 0, stream);
     stats.kernel_launches += 1;
   }
 
@@ -391,13 +392,15 @@ struct ss_ctx {
     Stage st(this, 5);
     const int W = g.W, H = g.H;
     const long N = g.N();
-    const long pstride = (long)H * (W + 1);
+    const long bt_x = bt_frame(W, H, 0), bt_p = bt_frame(W, H, 1);  // BT frame strides
     o.ensure(sizeof(double) * N * n);
     d.ensure(sizeof(double) * N * n);
     avg.ensure(sizeof(double) * N * n);
     b.ensure(sizeof(double) * N * n);
-    psum.ensure(sizeof(double) * pstride * n);
-    pcnt.ensure(sizeof(int) * pstride * n);
+    psum.ensure(sizeof(double) * bt_p * n);   // BT prefix (double)
+    pcnt.ensure(sizeof(int) * bt_p * n);      // BT prefix (int)
+    xbt.ensure(sizeof(double) * bt_x * n);    // BT scan input (double / int)
+    mbt.ensure(bt_x * n);                     // BT mask
     cnt.ensure(sizeof(int) * N * n);
     const int r = params.smoothing_radius;
     std::vector<int> sp(std::max(r, 0) + 1);
@@ -421,45 +424,51 @@ struct ss_ctx {
       trace_o.ensure(sizeof(double) * N * std::max(iters, 1));
       trace_d.ensure(sizeof(double) * N * std::max(iters, 1));
     }
-    launch_refine_init(disp_a.as<float>(), valid_a.as<uint8_t>(), o.as<double>(), d.as<double>(),
-                       W, H, n, N, stream);
-    launch_row_count(valid_a.as<uint8_t>(), pcnt.as<int>(), W, H, n, N, pstride, stream);
-    launch_disc_count(valid_a.as<uint8_t>(), pcnt.as<int>(), cnt.as<int>(), a, n, N, pstride,
-                      stream);
-    stats.kernel_launches += 3;
+    const uint8_t* vm = valid_a.as<uint8_t>();
+    uint8_t* mT = mbt.as<uint8_t>();
+    launch_refine_init(disp_a.as<float>(), vm, o.as<double>(), d.as<double>(), W, H, n, N,
+                       stream);
+    launch_mask_bt(vm, mT, W, H, n, N, stream);
+    launch_ones_bt(vm, xbt.as<int>(), W, H, n, N, stream);
+    launch_scan_bt_i(xbt.as<int>(), mT, pcnt.as<int>(), W, H, n, stream);
+    launch_disc_isum(vm, pcnt.as<int>(), cnt.as<int>(), a, n, N, stream);  // disc counts
+    stats.kernel_launches += 5;
     so.ensure(sizeof(int) * N * n);
     chg.ensure(sizeof(int2) * N * n);
     chg_count.ensure(sizeof(unsigned) * n);
-    const uint8_t* vm = valid_a.as<uint8_t>();
     const float* volp = have_volume ? vol.as<float>() : nullptr;
     for (int it = 0; it < iters; ++it) {
       if (it == 0) {
         // o is the cleanup output (fractional fills): the reference's FP64 path.
-        launch_row_scan(o.as<double>(), vm, psum.as<double>(), W, H, n, N, pstride, stream);
+        launch_double_bt(o.as<double>(), vm, xbt.as<double>(), W, H, n, N, stream);
+        launch_scan_bt_d(xbt.as<double>(), mT, psum.as<double>(), W, H, n, stream);
         launch_avg_b(psum.as<double>(), vm, cnt.as<int>(), o.as<double>(), d.as<double>(),
-                     avg.as<double>(), b.as<double>(), a, n, N, pstride, stream);
-        launch_row_scan(b.as<double>(), vm, psum.as<double>(), W, H, n, N, pstride, stream);
+                     avg.as<double>(), b.as<double>(), a, n, N, stream);
+        launch_double_bt(b.as<double>(), vm, xbt.as<double>(), W, H, n, N, stream);
+        launch_scan_bt_d(xbt.as<double>(), mT, psum.as<double>(), W, H, n, stream);
         launch_d_repick(psum.as<double>(), vm, cnt.as<int>(), avg.as<double>(), nullptr,
                         d.as<double>(), o.as<double>(), gray_l.as<uint8_t>(),
                         gray_r.as<uint8_t>(), lstat.as<int2>(), volp, nullptr, nullptr, a, n, N,
-                        pstride, N, N, (long)g.NC * N, ctr() + 1, stream);
-        stats.kernel_launches += 4;
+                        N, N, (long)g.NCP * N, ctr() + 1, stream);
+        stats.kernel_launches += 6;
         if (iters > 1) {
           // o is integer-valued from here on: exact integer disc sums S_o.
-          launch_int_scan(o.as<double>(), vm, pcnt.as<int>(), W, H, n, N, pstride, stream);
-          launch_disc_count(vm, pcnt.as<int>(), so.as<int>(), a, n, N, pstride, stream);
-          stats.kernel_launches += 2;
+          launch_int_bt(o.as<double>(), vm, xbt.as<int>(), W, H, n, N, stream);
+          launch_scan_bt_i(xbt.as<int>(), mT, pcnt.as<int>(), W, H, n, stream);
+          launch_disc_isum(vm, pcnt.as<int>(), so.as<int>(), a, n, N, stream);
+          stats.kernel_launches += 3;
         }
       } else {
         ck(cudaMemsetAsync(chg_count.p, 0, sizeof(unsigned) * n, stream), "memset");
-        launch_b_scan(so.as<int>(), cnt.as<int>(), o.as<double>(), d.as<double>(), a.alpha,
-                      a.one_minus_alpha, vm, psum.as<double>(), W, H, n, N, pstride, stream);
+        launch_b_bt(so.as<int>(), cnt.as<int>(), o.as<double>(), d.as<double>(), a.alpha,
+                    a.one_minus_alpha, vm, xbt.as<double>(), W, H, n, N, stream);
+        launch_scan_bt_d(xbt.as<double>(), mT, psum.as<double>(), W, H, n, stream);
         launch_d_repick(psum.as<double>(), vm, cnt.as<int>(), nullptr, so.as<int>(),
                         d.as<double>(), o.as<double>(), gray_l.as<uint8_t>(),
                         gray_r.as<uint8_t>(), lstat.as<int2>(), volp, chg.as<int2>(),
-                        chg_count.as<unsigned>(), a, n, N, pstride, N, N, (long)g.NC * N,
-                        ctr() + 1, stream);
-        stats.kernel_launches += 2;
+                        chg_count.as<unsigned>(), a, n, N, N, N, (long)g.NCP * N, ctr() + 1,
+                        stream);
+        stats.kernel_launches += 3;
         if (it + 1 < iters) {
           launch_so_update(chg.as<int2>(), chg_count.as<unsigned>(), vm, so.as<int>(), a, n, N,
                            stream);

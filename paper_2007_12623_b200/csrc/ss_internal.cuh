@@ -9,8 +9,10 @@
 //   lstat[N]                 int2 {chessboard sum, float bits of 1/sqrt(var)}
 //   rstat[H][SP]             int2 same for the right image, SPAD padded
 //                                columns each side hold {0, NaN}
-//   vol[NC][H][W]            f32 g(c) = num(c) / sqrt(var_r) for c in
-//                                [d_min-5, d_max+5] (the refine range)
+//   vol[H][W][NCP]           f32 g(c) = num(c) / sqrt(var_r) for c in
+//                                [d_min-5, d_max+5] (the refine range),
+//                                pixel-major so a re-pick reads 11 adjacent
+//                                floats instead of 11 scattered planes
 //   disp/valid               f32/u8 DisparityMap (image.hpp:46-67)
 //   refine state             f64 o, d, avg, b; psum[H][W+1]; cnt[N] (int)
 #pragma once
@@ -29,6 +31,7 @@ struct Geom {
   int half;        // window / 2
   int dmin, dmax;  // candidate range of the WTA
   int cmin, NC;    // volume range [cmin, cmin + NC)
+  int NCP;         // per-pixel volume pitch (NC rounded up to 4 floats)
   int PB, PP;      // plane padding (bytes) and row pitch (bytes)
   int SPAD, SP;    // right-stat padding (elements) and row pitch
   long N() const { return (long)W * H; }
@@ -76,29 +79,43 @@ struct RefineArgs {
 };
 void launch_refine_init(const float* disp, const uint8_t* valid, double* o, double* d,
                         int W, int H, int frames, long stride, cudaStream_t s);
+// normal-layout per-row prefix counts (cleanup disc support)
 void launch_row_count(const uint8_t* valid, int* pcnt, int W, int H, int frames, long stride,
                       long pstride, cudaStream_t s);
-void launch_disc_count(const uint8_t* valid, const int* pcnt, int* cnt, const RefineArgs& a,
-                       int frames, long stride, long pstride, cudaStream_t s);
-void launch_row_scan(const double* val, const uint8_t* valid, double* psum, int W, int H,
-                     int frames, long stride, long pstride, cudaStream_t s);
-void launch_int_scan(const double* val, const uint8_t* valid, int* ipsum, int W, int H,
-                     int frames, long stride, long pstride, cudaStream_t s);
-void launch_b_scan(const int* so, const int* cnt, const double* o, const double* d,
-                   double alpha, double one_minus_alpha, const uint8_t* valid, double* psum,
-                   int W, int H, int frames, long stride, long pstride, cudaStream_t s);
-void launch_avg_b(const double* psum, const uint8_t* valid, const int* cnt, const double* o,
+// ---- BT layout (row-blocked transposed, k_scan.cu): element (v, c) at
+// ((v/32) * CW + c) * 32 + v%32; frame stride ceil(H/32) * CW * 32 ----
+__host__ __device__ inline long bt_frame(int W, int H, int extra_col) { return (long)((H + 31) / 32) * (W + extra_col) * 32; }
+void launch_mask_bt(const uint8_t* mask, uint8_t* mT, int W, int H, int frames, long stride,
+                    cudaStream_t s);
+void launch_ones_bt(const uint8_t* mask, int* outT, int W, int H, int frames, long stride,
+                    cudaStream_t s);
+void launch_double_bt(const double* val, const uint8_t* mask, double* outT, int W, int H,
+                      int frames, long stride, cudaStream_t s);
+void launch_int_bt(const double* val, const uint8_t* mask, int* outT, int W, int H, int frames,
+                   long stride, cudaStream_t s);
+void launch_b_bt(const int* so, const int* cnt, const double* o, const double* d, double alpha,
+                 double one_minus_alpha, const uint8_t* mask, double* bT, int W, int H,
+                 int frames, long stride, cudaStream_t s);
+// masked serial row prefix (psum[.][0] = 0, W + 1 columns, BT layout)
+void launch_scan_bt_d(const double* xT, const uint8_t* mT, double* pT, int W, int H, int frames,
+                      cudaStream_t s);
+void launch_scan_bt_i(const int* xT, const uint8_t* mT, int* pT, int W, int H, int frames,
+                      cudaStream_t s);
+// exact integer disc sums from an int BT prefix (disc counts, S_o)
+void launch_disc_isum(const uint8_t* valid, const int* ipsumT, int* out, const RefineArgs& a,
+                      int frames, long stride, cudaStream_t s);
+// iteration 0: avg = disc mean of o (FP64, reference order), b (normal layout)
+void launch_avg_b(const double* psumT, const uint8_t* valid, const int* cnt, const double* o,
                   const double* d, double* avg, double* b, const RefineArgs& a, int frames,
-                  long stride, long pstride, cudaStream_t s);
+                  long stride, cudaStream_t s);
 // avg: the double disc mean of o (iteration 0) or nullptr to use the exact
 // integer disc sum `so` (iterations >= 1); o changes are appended to chg.
-void launch_d_repick(const double* psum, const uint8_t* valid, const int* cnt,
+void launch_d_repick(const double* psumT, const uint8_t* valid, const int* cnt,
                      const double* avg, const int* so, double* d, double* o,
                      const uint8_t* lgray, const uint8_t* rgray, const int2* lstat,
                      const float* vol, int2* chg, unsigned* chg_count, const RefineArgs& a,
-                     int frames, long stride, long pstride, long gray_stride,
-                     long lstat_stride, long vol_stride, unsigned long long* counters,
-                     cudaStream_t s);
+                     int frames, long stride, long gray_stride, long lstat_stride,
+                     long vol_stride, unsigned long long* counters, cudaStream_t s);
 // S_o += delta over the disc of every changed pixel (exact integers).
 void launch_so_update(const int2* chg, const unsigned* chg_count, const uint8_t* valid,
                       int* so, const RefineArgs& a, int frames, long stride, cudaStream_t s);
