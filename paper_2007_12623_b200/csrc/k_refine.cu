@@ -264,18 +264,20 @@ __device__ __forceinline__ double exact_cost(const uint8_t* L, const uint8_t* R,
 constexpr int kMaxCand = 2 * kRefineR + 1;
 
 // Re-pick of one pixel (smoothing.cpp:119-144) given its smoothed d.
+// Returns the new o, or INT_MIN when the pixel is deferred to the exact kernel
+// (or has no candidate at all).
 __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double dv,
-                                      const uint8_t* L, const uint8_t* R, const int2* lstat_f,
-                                      const float* vol_f, long pix,
-                                      unsigned long long* counters) {
+                                      const uint8_t* L, const uint8_t* R, const float* win_f,
+                                      const int* wbase_f, long pix, Deferred* defer,
+                                      unsigned* defer_count) {
   const int W = a.g.W, H = a.g.H, half = a.g.half;
   const int c_lo = max((int)ceil(__dsub_rn(dv, (double)kRefineR)), (int)ceil(a.lo));
   const int c_hi = min((int)floor(__dadd_rn(dv, (double)kRefineR)), (int)floor(a.hi));
   if (c_lo > c_hi) return INT_MIN;  // unreachable for a clamped d; mirrors `found`
   const bool fits = u >= half && u < W - half && v >= half && v < H - half;
 
-  if (vol_f == nullptr) {
-    // Generic window: every candidate in exact FP64.
+  if (win_f == nullptr) {
+    // Generic window size: every candidate in exact FP64 (no score windows).
     double best_cost = 0.0;
     int best = c_lo;
     for (int c = c_lo; c <= c_hi; ++c) {
@@ -288,9 +290,8 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
     return best;
   }
 
-  float rl = __int_as_float(0x7fc00000);
-  if (fits) rl = __int_as_float(__ldg(&lstat_f[pix].y));
-  if (isnan(rl)) {
+  const int wb = fits ? wbase_f[pix] : kNoWin;
+  if (wb == kNoWin) {
     // Window does not fit or var_l == 0: every match cost is exactly
     // 1/kZnccCostEpsilon, so the reference's double costs are computed as is.
     const double m = __ddiv_rn(1.0, kZnccEps);
@@ -306,52 +307,49 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
     }
     return best;
   }
-  const float* vp = vol_f + pix * a.g.NCP - a.g.cmin;  // vp[c]: candidate c of this pixel
-  float cf[kMaxCand];
-  float best_f = INFINITY;
+  int mask = 0;
   int best = c_lo;
-#pragma unroll
-  for (int k = 0; k < kMaxCand; ++k) {
-    const int c = c_lo + k;
-    cf[k] = INFINITY;
-    if (c <= c_hi) {
-      const int ru = u - c;
-      float m = 1000.f;  // 1 / kZnccCostEpsilon, exact
-      if (ru >= half && ru < W - half) {
-        const float sc = __ldg(vp + c) * rl;
-        if (!isnan(sc)) m = 1.f / fmaxf(sc, 1e-3f);
-      }
-      const float df = (float)__dsub_rn((double)c, dv);
-      cf[k] = m + a.eta_f * df * df;
-      if (cf[k] < best_f) {
-        best_f = cf[k];
-        best = c;
-      }
-    }
-  }
-  // Any candidate whose exact cost could undercut the float minimum
-  // (|cost_f - cost| <= 7 ulp = 4.2e-7 relative; margin 4e-6).
-  const float thr = best_f * (1.0f + 4e-6f);
-  int near = 0;
-#pragma unroll
-  for (int k = 0; k < kMaxCand; ++k) near += (cf[k] <= thr) ? 1 : 0;
-  if (near > 1) {
-    double best_cost = 0.0;
-    bool found = false;
+  if (c_lo < wb || c_hi > wb + kWin - 1) {
+    mask = (1 << (c_hi - c_lo + 1)) - 1;  // window miss: score every candidate exactly
+  } else {
+    const float* wp = win_f + pix * kWin - wb;  // wp[c]: score of candidate c
+    float cf[kMaxCand];
+    float best_f = INFINITY;
 #pragma unroll
     for (int k = 0; k < kMaxCand; ++k) {
-      if (!(cf[k] <= thr)) continue;
       const int c = c_lo + k;
-      const double cost = exact_cost(L, R, W, u, v, c, fits, half, dv, a.eta);
-      if (!found || cost < best_cost) {
-        found = true;
-        best_cost = cost;
-        best = c;
+      cf[k] = INFINITY;
+      if (c <= c_hi) {
+        const int ru = u - c;
+        float m = 1000.f;  // 1 / kZnccCostEpsilon, exact
+        if (ru >= half && ru < W - half) {
+          const float sc = __ldg(wp + c);
+          if (!isnan(sc)) m = 1.f / fmaxf(sc, 1e-3f);
+        }
+        const float df = (float)__dsub_rn((double)c, dv);
+        cf[k] = m + a.eta_f * df * df;
+        if (cf[k] < best_f) {
+          best_f = cf[k];
+          best = c;
+        }
       }
     }
-    atomicAdd(counters, 1ull);
+    // Any candidate whose exact cost could undercut the float minimum
+    // (|cost_f - cost| <= 7 ulp = 4.2e-7 relative; margin 4e-6).
+    const float thr = best_f * (1.0f + 4e-6f);
+#pragma unroll
+    for (int k = 0; k < kMaxCand; ++k)
+      if (cf[k] <= thr) mask |= 1 << k;
+    if (__popc(mask) == 1) return best;
   }
-  return best;
+  Deferred e;
+  e.pix = (int)pix;
+  e.c_lo = c_lo;
+  e.mask = mask;
+  e.pad = 0;
+  e.d = dv;
+  defer[atomicAdd(defer_count, 1u)] = e;
+  return INT_MIN;
 }
 
 template <int RF, bool USE_SO>
@@ -360,10 +358,10 @@ __global__ void __launch_bounds__(kTX * kBY)
                const int* __restrict__ cnt, const double* __restrict__ avg,
                const int* __restrict__ so, double* __restrict__ d, double* __restrict__ o,
                const uint8_t* __restrict__ lgray, const uint8_t* __restrict__ rgray,
-               const int2* __restrict__ lstat, const float* __restrict__ vol,
-               int2* __restrict__ chg, unsigned* __restrict__ chg_count, RefineArgs a,
-               long stride, long gray_stride, long lstat_stride, long vol_stride,
-               unsigned long long* __restrict__ counters) {
+               const float* __restrict__ win, const int* __restrict__ wbase,
+               int2* __restrict__ chg, unsigned* __restrict__ chg_count,
+               Deferred* __restrict__ defer, unsigned* __restrict__ defer_count, RefineArgs a,
+               long stride, long gray_stride) {
   const long f = blockIdx.z;
   const int W = a.g.W, H = a.g.H, R = a.radius;
   int* span;
@@ -371,8 +369,8 @@ __global__ void __launch_bounds__(kTX * kBY)
   const int u = blockIdx.x * kTX + threadIdx.x;
   const uint8_t* L = lgray + f * gray_stride;
   const uint8_t* Rg = rgray + f * gray_stride;
-  const int2* ls = lstat + f * lstat_stride;
-  const float* vf = vol ? vol + f * vol_stride : nullptr;
+  const float* wf = win ? win + f * stride * kWin : nullptr;
+  const int* wbf = wbase + f * stride;
 #pragma unroll 1
   for (int rr = 0; rr < kTY / kBY; ++rr) {
     const int v = blockIdx.y * kTY + threadIdx.y + rr * kBY;
@@ -389,11 +387,13 @@ __global__ void __launch_bounds__(kTX * kBY)
     const double x = __dsub_rn(av, bav);
     const double dv = x < a.lo ? a.lo : (a.hi < x ? a.hi : x);  // std::clamp
     d[i] = dv;
-    const int best = repick(a, u, v, dv, L, Rg, ls, vf, pix, counters);
+    const int best = repick(a, u, v, dv, L, Rg, wf, wbf, pix, defer + f * stride,
+                            defer_count + f);
     if (best != INT_MIN) {
       if (USE_SO) {
         const int old = (int)o[i];
-        if (best != old) chg[f * stride + atomicAdd(chg_count + f, 1u)] = make_int2((int)pix, best - old);
+        if (best != old)
+          chg[f * stride + atomicAdd(chg_count + f, 1u)] = make_int2((int)pix, best - old);
       }
       o[i] = best;
     }
@@ -402,17 +402,18 @@ __global__ void __launch_bounds__(kTX * kBY)
 
 void launch_d_repick(const double* psumT, const uint8_t* valid, const int* cnt,
                      const double* avg, const int* so, double* d, double* o,
-                     const uint8_t* lgray, const uint8_t* rgray, const int2* lstat,
-                     const float* vol, int2* chg, unsigned* chg_count, const RefineArgs& a,
-                     int frames, long stride, long gray_stride, long lstat_stride,
-                     long vol_stride, unsigned long long* counters, cudaStream_t s) {
+                     const uint8_t* lgray, const uint8_t* rgray, const float* win,
+                     const int* wbase, int2* chg, unsigned* chg_count, Deferred* defer,
+                     unsigned* defer_count, const RefineArgs& a, int frames, long stride,
+                     long gray_stride, unsigned long long* counters, cudaStream_t s) {
+  (void)counters;
   if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
   const size_t smem = tile_bytes<double>(a.radius);
   dim3 bl(kTX, kBY);
   dim3 grid((a.g.W + kTX - 1) / kTX, (a.g.H + kTY - 1) / kTY, frames);
-#define SS_REPICK_ARGS                                                                       \
-  psumT, valid, cnt, avg, so, d, o, lgray, rgray, lstat, vol, chg, chg_count, a, stride,     \
-      gray_stride, lstat_stride, vol_stride, counters
+#define SS_REPICK_ARGS                                                                        \
+  psumT, valid, cnt, avg, so, d, o, lgray, rgray, win, wbase, chg, chg_count, defer,          \
+      defer_count, a, stride, gray_stride
   if (a.radius == 15) {
     if (avg) k_d_repick<15, false><<<grid, bl, smem, s>>>(SS_REPICK_ARGS);
     else k_d_repick<15, true><<<grid, bl, smem, s>>>(SS_REPICK_ARGS);
@@ -429,6 +430,61 @@ void launch_d_repick(const double* psumT, const uint8_t* valid, const int* cnt,
     else k_d_repick<0, true><<<grid, bl, smem, s>>>(SS_REPICK_ARGS);
   }
 #undef SS_REPICK_ARGS
+}
+
+// Deferred re-picks: one warp per pixel, lane k scores candidate c_lo + k in
+// exact FP64 (zncc_exact, reference cost formula); the warp takes the first
+// minimum (smallest candidate among equal costs), as smoothing.cpp:138 does.
+__global__ void k_repick_exact(const Deferred* __restrict__ defer,
+                               const unsigned* __restrict__ defer_count, double* __restrict__ o,
+                               const uint8_t* __restrict__ lgray,
+                               const uint8_t* __restrict__ rgray, int2* __restrict__ chg,
+                               unsigned* __restrict__ chg_count, RefineArgs a, long stride,
+                               long gray_stride, unsigned long long* __restrict__ counters) {
+  const long f = blockIdx.y;
+  const unsigned n = defer_count[f];
+  if (blockIdx.x == 0 && threadIdx.x == 0 && counters) atomicAdd(counters, (unsigned long long)n);
+  const int lane = threadIdx.x & 31;
+  const int W = a.g.W, H = a.g.H, half = a.g.half;
+  const uint8_t* L = lgray + f * gray_stride;
+  const uint8_t* R = rgray + f * gray_stride;
+  const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
+  for (unsigned t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n; t += nwarps) {
+    const Deferred e = defer[f * stride + t];
+    const int u = e.pix % W, v = e.pix / W;
+    const bool fits = u >= half && u < W - half && v >= half && v < H - half;
+    double cost = INFINITY;
+    if (lane < kMaxCand && ((e.mask >> lane) & 1))
+      cost = exact_cost(L, R, W, u, v, e.c_lo + lane, fits, half, e.d, a.eta);
+    int k = (lane < kMaxCand && ((e.mask >> lane) & 1)) ? lane : 64;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double oc = __shfl_down_sync(0xffffffffu, cost, off);
+      const int ok = __shfl_down_sync(0xffffffffu, k, off);
+      if (oc < cost || (oc == cost && ok < k)) {
+        cost = oc;
+        k = ok;
+      }
+    }
+    if (lane == 0 && k < 64) {
+      const int best = e.c_lo + k;
+      const long i = f * stride + e.pix;
+      if (chg) {
+        const int old = (int)o[i];
+        if (best != old) chg[f * stride + atomicAdd(chg_count + f, 1u)] = make_int2(e.pix, best - old);
+      }
+      o[i] = best;
+    }
+  }
+}
+
+void launch_repick_exact(const Deferred* defer, const unsigned* defer_count, double* o,
+                         const uint8_t* lgray, const uint8_t* rgray, int2* chg,
+                         unsigned* chg_count, const RefineArgs& a, int frames, long stride,
+                         long gray_stride, unsigned long long* counters, cudaStream_t s) {
+  if (frames <= 0) return;
+  k_repick_exact<<<dim3(64, frames), 256, 0, s>>>(defer, defer_count, o, lgray, rgray, chg,
+                                                  chg_count, a, stride, gray_stride, counters);
 }
 
 // One warp per changed pixel j: S_o(i) += delta_j for every valid i whose disc

@@ -13,8 +13,10 @@
 //       X(v+1) = Y(v) - He(v-5) + Ho(v+6),   Y(v+1) = X(v) + He(v+6) - Ho(v-5)
 //   where X(v) = sum_{dv even} He(v+dv) + sum_{dv odd} Ho(v+dv) = slr(v).
 //   num = 61 slr - sl sr is exact; g = float(num) / sqrt(var_r) (FP32, <= 3 ulp)
-//   goes to the cost volume (read back by the refinement re-pick) and feeds a
-//   per-thread (best, second, arg) that NB warps merge through shared memory.
+//   feeds a per-thread (best, second, arg) that NB warps merge through shared
+//   memory, and is staged there so that, once a pixel's pick is known, the
+//   kWin = 16 candidates around it are written as the refinement's score
+//   window (64 B/pixel instead of a (D+10) x 4 B cost volume).
 //   A pick is final only when it is separated from the runner-up and from the
 //   min_zncc threshold by a margin far above the FP32 error (4e-6 relative);
 //   otherwise the pixel is appended to a list for k_wta_exact (FP64, exact),
@@ -117,23 +119,27 @@ __device__ __forceinline__ void row_terms(const ThreadGeom& tg, int y, uint32_t 
 
 __global__ void __launch_bounds__(512) k_wta11(
     const uint8_t* __restrict__ lplane, const uint8_t* __restrict__ rplane,
-    const int2* __restrict__ lstat, const int2* __restrict__ rstat, float* __restrict__ vol,
-    float* __restrict__ disp, uint8_t* __restrict__ valid, int* __restrict__ flag_list,
+    const int2* __restrict__ lstat, const int2* __restrict__ rstat, float* __restrict__ win,
+    int* __restrict__ wbase, const int* __restrict__ base_map, float* __restrict__ disp,
+    uint8_t* __restrict__ valid, int* __restrict__ flag_list,
     unsigned int* __restrict__ flag_count, Geom g, int TH, float min_zncc_f, float thr_tol,
-    int do_argmax, long plane_stride, long lstat_stride, long rstat_stride, long vol_stride,
-    long map_stride) {
+    int do_argmax, long plane_stride, long lstat_stride, long rstat_stride, long map_stride) {
   extern __shared__ unsigned char smem_raw[];
   const int lane = threadIdx.x, j = threadIdx.y, NB = blockDim.y;
+  const int NCB = NB * kDB;  // staged candidates per pixel
   float* s_best = reinterpret_cast<float*>(smem_raw);
   float* s_sec = s_best + kRB * NB * 32;
   int* s_arg = reinterpret_cast<int*>(s_sec + kRB * NB * 32);
+  float* s_g = reinterpret_cast<float*>(s_arg + kRB * NB * 32);  // [kRB][NCB][32]
 
   const long fr = blockIdx.z;
   lplane += fr * plane_stride;
   rplane += fr * plane_stride;
   lstat += fr * lstat_stride;
   rstat += fr * rstat_stride;
-  vol += fr * vol_stride;
+  win += fr * map_stride * kWin;
+  wbase += fr * map_stride;
+  if (base_map) base_map += fr * map_stride;
   disp += fr * map_stride;
   valid += fr * map_stride;
   flag_list += fr * map_stride;
@@ -197,22 +203,20 @@ __global__ void __launch_bounds__(512) k_wta11(
         Y[i] = yn;
       }
     }
+    const int slot = (v - v_begin) & (kRB - 1);
+    float* gs = s_g + (slot * NCB + j * kDB) * 32 + lane;  // staged g of this (row, block)
     float best = -INFINITY, second = -INFINITY;
     int arg = kNoArg;
     if (active) {
       const int sl = __ldg(&lstat[(long)v * W + u].x);
       const int2* rrow = rstat + (long)v * g.SP + g.SPAD + ru0;
-      // pixel-major volume: this thread's kDB candidates are 64 contiguous bytes
-      float4* vrow = reinterpret_cast<float4*>(vol + ((long)v * W + u) * g.NCP + j * kDB);
-      float gvs[kDB];
 #pragma unroll
       for (int i = 0; i < kDB; ++i) {
-        gvs[i] = 0.f;
         if (i < nact) {
           const int2 rs = __ldg(rrow - i);
           const int num = 61 * X[i] - sl * rs.x;
           const float gv = __int2float_rn(num) * __int_as_float(rs.y);
-          gvs[i] = gv;
+          gs[i * 32] = gv;
           const int c = c0 + i;
           if (c >= g.dmin && c <= g.dmax) {
             if (gv > best) {
@@ -225,13 +229,7 @@ __global__ void __launch_bounds__(512) k_wta11(
           }
         }
       }
-#pragma unroll
-      for (int q = 0; q < kDB / 4; ++q)
-        if (4 * q < nact)  // NCP is a multiple of 4: the tail vector stays in this pixel
-          __stcs(vrow + q, make_float4(gvs[4 * q], gvs[4 * q + 1], gvs[4 * q + 2], gvs[4 * q + 3]));
     }
-    if (!do_argmax) continue;
-    const int slot = (v - v_begin) & (kRB - 1);
     const int so = (slot * NB + j) * 32 + lane;
     s_best[so] = best;
     s_sec[so] = second;
@@ -258,21 +256,43 @@ __global__ void __launch_bounds__(512) k_wta11(
           const int vv = v - slot + r;
           const long idx = (long)vv * W + u;
           const float rl = __int_as_float(__ldg(&lstat[idx].y));
-          float dout = 0.f;
-          uint8_t vout = 0;
-          if (A != kNoArg && !isnan(rl)) {
-            const bool near_tie = S >= B - 4e-6f * fabsf(B);
-            const float sc = B * rl;
-            const bool amb = fabsf(sc - min_zncc_f) <= thr_tol;
-            if (near_tie || amb) {
-              flag_list[atomicAdd(flag_count, 1u)] = (int)idx;
-            } else if (sc >= min_zncc_f) {
-              dout = (float)A;
-              vout = 1;
+          if (do_argmax) {
+            float dout = 0.f;
+            uint8_t vout = 0;
+            if (A != kNoArg && !isnan(rl)) {
+              const bool near_tie = S >= B - 4e-6f * fabsf(B);
+              const float sc = B * rl;
+              const bool amb = fabsf(sc - min_zncc_f) <= thr_tol;
+              if (near_tie || amb) {
+                flag_list[atomicAdd(flag_count, 1u)] = (int)idx;
+              } else if (sc >= min_zncc_f) {
+                dout = (float)A;
+                vout = 1;
+              }
             }
+            disp[idx] = dout;
+            valid[idx] = vout;
           }
-          disp[idx] = dout;
-          valid[idx] = vout;
+          // Candidate window for the refinement: kWin consecutive scores
+          // s = g * rl around the pick (or the caller's base map).
+          const int anchor = base_map ? base_map[idx] : A;
+          int wb = kNoWin;
+          if (!isnan(rl) && anchor != kNoArg && anchor != kNoWin)
+            wb = window_base(anchor, g.cmin, g.NC);
+          wbase[idx] = wb;
+          if (wb != kNoWin) {
+            const float* gr = s_g + r * NCB * 32 + lane;
+            float w[kWin];
+#pragma unroll
+            for (int q = 0; q < kWin; ++q) {
+              const int ci = wb - g.cmin + q;
+              w[q] = ci < g.NC ? gr[ci * 32] * rl : __int_as_float(0x7fc00000);
+            }
+            float4* wp = reinterpret_cast<float4*>(win + idx * kWin);
+#pragma unroll
+            for (int q = 0; q < kWin / 4; ++q)
+              wp[q] = make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+          }
         }
       }
       __syncthreads();
@@ -281,22 +301,27 @@ __global__ void __launch_bounds__(512) k_wta11(
 }
 
 void launch_wta11(const uint8_t* lplane, const uint8_t* rplane, const int2* lstat,
-                  const int2* rstat, float* vol, float* disp, uint8_t* valid, int* flag_list,
-                  unsigned int* flag_count, const Geom& g, double min_zncc, int frames,
-                  long plane_stride, long lstat_stride, long rstat_stride, long vol_stride,
-                  long map_stride, int do_argmax, cudaStream_t s) {
+                  const int2* rstat, float* win, int* wbase, const int* base_map, float* disp,
+                  uint8_t* valid, int* flag_list, unsigned int* flag_count, const Geom& g,
+                  double min_zncc, int frames, long plane_stride, long lstat_stride,
+                  long rstat_stride, long map_stride, int do_argmax, cudaStream_t s) {
   const int h = 5;
   if (g.W - 2 * h <= 0 || g.H - 2 * h <= 0 || frames <= 0) return;
   const int NB = (g.NC + kDB - 1) / kDB;
   const int TH = 32;
   dim3 block(32, NB);
   dim3 grid((g.W - 2 * h + 31) / 32, (g.H - 2 * h + TH - 1) / TH, frames);
-  const size_t smem = (size_t)kRB * NB * 32 * 12;
+  const size_t smem = (size_t)kRB * NB * 32 * 12 + (size_t)kRB * NB * kDB * 32 * 4;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaFuncSetAttribute(k_wta11, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = smem;
+  }
   const float mz = (float)min_zncc;
   const float tol = 4e-6f * fmaxf(1.f, fabsf(mz));
-  k_wta11<<<grid, block, smem, s>>>(lplane, rplane, lstat, rstat, vol, disp, valid, flag_list,
-                                    flag_count, g, TH, mz, tol, do_argmax, plane_stride,
-                                    lstat_stride, rstat_stride, vol_stride, map_stride);
+  k_wta11<<<grid, block, smem, s>>>(lplane, rplane, lstat, rstat, win, wbase, base_map, disp,
+                                    valid, flag_list, flag_count, g, TH, mz, tol, do_argmax,
+                                    plane_stride, lstat_stride, rstat_stride, map_stride);
 }
 
 // ---- exact FP64 path: warp per pixel, lanes over d ----
@@ -387,6 +412,86 @@ void launch_wta_generic(const uint8_t* lgray, const uint8_t* rgray, float* disp,
   k_wta_exact<<<dim3(1184, frames), 256, 0, s>>>(lgray, rgray, nullptr, nullptr, disp, valid,
                                                  g, min_zncc, gray_stride, map_stride, 0, 1,
                                                  nullptr);
+}
+
+// ---- candidate windows for pixels the cleanup changed (post-cleanup) ----
+
+// Pass 1: a valid pixel needs a window centred on its (possibly filled)
+// disparity o0; if the sweep's window is centred elsewhere (the pixel was
+// removed/filled, or its WTA pick was resolved in FP64) queue it.
+__global__ void k_window_check(const float* __restrict__ disp, const uint8_t* __restrict__ valid,
+                               const int2* __restrict__ lstat, int* __restrict__ wbase,
+                               int* __restrict__ list, unsigned* __restrict__ count, Geom g,
+                               long stride) {
+  const long f = blockIdx.z;
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y * blockDim.y + threadIdx.y;
+  if (u >= g.W || v >= g.H) return;
+  const long pix = (long)v * g.W + u, i = f * stride + pix;
+  if (!valid[i]) return;
+  const int h = g.half;
+  const bool fits = u >= h && u < g.W - h && v >= h && v < g.H - h;
+  if (!fits || isnan(__int_as_float(__ldg(&lstat[i].y)))) {
+    wbase[i] = kNoWin;
+    return;
+  }
+  const int want = window_base((int)floor((double)disp[i]), g.cmin, g.NC);
+  if (wbase[i] != want) list[f * stride + atomicAdd(count + f, 1u)] = (int)pix;
+}
+
+// Pass 2: half a warp per queued pixel, lane q computes candidate wbase + q
+// with the sweep's exact integer arithmetic (61-tap chessboard cross sum,
+// num = 61 slr - sl sr, g = float(num) / sqrt(var_r), s = g / sqrt(var_l)),
+// so the window is bit-identical to one the sweep would have written.
+__global__ void k_window_build(const float* __restrict__ disp, const uint8_t* __restrict__ lgray,
+                               const uint8_t* __restrict__ rgray, const int2* __restrict__ lstat,
+                               const int2* __restrict__ rstat, float* __restrict__ win,
+                               int* __restrict__ wbase, const int* __restrict__ list,
+                               const unsigned* __restrict__ count, Geom g, long stride,
+                               long rstat_stride) {
+  const long f = blockIdx.y;
+  const unsigned n = count[f];
+  const int q = threadIdx.x & (kWin - 1);
+  const unsigned groups = gridDim.x * (blockDim.x / kWin);
+  const uint8_t* L = lgray + f * stride;
+  const uint8_t* R = rgray + f * stride;
+  const int W = g.W, h = g.half;
+  for (unsigned t = (blockIdx.x * blockDim.x + threadIdx.x) / kWin; t < n; t += groups) {
+    const int pix = list[f * stride + t];
+    const int u = pix % W, v = pix / W;
+    const long i = f * stride + pix;
+    const int wb = window_base((int)floor((double)disp[i]), g.cmin, g.NC);
+    const int c = wb + q;
+    const int ru = u - c;
+    float s = __int_as_float(0x7fc00000);
+    if (c < g.cmin + g.NC && ru >= h && ru < W - h) {
+      const int2 ls = __ldg(&lstat[i]);
+      const int2 rs = __ldg(&rstat[f * rstat_stride + (long)v * g.SP + g.SPAD + ru]);
+      int slr = 0;
+      for (int dv = -h; dv <= h; ++dv) {
+        const uint8_t* lr = L + (long)(v + dv) * W + u;
+        const uint8_t* rr = R + (long)(v + dv) * W + ru;
+        for (int du = -h + ((dv + h) & 1); du <= h; du += 2) slr += (int)__ldg(lr + du) * __ldg(rr + du);
+      }
+      const int num = 61 * slr - ls.x * rs.x;
+      s = (__int2float_rn(num) * __int_as_float(rs.y)) * __int_as_float(ls.y);
+    }
+    win[i * kWin + q] = s;
+    if (q == 0) wbase[i] = wb;
+  }
+}
+
+void launch_window_fix(const float* disp, const uint8_t* valid, const uint8_t* lgray,
+                       const uint8_t* rgray, const int2* lstat, const int2* rstat, float* win,
+                       int* wbase, int* list, unsigned* count, const Geom& g, int frames,
+                       long stride, long rstat_stride, cudaStream_t s) {
+  if (g.W <= 0 || g.H <= 0 || frames <= 0) return;
+  cudaMemsetAsync(count, 0, sizeof(unsigned) * frames, s);
+  dim3 b(32, 8);
+  k_window_check<<<dim3((g.W + 31) / 32, (g.H + 7) / 8, frames), b, 0, s>>>(
+      disp, valid, lstat, wbase, list, count, g, stride);
+  k_window_build<<<dim3(148, frames), 256, 0, s>>>(disp, lgray, rgray, lstat, rstat, win, wbase,
+                                                   list, count, g, stride, rstat_stride);
 }
 
 }  // namespace ssb

@@ -160,11 +160,11 @@ struct ss_ctx {
   bool has_rig = false;
   int max_w = 0, max_h = 0, max_batch = 1;
 
-  DevBuf in_l, in_r, gray_l, gray_r, plane_l, plane_r, lstat, rstat, vol;
+  DevBuf in_l, in_r, gray_l, gray_r, plane_l, plane_r, lstat, rstat, win, wbase;
   DevBuf disp_a, disp_b, valid_a, valid_b, flags, flag_count;
   DevBuf o, d, avg, b, psum, pcnt, cnt, span, wtab, fspan;
   DevBuf index, block_sums, npoints, pts_f, nrm_f, colors, pts_d, nrm_d, pixels, pts4;
-  DevBuf counters, trace_o, trace_d, so, chg, chg_count, xbt, mbt;
+  DevBuf counters, trace_o, trace_d, so, chg, chg_count, xbt, mbt, defer, defer_count;
   int wtab_radius = -1;
 
   ss_ctx_stats stats{};
@@ -186,11 +186,11 @@ struct ss_ctx {
   int last_frames = 0;
 
   ~ss_ctx() {
-    for (DevBuf* b : {&in_l, &in_r, &gray_l, &gray_r, &plane_l, &plane_r, &lstat, &rstat, &vol,
+    for (DevBuf* b : {&in_l, &in_r, &gray_l, &gray_r, &plane_l, &plane_r, &lstat, &rstat, &win, &wbase,
                       &disp_a, &disp_b, &valid_a, &valid_b, &flags, &flag_count, &o, &d, &avg,
                       &b, &psum, &pcnt, &cnt, &span, &wtab, &fspan, &index, &block_sums, &npoints,
                       &pts_f, &nrm_f, &colors, &pts_d, &nrm_d, &pixels, &pts4, &counters, &trace_o,
-                      &trace_d, &so, &chg, &chg_count, &xbt, &mbt})
+                      &trace_d, &so, &chg, &chg_count, &xbt, &mbt, &defer, &defer_count})
       b->release();
     for (auto& r : pending) {
       ev_pool.push_back(r.a);
@@ -283,7 +283,8 @@ struct ss_ctx {
     plane_r.ensure(plane_stride * n);
     lstat.ensure(sizeof(int2) * N * n);
     rstat.ensure(sizeof(int2) * rstride * n);
-    vol.ensure(sizeof(float) * (size_t)g.NCP * N * n);
+    win.ensure(sizeof(float) * kWin * N * n);
+    wbase.ensure(sizeof(int) * N * n);
     flags.ensure(sizeof(int) * N * n);
     flag_count.ensure(sizeof(unsigned) * n);
     {
@@ -301,9 +302,9 @@ struct ss_ctx {
     }
     Stage st(this, 2);
     launch_wta11(plane_l.as<uint8_t>(), plane_r.as<uint8_t>(), lstat.as<int2>(), rstat.as<int2>(),
-                 vol.as<float>(), disp_a.as<float>(), valid_a.as<uint8_t>(), flags.as<int>(),
-                 flag_count.as<unsigned>(), g, params.min_zncc, n, plane_stride, N, rstride,
-                 (long)g.NCP * N, N, do_argmax ? 1 : 0, stream);
+                 win.as<float>(), wbase.as<int>(), nullptr, disp_a.as<float>(),
+                 valid_a.as<uint8_t>(), flags.as<int>(), flag_count.as<unsigned>(), g,
+                 params.min_zncc, n, plane_stride, N, rstride, N, do_argmax ? 1 : 0, stream);
     stats.kernel_launches += 1;
   }
 
@@ -388,7 +389,7 @@ struct ss_ctx {
   }
 
   // refine_disparities: disp_a/valid_a (+ gray, volume) -> disp_b/valid_a.
-  void run_refine(int n, const Geom& g, bool have_volume, double* h_trace_o, double* h_trace_d) {
+  void run_refine(int n, const Geom& g, bool have_windows, double* h_trace_o, double* h_trace_d) {
     Stage st(this, 5);
     const int W = g.W, H = g.H;
     const long N = g.N();
@@ -436,7 +437,29 @@ struct ss_ctx {
     so.ensure(sizeof(int) * N * n);
     chg.ensure(sizeof(int2) * N * n);
     chg_count.ensure(sizeof(unsigned) * n);
-    const float* volp = have_volume ? vol.as<float>() : nullptr;
+    // Score windows: re-centre the sweep's windows on the cleanup output.
+    const float* winp = nullptr;
+    if (have_windows && iters > 0) {
+      launch_window_fix(disp_a.as<float>(), vm, gray_l.as<uint8_t>(), gray_r.as<uint8_t>(),
+                        lstat.as<int2>(), rstat.as<int2>(), win.as<float>(), wbase.as<int>(),
+                        flags.as<int>(), flag_count.as<unsigned>(), g, n, N, (long)H * g.SP,
+                        stream);
+      stats.kernel_launches += 2;
+      winp = win.as<float>();
+    }
+    defer.ensure(sizeof(Deferred) * N * n);
+    defer_count.ensure(sizeof(unsigned) * n);
+    auto repick = [&](const double* avgp, int2* chgp, unsigned* chgc) {
+      ck(cudaMemsetAsync(defer_count.p, 0, sizeof(unsigned) * n, stream), "memset");
+      launch_d_repick(psum.as<double>(), vm, cnt.as<int>(), avgp, so.as<int>(), d.as<double>(),
+                      o.as<double>(), gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), winp,
+                      wbase.as<int>(), chgp, chgc, defer.as<Deferred>(),
+                      defer_count.as<unsigned>(), a, n, N, N, ctr() + 1, stream);
+      launch_repick_exact(defer.as<Deferred>(), defer_count.as<unsigned>(), o.as<double>(),
+                          gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), chgp, chgc, a, n, N, N,
+                          ctr() + 1, stream);
+      stats.kernel_launches += 2;
+    };
     for (int it = 0; it < iters; ++it) {
       if (it == 0) {
         // o is the cleanup output (fractional fills): the reference's FP64 path.
@@ -446,11 +469,8 @@ struct ss_ctx {
                      avg.as<double>(), b.as<double>(), a, n, N, stream);
         launch_double_bt(b.as<double>(), vm, xbt.as<double>(), W, H, n, N, stream);
         launch_scan_bt_d(xbt.as<double>(), mT, psum.as<double>(), W, H, n, stream);
-        launch_d_repick(psum.as<double>(), vm, cnt.as<int>(), avg.as<double>(), nullptr,
-                        d.as<double>(), o.as<double>(), gray_l.as<uint8_t>(),
-                        gray_r.as<uint8_t>(), lstat.as<int2>(), volp, nullptr, nullptr, a, n, N,
-                        N, N, (long)g.NCP * N, ctr() + 1, stream);
-        stats.kernel_launches += 6;
+        stats.kernel_launches += 5;
+        repick(avg.as<double>(), nullptr, nullptr);
         if (iters > 1) {
           // o is integer-valued from here on: exact integer disc sums S_o.
           launch_int_bt(o.as<double>(), vm, xbt.as<int>(), W, H, n, N, stream);
@@ -463,12 +483,8 @@ struct ss_ctx {
         launch_b_bt(so.as<int>(), cnt.as<int>(), o.as<double>(), d.as<double>(), a.alpha,
                     a.one_minus_alpha, vm, xbt.as<double>(), W, H, n, N, stream);
         launch_scan_bt_d(xbt.as<double>(), mT, psum.as<double>(), W, H, n, stream);
-        launch_d_repick(psum.as<double>(), vm, cnt.as<int>(), nullptr, so.as<int>(),
-                        d.as<double>(), o.as<double>(), gray_l.as<uint8_t>(),
-                        gray_r.as<uint8_t>(), lstat.as<int2>(), volp, chg.as<int2>(),
-                        chg_count.as<unsigned>(), a, n, N, N, N, (long)g.NCP * N, ctr() + 1,
-                        stream);
-        stats.kernel_launches += 3;
+        stats.kernel_launches += 2;
+        repick(nullptr, chg.as<int2>(), chg_count.as<unsigned>());
         if (it + 1 < iters) {
           launch_so_update(chg.as<int2>(), chg_count.as<unsigned>(), vm, so.as<int>(), a, n, N,
                            stream);

@@ -25,6 +25,16 @@ namespace ssb {
 constexpr int kDB = 16;        // disparities per thread in the WTA sweep
 constexpr int kRefineR = 5;    // kRefineSearchRadius (params.hpp:38)
 constexpr double kZnccEps = 1e-3;  // kZnccCostEpsilon (params.hpp:34)
+constexpr int kWin = 16;           // candidate window per pixel for the refinement
+constexpr int kNoWin = -2147483647 - 1;  // INT_MIN: no window / no defined candidate
+
+// Window [base, base + kWin) around an anchor disparity, kept inside the
+// candidate range [cmin, cmin + NC).
+__host__ __device__ inline int window_base(int anchor, int cmin, int NC) {
+  const int hi = NC > kWin ? cmin + NC - kWin : cmin;
+  const int b = anchor - 7;
+  return b < cmin ? cmin : (b > hi ? hi : b);
+}
 
 struct Geom {
   int W, H;        // frame size
@@ -44,11 +54,21 @@ void launch_planes(const uint8_t* gray, uint8_t* plane, const Geom& g, int frame
                    long gray_stride, long plane_stride, cudaStream_t s);
 void launch_stats(const uint8_t* gray, int2* lstat, int2* rstat, int is_right, const Geom& g,
                   int frames, long gray_stride, long stat_stride, cudaStream_t s);
+// Sweep + WTA. Also writes, per interior pixel, the refinement's candidate
+// window: kWin scores s(c) = g(c) / sqrt(var_l) for c = wbase .. wbase+kWin-1,
+// wbase centred on the WTA pick, or on base_map[pixel] when base_map != NULL
+// (per-stage refine). wbase = kNoWin when var_l == 0 (no defined score).
 void launch_wta11(const uint8_t* lplane, const uint8_t* rplane, const int2* lstat,
-                  const int2* rstat, float* vol, float* disp, uint8_t* valid, int* flag_list,
-                  unsigned int* flag_count, const Geom& g, double min_zncc, int frames,
-                  long plane_stride, long lstat_stride, long rstat_stride, long vol_stride,
-                  long map_stride, int do_argmax, cudaStream_t s);
+                  const int2* rstat, float* win, int* wbase, const int* base_map, float* disp,
+                  uint8_t* valid, int* flag_list, unsigned int* flag_count, const Geom& g,
+                  double min_zncc, int frames, long plane_stride, long lstat_stride,
+                  long rstat_stride, long map_stride, int do_argmax, cudaStream_t s);
+// After cleanup: every valid pixel whose window is not centred on its
+// (possibly filled) disparity gets a freshly computed window.
+void launch_window_fix(const float* disp, const uint8_t* valid, const uint8_t* lgray,
+                       const uint8_t* rgray, const int2* lstat, const int2* rstat, float* win,
+                       int* wbase, int* list, unsigned* count, const Geom& g, int frames,
+                       long stride, long rstat_stride, cudaStream_t s);
 void launch_wta_resolve(const uint8_t* lgray, const uint8_t* rgray, const int* flag_list,
                         const unsigned int* flag_count, float* disp, uint8_t* valid,
                         const Geom& g, double min_zncc, int frames, long gray_stride,
@@ -110,12 +130,22 @@ void launch_avg_b(const double* psumT, const uint8_t* valid, const int* cnt, con
                   long stride, cudaStream_t s);
 // avg: the double disc mean of o (iteration 0) or nullptr to use the exact
 // integer disc sum `so` (iterations >= 1); o changes are appended to chg.
+// Re-picks whose FP32 window filter is ambiguous, or whose candidates leave
+// the window, are deferred to launch_repick_exact (warp per pixel, FP64).
+struct Deferred {
+  int pix, c_lo, mask, pad;  // mask: candidates c_lo + k to score exactly
+  double d;
+};
 void launch_d_repick(const double* psumT, const uint8_t* valid, const int* cnt,
                      const double* avg, const int* so, double* d, double* o,
-                     const uint8_t* lgray, const uint8_t* rgray, const int2* lstat,
-                     const float* vol, int2* chg, unsigned* chg_count, const RefineArgs& a,
-                     int frames, long stride, long gray_stride, long lstat_stride,
-                     long vol_stride, unsigned long long* counters, cudaStream_t s);
+                     const uint8_t* lgray, const uint8_t* rgray, const float* win,
+                     const int* wbase, int2* chg, unsigned* chg_count, Deferred* defer,
+                     unsigned* defer_count, const RefineArgs& a, int frames, long stride,
+                     long gray_stride, unsigned long long* counters, cudaStream_t s);
+void launch_repick_exact(const Deferred* defer, const unsigned* defer_count, double* o,
+                         const uint8_t* lgray, const uint8_t* rgray, int2* chg,
+                         unsigned* chg_count, const RefineArgs& a, int frames, long stride,
+                         long gray_stride, unsigned long long* counters, cudaStream_t s);
 // S_o += delta over the disc of every changed pixel (exact integers).
 void launch_so_update(const int2* chg, const unsigned* chg_count, const uint8_t* valid,
                       int* so, const RefineArgs& a, int frames, long stride, cudaStream_t s);
