@@ -264,19 +264,25 @@ __device__ __forceinline__ double exact_cost(const uint8_t* L, const uint8_t* R,
 constexpr int kMaxCand = 2 * kRefineR + 1;
 
 // Re-pick of one pixel (smoothing.cpp:119-144) given its smoothed d.
-// Returns the new o, or INT_MIN when the pixel is deferred to the exact kernel
-// (or has no candidate at all).
+// Returns the new o, or INT_MIN when the pixel is deferred to the exact kernel.
+//
+// Filter error budget: window scores are fp16 copies of
+// the FP32 sweep score s_f (|s_f - s| <= 5 ulp_f32), so |s16 - s| <= 2^-11 |s|
+// + 3e-8; M = 1/max(s, 1e-3) then carries <= 5.3e-4 relative error and the
+// float cost M + (eta diff) diff <= 5.4e-4. Candidates within 2.5e-3 of the
+// float minimum are re-scored exactly; a single survivor is provably the
+// reference's argmin.
 __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double dv,
-                                      const uint8_t* L, const uint8_t* R, const float* win_f,
-                                      const int* wbase_f, long pix, Deferred* defer,
-                                      unsigned* defer_count) {
+                                      const uint8_t* L, const uint8_t* R,
+                                      const wscore_t* win_row, int wb, long pix,
+                                      Deferred* defer, unsigned* defer_count) {
   const int W = a.g.W, H = a.g.H, half = a.g.half;
   const int c_lo = max((int)ceil(__dsub_rn(dv, (double)kRefineR)), (int)ceil(a.lo));
   const int c_hi = min((int)floor(__dadd_rn(dv, (double)kRefineR)), (int)floor(a.hi));
   if (c_lo > c_hi) return INT_MIN;  // unreachable for a clamped d; mirrors `found`
   const bool fits = u >= half && u < W - half && v >= half && v < H - half;
 
-  if (win_f == nullptr) {
+  if (win_row == nullptr) {
     // Generic window size: every candidate in exact FP64 (no score windows).
     double best_cost = 0.0;
     int best = c_lo;
@@ -289,9 +295,7 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
     }
     return best;
   }
-
-  const int wb = fits ? wbase_f[pix] : kNoWin;
-  if (wb == kNoWin) {
+  if (!fits || wb == kNoWin) {
     // Window does not fit or var_l == 0: every match cost is exactly
     // 1/kZnccCostEpsilon, so the reference's double costs are computed as is.
     const double m = __ddiv_rn(1.0, kZnccEps);
@@ -312,7 +316,7 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
   if (c_lo < wb || c_hi > wb + kWin - 1) {
     mask = (1 << (c_hi - c_lo + 1)) - 1;  // window miss: score every candidate exactly
   } else {
-    const float* wp = win_f + pix * kWin - wb;  // wp[c]: score of candidate c
+    const wscore_t* wp = win_row - wb;  // wp[c]: score of candidate c
     float cf[kMaxCand];
     float best_f = INFINITY;
 #pragma unroll
@@ -323,7 +327,7 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
         const int ru = u - c;
         float m = 1000.f;  // 1 / kZnccCostEpsilon, exact
         if (ru >= half && ru < W - half) {
-          const float sc = __ldg(wp + c);
+          const float sc = __half2float(wp[c]);
           if (!isnan(sc)) m = 1.f / fmaxf(sc, 1e-3f);
         }
         const float df = (float)__dsub_rn((double)c, dv);
@@ -334,9 +338,7 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
         }
       }
     }
-    // Any candidate whose exact cost could undercut the float minimum
-    // (|cost_f - cost| <= 7 ulp = 4.2e-7 relative; margin 4e-6).
-    const float thr = best_f * (1.0f + 4e-6f);
+    const float thr = best_f * (1.0f + 2.5e-3f);
 #pragma unroll
     for (int k = 0; k < kMaxCand; ++k)
       if (cf[k] <= thr) mask |= 1 << k;
@@ -356,53 +358,75 @@ template <int RF, bool USE_SO>
 __global__ void __launch_bounds__(kTX * kBY)
     k_d_repick(const double* __restrict__ psumT, const uint8_t* __restrict__ valid,
                const int* __restrict__ cnt, const double* __restrict__ avg,
-               const int* __restrict__ so, double* __restrict__ d, double* __restrict__ o,
+               const int* __restrict__ so, double* __restrict__ d, int* __restrict__ o,
                const uint8_t* __restrict__ lgray, const uint8_t* __restrict__ rgray,
-               const float* __restrict__ win, const int* __restrict__ wbase,
+               const wscore_t* __restrict__ win, const int* __restrict__ wbase,
                int2* __restrict__ chg, unsigned* __restrict__ chg_count,
                Deferred* __restrict__ defer, unsigned* __restrict__ defer_count, RefineArgs a,
                long stride, long gray_stride) {
+  constexpr int NR = kTY / kBY;  // pixels per thread
   const long f = blockIdx.z;
   const int W = a.g.W, H = a.g.H, R = a.radius;
+  const int u = blockIdx.x * kTX + threadIdx.x;
+  // Issue this thread's per-pixel loads before the tile barrier so their
+  // HBM latency overlaps the shared-memory staging.
+  bool act[NR];
+  int cn[NR], sv[NR], ol[NR], wb[NR];
+  double av[NR];
+#pragma unroll
+  for (int rr = 0; rr < NR; ++rr) {
+    const int v = blockIdx.y * kTY + threadIdx.y + rr * kBY;
+    const long i = f * stride + (long)v * W + u;
+    act[rr] = u < W && v < H && valid[i];
+    cn[rr] = sv[rr] = ol[rr] = 0;
+    wb[rr] = kNoWin;
+    av[rr] = 0.0;
+    if (act[rr]) {
+      cn[rr] = __ldg(cnt + i);
+      if (USE_SO) {
+        sv[rr] = __ldg(so + i);
+        ol[rr] = o[i];
+      } else {
+        av[rr] = __ldg(avg + i);
+      }
+      if (win) {
+        wb[rr] = __ldg(wbase + i);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(win + i * kWin));
+      }
+    }
+  }
   int* span;
   const PsumTile<double> T = load_tile(psumT + f * bt_frame(W, H, 1), W, H, R, a.span, span);
-  const int u = blockIdx.x * kTX + threadIdx.x;
   const uint8_t* L = lgray + f * gray_stride;
   const uint8_t* Rg = rgray + f * gray_stride;
-  const float* wf = win ? win + f * stride * kWin : nullptr;
-  const int* wbf = wbase + f * stride;
 #pragma unroll 1
-  for (int rr = 0; rr < kTY / kBY; ++rr) {
+  for (int rr = 0; rr < NR; ++rr) {
+    if (!act[rr]) continue;
     const int v = blockIdx.y * kTY + threadIdx.y + rr * kBY;
-    if (u >= W || v >= H) continue;
     const long pix = (long)v * W + u;
     const long i = f * stride + pix;
-    if (!valid[i]) continue;
     const double s = disc_sum_any<RF>(T, span, W, H, u, v, R);
-    const double c = (double)cnt[i];
+    const double c = (double)cn[rr];
     const double bav = __ddiv_rn(s, c);
     // avg = s_o / c: with integer o the reference's double disc sum is exact,
     // so the integer sum reproduces it bit for bit.
-    const double av = USE_SO ? __ddiv_rn((double)so[i], c) : avg[i];
-    const double x = __dsub_rn(av, bav);
+    const double a_o = USE_SO ? __ddiv_rn((double)sv[rr], c) : av[rr];
+    const double x = __dsub_rn(a_o, bav);
     const double dv = x < a.lo ? a.lo : (a.hi < x ? a.hi : x);  // std::clamp
     d[i] = dv;
-    const int best = repick(a, u, v, dv, L, Rg, wf, wbf, pix, defer + f * stride,
-                            defer_count + f);
+    const int best = repick(a, u, v, dv, L, Rg, win ? win + i * kWin : nullptr, wb[rr], pix,
+                            defer + f * stride, defer_count + f);
     if (best != INT_MIN) {
-      if (USE_SO) {
-        const int old = (int)o[i];
-        if (best != old)
-          chg[f * stride + atomicAdd(chg_count + f, 1u)] = make_int2((int)pix, best - old);
-      }
+      if (USE_SO && best != ol[rr])
+        chg[f * stride + atomicAdd(chg_count + f, 1u)] = make_int2((int)pix, best - ol[rr]);
       o[i] = best;
     }
   }
 }
 
 void launch_d_repick(const double* psumT, const uint8_t* valid, const int* cnt,
-                     const double* avg, const int* so, double* d, double* o,
-                     const uint8_t* lgray, const uint8_t* rgray, const float* win,
+                     const double* avg, const int* so, double* d, int* o,
+                     const uint8_t* lgray, const uint8_t* rgray, const wscore_t* win,
                      const int* wbase, int2* chg, unsigned* chg_count, Deferred* defer,
                      unsigned* defer_count, const RefineArgs& a, int frames, long stride,
                      long gray_stride, unsigned long long* counters, cudaStream_t s) {
@@ -436,7 +460,7 @@ void launch_d_repick(const double* psumT, const uint8_t* valid, const int* cnt,
 // exact FP64 (zncc_exact, reference cost formula); the warp takes the first
 // minimum (smallest candidate among equal costs), as smoothing.cpp:138 does.
 __global__ void k_repick_exact(const Deferred* __restrict__ defer,
-                               const unsigned* __restrict__ defer_count, double* __restrict__ o,
+                               const unsigned* __restrict__ defer_count, int* __restrict__ o,
                                const uint8_t* __restrict__ lgray,
                                const uint8_t* __restrict__ rgray, int2* __restrict__ chg,
                                unsigned* __restrict__ chg_count, RefineArgs a, long stride,
@@ -453,10 +477,10 @@ __global__ void k_repick_exact(const Deferred* __restrict__ defer,
     const Deferred e = defer[f * stride + t];
     const int u = e.pix % W, v = e.pix / W;
     const bool fits = u >= half && u < W - half && v >= half && v < H - half;
+    const bool mine = lane < kMaxCand && ((e.mask >> lane) & 1);
     double cost = INFINITY;
-    if (lane < kMaxCand && ((e.mask >> lane) & 1))
-      cost = exact_cost(L, R, W, u, v, e.c_lo + lane, fits, half, e.d, a.eta);
-    int k = (lane < kMaxCand && ((e.mask >> lane) & 1)) ? lane : 64;
+    if (mine) cost = exact_cost(L, R, W, u, v, e.c_lo + lane, fits, half, e.d, a.eta);
+    int k = mine ? lane : 64;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       const double oc = __shfl_down_sync(0xffffffffu, cost, off);
@@ -470,7 +494,7 @@ __global__ void k_repick_exact(const Deferred* __restrict__ defer,
       const int best = e.c_lo + k;
       const long i = f * stride + e.pix;
       if (chg) {
-        const int old = (int)o[i];
+        const int old = o[i];
         if (best != old) chg[f * stride + atomicAdd(chg_count + f, 1u)] = make_int2(e.pix, best - old);
       }
       o[i] = best;
@@ -478,13 +502,28 @@ __global__ void k_repick_exact(const Deferred* __restrict__ defer,
   }
 }
 
-void launch_repick_exact(const Deferred* defer, const unsigned* defer_count, double* o,
+void launch_repick_exact(const Deferred* defer, const unsigned* defer_count, int* o,
                          const uint8_t* lgray, const uint8_t* rgray, int2* chg,
                          unsigned* chg_count, const RefineArgs& a, int frames, long stride,
                          long gray_stride, unsigned long long* counters, cudaStream_t s) {
   if (frames <= 0) return;
   k_repick_exact<<<dim3(64, frames), 256, 0, s>>>(defer, defer_count, o, lgray, rgray, chg,
                                                   chg_count, a, stride, gray_stride, counters);
+}
+
+__global__ void k_int_to_double(const int* __restrict__ x, const uint8_t* __restrict__ valid,
+                                double* __restrict__ y, long n) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
+       i += (long)gridDim.x * blockDim.x)
+    if (valid[i]) y[i] = (double)x[i];
+}
+
+void launch_int_to_double(const int* x, const uint8_t* valid, double* y, long n,
+                          cudaStream_t s) {
+  if (n <= 0) return;
+  long blocks = (n + 255) / 256;
+  if (blocks > 2048) blocks = 2048;
+  k_int_to_double<<<(unsigned)blocks, 256, 0, s>>>(x, valid, y, n);
 }
 
 // One warp per changed pixel j: S_o(i) += delta_j for every valid i whose disc

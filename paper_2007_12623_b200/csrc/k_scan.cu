@@ -152,19 +152,19 @@ struct SrcDouble {  // a masked double field
   const double* val;
   __device__ double operator()(long i) const { return __ldg(val + i); }
 };
-struct SrcIntOf {  // an integer-valued double field as int (exact)
-  const double* val;
-  __device__ int operator()(long i) const { return (int)__ldg(val + i); }
+struct SrcInt {  // an int field (the integer disparities o)
+  const int* val;
+  __device__ int operator()(long i) const { return __ldg(val + i); }
 };
 struct SrcB {  // correction b (smoothing.cpp:96-97) from the exact integer disc sum of o
   const int* so;
   const int* cnt;
-  const double* o;
+  const int* o;
   const double* d;
   double alpha, one_minus_alpha;
   __device__ double operator()(long i) const {
     const double avg = __ddiv_rn((double)__ldg(so + i), (double)__ldg(cnt + i));
-    return __dsub_rn(__dsub_rn(avg, __dmul_rn(alpha, __ldg(o + i))),
+    return __dsub_rn(__dsub_rn(avg, __dmul_rn(alpha, (double)__ldg(o + i))),
                      __dmul_rn(one_minus_alpha, __ldg(d + i)));
   }
 };
@@ -216,11 +216,11 @@ void launch_double_bt(const double* val, const uint8_t* mask, double* outT, int 
                       int frames, long stride, cudaStream_t s) {
   launch_to_bt<double>(SrcDouble{val}, mask, outT, W, H, frames, stride, s);
 }
-void launch_int_bt(const double* val, const uint8_t* mask, int* outT, int W, int H, int frames,
+void launch_int_bt(const int* val, const uint8_t* mask, int* outT, int W, int H, int frames,
                    long stride, cudaStream_t s) {
-  launch_to_bt<int>(SrcIntOf{val}, mask, outT, W, H, frames, stride, s);
+  launch_to_bt<int>(SrcInt{val}, mask, outT, W, H, frames, stride, s);
 }
-void launch_b_bt(const int* so, const int* cnt, const double* o, const double* d, double alpha,
+void launch_b_bt(const int* so, const int* cnt, const int* o, const double* d, double alpha,
                  double one_minus_alpha, const uint8_t* mask, double* bT, int W, int H,
                  int frames, long stride, cudaStream_t s) {
   launch_to_bt<double>(SrcB{so, cnt, o, d, alpha, one_minus_alpha}, mask, bT, W, H, frames,

@@ -119,7 +119,7 @@ __device__ __forceinline__ void row_terms(const ThreadGeom& tg, int y, uint32_t 
 
 __global__ void __launch_bounds__(512) k_wta11(
     const uint8_t* __restrict__ lplane, const uint8_t* __restrict__ rplane,
-    const int2* __restrict__ lstat, const int2* __restrict__ rstat, float* __restrict__ win,
+    const int2* __restrict__ lstat, const int2* __restrict__ rstat, wscore_t* __restrict__ win,
     int* __restrict__ wbase, const int* __restrict__ base_map, float* __restrict__ disp,
     uint8_t* __restrict__ valid, int* __restrict__ flag_list,
     unsigned int* __restrict__ flag_count, Geom g, int TH, float min_zncc_f, float thr_tol,
@@ -282,16 +282,17 @@ __global__ void __launch_bounds__(512) k_wta11(
           wbase[idx] = wb;
           if (wb != kNoWin) {
             const float* gr = s_g + r * NCB * 32 + lane;
-            float w[kWin];
+            uint32_t w[kWin / 2];  // kWin fp16 scores, 32 B: one sector per pixel
 #pragma unroll
-            for (int q = 0; q < kWin; ++q) {
-              const int ci = wb - g.cmin + q;
-              w[q] = ci < g.NC ? gr[ci * 32] * rl : __int_as_float(0x7fc00000);
+            for (int q = 0; q < kWin / 2; ++q) {
+              const int ci = wb - g.cmin + 2 * q;
+              const float s0 = ci < g.NC ? gr[ci * 32] * rl : __int_as_float(0x7fc00000);
+              const float s1 = ci + 1 < g.NC ? gr[(ci + 1) * 32] * rl : __int_as_float(0x7fc00000);
+              w[q] = pack_score2(s0, s1);
             }
-            float4* wp = reinterpret_cast<float4*>(win + idx * kWin);
-#pragma unroll
-            for (int q = 0; q < kWin / 4; ++q)
-              wp[q] = make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+            uint4* wp = reinterpret_cast<uint4*>(win + idx * kWin);
+            wp[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            wp[1] = make_uint4(w[4], w[5], w[6], w[7]);
           }
         }
       }
@@ -301,7 +302,7 @@ __global__ void __launch_bounds__(512) k_wta11(
 }
 
 void launch_wta11(const uint8_t* lplane, const uint8_t* rplane, const int2* lstat,
-                  const int2* rstat, float* win, int* wbase, const int* base_map, float* disp,
+                  const int2* rstat, wscore_t* win, int* wbase, const int* base_map, float* disp,
                   uint8_t* valid, int* flag_list, unsigned int* flag_count, const Geom& g,
                   double min_zncc, int frames, long plane_stride, long lstat_stride,
                   long rstat_stride, long map_stride, int do_argmax, cudaStream_t s) {
@@ -445,7 +446,7 @@ __global__ void k_window_check(const float* __restrict__ disp, const uint8_t* __
 // so the window is bit-identical to one the sweep would have written.
 __global__ void k_window_build(const float* __restrict__ disp, const uint8_t* __restrict__ lgray,
                                const uint8_t* __restrict__ rgray, const int2* __restrict__ lstat,
-                               const int2* __restrict__ rstat, float* __restrict__ win,
+                               const int2* __restrict__ rstat, wscore_t* __restrict__ win,
                                int* __restrict__ wbase, const int* __restrict__ list,
                                const unsigned* __restrict__ count, Geom g, long stride,
                                long rstat_stride) {
@@ -476,13 +477,13 @@ __global__ void k_window_build(const float* __restrict__ disp, const uint8_t* __
       const int num = 61 * slr - ls.x * rs.x;
       s = (__int2float_rn(num) * __int_as_float(rs.y)) * __int_as_float(ls.y);
     }
-    win[i * kWin + q] = s;
+    win[i * kWin + q] = __float2half_rn(s);
     if (q == 0) wbase[i] = wb;
   }
 }
 
 void launch_window_fix(const float* disp, const uint8_t* valid, const uint8_t* lgray,
-                       const uint8_t* rgray, const int2* lstat, const int2* rstat, float* win,
+                       const uint8_t* rgray, const int2* lstat, const int2* rstat, wscore_t* win,
                        int* wbase, int* list, unsigned* count, const Geom& g, int frames,
                        long stride, long rstat_stride, cudaStream_t s) {
   if (g.W <= 0 || g.H <= 0 || frames <= 0) return;

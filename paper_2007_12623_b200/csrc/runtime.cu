@@ -162,7 +162,7 @@ struct ss_ctx {
 
   DevBuf in_l, in_r, gray_l, gray_r, plane_l, plane_r, lstat, rstat, win, wbase;
   DevBuf disp_a, disp_b, valid_a, valid_b, flags, flag_count;
-  DevBuf o, d, avg, b, psum, pcnt, cnt, span, wtab, fspan;
+  DevBuf o, oi, d, avg, b, psum, pcnt, cnt, span, wtab, fspan;
   DevBuf index, block_sums, npoints, pts_f, nrm_f, colors, pts_d, nrm_d, pixels, pts4;
   DevBuf counters, trace_o, trace_d, so, chg, chg_count, xbt, mbt, defer, defer_count;
   int wtab_radius = -1;
@@ -189,7 +189,7 @@ struct ss_ctx {
     for (DevBuf* b : {&in_l, &in_r, &gray_l, &gray_r, &plane_l, &plane_r, &lstat, &rstat, &win, &wbase,
                       &disp_a, &disp_b, &valid_a, &valid_b, &flags, &flag_count, &o, &d, &avg,
                       &b, &psum, &pcnt, &cnt, &span, &wtab, &fspan, &index, &block_sums, &npoints,
-                      &pts_f, &nrm_f, &colors, &pts_d, &nrm_d, &pixels, &pts4, &counters, &trace_o,
+                      &pts_f, &nrm_f, &colors, &pts_d, &nrm_d, &pixels, &pts4, &counters, &oi, &trace_o,
                       &trace_d, &so, &chg, &chg_count, &xbt, &mbt, &defer, &defer_count})
       b->release();
     for (auto& r : pending) {
@@ -283,7 +283,7 @@ struct ss_ctx {
     plane_r.ensure(plane_stride * n);
     lstat.ensure(sizeof(int2) * N * n);
     rstat.ensure(sizeof(int2) * rstride * n);
-    win.ensure(sizeof(float) * kWin * N * n);
+    win.ensure(sizeof(wscore_t) * kWin * N * n);
     wbase.ensure(sizeof(int) * N * n);
     flags.ensure(sizeof(int) * N * n);
     flag_count.ensure(sizeof(unsigned) * n);
@@ -302,7 +302,7 @@ struct ss_ctx {
     }
     Stage st(this, 2);
     launch_wta11(plane_l.as<uint8_t>(), plane_r.as<uint8_t>(), lstat.as<int2>(), rstat.as<int2>(),
-                 win.as<float>(), wbase.as<int>(), nullptr, disp_a.as<float>(),
+                 win.as<wscore_t>(), wbase.as<int>(), nullptr, disp_a.as<float>(),
                  valid_a.as<uint8_t>(), flags.as<int>(), flag_count.as<unsigned>(), g,
                  params.min_zncc, n, plane_stride, N, rstride, N, do_argmax ? 1 : 0, stream);
     stats.kernel_launches += 1;
@@ -421,10 +421,16 @@ struct ss_ctx {
     a.radius = r;
     a.span = span.as<int>();
     const int iters = params.refine_iterations;
+    if (iters > 0 && a.lo > a.hi)
+      raise(SS_EINVAL, "refine_disparities: d_min - 5 > d_max + 5 (empty candidate range)");
     if (h_trace_o || h_trace_d) {
       trace_o.ensure(sizeof(double) * N * std::max(iters, 1));
       trace_d.ensure(sizeof(double) * N * std::max(iters, 1));
+      // RefineTrace rows hold 0 at invalid pixels (smoothing.cpp:77-80)
+      ck(cudaMemsetAsync(trace_o.p, 0, sizeof(double) * N * std::max(iters, 1), stream), "memset");
     }
+    oi.ensure(sizeof(int) * N * n);
+    int* op = oi.as<int>();
     const uint8_t* vm = valid_a.as<uint8_t>();
     uint8_t* mT = mbt.as<uint8_t>();
     launch_refine_init(disp_a.as<float>(), vm, o.as<double>(), d.as<double>(), W, H, n, N,
@@ -438,24 +444,24 @@ struct ss_ctx {
     chg.ensure(sizeof(int2) * N * n);
     chg_count.ensure(sizeof(unsigned) * n);
     // Score windows: re-centre the sweep's windows on the cleanup output.
-    const float* winp = nullptr;
+    const wscore_t* winp = nullptr;
     if (have_windows && iters > 0) {
       launch_window_fix(disp_a.as<float>(), vm, gray_l.as<uint8_t>(), gray_r.as<uint8_t>(),
-                        lstat.as<int2>(), rstat.as<int2>(), win.as<float>(), wbase.as<int>(),
+                        lstat.as<int2>(), rstat.as<int2>(), win.as<wscore_t>(), wbase.as<int>(),
                         flags.as<int>(), flag_count.as<unsigned>(), g, n, N, (long)H * g.SP,
                         stream);
       stats.kernel_launches += 2;
-      winp = win.as<float>();
+      winp = win.as<wscore_t>();
     }
     defer.ensure(sizeof(Deferred) * N * n);
     defer_count.ensure(sizeof(unsigned) * n);
     auto repick = [&](const double* avgp, int2* chgp, unsigned* chgc) {
       ck(cudaMemsetAsync(defer_count.p, 0, sizeof(unsigned) * n, stream), "memset");
       launch_d_repick(psum.as<double>(), vm, cnt.as<int>(), avgp, so.as<int>(), d.as<double>(),
-                      o.as<double>(), gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), winp,
-                      wbase.as<int>(), chgp, chgc, defer.as<Deferred>(),
-                      defer_count.as<unsigned>(), a, n, N, N, ctr() + 1, stream);
-      launch_repick_exact(defer.as<Deferred>(), defer_count.as<unsigned>(), o.as<double>(),
+                      op, gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), winp, wbase.as<int>(),
+                      chgp, chgc, defer.as<Deferred>(), defer_count.as<unsigned>(), a, n, N, N,
+                      ctr() + 1, stream);
+      launch_repick_exact(defer.as<Deferred>(), defer_count.as<unsigned>(), op,
                           gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), chgp, chgc, a, n, N, N,
                           ctr() + 1, stream);
       stats.kernel_launches += 2;
@@ -473,14 +479,14 @@ struct ss_ctx {
         repick(avg.as<double>(), nullptr, nullptr);
         if (iters > 1) {
           // o is integer-valued from here on: exact integer disc sums S_o.
-          launch_int_bt(o.as<double>(), vm, xbt.as<int>(), W, H, n, N, stream);
+          launch_int_bt(op, vm, xbt.as<int>(), W, H, n, N, stream);
           launch_scan_bt_i(xbt.as<int>(), mT, pcnt.as<int>(), W, H, n, stream);
           launch_disc_isum(vm, pcnt.as<int>(), so.as<int>(), a, n, N, stream);
           stats.kernel_launches += 3;
         }
       } else {
         ck(cudaMemsetAsync(chg_count.p, 0, sizeof(unsigned) * n, stream), "memset");
-        launch_b_bt(so.as<int>(), cnt.as<int>(), o.as<double>(), d.as<double>(), a.alpha,
+        launch_b_bt(so.as<int>(), cnt.as<int>(), op, d.as<double>(), a.alpha,
                     a.one_minus_alpha, vm, xbt.as<double>(), W, H, n, N, stream);
         launch_scan_bt_d(xbt.as<double>(), mT, psum.as<double>(), W, H, n, stream);
         stats.kernel_launches += 2;
@@ -491,9 +497,7 @@ struct ss_ctx {
           stats.kernel_launches += 1;
         }
       }
-      if (h_trace_o)
-        ck(cudaMemcpyAsync(trace_o.as<double>() + (long)it * N, o.p, sizeof(double) * N,
-                           cudaMemcpyDeviceToDevice, stream), "trace");
+      if (h_trace_o) launch_int_to_double(op, vm, trace_o.as<double>() + (long)it * N, N, stream);
       if (h_trace_d)
         ck(cudaMemcpyAsync(trace_d.as<double>() + (long)it * N, d.p, sizeof(double) * N,
                            cudaMemcpyDeviceToDevice, stream), "trace");

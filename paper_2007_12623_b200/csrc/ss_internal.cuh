@@ -9,14 +9,14 @@
 //   lstat[N]                 int2 {chessboard sum, float bits of 1/sqrt(var)}
 //   rstat[H][SP]             int2 same for the right image, SPAD padded
 //                                columns each side hold {0, NaN}
-//   vol[H][W][NCP]           f32 g(c) = num(c) / sqrt(var_r) for c in
-//                                [d_min-5, d_max+5] (the refine range),
-//                                pixel-major so a re-pick reads 11 adjacent
-//                                floats instead of 11 scattered planes
+//   win[N][kWin]             f16 s(c) = num(c) / sqrt(var_l var_r) for the
+//                                16 candidates c = wbase[N] + q around the
+//                                pixel's disparity (refinement re-pick input)
 //   disp/valid               f32/u8 DisparityMap (image.hpp:46-67)
 //   refine state             f64 o, d, avg, b; psum[H][W+1]; cnt[N] (int)
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -26,6 +26,13 @@ constexpr int kDB = 16;        // disparities per thread in the WTA sweep
 constexpr int kRefineR = 5;    // kRefineSearchRadius (params.hpp:38)
 constexpr double kZnccEps = 1e-3;  // kZnccCostEpsilon (params.hpp:34)
 constexpr int kWin = 16;           // candidate window per pixel for the refinement
+// Window scores are stored as fp16 (32 B per pixel, one sector): the re-pick
+// filter's error budget covers it (|cost_f - cost| <= 5.4e-4 rel).
+typedef __half wscore_t;
+__device__ __forceinline__ uint32_t pack_score2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
 constexpr int kNoWin = -2147483647 - 1;  // INT_MIN: no window / no defined candidate
 
 // Window [base, base + kWin) around an anchor disparity, kept inside the
@@ -59,14 +66,14 @@ void launch_stats(const uint8_t* gray, int2* lstat, int2* rstat, int is_right, c
 // wbase centred on the WTA pick, or on base_map[pixel] when base_map != NULL
 // (per-stage refine). wbase = kNoWin when var_l == 0 (no defined score).
 void launch_wta11(const uint8_t* lplane, const uint8_t* rplane, const int2* lstat,
-                  const int2* rstat, float* win, int* wbase, const int* base_map, float* disp,
+                  const int2* rstat, wscore_t* win, int* wbase, const int* base_map, float* disp,
                   uint8_t* valid, int* flag_list, unsigned int* flag_count, const Geom& g,
                   double min_zncc, int frames, long plane_stride, long lstat_stride,
                   long rstat_stride, long map_stride, int do_argmax, cudaStream_t s);
 // After cleanup: every valid pixel whose window is not centred on its
 // (possibly filled) disparity gets a freshly computed window.
 void launch_window_fix(const float* disp, const uint8_t* valid, const uint8_t* lgray,
-                       const uint8_t* rgray, const int2* lstat, const int2* rstat, float* win,
+                       const uint8_t* rgray, const int2* lstat, const int2* rstat, wscore_t* win,
                        int* wbase, int* list, unsigned* count, const Geom& g, int frames,
                        long stride, long rstat_stride, cudaStream_t s);
 void launch_wta_resolve(const uint8_t* lgray, const uint8_t* rgray, const int* flag_list,
@@ -111,9 +118,9 @@ void launch_ones_bt(const uint8_t* mask, int* outT, int W, int H, int frames, lo
                     cudaStream_t s);
 void launch_double_bt(const double* val, const uint8_t* mask, double* outT, int W, int H,
                       int frames, long stride, cudaStream_t s);
-void launch_int_bt(const double* val, const uint8_t* mask, int* outT, int W, int H, int frames,
+void launch_int_bt(const int* val, const uint8_t* mask, int* outT, int W, int H, int frames,
                    long stride, cudaStream_t s);
-void launch_b_bt(const int* so, const int* cnt, const double* o, const double* d, double alpha,
+void launch_b_bt(const int* so, const int* cnt, const int* o, const double* d, double alpha,
                  double one_minus_alpha, const uint8_t* mask, double* bT, int W, int H,
                  int frames, long stride, cudaStream_t s);
 // masked serial row prefix (psum[.][0] = 0, W + 1 columns, BT layout)
@@ -136,13 +143,15 @@ struct Deferred {
   int pix, c_lo, mask, pad;  // mask: candidates c_lo + k to score exactly
   double d;
 };
+// o: integer disparities (written by every re-pick; read for the change list
+// when avg == nullptr, i.e. iterations >= 1).
 void launch_d_repick(const double* psumT, const uint8_t* valid, const int* cnt,
-                     const double* avg, const int* so, double* d, double* o,
-                     const uint8_t* lgray, const uint8_t* rgray, const float* win,
+                     const double* avg, const int* so, double* d, int* o,
+                     const uint8_t* lgray, const uint8_t* rgray, const wscore_t* win,
                      const int* wbase, int2* chg, unsigned* chg_count, Deferred* defer,
                      unsigned* defer_count, const RefineArgs& a, int frames, long stride,
                      long gray_stride, unsigned long long* counters, cudaStream_t s);
-void launch_repick_exact(const Deferred* defer, const unsigned* defer_count, double* o,
+void launch_repick_exact(const Deferred* defer, const unsigned* defer_count, int* o,
                          const uint8_t* lgray, const uint8_t* rgray, int2* chg,
                          unsigned* chg_count, const RefineArgs& a, int frames, long stride,
                          long gray_stride, unsigned long long* counters, cudaStream_t s);
@@ -151,6 +160,8 @@ void launch_so_update(const int2* chg, const unsigned* chg_count, const uint8_t*
                       int* so, const RefineArgs& a, int frames, long stride, cudaStream_t s);
 void launch_refine_out(const double* d, const uint8_t* valid, const float* din, float* dout,
                        int W, int H, int frames, long stride, cudaStream_t s);
+void launch_int_to_double(const int* x, const uint8_t* valid, double* y, long n,
+                          cudaStream_t s);
 
 struct CloudArgs {
   double fx, fy, cx, cy, baseline;
