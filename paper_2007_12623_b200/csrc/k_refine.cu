@@ -316,33 +316,51 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
   if (c_lo < wb || c_hi > wb + kWin - 1) {
     mask = (1 << (c_hi - c_lo + 1)) - 1;  // window miss: score every candidate exactly
   } else {
+    // cost(c) = M(c) + E(c). E = (eta diff) diff is computed exactly as the
+    // reference does (FP64); M = 1/max(s, 1e-3) is exact (1000) when the score
+    // is undefined or certainly below 1e-3, else derived from the fp16 score
+    // with relative error <= kErrM. Only candidates whose error bars overlap
+    // the minimum's are re-scored exactly.
+    constexpr double kErrM = 6e-4;  // fp16 score (2^-11) + FP32 sweep (5 ulp) + 1/x
     const wscore_t* wp = win_row - wb;  // wp[c]: score of candidate c
-    float cf[kMaxCand];
-    float best_f = INFINITY;
+    double cost[kMaxCand];
+    float err[kMaxCand];
+    double upper = INFINITY, best_cost = INFINITY;
 #pragma unroll
     for (int k = 0; k < kMaxCand; ++k) {
       const int c = c_lo + k;
-      cf[k] = INFINITY;
+      cost[k] = INFINITY;
+      err[k] = 0.f;
       if (c <= c_hi) {
         const int ru = u - c;
-        float m = 1000.f;  // 1 / kZnccCostEpsilon, exact
+        double m = 1000.0;  // 1 / kZnccCostEpsilon, exact
         if (ru >= half && ru < W - half) {
           const float sc = __half2float(wp[c]);
-          if (!isnan(sc)) m = 1.f / fmaxf(sc, 1e-3f);
+          if (!isnan(sc) && sc >= 0.99e-3f) {
+            const float mf = 1.f / fmaxf(sc, 1e-3f);
+            m = (double)mf;
+            err[k] = (float)(kErrM * mf);
+          }
         }
-        const float df = (float)__dsub_rn((double)c, dv);
-        cf[k] = m + a.eta_f * df * df;
-        if (cf[k] < best_f) {
-          best_f = cf[k];
+        const double diff = __dsub_rn((double)c, dv);
+        cost[k] = __dadd_rn(m, __dmul_rn(__dmul_rn(a.eta, diff), diff));
+        if (cost[k] < best_cost) {  // first minimum of the (approximate) costs
+          best_cost = cost[k];
           best = c;
         }
+        upper = fmin(upper, cost[k] + (double)err[k]);
       }
     }
-    const float thr = best_f * (1.0f + 2.5e-3f);
+    int approx = 0;
 #pragma unroll
     for (int k = 0; k < kMaxCand; ++k)
-      if (cf[k] <= thr) mask |= 1 << k;
-    if (__popc(mask) == 1) return best;
+      if (cost[k] - (double)err[k] <= upper) {
+        mask |= 1 << k;
+        approx |= (err[k] != 0.f) << k;
+      }
+    // A single survivor, or survivors whose costs are all exact (reference
+    // double arithmetic, first minimum already taken), is the answer.
+    if (__popc(mask) == 1 || approx == 0) return best;
   }
   Deferred e;
   e.pix = (int)pix;
