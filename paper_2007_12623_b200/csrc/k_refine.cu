@@ -81,26 +81,30 @@ __host__ __device__ inline size_t tile_bytes(int R) {
 }
 
 // Stage the BT-layout prefix rows [v0-R, v0+kTY+R) x columns [u0-R, u0+kTX+R]
-// of one frame. Consecutive threads walk rows first: within a 32-row block
-// of the BT layout those are consecutive addresses.
-template <typename T>
-__device__ __forceinline__ PsumTile<T> load_tile(const T* __restrict__ psumT, int W, int H, int R,
+// of one frame. Lanes walk rows (contiguous within a BT row block), warps walk
+// columns; RF > 0 makes the tile geometry compile-time.
+template <int RF, typename T>
+__device__ __forceinline__ PsumTile<T> load_tile(const T* __restrict__ psumT, int W, int H, int Rr,
                                                  const int* __restrict__ span_g, int*& span) {
   extern __shared__ double tile_raw[];
   T* tile_mem = reinterpret_cast<T*>(tile_raw);
+  const int R = RF > 0 ? RF : Rr;
   const int pitch = tile_pitch(R);
   const int rows = kTY + 2 * R;
   const int u0 = blockIdx.x * kTX, v0 = blockIdx.y * kTY;
   span = reinterpret_cast<int*>(tile_mem + (size_t)rows * pitch);
   const int tid = threadIdx.y * kTX + threadIdx.x;
   for (int k = tid; k <= R; k += kTX * kBY) span[k] = __ldg(span_g + k);
-  for (int k = tid; k < rows * pitch; k += kTX * kBY) {
-    const int r = k % rows, c = k / rows;
-    const int pr = v0 - R + r, pc = u0 - R + c;
-    T x = T(0);
-    if (pr >= 0 && pr < H && pc >= 0 && pc <= W)
-      x = __ldg(psumT + ((long)(pr >> 5) * (W + 1) + pc) * 32 + (pr & 31));
-    tile_mem[r * pitch + c] = x;
+  for (int c = threadIdx.y; c < pitch; c += kBY) {
+    const int pc = u0 - R + c;
+    const bool col_ok = pc >= 0 && pc <= W;
+    for (int r = threadIdx.x; r < rows; r += kTX) {
+      const int pr = v0 - R + r;
+      T x = T(0);
+      if (col_ok && pr >= 0 && pr < H)
+        x = __ldg(psumT + ((long)(pr >> 5) * (W + 1) + pc) * 32 + (pr & 31));
+      tile_mem[r * pitch + c] = x;
+    }
   }
   __syncthreads();
   return PsumTile<T>{tile_mem, pitch, u0, v0};
@@ -174,7 +178,7 @@ __global__ void __launch_bounds__(kTX * kBY)
   const long f = blockIdx.z;
   const int W = a.g.W, H = a.g.H, R = a.radius;
   int* span;
-  const PsumTile<int> P = load_tile(ipsumT + f * bt_frame(W, H, 1), W, H, R, a.span, span);
+  const PsumTile<int> P = load_tile<RF>(ipsumT + f * bt_frame(W, H, 1), W, H, R, a.span, span);
   const int u = blockIdx.x * kTX + threadIdx.x;
 #pragma unroll
   for (int rr = 0; rr < kTY / kBY; ++rr) {
@@ -213,7 +217,7 @@ __global__ void __launch_bounds__(kTX * kBY)
   const long f = blockIdx.z;
   const int W = a.g.W, H = a.g.H, R = a.radius;
   int* span;
-  const PsumTile<double> T = load_tile(psumT + f * bt_frame(W, H, 1), W, H, R, a.span, span);
+  const PsumTile<double> T = load_tile<RF>(psumT + f * bt_frame(W, H, 1), W, H, R, a.span, span);
   const int u = blockIdx.x * kTX + threadIdx.x;
 #pragma unroll
   for (int rr = 0; rr < kTY / kBY; ++rr) {
@@ -263,6 +267,26 @@ __device__ __forceinline__ double exact_cost(const uint8_t* L, const uint8_t* R,
 
 constexpr int kMaxCand = 2 * kRefineR + 1;
 
+// Approximate re-pick cost of candidate c with an error bar (see repick()).
+__device__ __forceinline__ void repick_cost(const RefineArgs& a, int u, int c, double dv,
+                                            const wscore_t* wp, int W, int half, double& cost,
+                                            double& err) {
+  constexpr float kErrM = 6e-4f;  // fp16 score (2^-11) + FP32 sweep (5 ulp) + 1/x, relative
+  double m = 1000.0;              // 1 / kZnccCostEpsilon, exact
+  err = 0.0;
+  const int ru = u - c;
+  if (ru >= half && ru < W - half) {
+    const float sc = __half2float(wp[c]);
+    if (!isnan(sc) && sc >= 0.99e-3f) {  // below: certainly clamped, M exact
+      const float mf = 1.f / fmaxf(sc, 1e-3f);
+      m = (double)mf;
+      err = (double)(kErrM * mf);
+    }
+  }
+  const double diff = __dsub_rn((double)c, dv);
+  cost = __dadd_rn(m, __dmul_rn(__dmul_rn(a.eta, diff), diff));
+}
+
 // Re-pick of one pixel (smoothing.cpp:119-144) given its smoothed d.
 // Returns the new o, or INT_MIN when the pixel is deferred to the exact kernel.
 //
@@ -311,64 +335,67 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
     }
     return best;
   }
-  int mask = 0;
   int best = c_lo;
-  if (c_lo < wb || c_hi > wb + kWin - 1) {
-    mask = (1 << (c_hi - c_lo + 1)) - 1;  // window miss: score every candidate exactly
-  } else {
+  bool ambiguous = true;
+  if (c_lo >= wb && c_hi <= wb + kWin - 1) {
     // cost(c) = M(c) + E(c). E = (eta diff) diff is computed exactly as the
     // reference does (FP64); M = 1/max(s, 1e-3) is exact (1000) when the score
     // is undefined or certainly below 1e-3, else derived from the fp16 score
-    // with relative error <= kErrM. Only candidates whose error bars overlap
-    // the minimum's are re-scored exactly.
-    constexpr double kErrM = 6e-4;  // fp16 score (2^-11) + FP32 sweep (5 ulp) + 1/x
+    // with relative error <= kErrM. The pick is final when no other
+    // candidate's lower bound reaches the minimum's upper bound.
     const wscore_t* wp = win_row - wb;  // wp[c]: score of candidate c
-    double cost[kMaxCand];
-    float err[kMaxCand];
-    double upper = INFINITY, best_cost = INFINITY;
+    double best_cost = INFINITY, upper = INFINITY, lo1 = INFINITY, lo2 = INFINITY;
 #pragma unroll
     for (int k = 0; k < kMaxCand; ++k) {
       const int c = c_lo + k;
-      cost[k] = INFINITY;
-      err[k] = 0.f;
       if (c <= c_hi) {
-        const int ru = u - c;
-        double m = 1000.0;  // 1 / kZnccCostEpsilon, exact
-        if (ru >= half && ru < W - half) {
-          const float sc = __half2float(wp[c]);
-          if (!isnan(sc) && sc >= 0.99e-3f) {
-            const float mf = 1.f / fmaxf(sc, 1e-3f);
-            m = (double)mf;
-            err[k] = (float)(kErrM * mf);
-          }
-        }
-        const double diff = __dsub_rn((double)c, dv);
-        cost[k] = __dadd_rn(m, __dmul_rn(__dmul_rn(a.eta, diff), diff));
-        if (cost[k] < best_cost) {  // first minimum of the (approximate) costs
-          best_cost = cost[k];
+        double cost, err;
+        repick_cost(a, u, c, dv, wp, W, half, cost, err);
+        if (cost < best_cost) {  // first minimum of the (approximate) costs
+          best_cost = cost;
           best = c;
         }
-        upper = fmin(upper, cost[k] + (double)err[k]);
+        upper = fmin(upper, cost + err);
+        const double lb = cost - err;
+        if (lb < lo1) {
+          lo2 = lo1;
+          lo1 = lb;
+        } else {
+          lo2 = fmin(lo2, lb);
+        }
       }
     }
-    int approx = 0;
-#pragma unroll
-    for (int k = 0; k < kMaxCand; ++k)
-      if (cost[k] - (double)err[k] <= upper) {
-        mask |= 1 << k;
-        approx |= (err[k] != 0.f) << k;
-      }
-    // A single survivor, or survivors whose costs are all exact (reference
-    // double arithmetic, first minimum already taken), is the answer.
-    if (__popc(mask) == 1 || approx == 0) return best;
+    ambiguous = lo2 <= upper;
+    if (!ambiguous) return best;
   }
-  Deferred e;
-  e.pix = (int)pix;
-  e.c_lo = c_lo;
-  e.mask = mask;
-  e.pad = 0;
-  e.d = dv;
-  defer[atomicAdd(defer_count, 1u)] = e;
+  // Rare path: collect the candidates whose error bars reach the minimum.
+  int mask = 0, approx = 0;
+  if (c_lo < wb || c_hi > wb + kWin - 1) {
+    mask = (1 << (c_hi - c_lo + 1)) - 1;  // window miss: score every candidate exactly
+    approx = mask;
+  } else {
+    const wscore_t* wp = win_row - wb;
+    double upper = INFINITY;
+    for (int c = c_lo; c <= c_hi; ++c) {
+      double cost, err;
+      repick_cost(a, u, c, dv, wp, W, half, cost, err);
+      upper = fmin(upper, cost + err);
+    }
+    for (int c = c_lo; c <= c_hi; ++c) {
+      double cost, err;
+      repick_cost(a, u, c, dv, wp, W, half, cost, err);
+      if (cost - err <= upper) {
+        mask |= 1 << (c - c_lo);
+        if (err != 0.0) approx |= 1 << (c - c_lo);
+      }
+    }
+    // Survivors with exact costs only: `best` (the first minimum over
+    // reference-exact doubles) is already the reference's pick.
+    if (approx == 0) return best;
+  }
+  Deferred* e = defer + atomicAdd(defer_count, 1u);
+  *reinterpret_cast<int4*>(e) = make_int4((int)pix, c_lo, mask, 0);
+  e->d = dv;
   return INT_MIN;
 }
 
@@ -414,7 +441,7 @@ __global__ void __launch_bounds__(kTX * kBY)
     }
   }
   int* span;
-  const PsumTile<double> T = load_tile(psumT + f * bt_frame(W, H, 1), W, H, R, a.span, span);
+  const PsumTile<double> T = load_tile<RF>(psumT + f * bt_frame(W, H, 1), W, H, R, a.span, span);
   const uint8_t* L = lgray + f * gray_stride;
   const uint8_t* Rg = rgray + f * gray_stride;
 #pragma unroll 1
