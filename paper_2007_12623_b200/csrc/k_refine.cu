@@ -394,7 +394,9 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
     if (approx == 0) return best;
   }
   Deferred* e = defer + atomicAdd(defer_count, 1u);
-  *reinterpret_cast<int4*>(e) = make_int4((int)pix, c_lo, mask, 0);
+  int2* ei = reinterpret_cast<int2*>(e);  // Deferred is 8-byte aligned
+  ei[0] = make_int2((int)pix, c_lo);
+  ei[1] = make_int2(mask, 0);
   e->d = dv;
   return INT_MIN;
 }
