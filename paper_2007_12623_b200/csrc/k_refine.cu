@@ -66,7 +66,7 @@ void launch_refine_init(const float* disp, const uint8_t* valid, double* o, doub
 // in shared memory once, so the 2 (2R+1) reads per pixel are LDS, not L2
 // round trips. Summation order and operands are the reference's: bit-exact.
 
-constexpr int kTX = 32, kTY = 16, kBY = 8;  // tile = 32 x 16 pixels, block = 32 x 8
+constexpr int kTX = 32, kTY = 16, kBY = 16;  // tile = block = 32 x 16 pixels
 
 template <typename T>
 struct PsumTile {
@@ -79,13 +79,32 @@ template <typename T>
 __host__ __device__ inline size_t tile_bytes(int R) {
   return sizeof(T) * (size_t)(kTY + 2 * R) * tile_pitch(R) + sizeof(int) * (R + 1);
 }
+// re-pick: the tile, then each thread's 32-byte score window (16-byte aligned)
+__host__ __device__ inline size_t repick_smem_bytes(int R) {
+  return (tile_bytes<double>(R) + 15) / 16 * 16 + (size_t)kTX * kBY * kWin * sizeof(wscore_t);
+}
+
+__device__ __forceinline__ void cp_async_bytes(void* dst, const void* src, int bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+  else if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
 
 // Stage the BT-layout prefix rows [v0-R, v0+kTY+R) x columns [u0-R, u0+kTX+R]
-// of one frame. Lanes walk rows (contiguous within a BT row block), warps walk
-// columns; RF > 0 makes the tile geometry compile-time.
+// of one frame with cp.async (every copy in flight at once; lanes walk rows,
+// contiguous within a BT row block). The caller may issue more copies, then
+// calls tile_wait(). RF > 0 makes the tile geometry compile-time.
 template <int RF, typename T>
-__device__ __forceinline__ PsumTile<T> load_tile(const T* __restrict__ psumT, int W, int H, int Rr,
-                                                 const int* __restrict__ span_g, int*& span) {
+__device__ __forceinline__ PsumTile<T> load_tile_issue(const T* __restrict__ psumT, int W, int H,
+                                                       int Rr, const int* __restrict__ span_g,
+                                                       int*& span) {
   extern __shared__ double tile_raw[];
   T* tile_mem = reinterpret_cast<T*>(tile_raw);
   const int R = RF > 0 ? RF : Rr;
@@ -100,14 +119,27 @@ __device__ __forceinline__ PsumTile<T> load_tile(const T* __restrict__ psumT, in
     const bool col_ok = pc >= 0 && pc <= W;
     for (int r = threadIdx.x; r < rows; r += kTX) {
       const int pr = v0 - R + r;
-      T x = T(0);
+      T* dst = tile_mem + r * pitch + c;
       if (col_ok && pr >= 0 && pr < H)
-        x = __ldg(psumT + ((long)(pr >> 5) * (W + 1) + pc) * 32 + (pr & 31));
-      tile_mem[r * pitch + c] = x;
+        cp_async_bytes(dst, psumT + ((long)(pr >> 5) * (W + 1) + pc) * 32 + (pr & 31), sizeof(T));
+      else
+        *dst = T(0);
     }
   }
-  __syncthreads();
   return PsumTile<T>{tile_mem, pitch, u0, v0};
+}
+
+__device__ __forceinline__ void tile_wait() {
+  cp_async_wait_all();
+  __syncthreads();
+}
+
+template <int RF, typename T>
+__device__ __forceinline__ PsumTile<T> load_tile(const T* __restrict__ psumT, int W, int H, int Rr,
+                                                 const int* __restrict__ span_g, int*& span) {
+  const PsumTile<T> P = load_tile_issue<RF>(psumT, W, H, Rr, span_g, span);
+  tile_wait();
+  return P;
 }
 
 template <typename T>
@@ -411,63 +443,56 @@ __global__ void __launch_bounds__(kTX * kBY)
                int2* __restrict__ chg, unsigned* __restrict__ chg_count,
                Deferred* __restrict__ defer, unsigned* __restrict__ defer_count, RefineArgs a,
                long stride, long gray_stride) {
-  constexpr int NR = kTY / kBY;  // pixels per thread
   const long f = blockIdx.z;
   const int W = a.g.W, H = a.g.H, R = a.radius;
   const int u = blockIdx.x * kTX + threadIdx.x;
-  // Issue this thread's per-pixel loads before the tile barrier so their
-  // HBM latency overlaps the shared-memory staging.
-  bool act[NR];
-  int cn[NR], sv[NR], ol[NR], wb[NR];
-  double av[NR];
-#pragma unroll
-  for (int rr = 0; rr < NR; ++rr) {
-    const int v = blockIdx.y * kTY + threadIdx.y + rr * kBY;
-    const long i = f * stride + (long)v * W + u;
-    act[rr] = u < W && v < H && valid[i];
-    cn[rr] = sv[rr] = ol[rr] = 0;
-    wb[rr] = kNoWin;
-    av[rr] = 0.0;
-    if (act[rr]) {
-      cn[rr] = __ldg(cnt + i);
-      if (USE_SO) {
-        sv[rr] = __ldg(so + i);
-        ol[rr] = o[i];
-      } else {
-        av[rr] = __ldg(avg + i);
-      }
-      if (win) {
-        wb[rr] = __ldg(wbase + i);
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(win + i * kWin));
-      }
-    }
-  }
+  const int v = blockIdx.y * kTY + threadIdx.y;
+  const long pix = (long)v * W + u;
+  const long i = f * stride + pix;
+  const bool inside = u < W && v < H;
+  // 1. issue every global->shared copy (prefix tile + this pixel's window)
   int* span;
-  const PsumTile<double> T = load_tile<RF>(psumT + f * bt_frame(W, H, 1), W, H, R, a.span, span);
-  const uint8_t* L = lgray + f * gray_stride;
-  const uint8_t* Rg = rgray + f * gray_stride;
-#pragma unroll 1
-  for (int rr = 0; rr < NR; ++rr) {
-    if (!act[rr]) continue;
-    const int v = blockIdx.y * kTY + threadIdx.y + rr * kBY;
-    const long pix = (long)v * W + u;
-    const long i = f * stride + pix;
-    const double s = disc_sum_any<RF>(T, span, W, H, u, v, R);
-    const double c = (double)cn[rr];
-    const double bav = __ddiv_rn(s, c);
-    // avg = s_o / c: with integer o the reference's double disc sum is exact,
-    // so the integer sum reproduces it bit for bit.
-    const double a_o = USE_SO ? __ddiv_rn((double)sv[rr], c) : av[rr];
-    const double x = __dsub_rn(a_o, bav);
-    const double dv = x < a.lo ? a.lo : (a.hi < x ? a.hi : x);  // std::clamp
-    d[i] = dv;
-    const int best = repick(a, u, v, dv, L, Rg, win ? win + i * kWin : nullptr, wb[rr], pix,
-                            defer + f * stride, defer_count + f);
-    if (best != INT_MIN) {
-      if (USE_SO && best != ol[rr])
-        chg[f * stride + atomicAdd(chg_count + f, 1u)] = make_int2((int)pix, best - ol[rr]);
-      o[i] = best;
+  const PsumTile<double> T =
+      load_tile_issue<RF>(psumT + f * bt_frame(W, H, 1), W, H, R, a.span, span);
+  extern __shared__ double tile_raw[];
+  wscore_t* swin = reinterpret_cast<wscore_t*>(reinterpret_cast<unsigned char*>(tile_raw) +
+                                               (tile_bytes<double>(R) + 15) / 16 * 16) +
+                   (threadIdx.y * kTX + threadIdx.x) * kWin;
+  if (win && inside) {
+    cp_async_bytes(swin, win + i * kWin, 16);
+    cp_async_bytes(swin + 8, win + i * kWin + 8, 16);
+  }
+  // 2. per-pixel scalars while the copies fly
+  const bool act = inside && valid[i];
+  int cn = 1, sv = 0, ol = 0, wb = kNoWin;
+  double av = 0.0;
+  if (act) {
+    cn = __ldg(cnt + i);
+    if (USE_SO) {
+      sv = __ldg(so + i);
+      ol = o[i];
+    } else {
+      av = __ldg(avg + i);
     }
+    if (win) wb = __ldg(wbase + i);
+  }
+  tile_wait();
+  if (!act) return;
+  const double s = disc_sum_any<RF>(T, span, W, H, u, v, R);
+  const double c = (double)cn;
+  const double bav = __ddiv_rn(s, c);
+  // avg = s_o / c: with integer o the reference's double disc sum is exact,
+  // so the integer sum reproduces it bit for bit.
+  const double a_o = USE_SO ? __ddiv_rn((double)sv, c) : av;
+  const double x = __dsub_rn(a_o, bav);
+  const double dv = x < a.lo ? a.lo : (a.hi < x ? a.hi : x);  // std::clamp
+  d[i] = dv;
+  const int best = repick(a, u, v, dv, lgray + f * gray_stride, rgray + f * gray_stride,
+                          win ? swin : nullptr, wb, pix, defer + f * stride, defer_count + f);
+  if (best != INT_MIN) {
+    if (USE_SO && best != ol)
+      chg[f * stride + atomicAdd(chg_count + f, 1u)] = make_int2((int)pix, best - ol);
+    o[i] = best;
   }
 }
 
@@ -479,7 +504,7 @@ void launch_d_repick(const double* psumT, const uint8_t* valid, const int* cnt,
                      long gray_stride, unsigned long long* counters, cudaStream_t s) {
   (void)counters;
   if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
-  const size_t smem = tile_bytes<double>(a.radius);
+  const size_t smem = repick_smem_bytes(a.radius);
   dim3 bl(kTX, kBY);
   dim3 grid((a.g.W + kTX - 1) / kTX, (a.g.H + kTY - 1) / kTY, frames);
 #define SS_REPICK_ARGS                                                                        \
