@@ -114,16 +114,19 @@ __device__ __forceinline__ PsumTile<T> load_tile_issue(const T* __restrict__ psu
   span = reinterpret_cast<int*>(tile_mem + (size_t)rows * pitch);
   const int tid = threadIdx.y * kTX + threadIdx.x;
   for (int k = tid; k <= R; k += kTX * kBY) span[k] = __ldg(span_g + k);
-  for (int c = threadIdx.y; c < pitch; c += kBY) {
-    const int pc = u0 - R + c;
-    const bool col_ok = pc >= 0 && pc <= W;
-    for (int r = threadIdx.x; r < rows; r += kTX) {
-      const int pr = v0 - R + r;
-      T* dst = tile_mem + r * pitch + c;
-      if (col_ok && pr >= 0 && pr < H)
-        cp_async_bytes(dst, psumT + ((long)(pr >> 5) * (W + 1) + pc) * 32 + (pr & 31), sizeof(T));
+  // Lanes walk rows, warps walk columns. A row's BT offset is fixed per lane
+  // and chunk; a column adds 32 elements.
+  for (int r = threadIdx.x; r < rows; r += kTX) {
+    const int pr = v0 - R + r;
+    const bool row_ok = pr >= 0 && pr < H;
+    const T* src = psumT + ((long)(pr >> 5) * (W + 1)) * 32 + (pr & 31);
+    T* dst = tile_mem + r * pitch;
+    for (int c = threadIdx.y; c < pitch; c += kBY) {
+      const int pc = u0 - R + c;
+      if (row_ok && pc >= 0 && pc <= W)
+        cp_async_bytes(dst + c, src + (long)pc * 32, sizeof(T));
       else
-        *dst = T(0);
+        dst[c] = T(0);
     }
   }
   return PsumTile<T>{tile_mem, pitch, u0, v0};
@@ -299,24 +302,57 @@ __device__ __forceinline__ double exact_cost(const uint8_t* L, const uint8_t* R,
 
 constexpr int kMaxCand = 2 * kRefineR + 1;
 
-// Approximate re-pick cost of candidate c with an error bar (see repick()).
-__device__ __forceinline__ void repick_cost(const RefineArgs& a, int u, int c, double dv,
-                                            const wscore_t* wp, int W, int half, double& cost,
-                                            double& err) {
+// Re-pick cost of candidate c in FP32 with an absolute error bar (see repick()).
+// exact_m reports whether the match cost is exactly 1/kZnccCostEpsilon.
+__device__ __forceinline__ void repick_cost_f(float eta_f, int u, int c, float dv_f,
+                                              const wscore_t* wp, int W, int half, float& cost,
+                                              float& err, bool& exact_m) {
   constexpr float kErrM = 6e-4f;  // fp16 score (2^-11) + FP32 sweep (5 ulp) + 1/x, relative
-  double m = 1000.0;              // 1 / kZnccCostEpsilon, exact
-  err = 0.0;
+  float m = 1000.f;               // 1 / kZnccCostEpsilon, exact
+  err = 0.f;                      // M uncertainty (E and rounding added by the caller)
+  exact_m = true;
   const int ru = u - c;
   if (ru >= half && ru < W - half) {
     const float sc = __half2float(wp[c]);
     if (!isnan(sc) && sc >= 0.99e-3f) {  // below: certainly clamped, M exact
+      m = 1.f / fmaxf(sc, 1e-3f);
+      err += kErrM * m;
+      exact_m = false;
+    }
+  }
+  const float df = (float)c - dv_f;
+  cost = m + eta_f * df * df;
+}
+
+// FP64 version for the rare paths: exact E (reference expression) and exact M
+// when the score is undefined/clamped; err is the FP16-derived M uncertainty.
+__device__ __forceinline__ void repick_cost_d(const RefineArgs& a, int u, int c, double dv,
+                                              const wscore_t* wp, int W, int half, double& cost,
+                                              double& err) {
+  constexpr double kErrM = 6e-4;
+  double m = 1000.0;
+  err = 0.0;
+  const int ru = u - c;
+  if (ru >= half && ru < W - half) {
+    const float sc = __half2float(wp[c]);
+    if (!isnan(sc) && sc >= 0.99e-3f) {
       const float mf = 1.f / fmaxf(sc, 1e-3f);
       m = (double)mf;
-      err = (double)(kErrM * mf);
+      err = kErrM * mf;
     }
   }
   const double diff = __dsub_rn((double)c, dv);
   cost = __dadd_rn(m, __dmul_rn(__dmul_rn(a.eta, diff), diff));
+}
+
+__device__ __forceinline__ int defer_pixel(Deferred* defer, unsigned* defer_count, long pix,
+                                           int c_lo, int mask, double dv) {
+  Deferred* e = defer + atomicAdd(defer_count, 1u);
+  int2* ei = reinterpret_cast<int2*>(e);  // Deferred is 8-byte aligned
+  ei[0] = make_int2((int)pix, c_lo);
+  ei[1] = make_int2(mask, 0);
+  e->d = dv;
+  return INT_MIN;
 }
 
 // Re-pick of one pixel (smoothing.cpp:119-144) given its smoothed d.
@@ -368,69 +404,65 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
     return best;
   }
   int best = c_lo;
-  bool ambiguous = true;
   if (c_lo >= wb && c_hi <= wb + kWin - 1) {
-    // cost(c) = M(c) + E(c). E = (eta diff) diff is computed exactly as the
-    // reference does (FP64); M = 1/max(s, 1e-3) is exact (1000) when the score
-    // is undefined or certainly below 1e-3, else derived from the fp16 score
-    // with relative error <= kErrM. The pick is final when no other
-    // candidate's lower bound reaches the minimum's upper bound.
+    // Common path, FP32: cost(c) = M(c) + E(c) with a rigorous absolute error
+    // bar per candidate (M from the fp16 score: 6e-4 relative; E from FP32 d;
+    // FP32 rounding of the sum). The pick is final when no other candidate's
+    // lower bound reaches the minimum's upper bound.
     const wscore_t* wp = win_row - wb;  // wp[c]: score of candidate c
-    double best_cost = INFINITY, upper = INFINITY, lo1 = INFINITY, lo2 = INFINITY;
+    const float dv_f = (float)dv;
+    // |df - (c - d)| <= delta = |d| 2^-23: E error <= |eta| (2*5 + delta) delta,
+    // plus a few ulp of E <= 25 |eta|.
+    const float delta = fabsf(dv_f) * 1.2e-7f;
+    const float errE = fabsf(a.eta_f) * (11.f * delta + 25.f * 4e-7f);
+    float best_cost = INFINITY, upper = INFINITY, lo1 = INFINITY, lo2 = INFINITY;
 #pragma unroll
     for (int k = 0; k < kMaxCand; ++k) {
       const int c = c_lo + k;
       if (c <= c_hi) {
-        double cost, err;
-        repick_cost(a, u, c, dv, wp, W, half, cost, err);
-        if (cost < best_cost) {  // first minimum of the (approximate) costs
+        float cost, err;
+        bool exact_m;
+        repick_cost_f(a.eta_f, u, c, dv_f, wp, W, half, cost, err, exact_m);
+        if (cost < best_cost) {
           best_cost = cost;
           best = c;
         }
-        upper = fmin(upper, cost + err);
-        const double lb = cost - err;
-        if (lb < lo1) {
-          lo2 = lo1;
-          lo1 = lb;
-        } else {
-          lo2 = fmin(lo2, lb);
-        }
+        err += errE + 1.2e-7f * fabsf(cost);  // E term + rounding of the FP32 sum
+        upper = fminf(upper, cost + err);
+        const float lb = cost - err;
+        lo2 = fminf(lo2, fmaxf(lo1, lb));  // second smallest lower bound
+        lo1 = fminf(lo1, lb);
       }
     }
-    ambiguous = lo2 <= upper;
-    if (!ambiguous) return best;
-  }
-  // Rare path: collect the candidates whose error bars reach the minimum.
-  int mask = 0, approx = 0;
-  if (c_lo < wb || c_hi > wb + kWin - 1) {
-    mask = (1 << (c_hi - c_lo + 1)) - 1;  // window miss: score every candidate exactly
-    approx = mask;
-  } else {
-    const wscore_t* wp = win_row - wb;
-    double upper = INFINITY;
+    if (lo2 > upper) return best;
+    // Ambiguous or in the exact-1000 regime: FP64 costs (exact E, exact
+    // clamped/undefined M) and error bars on the fp16-derived M only.
+    double bc = INFINITY, up = INFINITY;
     for (int c = c_lo; c <= c_hi; ++c) {
       double cost, err;
-      repick_cost(a, u, c, dv, wp, W, half, cost, err);
-      upper = fmin(upper, cost + err);
+      repick_cost_d(a, u, c, dv, wp, W, half, cost, err);
+      if (cost < bc) {
+        bc = cost;
+        best = c;
+      }
+      up = fmin(up, cost + err);
     }
+    int mask = 0, approx = 0;
     for (int c = c_lo; c <= c_hi; ++c) {
       double cost, err;
-      repick_cost(a, u, c, dv, wp, W, half, cost, err);
-      if (cost - err <= upper) {
+      repick_cost_d(a, u, c, dv, wp, W, half, cost, err);
+      if (cost - err <= up) {
         mask |= 1 << (c - c_lo);
         if (err != 0.0) approx |= 1 << (c - c_lo);
       }
     }
-    // Survivors with exact costs only: `best` (the first minimum over
-    // reference-exact doubles) is already the reference's pick.
-    if (approx == 0) return best;
+    // A single survivor, or survivors whose costs are all reference-exact
+    // doubles (first minimum already taken), is the reference's pick.
+    if (__popc(mask) == 1 || approx == 0) return best;
+    return defer_pixel(defer, defer_count, pix, c_lo, mask, dv);
   }
-  Deferred* e = defer + atomicAdd(defer_count, 1u);
-  int2* ei = reinterpret_cast<int2*>(e);  // Deferred is 8-byte aligned
-  ei[0] = make_int2((int)pix, c_lo);
-  ei[1] = make_int2(mask, 0);
-  e->d = dv;
-  return INT_MIN;
+  // Window miss: score every candidate exactly.
+  return defer_pixel(defer, defer_count, pix, c_lo, (1 << (c_hi - c_lo + 1)) - 1, dv);
 }
 
 template <int RF, bool USE_SO>
