@@ -114,19 +114,40 @@ __device__ __forceinline__ PsumTile<T> load_tile_issue(const T* __restrict__ psu
   span = reinterpret_cast<int*>(tile_mem + (size_t)rows * pitch);
   const int tid = threadIdx.y * kTX + threadIdx.x;
   for (int k = tid; k <= R; k += kTX * kBY) span[k] = __ldg(span_g + k);
-  // Lanes walk rows, warps walk columns. A row's BT offset is fixed per lane
-  // and chunk; a column adds 32 elements.
-  for (int r = threadIdx.x; r < rows; r += kTX) {
-    const int pr = v0 - R + r;
-    const bool row_ok = pr >= 0 && pr < H;
-    const T* src = psumT + ((long)(pr >> 5) * (W + 1)) * 32 + (pr & 31);
-    T* dst = tile_mem + r * pitch;
-    for (int c = threadIdx.y; c < pitch; c += kBY) {
-      const int pc = u0 - R + c;
-      if (row_ok && pc >= 0 && pc <= W)
-        cp_async_bytes(dst + c, src + (long)pc * 32, sizeof(T));
-      else
-        dst[c] = T(0);
+  // Lanes walk rows (contiguous within a BT row block), warps walk columns.
+  if constexpr (RF > 0) {
+    constexpr int P = kTX + 2 * RF + 1, ROWS = kTY + 2 * RF;
+    constexpr int RCH = (ROWS + kTX - 1) / kTX, CCH = (P + kBY - 1) / kBY;
+#pragma unroll
+    for (int rc = 0; rc < RCH; ++rc) {
+      const int r = threadIdx.x + rc * kTX;
+      const int pr = v0 - RF + r;
+      const bool row_ok = r < ROWS && pr >= 0 && pr < H;
+      const T* src = psumT + ((long)(pr >> 5) * (W + 1)) * 32 + (pr & 31);
+      T* dst = tile_mem + r * P;
+#pragma unroll
+      for (int cc = 0; cc < CCH; ++cc) {
+        const int c = threadIdx.y + cc * kBY;
+        const int pc = u0 - RF + c;
+        if (r < ROWS && c < P) {
+          if (row_ok && pc >= 0 && pc <= W) cp_async_bytes(dst + c, src + pc * 32, sizeof(T));
+          else dst[c] = T(0);
+        }
+      }
+    }
+  } else {
+    for (int r = threadIdx.x; r < rows; r += kTX) {
+      const int pr = v0 - R + r;
+      const bool row_ok = pr >= 0 && pr < H;
+      const T* src = psumT + ((long)(pr >> 5) * (W + 1)) * 32 + (pr & 31);
+      T* dst = tile_mem + r * pitch;
+      for (int c = threadIdx.y; c < pitch; c += kBY) {
+        const int pc = u0 - R + c;
+        if (row_ok && pc >= 0 && pc <= W)
+          cp_async_bytes(dst + c, src + (long)pc * 32, sizeof(T));
+        else
+          dst[c] = T(0);
+      }
     }
   }
   return PsumTile<T>{tile_mem, pitch, u0, v0};
@@ -302,28 +323,6 @@ __device__ __forceinline__ double exact_cost(const uint8_t* L, const uint8_t* R,
 
 constexpr int kMaxCand = 2 * kRefineR + 1;
 
-// Re-pick cost of candidate c in FP32 with an absolute error bar (see repick()).
-// exact_m reports whether the match cost is exactly 1/kZnccCostEpsilon.
-__device__ __forceinline__ void repick_cost_f(float eta_f, int u, int c, float dv_f,
-                                              const wscore_t* wp, int W, int half, float& cost,
-                                              float& err, bool& exact_m) {
-  constexpr float kErrM = 6e-4f;  // fp16 score (2^-11) + FP32 sweep (5 ulp) + 1/x, relative
-  float m = 1000.f;               // 1 / kZnccCostEpsilon, exact
-  err = 0.f;                      // M uncertainty (E and rounding added by the caller)
-  exact_m = true;
-  const int ru = u - c;
-  if (ru >= half && ru < W - half) {
-    const float sc = __half2float(wp[c]);
-    if (!isnan(sc) && sc >= 0.99e-3f) {  // below: certainly clamped, M exact
-      m = 1.f / fmaxf(sc, 1e-3f);
-      err += kErrM * m;
-      exact_m = false;
-    }
-  }
-  const float df = (float)c - dv_f;
-  cost = m + eta_f * df * df;
-}
-
 // FP64 version for the rare paths: exact E (reference expression) and exact M
 // when the score is undefined/clamped; err is the FP16-derived M uncertainty.
 __device__ __forceinline__ void repick_cost_d(const RefineArgs& a, int u, int c, double dv,
@@ -405,38 +404,37 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
   }
   int best = c_lo;
   if (c_lo >= wb && c_hi <= wb + kWin - 1) {
-    // Common path, FP32: cost(c) = M(c) + E(c) with a rigorous absolute error
-    // bar per candidate (M from the fp16 score: 6e-4 relative; E from FP32 d;
-    // FP32 rounding of the sum). The pick is final when no other candidate's
-    // lower bound reaches the minimum's upper bound.
+    // Common path, FP32. cost_f(c) = M_f + E_f with |cost_f - cost| <=
+    // eps cost + errE, eps = 6e-4 (fp16 score -> M) + 1.2e-7 (FP32 sum),
+    // errE from the FP32 copy of d. The first minimum is certified when the
+    // runner-up's lower bound stays above the minimum's upper bound.
     const wscore_t* wp = win_row - wb;  // wp[c]: score of candidate c
     const float dv_f = (float)dv;
-    // |df - (c - d)| <= delta = |d| 2^-23: E error <= |eta| (2*5 + delta) delta,
-    // plus a few ulp of E <= 25 |eta|.
-    const float delta = fabsf(dv_f) * 1.2e-7f;
-    const float errE = fabsf(a.eta_f) * (11.f * delta + 25.f * 4e-7f);
-    float best_cost = INFINITY, upper = INFINITY, lo1 = INFINITY, lo2 = INFINITY;
+    const float delta = fabsf(dv_f) * 1.2e-7f;  // |dv_f - d|, and FP32 rounding of c - dv_f
+    constexpr float kEps = 6e-4f + 1.2e-7f;
+    // (with eta < 0, E < 0 and the M error, relative to M, is bounded via |E| <= 25|eta|)
+    const float errE = fabsf(a.eta_f) * (11.f * delta + 25.f * 4e-7f + (a.eta_f < 0.f ? 25.f * kEps : 0.f));
+    float best_cost = INFINITY, second = INFINITY;
+    float cf = (float)c_lo;
 #pragma unroll
     for (int k = 0; k < kMaxCand; ++k) {
-      const int c = c_lo + k;
-      if (c <= c_hi) {
-        float cost, err;
-        bool exact_m;
-        repick_cost_f(a.eta_f, u, c, dv_f, wp, W, half, cost, err, exact_m);
+      if (c_lo + k <= c_hi) {
+        const float sc = __half2float(wp[c_lo + k]);  // NaN: undefined (incl. ru outside)
+        const bool appr = sc >= 0.99e-3f;             // below: certainly clamped to 1000
+        const float m = appr ? __fdividef(1.f, fmaxf(sc, 1e-3f)) : 1000.f;
+        const float df = cf - dv_f;
+        const float cost = m + a.eta_f * df * df;
+        second = fminf(second, fmaxf(best_cost, cost));
         if (cost < best_cost) {
           best_cost = cost;
-          best = c;
+          best = c_lo + k;
         }
-        err += errE + 1.2e-7f * fabsf(cost);  // E term + rounding of the FP32 sum
-        upper = fminf(upper, cost + err);
-        const float lb = cost - err;
-        lo2 = fminf(lo2, fmaxf(lo1, lb));  // second smallest lower bound
-        lo1 = fminf(lo1, lb);
       }
+      cf += 1.f;
     }
-    if (lo2 > upper) return best;
-    // Ambiguous or in the exact-1000 regime: FP64 costs (exact E, exact
-    // clamped/undefined M) and error bars on the fp16-derived M only.
+    if (second * (1.f - kEps) - errE > best_cost * (1.f + kEps) + errE) return best;
+    // Ambiguous: FP64 costs (exact E, exact clamped/undefined M) with error
+    // bars on the fp16-derived M only.
     double bc = INFINITY, up = INFINITY;
     for (int c = c_lo; c <= c_hi; ++c) {
       double cost, err;
