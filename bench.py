@@ -124,12 +124,14 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_frames(rank, frames, unique):
+def make_frames(rank, world, frames, unique):
+    from paper_2007_12623_b200.shard import frame_range
     from paper_2007_12623_b200.synth import as_rgb, stereo_pair
+    start, _ = frame_range(world * frames, rank, world)  # this rank's block of the global batch
     u = max(1, min(unique, frames))
     Ls, Rs = [], []
     for i in range(u):
-        L, R, _ = stereo_pair("textured", W, H, D, seed=rank * frames + i)
+        L, R, _ = stereo_pair("textured", W, H, D, seed=start + i)
         Ls.append(as_rgb(L))
         Rs.append(as_rgb(R))
     Ls, Rs = np.stack(Ls), np.stack(Rs)
@@ -171,7 +173,8 @@ def config_dict(args, world):
                         "D=64 (d 0..63), full chain luma+WTA+cleanup+refine+cloud(normals)",
             "width": W, "height": H, "disparities": D, "pairs_per_step_per_gpu": args.frames,
             "frames_per_launch": args.batch, "unique_seeded_frames": min(args.unique, args.frames),
-            "cache": "inputs > L2 (per-step input 796 MB RGB per GPU; 153 MB/frame cost volume)",
+            "cache": "inputs > L2 (per-step input 796 MB RGB per GPU, not flushed: each frame is "
+                     "read once per step)",
             "parallelism": f"frame-shard x{world}, no collective"}
 
 
@@ -219,7 +222,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     F, B = args.frames, args.batch
     N = W * H
-    Lh_np, Rh_np = make_frames(rank, F, args.unique)
+    Lh_np, Rh_np = make_frames(rank, world, F, args.unique)
     # pinned host inputs (e2e) and HBM-resident copies (device value)
     Lh = torch.from_numpy(Lh_np).pin_memory()
     Rh = torch.from_numpy(Rh_np).pin_memory()
@@ -268,10 +271,8 @@ def run_ours(args):
     stages = ctx.stage_times()
     stats = ctx.stats()
     ctx.enable_timing(False)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    from paper_2007_12623_b200.shard import max_over_ranks
+    ms_max = max_over_ranks(ms, device=dev)
     pairs = world * F * args.steps
     value = pairs / (ms_max / 1000.0)
 
@@ -290,11 +291,8 @@ def run_ours(args):
         f1e.record(stream)
         f1e.synchronize()
         barrier()
-        ems = f0e.elapsed_time(f1e)
-        te = torch.tensor([ems], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e_value = world * F * args.e2e_steps / (float(te.item()) / 1000.0)
+        ems = max_over_ranks(f0e.elapsed_time(f1e), device=dev)
+        e2e_value = world * F * args.e2e_steps / (ems / 1000.0)
         npts = int(ho["n_points"].sum())
         h2d = 2 * F * N * 3
         d2h = F * N * (4 + 1 + 4) + 4 * F + npts * (12 + 12 + 3)
@@ -319,10 +317,17 @@ def run_ours(args):
     ops_per_launch = per_frame_ops * frames_timed / launches
     achieved = ops_per_launch / (wta_ms / launches / 1000.0) if wta_ms > 0 else 0.0
     hbm_peak = float(peaks.get("hbm_gbs", 6446.9))
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(tpath):
+        t = json.load(open(tpath)).get("k_wta11", {})
+        if t.get("frames_per_launch") == B:
+            traffic = t.get("dram_bytes_per_launch")
     roofline = {
         "bound": "alu", "kernel": "k_wta11 (ZNCC cost sweep + WTA)",
         "achieved": achieved / 1e12, "peak": alu_peak / 1e12, "unit": "Tlane-op/s",
-        "frac": achieved / alu_peak if alu_peak else None, "traffic": None,
+        "frac": achieved / alu_peak if alu_peak else None, "traffic": traffic,
+        "traffic_unit": "DRAM bytes per launch (ncu, profiles/roofline_traffic.json)",
         "peak_source": f"{n_sm} SM x 128 lanes x sm_max_mhz {sm_max:.0f} (MEASURED_PEAKS.json); "
                        "ALU issue, not a bf16/HBM figure: the path is integer/FP64 ALU work",
         "ops_per_launch": ops_per_launch, "avg_launch_ms": wta_ms / launches,

@@ -1,0 +1,73 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): frame sharding, the
+max-over-ranks step time and the frame-ordered gather are independent of the
+rank count. The per-frame compute is the CPU oracle here (stand-in for the GPU
+call the bench makes on each rank); what is tested is the host side of §8e.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2007_12623_b200.shard import frame_range
+
+
+def test_frame_range_partitions():
+    for n in (0, 1, 5, 256, 1024):
+        for world in (1, 2, 3, 8):
+            spans = [frame_range(n, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            for (a, b), (c, d) in zip(spans, spans[1:]):
+                assert b == c
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, n_frames, result_path):
+    import torch.distributed as dist
+
+    from oracle.oracle import Oracle
+    from paper_2007_12623_b200.shard import gather_frames, max_over_ranks
+    from paper_2007_12623_b200.synth import params_for, stereo_pair
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Oracle("orc")
+    p = params_for(8)
+    start, end = frame_range(n_frames, rank, world)
+    disp, valid = [], []
+    for f in range(start, end):
+        L, R, _ = stereo_pair("textured", 48, 32, 8, seed=f)
+        d, v = orc.compute_disparity(L, R, p)
+        disp.append(d)
+        valid.append(v)
+    local = {"disparity": np.stack(disp) if disp else np.zeros((0, 32, 48), np.float32),
+             "valid": np.stack(valid) if valid else np.zeros((0, 32, 48), np.uint8)}
+    t = max_over_ranks(float(rank + 1))
+    out = gather_frames(local, n_frames, rank, world)
+    if rank == 0:
+        np.savez(result_path, t=t, **out)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_gather_matches_single_rank(tmp_path, orc, world):
+    from paper_2007_12623_b200.synth import params_for, stereo_pair
+    n_frames = 5
+    path = str(tmp_path / "gathered.npz")
+    mp.start_processes(_worker, args=(world, _free_port(), n_frames, path), nprocs=world,
+                       join=True, start_method="spawn")
+    g = np.load(path)
+    assert float(g["t"]) == float(world)  # max over ranks
+    p = params_for(8)
+    for f in range(n_frames):
+        L, R, _ = stereo_pair("textured", 48, 32, 8, seed=f)
+        d, v = orc.compute_disparity(L, R, p)
+        assert np.array_equal(g["disparity"][f], d) and np.array_equal(g["valid"][f], v)
