@@ -64,38 +64,22 @@ struct ThreadGeom {
   int wA, shA, wB, shB; // aligned word index + shift of the right streams A, B
 };
 
-template <int I>
-__device__ __forceinline__ void terms_i(uint32_t Lea, uint32_t Leb, uint32_t Loa, uint32_t Lob,
-                                        const uint32_t (&SA)[4], const uint32_t (&SB)[4],
-                                        uint32_t (&He)[kDB], uint32_t (&Ho)[kDB]) {
-  constexpr int t = I >> 1;
-  if constexpr ((I & 1) == 0) {
-    He[I] = __dp4a(Lea, win<8 - t>(SA), __dp4a(Leb, win<12 - t>(SA), 0u));
-    Ho[I] = __dp4a(Loa, win<7 - t>(SB), __dp4a(Lob, win<11 - t>(SB), 0u));
-  } else {
-    He[I] = __dp4a(Lea, win<7 - t>(SB), __dp4a(Leb, win<11 - t>(SB), 0u));
-    Ho[I] = __dp4a(Loa, win<7 - t>(SA), __dp4a(Lob, win<11 - t>(SA), 0u));
-  }
-}
+// The 4-byte windows of one image row that the thread's kDB candidates need:
+// the left tap words (fixed per thread) and the two right-image byte streams
+// A and B pre-aligned to the thread's misalignment.
+struct RowWords {
+  uint32_t Lea, Leb, Loa, Lob;
+  uint32_t SA[4], SB[4];
+};
 
-template <int... Is>
-__device__ __forceinline__ void terms_all(uint32_t Lea, uint32_t Leb, uint32_t Loa,
-                                          uint32_t Lob, const uint32_t (&SA)[4],
-                                          const uint32_t (&SB)[4], uint32_t (&He)[kDB],
-                                          uint32_t (&Ho)[kDB],
-                                          std::integer_sequence<int, Is...>) {
-  (terms_i<Is>(Lea, Leb, Loa, Lob, SA, SB, He, Ho), ...);
-}
-
-// He/Ho of image row y for the thread's kDB candidates.
-__device__ __forceinline__ void row_terms(const ThreadGeom& tg, int y, uint32_t (&He)[kDB],
-                                          uint32_t (&Ho)[kDB]) {
+__device__ __forceinline__ RowWords row_words(const ThreadGeom& tg, int y) {
+  RowWords w;
   const uint8_t* lre = tg.lplane + (long)(2 * y + tg.p) * tg.PP;
   const uint8_t* lro = tg.lplane + (long)(2 * y + 1 - tg.p) * tg.PP;
-  const uint32_t Lea = ld_win(lre, tg.Le);
-  const uint32_t Leb = ld_win(lre, tg.Le + 4) & 0xFFu;
-  const uint32_t Loa = ld_win(lro, tg.Lo);
-  const uint32_t Lob = ld_win(lro, tg.Lo + 4) & 0xFFFFu;
+  w.Lea = ld_win(lre, tg.Le);
+  w.Leb = ld_win(lre, tg.Le + 4) & 0xFFu;
+  w.Loa = ld_win(lro, tg.Lo);
+  w.Lob = ld_win(lro, tg.Lo + 4) & 0xFFFFu;
   const uint32_t* ar =
       reinterpret_cast<const uint32_t*>(tg.rplane + (long)(2 * y + tg.q0) * tg.PP) + tg.wA;
   const uint32_t* br =
@@ -106,13 +90,56 @@ __device__ __forceinline__ void row_terms(const ThreadGeom& tg, int y, uint32_t 
     a[t] = __ldg(ar + t);
     b[t] = __ldg(br + t);
   }
-  uint32_t SA[4], SB[4];
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
-    SA[t] = __funnelshift_r(a[t], a[t + 1], tg.shA);
-    SB[t] = __funnelshift_r(b[t], b[t + 1], tg.shB);
+    w.SA[t] = __funnelshift_r(a[t], a[t + 1], tg.shA);
+    w.SB[t] = __funnelshift_r(b[t], b[t + 1], tg.shB);
   }
-  terms_all(Lea, Leb, Loa, Lob, SA, SB, He, Ho, std::make_integer_sequence<int, kDB>{});
+  return w;
+}
+
+// He (even-offset taps, 5) and Ho (odd-offset taps, 6) of candidate I.
+template <int I>
+__device__ __forceinline__ uint32_t term_e(const RowWords& w) {
+  constexpr int t = I >> 1;
+  if constexpr ((I & 1) == 0) return __dp4a(w.Lea, win<8 - t>(w.SA), __dp4a(w.Leb, win<12 - t>(w.SA), 0u));
+  else return __dp4a(w.Lea, win<7 - t>(w.SB), __dp4a(w.Leb, win<11 - t>(w.SB), 0u));
+}
+template <int I>
+__device__ __forceinline__ uint32_t term_o(const RowWords& w) {
+  constexpr int t = I >> 1;
+  if constexpr ((I & 1) == 0) return __dp4a(w.Loa, win<7 - t>(w.SB), __dp4a(w.Lob, win<11 - t>(w.SB), 0u));
+  else return __dp4a(w.Loa, win<7 - t>(w.SA), __dp4a(w.Lob, win<11 - t>(w.SA), 0u));
+}
+
+// One row step of the running sums for candidate I (center v-1 -> v):
+//   X' = Y - He(v-6) + Ho(v+5),  Y' = X + He(v+5) - Ho(v-6)
+template <int I>
+__device__ __forceinline__ void step_i(const RowWords& wo, const RowWords& wn, int (&X)[kDB],
+                                       int (&Y)[kDB]) {
+  const int xn = Y[I] - (int)term_e<I>(wo) + (int)term_o<I>(wn);
+  const int yn = X[I] + (int)term_e<I>(wn) - (int)term_o<I>(wo);
+  X[I] = xn;
+  Y[I] = yn;
+}
+template <int... Is>
+__device__ __forceinline__ void step_all(const RowWords& wo, const RowWords& wn, int (&X)[kDB],
+                                         int (&Y)[kDB], std::integer_sequence<int, Is...>) {
+  (step_i<Is>(wo, wn, X, Y), ...);
+}
+
+// Warm-up accumulation of one row: dy even -> X += He, Y += Ho; odd swaps.
+template <int I>
+__device__ __forceinline__ void warm_i(const RowWords& w, bool even, int (&X)[kDB],
+                                       int (&Y)[kDB]) {
+  const int he = (int)term_e<I>(w), ho = (int)term_o<I>(w);
+  X[I] += even ? he : ho;
+  Y[I] += even ? ho : he;
+}
+template <int... Is>
+__device__ __forceinline__ void warm_all(const RowWords& w, bool even, int (&X)[kDB],
+                                         int (&Y)[kDB], std::integer_sequence<int, Is...>) {
+  (warm_i<Is>(w, even, X, Y), ...);
 }
 
 }  // namespace
@@ -154,6 +181,11 @@ __global__ void __launch_bounds__(512) k_wta11(
   const int c0 = g.cmin + j * kDB;
   const int nact = min(kDB, g.NC - j * kDB);
   const bool active = (u < W - h) && (nact > 0);
+  // candidates of this thread that take part in the WTA argmax
+  unsigned amask = 0;
+#pragma unroll
+  for (int i = 0; i < kDB; ++i)
+    amask |= (i < nact && c0 + i >= g.dmin && c0 + i <= g.dmax) ? (1u << i) : 0u;
 
   ThreadGeom tg;
   tg.lplane = lplane;
@@ -179,29 +211,17 @@ __global__ void __launch_bounds__(512) k_wta11(
 
   if (active) {
     for (int dy = -h; dy <= h; ++dy) {
-      uint32_t He[kDB], Ho[kDB];
-      row_terms(tg, v_begin + dy, He, Ho);
-      const bool even = ((dy + h) & 1) == 1;  // dy even <=> dy + 5 odd
-#pragma unroll
-      for (int i = 0; i < kDB; ++i) {
-        X[i] += (int)(even ? He[i] : Ho[i]);
-        Y[i] += (int)(even ? Ho[i] : He[i]);
-      }
+      const RowWords w = row_words(tg, v_begin + dy);
+      warm_all(w, ((dy + h) & 1) == 1 /* dy even */, X, Y,
+               std::make_integer_sequence<int, kDB>{});
     }
   }
 
   for (int v = v_begin; v < v_end; ++v) {
     if (v > v_begin && active) {
-      uint32_t Heo[kDB], Hoo[kDB], Hen[kDB], Hon[kDB];
-      row_terms(tg, v - 6, Heo, Hoo);
-      row_terms(tg, v + 5, Hen, Hon);
-#pragma unroll
-      for (int i = 0; i < kDB; ++i) {
-        const int xn = Y[i] - (int)Heo[i] + (int)Hon[i];
-        const int yn = X[i] + (int)Hen[i] - (int)Hoo[i];
-        X[i] = xn;
-        Y[i] = yn;
-      }
+      const RowWords wo = row_words(tg, v - 6);
+      const RowWords wn = row_words(tg, v + 5);
+      step_all(wo, wn, X, Y, std::make_integer_sequence<int, kDB>{});
     }
     const int slot = (v - v_begin) & (kRB - 1);
     float* gs = s_g + (slot * NCB + j * kDB) * 32 + lane;  // staged g of this (row, block)
@@ -210,24 +230,19 @@ __global__ void __launch_bounds__(512) k_wta11(
     if (active) {
       const int sl = __ldg(&lstat[(long)v * W + u].x);
       const int2* rrow = rstat + (long)v * g.SP + g.SPAD + ru0;
+      // Branch-free: every lane scores all kDB candidates (padded rstat keeps
+      // the loads in bounds); amask selects those inside [d_min, d_max] and
+      // the volume range, NaN (undefined) folds to -inf.
 #pragma unroll
       for (int i = 0; i < kDB; ++i) {
-        if (i < nact) {
-          const int2 rs = __ldg(rrow - i);
-          const int num = 61 * X[i] - sl * rs.x;
-          const float gv = __int2float_rn(num) * __int_as_float(rs.y);
-          gs[i * 32] = gv;
-          const int c = c0 + i;
-          if (c >= g.dmin && c <= g.dmax) {
-            if (gv > best) {
-              second = best;
-              best = gv;
-              arg = c;
-            } else {
-              second = fmaxf(second, gv);
-            }
-          }
-        }
+        const int2 rs = __ldg(rrow - i);
+        const int num = 61 * X[i] - sl * rs.x;
+        const float gv = __int2float_rn(num) * __int_as_float(rs.y);
+        gs[i * 32] = gv;
+        const float gc = ((amask >> i) & 1) ? fmaxf(gv, -INFINITY) : -INFINITY;
+        second = fmaxf(second, fminf(best, gc));
+        arg = gc > best ? c0 + i : arg;
+        best = fmaxf(best, gc);
       }
     }
     const int so = (slot * NB + j) * 32 + lane;
