@@ -1,13 +1,17 @@
 // Anti-shrink Laplacian refinement (refine_disparities, smoothing.cpp:68-159).
 //
+// Every refinement field lives in the BT layout (ss_internal.cuh): a warp owns
+// 32 consecutive rows of one column, so per-pixel loads/stores are single
+// lines and a block's 32 x 32 pixel tile is one contiguous 1024-entry range.
+//
 // Iteration 0 (o = the cleanup output, fractional where filled) follows the
 // reference literally: FP64 row prefix of o (k_scan.cu), k_avg_b, FP64 row
 // prefix of b, k_d_repick. After it, o is integer-valued, so its disc sum is an
 // exact integer S_o (and the reference's double sum of it is exact too):
-// S_o is built once (int prefix + k_disc_count) and then maintained by
-// k_so_update from the few pixels whose o changed (hundreds to thousands per
-// frame), and b is formed inside the b prefix scan (SrcB). Iterations >= 1 are
-// therefore one serial FP64 scan + one tiled gather + a small scatter.
+// S_o is built once (int prefix + k_disc_isum) and then maintained by
+// k_so_update from the pixels whose o changed; b is formed inside the b
+// prefix scan (k_scan_b). Iterations >= 1 are one serial FP64 scan + one
+// tiled gather/re-pick + a small scatter.
 //   k_avg_b       disc mean of o (31 row-span differences, dy ascending,
 //                 smoothing.cpp:43-63) fused with the correction
 //                 b = (avg - a o) - (1-a) d_prev (smoothing.cpp:91-99).
@@ -15,13 +19,15 @@
 //                 (smoothing.cpp:104-111) fused with the re-pick
 //                 (smoothing.cpp:114-146): argmin over integer candidates of
 //                 1/max(zncc, 1e-3) + (eta diff) diff, strict < (first min).
-//                 Candidate costs come from the WTA cost volume in FP32 with a
-//                 rigorous 4e-6 relative margin (error <= 7 ulp = 4.2e-7); when more than one
-//                 candidate lies within the margin of the minimum, those
-//                 candidates are re-scored in exact FP64 (zncc_exact), so the
-//                 pick equals the reference's. Without a volume (window != 11)
-//                 every candidate is scored exactly.
-// The mask is fixed, so the per-pixel disc count is computed once (k_disc_count).
+//                 Candidate costs come from the sweep's fp16 score windows in
+//                 FP32 with rigorous error bars; ambiguous pixels are settled
+//                 in FP64 or deferred to k_repick_exact (exact ZNCC), so the
+//                 pick equals the reference's.
+// Disc gathers: a block's psum tile (its 32 columns + the radius halo, its row
+// block + 16-row halo segments) is staged in shared memory column-major by
+// one 64/128-byte bulk copy (TMA) per column segment; a warp then reads 32
+// consecutive rows per access (conflict-free), and interior pixels use
+// compile-time offsets for the 31 disc rows.
 #include <limits.h>
 #include <math.h>
 
@@ -30,140 +36,42 @@
 
 #include "exact.cuh"
 #include "ss_internal.cuh"
+#include "tma.cuh"
+
+#include <cudaTypedefs.h>
+#include <stdio.h>
 
 namespace ssb {
 
-__global__ void k_refine_init(const float* __restrict__ disp, const uint8_t* __restrict__ valid,
-                              double* __restrict__ o, double* __restrict__ d, long n,
-                              long stride) {
-  const long f = blockIdx.y;
-  disp += f * stride;
-  valid += f * stride;
-  o += f * stride;
-  d += f * stride;
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
-       i += (long)gridDim.x * blockDim.x) {
-    const double x = valid[i] ? (double)disp[i] : 0.0;
-    o[i] = x;
-    d[i] = x;
-  }
+namespace {
+
+constexpr int kTC = 32;                 // tile columns; tile rows = one BT row block
+constexpr int kTWarps = 16;             // warp w owns tile columns w and w + 16
+constexpr int kPX = kTC / kTWarps;      // pixels per thread
+constexpr int kThreads = 32 * kTWarps;  // 512
+constexpr size_t kSmemCap = 200 * 1024; // larger tiles: read psum from global
+
+// Tile: the block's row block plus ceil(R/32) whole row blocks above and
+// below (one TMA box), psum columns [u0 - R, u0 + kTC + R].
+__host__ __device__ constexpr int tile_halo_blocks(int R) { return (R + 31) / 32; }
+__host__ __device__ constexpr int tile_nb(int R) { return 1 + 2 * tile_halo_blocks(R); }
+__host__ __device__ constexpr int tile_rows(int R) { return 32 * tile_nb(R); }
+__host__ __device__ constexpr int tile_cols(int R) { return kTC + 2 * R + 1; }
+template <typename T>
+__host__ __device__ constexpr size_t tile_bytes(int R) {
+  return (sizeof(T) * (size_t)tile_rows(R) * tile_cols(R) + 127) / 128 * 128;
 }
-
-void launch_refine_init(const float* disp, const uint8_t* valid, double* o, double* d,
-                        int W, int H, int frames, long stride, cudaStream_t s) {
-  const long n = (long)W * H;
-  if (n <= 0 || frames <= 0) return;
-  long blocks = (n + 255) / 256;
-  if (blocks > 2048) blocks = 2048;
-  k_refine_init<<<dim3((unsigned)blocks, frames), 256, 0, s>>>(disp, valid, o, d, n, stride);
-}
-
-// ---- disc sums of a masked field from its row prefixes (smoothing.cpp:43-63) ----
-//
-// The reference sums, for dy ascending, the span difference
-// psum[row][u1+1] - psum[row][u0] of each disc row. Both gathers run on a
-// 32 x 16 pixel tile whose psum rows/columns (plus the radius halo) are staged
-// in shared memory once, so the 2 (2R+1) reads per pixel are LDS, not L2
-// round trips. Summation order and operands are the reference's: bit-exact.
-
-constexpr int kTX = 32, kTY = 16, kBY = 16;  // tile = block = 32 x 16 pixels
+// score windows stashed as 8 u32 planes (2 fp16 scores each) x kThreads*kPX slots
+constexpr size_t kWinSmem = (size_t)(kWin / 2) * kThreads * kPX * sizeof(uint32_t);
+constexpr int kWinPlane = kThreads * kPX;
+// per-pixel fields of a tile staged by bulk copies: avg (double) or S_o, cnt,
+// o, wbase (int), mask (u8)
+constexpr int kTilePx = kTC * 32;
+constexpr size_t kPxSmem = (size_t)kTilePx * (8 + 4 + 4 + 4 + 1);
 
 template <typename T>
-struct PsumTile {
-  const T* t;         // smem [(kTY + 2R)][(kTX + 2R + 1)]
-  int pitch, u0, v0;  // psum column of t[.][0] is u0 - R; row of t[0] is v0 - R
-};
-
-__host__ __device__ inline int tile_pitch(int R) { return kTX + 2 * R + 1; }
-template <typename T>
-__host__ __device__ inline size_t tile_bytes(int R) {
-  return sizeof(T) * (size_t)(kTY + 2 * R) * tile_pitch(R) + sizeof(int) * (R + 1);
-}
-// re-pick: the tile, then each thread's 32-byte score window (16-byte aligned)
-__host__ __device__ inline size_t repick_smem_bytes(int R) {
-  return (tile_bytes<double>(R) + 15) / 16 * 16 + (size_t)kTX * kBY * kWin * sizeof(wscore_t);
-}
-
-__device__ __forceinline__ void cp_async_bytes(void* dst, const void* src, int bytes) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  if (bytes == 16)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-  else if (bytes == 8)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
-// Stage the BT-layout prefix rows [v0-R, v0+kTY+R) x columns [u0-R, u0+kTX+R]
-// of one frame with cp.async (every copy in flight at once; lanes walk rows,
-// contiguous within a BT row block). The caller may issue more copies, then
-// calls tile_wait(). RF > 0 makes the tile geometry compile-time.
-template <int RF, typename T>
-__device__ __forceinline__ PsumTile<T> load_tile_issue(const T* __restrict__ psumT, int W, int H,
-                                                       int Rr, const int* __restrict__ span_g,
-                                                       int*& span) {
-  extern __shared__ double tile_raw[];
-  T* tile_mem = reinterpret_cast<T*>(tile_raw);
-  const int R = RF > 0 ? RF : Rr;
-  const int pitch = tile_pitch(R);
-  const int rows = kTY + 2 * R;
-  const int u0 = blockIdx.x * kTX, v0 = blockIdx.y * kTY;
-  span = reinterpret_cast<int*>(tile_mem + (size_t)rows * pitch);
-  const int tid = threadIdx.y * kTX + threadIdx.x;
-  for (int k = tid; k <= R; k += kTX * kBY) span[k] = __ldg(span_g + k);
-  // Lanes walk rows (contiguous within a BT row block), warps walk columns.
-  if constexpr (RF > 0) {
-    constexpr int P = kTX + 2 * RF + 1, ROWS = kTY + 2 * RF;
-    constexpr int RCH = (ROWS + kTX - 1) / kTX, CCH = (P + kBY - 1) / kBY;
-#pragma unroll
-    for (int rc = 0; rc < RCH; ++rc) {
-      const int r = threadIdx.x + rc * kTX;
-      const int pr = v0 - RF + r;
-      const bool row_ok = r < ROWS && pr >= 0 && pr < H;
-      const T* src = psumT + ((long)(pr >> 5) * (W + 1)) * 32 + (pr & 31);
-      T* dst = tile_mem + r * P;
-#pragma unroll
-      for (int cc = 0; cc < CCH; ++cc) {
-        const int c = threadIdx.y + cc * kBY;
-        const int pc = u0 - RF + c;
-        if (r < ROWS && c < P) {
-          if (row_ok && pc >= 0 && pc <= W) cp_async_bytes(dst + c, src + pc * 32, sizeof(T));
-          else dst[c] = T(0);
-        }
-      }
-    }
-  } else {
-    for (int r = threadIdx.x; r < rows; r += kTX) {
-      const int pr = v0 - R + r;
-      const bool row_ok = pr >= 0 && pr < H;
-      const T* src = psumT + ((long)(pr >> 5) * (W + 1)) * 32 + (pr & 31);
-      T* dst = tile_mem + r * pitch;
-      for (int c = threadIdx.y; c < pitch; c += kBY) {
-        const int pc = u0 - R + c;
-        if (row_ok && pc >= 0 && pc <= W)
-          cp_async_bytes(dst + c, src + (long)pc * 32, sizeof(T));
-        else
-          dst[c] = T(0);
-      }
-    }
-  }
-  return PsumTile<T>{tile_mem, pitch, u0, v0};
-}
-
-__device__ __forceinline__ void tile_wait() {
-  cp_async_wait_all();
-  __syncthreads();
-}
-
-template <int RF, typename T>
-__device__ __forceinline__ PsumTile<T> load_tile(const T* __restrict__ psumT, int W, int H, int Rr,
-                                                 const int* __restrict__ span_g, int*& span) {
-  const PsumTile<T> P = load_tile_issue<RF>(psumT, W, H, Rr, span_g, span);
-  tile_wait();
-  return P;
+bool use_tile(int R, size_t extra) {
+  return tile_cols(R) <= 256 && tile_bytes<T>(R) + extra <= kSmemCap;  // TMA box <= 256
 }
 
 template <typename T>
@@ -177,23 +85,68 @@ __device__ __forceinline__ T tadd(T a, T b) {
   else return a + b;
 }
 
+// Row-prefix view: the shared-memory tile (element (row r, psum column c) at
+// (c - c0) * pitch + (r - r0)) or, when pitch == 0, the global BT prefix.
 template <typename T>
-__device__ __forceinline__ T disc_sum_tile(const PsumTile<T>& P, const int* span, int W, int H,
-                                           int u, int v, int R) {
+struct Tile {
+  const T* t;   // shared-memory tile (kept apart from `g` so loads stay LDS)
+  const T* g;   // global BT prefix of the frame
+  int pitch, c0, r0, CW;
+  __device__ __forceinline__ T at(int r, int c) const {
+    return pitch ? t[(c - c0) * pitch + (r - r0)]
+                 : __ldg(g + ((long)(r >> 5) * CW + c) * 32 + (r & 31));
+  }
+};
+
+// Thread 0 arms `bar` for the tile (one TMA tensor copy; out-of-range rows and
+// columns arrive as zeros) plus `extra_bytes` of copies the caller issues.
+// Callers wait with tile_wait().
+template <int RF, typename T>
+__device__ __forceinline__ Tile<T> tile_issue(T* sm, const T* psf, const CUtensorMap* map,
+                                              int W, int Rr, bool glob, uint64_t* bar,
+                                              unsigned extra_bytes = 0) {
+  const int R = RF > 0 ? RF : Rr;
+  const int u0 = blockIdx.x * kTC;
+  const int hb = tile_halo_blocks(R), rows = tile_rows(R), cols = tile_cols(R);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(bar, extra_bytes + (glob ? 0u : (unsigned)(rows * cols * sizeof(T))));
+    if (!glob) tma_load_4d(sm, map, 0, (int)blockIdx.y - hb, u0 - R, (int)blockIdx.z, bar);
+  }
+  __syncthreads();
+  Tile<T> tl;
+  tl.CW = W + 1;
+  tl.t = sm;
+  tl.g = psf;
+  tl.pitch = glob ? 0 : rows;
+  tl.c0 = u0 - R;
+  tl.r0 = ((int)blockIdx.y - hb) * 32;
+  return tl;
+}
+
+__device__ __forceinline__ void tile_wait(uint64_t* bar) {
+  mbar_wait(bar, 0);
+  __syncthreads();
+}
+
+// ---- disc sums of a masked field from its row prefixes (smoothing.cpp:43-63) ----
+// For dy ascending, the span difference psum[row][u1+1] - psum[row][u0]:
+// the reference's operands and order, so bit-exact.
+
+template <typename T>
+__device__ __forceinline__ T disc_sum_generic(const Tile<T>& P, const int* __restrict__ span,
+                                              int W, int H, int u, int v, int R) {
   const int lo = max(-R, -v), hi = min(R, H - 1 - v);
   T s = T(0);
   for (int dy = lo; dy <= hi; ++dy) {
-    const int sx = span[dy < 0 ? -dy : dy];
-    const int c0 = max(0, u - sx) - (P.u0 - R);
-    const int c1 = min(W - 1, u + sx) + 1 - (P.u0 - R);
-    const T* row = P.t + (v + dy - (P.v0 - R)) * P.pitch;
-    s = tadd(s, tsub(row[c1], row[c0]));
+    const int sx = __ldg(span + (dy < 0 ? -dy : dy));
+    const int c0 = max(0, u - sx), c1 = min(W - 1, u + sx) + 1;
+    s = tadd(s, tsub(P.at(v + dy, c1), P.at(v + dy, c0)));
   }
   return s;
 }
 
-// Compile-time radius: interior pixels (no clamping) read the tile at
-// immediate offsets from one base pointer — no index arithmetic per disc row.
 __host__ __device__ constexpr int isqrt_floor(int x) {
   int r = 0;
   while ((r + 1) * (r + 1) <= x) ++r;
@@ -202,9 +155,9 @@ __host__ __device__ constexpr int isqrt_floor(int x) {
 
 template <typename T, int R, int DY>
 __device__ __forceinline__ T span_diff(const T* q) {
-  constexpr int P = kTX + 2 * R + 1;
+  constexpr int P = tile_rows(R);
   constexpr int SX = isqrt_floor(R * R - DY * DY);
-  return tsub(q[DY * P + SX + 1], q[DY * P - SX]);
+  return tsub(q[(SX + 1) * P + DY], q[-SX * P + DY]);
 }
 
 template <typename T, int R, int... I>
@@ -214,103 +167,280 @@ __device__ __forceinline__ T disc_sum_fixed(const T* q, std::integer_sequence<in
   return s;
 }
 
-template <int R, typename T>
-__device__ __forceinline__ T disc_sum_any(const PsumTile<T>& P, const int* span, int W, int H,
+// Interior pixels with a compile-time radius read the tile at immediate
+// offsets from one base pointer.
+template <int RF, typename T>
+__device__ __forceinline__ T disc_sum_any(const Tile<T>& P, const int* span, int W, int H,
                                           int u, int v, int Rr) {
-  if constexpr (R > 0) {
-    if (u >= R && u + R <= W - 1 && v >= R && v + R <= H - 1) {
-      const T* q = P.t + (v - P.v0 + R) * P.pitch + (u - P.u0 + R);
-      return disc_sum_fixed<T, R>(q, std::make_integer_sequence<int, 2 * R + 1>{});
+  if constexpr (RF > 0) {
+    if (u >= RF && u + RF <= W - 1 && v >= RF && v + RF <= H - 1) {
+      const T* q = P.t + (u - P.c0) * tile_rows(RF) + (v - P.r0);
+      return disc_sum_fixed<T, RF>(q, std::make_integer_sequence<int, 2 * RF + 1>{});
     }
   }
-  return disc_sum_tile(P, span, W, H, u, v, Rr);
+  return disc_sum_generic(P, span, W, H, u, v, Rr);
 }
+
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+// Tensor map for a launch's prefix tiles; false (global reads) when the tile
+// does not fit or the driver rejects the map (reported once on stderr).
+template <typename T>
+bool psum_map(CUtensorMap* m, const T* psumT, const RefineArgs& a, int frames, bool tile) {
+  *m = CUtensorMap{};
+  if (!tile) return false;
+  if (make_psum_tmap(m, psumT, std::is_same<T, double>::value, a.g.W, a.g.H, frames,
+                     tile_nb(a.radius), tile_cols(a.radius)))
+    return true;
+  static bool warned = false;
+  if (!warned) {
+    fprintf(stderr, "stereoscan-b200: TMA tensor map rejected; disc gathers read global memory\n");
+    warned = true;
+  }
+  return false;
+}
+
+}  // namespace
+
+bool make_psum_tmap(CUtensorMap* map, const void* base, bool is_double, int W, int H, int frames,
+                    int nb, int cols) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t es = is_double ? 8 : 4;
+  const cuuint64_t RB = (H + 31) / 32, CW = W + 1;
+  const cuuint64_t dims[4] = {32, RB, CW, (cuuint64_t)frames};
+  const cuuint64_t strides[3] = {CW * 32 * es, 32 * es, RB * CW * 32 * es};
+  const cuuint32_t box[4] = {32, (cuuint32_t)nb, (cuuint32_t)cols, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return encode(map, is_double ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_INT32,
+                4, const_cast<void*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// ---------------- normal <-> BT ----------------
+
+__global__ void __launch_bounds__(256)
+    k_refine_init(const float* __restrict__ disp, const uint8_t* __restrict__ valid,
+                  uint8_t* __restrict__ mT, double* __restrict__ oT, double* __restrict__ dT,
+                  int W, int H, long stride, long bs) {
+  __shared__ float td[32][33];
+  __shared__ uint8_t tv[32][33];
+  const long f = blockIdx.z;
+  const int u0 = blockIdx.x * 32, rb = blockIdx.y, v0 = rb * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int v = v0 + r, c = u0 + threadIdx.x;
+    float x = 0.f;
+    uint8_t m = 0;
+    if (v < H && c < W) {
+      const long i = f * stride + (long)v * W + c;
+      m = valid[i] ? 1 : 0;
+      x = disp[i];
+    }
+    td[r][threadIdx.x] = x;
+    tv[r][threadIdx.x] = m;
+  }
+  __syncthreads();
+  for (int cc = threadIdx.y; cc < 32; cc += 8) {
+    const int c = u0 + cc;
+    if (c >= W) continue;
+    const long bi = f * bs + ((long)rb * W + c) * 32 + threadIdx.x;
+    const uint8_t m = tv[threadIdx.x][cc];
+    const double x = m ? (double)td[threadIdx.x][cc] : 0.0;  // rows past H: m = 0
+    mT[bi] = m;
+    oT[bi] = x;
+    dT[bi] = x;
+  }
+}
+
+void launch_refine_init(const float* disp, const uint8_t* valid, uint8_t* mT, double* oT,
+                        double* dT, int W, int H, int frames, long stride, long bs,
+                        cudaStream_t s) {
+  if (W <= 0 || H <= 0 || frames <= 0) return;
+  k_refine_init<<<dim3((W + 31) / 32, (H + 31) / 32, frames), dim3(32, 8), 0, s>>>(
+      disp, valid, mT, oT, dT, W, H, stride, bs);
+}
+
+__global__ void __launch_bounds__(256)
+    k_refine_out(const double* __restrict__ dT, const uint8_t* __restrict__ valid,
+                 const float* __restrict__ din, float* __restrict__ dout, int W, int H,
+                 long stride, long bs) {
+  __shared__ float td[32][33];
+  const long f = blockIdx.z;
+  const int u0 = blockIdx.x * 32, rb = blockIdx.y, v0 = rb * 32;
+  for (int cc = threadIdx.y; cc < 32; cc += 8) {
+    const int c = u0 + cc;
+    td[cc][threadIdx.x] = c < W ? (float)dT[f * bs + ((long)rb * W + c) * 32 + threadIdx.x] : 0.f;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int v = v0 + r, c = u0 + threadIdx.x;
+    if (v < H && c < W) {
+      const long i = f * stride + (long)v * W + c;
+      dout[i] = valid[i] ? td[threadIdx.x][r] : din[i];
+    }
+  }
+}
+
+void launch_refine_out(const double* dT, const uint8_t* valid, const float* din, float* dout,
+                       int W, int H, int frames, long stride, cudaStream_t s) {
+  if (W <= 0 || H <= 0 || frames <= 0) return;
+  k_refine_out<<<dim3((W + 31) / 32, (H + 31) / 32, frames), dim3(32, 8), 0, s>>>(
+      dT, valid, din, dout, W, H, stride, bt_frame(W, H, 0));
+}
+
+// RefineTrace rows (one frame): discrete = valid ? o : 0, smooth = d.
+__global__ void __launch_bounds__(256)
+    k_trace_rows(const int* __restrict__ oT, const double* __restrict__ dT,
+                 const uint8_t* __restrict__ valid, double* __restrict__ to,
+                 double* __restrict__ td_out, int W, int H) {
+  __shared__ double to_s[32][33], td_s[32][33];
+  const int u0 = blockIdx.x * 32, rb = blockIdx.y, v0 = rb * 32;
+  for (int cc = threadIdx.y; cc < 32; cc += 8) {
+    const int c = u0 + cc;
+    if (c < W) {
+      const long bi = ((long)rb * W + c) * 32 + threadIdx.x;
+      to_s[cc][threadIdx.x] = (double)oT[bi];
+      td_s[cc][threadIdx.x] = dT[bi];
+    }
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int v = v0 + r, c = u0 + threadIdx.x;
+    if (v < H && c < W) {
+      const long i = (long)v * W + c;
+      if (to) to[i] = valid[i] ? to_s[threadIdx.x][r] : 0.0;
+      if (td_out) td_out[i] = td_s[threadIdx.x][r];
+    }
+  }
+}
+
+void launch_trace_rows(const int* oT, const double* dT, const uint8_t* valid, double* trace_o,
+                       double* trace_d, int W, int H, cudaStream_t s) {
+  if (W <= 0 || H <= 0) return;
+  k_trace_rows<<<dim3((W + 31) / 32, (H + 31) / 32), dim3(32, 8), 0, s>>>(oT, dT, valid, trace_o,
+                                                                         trace_d, W, H);
+}
+
+// ---------------- tiled disc gathers ----------------
 
 // Exact integer disc sums (disc counts, S_o) from an int BT prefix.
 template <int RF>
-__global__ void __launch_bounds__(kTX * kBY)
-    k_disc_isum(const uint8_t* __restrict__ valid, const int* __restrict__ ipsumT,
-                int* __restrict__ out, RefineArgs a, long stride) {
+__global__ void __launch_bounds__(kThreads)
+    k_disc_isum(const uint8_t* __restrict__ mT, const int* __restrict__ ipsumT,
+                int* __restrict__ outT, RefineArgs a, const __grid_constant__ CUtensorMap map,
+                int glob) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar;
   const long f = blockIdx.z;
   const int W = a.g.W, H = a.g.H, R = a.radius;
-  int* span;
-  const PsumTile<int> P = load_tile<RF>(ipsumT + f * bt_frame(W, H, 1), W, H, R, a.span, span);
-  const int u = blockIdx.x * kTX + threadIdx.x;
+  const long bs = bt_frame(W, H, 0);
+  const Tile<int> P = tile_issue<RF>(reinterpret_cast<int*>(smem), ipsumT + f * bt_frame(W, H, 1),
+                                     &map, W, R, glob, &bar);
+  tile_wait(&bar);
+  const int v = blockIdx.y * 32 + threadIdx.x;
 #pragma unroll
-  for (int rr = 0; rr < kTY / kBY; ++rr) {
-    const int v = blockIdx.y * kTY + threadIdx.y + rr * kBY;
+  for (int k = 0; k < kPX; ++k) {
+    const int u = blockIdx.x * kTC + threadIdx.y + kTWarps * k;
     if (u >= W || v >= H) continue;
-    const long i = f * stride + (long)v * W + u;
-    out[i] = valid[i] ? disc_sum_any<RF>(P, span, W, H, u, v, R) : 0;
+    const long bi = f * bs + bt_index(W, v, u);
+    outT[bi] = mT[bi] ? disc_sum_any<RF>(P, a.span, W, H, u, v, R) : 0;
   }
 }
 
-void launch_disc_isum(const uint8_t* valid, const int* ipsumT, int* out, const RefineArgs& a,
-                      int frames, long stride, cudaStream_t s) {
+void launch_disc_isum(const uint8_t* mT, const int* ipsumT, int* outT, const RefineArgs& a,
+                      int frames, cudaStream_t s) {
   if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
-  const size_t smem = tile_bytes<int>(a.radius);
-  dim3 bl(kTX, kBY);
-  dim3 grid((a.g.W + kTX - 1) / kTX, (a.g.H + kTY - 1) / kTY, frames);
-  if (a.radius == 15) {
-    k_disc_isum<15><<<grid, bl, smem, s>>>(valid, ipsumT, out, a, stride);
+  CUtensorMap map;
+  const bool tile = psum_map(&map, ipsumT, a, frames, use_tile<int>(a.radius, 0));
+  const size_t smem = tile ? tile_bytes<int>(a.radius) : 0;
+  dim3 grid((a.g.W + kTC - 1) / kTC, (a.g.H + 31) / 32, frames);
+  dim3 bl(32, kTWarps);
+  if (a.radius == 15 && tile) {
+    k_disc_isum<15><<<grid, bl, smem, s>>>(mT, ipsumT, outT, a, map, 0);
   } else {
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-      cudaFuncSetAttribute(k_disc_isum<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      configured = smem;
-    }
-    k_disc_isum<0><<<grid, bl, smem, s>>>(valid, ipsumT, out, a, stride);
+    set_smem(k_disc_isum<0>, smem);
+    k_disc_isum<0><<<grid, bl, smem, s>>>(mT, ipsumT, outT, a, map, tile ? 0 : 1);
   }
 }
 
 template <int RF>
-__global__ void __launch_bounds__(kTX * kBY)
-    k_avg_b(const double* __restrict__ psumT, const uint8_t* __restrict__ valid,
-            const int* __restrict__ cnt, const double* __restrict__ o,
-            const double* __restrict__ d, double* __restrict__ avg, double* __restrict__ b,
-            RefineArgs a, long stride) {
+__global__ void __launch_bounds__(kThreads)
+    k_avg_b(const double* __restrict__ psumT, const uint8_t* __restrict__ mT,
+            const int* __restrict__ cntT, const double* __restrict__ oT,
+            const double* __restrict__ dT, double* __restrict__ avgT, double* __restrict__ bT,
+            RefineArgs a, const __grid_constant__ CUtensorMap map, int glob) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar;
   const long f = blockIdx.z;
   const int W = a.g.W, H = a.g.H, R = a.radius;
-  int* span;
-  const PsumTile<double> T = load_tile<RF>(psumT + f * bt_frame(W, H, 1), W, H, R, a.span, span);
-  const int u = blockIdx.x * kTX + threadIdx.x;
+  const long bs = bt_frame(W, H, 0);
+  const Tile<double> P = tile_issue<RF>(reinterpret_cast<double*>(smem),
+                                        psumT + f * bt_frame(W, H, 1), &map, W, R, glob, &bar);
+  tile_wait(&bar);
+  const int v = blockIdx.y * 32 + threadIdx.x;
 #pragma unroll
-  for (int rr = 0; rr < kTY / kBY; ++rr) {
-    const int v = blockIdx.y * kTY + threadIdx.y + rr * kBY;
+  for (int k = 0; k < kPX; ++k) {
+    const int u = blockIdx.x * kTC + threadIdx.y + kTWarps * k;
     if (u >= W || v >= H) continue;
-    const long i = f * stride + (long)v * W + u;
-    if (!valid[i]) continue;
-    const double s = disc_sum_any<RF>(T, span, W, H, u, v, R);
-    const double av = __ddiv_rn(s, (double)cnt[i]);
-    avg[i] = av;
+    const long bi = f * bs + bt_index(W, v, u);
+    if (!mT[bi]) continue;
+    const double s = disc_sum_any<RF>(P, a.span, W, H, u, v, R);
+    const double av = __ddiv_rn(s, (double)cntT[bi]);
+    avgT[bi] = av;
     // averaged - alpha * discrete - (1 - alpha) * smooth, left to right.
-    b[i] = __dsub_rn(__dsub_rn(av, __dmul_rn(a.alpha, o[i])), __dmul_rn(a.one_minus_alpha, d[i]));
+    bT[bi] = __dsub_rn(__dsub_rn(av, __dmul_rn(a.alpha, oT[bi])),
+                       __dmul_rn(a.one_minus_alpha, dT[bi]));
   }
 }
 
-void launch_avg_b(const double* psumT, const uint8_t* valid, const int* cnt, const double* o,
-                  const double* d, double* avg, double* b, const RefineArgs& a, int frames,
-                  long stride, cudaStream_t s) {
+void launch_avg_b(const double* psumT, const uint8_t* mT, const int* cntT, const double* oT,
+                  const double* dT, double* avgT, double* bT, const RefineArgs& a, int frames,
+                  cudaStream_t s) {
   if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
-  const size_t smem = tile_bytes<double>(a.radius);
-  dim3 bl(kTX, kBY);
-  dim3 grid((a.g.W + kTX - 1) / kTX, (a.g.H + kTY - 1) / kTY, frames);
-  if (a.radius == 15) {
-    k_avg_b<15><<<grid, bl, smem, s>>>(psumT, valid, cnt, o, d, avg, b, a, stride);
+  CUtensorMap map;
+  const bool tile = psum_map(&map, psumT, a, frames, use_tile<double>(a.radius, 0));
+  const size_t smem = tile ? tile_bytes<double>(a.radius) : 0;
+  dim3 grid((a.g.W + kTC - 1) / kTC, (a.g.H + 31) / 32, frames);
+  dim3 bl(32, kTWarps);
+  if (a.radius == 15 && tile) {
+    set_smem(k_avg_b<15>, smem);
+    k_avg_b<15><<<grid, bl, smem, s>>>(psumT, mT, cntT, oT, dT, avgT, bT, a, map, 0);
   } else {
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-      cudaFuncSetAttribute(k_avg_b<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      configured = smem;
-    }
-    k_avg_b<0><<<grid, bl, smem, s>>>(psumT, valid, cnt, o, d, avg, b, a, stride);
+    set_smem(k_avg_b<0>, smem);
+    k_avg_b<0><<<grid, bl, smem, s>>>(psumT, mT, cntT, oT, dT, avgT, bT, a, map, tile ? 0 : 1);
   }
 }
 
-__device__ __forceinline__ double exact_cost(const uint8_t* L, const uint8_t* R, int W,
-                                             int u, int v, int c, bool fits, int half,
-                                             double dval, double eta) {
+// ---------------- re-pick ----------------
+
+namespace {
+
+// A thread's window: 16 fp16 match costs (m_code) in 8 u32 planes of shared memory.
+struct WinView {
+  const uint32_t* p;  // plane 0 word of this pixel; plane j at p[j * kWinPlane]
+  __device__ __forceinline__ float mcost(int k) const {  // k in [0, kWin)
+    const uint32_t w = p[(k >> 1) * kWinPlane];
+    return __half2float(__ushort_as_half((unsigned short)((k & 1) ? (w >> 16) : (w & 0xFFFFu))));
+  }
+};
+
+__device__ __forceinline__ double exact_cost(const uint8_t* L, const uint8_t* R, int W, int u,
+                                             int v, int c, bool fits, int half, double dval,
+                                             double eta) {
   double match = __ddiv_rn(1.0, kZnccEps);
   const int ru = u - c;
   if (fits && ru >= half && ru < W - half) {
@@ -324,18 +454,18 @@ __device__ __forceinline__ double exact_cost(const uint8_t* L, const uint8_t* R,
 constexpr int kMaxCand = 2 * kRefineR + 1;
 
 // FP64 version for the rare paths: exact E (reference expression) and exact M
-// when the score is undefined/clamped; err is the FP16-derived M uncertainty.
+// when the score is undefined/clamped (code 1000); err is the fp16 M's
+// uncertainty.
 __device__ __forceinline__ void repick_cost_d(const RefineArgs& a, int u, int c, double dv,
-                                              const wscore_t* wp, int W, int half, double& cost,
-                                              double& err) {
+                                              const WinView& wv, int wb, int W, int half,
+                                              double& cost, double& err) {
   constexpr double kErrM = 6e-4;
   double m = 1000.0;
   err = 0.0;
   const int ru = u - c;
   if (ru >= half && ru < W - half) {
-    const float sc = __half2float(wp[c]);
-    if (!isnan(sc) && sc >= 0.99e-3f) {
-      const float mf = 1.f / fmaxf(sc, 1e-3f);
+    const float mf = wv.mcost(c - wb);
+    if (mf != 1000.f) {
       m = (double)mf;
       err = kErrM * mf;
     }
@@ -357,23 +487,23 @@ __device__ __forceinline__ int defer_pixel(Deferred* defer, unsigned* defer_coun
 // Re-pick of one pixel (smoothing.cpp:119-144) given its smoothed d.
 // Returns the new o, or INT_MIN when the pixel is deferred to the exact kernel.
 //
-// Filter error budget: window scores are fp16 copies of
-// the FP32 sweep score s_f (|s_f - s| <= 5 ulp_f32), so |s16 - s| <= 2^-11 |s|
-// + 3e-8; M = 1/max(s, 1e-3) then carries <= 5.3e-4 relative error and the
-// float cost M + (eta diff) diff <= 5.4e-4. Candidates within 2.5e-3 of the
-// float minimum are re-scored exactly; a single survivor is provably the
+// Filter error budget: window entries are fp16 match
+// costs M16 from the FP32 sweep score s_f (|s_f - s| <= 5 ulp_f32) with
+// |M16 - M| <= 5.01e-4 M (m_code), and the float cost M16 + (eta diff) diff
+// adds FP32 rounding. Candidates within the error bars of the float minimum
+// are re-scored in FP64 / exactly; a single survivor is provably the
 // reference's argmin.
 __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double dv,
-                                      const uint8_t* L, const uint8_t* R,
-                                      const wscore_t* win_row, int wb, long pix,
-                                      Deferred* defer, unsigned* defer_count) {
+                                      const uint8_t* L, const uint8_t* R, bool has_win,
+                                      const WinView& wv, int wb, long pix, Deferred* defer,
+                                      unsigned* defer_count) {
   const int W = a.g.W, H = a.g.H, half = a.g.half;
   const int c_lo = max((int)ceil(__dsub_rn(dv, (double)kRefineR)), (int)ceil(a.lo));
   const int c_hi = min((int)floor(__dadd_rn(dv, (double)kRefineR)), (int)floor(a.hi));
   if (c_lo > c_hi) return INT_MIN;  // unreachable for a clamped d; mirrors `found`
   const bool fits = u >= half && u < W - half && v >= half && v < H - half;
 
-  if (win_row == nullptr) {
+  if (!has_win) {
     // Generic window size: every candidate in exact FP64 (no score windows).
     double best_cost = 0.0;
     int best = c_lo;
@@ -404,24 +534,31 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
   }
   int best = c_lo;
   if (c_lo >= wb && c_hi <= wb + kWin - 1) {
-    // Common path, FP32. cost_f(c) = M_f + E_f with |cost_f - cost| <=
-    // eps cost + errE, eps = 6e-4 (fp16 score -> M) + 1.2e-7 (FP32 sum),
+    // Common path, FP32. cost_f(c) = M16 + E_f with |cost_f - cost| <=
+    // eps cost + errE, eps = 6e-4 (fp16 M) + 1.2e-7 (FP32 sum),
     // errE from the FP32 copy of d. The first minimum is certified when the
     // runner-up's lower bound stays above the minimum's upper bound.
-    const wscore_t* wp = win_row - wb;  // wp[c]: score of candidate c
     const float dv_f = (float)dv;
     const float delta = fabsf(dv_f) * 1.2e-7f;  // |dv_f - d|, and FP32 rounding of c - dv_f
     constexpr float kEps = 6e-4f + 1.2e-7f;
     // (with eta < 0, E < 0 and the M error, relative to M, is bounded via |E| <= 25|eta|)
-    const float errE = fabsf(a.eta_f) * (11.f * delta + 25.f * 4e-7f + (a.eta_f < 0.f ? 25.f * kEps : 0.f));
+    const float errE =
+        fabsf(a.eta_f) * (11.f * delta + 25.f * 4e-7f + (a.eta_f < 0.f ? 25.f * kEps : 0.f));
+    // The <= 11 candidates are entries off .. off+10 of the window: 6 words
+    // from the planes, then one byte-permute per candidate.
+    const int off = c_lo - wb, par = off & 1, w0 = off >> 1;
+    uint32_t wd[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) wd[i] = wv.p[min(w0 + i, kWin / 2 - 1) * kWinPlane];
+    const unsigned sel_e = par ? 0x3232u : 0x1010u, sel_o = par ? 0x5454u : 0x3232u;
     float best_cost = INFINITY, second = INFINITY;
     float cf = (float)c_lo;
 #pragma unroll
     for (int k = 0; k < kMaxCand; ++k) {
       if (c_lo + k <= c_hi) {
-        const float sc = __half2float(wp[c_lo + k]);  // NaN: undefined (incl. ru outside)
-        const bool appr = sc >= 0.99e-3f;             // below: certainly clamped to 1000
-        const float m = appr ? __fdividef(1.f, fmaxf(sc, 1e-3f)) : 1000.f;
+        const uint32_t hw = (k & 1) ? __byte_perm(wd[k >> 1], wd[(k + 1) >> 1], sel_o)
+                                    : __byte_perm(wd[k >> 1], 0u, sel_e);
+        const float m = __half2float(__ushort_as_half((unsigned short)(hw & 0xFFFFu)));
         const float df = cf - dv_f;
         const float cost = m + a.eta_f * df * df;
         second = fminf(second, fmaxf(best_cost, cost));
@@ -438,7 +575,7 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
     double bc = INFINITY, up = INFINITY;
     for (int c = c_lo; c <= c_hi; ++c) {
       double cost, err;
-      repick_cost_d(a, u, c, dv, wp, W, half, cost, err);
+      repick_cost_d(a, u, c, dv, wv, wb, W, half, cost, err);
       if (cost < bc) {
         bc = cost;
         best = c;
@@ -448,7 +585,7 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
     int mask = 0, approx = 0;
     for (int c = c_lo; c <= c_hi; ++c) {
       double cost, err;
-      repick_cost_d(a, u, c, dv, wp, W, half, cost, err);
+      repick_cost_d(a, u, c, dv, wv, wb, W, half, cost, err);
       if (cost - err <= up) {
         mask |= 1 << (c - c_lo);
         if (err != 0.0) approx |= 1 << (c - c_lo);
@@ -463,97 +600,129 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
   return defer_pixel(defer, defer_count, pix, c_lo, (1 << (c_hi - c_lo + 1)) - 1, dv);
 }
 
+}  // namespace
+
+// Block = 32 rows (lanes) x 32 columns (16 warps x 2). Everything a block
+// needs is issued up front — the psum tile (bulk copies) and, per pixel, the
+// scalars and the 32-byte score window (coalesced: a warp's 32 pixels are one
+// 1 KB line run) — and consumed after one barrier.
 template <int RF, bool USE_SO>
-__global__ void __launch_bounds__(kTX * kBY)
-    k_d_repick(const double* __restrict__ psumT, const uint8_t* __restrict__ valid,
-               const int* __restrict__ cnt, const double* __restrict__ avg,
-               const int* __restrict__ so, double* __restrict__ d, int* __restrict__ o,
+__global__ void __launch_bounds__(kThreads, 2)
+    k_d_repick(const double* __restrict__ psumT, const uint8_t* __restrict__ mT,
+               const int* __restrict__ cntT, const double* __restrict__ avgT,
+               const int* __restrict__ soT, double* __restrict__ dT, int* __restrict__ oT,
                const uint8_t* __restrict__ lgray, const uint8_t* __restrict__ rgray,
                const wscore_t* __restrict__ win, const int* __restrict__ wbase,
                int2* __restrict__ chg, unsigned* __restrict__ chg_count,
                Deferred* __restrict__ defer, unsigned* __restrict__ defer_count, RefineArgs a,
-               long stride, long gray_stride) {
+               long gray_stride, const __grid_constant__ CUtensorMap map, int glob) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar;
   const long f = blockIdx.z;
-  const int W = a.g.W, H = a.g.H, R = a.radius;
-  const int u = blockIdx.x * kTX + threadIdx.x;
-  const int v = blockIdx.y * kTY + threadIdx.y;
-  const long pix = (long)v * W + u;
-  const long i = f * stride + pix;
-  const bool inside = u < W && v < H;
-  // 1. issue every global->shared copy (prefix tile + this pixel's window)
-  int* span;
-  const PsumTile<double> T =
-      load_tile_issue<RF>(psumT + f * bt_frame(W, H, 1), W, H, R, a.span, span);
-  extern __shared__ double tile_raw[];
-  wscore_t* swin = reinterpret_cast<wscore_t*>(reinterpret_cast<unsigned char*>(tile_raw) +
-                                               (tile_bytes<double>(R) + 15) / 16 * 16) +
-                   (threadIdx.y * kTX + threadIdx.x) * kWin;
-  if (win && inside) {
-    cp_async_bytes(swin, win + i * kWin, 16);
-    cp_async_bytes(swin + 8, win + i * kWin + 8, 16);
-  }
-  // 2. per-pixel scalars while the copies fly
-  const bool act = inside && valid[i];
-  int cn = 1, sv = 0, ol = 0, wb = kNoWin;
-  double av = 0.0;
-  if (act) {
-    cn = __ldg(cnt + i);
-    if (USE_SO) {
-      sv = __ldg(so + i);
-      ol = o[i];
-    } else {
-      av = __ldg(avg + i);
+  const int W = a.g.W, H = a.g.H, R = RF > 0 ? RF : a.radius;
+  const long bs = bt_frame(W, H, 0);
+  const int lane = threadIdx.x, warp = threadIdx.y;
+  const int tid = warp * 32 + lane;
+  const int v = blockIdx.y * 32 + lane;
+  const int u0 = blockIdx.x * kTC, rb = blockIdx.y;
+  const int ncols = min(kTC, W - u0);
+  const unsigned npx = ncols * 32;
+  const long e0 = f * bs + ((long)rb * W + u0) * 32;  // first BT entry of the tile
+  const size_t tb = glob ? 0 : tile_bytes<double>(R);
+  uint32_t* planes = reinterpret_cast<uint32_t*>(smem + tb);
+  double* s_av = reinterpret_cast<double*>(smem + tb + kWinSmem);
+  int* s_so = reinterpret_cast<int*>(s_av);
+  int* s_cnt = reinterpret_cast<int*>(s_av + kTilePx);
+  int* s_o = s_cnt + kTilePx;
+  int* s_wb = s_o + kTilePx;
+  uint8_t* s_m = reinterpret_cast<uint8_t*>(s_wb + kTilePx);
+  // windows + wbase, S_o + o (or avg), cnt, mask
+  const unsigned extra = (win ? (kWin / 2) * npx * 4 + npx * 4 : 0) + npx * 8 + npx * 4 + npx;
+  const Tile<double> P = tile_issue<RF>(reinterpret_cast<double*>(smem),
+                                        psumT + f * bt_frame(W, H, 1), &map, W, R, glob, &bar,
+                                        extra);
+  if (tid == 0) {
+    // the tile's per-pixel fields: contiguous BT ranges of npx entries
+    if (win) {
+      const uint32_t* wsrc = reinterpret_cast<const uint32_t*>(win) + f * bs * (kWin / 2);
+#pragma unroll 1
+      for (int j = 0; j < kWin / 2; ++j)
+        bulk_g2s(planes + j * kWinPlane, wsrc + (((long)rb * (kWin / 2) + j) * W + u0) * 32,
+                 npx * 4, &bar);
+      bulk_g2s(s_wb, wbase + e0, npx * 4, &bar);
     }
-    if (win) wb = __ldg(wbase + i);
+    if (USE_SO) {
+      bulk_g2s(s_so, soT + e0, npx * 4, &bar);
+      bulk_g2s(s_o, oT + e0, npx * 4, &bar);
+    } else {
+      bulk_g2s(s_av, avgT + e0, npx * 8, &bar);
+    }
+    bulk_g2s(s_cnt, cntT + e0, npx * 4, &bar);
+    bulk_g2s(s_m, mT + e0, npx, &bar);
   }
-  tile_wait();
-  if (!act) return;
-  const double s = disc_sum_any<RF>(T, span, W, H, u, v, R);
-  const double c = (double)cn;
-  const double bav = __ddiv_rn(s, c);
-  // avg = s_o / c: with integer o the reference's double disc sum is exact,
-  // so the integer sum reproduces it bit for bit.
-  const double a_o = USE_SO ? __ddiv_rn((double)sv, c) : av;
-  const double x = __dsub_rn(a_o, bav);
-  const double dv = x < a.lo ? a.lo : (a.hi < x ? a.hi : x);  // std::clamp
-  d[i] = dv;
-  const int best = repick(a, u, v, dv, lgray + f * gray_stride, rgray + f * gray_stride,
-                          win ? swin : nullptr, wb, pix, defer + f * stride, defer_count + f);
-  if (best != INT_MIN) {
-    if (USE_SO && best != ol)
-      chg[f * stride + atomicAdd(chg_count + f, 1u)] = make_int2((int)pix, best - ol);
-    o[i] = best;
+  tile_wait(&bar);
+  const uint8_t* L = lgray + f * gray_stride;
+  const uint8_t* Rg = rgray + f * gray_stride;
+#pragma unroll 1
+  for (int k = 0; k < kPX; ++k) {
+    const int t = warp + kTWarps * k;  // tile column
+    const int slot = t * 32 + lane;
+    if (t >= ncols || v >= H || !s_m[slot]) continue;
+    const int u = u0 + t;
+    const long px = ((long)rb * W + u) * 32 + lane;  // frame-local BT index
+    const long bi = f * bs + px;
+    const int cnk = s_cnt[slot];
+    const int olk = USE_SO ? s_o[slot] : 0;
+    const int wbk = win ? s_wb[slot] : kNoWin;
+    const WinView wv{planes + slot};
+    const double s = disc_sum_any<RF>(P, a.span, W, H, u, v, R);
+    const double c = (double)cnk;
+    const double bav = __ddiv_rn(s, c);
+    // avg = s_o / c: with integer o the reference's double disc sum is exact,
+    // so the integer sum reproduces it bit for bit.
+    const double a_o = USE_SO ? __ddiv_rn((double)s_so[slot], c) : s_av[slot];
+    const double x = __dsub_rn(a_o, bav);
+    const double dv = x < a.lo ? a.lo : (a.hi < x ? a.hi : x);  // std::clamp
+    dT[bi] = dv;
+    const int best = repick(a, u, v, dv, L, Rg, win != nullptr, wv, wbk, px, defer + f * bs,
+                            defer_count + f);
+    if (best != INT_MIN) {
+      if (USE_SO && best != olk)
+        chg[f * bs + atomicAdd(chg_count + f, 1u)] = make_int2((int)px, best - olk);
+      oT[bi] = best;
+    }
   }
 }
 
-void launch_d_repick(const double* psumT, const uint8_t* valid, const int* cnt,
-                     const double* avg, const int* so, double* d, int* o,
+void launch_d_repick(const double* psumT, const uint8_t* mT, const int* cntT,
+                     const double* avgT, const int* soT, double* dT, int* oT,
                      const uint8_t* lgray, const uint8_t* rgray, const wscore_t* win,
                      const int* wbase, int2* chg, unsigned* chg_count, Deferred* defer,
-                     unsigned* defer_count, const RefineArgs& a, int frames, long stride,
-                     long gray_stride, unsigned long long* counters, cudaStream_t s) {
-  (void)counters;
+                     unsigned* defer_count, const RefineArgs& a, int frames, long gray_stride,
+                     cudaStream_t s) {
   if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
-  const size_t smem = repick_smem_bytes(a.radius);
-  dim3 bl(kTX, kBY);
-  dim3 grid((a.g.W + kTX - 1) / kTX, (a.g.H + kTY - 1) / kTY, frames);
+  CUtensorMap map;
+  const bool tile = psum_map(&map, psumT, a, frames, use_tile<double>(a.radius, kWinSmem + kPxSmem));
+  const size_t smem = (tile ? tile_bytes<double>(a.radius) : 0) + kWinSmem + kPxSmem;
+  dim3 grid((a.g.W + kTC - 1) / kTC, (a.g.H + 31) / 32, frames);
+  dim3 bl(32, kTWarps);
 #define SS_REPICK_ARGS                                                                        \
-  psumT, valid, cnt, avg, so, d, o, lgray, rgray, win, wbase, chg, chg_count, defer,          \
-      defer_count, a, stride, gray_stride
-  if (a.radius == 15) {
-    if (avg) k_d_repick<15, false><<<grid, bl, smem, s>>>(SS_REPICK_ARGS);
-    else k_d_repick<15, true><<<grid, bl, smem, s>>>(SS_REPICK_ARGS);
-  } else {
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-      cudaFuncSetAttribute(k_d_repick<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      cudaFuncSetAttribute(k_d_repick<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      configured = smem;
+  psumT, mT, cntT, avgT, soT, dT, oT, lgray, rgray, win, wbase, chg, chg_count, defer,        \
+      defer_count, a, gray_stride
+  if (a.radius == 15 && tile) {
+    static bool configured = false;
+    if (!configured) {
+      set_smem(k_d_repick<15, false>, smem);
+      set_smem(k_d_repick<15, true>, smem);
+      configured = true;
     }
-    if (avg) k_d_repick<0, false><<<grid, bl, smem, s>>>(SS_REPICK_ARGS);
-    else k_d_repick<0, true><<<grid, bl, smem, s>>>(SS_REPICK_ARGS);
+    if (avgT) k_d_repick<15, false><<<grid, bl, smem, s>>>(SS_REPICK_ARGS, map, 0);
+    else k_d_repick<15, true><<<grid, bl, smem, s>>>(SS_REPICK_ARGS, map, 0);
+  } else {
+    set_smem(k_d_repick<0, false>, smem);
+    set_smem(k_d_repick<0, true>, smem);
+    if (avgT) k_d_repick<0, false><<<grid, bl, smem, s>>>(SS_REPICK_ARGS, map, tile ? 0 : 1);
+    else k_d_repick<0, true><<<grid, bl, smem, s>>>(SS_REPICK_ARGS, map, tile ? 0 : 1);
   }
 #undef SS_REPICK_ARGS
 }
@@ -562,22 +731,24 @@ void launch_d_repick(const double* psumT, const uint8_t* valid, const int* cnt,
 // exact FP64 (zncc_exact, reference cost formula); the warp takes the first
 // minimum (smallest candidate among equal costs), as smoothing.cpp:138 does.
 __global__ void k_repick_exact(const Deferred* __restrict__ defer,
-                               const unsigned* __restrict__ defer_count, int* __restrict__ o,
+                               const unsigned* __restrict__ defer_count, int* __restrict__ oT,
                                const uint8_t* __restrict__ lgray,
                                const uint8_t* __restrict__ rgray, int2* __restrict__ chg,
-                               unsigned* __restrict__ chg_count, RefineArgs a, long stride,
-                               long gray_stride, unsigned long long* __restrict__ counters) {
+                               unsigned* __restrict__ chg_count, RefineArgs a, long gray_stride,
+                               unsigned long long* __restrict__ counters) {
   const long f = blockIdx.y;
   const unsigned n = defer_count[f];
   if (blockIdx.x == 0 && threadIdx.x == 0 && counters) atomicAdd(counters, (unsigned long long)n);
   const int lane = threadIdx.x & 31;
   const int W = a.g.W, H = a.g.H, half = a.g.half;
+  const long bs = bt_frame(W, H, 0);
   const uint8_t* L = lgray + f * gray_stride;
   const uint8_t* R = rgray + f * gray_stride;
   const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
   for (unsigned t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n; t += nwarps) {
-    const Deferred e = defer[f * stride + t];
-    const int u = e.pix % W, v = e.pix / W;
+    const Deferred e = defer[f * bs + t];
+    int u, v;
+    bt_decode(W, e.pix, v, u);
     const bool fits = u >= half && u < W - half && v >= half && v < H - half;
     const bool mine = lane < kMaxCand && ((e.mask >> lane) & 1);
     double cost = INFINITY;
@@ -594,88 +765,64 @@ __global__ void k_repick_exact(const Deferred* __restrict__ defer,
     }
     if (lane == 0 && k < 64) {
       const int best = e.c_lo + k;
-      const long i = f * stride + e.pix;
+      const long i = f * bs + e.pix;
       if (chg) {
-        const int old = o[i];
-        if (best != old) chg[f * stride + atomicAdd(chg_count + f, 1u)] = make_int2(e.pix, best - old);
+        const int old = oT[i];
+        if (best != old)
+          chg[f * bs + atomicAdd(chg_count + f, 1u)] = make_int2(e.pix, best - old);
       }
-      o[i] = best;
+      oT[i] = best;
     }
   }
 }
 
-void launch_repick_exact(const Deferred* defer, const unsigned* defer_count, int* o,
+void launch_repick_exact(const Deferred* defer, const unsigned* defer_count, int* oT,
                          const uint8_t* lgray, const uint8_t* rgray, int2* chg,
-                         unsigned* chg_count, const RefineArgs& a, int frames, long stride,
-                         long gray_stride, unsigned long long* counters, cudaStream_t s) {
+                         unsigned* chg_count, const RefineArgs& a, int frames, long gray_stride,
+                         unsigned long long* counters, cudaStream_t s) {
   if (frames <= 0) return;
-  k_repick_exact<<<dim3(64, frames), 256, 0, s>>>(defer, defer_count, o, lgray, rgray, chg,
-                                                  chg_count, a, stride, gray_stride, counters);
-}
-
-__global__ void k_int_to_double(const int* __restrict__ x, const uint8_t* __restrict__ valid,
-                                double* __restrict__ y, long n) {
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
-       i += (long)gridDim.x * blockDim.x)
-    if (valid[i]) y[i] = (double)x[i];
-}
-
-void launch_int_to_double(const int* x, const uint8_t* valid, double* y, long n,
-                          cudaStream_t s) {
-  if (n <= 0) return;
-  long blocks = (n + 255) / 256;
-  if (blocks > 2048) blocks = 2048;
-  k_int_to_double<<<(unsigned)blocks, 256, 0, s>>>(x, valid, y, n);
+  k_repick_exact<<<dim3(64, frames), 256, 0, s>>>(defer, defer_count, oT, lgray, rgray, chg,
+                                                  chg_count, a, gray_stride, counters);
 }
 
 // One warp per changed pixel j: S_o(i) += delta_j for every valid i whose disc
-// contains j (the disc relation is symmetric, clipped to the image exactly as
-// the reference's row spans are).
+// contains j. The relation is symmetric (|dx| <= span(|dy|) <=> dx^2 + dy^2 <=
+// R^2) and clipped to the image exactly as the reference's row spans are.
+// Lanes walk rows (contiguous in BT), the loop walks columns.
 __global__ void k_so_update(const int2* __restrict__ chg, const unsigned* __restrict__ chg_count,
-                            const uint8_t* __restrict__ valid, int* __restrict__ so,
-                            RefineArgs a, long stride) {
+                            const uint8_t* __restrict__ mT, int* __restrict__ soT,
+                            RefineArgs a) {
   const long f = blockIdx.y;
   const int W = a.g.W, H = a.g.H, R = a.radius;
+  const long bs = bt_frame(W, H, 0);
   const unsigned n = chg_count[f];
   const int lane = threadIdx.x & 31;
   const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
   for (unsigned t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n; t += nwarps) {
-    const int2 e = chg[f * stride + t];
-    const int v = e.x / W, u = e.x % W;
-    for (int dy = max(-R, -v); dy <= min(R, H - 1 - v); ++dy) {
-      const int sx = __ldg(a.span + (dy < 0 ? -dy : dy));
-      const int u0 = max(0, u - sx), u1 = min(W - 1, u + sx);
-      const long row = f * stride + (long)(v + dy) * W;
-      for (int x = u0 + lane; x <= u1; x += 32)
-        if (__ldg(valid + row + x)) atomicAdd(so + row + x, e.y);
+    const int2 e = chg[f * bs + t];
+    int v, u;
+    bt_decode(W, e.x, v, u);
+    const int xlo = max(0, u - R), xhi = min(W - 1, u + R);
+    for (int dy0 = -R; dy0 <= R; dy0 += 32) {
+      const int dy = dy0 + lane, y = v + dy;
+      const bool rok = dy <= R && y >= 0 && y < H;
+      const int sy = rok ? __ldg(a.span + (dy < 0 ? -dy : dy)) : -1;
+      const long rowbase = rok ? f * bs + ((long)(y >> 5) * W) * 32 + (y & 31) : 0;
+      for (int x = xlo; x <= xhi; ++x) {
+        const int dx = x - u;
+        if ((dx < 0 ? -dx : dx) <= sy) {
+          const long bi = rowbase + (long)x * 32;
+          if (mT[bi]) atomicAdd(soT + bi, e.y);
+        }
+      }
     }
   }
 }
 
-void launch_so_update(const int2* chg, const unsigned* chg_count, const uint8_t* valid,
-                      int* so, const RefineArgs& a, int frames, long stride, cudaStream_t s) {
+void launch_so_update(const int2* chg, const unsigned* chg_count, const uint8_t* mT, int* soT,
+                      const RefineArgs& a, int frames, cudaStream_t s) {
   if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
-  k_so_update<<<dim3(148, frames), 256, 0, s>>>(chg, chg_count, valid, so, a, stride);
-}
-
-__global__ void k_refine_out(const double* __restrict__ d, const uint8_t* __restrict__ valid,
-                             const float* __restrict__ din, float* __restrict__ dout, long n,
-                             long stride) {
-  const long f = blockIdx.y;
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
-       i += (long)gridDim.x * blockDim.x) {
-    const long k = f * stride + i;
-    dout[k] = valid[k] ? (float)d[k] : din[k];
-  }
-}
-
-void launch_refine_out(const double* d, const uint8_t* valid, const float* din, float* dout,
-                       int W, int H, int frames, long stride, cudaStream_t s) {
-  const long n = (long)W * H;
-  if (n <= 0 || frames <= 0) return;
-  long blocks = (n + 255) / 256;
-  if (blocks > 2048) blocks = 2048;
-  k_refine_out<<<dim3((unsigned)blocks, frames), 256, 0, s>>>(d, valid, din, dout, n, stride);
+  k_so_update<<<dim3(148, frames), 256, 0, s>>>(chg, chg_count, mT, soT, a);
 }
 
 }  // namespace ssb

@@ -19,6 +19,7 @@
 #include <type_traits>
 
 #include "ss_internal.cuh"
+#include "tma.cuh"
 
 namespace ssb {
 
@@ -27,39 +28,17 @@ constexpr int kScanWarps = 4;
 constexpr int kRowsPerWarp = 8;
 constexpr int kChunk = 64;  // columns per TMA chunk
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
 }  // namespace
 
 // ---------------- BT-layout scan (refinement) ----------------
 
+template <typename T>
+__device__ __forceinline__ T add_rn(T s, T x) {
+  if constexpr (std::is_same<T, double>::value) return __dadd_rn(s, x);
+  else return s + x;
+}
+
+// xT == nullptr (int only): x = 1 under the mask, i.e. per-row valid counts.
 template <typename T>
 __global__ void __launch_bounds__(32)
     k_scan_bt(const T* __restrict__ xT, const uint8_t* __restrict__ mT, T* __restrict__ pT, int W,
@@ -70,7 +49,8 @@ __global__ void __launch_bounds__(32)
   const int lane = threadIdx.x;
   const long f = blockIdx.y;
   const int rb = blockIdx.x;
-  const T* xs = xT + (f * RB + rb) * (long)W * 32;
+  const bool ones = xT == nullptr;
+  const T* xs = ones ? nullptr : xT + (f * RB + rb) * (long)W * 32;
   const uint8_t* ms = mT + (f * RB + rb) * (long)W * 32;
   T* dst = pT + (f * RB + rb) * (long)(W + 1) * 32;
   const int nchunks = (W + kChunk - 1) / kChunk;
@@ -82,10 +62,10 @@ __global__ void __launch_bounds__(32)
   __syncwarp();
   auto issue = [&](int k) {
     const int c0 = k * kChunk, cols = min(kChunk, W - c0);
-    const unsigned xbytes = cols * 32 * sizeof(T), mbytes = cols * 32;
+    const unsigned xbytes = ones ? 0u : cols * 32 * sizeof(T), mbytes = cols * 32;
     uint64_t* b = &bar[k & 1];
     mbar_expect_tx(b, xbytes + mbytes);
-    bulk_g2s(&xb[k & 1][0][0], xs + (long)c0 * 32, xbytes, b);
+    if (!ones) bulk_g2s(&xb[k & 1][0][0], xs + (long)c0 * 32, xbytes, b);
     bulk_g2s(&mb[k & 1][0][0], ms + (long)c0 * 32, mbytes, b);
   };
   if (lane == 0 && nchunks > 0) issue(0);
@@ -105,20 +85,14 @@ __global__ void __launch_bounds__(32)
     if (cols == kChunk) {
 #pragma unroll 16
       for (int c = 0; c < kChunk; ++c) {
-        const T x = xk[c][lane];
-        if (mk[c][lane]) {
-          if constexpr (std::is_same<T, double>::value) s = __dadd_rn(s, x);
-          else s += x;
-        }
+        const T x = ones ? T(1) : xk[c][lane];
+        if (mk[c][lane]) s = add_rn(s, x);
         out[(long)c * 32] = s;
       }
     } else {
       for (int c = 0; c < cols; ++c) {
-        const T x = xk[c][lane];
-        if (mk[c][lane]) {
-          if constexpr (std::is_same<T, double>::value) s = __dadd_rn(s, x);
-          else s += x;
-        }
+        const T x = ones ? T(1) : xk[c][lane];
+        if (mk[c][lane]) s = add_rn(s, x);
         out[(long)c * 32] = s;
       }
     }
@@ -140,91 +114,117 @@ void launch_scan_bt_i(const int* xT, const uint8_t* mT, int* pT, int W, int H, i
   k_scan_bt<int><<<dim3(RB, frames), 32, 0, s>>>(xT, mT, pT, W, RB);
 }
 
-// ---------------- normal layout -> BT layout (value sources) ----------------
-
-struct SrcMask {  // the mask itself
-  __device__ uint8_t operator()(long) const { return 1; }
+// Iterations >= 1: the correction b (smoothing.cpp:91-99) formed from the
+// exact integer disc sum S_o, o and d, b = (S_o / cnt - a o) - (1 - a) d left
+// to right in IEEE double, then the serial prefix. One block per row block:
+// thread 0 streams the five fields through shared memory with bulk copies
+// (double-buffered 32-column chunks), warps 1..7 form b for chunk k while
+// warp 0 runs the add chains over chunk k-1. Invalid pixels contribute +0.0,
+// which leaves a prefix bit-identical (it is never -0.0: it starts at +0.0 and
+// an exactly-zero round-to-nearest sum is +0.0).
+constexpr int kChunkB = 32;
+constexpr int kScanBWarps = 8;
+struct ScanBRaw {  // [column][row]
+  int so[kChunkB][32], cnt[kChunkB][32], o[kChunkB][32];
+  double d[kChunkB][32];
+  uint8_t m[kChunkB][32];
 };
-struct SrcOne {  // 1 under the mask (disc counts)
-  __device__ int operator()(long) const { return 1; }
-};
-struct SrcDouble {  // a masked double field
-  const double* val;
-  __device__ double operator()(long i) const { return __ldg(val + i); }
-};
-struct SrcInt {  // an int field (the integer disparities o)
-  const int* val;
-  __device__ int operator()(long i) const { return __ldg(val + i); }
-};
-struct SrcB {  // correction b (smoothing.cpp:96-97) from the exact integer disc sum of o
-  const int* so;
-  const int* cnt;
-  const int* o;
-  const double* d;
-  double alpha, one_minus_alpha;
-  __device__ double operator()(long i) const {
-    const double avg = __ddiv_rn((double)__ldg(so + i), (double)__ldg(cnt + i));
-    return __dsub_rn(__dsub_rn(avg, __dmul_rn(alpha, (double)__ldg(o + i))),
-                     __dmul_rn(one_minus_alpha, __ldg(d + i)));
-  }
+struct ScanBSmem {
+  ScanBRaw raw[2];
+  double b[2][kChunkB][32];
+  uint64_t bar[2];
 };
 
-// 32 x 32 tile transpose through shared memory; unmasked entries are 0 and
-// rows past H (BT padding) are written as 0 so scans over them are inert.
-template <typename T, class Src>
-__global__ void __launch_bounds__(32 * 8)
-    k_to_bt(Src src, const uint8_t* __restrict__ mask, T* __restrict__ outT, int W, int H, int RB,
-            long stride) {
-  __shared__ T tile[32][33];
-  const long f = blockIdx.z;
-  const int c0 = blockIdx.x * 32, v0 = blockIdx.y * 32;
-  for (int r = threadIdx.y; r < 32; r += 8) {
-    const int v = v0 + r, c = c0 + threadIdx.x;
-    T x = T(0);
-    if (v < H && c < W) {
-      const long i = f * stride + (long)v * W + c;
-      if (mask[i]) x = src(i);
-    }
-    tile[r][threadIdx.x] = x;
+__global__ void __launch_bounds__(32 * kScanBWarps)
+    k_scan_b(const int* __restrict__ soT, const int* __restrict__ cntT, const int* __restrict__ oT,
+             const double* __restrict__ dT, const uint8_t* __restrict__ mT, double alpha,
+             double one_minus_alpha, double* __restrict__ pT, int W, int RB) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  ScanBSmem& S = *reinterpret_cast<ScanBSmem*>(smem_raw);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long f = blockIdx.y;
+  const int rb = blockIdx.x;
+  const long base = (f * RB + rb) * (long)W * 32;
+  double* dst = pT + (f * RB + rb) * (long)(W + 1) * 32;
+  const int nchunks = (W + kChunkB - 1) / kChunkB;
+  auto issue = [&](int k) {
+    const int c0 = k * kChunkB, cols = min(kChunkB, W - c0);
+    const long e0 = base + (long)c0 * 32;
+    const unsigned n = cols * 32;
+    ScanBRaw& B = S.raw[k & 1];
+    uint64_t* bar = &S.bar[k & 1];
+    mbar_expect_tx(bar, n * (3 * sizeof(int) + sizeof(double) + 1));
+    bulk_g2s(&B.so[0][0], soT + e0, n * sizeof(int), bar);
+    bulk_g2s(&B.cnt[0][0], cntT + e0, n * sizeof(int), bar);
+    bulk_g2s(&B.o[0][0], oT + e0, n * sizeof(int), bar);
+    bulk_g2s(&B.d[0][0], dT + e0, n * sizeof(double), bar);
+    bulk_g2s(&B.m[0][0], mT + e0, n, bar);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    mbar_fence_init();
+    if (nchunks > 0) issue(0);
+    if (nchunks > 1) issue(1);
   }
   __syncthreads();
-  T* o = outT + (f * RB + blockIdx.y) * (long)W * 32;
-  for (int cc = threadIdx.y; cc < 32; cc += 8) {
-    const int c = c0 + cc;
-    if (c < W) o[(long)c * 32 + threadIdx.x] = tile[threadIdx.x][cc];
+  double s = 0.0;
+  if (warp == 0) dst[lane] = 0.0;
+  for (int k = 0; k <= nchunks; ++k) {
+    if (warp == 0) {
+      if (k >= 1) {  // add chains over chunk k-1
+        const int c0 = (k - 1) * kChunkB, cols = min(kChunkB, W - c0);
+        const double(*bk)[32] = S.b[(k - 1) & 1];
+        double* out = dst + (long)(c0 + 1) * 32 + lane;
+        if (cols == kChunkB) {
+#pragma unroll 8
+          for (int c = 0; c < kChunkB; ++c) {
+            s = __dadd_rn(s, bk[c][lane]);
+            out[(long)c * 32] = s;
+          }
+        } else {
+          for (int c = 0; c < cols; ++c) {
+            s = __dadd_rn(s, bk[c][lane]);
+            out[(long)c * 32] = s;
+          }
+        }
+      }
+    } else if (k < nchunks) {  // form b for chunk k
+      mbar_wait(&S.bar[k & 1], (k >> 1) & 1);
+      const int cols = min(kChunkB, W - k * kChunkB);
+      const ScanBRaw& B = S.raw[k & 1];
+      double(*bk)[32] = S.b[k & 1];
+      for (int c = warp - 1; c < cols; c += kScanBWarps - 1) {
+        double b = 0.0;
+        if (B.m[c][lane]) {
+          const double avg = __ddiv_rn((double)B.so[c][lane], (double)B.cnt[c][lane]);
+          b = __dsub_rn(__dsub_rn(avg, __dmul_rn(alpha, (double)B.o[c][lane])),
+                        __dmul_rn(one_minus_alpha, B.d[c][lane]));
+        }
+        bk[c][lane] = b;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && k + 2 < nchunks) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(k + 2);  // raw[k & 1] was last read in step k
+    }
   }
 }
 
-template <typename T, class Src>
-static void launch_to_bt(Src src, const uint8_t* mask, T* outT, int W, int H, int frames,
-                         long stride, cudaStream_t s) {
+void launch_scan_b(const int* soT, const int* cntT, const int* oT, const double* dT,
+                   const uint8_t* mT, double alpha, double one_minus_alpha, double* pT, int W,
+                   int H, int frames, cudaStream_t s) {
   if (W <= 0 || H <= 0 || frames <= 0) return;
   const int RB = (H + 31) / 32;
-  k_to_bt<T, Src><<<dim3((W + 31) / 32, RB, frames), dim3(32, 8), 0, s>>>(src, mask, outT, W, H,
-                                                                          RB, stride);
-}
-
-void launch_mask_bt(const uint8_t* mask, uint8_t* mT, int W, int H, int frames, long stride,
-                    cudaStream_t s) {
-  launch_to_bt<uint8_t>(SrcMask{}, mask, mT, W, H, frames, stride, s);
-}
-void launch_ones_bt(const uint8_t* mask, int* outT, int W, int H, int frames, long stride,
-                    cudaStream_t s) {
-  launch_to_bt<int>(SrcOne{}, mask, outT, W, H, frames, stride, s);
-}
-void launch_double_bt(const double* val, const uint8_t* mask, double* outT, int W, int H,
-                      int frames, long stride, cudaStream_t s) {
-  launch_to_bt<double>(SrcDouble{val}, mask, outT, W, H, frames, stride, s);
-}
-void launch_int_bt(const int* val, const uint8_t* mask, int* outT, int W, int H, int frames,
-                   long stride, cudaStream_t s) {
-  launch_to_bt<int>(SrcInt{val}, mask, outT, W, H, frames, stride, s);
-}
-void launch_b_bt(const int* so, const int* cnt, const int* o, const double* d, double alpha,
-                 double one_minus_alpha, const uint8_t* mask, double* bT, int W, int H,
-                 int frames, long stride, cudaStream_t s) {
-  launch_to_bt<double>(SrcB{so, cnt, o, d, alpha, one_minus_alpha}, mask, bT, W, H, frames,
-                       stride, s);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_scan_b, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(ScanBSmem));
+    configured = true;
+  }
+  k_scan_b<<<dim3(RB, frames), 32 * kScanBWarps, sizeof(ScanBSmem), s>>>(
+      soT, cntT, oT, dT, mT, alpha, one_minus_alpha, pT, W, RB);
 }
 
 // ---------------- normal-layout count scan (cleanup disc support) ----------------

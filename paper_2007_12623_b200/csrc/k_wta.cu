@@ -150,7 +150,8 @@ __global__ void __launch_bounds__(512) k_wta11(
     int* __restrict__ wbase, const int* __restrict__ base_map, float* __restrict__ disp,
     uint8_t* __restrict__ valid, int* __restrict__ flag_list,
     unsigned int* __restrict__ flag_count, Geom g, int TH, float min_zncc_f, float thr_tol,
-    int do_argmax, long plane_stride, long lstat_stride, long rstat_stride, long map_stride) {
+    int do_argmax, long plane_stride, long lstat_stride, long rstat_stride, long map_stride,
+    long win_stride) {
   extern __shared__ unsigned char smem_raw[];
   const int lane = threadIdx.x, j = threadIdx.y, NB = blockDim.y;
   const int NCB = NB * kDB;  // staged candidates per pixel
@@ -164,8 +165,8 @@ __global__ void __launch_bounds__(512) k_wta11(
   rplane += fr * plane_stride;
   lstat += fr * lstat_stride;
   rstat += fr * rstat_stride;
-  win += fr * map_stride * kWin;
-  wbase += fr * map_stride;
+  win += fr * win_stride * kWin;
+  wbase += fr * win_stride;
   if (base_map) base_map += fr * map_stride;
   disp += fr * map_stride;
   valid += fr * map_stride;
@@ -294,20 +295,21 @@ __global__ void __launch_bounds__(512) k_wta11(
           int wb = kNoWin;
           if (!isnan(rl) && anchor != kNoArg && anchor != kNoWin)
             wb = window_base(anchor, g.cmin, g.NC);
-          wbase[idx] = wb;
+          const long bi = bt_index(W, vv, u);
+          wbase[bi] = wb;
           if (wb != kNoWin) {
             const float* gr = s_g + r * NCB * 32 + lane;
-            uint32_t w[kWin / 2];  // kWin fp16 scores, 32 B: one sector per pixel
+            uint32_t w[kWin / 2];  // kWin fp16 match costs (m_code)
 #pragma unroll
             for (int q = 0; q < kWin / 2; ++q) {
               const int ci = wb - g.cmin + 2 * q;
               const float s0 = ci < g.NC ? gr[ci * 32] * rl : __int_as_float(0x7fc00000);
               const float s1 = ci + 1 < g.NC ? gr[(ci + 1) * 32] * rl : __int_as_float(0x7fc00000);
-              w[q] = pack_score2(s0, s1);
+              w[q] = pack_m2(s0, s1);
             }
-            uint4* wp = reinterpret_cast<uint4*>(win + idx * kWin);
-            wp[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            wp[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            uint32_t* wq = reinterpret_cast<uint32_t*>(win) + win_word(W, vv, u, 0);
+#pragma unroll
+            for (int q = 0; q < kWin / 2; ++q) wq[(long)q * W * 32] = w[q];
           }
         }
       }
@@ -320,7 +322,8 @@ void launch_wta11(const uint8_t* lplane, const uint8_t* rplane, const int2* lsta
                   const int2* rstat, wscore_t* win, int* wbase, const int* base_map, float* disp,
                   uint8_t* valid, int* flag_list, unsigned int* flag_count, const Geom& g,
                   double min_zncc, int frames, long plane_stride, long lstat_stride,
-                  long rstat_stride, long map_stride, int do_argmax, cudaStream_t s) {
+                  long rstat_stride, long map_stride, long win_stride, int do_argmax,
+                  cudaStream_t s) {
   const int h = 5;
   if (g.W - 2 * h <= 0 || g.H - 2 * h <= 0 || frames <= 0) return;
   const int NB = (g.NC + kDB - 1) / kDB;
@@ -337,7 +340,8 @@ void launch_wta11(const uint8_t* lplane, const uint8_t* rplane, const int2* lsta
   const float tol = 4e-6f * fmaxf(1.f, fabsf(mz));
   k_wta11<<<grid, block, smem, s>>>(lplane, rplane, lstat, rstat, win, wbase, base_map, disp,
                                     valid, flag_list, flag_count, g, TH, mz, tol, do_argmax,
-                                    plane_stride, lstat_stride, rstat_stride, map_stride);
+                                    plane_stride, lstat_stride, rstat_stride, map_stride,
+                                    win_stride);
 }
 
 // ---- exact FP64 path: warp per pixel, lanes over d ----
@@ -438,7 +442,7 @@ void launch_wta_generic(const uint8_t* lgray, const uint8_t* rgray, float* disp,
 __global__ void k_window_check(const float* __restrict__ disp, const uint8_t* __restrict__ valid,
                                const int2* __restrict__ lstat, int* __restrict__ wbase,
                                int* __restrict__ list, unsigned* __restrict__ count, Geom g,
-                               long stride) {
+                               long stride, long win_stride) {
   const long f = blockIdx.z;
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = blockIdx.y * blockDim.y + threadIdx.y;
@@ -447,12 +451,13 @@ __global__ void k_window_check(const float* __restrict__ disp, const uint8_t* __
   if (!valid[i]) return;
   const int h = g.half;
   const bool fits = u >= h && u < g.W - h && v >= h && v < g.H - h;
+  int* wb = wbase + f * win_stride + bt_index(g.W, v, u);
   if (!fits || isnan(__int_as_float(__ldg(&lstat[i].y)))) {
-    wbase[i] = kNoWin;
+    *wb = kNoWin;
     return;
   }
   const int want = window_base((int)floor((double)disp[i]), g.cmin, g.NC);
-  if (wbase[i] != want) list[f * stride + atomicAdd(count + f, 1u)] = (int)pix;
+  if (*wb != want) list[f * stride + atomicAdd(count + f, 1u)] = (int)pix;
 }
 
 // Pass 2: half a warp per queued pixel, lane q computes candidate wbase + q
@@ -464,7 +469,7 @@ __global__ void k_window_build(const float* __restrict__ disp, const uint8_t* __
                                const int2* __restrict__ rstat, wscore_t* __restrict__ win,
                                int* __restrict__ wbase, const int* __restrict__ list,
                                const unsigned* __restrict__ count, Geom g, long stride,
-                               long rstat_stride) {
+                               long rstat_stride, long win_stride) {
   const long f = blockIdx.y;
   const unsigned n = count[f];
   const int q = threadIdx.x & (kWin - 1);
@@ -492,22 +497,24 @@ __global__ void k_window_build(const float* __restrict__ disp, const uint8_t* __
       const int num = 61 * slr - ls.x * rs.x;
       s = (__int2float_rn(num) * __int_as_float(rs.y)) * __int_as_float(ls.y);
     }
-    win[i * kWin + q] = __float2half_rn(s);
-    if (q == 0) wbase[i] = wb;
+    win[(f * win_stride * (kWin / 2) + win_word(W, v, u, q >> 1)) * 2 + (q & 1)] =
+        __ushort_as_half(m_code(s));
+    if (q == 0) wbase[f * win_stride + bt_index(W, v, u)] = wb;
   }
 }
 
 void launch_window_fix(const float* disp, const uint8_t* valid, const uint8_t* lgray,
                        const uint8_t* rgray, const int2* lstat, const int2* rstat, wscore_t* win,
                        int* wbase, int* list, unsigned* count, const Geom& g, int frames,
-                       long stride, long rstat_stride, cudaStream_t s) {
+                       long stride, long rstat_stride, long win_stride, cudaStream_t s) {
   if (g.W <= 0 || g.H <= 0 || frames <= 0) return;
   cudaMemsetAsync(count, 0, sizeof(unsigned) * frames, s);
   dim3 b(32, 8);
   k_window_check<<<dim3((g.W + 31) / 32, (g.H + 7) / 8, frames), b, 0, s>>>(
-      disp, valid, lstat, wbase, list, count, g, stride);
+      disp, valid, lstat, wbase, list, count, g, stride, win_stride);
   k_window_build<<<dim3(148, frames), 256, 0, s>>>(disp, lgray, rgray, lstat, rstat, win, wbase,
-                                                   list, count, g, stride, rstat_stride);
+                                                   list, count, g, stride, rstat_stride,
+                                                   win_stride);
 }
 
 }  // namespace ssb

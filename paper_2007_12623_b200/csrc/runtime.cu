@@ -162,9 +162,9 @@ struct ss_ctx {
 
   DevBuf in_l, in_r, gray_l, gray_r, plane_l, plane_r, lstat, rstat, win, wbase;
   DevBuf disp_a, disp_b, valid_a, valid_b, flags, flag_count;
-  DevBuf o, oi, d, avg, b, psum, pcnt, cnt, span, wtab, fspan;
+  DevBuf o, oi, d, avg, b, psum, pcnt, cnt, span, wtab, fspan, fx, emap;
   DevBuf index, block_sums, npoints, pts_f, nrm_f, colors, pts_d, nrm_d, pixels, pts4;
-  DevBuf counters, trace_o, trace_d, so, chg, chg_count, xbt, mbt, defer, defer_count;
+  DevBuf counters, trace_o, trace_d, so, chg, chg_count, mbt, defer, defer_count;
   int wtab_radius = -1;
 
   ss_ctx_stats stats{};
@@ -188,9 +188,9 @@ struct ss_ctx {
   ~ss_ctx() {
     for (DevBuf* b : {&in_l, &in_r, &gray_l, &gray_r, &plane_l, &plane_r, &lstat, &rstat, &win, &wbase,
                       &disp_a, &disp_b, &valid_a, &valid_b, &flags, &flag_count, &o, &d, &avg,
-                      &b, &psum, &pcnt, &cnt, &span, &wtab, &fspan, &index, &block_sums, &npoints,
+                      &b, &psum, &pcnt, &cnt, &span, &wtab, &fspan, &fx, &emap, &index, &block_sums, &npoints,
                       &pts_f, &nrm_f, &colors, &pts_d, &nrm_d, &pixels, &pts4, &counters, &oi, &trace_o,
-                      &trace_d, &so, &chg, &chg_count, &xbt, &mbt, &defer, &defer_count})
+                      &trace_d, &so, &chg, &chg_count, &mbt, &defer, &defer_count})
       b->release();
     for (auto& r : pending) {
       ev_pool.push_back(r.a);
@@ -283,8 +283,9 @@ struct ss_ctx {
     plane_r.ensure(plane_stride * n);
     lstat.ensure(sizeof(int2) * N * n);
     rstat.ensure(sizeof(int2) * rstride * n);
-    win.ensure(sizeof(wscore_t) * kWin * N * n);
-    wbase.ensure(sizeof(int) * N * n);
+    const long bs = bt_frame(g.W, g.H, 0);  // windows are BT-indexed
+    win.ensure(sizeof(wscore_t) * kWin * bs * n);
+    wbase.ensure(sizeof(int) * bs * n);
     flags.ensure(sizeof(int) * N * n);
     flag_count.ensure(sizeof(unsigned) * n);
     {
@@ -304,7 +305,7 @@ struct ss_ctx {
     launch_wta11(plane_l.as<uint8_t>(), plane_r.as<uint8_t>(), lstat.as<int2>(), rstat.as<int2>(),
                  win.as<wscore_t>(), wbase.as<int>(), nullptr, disp_a.as<float>(),
                  valid_a.as<uint8_t>(), flags.as<int>(), flag_count.as<unsigned>(), g,
-                 params.min_zncc, n, plane_stride, N, rstride, N, do_argmax ? 1 : 0, stream);
+                 params.min_zncc, n, plane_stride, N, rstride, N, bs, do_argmax ? 1 : 0, stream);
     stats.kernel_launches += 1;
   }
 
@@ -339,14 +340,21 @@ struct ss_ctx {
 
   void ensure_wtab(int radius) {
     if (radius == wtab_radius) return;
-    const int r2 = std::max(radius, 0) * std::max(radius, 0);
-    std::vector<double> w(r2 + 1, 0.0);
-    for (int dd = 1; dd <= r2; ++dd) w[dd] = 1.0 / std::sqrt(static_cast<double>(dd));
-    wtab.ensure(sizeof(double) * (r2 + 1));
-    ck(cudaMemcpy(wtab.p, w.data(), sizeof(double) * (r2 + 1), cudaMemcpyHostToDevice), "wtab");
+    const int R = std::max(radius, 0), D = 2 * R + 1;
+    const int r2 = R * R;
+    // w[dv + R][du + R] = 1 / sqrt(du^2 + dv^2) inside the disc (cleanup.cpp:76-78)
+    std::vector<double> w((size_t)D * D, 0.0);
+    for (int dv = -R; dv <= R; ++dv)
+      for (int du = -R; du <= R; ++du) {
+        const int dd = du * du + dv * dv;
+        if (dd > 0 && dd <= r2)
+          w[(size_t)(dv + R) * D + (du + R)] = 1.0 / std::sqrt(static_cast<double>(dd));
+      }
+    wtab.ensure(sizeof(double) * w.size());
+    ck(cudaMemcpy(wtab.p, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice), "wtab");
     // disc rows: |du| <= floor(sqrt(r^2 - dv^2))  <=>  du^2 + dv^2 <= r^2
-    std::vector<int> sp(std::max(radius, 0) + 1);
-    for (int dv = 0; dv <= radius; ++dv)
+    std::vector<int> sp(R + 1);
+    for (int dv = 0; dv <= R; ++dv)
       sp[dv] = (int)std::floor(std::sqrt((double)(r2 - dv * dv)));
     fspan.ensure(sizeof(int) * sp.size());
     ck(cudaMemcpy(fspan.p, sp.data(), sizeof(int) * sp.size(), cudaMemcpyHostToDevice), "fspan");
@@ -360,9 +368,10 @@ struct ss_ctx {
     pcnt.ensure(sizeof(int) * (long)H * (W + 1) * n);
     flags.ensure(sizeof(int) * N * n);
     flag_count.ensure(sizeof(unsigned) * n);
+    fx.ensure(sizeof(double) * N * n);
     launch_fill_disc(din, vin, dout, vout, W, H, radius, min_support, wtab.as<double>(),
                      fspan.as<int>(), pcnt.as<int>(), flags.as<int>(), flag_count.as<unsigned>(),
-                     n, N, stream);
+                     fx.as<double>(), n, N, stream);
     stats.kernel_launches += 3;
   }
 
@@ -372,11 +381,12 @@ struct ss_ctx {
     const long N = (long)W * H;
     const int disc_support = disc_fill_min_support(params.fill_radius_disc);
     ensure_wtab(params.fill_radius_disc);
+    emap.ensure(sizeof(uint32_t) * edge_map_words(W, H) * n);
     for (int k = 0; k < params.cleanup_iterations; ++k) {
       const int r = params.outlier_radius_start + k * params.outlier_radius_step;
       launch_remove_outliers(disp_a.as<float>(), valid_a.as<uint8_t>(), disp_b.as<float>(),
-                             valid_b.as<uint8_t>(), W, H, r, params.neighbor_jump_threshold, n, N,
-                             stream);
+                             valid_b.as<uint8_t>(), W, H, r, params.neighbor_jump_threshold,
+                             emap.as<uint32_t>(), n, N, stream);
       launch_fill_radial(disp_b.as<float>(), valid_b.as<uint8_t>(), disp_a.as<float>(),
                          valid_a.as<uint8_t>(), W, H, params.fill_radius_radial, 4, n, N, stream);
       fill_disc(n, W, H, disp_a.as<float>(), valid_a.as<uint8_t>(), disp_b.as<float>(),
@@ -393,16 +403,16 @@ struct ss_ctx {
     Stage st(this, 5);
     const int W = g.W, H = g.H;
     const long N = g.N();
-    const long bt_x = bt_frame(W, H, 0), bt_p = bt_frame(W, H, 1);  // BT frame strides
-    o.ensure(sizeof(double) * N * n);
-    d.ensure(sizeof(double) * N * n);
-    avg.ensure(sizeof(double) * N * n);
-    b.ensure(sizeof(double) * N * n);
-    psum.ensure(sizeof(double) * bt_p * n);   // BT prefix (double)
-    pcnt.ensure(sizeof(int) * bt_p * n);      // BT prefix (int)
-    xbt.ensure(sizeof(double) * bt_x * n);    // BT scan input (double / int)
-    mbt.ensure(bt_x * n);                     // BT mask
-    cnt.ensure(sizeof(int) * N * n);
+    const long bs = bt_frame(W, H, 0), bp = bt_frame(W, H, 1);  // BT frame strides
+    // every refinement field is BT (ss_internal.cuh)
+    o.ensure(sizeof(double) * bs * n);     // iteration-0 o (double)
+    d.ensure(sizeof(double) * bs * n);
+    avg.ensure(sizeof(double) * bs * n);
+    b.ensure(sizeof(double) * bs * n);
+    psum.ensure(sizeof(double) * bp * n);  // BT prefix (double)
+    pcnt.ensure(sizeof(int) * bp * n);     // BT prefix (int)
+    mbt.ensure(bs * n);                    // BT mask
+    cnt.ensure(sizeof(int) * bs * n);
     const int r = params.smoothing_radius;
     std::vector<int> sp(std::max(r, 0) + 1);
     for (int dy = 0; dy <= r; ++dy)
@@ -426,81 +436,75 @@ struct ss_ctx {
     if (h_trace_o || h_trace_d) {
       trace_o.ensure(sizeof(double) * N * std::max(iters, 1));
       trace_d.ensure(sizeof(double) * N * std::max(iters, 1));
-      // RefineTrace rows hold 0 at invalid pixels (smoothing.cpp:77-80)
-      ck(cudaMemsetAsync(trace_o.p, 0, sizeof(double) * N * std::max(iters, 1), stream), "memset");
     }
-    oi.ensure(sizeof(int) * N * n);
+    oi.ensure(sizeof(int) * bs * n);
     int* op = oi.as<int>();
-    const uint8_t* vm = valid_a.as<uint8_t>();
     uint8_t* mT = mbt.as<uint8_t>();
-    launch_refine_init(disp_a.as<float>(), vm, o.as<double>(), d.as<double>(), W, H, n, N,
-                       stream);
-    launch_mask_bt(vm, mT, W, H, n, N, stream);
-    launch_ones_bt(vm, xbt.as<int>(), W, H, n, N, stream);
-    launch_scan_bt_i(xbt.as<int>(), mT, pcnt.as<int>(), W, H, n, stream);
-    launch_disc_isum(vm, pcnt.as<int>(), cnt.as<int>(), a, n, N, stream);  // disc counts
-    stats.kernel_launches += 5;
-    so.ensure(sizeof(int) * N * n);
-    chg.ensure(sizeof(int2) * N * n);
+    launch_refine_init(disp_a.as<float>(), valid_a.as<uint8_t>(), mT, o.as<double>(),
+                       d.as<double>(), W, H, n, N, bs, stream);
+    launch_scan_bt_i(nullptr, mT, pcnt.as<int>(), W, H, n, stream);  // per-row valid counts
+    launch_disc_isum(mT, pcnt.as<int>(), cnt.as<int>(), a, n, stream);  // disc counts
+    stats.kernel_launches += 3;
+    so.ensure(sizeof(int) * bs * n);
+    chg.ensure(sizeof(int2) * bs * n);
     chg_count.ensure(sizeof(unsigned) * n);
     // Score windows: re-centre the sweep's windows on the cleanup output.
     const wscore_t* winp = nullptr;
     if (have_windows && iters > 0) {
-      launch_window_fix(disp_a.as<float>(), vm, gray_l.as<uint8_t>(), gray_r.as<uint8_t>(),
-                        lstat.as<int2>(), rstat.as<int2>(), win.as<wscore_t>(), wbase.as<int>(),
-                        flags.as<int>(), flag_count.as<unsigned>(), g, n, N, (long)H * g.SP,
-                        stream);
+      launch_window_fix(disp_a.as<float>(), valid_a.as<uint8_t>(), gray_l.as<uint8_t>(),
+                        gray_r.as<uint8_t>(), lstat.as<int2>(), rstat.as<int2>(),
+                        win.as<wscore_t>(), wbase.as<int>(), flags.as<int>(),
+                        flag_count.as<unsigned>(), g, n, N, (long)H * g.SP, bs, stream);
       stats.kernel_launches += 2;
       winp = win.as<wscore_t>();
     }
-    defer.ensure(sizeof(Deferred) * N * n);
+    defer.ensure(sizeof(Deferred) * bs * n);
     defer_count.ensure(sizeof(unsigned) * n);
     auto repick = [&](const double* avgp, int2* chgp, unsigned* chgc) {
       ck(cudaMemsetAsync(defer_count.p, 0, sizeof(unsigned) * n, stream), "memset");
-      launch_d_repick(psum.as<double>(), vm, cnt.as<int>(), avgp, so.as<int>(), d.as<double>(),
+      launch_d_repick(psum.as<double>(), mT, cnt.as<int>(), avgp, so.as<int>(), d.as<double>(),
                       op, gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), winp, wbase.as<int>(),
-                      chgp, chgc, defer.as<Deferred>(), defer_count.as<unsigned>(), a, n, N, N,
-                      ctr() + 1, stream);
+                      chgp, chgc, defer.as<Deferred>(), defer_count.as<unsigned>(), a, n, N,
+                      stream);
       launch_repick_exact(defer.as<Deferred>(), defer_count.as<unsigned>(), op,
-                          gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), chgp, chgc, a, n, N, N,
+                          gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), chgp, chgc, a, n, N,
                           ctr() + 1, stream);
       stats.kernel_launches += 2;
     };
     for (int it = 0; it < iters; ++it) {
       if (it == 0) {
         // o is the cleanup output (fractional fills): the reference's FP64 path.
-        launch_double_bt(o.as<double>(), vm, xbt.as<double>(), W, H, n, N, stream);
-        launch_scan_bt_d(xbt.as<double>(), mT, psum.as<double>(), W, H, n, stream);
-        launch_avg_b(psum.as<double>(), vm, cnt.as<int>(), o.as<double>(), d.as<double>(),
-                     avg.as<double>(), b.as<double>(), a, n, N, stream);
-        launch_double_bt(b.as<double>(), vm, xbt.as<double>(), W, H, n, N, stream);
-        launch_scan_bt_d(xbt.as<double>(), mT, psum.as<double>(), W, H, n, stream);
-        stats.kernel_launches += 5;
+        launch_scan_bt_d(o.as<double>(), mT, psum.as<double>(), W, H, n, stream);
+        launch_avg_b(psum.as<double>(), mT, cnt.as<int>(), o.as<double>(), d.as<double>(),
+                     avg.as<double>(), b.as<double>(), a, n, stream);
+        launch_scan_bt_d(b.as<double>(), mT, psum.as<double>(), W, H, n, stream);
+        stats.kernel_launches += 3;
         repick(avg.as<double>(), nullptr, nullptr);
         if (iters > 1) {
           // o is integer-valued from here on: exact integer disc sums S_o.
-          launch_int_bt(op, vm, xbt.as<int>(), W, H, n, N, stream);
-          launch_scan_bt_i(xbt.as<int>(), mT, pcnt.as<int>(), W, H, n, stream);
-          launch_disc_isum(vm, pcnt.as<int>(), so.as<int>(), a, n, N, stream);
-          stats.kernel_launches += 3;
+          launch_scan_bt_i(op, mT, pcnt.as<int>(), W, H, n, stream);
+          launch_disc_isum(mT, pcnt.as<int>(), so.as<int>(), a, n, stream);
+          stats.kernel_launches += 2;
         }
       } else {
         ck(cudaMemsetAsync(chg_count.p, 0, sizeof(unsigned) * n, stream), "memset");
-        launch_b_bt(so.as<int>(), cnt.as<int>(), op, d.as<double>(), a.alpha,
-                    a.one_minus_alpha, vm, xbt.as<double>(), W, H, n, N, stream);
-        launch_scan_bt_d(xbt.as<double>(), mT, psum.as<double>(), W, H, n, stream);
-        stats.kernel_launches += 2;
+        launch_scan_b(so.as<int>(), cnt.as<int>(), op, d.as<double>(), mT, a.alpha,
+                      a.one_minus_alpha, psum.as<double>(), W, H, n, stream);
+        stats.kernel_launches += 1;
         repick(nullptr, chg.as<int2>(), chg_count.as<unsigned>());
         if (it + 1 < iters) {
-          launch_so_update(chg.as<int2>(), chg_count.as<unsigned>(), vm, so.as<int>(), a, n, N,
+          launch_so_update(chg.as<int2>(), chg_count.as<unsigned>(), mT, so.as<int>(), a, n,
                            stream);
           stats.kernel_launches += 1;
         }
       }
-      if (h_trace_o) launch_int_to_double(op, vm, trace_o.as<double>() + (long)it * N, N, stream);
-      if (h_trace_d)
-        ck(cudaMemcpyAsync(trace_d.as<double>() + (long)it * N, d.p, sizeof(double) * N,
-                           cudaMemcpyDeviceToDevice, stream), "trace");
+      if (h_trace_o || h_trace_d) {
+        launch_trace_rows(op, d.as<double>(), valid_a.as<uint8_t>(),
+                          h_trace_o ? trace_o.as<double>() + (long)it * N : nullptr,
+                          h_trace_d ? trace_d.as<double>() + (long)it * N : nullptr, W, H,
+                          stream);
+        stats.kernel_launches += 1;
+      }
     }
     launch_refine_out(d.as<double>(), valid_a.as<uint8_t>(), disp_a.as<float>(),
                       disp_b.as<float>(), W, H, n, N, stream);
@@ -691,8 +695,10 @@ ss_status ss_remove_outliers(const float* disparity, const uint8_t* valid, int32
     ck(cudaMemcpyAsync(c->disp_a.p, disparity, sizeof(float) * N, cudaMemcpyHostToDevice,
                        c->stream), "H2D");
     ck(cudaMemcpyAsync(c->valid_a.p, valid, N, cudaMemcpyHostToDevice, c->stream), "H2D");
+    c->emap.ensure(sizeof(uint32_t) * edge_map_words(w, h));
     launch_remove_outliers(c->disp_a.as<float>(), c->valid_a.as<uint8_t>(), c->disp_b.as<float>(),
-                           c->valid_b.as<uint8_t>(), w, h, radius, threshold, 1, N, c->stream);
+                           c->valid_b.as<uint8_t>(), w, h, radius, threshold,
+                           c->emap.as<uint32_t>(), 1, N, c->stream);
     c->stats.kernel_launches += 1;
     d2h(out_disparity, c->disp_b.p, sizeof(float) * N, c->stream);
     d2h(out_valid, c->valid_b.p, N, c->stream);

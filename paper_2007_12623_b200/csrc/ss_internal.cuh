@@ -26,12 +26,21 @@ constexpr int kDB = 16;        // disparities per thread in the WTA sweep
 constexpr int kRefineR = 5;    // kRefineSearchRadius (params.hpp:38)
 constexpr double kZnccEps = 1e-3;  // kZnccCostEpsilon (params.hpp:34)
 constexpr int kWin = 16;           // candidate window per pixel for the refinement
-// Window scores are stored as fp16 (32 B per pixel, one sector): the re-pick
-// filter's error budget covers it (|cost_f - cost| <= 5.4e-4 rel).
+// Window entries hold the re-pick's match cost M = 1/max(s, kZnccCostEpsilon)
+// as fp16 (32 B per pixel): exactly 1000 (= 1/1e-3 in double) when the score
+// is undefined or certainly clamped (s_f < 0.99e-3), otherwise
+// fp16(1/max(s_f, 1e-3)) capped at 999.5, so the code 1000 always means
+// "exact". |M16 - M| <= 5.01e-4 M (fp16 rounding, the cap, the FP32 score's
+// 5-ulp error): the re-pick filter's budget uses 6e-4.
 typedef __half wscore_t;
-__device__ __forceinline__ uint32_t pack_score2(float a, float b) {
-  const __half2 h = __floats2half2_rn(a, b);
-  return *reinterpret_cast<const uint32_t*>(&h);
+__device__ __forceinline__ unsigned short m_code(float s) {
+  if (!(s >= 0.99e-3f)) return __half_as_ushort(__float2half_rn(1000.f));
+  float r;  // 1 ulp reciprocal of a normal number: negligible next to fp16 rounding
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaxf(s, 1e-3f)));
+  return __half_as_ushort(__float2half_rn(fminf(r, 999.5f)));
+}
+__device__ __forceinline__ uint32_t pack_m2(float s0, float s1) {
+  return (uint32_t)m_code(s0) | ((uint32_t)m_code(s1) << 16);
 }
 constexpr int kNoWin = -2147483647 - 1;  // INT_MIN: no window / no defined candidate
 
@@ -65,17 +74,19 @@ void launch_stats(const uint8_t* gray, int2* lstat, int2* rstat, int is_right, c
 // window: kWin scores s(c) = g(c) / sqrt(var_l) for c = wbase .. wbase+kWin-1,
 // wbase centred on the WTA pick, or on base_map[pixel] when base_map != NULL
 // (per-stage refine). wbase = kNoWin when var_l == 0 (no defined score).
+// win / wbase are BT-indexed (bt_index, frame stride win_stride).
 void launch_wta11(const uint8_t* lplane, const uint8_t* rplane, const int2* lstat,
                   const int2* rstat, wscore_t* win, int* wbase, const int* base_map, float* disp,
                   uint8_t* valid, int* flag_list, unsigned int* flag_count, const Geom& g,
                   double min_zncc, int frames, long plane_stride, long lstat_stride,
-                  long rstat_stride, long map_stride, int do_argmax, cudaStream_t s);
+                  long rstat_stride, long map_stride, long win_stride, int do_argmax,
+                  cudaStream_t s);
 // After cleanup: every valid pixel whose window is not centred on its
 // (possibly filled) disparity gets a freshly computed window.
 void launch_window_fix(const float* disp, const uint8_t* valid, const uint8_t* lgray,
                        const uint8_t* rgray, const int2* lstat, const int2* rstat, wscore_t* win,
                        int* wbase, int* list, unsigned* count, const Geom& g, int frames,
-                       long stride, long rstat_stride, cudaStream_t s);
+                       long stride, long rstat_stride, long win_stride, cudaStream_t s);
 void launch_wta_resolve(const uint8_t* lgray, const uint8_t* rgray, const int* flag_list,
                         const unsigned int* flag_count, float* disp, uint8_t* valid,
                         const Geom& g, double min_zncc, int frames, long gray_stride,
@@ -85,17 +96,23 @@ void launch_wta_generic(const uint8_t* lgray, const uint8_t* rgray, float* disp,
                         uint8_t* valid, const Geom& g, double min_zncc, int frames,
                         long gray_stride, long map_stride, cudaStream_t s);
 
+// emap: scratch of edge_map_words(W, H) * frames words (smooth-edge bitmaps)
+inline long edge_map_words(int W, int H) {
+  const long w32 = (W + 31) / 32 + 1, h32 = (H + 31) / 32 + 1;
+  return (long)H * w32 + (long)W * h32 + 2L * (W + H - 1) * h32;
+}
 void launch_remove_outliers(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
-                            int W, int H, int radius, double thr, int frames, long stride,
-                            cudaStream_t s);
+                            int W, int H, int radius, double thr, uint32_t* emap, int frames,
+                            long stride, cudaStream_t s);
 void launch_fill_radial(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
                         int W, int H, int radius, int min_support, int frames, long stride,
                         cudaStream_t s);
-// pcnt: scratch [frames][H][W+1] ints; list: scratch [frames][W*H]; count: [frames]
+// pcnt: scratch [frames][H][W+1] ints; list: scratch [frames][W*H]; count: [frames];
+// fx: scratch [frames][W*H] doubles; wtab: [(2R+1)^2] disc weights (dv-major)
 void launch_fill_disc(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
                       int W, int H, int radius, int min_support, const double* wtab,
-                      const int* span, int* pcnt, int* list, unsigned* count, int frames,
-                      long stride, cudaStream_t s);
+                      const int* span, int* pcnt, int* list, unsigned* count, double* fx,
+                      int frames, long stride, cudaStream_t s);
 
 struct RefineArgs {
   Geom g;
@@ -104,64 +121,82 @@ struct RefineArgs {
   int radius;       // smoothing_radius
   const int* span;  // [radius + 1]
 };
-void launch_refine_init(const float* disp, const uint8_t* valid, double* o, double* d,
-                        int W, int H, int frames, long stride, cudaStream_t s);
 // normal-layout per-row prefix counts (cleanup disc support)
 void launch_row_count(const uint8_t* valid, int* pcnt, int W, int H, int frames, long stride,
                       long pstride, cudaStream_t s);
-// ---- BT layout (row-blocked transposed, k_scan.cu): element (v, c) at
-// ((v/32) * CW + c) * 32 + v%32; frame stride ceil(H/32) * CW * 32 ----
-__host__ __device__ inline long bt_frame(int W, int H, int extra_col) { return (long)((H + 31) / 32) * (W + extra_col) * 32; }
-void launch_mask_bt(const uint8_t* mask, uint8_t* mT, int W, int H, int frames, long stride,
-                    cudaStream_t s);
-void launch_ones_bt(const uint8_t* mask, int* outT, int W, int H, int frames, long stride,
-                    cudaStream_t s);
-void launch_double_bt(const double* val, const uint8_t* mask, double* outT, int W, int H,
-                      int frames, long stride, cudaStream_t s);
-void launch_int_bt(const int* val, const uint8_t* mask, int* outT, int W, int H, int frames,
-                   long stride, cudaStream_t s);
-void launch_b_bt(const int* so, const int* cnt, const int* o, const double* d, double alpha,
-                 double one_minus_alpha, const uint8_t* mask, double* bT, int W, int H,
-                 int frames, long stride, cudaStream_t s);
-// masked serial row prefix (psum[.][0] = 0, W + 1 columns, BT layout)
+
+// ---- BT layout (row-blocked transposed): element (v, c) at
+// ((v/32) * CW + c) * 32 + v%32; frame stride ceil(H/32) * CW * 32. Every
+// refinement field is BT with CW = W (pixel fields, incl. the score windows
+// and wbase) or CW = W + 1 (row prefixes). A warp owns 32 consecutive rows of
+// one column: its loads and stores are single 128/256-byte lines. ----
+__host__ __device__ inline long bt_frame(int W, int H, int extra_col) {
+  return (long)((H + 31) / 32) * (W + extra_col) * 32;
+}
+__host__ __device__ inline long bt_index(int W, int v, int u) {
+  return ((long)(v >> 5) * W + u) * 32 + (v & 31);
+}
+// Score windows: kWin/2 u32 words (2 fp16 scores each) per pixel, stored as
+// BT word planes — word j of pixel (v, u) at ((v/32 * 8 + j) * W + u) * 32 +
+// v%32; frame stride 8 * bt_frame(W, H, 0) words — so a tile's plane j is one
+// contiguous range (a single bulk copy) and a warp reads it conflict-free.
+__host__ __device__ inline long win_word(int W, int v, int u, int j) {
+  return (((long)(v >> 5) * (kWin / 2) + j) * W + u) * 32 + (v & 31);
+}
+__host__ __device__ inline void bt_decode(int W, long idx, int& v, int& u) {
+  const long q = idx >> 5;
+  u = (int)(q % W);
+  v = (int)(q / W) * 32 + (int)(idx & 31);
+}
+// normal (disp, valid) -> BT mask m, o = d = valid ? disp : 0 (double)
+void launch_refine_init(const float* disp, const uint8_t* valid, uint8_t* mT, double* oT,
+                        double* dT, int W, int H, int frames, long stride, long bs,
+                        cudaStream_t s);
+// masked serial row prefix (psum[.][0] = 0, W + 1 columns, BT layout);
+// xT == nullptr for the int scan means x = 1 (disc counts)
 void launch_scan_bt_d(const double* xT, const uint8_t* mT, double* pT, int W, int H, int frames,
                       cudaStream_t s);
 void launch_scan_bt_i(const int* xT, const uint8_t* mT, int* pT, int W, int H, int frames,
                       cudaStream_t s);
+// iterations >= 1: b = (S_o / cnt - a o) - (1 - a) d formed inside the scan
+void launch_scan_b(const int* soT, const int* cntT, const int* oT, const double* dT,
+                   const uint8_t* mT, double alpha, double one_minus_alpha, double* pT, int W,
+                   int H, int frames, cudaStream_t s);
 // exact integer disc sums from an int BT prefix (disc counts, S_o)
-void launch_disc_isum(const uint8_t* valid, const int* ipsumT, int* out, const RefineArgs& a,
-                      int frames, long stride, cudaStream_t s);
-// iteration 0: avg = disc mean of o (FP64, reference order), b (normal layout)
-void launch_avg_b(const double* psumT, const uint8_t* valid, const int* cnt, const double* o,
-                  const double* d, double* avg, double* b, const RefineArgs& a, int frames,
-                  long stride, cudaStream_t s);
+void launch_disc_isum(const uint8_t* mT, const int* ipsumT, int* outT, const RefineArgs& a,
+                      int frames, cudaStream_t s);
+// iteration 0: avg = disc mean of o (FP64, reference order), b
+void launch_avg_b(const double* psumT, const uint8_t* mT, const int* cntT, const double* oT,
+                  const double* dT, double* avgT, double* bT, const RefineArgs& a, int frames,
+                  cudaStream_t s);
 // avg: the double disc mean of o (iteration 0) or nullptr to use the exact
 // integer disc sum `so` (iterations >= 1); o changes are appended to chg.
 // Re-picks whose FP32 window filter is ambiguous, or whose candidates leave
 // the window, are deferred to launch_repick_exact (warp per pixel, FP64).
 struct Deferred {
-  int pix, c_lo, mask, pad;  // mask: candidates c_lo + k to score exactly
+  int pix, c_lo, mask, pad;  // pix: BT index; mask: candidates c_lo + k to score exactly
   double d;
 };
 // o: integer disparities (written by every re-pick; read for the change list
-// when avg == nullptr, i.e. iterations >= 1).
-void launch_d_repick(const double* psumT, const uint8_t* valid, const int* cnt,
-                     const double* avg, const int* so, double* d, int* o,
+// when avg == nullptr, i.e. iterations >= 1). All per-pixel arrays BT.
+void launch_d_repick(const double* psumT, const uint8_t* mT, const int* cntT,
+                     const double* avgT, const int* soT, double* dT, int* oT,
                      const uint8_t* lgray, const uint8_t* rgray, const wscore_t* win,
                      const int* wbase, int2* chg, unsigned* chg_count, Deferred* defer,
-                     unsigned* defer_count, const RefineArgs& a, int frames, long stride,
-                     long gray_stride, unsigned long long* counters, cudaStream_t s);
-void launch_repick_exact(const Deferred* defer, const unsigned* defer_count, int* o,
+                     unsigned* defer_count, const RefineArgs& a, int frames, long gray_stride,
+                     cudaStream_t s);
+void launch_repick_exact(const Deferred* defer, const unsigned* defer_count, int* oT,
                          const uint8_t* lgray, const uint8_t* rgray, int2* chg,
-                         unsigned* chg_count, const RefineArgs& a, int frames, long stride,
-                         long gray_stride, unsigned long long* counters, cudaStream_t s);
+                         unsigned* chg_count, const RefineArgs& a, int frames, long gray_stride,
+                         unsigned long long* counters, cudaStream_t s);
 // S_o += delta over the disc of every changed pixel (exact integers).
-void launch_so_update(const int2* chg, const unsigned* chg_count, const uint8_t* valid,
-                      int* so, const RefineArgs& a, int frames, long stride, cudaStream_t s);
-void launch_refine_out(const double* d, const uint8_t* valid, const float* din, float* dout,
+void launch_so_update(const int2* chg, const unsigned* chg_count, const uint8_t* mT, int* soT,
+                      const RefineArgs& a, int frames, cudaStream_t s);
+// BT -> normal: refined disparity (valid ? float(d) : din), trace rows
+void launch_refine_out(const double* dT, const uint8_t* valid, const float* din, float* dout,
                        int W, int H, int frames, long stride, cudaStream_t s);
-void launch_int_to_double(const int* x, const uint8_t* valid, double* y, long n,
-                          cudaStream_t s);
+void launch_trace_rows(const int* oT, const double* dT, const uint8_t* valid, double* trace_o,
+                       double* trace_d, int W, int H, cudaStream_t s);
 
 struct CloudArgs {
   double fx, fy, cx, cy, baseline;

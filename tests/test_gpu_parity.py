@@ -122,6 +122,21 @@ def test_random_fields_remove_outliers(ss, orc):
                          "outliers")
 
 
+def test_remove_outliers_long_rays(ss, orc):
+    """Rays longer than one 32-bit word of the edge bitmaps, ragged sizes,
+    smooth fields with sparse spikes and holes (every direction must decide)."""
+    rng = np.random.default_rng(11)
+    for h, w in ((131, 203), (77, 64), (33, 95), (1, 40), (40, 1)):
+        base = 20 + np.add.outer(np.arange(h) * 0.05, np.arange(w) * 0.03)
+        f = (base + rng.standard_normal((h, w)) * 0.2).astype(np.float32)
+        sp = rng.random(f.shape) < 0.01
+        f[sp] += rng.uniform(-20, 20, sp.sum()).astype(np.float32)
+        v = (rng.random(f.shape) > 0.02).astype(np.uint8)
+        for r in (1, 5, 31, 32, 33, 40, 64, 70):
+            assert_map_equal(ss.remove_outliers(f, v, r, 2.5), orc.remove_outliers(f, v, r, 2.5),
+                             f"outliers {h}x{w} r={r}")
+
+
 def test_fill_holes_properties(ss, orc):
     """never touches valid pixels; support threshold honoured."""
     rng = np.random.default_rng(9)
