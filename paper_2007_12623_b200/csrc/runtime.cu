@@ -167,6 +167,26 @@ struct ss_ctx {
   DevBuf counters, trace_o, trace_d, so, chg, chg_count, mbt, defer, defer_count;
   int wtab_radius = -1;
 
+  // ss_stereo_batch pipeline: chunk k uses slot k % 2 — its inputs arrive on
+  // s_in while chunk k-1 computes on `stream` and chunk k-2's outputs leave on
+  // s_out. A slot owns the input buffers and the chain's output buffers, which
+  // are swapped into the ctx for the duration of its chunk's chain.
+  struct Slot {
+    DevBuf in_l, in_r, disp_b, valid_a, index, npoints, pts_f, colors, nrm_f;
+    cudaEvent_t in_ready = nullptr, done = nullptr, out_free = nullptr;
+  };
+  Slot slots[2];
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  void swap_outputs(Slot& sl) {
+    std::swap(disp_b, sl.disp_b);
+    std::swap(valid_a, sl.valid_a);
+    std::swap(index, sl.index);
+    std::swap(npoints, sl.npoints);
+    std::swap(pts_f, sl.pts_f);
+    std::swap(colors, sl.colors);
+    std::swap(nrm_f, sl.nrm_f);
+  }
+
   ss_ctx_stats stats{};
   // per-stage event timing (ss_ctx_enable_timing)
   bool timing = false;
@@ -192,6 +212,15 @@ struct ss_ctx {
                       &pts_f, &nrm_f, &colors, &pts_d, &nrm_d, &pixels, &pts4, &counters, &oi, &trace_o,
                       &trace_d, &so, &chg, &chg_count, &mbt, &defer, &defer_count})
       b->release();
+    for (Slot& sl : slots) {
+      for (DevBuf* b : {&sl.in_l, &sl.in_r, &sl.disp_b, &sl.valid_a, &sl.index, &sl.npoints,
+                        &sl.pts_f, &sl.colors, &sl.nrm_f})
+        b->release();
+      for (cudaEvent_t e : {sl.in_ready, sl.done, sl.out_free})
+        if (e) cudaEventDestroy(e);
+    }
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
     for (auto& r : pending) {
       ev_pool.push_back(r.a);
       ev_pool.push_back(r.b);
@@ -251,6 +280,11 @@ struct ss_ctx {
     device = dev;
     activate();
     ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (Slot& sl : slots)
+      for (cudaEvent_t* e : {&sl.in_ready, &sl.done, &sl.out_free})
+        ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
     counters.ensure(4 * sizeof(unsigned long long));
     ck(cudaMemsetAsync(counters.p, 0, 4 * sizeof(unsigned long long), stream), "memset");
   }
@@ -980,32 +1014,46 @@ ss_status ss_stereo_batch(ss_ctx* ctx, int32_t n, int32_t w, int32_t h, int32_t 
     ctx->activate();
     const long N = (long)w * h;
     const long in_bytes = (in_format == SS_IN_RGB ? 3 : 1) * N;
-    std::vector<int> np(ctx->max_batch);
-    for (int f0 = 0; f0 < n; f0 += ctx->max_batch) {
+    const bool cloud = (out_flags & (SS_OUT_CLOUD | SS_OUT_NORMALS)) != 0;
+    // Chunk k on slot k % 2: H2D (s_in) || chain (stream) || D2H (s_out).
+    // Cloud arrays leave at full per-frame capacity (no host round trip for
+    // the point counts); entries past n_points[f] are unspecified.
+    int k = 0;
+    for (int f0 = 0; f0 < n; f0 += ctx->max_batch, ++k) {
       const int m = std::min(ctx->max_batch, n - f0);
-      h2d(ctx->in_l, left + f0 * in_bytes, in_bytes * m, ctx->stream);
-      h2d(ctx->in_r, right + f0 * in_bytes, in_bytes * m, ctx->stream);
-      ctx->run_chain(m, w, h, in_format, ctx->in_l.as<uint8_t>(), ctx->in_r.as<uint8_t>(),
-                     out_flags);
-      if (out->disparity) d2h(out->disparity + f0 * N, ctx->last_disp, sizeof(float) * N * m, ctx->stream);
-      if (out->valid) d2h(out->valid + f0 * N, ctx->last_valid, N * m, ctx->stream);
-      if (out_flags & (SS_OUT_CLOUD | SS_OUT_NORMALS)) {
-        d2h(np.data(), ctx->npoints.p, sizeof(int) * m, ctx->stream);
-        if (out->index) d2h(out->index + f0 * N, ctx->index.p, sizeof(int) * N * m, ctx->stream);
-        sync(ctx);
-        for (int f = 0; f < m; ++f) {
-          const long k = np[f];
-          if (out->n_points) out->n_points[f0 + f] = (int32_t)k;
-          const long po = (long)(f0 + f) * N * 3, so = (long)f * N * 3;
-          if (out->points)
-            d2h(out->points + po, ctx->pts_f.as<float>() + so, sizeof(float) * 3 * k, ctx->stream);
-          if (out->colors) d2h(out->colors + po, ctx->colors.as<uint8_t>() + so, 3 * k, ctx->stream);
-          if (out->normals && (out_flags & SS_OUT_NORMALS))
-            d2h(out->normals + po, ctx->nrm_f.as<float>() + so, sizeof(float) * 3 * k, ctx->stream);
-        }
+      ss_ctx::Slot& sl = ctx->slots[k & 1];
+      ck(cudaStreamWaitEvent(ctx->s_in, sl.done, 0), "wait");  // slot inputs consumed
+      h2d(sl.in_l, left + f0 * in_bytes, in_bytes * m, ctx->s_in);
+      h2d(sl.in_r, right + f0 * in_bytes, in_bytes * m, ctx->s_in);
+      ck(cudaEventRecord(sl.in_ready, ctx->s_in), "record");
+      ck(cudaStreamWaitEvent(ctx->stream, sl.in_ready, 0), "wait");
+      ck(cudaStreamWaitEvent(ctx->stream, sl.out_free, 0), "wait");  // slot outputs drained
+      ctx->swap_outputs(sl);
+      try {
+        ctx->run_chain(m, w, h, in_format, sl.in_l.as<uint8_t>(), sl.in_r.as<uint8_t>(),
+                       out_flags);
+      } catch (...) {
+        ctx->swap_outputs(sl);
+        throw;
       }
-      sync(ctx);
+      ctx->swap_outputs(sl);
+      ck(cudaEventRecord(sl.done, ctx->stream), "record");
+      cudaStream_t so = ctx->s_out;
+      ck(cudaStreamWaitEvent(so, sl.done, 0), "wait");
+      if (out->disparity) d2h(out->disparity + f0 * N, ctx->last_disp, sizeof(float) * N * m, so);
+      if (out->valid) d2h(out->valid + f0 * N, ctx->last_valid, N * m, so);
+      if (cloud) {
+        if (out->n_points) d2h(out->n_points + f0, sl.npoints.p, sizeof(int) * m, so);
+        if (out->index) d2h(out->index + f0 * N, sl.index.p, sizeof(int) * N * m, so);
+        if (out->points) d2h(out->points + f0 * N * 3, sl.pts_f.p, sizeof(float) * 3 * N * m, so);
+        if (out->colors) d2h(out->colors + f0 * N * 3, sl.colors.p, 3 * N * m, so);
+        if (out->normals && (out_flags & SS_OUT_NORMALS))
+          d2h(out->normals + f0 * N * 3, sl.nrm_f.p, sizeof(float) * 3 * N * m, so);
+      }
+      ck(cudaEventRecord(sl.out_free, so), "record");
     }
+    ck(cudaStreamSynchronize(ctx->s_out), "cudaStreamSynchronize");
+    sync(ctx);
   });
 }
 
