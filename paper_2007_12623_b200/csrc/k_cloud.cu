@@ -267,78 +267,140 @@ __device__ void sym3_smallest(const T a[6], T ev[3], T n[3]) {
   n[2] = cr[bi][2] * inv;
 }
 
-constexpr int kNW = 3;            // kNormalWindowHalf (cloud.cpp:10)
+constexpr int kNW = 3;              // kNormalWindowHalf (cloud.cpp:10)
 constexpr int kNTX = 32, kNTY = 8;  // output tile
+constexpr int kNIX = kNTX + 2 * kNW, kNIY = kNTY + 2 * kNW;  // input tile (38 x 14)
+constexpr int kNQ = 10;             // window moments: n, sx, sy, sz, sxx, sxy, sxz, syy, syz, szz
+constexpr int kNSeg = 4;            // output columns per horizontal running-sum task
 
-// Normals from a shared-memory tile of pixel-indexed float points. Neighbour
-// coordinates are taken relative to the centre point (local frame, no
-// cancellation at 100 mm depth), mean and covariance in two passes. Windows
-// whose middle eigenvalue is within 1e-4 of degenerate are re-fitted in FP64
-// so the reference's 1e-9 acceptance test (cloud.cpp:81) decides them.
-__global__ void __launch_bounds__(kNTX * kNTY)
+struct NormalSmem {
+  double p[4][kNIY][kNIX];    // per input pixel: point flag (1/0), x, y, z (0 where no point)
+  double h[kNQ][kNIY][kNTX];  // 7-wide horizontal window sums of the kNQ quantities
+};
+
+// Normals from 7x7 window moments (cloud.cpp:41-90). The window's point count,
+// coordinate sums and second-moment sums are box sums of per-point
+// quantities, computed in FP64 for a whole 32 x 8 tile at once (7-wide
+// horizontal running sums of the per-point products, 7-high vertical sums), so a pixel
+// costs ~10 products + ~65 adds instead of two 49-point passes. The
+// covariance sum (q - mean)(q - mean)^T = S_qq - S_q S_q^T / n is formed in
+// FP64 (point magnitudes <= 1e4 mm keep the cancellation error ~1e-7 of the
+// entries) and solved in FP32 (closed-form eigenpairs); windows whose middle
+// eigenvalue is within 1e-4 of degenerate are re-fitted from FP64 points so
+// the reference's 1e-9 acceptance test (cloud.cpp:81) decides them.
+__global__ void __launch_bounds__(kNTX * kNTY, 2)
     k_cloud_normals(const float4* __restrict__ pts4, const float* __restrict__ disp, int W,
                     int H, CloudArgs cargs, double* __restrict__ nrm_d,
                     float* __restrict__ nrm_f, const int* __restrict__ index, long stride) {
-  __shared__ float4 tile[kNTY + 2 * kNW][kNTX + 2 * kNW];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  NormalSmem& S = *reinterpret_cast<NormalSmem*>(smem_raw);
   const long f = blockIdx.z;
   pts4 += f * stride;
   const int bx = blockIdx.x * kNTX, by = blockIdx.y * kNTY;
-  for (int t = threadIdx.y * kNTX + threadIdx.x; t < (kNTY + 2 * kNW) * (kNTX + 2 * kNW);
-       t += kNTX * kNTY) {
-    const int ty = t / (kNTX + 2 * kNW), tx = t % (kNTX + 2 * kNW);
+  const int tid = threadIdx.y * kNTX + threadIdx.x;
+  for (int t = tid; t < kNIY * kNIX; t += kNTX * kNTY) {
+    const int ty = t / kNIX, tx = t - ty * kNIX;
     const int gx = bx + tx - kNW, gy = by + ty - kNW;
-    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (gx >= 0 && gx < W && gy >= 0 && gy < H) q = pts4[(long)gy * W + gx];
-    tile[ty][tx] = q;
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (gx >= 0 && gx < W && gy >= 0 && gy < H) p = pts4[(long)gy * W + gx];
+    S.p[0][ty][tx] = p.w != 0.f ? 1.0 : 0.0;
+    S.p[1][ty][tx] = p.x;
+    S.p[2][ty][tx] = p.y;
+    S.p[3][ty][tx] = p.z;
+  }
+  __syncthreads();
+  // horizontal: task = (input row, kNSeg output columns); the 10 quantities of
+  // the segment's kNSeg + 6 points are formed on the fly (products of floats
+  // are exact in FP64) and slid across the segment.
+  constexpr int kSegs = kNTX / kNSeg;
+  for (int t = tid; t < kNIY * kSegs; t += kNTX * kNTY) {
+    const int r = t / kSegs, c0 = (t % kSegs) * kNSeg;
+    auto quant = [&](int c, double (&q)[kNQ]) {
+      const double w = S.p[0][r][c], x = S.p[1][r][c], y = S.p[2][r][c], z = S.p[3][r][c];
+      q[0] = w;
+      q[1] = x;
+      q[2] = y;
+      q[3] = z;
+      q[4] = x * x;
+      q[5] = x * y;
+      q[6] = x * z;
+      q[7] = y * y;
+      q[8] = y * z;
+      q[9] = z * z;
+    };
+    double acc[kNQ], q[kNQ];
+#pragma unroll
+    for (int k = 0; k < kNQ; ++k) acc[k] = 0.0;
+#pragma unroll
+    for (int du = 0; du <= 2 * kNW; ++du) {
+      quant(c0 + du, q);
+#pragma unroll
+      for (int k = 0; k < kNQ; ++k) acc[k] += q[k];
+    }
+#pragma unroll
+    for (int k = 0; k < kNQ; ++k) S.h[k][r][c0] = acc[k];
+#pragma unroll
+    for (int j = 1; j < kNSeg; ++j) {
+      double qo[kNQ];
+      quant(c0 + j + 2 * kNW, q);
+      quant(c0 + j - 1, qo);
+#pragma unroll
+      for (int k = 0; k < kNQ; ++k) {
+        acc[k] += q[k] - qo[k];
+        S.h[k][r][c0 + j] = acc[k];
+      }
+    }
   }
   __syncthreads();
   const int u = bx + threadIdx.x, v = by + threadIdx.y;
   if (u >= W || v >= H) return;
-  const float4 c = tile[threadIdx.y + kNW][threadIdx.x + kNW];
+  const float4 c = pts4[(long)v * W + u];
   if (c.w == 0.f) return;
   const int k = index[f * stride + (long)v * W + u];
-  float sx = 0.f, sy = 0.f, sz = 0.f;
-  int count = 0;
+  double m[kNQ];
 #pragma unroll
-  for (int dv = 0; dv <= 2 * kNW; ++dv)
+  for (int q = 0; q < kNQ; ++q) {
+    double acc = 0.0;
 #pragma unroll
-    for (int du = 0; du <= 2 * kNW; ++du) {
-      const float4 q = tile[threadIdx.y + dv][threadIdx.x + du];
-      if (q.w != 0.f) {
-        sx += q.x - c.x;
-        sy += q.y - c.y;
-        sz += q.z - c.z;
-        ++count;
-      }
-    }
+    for (int dv = 0; dv <= 2 * kNW; ++dv) acc += S.h[q][threadIdx.y + dv][threadIdx.x];
+    m[q] = acc;
+  }
+  const int count = (int)m[0];
   float n[3] = {0.f, 0.f, -1.f};
   bool fitted = false;
   if (count >= 3) {
-    const float inv = 1.f / (float)count;
-    const float mx = sx * inv, my = sy * inv, mz = sz * inv;
-    float a[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int dv = 0; dv <= 2 * kNW; ++dv)
-#pragma unroll
-      for (int du = 0; du <= 2 * kNW; ++du) {
-        const float4 q = tile[threadIdx.y + dv][threadIdx.x + du];
-        if (q.w != 0.f) {
-          const float x = (q.x - c.x) - mx, y = (q.y - c.y) - my, z = (q.z - c.z) - mz;
-          a[0] += x * x;
-          a[1] += x * y;
-          a[2] += x * z;
-          a[3] += y * y;
-          a[4] += y * z;
-          a[5] += z * z;
-        }
-      }
+    const double inv = 1.0 / m[0];
+    const double ad[6] = {m[4] - m[1] * m[1] * inv, m[5] - m[1] * m[2] * inv,
+                          m[6] - m[1] * m[3] * inv, m[7] - m[2] * m[2] * inv,
+                          m[8] - m[2] * m[3] * inv, m[9] - m[3] * m[3] * inv};
+    const float a[6] = {(float)ad[0], (float)ad[1], (float)ad[2],
+                        (float)ad[3], (float)ad[4], (float)ad[5]};
     float ev[3], e[3];
     sym3_smallest<float>(a, ev, e);
     const float scale = fmaxf(1.f, ev[2]);
     if (ev[1] > 1e-4f * scale) {
-      n[0] = e[0];
-      n[1] = e[1];
-      n[2] = e[2];
+      // One FP64 inverse-iteration step, x = adj(A - mu I) e: the FP32
+      // eigenvector's error shrinks by |lambda0 - mu| / |lambda1 - mu|, so
+      // small eigen gaps (1e-3 of lambda2) still give ~1e-7 rad normals.
+      const double mu = ev[0];
+      const double b00 = ad[0] - mu, b11 = ad[3] - mu, b22 = ad[5] - mu;
+      const double b01 = ad[1], b02 = ad[2], b12 = ad[4];
+      const double c00 = b11 * b22 - b12 * b12, c01 = b02 * b12 - b01 * b22,
+                   c02 = b01 * b12 - b02 * b11, c11 = b00 * b22 - b02 * b02,
+                   c12 = b01 * b02 - b00 * b12, c22 = b00 * b11 - b01 * b01;
+      const double x0 = c00 * e[0] + c01 * e[1] + c02 * e[2];
+      const double x1 = c01 * e[0] + c11 * e[1] + c12 * e[2];
+      const double x2 = c02 * e[0] + c12 * e[1] + c22 * e[2];
+      const double len = sqrt(x0 * x0 + x1 * x1 + x2 * x2);
+      if (len > 0.0 && isfinite(len)) {
+        n[0] = (float)(x0 / len);
+        n[1] = (float)(x1 / len);
+        n[2] = (float)(x2 / len);
+      } else {
+        n[0] = e[0];
+        n[1] = e[1];
+        n[2] = e[2];
+      }
       fitted = true;
     } else {
       // Near-degenerate neighbourhood: refit in FP64 from FP64 points.
@@ -346,7 +408,7 @@ __global__ void __launch_bounds__(kNTX * kNTY)
       double mean[3] = {0.0, 0.0, 0.0};
       for (int dv = -kNW; dv <= kNW; ++dv)
         for (int du = -kNW; du <= kNW; ++du) {
-          if (tile[threadIdx.y + kNW + dv][threadIdx.x + kNW + du].w == 0.f) continue;
+          if (S.p[0][threadIdx.y + kNW + dv][threadIdx.x + kNW + du] == 0.0) continue;
           point_of(cargs, u + du, v + dv, (double)disp[f * stride + (long)(v + dv) * W + u + du], pd);
           mean[0] += pd[0];
           mean[1] += pd[1];
@@ -358,7 +420,7 @@ __global__ void __launch_bounds__(kNTX * kNTY)
       double ad[6] = {0, 0, 0, 0, 0, 0};
       for (int dv = -kNW; dv <= kNW; ++dv)
         for (int du = -kNW; du <= kNW; ++du) {
-          if (tile[threadIdx.y + kNW + dv][threadIdx.x + kNW + du].w == 0.f) continue;
+          if (S.p[0][threadIdx.y + kNW + dv][threadIdx.x + kNW + du] == 0.0) continue;
           point_of(cargs, u + du, v + dv, (double)disp[f * stride + (long)(v + dv) * W + u + du], pd);
           const double x = pd[0] - mean[0], y = pd[1] - mean[1], z = pd[2] - mean[2];
           ad[0] += x * x;
@@ -379,8 +441,7 @@ __global__ void __launch_bounds__(kNTX * kNTY)
     }
   }
   double nd[3] = {n[0], n[1], n[2]};
-  double pc[3];
-  point_of(cargs, u, v, (double)disp[f * stride + (long)v * W + u], pc);
+  const double pc[3] = {c.x, c.y, c.z};
   if (!fitted) {
     const double len = sqrt(pc[0] * pc[0] + pc[1] * pc[1] + pc[2] * pc[2]);
     nd[0] = -pc[0] / len;
@@ -411,7 +472,14 @@ void launch_cloud_normals(const float4* pts4, const float* disp, const int* inde
   if (W <= 0 || H <= 0 || frames <= 0) return;
   dim3 b(kNTX, kNTY);
   dim3 grid((W + kNTX - 1) / kNTX, (H + kNTY - 1) / kNTY, frames);
-  k_cloud_normals<<<grid, b, 0, s>>>(pts4, disp, W, H, c, nrm_d, nrm_f, index, stride);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_cloud_normals, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(NormalSmem));
+    configured = true;
+  }
+  k_cloud_normals<<<grid, b, sizeof(NormalSmem), s>>>(pts4, disp, W, H, c, nrm_d, nrm_f, index,
+                                                      stride);
 }
 
 }  // namespace ssb
