@@ -116,7 +116,7 @@ __device__ __forceinline__ Tile<T> tile_issue(T* sm, const T* psf, const CUtenso
   }
   __syncthreads();
   Tile<T> tl;
-  tl.CW = W + 1;
+  tl.CW = psum_cw(W, R);
   tl.t = sm;
   tl.g = psf;
   tl.pitch = glob ? 0 : rows;
@@ -167,18 +167,19 @@ __device__ __forceinline__ T disc_sum_fixed(const T* q, std::integer_sequence<in
   return s;
 }
 
-// Interior pixels with a compile-time radius read the tile at immediate
-// offsets from one base pointer.
+// With a compile-time radius (always a shared-memory tile) every pixel reads
+// the tile at immediate offsets from one base pointer: the extended prefix
+// layout (psum_cw) makes the clipped spans of border pixels read the values
+// the clipped indices would, and out-of-image rows contribute +0.0 terms.
 template <int RF, typename T>
 __device__ __forceinline__ T disc_sum_any(const Tile<T>& P, const int* span, int W, int H,
                                           int u, int v, int Rr) {
   if constexpr (RF > 0) {
-    if (u >= RF && u + RF <= W - 1 && v >= RF && v + RF <= H - 1) {
-      const T* q = P.t + (u - P.c0) * tile_rows(RF) + (v - P.r0);
-      return disc_sum_fixed<T, RF>(q, std::make_integer_sequence<int, 2 * RF + 1>{});
-    }
+    const T* q = P.t + (u - P.c0) * tile_rows(RF) + (v - P.r0);
+    return disc_sum_fixed<T, RF>(q, std::make_integer_sequence<int, 2 * RF + 1>{});
+  } else {
+    return disc_sum_generic(P, span, W, H, u, v, Rr);
   }
-  return disc_sum_generic(P, span, W, H, u, v, Rr);
 }
 
 template <typename K>
@@ -193,7 +194,7 @@ template <typename T>
 bool psum_map(CUtensorMap* m, const T* psumT, const RefineArgs& a, int frames, bool tile) {
   *m = CUtensorMap{};
   if (!tile) return false;
-  if (make_psum_tmap(m, psumT, std::is_same<T, double>::value, a.g.W, a.g.H, frames,
+  if (make_psum_tmap(m, psumT, std::is_same<T, double>::value, a.g.W, a.g.H, a.radius, frames,
                      tile_nb(a.radius), tile_cols(a.radius)))
     return true;
   static bool warned = false;
@@ -206,8 +207,8 @@ bool psum_map(CUtensorMap* m, const T* psumT, const RefineArgs& a, int frames, b
 
 }  // namespace
 
-bool make_psum_tmap(CUtensorMap* map, const void* base, bool is_double, int W, int H, int frames,
-                    int nb, int cols) {
+bool make_psum_tmap(CUtensorMap* map, const void* base, bool is_double, int W, int H, int ext,
+                    int frames, int nb, int cols) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     void* fn = nullptr;
@@ -219,7 +220,7 @@ bool make_psum_tmap(CUtensorMap* map, const void* base, bool is_double, int W, i
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   const cuuint64_t es = is_double ? 8 : 4;
-  const cuuint64_t RB = (H + 31) / 32, CW = W + 1;
+  const cuuint64_t RB = (H + 31) / 32, CW = psum_cw(W, ext);
   const cuuint64_t dims[4] = {32, RB, CW, (cuuint64_t)frames};
   const cuuint64_t strides[3] = {CW * 32 * es, 32 * es, RB * CW * 32 * es};
   const cuuint32_t box[4] = {32, (cuuint32_t)nb, (cuuint32_t)cols, 1};
@@ -348,7 +349,7 @@ __global__ void __launch_bounds__(kThreads)
   const long f = blockIdx.z;
   const int W = a.g.W, H = a.g.H, R = a.radius;
   const long bs = bt_frame(W, H, 0);
-  const Tile<int> P = tile_issue<RF>(reinterpret_cast<int*>(smem), ipsumT + f * bt_frame(W, H, 1),
+  const Tile<int> P = tile_issue<RF>(reinterpret_cast<int*>(smem), ipsumT + f * bt_frame(W, H, 1 + R),
                                      &map, W, R, glob, &bar);
   tile_wait(&bar);
   const int v = blockIdx.y * 32 + threadIdx.x;
@@ -389,7 +390,7 @@ __global__ void __launch_bounds__(kThreads)
   const int W = a.g.W, H = a.g.H, R = a.radius;
   const long bs = bt_frame(W, H, 0);
   const Tile<double> P = tile_issue<RF>(reinterpret_cast<double*>(smem),
-                                        psumT + f * bt_frame(W, H, 1), &map, W, R, glob, &bar);
+                                        psumT + f * bt_frame(W, H, 1 + R), &map, W, R, glob, &bar);
   tile_wait(&bar);
   const int v = blockIdx.y * 32 + threadIdx.x;
 #pragma unroll
@@ -551,23 +552,20 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
 #pragma unroll
     for (int i = 0; i < 6; ++i) wd[i] = wv.p[min(w0 + i, kWin / 2 - 1) * kWinPlane];
     const unsigned sel_e = par ? 0x3232u : 0x1010u, sel_o = par ? 0x5454u : 0x3232u;
+    // Branch-free over the 11 slots: slots past c_hi cost +inf. The FMA
+    // rounds once where M16 + (eta df) df rounded twice, inside the same bar.
     float best_cost = INFINITY, second = INFINITY;
-    float cf = (float)c_lo;
+    const int nk = c_hi - c_lo;
 #pragma unroll
     for (int k = 0; k < kMaxCand; ++k) {
-      if (c_lo + k <= c_hi) {
-        const uint32_t hw = (k & 1) ? __byte_perm(wd[k >> 1], wd[(k + 1) >> 1], sel_o)
-                                    : __byte_perm(wd[k >> 1], 0u, sel_e);
-        const float m = __half2float(__ushort_as_half((unsigned short)(hw & 0xFFFFu)));
-        const float df = cf - dv_f;
-        const float cost = m + a.eta_f * df * df;
-        second = fminf(second, fmaxf(best_cost, cost));
-        if (cost < best_cost) {
-          best_cost = cost;
-          best = c_lo + k;
-        }
-      }
-      cf += 1.f;
+      const uint32_t hw = (k & 1) ? __byte_perm(wd[k >> 1], wd[(k + 1) >> 1], sel_o)
+                                  : __byte_perm(wd[k >> 1], 0u, sel_e);
+      const float m = __half2float(__ushort_as_half((unsigned short)(hw & 0xFFFFu)));
+      const float df = (float)((float)c_lo + (float)k) - dv_f;
+      const float cost = k <= nk ? __fmaf_rn(__fmul_rn(a.eta_f, df), df, m) : INFINITY;
+      second = fminf(second, fmaxf(best_cost, cost));
+      best = cost < best_cost ? c_lo + k : best;
+      best_cost = fminf(best_cost, cost);
     }
     if (second * (1.f - kEps) - errE > best_cost * (1.f + kEps) + errE) return best;
     // Ambiguous: FP64 costs (exact E, exact clamped/undefined M) with error
@@ -639,7 +637,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   // windows + wbase, S_o + o (or avg), cnt, mask
   const unsigned extra = (win ? (kWin / 2) * npx * 4 + npx * 4 : 0) + npx * 8 + npx * 4 + npx;
   const Tile<double> P = tile_issue<RF>(reinterpret_cast<double*>(smem),
-                                        psumT + f * bt_frame(W, H, 1), &map, W, R, glob, &bar,
+                                        psumT + f * bt_frame(W, H, 1 + R), &map, W, R, glob, &bar,
                                         extra);
   if (tid == 0) {
     // the tile's per-pixel fields: contiguous BT ranges of npx entries

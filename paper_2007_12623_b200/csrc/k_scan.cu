@@ -42,7 +42,7 @@ __device__ __forceinline__ T add_rn(T s, T x) {
 template <typename T>
 __global__ void __launch_bounds__(32)
     k_scan_bt(const T* __restrict__ xT, const uint8_t* __restrict__ mT, T* __restrict__ pT, int W,
-              int RB) {
+              int RB, int ext) {
   __shared__ alignas(128) T xb[2][kChunk][32];
   __shared__ alignas(128) uint8_t mb[2][kChunk][32];
   __shared__ alignas(8) uint64_t bar[2];
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(32)
   const bool ones = xT == nullptr;
   const T* xs = ones ? nullptr : xT + (f * RB + rb) * (long)W * 32;
   const uint8_t* ms = mT + (f * RB + rb) * (long)W * 32;
-  T* dst = pT + (f * RB + rb) * (long)(W + 1) * 32;
+  T* dst = pT + (f * RB + rb) * (long)psum_cw(W, ext) * 32;
   const int nchunks = (W + kChunk - 1) / kChunk;
   if (lane == 0) {
     mbar_init(&bar[0], 1);
@@ -98,20 +98,21 @@ __global__ void __launch_bounds__(32)
     }
     __syncwarp();
   }
+  for (int c = W + 1; c < W + 1 + ext; ++c) dst[(long)c * 32 + lane] = s;  // row total
 }
 
-void launch_scan_bt_d(const double* xT, const uint8_t* mT, double* pT, int W, int H, int frames,
+void launch_scan_bt_d(const double* xT, const uint8_t* mT, double* pT, int W, int H, int ext,
+                      int frames, cudaStream_t s) {
+  if (W <= 0 || H <= 0 || frames <= 0) return;
+  const int RB = (H + 31) / 32;
+  k_scan_bt<double><<<dim3(RB, frames), 32, 0, s>>>(xT, mT, pT, W, RB, ext);
+}
+
+void launch_scan_bt_i(const int* xT, const uint8_t* mT, int* pT, int W, int H, int ext, int frames,
                       cudaStream_t s) {
   if (W <= 0 || H <= 0 || frames <= 0) return;
   const int RB = (H + 31) / 32;
-  k_scan_bt<double><<<dim3(RB, frames), 32, 0, s>>>(xT, mT, pT, W, RB);
-}
-
-void launch_scan_bt_i(const int* xT, const uint8_t* mT, int* pT, int W, int H, int frames,
-                      cudaStream_t s) {
-  if (W <= 0 || H <= 0 || frames <= 0) return;
-  const int RB = (H + 31) / 32;
-  k_scan_bt<int><<<dim3(RB, frames), 32, 0, s>>>(xT, mT, pT, W, RB);
+  k_scan_bt<int><<<dim3(RB, frames), 32, 0, s>>>(xT, mT, pT, W, RB, ext);
 }
 
 // Iterations >= 1: the correction b (smoothing.cpp:91-99) formed from the
@@ -138,14 +139,14 @@ struct ScanBSmem {
 __global__ void __launch_bounds__(32 * kScanBWarps)
     k_scan_b(const int* __restrict__ soT, const int* __restrict__ cntT, const int* __restrict__ oT,
              const double* __restrict__ dT, const uint8_t* __restrict__ mT, double alpha,
-             double one_minus_alpha, double* __restrict__ pT, int W, int RB) {
+             double one_minus_alpha, double* __restrict__ pT, int W, int RB, int ext) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   ScanBSmem& S = *reinterpret_cast<ScanBSmem*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long f = blockIdx.y;
   const int rb = blockIdx.x;
   const long base = (f * RB + rb) * (long)W * 32;
-  double* dst = pT + (f * RB + rb) * (long)(W + 1) * 32;
+  double* dst = pT + (f * RB + rb) * (long)psum_cw(W, ext) * 32;
   const int nchunks = (W + kChunkB - 1) / kChunkB;
   auto issue = [&](int k) {
     const int c0 = k * kChunkB, cols = min(kChunkB, W - c0);
@@ -210,11 +211,13 @@ __global__ void __launch_bounds__(32 * kScanBWarps)
       issue(k + 2);  // raw[k & 1] was last read in step k
     }
   }
+  if (warp == 0)
+    for (int c = W + 1; c < W + 1 + ext; ++c) dst[(long)c * 32 + lane] = s;  // row total
 }
 
 void launch_scan_b(const int* soT, const int* cntT, const int* oT, const double* dT,
                    const uint8_t* mT, double alpha, double one_minus_alpha, double* pT, int W,
-                   int H, int frames, cudaStream_t s) {
+                   int H, int ext, int frames, cudaStream_t s) {
   if (W <= 0 || H <= 0 || frames <= 0) return;
   const int RB = (H + 31) / 32;
   static bool configured = false;
@@ -224,7 +227,7 @@ void launch_scan_b(const int* soT, const int* cntT, const int* oT, const double*
     configured = true;
   }
   k_scan_b<<<dim3(RB, frames), 32 * kScanBWarps, sizeof(ScanBSmem), s>>>(
-      soT, cntT, oT, dT, mT, alpha, one_minus_alpha, pT, W, RB);
+      soT, cntT, oT, dT, mT, alpha, one_minus_alpha, pT, W, RB, ext);
 }
 
 // ---------------- normal-layout count scan (cleanup disc support) ----------------

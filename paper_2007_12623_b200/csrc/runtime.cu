@@ -437,7 +437,8 @@ struct ss_ctx {
     Stage st(this, 5);
     const int W = g.W, H = g.H;
     const long N = g.N();
-    const long bs = bt_frame(W, H, 0), bp = bt_frame(W, H, 1);  // BT frame strides
+    const int r = params.smoothing_radius;
+    const long bs = bt_frame(W, H, 0), bp = bt_frame(W, H, 1 + r);  // BT frame strides
     // every refinement field is BT (ss_internal.cuh)
     o.ensure(sizeof(double) * bs * n);     // iteration-0 o (double)
     d.ensure(sizeof(double) * bs * n);
@@ -447,7 +448,6 @@ struct ss_ctx {
     pcnt.ensure(sizeof(int) * bp * n);     // BT prefix (int)
     mbt.ensure(bs * n);                    // BT mask
     cnt.ensure(sizeof(int) * bs * n);
-    const int r = params.smoothing_radius;
     std::vector<int> sp(std::max(r, 0) + 1);
     for (int dy = 0; dy <= r; ++dy)
       sp[dy] = (int)std::floor(std::sqrt((double)r * r - (double)dy * dy));
@@ -476,7 +476,7 @@ struct ss_ctx {
     uint8_t* mT = mbt.as<uint8_t>();
     launch_refine_init(disp_a.as<float>(), valid_a.as<uint8_t>(), mT, o.as<double>(),
                        d.as<double>(), W, H, n, N, bs, stream);
-    launch_scan_bt_i(nullptr, mT, pcnt.as<int>(), W, H, n, stream);  // per-row valid counts
+    launch_scan_bt_i(nullptr, mT, pcnt.as<int>(), W, H, r, n, stream);  // per-row valid counts
     launch_disc_isum(mT, pcnt.as<int>(), cnt.as<int>(), a, n, stream);  // disc counts
     stats.kernel_launches += 3;
     so.ensure(sizeof(int) * bs * n);
@@ -508,22 +508,22 @@ struct ss_ctx {
     for (int it = 0; it < iters; ++it) {
       if (it == 0) {
         // o is the cleanup output (fractional fills): the reference's FP64 path.
-        launch_scan_bt_d(o.as<double>(), mT, psum.as<double>(), W, H, n, stream);
+        launch_scan_bt_d(o.as<double>(), mT, psum.as<double>(), W, H, r, n, stream);
         launch_avg_b(psum.as<double>(), mT, cnt.as<int>(), o.as<double>(), d.as<double>(),
                      avg.as<double>(), b.as<double>(), a, n, stream);
-        launch_scan_bt_d(b.as<double>(), mT, psum.as<double>(), W, H, n, stream);
+        launch_scan_bt_d(b.as<double>(), mT, psum.as<double>(), W, H, r, n, stream);
         stats.kernel_launches += 3;
         repick(avg.as<double>(), nullptr, nullptr);
         if (iters > 1) {
           // o is integer-valued from here on: exact integer disc sums S_o.
-          launch_scan_bt_i(op, mT, pcnt.as<int>(), W, H, n, stream);
+          launch_scan_bt_i(op, mT, pcnt.as<int>(), W, H, r, n, stream);
           launch_disc_isum(mT, pcnt.as<int>(), so.as<int>(), a, n, stream);
           stats.kernel_launches += 2;
         }
       } else {
         ck(cudaMemsetAsync(chg_count.p, 0, sizeof(unsigned) * n, stream), "memset");
         launch_scan_b(so.as<int>(), cnt.as<int>(), op, d.as<double>(), mT, a.alpha,
-                      a.one_minus_alpha, psum.as<double>(), W, H, n, stream);
+                      a.one_minus_alpha, psum.as<double>(), W, H, r, n, stream);
         stats.kernel_launches += 1;
         repick(nullptr, chg.as<int2>(), chg_count.as<unsigned>());
         if (it + 1 < iters) {

@@ -152,16 +152,24 @@ __host__ __device__ inline void bt_decode(int W, long idx, int& v, int& u) {
 void launch_refine_init(const float* disp, const uint8_t* valid, uint8_t* mT, double* oT,
                         double* dT, int W, int H, int frames, long stride, long bs,
                         cudaStream_t s);
-// masked serial row prefix (psum[.][0] = 0, W + 1 columns, BT layout);
-// xT == nullptr for the int scan means x = 1 (disc counts)
-void launch_scan_bt_d(const double* xT, const uint8_t* mT, double* pT, int W, int H, int frames,
-                      cudaStream_t s);
-void launch_scan_bt_i(const int* xT, const uint8_t* mT, int* pT, int W, int H, int frames,
+// Row prefixes carry `ext` (= the smoothing radius) columns past psum[W]
+// that repeat the row total: a disc span clipped at the right edge,
+// min(W - 1, u + sx) + 1 = W, reads the same value unclipped at u + sx + 1,
+// and columns left of 0 arrive as TMA zero fill = psum[0]. With all-zero
+// rows past H (mask 0) and zero-filled rows above 0 (whose +0.0 terms leave
+// the reference's double sum unchanged), every pixel takes the unclipped
+// compile-time disc gather.
+__host__ __device__ inline int psum_cw(int W, int ext) { return W + 1 + ext; }
+// masked serial row prefix (psum[.][0] = 0, psum_cw(W, ext) columns, BT
+// layout); xT == nullptr for the int scan means x = 1 (disc counts)
+void launch_scan_bt_d(const double* xT, const uint8_t* mT, double* pT, int W, int H, int ext,
+                      int frames, cudaStream_t s);
+void launch_scan_bt_i(const int* xT, const uint8_t* mT, int* pT, int W, int H, int ext, int frames,
                       cudaStream_t s);
 // iterations >= 1: b = (S_o / cnt - a o) - (1 - a) d formed inside the scan
 void launch_scan_b(const int* soT, const int* cntT, const int* oT, const double* dT,
                    const uint8_t* mT, double alpha, double one_minus_alpha, double* pT, int W,
-                   int H, int frames, cudaStream_t s);
+                   int H, int ext, int frames, cudaStream_t s);
 // exact integer disc sums from an int BT prefix (disc counts, S_o)
 void launch_disc_isum(const uint8_t* mT, const int* ipsumT, int* outT, const RefineArgs& a,
                       int frames, cudaStream_t s);

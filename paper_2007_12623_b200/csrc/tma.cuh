@@ -63,7 +63,7 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
 // columns) that delivers a block's tile column-major: dims {32 rows, row
 // blocks, columns, frames} with strides {es, CW*32*es, 32*es, frame}, box
 // {32, nb, cols, 1} -> shared [cols][nb * 32 rows].
-bool make_psum_tmap(CUtensorMap* map, const void* base, bool is_double, int W, int H, int frames,
-                    int nb, int cols);
+bool make_psum_tmap(CUtensorMap* map, const void* base, bool is_double, int W, int H, int ext,
+                    int frames, int nb, int cols);
 
 }  // namespace ssb
