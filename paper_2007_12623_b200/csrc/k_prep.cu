@@ -1,8 +1,8 @@
-// Frame preparation kernels: luma, parity planes, chessboard window stats.
+// Frame preparation kernels: luma, tap words / parity planes, chessboard window stats.
 //
 //   k_to_gray   to_gray, matcher.cpp:21-30 (FP64, no FMA, lround)
-//   k_planes    parity-split rows for the dp4a cross-correlation (layout in
-//               ss_internal.cuh)
+//   k_ltap      left tap words and k_rcopy byte-shifted right parity planes
+//               for the dp4a cross-correlation (layout in ss_internal.cuh)
 //   k_stats     patch_stats, matcher.cpp:112-137, plus the float reciprocal
 //               sqrt of the variance used by the FP32 filter of the WTA sweep
 //
@@ -37,39 +37,64 @@ void launch_to_gray(const uint8_t* rgb, uint8_t* gray, long n, int frames, long 
                                                               out_stride);
 }
 
-// One thread per 32-bit word of a plane row; padding words are written as 0.
-__global__ void k_planes(const uint8_t* __restrict__ gray, uint8_t* __restrict__ plane,
-                         int W, int H, int PB, int PP, long gray_stride, long plane_stride) {
+// Left tap words, one uint4 per pixel (u, y) (ss_internal.cuh):
+//   x = L(u-4) L(u-2) L(u) L(u+2)   y = L(u+4) 0 0 0
+//   z = L(u-5) L(u-3) L(u-1) L(u+1) w = L(u+3) L(u+5) 0 0
+// byte 0 lowest; bytes outside the row are 0 (such pixels never score).
+__global__ void k_ltap(const uint8_t* __restrict__ gray, uint4* __restrict__ ltap, int W,
+                       long gray_stride, long tap_stride) {
   const long f = blockIdx.z;
-  gray += f * gray_stride;
-  plane += f * plane_stride;
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y;
+  if (u >= W) return;
+  const uint8_t* row = gray + f * gray_stride + (long)y * W;
+  auto at = [&](int x) -> uint32_t { return (x >= 0 && x < W) ? (uint32_t)__ldg(row + x) : 0u; };
+  uint4 t;
+  t.x = at(u - 4) | at(u - 2) << 8 | at(u) << 16 | at(u + 2) << 24;
+  t.y = at(u + 4);
+  t.z = at(u - 5) | at(u - 3) << 8 | at(u - 1) << 16 | at(u + 1) << 24;
+  t.w = at(u + 3) | at(u + 5) << 8;
+  ltap[f * tap_stride + (long)y * W + u] = t;
+}
+
+// Right parity planes in 4 byte-shifted copies: rcopy[y][par][s] byte j =
+// plane byte j + s, plane byte i = R(2 (i - PB) + par) (0 in the padding), so
+// any byte offset of a plane row starts an aligned word in one of the copies.
+// One thread per output word.
+__global__ void k_rcopy(const uint8_t* __restrict__ gray, uint32_t* __restrict__ rcopy, int W,
+                        int PB, int PP, long gray_stride, long copy_stride) {
+  const long f = blockIdx.z;
   const int words = PP / 4;
   const int wi = blockIdx.x * blockDim.x + threadIdx.x;
-  const int row = blockIdx.y;  // y * 2 + parity
+  const int row = blockIdx.y;  // (y * 2 + par) * 4 + s
   if (wi >= words) return;
-  const int y = row >> 1, par = row & 1;
+  const int s = row & 3, par = (row >> 2) & 1, y = row >> 3;
   const int half_w = (W + 1) / 2;
-  const uint8_t* src = gray + (long)y * W;
+  const uint8_t* src = gray + f * gray_stride + (long)y * W;
   uint32_t word = 0;
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
-    const int j = wi * 4 + b - PB;  // plane index
+    const int j = wi * 4 + b + s - PB;  // plane index
     const int x = 2 * j + par;
-    uint32_t val = 0;
-    if (j >= 0 && j < half_w && x < W) val = src[x];
+    const uint32_t val = (j >= 0 && j < half_w && x < W) ? (uint32_t)__ldg(src + x) : 0u;
     word |= val << (8 * b);
   }
-  reinterpret_cast<uint32_t*>(plane + (long)row * PP)[wi] = word;
+  rcopy[f * copy_stride + (long)row * words + wi] = word;
 }
 
-void launch_planes(const uint8_t* gray, uint8_t* plane, const Geom& g, int frames,
-                   long gray_stride, long plane_stride, cudaStream_t s) {
+void launch_ltap(const uint8_t* gray, uint4* ltap, const Geom& g, int frames, long gray_stride,
+                 long tap_stride, cudaStream_t s) {
+  if (g.W <= 0 || g.H <= 0 || frames <= 0) return;
+  k_ltap<<<dim3((g.W + 127) / 128, g.H, frames), 128, 0, s>>>(gray, ltap, g.W, gray_stride,
+                                                              tap_stride);
+}
+
+void launch_rcopy(const uint8_t* gray, uint32_t* rcopy, const Geom& g, int frames,
+                  long gray_stride, long copy_stride, cudaStream_t s) {
   if (g.W <= 0 || g.H <= 0 || frames <= 0) return;
   const int words = g.PP / 4;
-  const int threads = 128;
-  dim3 grid((words + threads - 1) / threads, 2 * g.H, frames);
-  k_planes<<<grid, threads, 0, s>>>(gray, plane, g.W, g.H, g.PB, g.PP, gray_stride,
-                                    plane_stride);
+  k_rcopy<<<dim3((words + 127) / 128, 8 * g.H, frames), 128, 0, s>>>(
+      gray, rcopy, g.W, g.PB, g.PP, gray_stride, copy_stride);
 }
 
 // Chessboard window statistics of one image. out[i] = {sum, bits(1/sqrt(var))}

@@ -31,18 +31,21 @@
 
 #include "exact.cuh"
 #include "ss_internal.cuh"
+#include "tma.cuh"
 
 namespace ssb {
 
 namespace {
 
-constexpr int kRB = 4;  // output rows per shared-memory reduction chunk
+constexpr int kRB = 2;  // output rows per shared-memory reduction chunk
+constexpr int kTH = 64;  // rows per block strip (11-row warm-up amortised over 64)
 constexpr int kNoArg = INT_MIN;  // "no defined candidate" (disparities may be negative)
 
-__device__ __forceinline__ uint32_t ld_win(const uint8_t* row, int start) {
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(row);
-  const int wi = start >> 2;
-  return __funnelshift_r(__ldg(w + wi), __ldg(w + wi + 1), (start & 3) * 8);
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 template <int O>
@@ -55,61 +58,30 @@ __device__ __forceinline__ uint32_t win(const uint32_t (&S)[4]) {
   }
 }
 
-struct ThreadGeom {
-  const uint8_t* lplane;
-  const uint8_t* rplane;
-  long PP;
-  int p, q0;            // parity of u, parity of u - c0
-  int Le, Lo;           // byte offsets of the left even / odd tap windows
-  int wA, shA, wB, shB; // aligned word index + shift of the right streams A, B
-};
-
-// The 4-byte windows of one image row that the thread's kDB candidates need:
-// the left tap words (fixed per thread) and the two right-image byte streams
-// A and B pre-aligned to the thread's misalignment.
+// One image row as the thread's kDB candidates need it (read from the row
+// ring): the left tap words (k_ltap) and 16 aligned bytes of each right
+// parity stream (k_rcopy):
+// stream A = plane (u - c0) & 1 from plane byte m0 - 10, stream B = the other
+// plane from m0 - 10 + q0 (m0 = (u - c0) >> 1).
 struct RowWords {
-  uint32_t Lea, Leb, Loa, Lob;
-  uint32_t SA[4], SB[4];
+  uint4 L;
+  uint32_t A[4], B[4];
 };
 
-__device__ __forceinline__ RowWords row_words(const ThreadGeom& tg, int y) {
-  RowWords w;
-  const uint8_t* lre = tg.lplane + (long)(2 * y + tg.p) * tg.PP;
-  const uint8_t* lro = tg.lplane + (long)(2 * y + 1 - tg.p) * tg.PP;
-  w.Lea = ld_win(lre, tg.Le);
-  w.Leb = ld_win(lre, tg.Le + 4) & 0xFFu;
-  w.Loa = ld_win(lro, tg.Lo);
-  w.Lob = ld_win(lro, tg.Lo + 4) & 0xFFFFu;
-  const uint32_t* ar =
-      reinterpret_cast<const uint32_t*>(tg.rplane + (long)(2 * y + tg.q0) * tg.PP) + tg.wA;
-  const uint32_t* br =
-      reinterpret_cast<const uint32_t*>(tg.rplane + (long)(2 * y + 1 - tg.q0) * tg.PP) + tg.wB;
-  uint32_t a[5], b[5];
-#pragma unroll
-  for (int t = 0; t < 5; ++t) {
-    a[t] = __ldg(ar + t);
-    b[t] = __ldg(br + t);
-  }
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    w.SA[t] = __funnelshift_r(a[t], a[t + 1], tg.shA);
-    w.SB[t] = __funnelshift_r(b[t], b[t + 1], tg.shB);
-  }
-  return w;
-}
-
-// He (even-offset taps, 5) and Ho (odd-offset taps, 6) of candidate I.
+// He (even-offset taps, 5) and Ho (odd-offset taps, 6) of candidate I = 2i + e:
+// e = 0: even taps from A at byte 8 - i, odd taps from B at 7 - i;
+// e = 1: even taps from B at 7 - i, odd taps from A at 7 - i.
 template <int I>
 __device__ __forceinline__ uint32_t term_e(const RowWords& w) {
   constexpr int t = I >> 1;
-  if constexpr ((I & 1) == 0) return __dp4a(w.Lea, win<8 - t>(w.SA), __dp4a(w.Leb, win<12 - t>(w.SA), 0u));
-  else return __dp4a(w.Lea, win<7 - t>(w.SB), __dp4a(w.Leb, win<11 - t>(w.SB), 0u));
+  if constexpr ((I & 1) == 0) return __dp4a(w.L.x, win<8 - t>(w.A), __dp4a(w.L.y, win<12 - t>(w.A), 0u));
+  else return __dp4a(w.L.x, win<7 - t>(w.B), __dp4a(w.L.y, win<11 - t>(w.B), 0u));
 }
 template <int I>
 __device__ __forceinline__ uint32_t term_o(const RowWords& w) {
   constexpr int t = I >> 1;
-  if constexpr ((I & 1) == 0) return __dp4a(w.Loa, win<7 - t>(w.SB), __dp4a(w.Lob, win<11 - t>(w.SB), 0u));
-  else return __dp4a(w.Loa, win<7 - t>(w.SA), __dp4a(w.Lob, win<11 - t>(w.SA), 0u));
+  if constexpr ((I & 1) == 0) return __dp4a(w.L.z, win<7 - t>(w.B), __dp4a(w.L.w, win<11 - t>(w.B), 0u));
+  else return __dp4a(w.L.z, win<7 - t>(w.A), __dp4a(w.L.w, win<11 - t>(w.A), 0u));
 }
 
 // One row step of the running sums for candidate I (center v-1 -> v):
@@ -142,29 +114,75 @@ __device__ __forceinline__ void warm_all(const RowWords& w, bool even, int (&X)[
   (warm_i<Is>(w, even, X, Y), ...);
 }
 
+// Score candidate I: g = float(61 slr - sl sr) / sqrt(var_r) (NaN when
+// undefined), staged for the window; (best, second, arg) kept NaN-safe:
+// second' = min(best, max(second, g)) is the runner-up for any g order.
+template <bool MASKED, int I>
+__device__ __forceinline__ void score_i(const int (&X)[kDB], const int2* rrow, int sl,
+                                        unsigned amask, float* gs, float& best, float& second,
+                                        int& arg) {
+  const int2 rs = rrow[-I];  // shared-memory row ring
+  const int num = 61 * X[I] - sl * rs.x;
+  float gv = __int2float_rn(num) * __int_as_float(rs.y);
+  gs[I * 32] = gv;
+  if constexpr (MASKED) gv = ((amask >> I) & 1) ? gv : __int_as_float(0x7fc00000);
+  second = fminf(best, fmaxf(second, gv));
+  arg = gv > best ? I : arg;
+  best = fmaxf(best, gv);
+}
+template <bool MASKED, int... Is>
+__device__ __forceinline__ void score_all(const int (&X)[kDB], const int2* rrow, int sl,
+                                          unsigned amask, float* gs, float& best, float& second,
+                                          int& arg, std::integer_sequence<int, Is...>) {
+  (score_i<MASKED, Is>(X, rrow, sl, amask, gs, best, second, arg), ...);
+}
+
 }  // namespace
 
+// Shared-memory row ring of the staged sweep. Slot of image row y:
+//   [0, 512)                 ltap[y][u0 .. u0+31]
+//   [512, 512 + 32 RW)       rcopy[y][par][s][wlo .. wlo+RW) (8 sub-rows)
+//   [512 + 32 RW, +8 RSN)    rstat[y][e_lo .. e_lo+RSN) (int2)
+// filled by one thread with bulk copies completing on the slot's mbarrier.
+// Rows in flight: 12 live rows (v - 6 .. v + 5) + kRB rows of the next chunk
+// + prefetch depth; a power of two so slot indices are masks.
+constexpr int kNSlots = 16;
+static_assert(kNSlots >= 11 + 2 * kRB + 1, "row ring too small");
+struct RingGeom {
+  int RW, RSN, slot_bytes;
+};
+__host__ __device__ inline RingGeom ring_geom(int NB) {
+  RingGeom r;
+  const int span_m = (31 + kDB * (NB - 1)) / 2 + 2;  // m0 range of a block (+ slack)
+  r.RW = ((span_m + 3) / 4 + 9 + 3) / 4 * 4;            // words per sub-row, 16 B multiple
+  r.RSN = (kDB * NB + 31 + 2 + 1) / 2 * 2;              // rstat elements, 16 B multiple
+  r.slot_bytes = (512 + 32 * r.RW + 8 * r.RSN + 127) / 128 * 128;
+  return r;
+}
+
 __global__ void __launch_bounds__(512) k_wta11(
-    const uint8_t* __restrict__ lplane, const uint8_t* __restrict__ rplane,
+    const uint4* __restrict__ ltap, const uint32_t* __restrict__ rcopy,
     const int2* __restrict__ lstat, const int2* __restrict__ rstat, wscore_t* __restrict__ win,
     int* __restrict__ wbase, const int* __restrict__ base_map, float* __restrict__ disp,
     uint8_t* __restrict__ valid, int* __restrict__ flag_list,
-    unsigned int* __restrict__ flag_count, Geom g, int TH, float min_zncc_f, float thr_tol,
-    int do_argmax, long plane_stride, long lstat_stride, long rstat_stride, long map_stride,
-    long win_stride) {
-  extern __shared__ unsigned char smem_raw[];
+    unsigned int* __restrict__ flag_count, Geom g, float min_zncc_f, float thr_tol,
+    int do_argmax, long tap_stride, long copy_stride, long lstat_stride, long rstat_stride,
+    long map_stride, long win_stride) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x, j = threadIdx.y, NB = blockDim.y;
   const int NCB = NB * kDB;  // staged candidates per pixel
-  float* s_best = reinterpret_cast<float*>(smem_raw);
+  const RingGeom rg = ring_geom(NB);
+  unsigned char* ring = smem_raw;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kNSlots * rg.slot_bytes);
+  float* s_best = reinterpret_cast<float*>(bars + kNSlots);
   float* s_sec = s_best + kRB * NB * 32;
   int* s_arg = reinterpret_cast<int*>(s_sec + kRB * NB * 32);
   float* s_g = reinterpret_cast<float*>(s_arg + kRB * NB * 32);  // [kRB][NCB][32]
 
   const long fr = blockIdx.z;
-  lplane += fr * plane_stride;
-  rplane += fr * plane_stride;
+  ltap += fr * tap_stride;
+  rcopy += fr * copy_stride;
   lstat += fr * lstat_stride;
-  rstat += fr * rstat_stride;
   win += fr * win_stride * kWin;
   wbase += fr * win_stride;
   if (base_map) base_map += fr * map_stride;
@@ -175,83 +193,145 @@ __global__ void __launch_bounds__(512) k_wta11(
 
   constexpr int h = 5;
   const int W = g.W, H = g.H;
-  const int u = h + blockIdx.x * 32 + lane;
-  const int v_begin = h + blockIdx.y * TH;
-  const int v_end = min(v_begin + TH, H - h);
+  const int u0 = h + blockIdx.x * 32;
+  const int u = u0 + lane;
+  const int v_begin = h + blockIdx.y * kTH;
+  const int v_end = min(v_begin + kTH, H - h);
   if (v_begin >= v_end) return;  // uniform over the block
   const int c0 = g.cmin + j * kDB;
   const int nact = min(kDB, g.NC - j * kDB);
   const bool active = (u < W - h) && (nact > 0);
-  // candidates of this thread that take part in the WTA argmax
   unsigned amask = 0;
 #pragma unroll
   for (int i = 0; i < kDB; ++i)
     amask |= (i < nact && c0 + i >= g.dmin && c0 + i <= g.dmax) ? (1u << i) : 0u;
+  // warps whose candidates all take part in the WTA argmax skip the mask
+  const bool full = __all_sync(0xffffffffu, amask == 0xFFFFu || !active);
 
-  ThreadGeom tg;
-  tg.lplane = lplane;
-  tg.rplane = rplane;
-  tg.PP = g.PP;
-  tg.p = u & 1;
-  const int k = u >> 1;
+  // ---- block-uniform copy geometry ----
+  const int PW = g.PP / 4;
+  const int c0_last = g.cmin + kDB * (NB - 1);
+  const int m0_min = (u0 - c0_last) >> 1;
+  const int wlo = ((g.PB + m0_min - 10) >> 2) & ~3;
+  const int ru_lo = u0 - c0_last - (kDB - 1);  // lowest right column any thread scores
+  const long rs_base = fr * rstat_stride + g.SPAD + ru_lo;  // + y * SP: element of ru_lo
+  // ---- per-thread stream offsets (words into a slot's rcopy area) ----
   const int ru0 = u - c0;
-  tg.q0 = ru0 & 1;
+  const int q0 = ru0 & 1;
   const int m0 = ru0 >> 1;  // arithmetic shift: floor for negative ru0
-  const int startA = g.PB + m0 - 10;
-  const int startB = g.PB + (m0 - 1 + tg.q0) - 9;
-  tg.wA = startA >> 2;
-  tg.shA = (startA & 3) * 8;
-  tg.wB = startB >> 2;
-  tg.shB = (startB & 3) * 8;
-  tg.Le = g.PB + k - 2;
-  tg.Lo = g.PB + k - 3 + tg.p;
+  const int stA = g.PB + m0 - 10, stB = stA + q0;
+  const int offA = (q0 * 4 + (stA & 3)) * rg.RW + (stA >> 2) - wlo;
+  const int offB = ((1 - q0) * 4 + (stB & 3)) * rg.RW + (stB >> 2) - wlo;
+  const int offR = ru0 - ru_lo;  // + (row parity of rs_base + y SP) -> rstat element
+
+  const int y_first = v_begin - h, y_last = v_end + h - 1;  // rows this strip reads
+  const int tid = j * 32 + lane;
+  auto issue = [&](int y) {  // thread 0 only
+    const int k = (y - y_first) & (kNSlots - 1);
+    unsigned char* sl = ring + (size_t)k * rg.slot_bytes;
+    uint64_t* bar = bars + k;
+    const long rsg = rs_base + (long)y * g.SP;
+    const long rse = rsg & ~1L;
+    mbar_expect_tx(bar, 512u + 32u * rg.RW + 8u * rg.RSN);
+    bulk_g2s(sl, ltap + (long)y * W + u0, 512u, bar);
+    const uint32_t* rrow = rcopy + (long)y * 8 * PW + wlo;
+#pragma unroll 1
+    for (int r = 0; r < 8; ++r)
+      bulk_g2s(sl + 512 + r * rg.RW * 4, rrow + (long)r * PW, rg.RW * 4u, bar);
+    bulk_g2s(sl + 512 + 32 * rg.RW, rstat + rse, 8u * rg.RSN, bar);
+  };
+  auto slot_of = [&](int y) {
+    return ring + (size_t)((y - y_first) & (kNSlots - 1)) * rg.slot_bytes;
+  };
+  auto wait_row = [&](int y) {
+    const int n = y - y_first;
+    mbar_wait(bars + (n & (kNSlots - 1)), (unsigned)(n / kNSlots) & 1u);
+  };
+  int issued = y_first - 1;  // last row issued
+  if (tid == 0) {
+    for (int k = 0; k < kNSlots; ++k) mbar_init(bars + k, 1);
+    mbar_fence_init();
+    for (int y = y_first; y <= min(y_last, y_first + kNSlots - 1); ++y) issue(y);
+  }
+  issued = min(y_last, y_first + kNSlots - 1);
+  __syncthreads();
+
+  auto words = [&](int y) {
+    const unsigned char* sl = slot_of(y);
+    RowWords w;
+    w.L = reinterpret_cast<const uint4*>(sl)[lane];
+    const uint32_t* rc = reinterpret_cast<const uint32_t*>(sl + 512);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      w.A[t] = rc[offA + t];
+      w.B[t] = rc[offB + t];
+    }
+    return w;
+  };
 
   int X[kDB], Y[kDB];
 #pragma unroll
   for (int i = 0; i < kDB; ++i) X[i] = Y[i] = 0;
 
-  if (active) {
-    for (int dy = -h; dy <= h; ++dy) {
-      const RowWords w = row_words(tg, v_begin + dy);
-      warm_all(w, ((dy + h) & 1) == 1 /* dy even */, X, Y,
-               std::make_integer_sequence<int, kDB>{});
+#pragma unroll 1
+  for (int dy = -h; dy <= h; ++dy) {
+    const int y = v_begin + dy;
+    wait_row(y);
+    if (active) {
+      const RowWords w = words(y);
+      warm_all(w, ((dy + h) & 1) == 1 /* dy even */, X, Y, std::make_integer_sequence<int, kDB>{});
     }
   }
 
   for (int v = v_begin; v < v_end; ++v) {
-    if (v > v_begin && active) {
-      const RowWords wo = row_words(tg, v - 6);
-      const RowWords wn = row_words(tg, v + 5);
-      step_all(wo, wn, X, Y, std::make_integer_sequence<int, kDB>{});
+    if (v > v_begin) {
+      wait_row(v + 5);
+      if (active) {
+        const RowWords wo = words(v - 6);
+        const RowWords wn = words(v + 5);
+        step_all(wo, wn, X, Y, std::make_integer_sequence<int, kDB>{});
+      }
     }
     const int slot = (v - v_begin) & (kRB - 1);
+    // Staging of a new chunk waits until the previous chunk's merges are done
+    // (the merges overlap the non-merging warps' step of this row).
+    if (slot == 0 && v > v_begin) bar_sync(2, NB * 32);
     float* gs = s_g + (slot * NCB + j * kDB) * 32 + lane;  // staged g of this (row, block)
     float best = -INFINITY, second = -INFINITY;
     int arg = kNoArg;
     if (active) {
       const int sl = __ldg(&lstat[(long)v * W + u].x);
-      const int2* rrow = rstat + (long)v * g.SP + g.SPAD + ru0;
-      // Branch-free: every lane scores all kDB candidates (padded rstat keeps
-      // the loads in bounds); amask selects those inside [d_min, d_max] and
-      // the volume range, NaN (undefined) folds to -inf.
-#pragma unroll
-      for (int i = 0; i < kDB; ++i) {
-        const int2 rs = __ldg(rrow - i);
-        const int num = 61 * X[i] - sl * rs.x;
-        const float gv = __int2float_rn(num) * __int_as_float(rs.y);
-        gs[i * 32] = gv;
-        const float gc = ((amask >> i) & 1) ? fmaxf(gv, -INFINITY) : -INFINITY;
-        second = fmaxf(second, fminf(best, gc));
-        arg = gc > best ? c0 + i : arg;
-        best = fmaxf(best, gc);
-      }
+      const int2* rrow = reinterpret_cast<const int2*>(slot_of(v) + 512 + 32 * rg.RW) + offR +
+                         (int)((rs_base + (long)v * g.SP) & 1);
+      int ai = -1;
+      if (full)
+        score_all<false>(X, rrow, sl, amask, gs, best, second, ai,
+                         std::make_integer_sequence<int, kDB>{});
+      else
+        score_all<true>(X, rrow, sl, amask, gs, best, second, ai,
+                        std::make_integer_sequence<int, kDB>{});
+      arg = ai >= 0 ? c0 + ai : kNoArg;
     }
     const int so = (slot * NB + j) * 32 + lane;
     s_best[so] = best;
     s_sec[so] = second;
     s_arg[so] = arg;
     if (slot == kRB - 1 || v == v_end - 1) {
-      __syncthreads();
+      // Barrier 1: the chunk's partials are staged. Warps j <= slot merge one
+      // row each (and wait for all partials); the others only arrive and go
+      // on with the next row's step.
+      if (j > slot) {
+        bar_arrive(1, NB * 32);
+        continue;
+      }
+      bar_sync(1, NB * 32);
+      // every warp is past step v: rows <= v - 6 are dead, their slots free
+      if (tid == 0) {
+        const int hi = min(y_last, v - 6 + kNSlots);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int y = issued + 1; y <= hi; ++y) issue(y);
+      }
+      issued = min(y_last, max(issued, v - 6 + kNSlots));
       for (int r = j; r <= slot; r += NB) {
         float B = -INFINITY, S = -INFINITY;
         int A = kNoArg;
@@ -313,24 +393,24 @@ __global__ void __launch_bounds__(512) k_wta11(
           }
         }
       }
-      __syncthreads();
     }
   }
 }
 
-void launch_wta11(const uint8_t* lplane, const uint8_t* rplane, const int2* lstat,
-                  const int2* rstat, wscore_t* win, int* wbase, const int* base_map, float* disp,
-                  uint8_t* valid, int* flag_list, unsigned int* flag_count, const Geom& g,
-                  double min_zncc, int frames, long plane_stride, long lstat_stride,
+void launch_wta11(const uint4* ltap, const uint32_t* rcopy, const int2* lstat, const int2* rstat,
+                  wscore_t* win, int* wbase, const int* base_map, float* disp, uint8_t* valid,
+                  int* flag_list, unsigned int* flag_count, const Geom& g, double min_zncc,
+                  int frames, long tap_stride, long copy_stride, long lstat_stride,
                   long rstat_stride, long map_stride, long win_stride, int do_argmax,
                   cudaStream_t s) {
   const int h = 5;
   if (g.W - 2 * h <= 0 || g.H - 2 * h <= 0 || frames <= 0) return;
   const int NB = (g.NC + kDB - 1) / kDB;
-  const int TH = 32;
+  const RingGeom rg = ring_geom(NB);
   dim3 block(32, NB);
-  dim3 grid((g.W - 2 * h + 31) / 32, (g.H - 2 * h + TH - 1) / TH, frames);
-  const size_t smem = (size_t)kRB * NB * 32 * 12 + (size_t)kRB * NB * kDB * 32 * 4;
+  dim3 grid((g.W - 2 * h + 31) / 32, (g.H - 2 * h + kTH - 1) / kTH, frames);
+  const size_t smem = (size_t)kNSlots * rg.slot_bytes + 8 * kNSlots +
+                      (size_t)kRB * NB * 32 * 12 + (size_t)kRB * NB * kDB * 32 * 4;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     cudaFuncSetAttribute(k_wta11, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -338,9 +418,9 @@ void launch_wta11(const uint8_t* lplane, const uint8_t* rplane, const int2* lsta
   }
   const float mz = (float)min_zncc;
   const float tol = 4e-6f * fmaxf(1.f, fabsf(mz));
-  k_wta11<<<grid, block, smem, s>>>(lplane, rplane, lstat, rstat, win, wbase, base_map, disp,
-                                    valid, flag_list, flag_count, g, TH, mz, tol, do_argmax,
-                                    plane_stride, lstat_stride, rstat_stride, map_stride,
+  k_wta11<<<grid, block, smem, s>>>(ltap, rcopy, lstat, rstat, win, wbase, base_map, disp, valid,
+                                    flag_list, flag_count, g, mz, tol, do_argmax, tap_stride,
+                                    copy_stride, lstat_stride, rstat_stride, map_stride,
                                     win_stride);
 }
 

@@ -39,10 +39,15 @@ void ck(cudaError_t e, const char* what) {
   }
 }
 
+thread_local bool tl_gpu = false;  // this thread has used the CUDA runtime
+
 template <class F>
 ss_status guarded(F&& f) {
   try {
     f();
+    // launch-configuration errors are not sticky and never reach a stream
+    // sync: every API call checks them once its kernels are enqueued.
+    if (tl_gpu) ck(cudaGetLastError(), "kernel launch");
     return SS_OK;
   } catch (const SsError& e) {
     tl_err = e.msg;
@@ -63,6 +68,7 @@ void require_device() {
     raise(SS_ENODEV,
           "no CUDA device: the B200 stereo path has no CPU fallback (cudaGetDeviceCount: " +
               std::string(cudaGetErrorString(e)) + ")");
+  tl_gpu = true;
 }
 
 // Growable device arena.
@@ -247,6 +253,7 @@ struct ss_ctx {
     cudaEvent_t a = nullptr;
     int64_t l0;
     Stage(ss_ctx* ctx, int stage) : c(ctx), id(stage), l0(ctx->stats.kernel_launches) {
+      ck(cudaGetLastError(), "kernel launch");
       if (c->timing) {
         a = c->take_event();
         ck(cudaEventRecord(a, c->stream), "cudaEventRecord");
@@ -311,10 +318,13 @@ struct ss_ctx {
   // Stats, planes and the cost volume for the fast path (window 11).
   void build_volume(int n, const Geom& g, bool do_argmax) {
     const long N = g.N();
-    const long plane_stride = (long)g.H * 2 * g.PP;
+    const long tap_stride = N;                       // uint4 per pixel
+    const long copy_stride = (long)g.H * 2 * g.PP;  // words: 8 rows of PP bytes per y
     const long rstride = (long)g.H * g.SP;
-    plane_l.ensure(plane_stride * n);
-    plane_r.ensure(plane_stride * n);
+    // (+ slack: the sweep's row copies are fixed-size and may run past the
+    // last row of the last frame; those bytes feed only inactive lanes)
+    plane_l.ensure(sizeof(uint4) * tap_stride * n + 4096);
+    plane_r.ensure(sizeof(uint32_t) * copy_stride * n + 4096);
     lstat.ensure(sizeof(int2) * N * n);
     rstat.ensure(sizeof(int2) * rstride * n);
     const long bs = bt_frame(g.W, g.H, 0);  // windows are BT-indexed
@@ -324,8 +334,8 @@ struct ss_ctx {
     flag_count.ensure(sizeof(unsigned) * n);
     {
     Stage st(this, 1);
-    launch_planes(gray_l.as<uint8_t>(), plane_l.as<uint8_t>(), g, n, N, plane_stride, stream);
-    launch_planes(gray_r.as<uint8_t>(), plane_r.as<uint8_t>(), g, n, N, plane_stride, stream);
+    launch_ltap(gray_l.as<uint8_t>(), plane_l.as<uint4>(), g, n, N, tap_stride, stream);
+    launch_rcopy(gray_r.as<uint8_t>(), plane_r.as<uint32_t>(), g, n, N, copy_stride, stream);
     launch_stats(gray_l.as<uint8_t>(), lstat.as<int2>(), nullptr, 0, g, n, N, N, stream);
     launch_stats(gray_r.as<uint8_t>(), nullptr, rstat.as<int2>(), 1, g, n, N, rstride, stream);
     stats.kernel_launches += 4;
@@ -336,10 +346,11 @@ struct ss_ctx {
       ck(cudaMemsetAsync(valid_a.p, 0, N * n, stream), "memset");
     }
     Stage st(this, 2);
-    launch_wta11(plane_l.as<uint8_t>(), plane_r.as<uint8_t>(), lstat.as<int2>(), rstat.as<int2>(),
+    launch_wta11(plane_l.as<uint4>(), plane_r.as<uint32_t>(), lstat.as<int2>(), rstat.as<int2>(),
                  win.as<wscore_t>(), wbase.as<int>(), nullptr, disp_a.as<float>(),
                  valid_a.as<uint8_t>(), flags.as<int>(), flag_count.as<unsigned>(), g,
-                 params.min_zncc, n, plane_stride, N, rstride, N, bs, do_argmax ? 1 : 0, stream);
+                 params.min_zncc, n, tap_stride, copy_stride, N, rstride, N, bs,
+                 do_argmax ? 1 : 0, stream);
     stats.kernel_launches += 1;
   }
 

@@ -2,10 +2,13 @@
 //
 // HBM layout of one frame (all frame-major; frame f of a batch at f * stride):
 //   gray[N]                  u8  row-major luma (exact path, cloud colours)
-//   plane[H][2][PP]          u8  parity-split rows: [.][0] even columns,
-//                                [.][1] odd columns, PB bytes of zero padding
-//                                each side -> any 4-byte window of a chessboard
-//                                row is two aligned loads + one funnel shift
+//   ltap[N]                  uint4 left tap words of pixel (u, v): the 5 even-
+//                                and 6 odd-offset bytes of its chessboard row
+//                                window, packed for dp4a (k_ltap)
+//   rcopy[H][2][4][PP]       u8  right parity-split rows ([.][0] even columns,
+//                                [.][1] odd, PB bytes of zero padding each
+//                                side) in 4 copies shifted by 0..3 bytes: any
+//                                byte offset of a row starts an aligned word
 //   lstat[N]                 int2 {chessboard sum, float bits of 1/sqrt(var)}
 //   rstat[H][SP]             int2 same for the right image, SPAD padded
 //                                columns each side hold {0, NaN}
@@ -66,8 +69,10 @@ struct Geom {
 // ---- launchers (stream-ordered, frame index in blockIdx.z / y) ----
 void launch_to_gray(const uint8_t* rgb, uint8_t* gray, long n_pixels, int frames,
                     long in_stride, long out_stride, cudaStream_t s);
-void launch_planes(const uint8_t* gray, uint8_t* plane, const Geom& g, int frames,
-                   long gray_stride, long plane_stride, cudaStream_t s);
+void launch_ltap(const uint8_t* gray, uint4* ltap, const Geom& g, int frames, long gray_stride,
+                 long tap_stride, cudaStream_t s);
+void launch_rcopy(const uint8_t* gray, uint32_t* rcopy, const Geom& g, int frames,
+                  long gray_stride, long copy_stride, cudaStream_t s);
 void launch_stats(const uint8_t* gray, int2* lstat, int2* rstat, int is_right, const Geom& g,
                   int frames, long gray_stride, long stat_stride, cudaStream_t s);
 // Sweep + WTA. Also writes, per interior pixel, the refinement's candidate
@@ -75,12 +80,12 @@ void launch_stats(const uint8_t* gray, int2* lstat, int2* rstat, int is_right, c
 // wbase centred on the WTA pick, or on base_map[pixel] when base_map != NULL
 // (per-stage refine). wbase = kNoWin when var_l == 0 (no defined score).
 // win / wbase are BT-indexed (bt_index, frame stride win_stride).
-void launch_wta11(const uint8_t* lplane, const uint8_t* rplane, const int2* lstat,
+void launch_wta11(const uint4* ltap, const uint32_t* rcopy, const int2* lstat,
                   const int2* rstat, wscore_t* win, int* wbase, const int* base_map, float* disp,
                   uint8_t* valid, int* flag_list, unsigned int* flag_count, const Geom& g,
-                  double min_zncc, int frames, long plane_stride, long lstat_stride,
-                  long rstat_stride, long map_stride, long win_stride, int do_argmax,
-                  cudaStream_t s);
+                  double min_zncc, int frames, long tap_stride, long copy_stride,
+                  long lstat_stride, long rstat_stride, long map_stride, long win_stride,
+                  int do_argmax, cudaStream_t s);
 // After cleanup: every valid pixel whose window is not centred on its
 // (possibly filled) disparity gets a freshly computed window.
 void launch_window_fix(const float* disp, const uint8_t* valid, const uint8_t* lgray,
