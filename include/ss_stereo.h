@@ -91,6 +91,18 @@ ss_status ss_compute_disparity(const ss_stereo_params* p, const uint8_t* left, i
                                int32_t lh, const uint8_t* right, int32_t rw, int32_t rh,
                                float* disparity, uint8_t* valid);
 
+/* Opt-in left-right consistency (no reference analogue: an extension named by
+ * the north star). compute_disparity plus the right-view
+ * WTA d_R(x) = first argmax over d of zncc(left at x + d, right at x); a valid
+ * left pixel u with disparity d is kept iff x = u - d is inside the image, the
+ * right view is valid there and |d_R(x) - d| <= max_diff, else it becomes
+ * (0, invalid). right_disparity / right_valid (nullable) receive the
+ * right-view map in right-image coordinates. */
+ss_status ss_compute_disparity_lr(const ss_stereo_params* p, const uint8_t* left, int32_t lw,
+                                  int32_t lh, const uint8_t* right, int32_t rw, int32_t rh,
+                                  int32_t max_diff, float* disparity, uint8_t* valid,
+                                  float* right_disparity, uint8_t* right_valid);
+
 ss_status ss_remove_outliers(const float* disparity, const uint8_t* valid, int32_t w,
                              int32_t h, int32_t radius, double threshold, float* out_disparity,
                              uint8_t* out_valid);
@@ -161,6 +173,9 @@ void* ss_ctx_stream(ss_ctx* ctx);
 ss_status ss_ctx_sync(ss_ctx* ctx);
 ss_status ss_ctx_get_stats(ss_ctx* ctx, ss_ctx_stats* st);
 ss_status ss_ctx_reset_stats(ss_ctx* ctx);
+/* Opt-in LR consistency inside the batch chain (after the WTA, before the
+ * cleanup); off by default, which keeps the reference's output. */
+ss_status ss_ctx_set_lr_check(ss_ctx* ctx, int32_t enable, int32_t max_diff);
 
 /* Per-stage device time (CUDA events on the ctx stream), the Table III-style
  * RuntimeReport of SPEC.md:566-569 for the stereo stage. Stages:

@@ -156,6 +156,37 @@ class Oracle:
                        _p(valid, _U8)))
         return disp, valid
 
+    def compute_disparity_right(self, left, right, params=None):
+        """Right-view WTA (restatement only; the LR-check extension)."""
+        left = np.ascontiguousarray(left, np.uint8)
+        right = np.ascontiguousarray(right, np.uint8)
+        h, w = left.shape
+        disp = np.zeros((h, w), np.float32)
+        valid = np.zeros((h, w), np.uint8)
+        pp = to_orc_params(params)
+        self._check(self.lib.orc_compute_disparity_right(
+            C.byref(pp), _p(left, _U8), _p(right, _U8), w, h, _p(disp, _F32), _p(valid, _U8)))
+        return disp, valid
+
+    def lr_check(self, disp, valid, disp_r, valid_r, max_diff=1):
+        disp = np.ascontiguousarray(disp, np.float32)
+        valid = np.ascontiguousarray(valid, np.uint8)
+        disp_r = np.ascontiguousarray(disp_r, np.float32)
+        valid_r = np.ascontiguousarray(valid_r, np.uint8)
+        h, w = disp.shape
+        od = np.empty_like(disp)
+        ov = np.empty_like(valid)
+        self._check(self.lib.orc_lr_check(_p(disp, _F32), _p(valid, _U8), _p(disp_r, _F32),
+                                          _p(valid_r, _U8), w, h, max_diff, _p(od, _F32),
+                                          _p(ov, _U8)))
+        return od, ov
+
+    def compute_disparity_lr(self, left, right, params=None, max_diff=1):
+        d, v = self.compute_disparity(left, right, params)
+        dr, vr = self.compute_disparity_right(left, right, params)
+        od, ov = self.lr_check(d, v, dr, vr, max_diff)
+        return od, ov, dr, vr
+
     def remove_outliers(self, disp, valid, radius, threshold, naive=False):
         disp = np.ascontiguousarray(disp, np.float32)
         valid = np.ascontiguousarray(valid, np.uint8)

@@ -166,6 +166,80 @@ int orc_compute_disparity(const orc_params* p, const uint8_t* L, const uint8_t* 
   return 0;
 }
 
+/* ---- Opt-in left-right consistency (extension: the reference has none;
+ * SURVEY.md §8f row 1). Restated from its definition, independently of the
+ * GPU's mirrored-sweep implementation (paper_2007_12623_b200/csrc/k_lr.cu).
+ *
+ * Right-view WTA: for a right pixel (x, v) whose window fits, the first
+ * maximum over d in [d_min, d_max] of the chessboard ZNCC of (left at x + d,
+ * right at x), the left window fitting and both variances non-zero (the same
+ * arithmetic as compute_disparity above); valid iff found and >= min_zncc. */
+int orc_compute_disparity_right(const orc_params* p, const uint8_t* L, const uint8_t* R,
+                                int32_t w, int32_t h, float* disp, uint8_t* valid) {
+  const int rc = orc_params_validate(p);
+  if (rc) return rc;
+  const long n = (long)w * h;
+  memset(disp, 0, (size_t)n * sizeof(float));
+  memset(valid, 0, (size_t)n);
+  const int half = p->window / 2;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int v = half; v < h - half; ++v) {
+    for (int x = half; x < w - half; ++x) {
+      int found = 0, best_d = 0;
+      double best = 0.0;
+      for (int d = p->d_min; d <= p->d_max; ++d) {
+        const int u = x + d;
+        if (u < half || u >= w - half) continue;
+        const orc_stats s = chess_stats(L, R, w, u, v, x, v, half);
+        const int64_t var_l = (int32_t)(s.n * s.sll - s.sl * s.sl);
+        const int64_t var_r = (int32_t)(s.n * s.srr - s.sr * s.sr);
+        if (var_l == 0 || var_r == 0) continue;
+        const int64_t num = s.n * s.slr - (int64_t)(int32_t)s.sl * (int32_t)s.sr;
+        const double score = (double)num / sqrt((double)(var_l * var_r));
+        if (!found || score > best) {
+          found = 1;
+          best = score;
+          best_d = d;
+        }
+      }
+      if (found && best >= p->min_zncc) {
+        disp[(long)v * w + x] = (float)best_d;
+        valid[(long)v * w + x] = 1;
+      }
+    }
+  }
+  return 0;
+}
+
+/* LR check: a valid left pixel u with disparity d is kept iff x = u - d is in
+ * the image, the right view is valid at x and |d_R(x) - d| <= max_diff;
+ * otherwise it becomes (0, invalid), the WTA's own "no match" output
+ * (matcher.cpp:172). */
+int orc_lr_check(const float* disp, const uint8_t* valid, const float* disp_r,
+                 const uint8_t* valid_r, int32_t w, int32_t h, int32_t max_diff,
+                 float* out_disp, uint8_t* out_valid) {
+  if (max_diff < 0) return fail(1, "lr_check: max_diff must be >= 0");
+  for (int v = 0; v < h; ++v) {
+    for (int u = 0; u < w; ++u) {
+      const long i = (long)v * w + u;
+      out_disp[i] = disp[i];
+      out_valid[i] = valid[i];
+      if (!valid[i]) continue;
+      const int x = u - (int)disp[i];
+      int ok = x >= 0 && x < w;
+      if (ok) {
+        const long j = (long)v * w + x;
+        ok = valid_r[j] && fabsf(disp_r[j] - disp[i]) <= (float)max_diff;
+      }
+      if (!ok) {
+        out_disp[i] = 0.f;
+        out_valid[i] = 0;
+      }
+    }
+  }
+  return 0;
+}
+
 /* Ray directions of cleanup.cpp:8-9. */
 static const int kDU[8] = {1, -1, 0, 0, 1, 1, -1, -1};
 static const int kDV[8] = {0, 0, 1, -1, 1, -1, 1, -1};

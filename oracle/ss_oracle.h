@@ -100,6 +100,14 @@ int orc_disparity_to_cloud(const float* disp, const uint8_t* valid, int32_t w,
                            double* points, double* normals, uint8_t* colors,
                            int32_t* pixels, int32_t* n_points,
                            double* eigen_gap);
+/* Restatement-only: opt-in left-right consistency (extension, no reference
+ * analogue): right-view WTA and the check (ss_compute_disparity_lr). */
+int orc_compute_disparity_right(const orc_params* p, const uint8_t* left,
+                                const uint8_t* right, int32_t w, int32_t h,
+                                float* disp, uint8_t* valid);
+int orc_lr_check(const float* disp, const uint8_t* valid, const float* disp_r,
+                 const uint8_t* valid_r, int32_t w, int32_t h, int32_t max_diff,
+                 float* out_disp, uint8_t* out_valid);
 int orc_params_validate(const orc_params* p);
 int orc_rig_validate(const orc_rig* rig);
 

@@ -15,6 +15,7 @@ from .stereo import (  # noqa: F401
     StereoRig,
     cleanup_pass,
     compute_disparity,
+    compute_disparity_lr,
     device_count,
     disc_fill_min_support,
     disc_neighbor_count,

@@ -71,6 +71,8 @@ def lib():
         "ss_device_count": (i32, []),
         "ss_to_gray": (i32, [vp, i32, i32, vp]),
         "ss_compute_disparity": (i32, [P(SsParams), vp, i32, i32, vp, i32, i32, vp, vp]),
+        "ss_compute_disparity_lr": (i32, [P(SsParams), vp, i32, i32, vp, i32, i32, i32, vp, vp,
+                                          vp, vp]),
         "ss_remove_outliers": (i32, [vp, vp, i32, i32, i32, f64, vp, vp]),
         "ss_fill_holes": (i32, [vp, vp, i32, i32, i32, i32, i32, vp, vp]),
         "ss_cleanup_pass": (i32, [P(SsParams), vp, vp, i32, i32, vp, vp]),
@@ -88,6 +90,7 @@ def lib():
         "ss_stereo_batch_device": (i32, [vp, i32, i32, i32, i32, vp, vp, C.c_uint32,
                                          P(SsBatchOut), vp]),
         "ss_ctx_device_outputs": (i32, [vp, P(SsBatchOut)]),
+        "ss_ctx_set_lr_check": (i32, [vp, i32, i32]),
         "ss_ctx_enable_timing": (i32, [vp, i32]),
         "ss_ctx_stage_times": (i32, [vp, P(C.c_double), P(C.c_int64)]),
         "ss_host_alloc": (vp, [C.c_size_t]),

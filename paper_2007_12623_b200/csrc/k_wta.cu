@@ -183,8 +183,10 @@ __global__ void __launch_bounds__(512) k_wta11(
   ltap += fr * tap_stride;
   rcopy += fr * copy_stride;
   lstat += fr * lstat_stride;
-  win += fr * win_stride * kWin;
-  wbase += fr * win_stride;
+  if (win) {
+    win += fr * win_stride * kWin;
+    wbase += fr * win_stride;
+  }
   if (base_map) base_map += fr * map_stride;
   disp += fr * map_stride;
   valid += fr * map_stride;
@@ -371,6 +373,7 @@ __global__ void __launch_bounds__(512) k_wta11(
           }
           // Candidate window for the refinement: kWin consecutive scores
           // s = g * rl around the pick (or the caller's base map).
+          if (!win) continue;  // argmax only (right view of the LR check)
           const int anchor = base_map ? base_map[idx] : A;
           int wb = kNoWin;
           if (!isnan(rl) && anchor != kNoArg && anchor != kNoWin)

@@ -167,6 +167,10 @@ struct ss_ctx {
   int max_w = 0, max_h = 0, max_batch = 1;
 
   DevBuf in_l, in_r, gray_l, gray_r, plane_l, plane_r, lstat, rstat, win, wbase;
+  // opt-in left-right consistency (k_lr.cu)
+  DevBuf gray_fl, gray_fr, disp_r, valid_r;
+  bool lr_check = false;
+  int lr_max_diff = 1;
   DevBuf disp_a, disp_b, valid_a, valid_b, flags, flag_count;
   DevBuf o, oi, d, avg, b, psum, pcnt, cnt, span, wtab, fspan, fx, emap;
   DevBuf index, block_sums, npoints, pts_f, nrm_f, colors, pts_d, nrm_d, pixels, pts4;
@@ -216,7 +220,8 @@ struct ss_ctx {
                       &disp_a, &disp_b, &valid_a, &valid_b, &flags, &flag_count, &o, &d, &avg,
                       &b, &psum, &pcnt, &cnt, &span, &wtab, &fspan, &fx, &emap, &index, &block_sums, &npoints,
                       &pts_f, &nrm_f, &colors, &pts_d, &nrm_d, &pixels, &pts4, &counters, &oi, &trace_o,
-                      &trace_d, &so, &chg, &chg_count, &mbt, &defer, &defer_count})
+                      &trace_d, &so, &chg, &chg_count, &mbt, &defer, &defer_count, &gray_fl,
+                      &gray_fr, &disp_r, &valid_r})
       b->release();
     for (Slot& sl : slots) {
       for (DevBuf* b : {&sl.in_l, &sl.in_r, &sl.disp_b, &sl.valid_a, &sl.index, &sl.npoints,
@@ -315,8 +320,11 @@ struct ss_ctx {
     }
   }
 
-  // Stats, planes and the cost volume for the fast path (window 11).
-  void build_volume(int n, const Geom& g, bool do_argmax) {
+  // Stats, tap words and the sweep for the fast path (window 11) of the pair
+  // (gl, gr) into (dsp, vld); windows = false skips the refinement's score
+  // windows (the LR check's right-view sweep).
+  void build_volume(int n, const Geom& g, bool do_argmax, const uint8_t* gl, const uint8_t* gr,
+                    float* dsp, uint8_t* vld, bool windows) {
     const long N = g.N();
     const long tap_stride = N;                       // uint4 per pixel
     const long copy_stride = (long)g.H * 2 * g.PP;  // words: 8 rows of PP bytes per y
@@ -334,21 +342,21 @@ struct ss_ctx {
     flag_count.ensure(sizeof(unsigned) * n);
     {
     Stage st(this, 1);
-    launch_ltap(gray_l.as<uint8_t>(), plane_l.as<uint4>(), g, n, N, tap_stride, stream);
-    launch_rcopy(gray_r.as<uint8_t>(), plane_r.as<uint32_t>(), g, n, N, copy_stride, stream);
-    launch_stats(gray_l.as<uint8_t>(), lstat.as<int2>(), nullptr, 0, g, n, N, N, stream);
-    launch_stats(gray_r.as<uint8_t>(), nullptr, rstat.as<int2>(), 1, g, n, N, rstride, stream);
+    launch_ltap(gl, plane_l.as<uint4>(), g, n, N, tap_stride, stream);
+    launch_rcopy(gr, plane_r.as<uint32_t>(), g, n, N, copy_stride, stream);
+    launch_stats(gl, lstat.as<int2>(), nullptr, 0, g, n, N, N, stream);
+    launch_stats(gr, nullptr, rstat.as<int2>(), 1, g, n, N, rstride, stream);
     stats.kernel_launches += 4;
     }
     ck(cudaMemsetAsync(flag_count.p, 0, sizeof(unsigned) * n, stream), "memset");
     if (do_argmax) {
-      ck(cudaMemsetAsync(disp_a.p, 0, sizeof(float) * N * n, stream), "memset");
-      ck(cudaMemsetAsync(valid_a.p, 0, N * n, stream), "memset");
+      ck(cudaMemsetAsync(dsp, 0, sizeof(float) * N * n, stream), "memset");
+      ck(cudaMemsetAsync(vld, 0, N * n, stream), "memset");
     }
     Stage st(this, 2);
     launch_wta11(plane_l.as<uint4>(), plane_r.as<uint32_t>(), lstat.as<int2>(), rstat.as<int2>(),
-                 win.as<wscore_t>(), wbase.as<int>(), nullptr, disp_a.as<float>(),
-                 valid_a.as<uint8_t>(), flags.as<int>(), flag_count.as<unsigned>(), g,
+                 windows ? win.as<wscore_t>() : nullptr, wbase.as<int>(), nullptr, dsp, vld,
+                 flags.as<int>(), flag_count.as<unsigned>(), g,
                  params.min_zncc, n, tap_stride, copy_stride, N, rstride, N, bs,
                  do_argmax ? 1 : 0, stream);
     stats.kernel_launches += 1;
@@ -361,26 +369,60 @@ struct ss_ctx {
     valid_b.ensure(N * n);
   }
 
-  // compute_disparity on gray_l/gray_r -> disp_a/valid_a.
-  bool run_wta(int n, const Geom& g) {
+  // compute_disparity of the pair (gl, gr) -> (dsp, vld); returns whether the
+  // fast path (and hence score windows, when asked for) was used.
+  bool wta_pair(int n, const Geom& g, const uint8_t* gl, const uint8_t* gr, float* dsp,
+                uint8_t* vld, bool windows) {
     const long N = g.N();
-    ensure_maps(N, n);
     if (fast_path(g, &params)) {
-      build_volume(n, g, true);
+      build_volume(n, g, true, gl, gr, dsp, vld, windows);
       Stage st(this, 3);
-      launch_wta_resolve(gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), flags.as<int>(),
-                         flag_count.as<unsigned>(), disp_a.as<float>(), valid_a.as<uint8_t>(),
-                         g, params.min_zncc, n, N, N, N, ctr() + 0, stream);
+      launch_wta_resolve(gl, gr, flags.as<int>(), flag_count.as<unsigned>(), dsp, vld, g,
+                         params.min_zncc, n, N, N, N, ctr() + 0, stream);
       stats.kernel_launches += 1;
       return true;
     }
     Stage st(this, 2);
-    ck(cudaMemsetAsync(disp_a.p, 0, sizeof(float) * N * n, stream), "memset");
-    ck(cudaMemsetAsync(valid_a.p, 0, N * n, stream), "memset");
-    launch_wta_generic(gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), disp_a.as<float>(),
-                       valid_a.as<uint8_t>(), g, params.min_zncc, n, N, N, stream);
+    ck(cudaMemsetAsync(dsp, 0, sizeof(float) * N * n, stream), "memset");
+    ck(cudaMemsetAsync(vld, 0, N * n, stream), "memset");
+    launch_wta_generic(gl, gr, dsp, vld, g, params.min_zncc, n, N, N, stream);
     stats.kernel_launches += 1;
     return false;
+  }
+
+  // Right view (mirrored coordinates) into disp_r/valid_r: the left-view
+  // sweep of (flip R, flip L), k_lr.cu.
+  void run_wta_right(int n, const Geom& g) {
+    const long N = g.N();
+    gray_fl.ensure(N * n);
+    gray_fr.ensure(N * n);
+    disp_r.ensure(sizeof(float) * N * n);
+    valid_r.ensure(N * n);
+    {
+      Stage st(this, 0);
+      launch_flip_pair(gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), gray_fl.as<uint8_t>(),
+                       gray_fr.as<uint8_t>(), g.W, g.H, n, N, stream);
+      stats.kernel_launches += 1;
+    }
+    wta_pair(n, g, gray_fl.as<uint8_t>(), gray_fr.as<uint8_t>(), disp_r.as<float>(),
+             valid_r.as<uint8_t>(), false);
+  }
+
+  // compute_disparity on gray_l/gray_r -> disp_a/valid_a (+ the opt-in LR
+  // check: right view first, so the left sweep's buffers stay for refine).
+  bool run_wta(int n, const Geom& g) {
+    const long N = g.N();
+    ensure_maps(N, n);
+    if (lr_check) run_wta_right(n, g);
+    const bool fast = wta_pair(n, g, gray_l.as<uint8_t>(), gray_r.as<uint8_t>(),
+                               disp_a.as<float>(), valid_a.as<uint8_t>(), true);
+    if (lr_check) {
+      Stage st(this, 3);
+      launch_lr_check(disp_a.as<float>(), valid_a.as<uint8_t>(), disp_r.as<float>(),
+                      valid_r.as<uint8_t>(), g.W, g.H, lr_max_diff, n, N, stream);
+      stats.kernel_launches += 1;
+    }
+    return fast;
   }
 
   void ensure_wtab(int radius) {
@@ -728,6 +770,46 @@ ss_status ss_compute_disparity(const ss_stereo_params* p, const uint8_t* left, i
   });
 }
 
+ss_status ss_compute_disparity_lr(const ss_stereo_params* p, const uint8_t* left, int32_t lw,
+                                  int32_t lh, const uint8_t* right, int32_t rw, int32_t rh,
+                                  int32_t max_diff, float* disparity, uint8_t* valid,
+                                  float* right_disparity, uint8_t* right_valid) {
+  return guarded([&] {
+    if (lw != rw || lh != rh) raise(SS_EINVAL, "compute_disparity: image sizes differ");
+    validate_params(p);
+    check_dims(lw, lh, "compute_disparity");
+    if (max_diff < 0) raise(SS_EINVAL, "compute_disparity_lr: max_diff must be >= 0");
+    const long N = (long)lw * lh;
+    if (N == 0) return;
+    ss_ctx* c = thread_ctx();
+    c->params = *p;
+    h2d(c->gray_l, left, N, c->stream);
+    h2d(c->gray_r, right, N, c->stream);
+    const Geom g = make_geom(lw, lh, p);
+    c->lr_check = true;
+    c->lr_max_diff = max_diff;
+    try {
+      c->run_wta(1, g);
+    } catch (...) {
+      c->lr_check = false;
+      throw;
+    }
+    c->lr_check = false;
+    d2h(disparity, c->disp_a.p, sizeof(float) * N, c->stream);
+    d2h(valid, c->valid_a.p, N, c->stream);
+    if (right_disparity || right_valid) {
+      c->disp_b.ensure(sizeof(float) * N);
+      c->valid_b.ensure(N);
+      launch_unflip_map(c->disp_r.as<float>(), c->valid_r.as<uint8_t>(), c->disp_b.as<float>(),
+                        c->valid_b.as<uint8_t>(), lw, lh, 1, N, c->stream);
+      c->stats.kernel_launches += 1;
+      if (right_disparity) d2h(right_disparity, c->disp_b.p, sizeof(float) * N, c->stream);
+      if (right_valid) d2h(right_valid, c->valid_b.p, N, c->stream);
+    }
+    sync(c);
+  });
+}
+
 ss_status ss_remove_outliers(const float* disparity, const uint8_t* valid, int32_t w, int32_t h,
                              int32_t radius, double threshold, float* out_disparity,
                              uint8_t* out_valid) {
@@ -820,7 +902,9 @@ ss_status ss_refine_disparities(const ss_stereo_params* p, const float* disparit
     h2d(c->gray_l, left, N, c->stream);
     h2d(c->gray_r, right, N, c->stream);
     const bool vol_ok = fast_path(g, p);
-    if (vol_ok) c->build_volume(1, g, false);
+    if (vol_ok)
+      c->build_volume(1, g, false, c->gray_l.as<uint8_t>(), c->gray_r.as<uint8_t>(),
+                      c->disp_a.as<float>(), c->valid_a.as<uint8_t>(), true);
     ck(cudaMemcpyAsync(c->disp_a.p, disparity, sizeof(float) * N, cudaMemcpyHostToDevice,
                        c->stream), "H2D");
     ck(cudaMemcpyAsync(c->valid_a.p, valid, N, cudaMemcpyHostToDevice, c->stream), "H2D");
@@ -901,6 +985,15 @@ ss_status ss_ctx_destroy(ss_ctx* ctx) {
     ctx->activate();
     cudaStreamSynchronize(ctx->stream);
     delete ctx;
+  });
+}
+
+ss_status ss_ctx_set_lr_check(ss_ctx* ctx, int32_t enable, int32_t max_diff) {
+  return guarded([&] {
+    if (!ctx) raise(SS_EINVAL, "ss_ctx_set_lr_check: null ctx");
+    if (max_diff < 0) raise(SS_EINVAL, "ss_ctx_set_lr_check: max_diff must be >= 0");
+    ctx->lr_check = enable != 0;
+    ctx->lr_max_diff = max_diff;
   });
 }
 

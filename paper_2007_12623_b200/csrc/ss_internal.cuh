@@ -79,6 +79,7 @@ void launch_stats(const uint8_t* gray, int2* lstat, int2* rstat, int is_right, c
 // window: kWin scores s(c) = g(c) / sqrt(var_l) for c = wbase .. wbase+kWin-1,
 // wbase centred on the WTA pick, or on base_map[pixel] when base_map != NULL
 // (per-stage refine). wbase = kNoWin when var_l == 0 (no defined score).
+// win == NULL: argmax only (the right-view sweep of the LR check).
 // win / wbase are BT-indexed (bt_index, frame stride win_stride).
 void launch_wta11(const uint4* ltap, const uint32_t* rcopy, const int2* lstat,
                   const int2* rstat, wscore_t* win, int* wbase, const int* base_map, float* disp,
@@ -100,6 +101,15 @@ void launch_wta_resolve(const uint8_t* lgray, const uint8_t* rgray, const int* f
 void launch_wta_generic(const uint8_t* lgray, const uint8_t* rgray, float* disp,
                         uint8_t* valid, const Geom& g, double min_zncc, int frames,
                         long gray_stride, long map_stride, cudaStream_t s);
+
+// Left-right consistency (k_lr.cu): mirrored swapped pair for the right-view
+// sweep, the check itself, and mirroring a right-view map back.
+void launch_flip_pair(const uint8_t* gl, const uint8_t* gr, uint8_t* out_l, uint8_t* out_r,
+                      int W, int H, int frames, long stride, cudaStream_t s);
+void launch_lr_check(float* disp, uint8_t* valid, const float* disp_rm, const uint8_t* valid_rm,
+                     int W, int H, int max_diff, int frames, long stride, cudaStream_t s);
+void launch_unflip_map(const float* dm, const uint8_t* vm, float* d, uint8_t* v, int W, int H,
+                       int frames, long stride, cudaStream_t s);
 
 // emap: scratch of edge_map_words(W, H) * frames words (smooth-edge bitmaps)
 inline long edge_map_words(int W, int H) {

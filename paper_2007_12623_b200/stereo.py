@@ -5,6 +5,7 @@ Same names, argument meaning and error behaviour as
 the C-ABI (include/ss_stereo.h) to the sm_100a kernels.
 
     compute_disparity(left, right, params)         -> (disparity, valid)
+    compute_disparity_lr(left, right, params, max_diff)  opt-in LR consistency
     remove_outliers(disp, valid, radius, thr)      -> (disparity, valid)
     fill_holes(disp, valid, mode, radius, support) -> (disparity, valid)
     cleanup_pass(disp, valid, params)              -> (disparity, valid)
@@ -142,6 +143,22 @@ def compute_disparity(left, right, params=None):
     return disp, valid
 
 
+def compute_disparity_lr(left, right, params=None, max_diff=1):
+    """compute_disparity + opt-in left-right consistency (extension; the
+    reference has none). Returns (disparity, valid, right_disparity,
+    right_valid): the LR-checked left map and the right-view WTA map."""
+    left, right = _u8(left), _u8(right)
+    (lh, lw), (rh, rw) = left.shape, right.shape
+    disp = np.zeros((lh, lw), np.float32)
+    valid = np.zeros((lh, lw), np.uint8)
+    rdisp = np.zeros((lh, lw), np.float32)
+    rvalid = np.zeros((lh, lw), np.uint8)
+    _check(L.lib().ss_compute_disparity_lr(C.byref(_params(params)), _ptr(left), lw, lh,
+                                           _ptr(right), rw, rh, int(max_diff), _ptr(disp),
+                                           _ptr(valid), _ptr(rdisp), _ptr(rvalid)))
+    return disp, valid, rdisp, rvalid
+
+
 def remove_outliers(disp, valid, radius, threshold):
     disp, valid = _f32(disp), _u8(valid)
     h, w = disp.shape
@@ -220,13 +237,20 @@ class StereoContext:
     one GPU. ``run`` takes host arrays (pinned via ``pinned_empty`` for speed);
     ``run_device`` takes raw device pointers (e.g. torch ``data_ptr()``)."""
 
-    def __init__(self, device=0, max_w=960, max_h=540, max_batch=8, params=None, rig=None):
+    def __init__(self, device=0, max_w=960, max_h=540, max_batch=8, params=None, rig=None,
+                 lr_check=False, lr_max_diff=1):
         self._ctx = C.c_void_p()
         self.params = params
         r = C.byref(_rig(rig)) if rig is not None else None
         _check(L.lib().ss_ctx_create(device, max_w, max_h, max_batch,
                                      C.byref(_params(params)), r, C.byref(self._ctx)))
         self.max_batch = max_batch
+        if lr_check:
+            self.set_lr_check(True, lr_max_diff)
+
+    def set_lr_check(self, enable=True, max_diff=1):
+        """Opt-in left-right consistency after the WTA (off: reference output)."""
+        _check(L.lib().ss_ctx_set_lr_check(self._ctx, 1 if enable else 0, int(max_diff)))
 
     def close(self):
         if self._ctx:

@@ -1,0 +1,139 @@
+"""Opt-in left-right consistency (north_star "winner-take-
+all disparity selection with left-right consistency"). The reference has no LR
+check, so this extension is pinned two ways:
+
+* the right-view WTA restatement (orc_compute_disparity_right, written from
+  the definition d_R(x) = first argmax_d zncc(left at x + d, right at x)) is
+  checked against the REFERENCE's own compute_disparity run on the mirrored,
+  swapped pair — the identity the GPU implementation relies on;
+* the LR rule itself is checked on hand-built maps;
+
+and the GPU path (ss_compute_disparity_lr, ss_ctx_set_lr_check) is bit-exact
+against the oracle (-m gpu). With the check off, the chain is the reference's
+(test_gpu_parity.py).
+"""
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from paper_2007_12623_b200.synth import as_rgb, default_rig, params_for, stereo_pair
+
+
+def _mirror_identity(orc, ref, L, R, p):
+    dr, vr = orc.compute_disparity_right(L, R, p)
+    dm, vm = ref.compute_disparity(np.fliplr(R), np.fliplr(L), p)
+    assert np.array_equal(vr, np.fliplr(vm))
+    assert np.array_equal(dr.view(np.uint32), np.fliplr(dm).copy().view(np.uint32))
+    return dr, vr
+
+
+@pytest.mark.parametrize("kind,D", [("textured", 16), ("lowtex", 16)])
+def test_right_view_restatement_is_the_mirrored_reference(orc, ref, kind, D):
+    L, R, _ = stereo_pair(kind, 96, 64, D, seed=3)
+    dr, vr = _mirror_identity(orc, ref, L, R, params_for(D))
+    assert vr.sum() > 0
+
+
+def test_right_view_restatement_default_params(orc, ref):
+    g = load_golden("tex_default")
+    _mirror_identity(orc, ref, g["left"], g["right"], g["params"])
+
+
+def test_right_view_restatement_random(orc, ref):
+    rng = np.random.default_rng(11)
+    p = params_for(8, d_min=-3, d_max=9)
+    for _ in range(4):
+        L = rng.integers(0, 256, (40, 48), dtype=np.uint8)
+        R = rng.integers(0, 256, (40, 48), dtype=np.uint8)
+        _mirror_identity(orc, ref, L, R, p)
+
+
+def test_lr_rule(orc):
+    d = np.array([[2, 3, 0, 5, 1, 7]], np.float32)
+    v = np.array([[1, 1, 0, 1, 1, 1]], np.uint8)
+    dr = np.array([[2, 1, 2, 9, 0, 0]], np.float32)
+    vr = np.array([[1, 1, 1, 1, 0, 1]], np.uint8)
+    od, ov = orc.lr_check(d, v, dr, vr, max_diff=1)
+    # u=0: x=-2 out of image -> rejected; u=1: x=-2 -> rejected; u=2 invalid kept as is;
+    # u=3: x=-2 -> rejected; u=4: x=3, d_R=9 -> |9-1|>1 rejected; u=5: x=-2 rejected
+    assert ov.tolist() == [[0, 0, 0, 0, 0, 0]]
+    d = np.array([[0, 1, 1, 2, 3, 3]], np.float32)
+    v = np.ones((1, 6), np.uint8)
+    dr = np.array([[1, 2, 1, 1, 0, 9]], np.float32)
+    vr = np.array([[1, 1, 1, 1, 1, 0]], np.uint8)
+    od, ov = orc.lr_check(d, v, dr, vr, max_diff=1)
+    # u=0: x=0 d_R=1 ok; u=1: x=0 ok (|1-1|); u=2: x=1 d_R=2 ok; u=3: x=1 d_R=2 ok;
+    # u=4: x=1 d_R=2 |2-3|=1 ok; u=5: x=2 d_R=1 |1-3|=2 rejected
+    assert ov.tolist() == [[1, 1, 1, 1, 1, 0]]
+    assert od[0, 5] == 0.0 and np.array_equal(od[0, :5], d[0, :5])
+    od, ov = orc.lr_check(d, v, dr, vr, max_diff=0)
+    assert ov.tolist() == [[0, 1, 0, 1, 0, 0]]
+
+
+def test_lr_removes_mismatches_on_lowtex(orc):
+    L, R, _ = stereo_pair("lowtex", 128, 80, 16, seed=5)
+    p = params_for(16)
+    d, v = orc.compute_disparity(L, R, p)
+    od, ov, _, _ = orc.compute_disparity_lr(L, R, p, max_diff=1)
+    assert np.all(ov <= v) and ov.sum() < v.sum()
+
+
+# ---------------- GPU (through the C-ABI) ----------------
+
+@pytest.fixture(scope="module")
+def ss():
+    import paper_2007_12623_b200 as ss
+    from paper_2007_12623_b200.build import build
+    build(verbose=False)
+    if ss.device_count() < 1:
+        pytest.fail("no CUDA device visible to the GPU tests")
+    return ss
+
+
+def _eq(a, b):
+    a, b = np.ascontiguousarray(a), np.ascontiguousarray(b)
+    return np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,W,H,D", [("textured", 320, 180, 32), ("lowtex", 320, 180, 32),
+                                        ("textured", 960, 540, 64)])
+def test_gpu_lr_matches_oracle(ss, orc, kind, W, H, D):
+    L, R, _ = stereo_pair(kind, W, H, D, seed=7)
+    p = params_for(D)
+    got = ss.compute_disparity_lr(L, R, p, max_diff=1)
+    want = orc.compute_disparity_lr(L, R, p, max_diff=1)
+    for g, w, what in zip(got, want, ["disp", "valid", "right disp", "right valid"]):
+        assert _eq(g, w), f"{kind} {W}x{H}: {what} differs"
+
+
+@pytest.mark.gpu
+def test_gpu_lr_default_params_and_windows(ss, orc):
+    g = load_golden("tex_default")
+    got = ss.compute_disparity_lr(g["left"], g["right"], g["params"], max_diff=0)
+    want = orc.compute_disparity_lr(g["left"], g["right"], g["params"], max_diff=0)
+    assert all(_eq(a, b) for a, b in zip(got, want))
+    p = dict(g["params"], window=7)  # generic (non-fast) sweep path
+    got = ss.compute_disparity_lr(g["left"], g["right"], p)
+    want = orc.compute_disparity_lr(g["left"], g["right"], p)
+    assert all(_eq(a, b) for a, b in zip(got, want))
+
+
+@pytest.mark.gpu
+def test_gpu_batch_chain_with_lr(ss, orc):
+    W, H, D = 192, 112, 24
+    p = params_for(D)
+    rig = default_rig(W, H)
+    frames = [stereo_pair(k, W, H, D, seed=s)[:2] for k, s in
+              [("textured", 1), ("lowtex", 2), ("textured", 3)]]
+    Ls = np.stack([as_rgb(f[0]) for f in frames])
+    Rs = np.stack([as_rgb(f[1]) for f in frames])
+    ctx = ss.StereoContext(0, W, H, len(frames), ss.StereoParams(**p), ss.StereoRig(**rig),
+                           lr_check=True, lr_max_diff=1)
+    out = ctx.run(Ls, Rs, ss.SS_OUT_DISPARITY)
+    ctx.close()
+    for i, (L, R) in enumerate(frames):
+        d, v, _, _ = orc.compute_disparity_lr(L, R, p, max_diff=1)
+        d, v = orc.cleanup_pass(d, v, p)
+        d, v = orc.refine_disparities(d, v, L, R, p)
+        assert _eq(out["valid"][i], v) and _eq(out["disparity"][i], d), f"frame {i}"
