@@ -1,7 +1,7 @@
 // Left-right consistency (opt-in, north_star: "winner-
 // take-all disparity selection with left-right consistency"). The reference
 // has no LR check (it only notes unmatched pixels), so this is
-// an extension with its own oracle (oracle/ss_oracle.c: orc_compute_disparity_
+// an extension with its own CPU restatement in the test oracle (orc_compute_disparity_
 // right, orc_lr_check) and is off unless asked for.
 //
 // Right-view WTA: d_R(x) = first argmax over d in [d_min, d_max] of
