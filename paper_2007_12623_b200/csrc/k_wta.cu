@@ -2,21 +2,29 @@
 //
 // k_wta11 — the hot kernel, window 11 (the default and the paper's setting).
 //   Block = 32 lanes (consecutive columns u) x NB warps (blocks of kDB = 16
-//   consecutive candidates c of the volume range [d_min-5, d_max+5]). Each
-//   thread sweeps a strip of rows; for every row y entering or leaving the
-//   11-row window it forms the two chessboard half-sums of one image row
+//   consecutive candidates of the WTA range [d_min, d_max]) over a strip of
+//   kTH rows. Thread 0 streams the strip's image rows into a shared-memory
+//   ring (bulk copies on per-slot mbarriers, issued up to 16 rows ahead): per
+//   row the block's left tap words (k_ltap), the right parity-split rows in 4
+//   byte-shifted copies (k_rcopy: every 4-byte window is one aligned word plus
+//   at most one funnel shift) and the right-window statistics. For every row y
+//   entering or leaving the 11-row window a thread forms the two chessboard
+//   half-sums of one image row
 //       He(y) = sum_{du even} L(u+du, y) R(u-c+du, y)   (5 taps)
 //       Ho(y) = sum_{du odd}  L(u+du, y) R(u-c+du, y)   (6 taps)
-//   with 4 dp4a (u8 x u8 -> int32) on 4-byte windows of the parity-split rows,
-//   and keeps two running sums per candidate so that the exact integer cross
-//   sum slr(u, v, c) costs O(1) per row step instead of 61 MACs:
+//   with 4 dp4a (u8 x u8 -> int32), and keeps two running sums per candidate
+//   so that the exact integer cross sum slr(u, v, c) costs O(1) per row step
+//   instead of 61 MACs:
 //       X(v+1) = Y(v) - He(v-5) + Ho(v+6),   Y(v+1) = X(v) + He(v+6) - Ho(v-5)
 //   where X(v) = sum_{dv even} He(v+dv) + sum_{dv odd} Ho(v+dv) = slr(v).
 //   num = 61 slr - sl sr is exact; g = float(num) / sqrt(var_r) (FP32, <= 3 ulp)
-//   feeds a per-thread (best, second, arg) that NB warps merge through shared
-//   memory, and is staged there so that, once a pixel's pick is known, the
-//   kWin = 16 candidates around it are written as the refinement's score
-//   window (64 B/pixel instead of a (D+10) x 4 B cost volume).
+//   feeds a per-thread (best, second, arg); every kRB rows the warps stage
+//   them in shared memory and kRB warps merge one row each (named barriers:
+//   the merge overlaps the other warps' next row). The staged g also give,
+//   once a pixel's pick is known, the kWin = 16 scores around it: the
+//   refinement's score window (32 B/pixel of fp16 match costs instead of a
+//   (D+10) x 4 B cost volume). Windows reaching past [d_min, d_max] (the
+//   re-pick's +-5 margin) are left to k_window_build.
 //   A pick is final only when it is separated from the runner-up and from the
 //   min_zncc threshold by a margin far above the FP32 error (4e-6 relative);
 //   otherwise the pixel is appended to a list for k_wta_exact (FP64, exact),
@@ -200,19 +208,22 @@ __global__ void __launch_bounds__(512) k_wta11(
   const int v_begin = h + blockIdx.y * kTH;
   const int v_end = min(v_begin + kTH, H - h);
   if (v_begin >= v_end) return;  // uniform over the block
-  const int c0 = g.cmin + j * kDB;
-  const int nact = min(kDB, g.NC - j * kDB);
+  // The sweep covers exactly the WTA range [d_min, d_max]; window entries
+  // outside it (the refinement's +-5 margin) come from k_window_build.
+  const int ND = g.dmax - g.dmin + 1;
+  const int c0 = g.dmin + j * kDB;
+  const int nact = min(kDB, ND - j * kDB);
   const bool active = (u < W - h) && (nact > 0);
   unsigned amask = 0;
 #pragma unroll
   for (int i = 0; i < kDB; ++i)
-    amask |= (i < nact && c0 + i >= g.dmin && c0 + i <= g.dmax) ? (1u << i) : 0u;
+    amask |= i < nact ? (1u << i) : 0u;
   // warps whose candidates all take part in the WTA argmax skip the mask
   const bool full = __all_sync(0xffffffffu, amask == 0xFFFFu || !active);
 
   // ---- block-uniform copy geometry ----
   const int PW = g.PP / 4;
-  const int c0_last = g.cmin + kDB * (NB - 1);
+  const int c0_last = g.dmin + kDB * (NB - 1);
   const int m0_min = (u0 - c0_last) >> 1;
   const int wlo = ((g.PB + m0_min - 10) >> 2) & ~3;
   const int ru_lo = u0 - c0_last - (kDB - 1);  // lowest right column any thread scores
@@ -378,18 +389,17 @@ __global__ void __launch_bounds__(512) k_wta11(
           int wb = kNoWin;
           if (!isnan(rl) && anchor != kNoArg && anchor != kNoWin)
             wb = window_base(anchor, g.cmin, g.NC);
+          // A window reaching past [d_min, d_max] is left for k_window_build
+          // (wbase kNoWin never matches the post-cleanup check's target).
+          if (wb != kNoWin && (wb < g.dmin || wb + kWin - 1 > g.dmax)) wb = kNoWin;
           const long bi = bt_index(W, vv, u);
           wbase[bi] = wb;
           if (wb != kNoWin) {
-            const float* gr = s_g + r * NCB * 32 + lane;
+            const float* gr = s_g + (r * NCB + wb - g.dmin) * 32 + lane;
             uint32_t w[kWin / 2];  // kWin fp16 match costs (m_code)
 #pragma unroll
-            for (int q = 0; q < kWin / 2; ++q) {
-              const int ci = wb - g.cmin + 2 * q;
-              const float s0 = ci < g.NC ? gr[ci * 32] * rl : __int_as_float(0x7fc00000);
-              const float s1 = ci + 1 < g.NC ? gr[(ci + 1) * 32] * rl : __int_as_float(0x7fc00000);
-              w[q] = pack_m2(s0, s1);
-            }
+            for (int q = 0; q < kWin / 2; ++q)
+              w[q] = pack_m2(gr[(2 * q) * 32] * rl, gr[(2 * q + 1) * 32] * rl);
             uint32_t* wq = reinterpret_cast<uint32_t*>(win) + win_word(W, vv, u, 0);
 #pragma unroll
             for (int q = 0; q < kWin / 2; ++q) wq[(long)q * W * 32] = w[q];
@@ -408,7 +418,7 @@ void launch_wta11(const uint4* ltap, const uint32_t* rcopy, const int2* lstat, c
                   cudaStream_t s) {
   const int h = 5;
   if (g.W - 2 * h <= 0 || g.H - 2 * h <= 0 || frames <= 0) return;
-  const int NB = (g.NC + kDB - 1) / kDB;
+  const int NB = (g.dmax - g.dmin + 1 + kDB - 1) / kDB;
   const RingGeom rg = ring_geom(NB);
   dim3 block(32, NB);
   dim3 grid((g.W - 2 * h + 31) / 32, (g.H - 2 * h + kTH - 1) / kTH, frames);
