@@ -615,13 +615,20 @@ __global__ void __launch_bounds__(kThreads, 2)
                Deferred* __restrict__ defer, unsigned* __restrict__ defer_count, RefineArgs a,
                long gray_stride, const __grid_constant__ CUtensorMap map, int glob) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar, bar_win;
   const long f = blockIdx.z;
   const int W = a.g.W, H = a.g.H, R = RF > 0 ? RF : a.radius;
   const long bs = bt_frame(W, H, 0);
   const int lane = threadIdx.x, warp = threadIdx.y;
   const int tid = warp * 32 + lane;
   const int v = blockIdx.y * 32 + lane;
+  // The score windows (a third of the bytes) land on their own barrier,
+  // waited for only before the re-picks: the disc gathers start as soon as
+  // the psum box and the scalars are in.
+  if (tid == 0 && win) {
+    mbar_init(&bar_win, 1);
+    mbar_fence_init();
+  }
   const int u0 = blockIdx.x * kTC, rb = blockIdx.y;
   const int ncols = min(kTC, W - u0);
   const unsigned npx = ncols * 32;
@@ -634,21 +641,14 @@ __global__ void __launch_bounds__(kThreads, 2)
   int* s_o = s_cnt + kTilePx;
   int* s_wb = s_o + kTilePx;
   uint8_t* s_m = reinterpret_cast<uint8_t*>(s_wb + kTilePx);
-  // windows + wbase, S_o + o (or avg), cnt, mask
-  const unsigned extra = (win ? (kWin / 2) * npx * 4 + npx * 4 : 0) + npx * 8 + npx * 4 + npx;
+  // wbase, S_o + o (or avg), cnt, mask (the windows: bar_win)
+  const unsigned extra = (win ? npx * 4 : 0) + npx * 8 + npx * 4 + npx;
   const Tile<double> P = tile_issue<RF>(reinterpret_cast<double*>(smem),
                                         psumT + f * bt_frame(W, H, 1 + R), &map, W, R, glob, &bar,
                                         extra);
   if (tid == 0) {
     // the tile's per-pixel fields: contiguous BT ranges of npx entries
-    if (win) {
-      const uint32_t* wsrc = reinterpret_cast<const uint32_t*>(win) + f * bs * (kWin / 2);
-#pragma unroll 1
-      for (int j = 0; j < kWin / 2; ++j)
-        bulk_g2s(planes + j * kWinPlane, wsrc + (((long)rb * (kWin / 2) + j) * W + u0) * 32,
-                 npx * 4, &bar);
-      bulk_g2s(s_wb, wbase + e0, npx * 4, &bar);
-    }
+    if (win) bulk_g2s(s_wb, wbase + e0, npx * 4, &bar);
     if (USE_SO) {
       bulk_g2s(s_so, soT + e0, npx * 4, &bar);
       bulk_g2s(s_o, oT + e0, npx * 4, &bar);
@@ -657,8 +657,17 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     bulk_g2s(s_cnt, cntT + e0, npx * 4, &bar);
     bulk_g2s(s_m, mT + e0, npx, &bar);
+    if (win) {
+      mbar_expect_tx(&bar_win, (kWin / 2) * npx * 4);
+      const uint32_t* wsrc = reinterpret_cast<const uint32_t*>(win) + f * bs * (kWin / 2);
+#pragma unroll 1
+      for (int j = 0; j < kWin / 2; ++j)
+        bulk_g2s(planes + j * kWinPlane, wsrc + (((long)rb * (kWin / 2) + j) * W + u0) * 32,
+                 npx * 4, &bar_win);
+    }
   }
   tile_wait(&bar);
+  bool win_ready = win == nullptr;
   const uint8_t* L = lgray + f * gray_stride;
   const uint8_t* Rg = rgray + f * gray_stride;
 #pragma unroll 1
@@ -682,6 +691,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     const double x = __dsub_rn(a_o, bav);
     const double dv = x < a.lo ? a.lo : (a.hi < x ? a.hi : x);  // std::clamp
     dT[bi] = dv;
+    if (!win_ready) {
+      mbar_wait(&bar_win, 0);
+      win_ready = true;
+    }
     const int best = repick(a, u, v, dv, L, Rg, win != nullptr, wv, wbk, px, defer + f * bs,
                             defer_count + f);
     if (best != INT_MIN) {
@@ -690,6 +703,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       oT[bi] = best;
     }
   }
+  // the window copies must land before the block's shared memory is released
+  if (!win_ready) mbar_wait(&bar_win, 0);
 }
 
 void launch_d_repick(const double* psumT, const uint8_t* mT, const int* cntT,
