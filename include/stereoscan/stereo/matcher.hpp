@@ -22,4 +22,14 @@ std::optional<int> match_pixel(const GrayImage& left, const GrayImage& right, in
 DisparityMap compute_disparity(const GrayImage& left, const GrayImage& right,
                                const StereoParams& params);
 
+// Extension (no reference analogue): compute_disparity
+// followed by a left-right consistency check. A valid pixel u with disparity d
+// is kept iff x = u - d is inside the image, the right-view WTA (first argmax
+// over d of zncc(left at x + d, right at x)) is valid at x and within max_diff
+// of d; rejected pixels become (0, invalid). `right_map`, when given, receives
+// the right-view map. max_diff < 0 throws std::invalid_argument.
+DisparityMap compute_disparity_lr(const GrayImage& left, const GrayImage& right,
+                                  const StereoParams& params, int max_diff = 1,
+                                  DisparityMap* right_map = nullptr);
+
 }  // namespace stereoscan

@@ -160,6 +160,24 @@ DisparityMap compute_disparity(const GrayImage& left, const GrayImage& right,
   return map;
 }
 
+DisparityMap compute_disparity_lr(const GrayImage& left, const GrayImage& right,
+                                  const StereoParams& params, int max_diff,
+                                  DisparityMap* right_map) {
+  if (left.width != right.width || left.height != right.height) {
+    throw std::invalid_argument("compute_disparity: image sizes differ");
+  }
+  const ss_stereo_params c = to_c(params);
+  throw_on(ss_params_validate(&c));
+  DisparityMap map(left.width, left.height);
+  DisparityMap rmap(left.width, left.height);
+  throw_on(ss_compute_disparity_lr(&c, left.pixels.data(), left.width, left.height,
+                                   right.pixels.data(), right.width, right.height, max_diff,
+                                   map.disparity.data(), map.valid.data(),
+                                   rmap.disparity.data(), rmap.valid.data()));
+  if (right_map) *right_map = std::move(rmap);
+  return map;
+}
+
 DisparityMap remove_outliers(const DisparityMap& map, int radius, double threshold) {
   DisparityMap out(map.width, map.height);
   throw_on(ss_remove_outliers(map.disparity.data(), map.valid.data(), map.width, map.height,

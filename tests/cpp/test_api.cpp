@@ -45,6 +45,20 @@ int main() {
   // match_pixel agrees with the dense search
   const auto mp = match_pixel(left, right, 80, 30, p);
   CHECK(mp.has_value() && *mp == 7);
+  // LR-consistency extension: a pure shift is consistent wherever the right
+  // view sees the same match; the right view holds 7 too.
+  DisparityMap rm;
+  const DisparityMap lr = compute_disparity_lr(left, right, p, 1, &rm);
+  CHECK(lr.valid_count() > 0 && lr.valid_count() <= m.valid_count());
+  for (size_t i = 0; i < lr.valid.size(); ++i)
+    if (lr.valid[i]) CHECK(m.valid[i] && lr.disparity[i] == 7.0f);
+  for (size_t i = 0; i < rm.valid.size(); ++i)
+    if (rm.valid[i]) CHECK(rm.disparity[i] == 7.0f);
+  try {
+    compute_disparity_lr(left, right, p, -1);
+    CHECK(false);
+  } catch (const std::invalid_argument&) {
+  }
 
   // uniform pair -> all invalid
   GrayImage flat(64, 48, 77);
