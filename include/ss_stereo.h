@@ -16,6 +16,9 @@
  *   ss_disparity_to_cloud   replaces disparity_to_cloud  cloud.hpp:34-35, cloud.cpp:14-94
  *   ss_params_validate      replaces StereoParams::validate  params.hpp:23, matcher.cpp:9-19
  *   ss_rig_validate         replaces StereoRig::validate     types.hpp:39, geometry.cpp:7-19
+ *   ss_detect_corners       replaces features::detect_corners  features.hpp:52, features.cpp:86-124
+ *   ss_describe             replaces features::describe        features.hpp:57, features.cpp:126-166
+ *   ss_match_features       replaces features::match_features  features.hpp:61, features.cpp:168-208
  *
  * Throughput entry (no reference analogue): ss_ctx_* run the
  * whole run_stereo_only chain for a batch of frames on one
@@ -131,6 +134,33 @@ ss_status ss_disparity_to_cloud(const float* disparity, const uint8_t* valid, in
                                 const ss_stereo_rig* rig, int32_t* index, double* points,
                                 double* normals, uint8_t* colors, int32_t* pixels,
                                 int32_t* n_points);
+
+/* ---- feature front end (features.hpp:45-66) ----
+ * Same results as the reference (integer work, bit-exact). */
+
+/* detect_corners (features.hpp:52, features.cpp:86-124): u/v/score arrays of
+ * capacity max_count, sorted by score descending then raster order; *n gets
+ * the count. threshold < 1 -> SS_EINVAL "detect_corners: threshold must be >= 1". */
+ss_status ss_detect_corners(const uint8_t* gray, int32_t w, int32_t h, int32_t max_count,
+                            int32_t threshold, int32_t* u, int32_t* v, int32_t* score,
+                            int32_t* n);
+
+/* describe (features.hpp:57, features.cpp:126-166): for the given corners (in
+ * order; those within 16 px of the border dropped) the position (u, v) as
+ * doubles and the 256-bit descriptor as 4 x uint64 (Descriptor256::bits);
+ * capacity n_corners; *n gets the count. */
+ss_status ss_describe(const uint8_t* gray, int32_t w, int32_t h, const int32_t* u,
+                      const int32_t* v, const int32_t* score, int32_t n_corners, double* pos,
+                      uint64_t* desc, int32_t* n);
+
+/* match_features (features.hpp:61, features.cpp:168-208): mutual Hamming
+ * nearest neighbours gated at max_hamming, in index_a order; per match
+ * index_a, index_b, hamming and displacement (b - a, 2 doubles); capacity
+ * min(na, nb); *n gets the count. */
+ss_status ss_match_features(const double* pos_a, const uint64_t* desc_a, int32_t na,
+                            const double* pos_b, const uint64_t* desc_b, int32_t nb,
+                            int32_t max_hamming, int32_t* index_a, int32_t* index_b,
+                            int32_t* hamming, double* displacement, int32_t* n);
 
 /* ---- throughput API: a batch of frames through the whole chain on one GPU ---- */
 

@@ -187,6 +187,63 @@ class Oracle:
         od, ov = self.lr_check(d, v, dr, vr, max_diff)
         return od, ov, dr, vr
 
+    # --- feature front end (reference only: features.cpp) ---
+    def detect_corners(self, gray, max_count, threshold):
+        g = np.ascontiguousarray(gray, np.uint8)
+        h, w = g.shape
+        cap = max(int(max_count), 0)
+        u, v, sc = (np.zeros(max(cap, 1), np.int32) for _ in range(3))
+        n = _I32(0)
+        self._check(self.lib.ref_detect_corners(_p(g, _U8), w, h, int(max_count), int(threshold),
+                                                _p(u, _I32), _p(v, _I32), _p(sc, _I32),
+                                                C.byref(n)))
+        k = n.value
+        return np.stack([u[:k], v[:k], sc[:k]], axis=1) if k else np.zeros((0, 3), np.int32)
+
+    def describe(self, gray, corners):
+        g = np.ascontiguousarray(gray, np.uint8)
+        h, w = g.shape
+        c = np.ascontiguousarray(np.asarray(corners, np.int32).reshape(-1, 3))
+        nc = len(c)
+        u, v, sc = (np.ascontiguousarray(c[:, i]) for i in range(3))
+        pos = np.zeros((max(nc, 1), 2), np.float64)
+        desc = np.zeros((max(nc, 1), 4), np.uint64)
+        n = _I32(0)
+        self._check(self.lib.ref_describe(_p(g, _U8), w, h, _p(u, _I32), _p(v, _I32),
+                                          _p(sc, _I32), nc, _p(pos, _F64),
+                                          desc.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                          C.byref(n)))
+        return pos[:n.value].copy(), desc[:n.value].copy()
+
+    def match_features(self, pos_a, desc_a, pos_b, desc_b, max_hamming):
+        pa = np.ascontiguousarray(pos_a, np.float64).reshape(-1, 2)
+        pb = np.ascontiguousarray(pos_b, np.float64).reshape(-1, 2)
+        da = np.ascontiguousarray(desc_a, np.uint64).reshape(-1, 4)
+        db = np.ascontiguousarray(desc_b, np.uint64).reshape(-1, 4)
+        cap = max(min(len(da), len(db)), 1)
+        ia, ib, hm = (np.zeros(cap, np.int32) for _ in range(3))
+        dp = np.zeros((cap, 2), np.float64)
+        n = _I32(0)
+        u64 = C.POINTER(C.c_uint64)
+        self._check(self.lib.ref_match_features(
+            _p(pa, _F64), da.ctypes.data_as(u64), len(da), _p(pb, _F64), db.ctypes.data_as(u64),
+            len(db), int(max_hamming), _p(ia, _I32), _p(ib, _I32), _p(hm, _I32), _p(dp, _F64),
+            C.byref(n)))
+        k = n.value
+        return {"index_a": ia[:k].copy(), "index_b": ib[:k].copy(), "hamming": hm[:k].copy(),
+                "displacement": dp[:k].copy()}
+
+    def histogram_vote(self, matches, bin_size):
+        ia = np.ascontiguousarray(matches["index_a"], np.int32)
+        ib = np.ascontiguousarray(matches["index_b"], np.int32)
+        hm = np.ascontiguousarray(matches["hamming"], np.int32)
+        dp = np.ascontiguousarray(matches["displacement"], np.float64).reshape(-1, 2)
+        order = np.zeros(max(len(ia), 1), np.int32)
+        self._check(self.lib.ref_histogram_vote(_p(ia, _I32), _p(ib, _I32), _p(hm, _I32),
+                                                _p(dp, _F64), len(ia), C.c_double(bin_size),
+                                                _p(order, _I32)))
+        return order[:len(ia)].copy()
+
     def remove_outliers(self, disp, valid, radius, threshold, naive=False):
         disp = np.ascontiguousarray(disp, np.float32)
         valid = np.ascontiguousarray(valid, np.uint8)

@@ -13,6 +13,8 @@
 //   refine_disparities  smoothing.cpp:68-159
 //   to_gray             matcher.cpp:21-30
 //   zncc_chessboard     matcher.cpp:38-64
+//   features::*         features.cpp:86-258 (detect_corners, describe,
+//                       match_features, histogram_vote)
 //
 // Built by oracle/Makefile against /root/reference/proj/src (never copied).
 
@@ -20,6 +22,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "stereoscan/features/features.hpp"
 #include "stereoscan/stereo/cleanup.hpp"
 #include "stereoscan/stereo/matcher.hpp"
 #include "stereoscan/stereo/reference.hpp"
@@ -193,6 +196,91 @@ int ref_refine_disparities(const orc_params* p, const float* disp, const uint8_t
     for (size_t it = 0; want && it < trace.discrete.size(); ++it) {
       if (trace_discrete) std::memcpy(trace_discrete + it * n, trace.discrete[it].data(), n * 8);
       if (trace_smooth) std::memcpy(trace_smooth + it * n, trace.smooth[it].data(), n * 8);
+    }
+  });
+}
+
+// ---- features (features.cpp) ----
+// Corners: u/v/score arrays of capacity max_count; *n receives the count.
+int ref_detect_corners(const uint8_t* gray, int32_t w, int32_t h, int32_t max_count,
+                       int32_t threshold, int32_t* us, int32_t* vs, int32_t* scores,
+                       int32_t* n) {
+  return guarded([&] {
+    const auto cs = ss::features::detect_corners(gray_of(gray, w, h), max_count, threshold);
+    for (size_t i = 0; i < cs.size(); ++i) {
+      us[i] = cs[i].u;
+      vs[i] = cs[i].v;
+      scores[i] = cs[i].score;
+    }
+    *n = static_cast<int32_t>(cs.size());
+  });
+}
+
+// Features of the given corners: pos (u, v) doubles and 4 x u64 descriptor
+// words per feature, capacity nc; *n receives the count.
+int ref_describe(const uint8_t* gray, int32_t w, int32_t h, const int32_t* us,
+                 const int32_t* vs, const int32_t* scores, int32_t nc, double* pos,
+                 uint64_t* desc, int32_t* n) {
+  return guarded([&] {
+    std::vector<ss::features::Corner> cs(nc);
+    for (int i = 0; i < nc; ++i) cs[i] = {us[i], vs[i], scores[i]};
+    const auto fs = ss::features::describe(gray_of(gray, w, h), cs);
+    for (size_t i = 0; i < fs.size(); ++i) {
+      pos[2 * i] = fs[i].position.x();
+      pos[2 * i + 1] = fs[i].position.y();
+      for (int k = 0; k < 4; ++k) desc[4 * i + k] = fs[i].descriptor.bits[k];
+    }
+    *n = static_cast<int32_t>(fs.size());
+  });
+}
+
+static std::vector<ss::features::Feature> feats_of(const double* pos, const uint64_t* desc,
+                                                   int32_t n) {
+  std::vector<ss::features::Feature> fs(n);
+  for (int i = 0; i < n; ++i) {
+    fs[i].position = ss::Vec2(pos[2 * i], pos[2 * i + 1]);
+    for (int k = 0; k < 4; ++k) fs[i].descriptor.bits[k] = desc[4 * i + k];
+  }
+  return fs;
+}
+
+// Matches: index_a, index_b, hamming per match (capacity min(na, nb)),
+// displacement (du, dv) doubles; *n receives the count.
+int ref_match_features(const double* pos_a, const uint64_t* desc_a, int32_t na,
+                       const double* pos_b, const uint64_t* desc_b, int32_t nb,
+                       int32_t max_hamming, int32_t* ia, int32_t* ib, int32_t* ham,
+                       double* disp, int32_t* n) {
+  return guarded([&] {
+    const auto ms = ss::features::match_features(feats_of(pos_a, desc_a, na),
+                                                 feats_of(pos_b, desc_b, nb), max_hamming);
+    for (size_t i = 0; i < ms.size(); ++i) {
+      ia[i] = ms[i].index_a;
+      ib[i] = ms[i].index_b;
+      ham[i] = ms[i].hamming;
+      disp[2 * i] = ms[i].displacement.x();
+      disp[2 * i + 1] = ms[i].displacement.y();
+    }
+    *n = static_cast<int32_t>(ms.size());
+  });
+}
+
+// histogram_vote over n matches (index_a, index_b, hamming, displacement);
+// writes the permutation `order` (input index at each rank).
+int ref_histogram_vote(const int32_t* ia, const int32_t* ib, const int32_t* ham,
+                       const double* disp, int32_t n, double bin_size, int32_t* order) {
+  return guarded([&] {
+    ss::features::MatchSet ms(n);
+    for (int i = 0; i < n; ++i) {
+      ms[i].index_a = ia[i];
+      ms[i].index_b = ib[i];
+      ms[i].hamming = ham[i];
+      ms[i].displacement = ss::Vec2(disp[2 * i], disp[2 * i + 1]);
+    }
+    const auto out = ss::features::histogram_vote(ms, bin_size);
+    for (size_t r = 0; r < out.size(); ++r) {
+      int k = 0;  // recover the input index (index_a is unique per input match)
+      while (k < n && !(ms[k].index_a == out[r].index_a && ms[k].index_b == out[r].index_b)) ++k;
+      order[r] = k;
     }
   });
 }

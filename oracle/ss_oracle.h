@@ -91,6 +91,21 @@ int ref_naive_remove_outliers(const float* disp, const uint8_t* valid,
                               uint8_t* out_valid);
 int ref_params_validate(const orc_params* p);
 
+/* Reference-only: the feature front end (features.cpp:86-258; SURVEY.md §8f
+ * row 4), the oracle of the GPU feature kernels. */
+int ref_detect_corners(const uint8_t* gray, int32_t w, int32_t h, int32_t max_count,
+                       int32_t threshold, int32_t* us, int32_t* vs, int32_t* scores,
+                       int32_t* n);
+int ref_describe(const uint8_t* gray, int32_t w, int32_t h, const int32_t* us,
+                 const int32_t* vs, const int32_t* scores, int32_t nc, double* pos,
+                 uint64_t* desc, int32_t* n);
+int ref_match_features(const double* pos_a, const uint64_t* desc_a, int32_t na,
+                       const double* pos_b, const uint64_t* desc_b, int32_t nb,
+                       int32_t max_hamming, int32_t* ia, int32_t* ib, int32_t* ham,
+                       double* disp, int32_t* n);
+int ref_histogram_vote(const int32_t* ia, const int32_t* ib, const int32_t* ham,
+                       const double* disp, int32_t n, double bin_size, int32_t* order);
+
 /* Restatement-only: disparity_to_cloud (cloud.cpp:14-94), Eigen-free.
  * Outputs are sized for w*h points; *n_points receives the count.
  * points/normals are xyz doubles per point, colors rgb bytes, pixels (u,v). */

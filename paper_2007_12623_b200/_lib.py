@@ -73,6 +73,9 @@ def lib():
         "ss_compute_disparity": (i32, [P(SsParams), vp, i32, i32, vp, i32, i32, vp, vp]),
         "ss_compute_disparity_lr": (i32, [P(SsParams), vp, i32, i32, vp, i32, i32, i32, vp, vp,
                                           vp, vp]),
+        "ss_detect_corners": (i32, [vp, i32, i32, i32, i32, vp, vp, vp, P(i32)]),
+        "ss_describe": (i32, [vp, i32, i32, vp, vp, vp, i32, vp, vp, P(i32)]),
+        "ss_match_features": (i32, [vp, vp, i32, vp, vp, i32, i32, vp, vp, vp, vp, P(i32)]),
         "ss_remove_outliers": (i32, [vp, vp, i32, i32, i32, f64, vp, vp]),
         "ss_fill_holes": (i32, [vp, vp, i32, i32, i32, i32, i32, vp, vp]),
         "ss_cleanup_pass": (i32, [P(SsParams), vp, vp, i32, i32, vp, vp]),

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstring>
 #include <memory>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -169,6 +170,9 @@ struct ss_ctx {
   DevBuf in_l, in_r, gray_l, gray_r, plane_l, plane_r, lstat, rstat, win, wbase;
   // opt-in left-right consistency (k_lr.cu)
   DevBuf gray_fl, gray_fr, disp_r, valid_r;
+  // feature front end scratch (k_features.cu)
+  DevBuf fe[20];
+  bool pattern_uploaded = false;
   bool lr_check = false;
   int lr_max_diff = 1;
   DevBuf disp_a, disp_b, valid_a, valid_b, flags, flag_count;
@@ -223,6 +227,7 @@ struct ss_ctx {
                       &trace_d, &so, &chg, &chg_count, &mbt, &defer, &defer_count, &gray_fl,
                       &gray_fr, &disp_r, &valid_r})
       b->release();
+    for (DevBuf& b : fe) b.release();
     for (Slot& sl : slots) {
       for (DevBuf* b : {&sl.in_l, &sl.in_r, &sl.disp_b, &sl.valid_a, &sl.index, &sl.npoints,
                         &sl.pts_f, &sl.colors, &sl.nrm_f})
@@ -807,6 +812,151 @@ ss_status ss_compute_disparity_lr(const ss_stereo_params* p, const uint8_t* left
       if (right_valid) d2h(right_valid, c->valid_b.p, N, c->stream);
     }
     sync(c);
+  });
+}
+
+// ---- feature front end (features.cpp:86-208) ----
+
+namespace {
+
+// The descriptor's sampling pattern (features.cpp:52-70): std::mt19937's
+// output is fixed by the standard, so the host draws the same 256 pairs.
+void ensure_pattern(ss_ctx* c) {
+  if (c->pattern_uploaded) return;
+  int pat[256 * 4];
+  std::mt19937 rng(0x51f0a3c9u);
+  for (int i = 0; i < 256 * 4; ++i) pat[i] = static_cast<int>(rng() % 27u) - 13;
+  upload_feature_pattern(pat, c->stream);
+  c->pattern_uploaded = true;
+}
+
+enum {
+  FE_GRAY, FE_SCORE, FE_KEYS, FE_KEYS2, FE_TMP, FE_COUNT, FE_CU, FE_CV, FE_CS, FE_KEEP,
+  FE_DTMP, FE_POS, FE_DESC, FE_N, FE_DA, FE_PA, FE_DB, FE_PB, FE_BEST, FE_OUT
+};
+
+}  // namespace
+
+ss_status ss_detect_corners(const uint8_t* gray, int32_t w, int32_t h, int32_t max_count,
+                            int32_t threshold, int32_t* us, int32_t* vs, int32_t* scores,
+                            int32_t* n) {
+  return guarded([&] {
+    if (threshold < 1) raise(SS_EINVAL, "detect_corners: threshold must be >= 1");
+    check_dims(w, h, "detect_corners");
+    *n = 0;
+    const long N = (long)w * h;
+    if (N == 0 || max_count <= 0) return;
+    ss_ctx* c = thread_ctx();
+    DevBuf* F = c->fe;
+    h2d(F[FE_GRAY], gray, N, c->stream);
+    F[FE_SCORE].ensure(sizeof(int) * N);
+    F[FE_KEYS].ensure(sizeof(unsigned long long) * N);
+    F[FE_KEYS2].ensure(sizeof(unsigned long long) * N);
+    F[FE_COUNT].ensure(sizeof(unsigned));
+    ck(cudaMemsetAsync(F[FE_COUNT].p, 0, sizeof(unsigned), c->stream), "memset");
+    launch_fast_score(F[FE_GRAY].as<uint8_t>(), F[FE_SCORE].as<int>(), w, h, threshold,
+                      c->stream);
+    launch_corner_keys(F[FE_SCORE].as<int>(), w, h, F[FE_KEYS].as<unsigned long long>(),
+                       F[FE_COUNT].as<unsigned>(), c->stream);
+    unsigned cnt = 0;
+    ck(cudaMemcpyAsync(&cnt, F[FE_COUNT].p, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream),
+       "D2H");
+    sync(c);
+    c->stats.kernel_launches += 2;
+    if (cnt == 0) return;
+    size_t tb = 0;
+    ck(sort_corner_keys(nullptr, &tb, nullptr, nullptr, (int)cnt, c->stream), "cub sort size");
+    F[FE_TMP].ensure(std::max<size_t>(tb, 16));
+    ck(sort_corner_keys(F[FE_TMP].p, &tb, F[FE_KEYS].as<unsigned long long>(),
+                        F[FE_KEYS2].as<unsigned long long>(), (int)cnt, c->stream),
+       "cub sort");
+    const int m = std::min<int>((int)cnt, max_count);
+    F[FE_CU].ensure(sizeof(int) * m);
+    F[FE_CV].ensure(sizeof(int) * m);
+    F[FE_CS].ensure(sizeof(int) * m);
+    launch_keys_to_corners(F[FE_KEYS2].as<unsigned long long>(), m, F[FE_CU].as<int>(),
+                           F[FE_CV].as<int>(), F[FE_CS].as<int>(), c->stream);
+    c->stats.kernel_launches += 2;
+    d2h(us, F[FE_CU].p, sizeof(int) * m, c->stream);
+    d2h(vs, F[FE_CV].p, sizeof(int) * m, c->stream);
+    d2h(scores, F[FE_CS].p, sizeof(int) * m, c->stream);
+    sync(c);
+    *n = m;
+  });
+}
+
+ss_status ss_describe(const uint8_t* gray, int32_t w, int32_t h, const int32_t* us,
+                      const int32_t* vs, const int32_t* scores, int32_t n_corners, double* pos,
+                      uint64_t* desc, int32_t* n) {
+  return guarded([&] {
+    (void)scores;  // the descriptor depends on positions only (features.cpp:150-166)
+    check_dims(w, h, "describe");
+    *n = 0;
+    const long N = (long)w * h;
+    if (N == 0 || n_corners <= 0) return;
+    ss_ctx* c = thread_ctx();
+    ensure_pattern(c);
+    DevBuf* F = c->fe;
+    h2d(F[FE_GRAY], gray, N, c->stream);
+    h2d(F[FE_CU], us, sizeof(int) * n_corners, c->stream);
+    h2d(F[FE_CV], vs, sizeof(int) * n_corners, c->stream);
+    F[FE_KEEP].ensure(sizeof(int) * n_corners);
+    F[FE_DTMP].ensure(sizeof(uint64_t) * 4 * n_corners);
+    F[FE_POS].ensure(sizeof(double) * 2 * n_corners);
+    F[FE_DESC].ensure(sizeof(uint64_t) * 4 * n_corners);
+    F[FE_N].ensure(sizeof(int));
+    launch_describe(F[FE_GRAY].as<uint8_t>(), w, h, F[FE_CU].as<int>(), F[FE_CV].as<int>(),
+                    n_corners, F[FE_DTMP].as<unsigned long long>(), F[FE_KEEP].as<int>(),
+                    F[FE_POS].as<double>(), F[FE_DESC].as<unsigned long long>(),
+                    F[FE_N].as<int>(), c->stream);
+    c->stats.kernel_launches += 2;
+    int m = 0;
+    ck(cudaMemcpyAsync(&m, F[FE_N].p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    sync(c);
+    d2h(pos, F[FE_POS].p, sizeof(double) * 2 * m, c->stream);
+    d2h(desc, F[FE_DESC].p, sizeof(uint64_t) * 4 * m, c->stream);
+    sync(c);
+    *n = m;
+  });
+}
+
+ss_status ss_match_features(const double* pos_a, const uint64_t* desc_a, int32_t na,
+                            const double* pos_b, const uint64_t* desc_b, int32_t nb,
+                            int32_t max_hamming, int32_t* index_a, int32_t* index_b,
+                            int32_t* hamming, double* displacement, int32_t* n) {
+  return guarded([&] {
+    *n = 0;
+    if (na <= 0 || nb <= 0) return;  // features.cpp:170
+    ss_ctx* c = thread_ctx();
+    DevBuf* F = c->fe;
+    h2d(F[FE_DA], desc_a, sizeof(uint64_t) * 4 * na, c->stream);
+    h2d(F[FE_PA], pos_a, sizeof(double) * 2 * na, c->stream);
+    h2d(F[FE_DB], desc_b, sizeof(uint64_t) * 4 * nb, c->stream);
+    h2d(F[FE_PB], pos_b, sizeof(double) * 2 * nb, c->stream);
+    const int mx = std::max(na, nb);
+    F[FE_BEST].ensure(sizeof(int) * 5 * mx);
+    F[FE_OUT].ensure(sizeof(int) * 3 * na + 8 + sizeof(double) * 2 * na + 8);
+    int* best = F[FE_BEST].as<int>();
+    char* o = static_cast<char*>(F[FE_OUT].p);
+    int* ia = reinterpret_cast<int*>(o);
+    int* ib = ia + na;
+    int* hm = ib + na;
+    double* dp = reinterpret_cast<double*>(o + ((sizeof(int) * 3 * na + 7) / 8) * 8);
+    int* nout = reinterpret_cast<int*>(dp + 2 * na);
+    launch_match(F[FE_DA].as<unsigned long long>(), F[FE_PA].as<double>(), na,
+                 F[FE_DB].as<unsigned long long>(), F[FE_PB].as<double>(), nb, max_hamming,
+                 best, best + mx, best + 2 * mx, best + 3 * mx, best + 4 * mx, ia, ib, hm, dp,
+                 nout, c->stream);
+    c->stats.kernel_launches += 4;
+    int m = 0;
+    ck(cudaMemcpyAsync(&m, nout, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    sync(c);
+    d2h(index_a, ia, sizeof(int) * m, c->stream);
+    d2h(index_b, ib, sizeof(int) * m, c->stream);
+    d2h(hamming, hm, sizeof(int) * m, c->stream);
+    d2h(displacement, dp, sizeof(double) * 2 * m, c->stream);
+    sync(c);
+    *n = m;
   });
 }
 

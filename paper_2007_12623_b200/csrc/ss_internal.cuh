@@ -111,6 +111,23 @@ void launch_lr_check(float* disp, uint8_t* valid, const float* disp_rm, const ui
 void launch_unflip_map(const float* dm, const uint8_t* vm, float* d, uint8_t* v, int W, int H,
                        int frames, long stride, cudaStream_t s);
 
+// Feature front end (k_features.cu; features.cpp:86-208).
+void upload_feature_pattern(const int* pat4x256, cudaStream_t s);
+void launch_fast_score(const uint8_t* g, int* score, int W, int H, int thr, cudaStream_t s);
+void launch_corner_keys(const int* score, int W, int H, unsigned long long* keys,
+                        unsigned* count, cudaStream_t s);
+cudaError_t sort_corner_keys(void* tmp, size_t* tmp_bytes, const unsigned long long* keys,
+                             unsigned long long* keys_out, int n, cudaStream_t s);
+void launch_keys_to_corners(const unsigned long long* keys, int n, int* cu, int* cv, int* cs,
+                            cudaStream_t s);
+void launch_describe(const uint8_t* g, int W, int H, const int* cu, const int* cv, int n,
+                     unsigned long long* desc_tmp, int* keep, double* pos,
+                     unsigned long long* desc, int* n_out, cudaStream_t s);
+void launch_match(const unsigned long long* da, const double* pa, int na,
+                  const unsigned long long* db, const double* pb, int nb, int max_hamming,
+                  int* best_b, int* best_b_d, int* best_a, int* best_a_d, int* keep, int* ia,
+                  int* ib, int* ham, double* disp, int* n_out, cudaStream_t s);
+
 // emap: scratch of edge_map_words(W, H) * frames words (smooth-edge bitmaps)
 inline long edge_map_words(int W, int H) {
   const long w32 = (W + 31) / 32 + 1, h32 = (H + 31) / 32 + 1;
