@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--streams", type=int, default=3,
                     help="concurrent contexts (one CUDA stream each) sharing the frames")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extensions", action="store_true",
+                    help="skip the LR-check / feature side measurements")
     ap.add_argument("--cpu-pairs", type=int, default=2)
     return ap.parse_args()
 
@@ -208,6 +210,72 @@ def run_reference(args):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def extensions(ss, ctxs, step_device, barrier, stream, F, Lh_first, Rh_first):
+    """Side measurements of the SURVEY §8f rows (not the headline metric):
+    the chain with the opt-in LR check (device pairs/s, same workload), and
+    the feature front end on one C1 frame pair through the per-stage C-ABI
+    (host buffers, transfers included) beside the reference's CPU code."""
+    import torch
+    out = {}
+    for c in ctxs:
+        c.set_lr_check(True, 1)
+    step_device()  # warm: the right-view buffers are allocated on first use
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for st in [torch.cuda.ExternalStream(c.stream) for c in ctxs][1:]:
+        st.wait_event(a)
+    step_device()
+    for c in ctxs[1:]:
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.ExternalStream(c.stream))
+        stream.wait_event(ev)
+    b.record(stream)
+    b.synchronize()
+    out["lr_check_chain"] = {"value": F / (a.elapsed_time(b) / 1000.0), "unit": "pairs/s",
+                             "note": "full chain + right-view sweep + LR check, 1 step"}
+    for c in ctxs:
+        c.set_lr_check(False)
+    barrier()
+    gl = ss.to_gray(Lh_first)
+    gr = ss.to_gray(Rh_first)
+
+    def feat_gpu():
+        fl = ss.features.describe(gl, ss.features.detect_corners(gl, 2000, 20))
+        fr = ss.features.describe(gr, ss.features.detect_corners(gr, 2000, 20))
+        return ss.features.match_features(*fl, *fr, 64)
+
+    def feat_cpu(ref):
+        cl = ref.detect_corners(gl, 2000, 20)
+        cr = ref.detect_corners(gr, 2000, 20)
+        fl, fr = ref.describe(gl, cl), ref.describe(gr, cr)
+        return ref.match_features(*fl, *fr, 64)
+
+    feat_gpu()
+    t = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        m = feat_gpu()
+        t.append(time.perf_counter() - t0)
+    out["features_pair"] = {"gpu_ms": 1000 * statistics.median(t), "matches": int(len(m["index_a"])),
+                            "what": "detect_corners(2000, thr 20) + describe on both C1 views + "
+                                    "match_features(64), per-stage C-ABI incl. H2D/D2H"}
+    try:
+        from oracle.oracle import Oracle
+        if Oracle.available("ref"):
+            ref = Oracle("ref")
+            t = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                feat_cpu(ref)
+                t.append(time.perf_counter() - t0)
+            out["features_pair"]["cpu_reference_ms"] = 1000 * statistics.median(t)
+            out["features_pair"]["cpu_cores"] = os.cpu_count()
+    except Exception as e:  # the CPU side is informational
+        out["features_pair"]["cpu_reference_error"] = str(e)[:200]
+    return out
 
 
 def run_ours(args):
@@ -383,6 +451,8 @@ def run_ours(args):
                "sample": f"{len(pairs_cpu)} C1 pairs (960x540 D=64) through oracle/_ref "
                          "(unmodified reference, OpenMP all cores) + restated cloud"}
     stage_ms_per_pair = {k: v[0] / frames_timed for k, v in stages.items()}
+    ext = None if (args.no_extensions or world > 1) else extensions(ss, ctxs, step_device, barrier, stream, F,
+                                                     Lh_first=Lh[0].numpy(), Rh_first=Rh[0].numpy())
     line = {
         "metric": "stereo pairs/sec at 960x540 D=64", "value": value, "unit": "pairs/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -399,6 +469,7 @@ def run_ours(args):
         "exact_resolves": {"wta_pixels": stats["wta_resolved"],
                            "refine_repicks": stats["refine_resolved"],
                            "frames": stats["frames"]},
+        "extensions": ext,
     }
     print(json.dumps(line), flush=True)
     for c in ctxs:

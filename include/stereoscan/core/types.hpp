@@ -1,7 +1,7 @@
 // Eigen-free core types of the B200 stereo path.
 // Mirrors /root/reference/proj/include/stereoscan/core/types.hpp:16-40
-// (Error, CameraIntrinsics, StereoRig). Vec3 replaces Eigen::Vector3d with a
-// POD exposing the x()/y()/z() accessors the stereo path uses; RigidPose and
+// (Error, CameraIntrinsics, StereoRig). Vec2 / Vec3 replace Eigen::Vector2d /
+// Vector3d with PODs exposing the accessors the stereo and feature paths use; RigidPose and
 // the rest of the SLAM types are out of scope.
 #pragma once
 
@@ -16,6 +16,16 @@ namespace stereoscan {
 class Error : public std::runtime_error {
  public:
   using std::runtime_error::runtime_error;
+};
+
+struct Vec2 {
+  double v[2] = {0.0, 0.0};
+  Vec2() = default;
+  Vec2(double x, double y) : v{x, y} {}
+  double x() const { return v[0]; }
+  double y() const { return v[1]; }
+  Vec2 operator-(const Vec2& o) const { return Vec2(v[0] - o.v[0], v[1] - o.v[1]); }
+  bool operator==(const Vec2& o) const { return v[0] == o.v[0] && v[1] == o.v[1]; }
 };
 
 struct Vec3 {

@@ -5,12 +5,17 @@
 // runs on the GPU. The scalar helpers zncc_chessboard / zncc_score /
 // match_pixel (matcher.cpp:38-100) are per-pixel API utilities, not part of
 // the frame path, and stay on the host with the reference's exact arithmetic.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <fstream>
+#include <map>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 
 #include "ss_stereo.h"
+#include "stereoscan/features/features.hpp"
 #include "stereoscan/stereo/cleanup.hpp"
 #include "stereoscan/stereo/cloud.hpp"
 #include "stereoscan/stereo/matcher.hpp"
@@ -260,3 +265,129 @@ StereoCloud disparity_to_cloud(const DisparityMap& map, const ColorImage& color,
 }
 
 }  // namespace stereoscan
+
+// ---------------- feature front end (features.hpp) ----------------
+
+namespace stereoscan::features {
+
+int Descriptor256::hamming(const Descriptor256& other) const {
+  int d = 0;
+  for (size_t k = 0; k < bits.size(); ++k) d += __builtin_popcountll(bits[k] ^ other.bits[k]);
+  return d;
+}
+
+std::vector<Corner> detect_corners(const GrayImage& img, int max_count, int threshold) {
+  const int cap = std::max(max_count, 0);
+  std::vector<int32_t> u(std::max(cap, 1)), v(std::max(cap, 1)), s(std::max(cap, 1));
+  int32_t n = 0;
+  throw_on(ss_detect_corners(img.pixels.data(), img.width, img.height, max_count, threshold,
+                             u.data(), v.data(), s.data(), &n));
+  std::vector<Corner> out(n);
+  for (int i = 0; i < n; ++i) out[i] = {u[i], v[i], s[i]};
+  return out;
+}
+
+std::vector<Feature> describe(const GrayImage& img, const std::vector<Corner>& corners) {
+  const int nc = static_cast<int>(corners.size());
+  std::vector<int32_t> u(nc), v(nc), s(nc);
+  for (int i = 0; i < nc; ++i) {
+    u[i] = corners[i].u;
+    v[i] = corners[i].v;
+    s[i] = corners[i].score;
+  }
+  std::vector<double> pos(2 * std::max(nc, 1));
+  std::vector<uint64_t> desc(4 * std::max(nc, 1));
+  int32_t n = 0;
+  throw_on(ss_describe(img.pixels.data(), img.width, img.height, u.data(), v.data(), s.data(),
+                       nc, pos.data(), desc.data(), &n));
+  std::vector<Feature> out(n);
+  for (int i = 0; i < n; ++i) {
+    out[i].position = Vec2(pos[2 * i], pos[2 * i + 1]);
+    for (int k = 0; k < 4; ++k) out[i].descriptor.bits[k] = desc[4 * i + k];
+  }
+  return out;
+}
+
+MatchSet match_features(const std::vector<Feature>& a, const std::vector<Feature>& b,
+                        int max_hamming) {
+  const int na = static_cast<int>(a.size()), nb = static_cast<int>(b.size());
+  auto pack = [](const std::vector<Feature>& f, std::vector<double>& p,
+                 std::vector<uint64_t>& d) {
+    p.resize(2 * std::max<size_t>(f.size(), 1));
+    d.resize(4 * std::max<size_t>(f.size(), 1));
+    for (size_t i = 0; i < f.size(); ++i) {
+      p[2 * i] = f[i].position.x();
+      p[2 * i + 1] = f[i].position.y();
+      for (int k = 0; k < 4; ++k) d[4 * i + k] = f[i].descriptor.bits[k];
+    }
+  };
+  std::vector<double> pa, pb;
+  std::vector<uint64_t> da, db;
+  pack(a, pa, da);
+  pack(b, pb, db);
+  const int cap = std::max(std::min(na, nb), 1);
+  std::vector<int32_t> ia(cap), ib(cap), hm(cap);
+  std::vector<double> dp(2 * cap);
+  int32_t n = 0;
+  throw_on(ss_match_features(pa.data(), da.data(), na, pb.data(), db.data(), nb, max_hamming,
+                             ia.data(), ib.data(), hm.data(), dp.data(), &n));
+  MatchSet out(n);
+  for (int i = 0; i < n; ++i) {
+    out[i].index_a = ia[i];
+    out[i].index_b = ib[i];
+    out[i].hamming = hm[i];
+    out[i].weight = 1.0;
+    out[i].displacement = Vec2(dp[2 * i], dp[2 * i + 1]);
+  }
+  return out;
+}
+
+MatchSet histogram_vote(const MatchSet& matches, double bin_size) {
+  if (!(bin_size > 0.0)) throw std::invalid_argument("histogram_vote: bin_size must be > 0");
+  const size_t n = matches.size();
+  // bin of each displacement (floor(x / bin)), counts per occupied bin
+  std::vector<std::pair<int64_t, int64_t>> bin(n);
+  std::map<std::pair<int64_t, int64_t>, int> count;
+  for (size_t i = 0; i < n; ++i) {
+    bin[i] = {static_cast<int64_t>(std::floor(matches[i].displacement.x() / bin_size)),
+              static_cast<int64_t>(std::floor(matches[i].displacement.y() / bin_size))};
+    ++count[bin[i]];
+  }
+  std::vector<int> prio(n, 0);
+  for (size_t i = 0; i < n; ++i)
+    for (int64_t dy = -1; dy <= 1; ++dy)
+      for (int64_t dx = -1; dx <= 1; ++dx) {
+        const auto it = count.find({bin[i].first + dx, bin[i].second + dy});
+        if (it != count.end()) prio[i] += it->second;
+      }
+  std::vector<int> order(n);
+  for (size_t i = 0; i < n; ++i) order[i] = static_cast<int>(i);
+  std::stable_sort(order.begin(), order.end(), [&](int l, int r) {
+    return prio[l] != prio[r] ? prio[l] > prio[r] : matches[l].hamming < matches[r].hamming;
+  });
+  MatchSet out;
+  out.reserve(n);
+  for (size_t r = 0; r < n; ++r) {
+    out.push_back(matches[order[r]]);
+    out.back().rank = static_cast<int>(r);
+  }
+  return out;
+}
+
+std::vector<std::pair<Vec2, Vec2>> read_match_file(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw Error("cannot open match file: " + path);
+  std::vector<std::pair<Vec2, Vec2>> out;
+  std::string line;
+  for (int no = 1; std::getline(in, line); ++no) {
+    if (line.empty() || line[0] == '#') continue;
+    std::istringstream fields(line);
+    double a, b, c, d;
+    if (!(fields >> a >> b >> c >> d))
+      throw Error(path + ":" + std::to_string(no) + ": expected 'u1 v1 u2 v2'");
+    out.push_back({Vec2(a, b), Vec2(c, d)});
+  }
+  return out;
+}
+
+}  // namespace stereoscan::features

@@ -14,4 +14,4 @@ except Exception as e:
     print("bench parse failed", e); print(open(f"gpurun_out/bench_{t}.err").read()[-2000:])
 PY
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
-    python bench.py --frames 16 --batch 16 --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1; echo "ncu rc=$?"
+    python bench.py --frames 16 --batch 16 --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 0 --streams 1 --no-extensions > /dev/null 2>&1; echo "ncu rc=$?"

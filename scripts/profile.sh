@@ -7,7 +7,7 @@ set -u
 TAG=${1:-r1}
 OUT=gpurun_out
 mkdir -p "$OUT"
-BENCH="python bench.py --frames 16 --batch 16 --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 0"
+BENCH="python bench.py --frames 16 --batch 16 --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 0 --streams 1 --no-extensions"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file "$OUT/launches_${TAG}.csv" $BENCH > "$OUT/launches_${TAG}.log" 2>&1
 echo "launch list rc=$?"

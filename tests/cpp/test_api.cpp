@@ -8,6 +8,7 @@
 #include <random>
 #include <stdexcept>
 
+#include "stereoscan/features/features.hpp"
 #include "stereoscan/stereo/cleanup.hpp"
 #include "stereoscan/stereo/cloud.hpp"
 #include "stereoscan/stereo/matcher.hpp"
@@ -153,6 +154,37 @@ int main() {
     CHECK(false);
   } catch (const Error& e) {
     CHECK(std::string(e.what()) == "rig: baseline_mm must be > 0");
+  }
+
+  // ---- feature front end (features.hpp) ----
+  {
+    namespace fe = stereoscan::features;
+    GrayImage sq(64, 64, 0);
+    for (int v = 20; v < 44; ++v)
+      for (int u = 20; u < 44; ++u) sq.at(u, v) = 255;
+    const auto cs = fe::detect_corners(sq, 100, 30);
+    CHECK(cs.size() == 4 && cs[0].score == 255 && cs[0].u == 20 && cs[0].v == 20);
+    try {
+      fe::detect_corners(sq, 10, 0);
+      CHECK(false);
+    } catch (const std::invalid_argument& e) {
+      CHECK(std::string(e.what()) == "detect_corners: threshold must be >= 1");
+    }
+    // self-matching a textured frame: every feature matches itself at distance 0
+    const auto corners = fe::detect_corners(left, 200, 10);
+    const auto feats = fe::describe(left, corners);
+    CHECK(!feats.empty() && feats.size() <= corners.size());
+    const auto ms = fe::match_features(feats, feats, 0);
+    CHECK(ms.size() >= feats.size() / 2);
+    for (const auto& m : ms) CHECK(m.hamming == 0 && m.displacement.x() == 0.0);
+    const auto ranked = fe::histogram_vote(ms, 4.0);
+    CHECK(ranked.size() == ms.size());
+    for (size_t r = 0; r < ranked.size(); ++r) CHECK(ranked[r].rank == static_cast<int>(r));
+    try {
+      fe::read_match_file("/nonexistent/matches.txt");
+      CHECK(false);
+    } catch (const stereoscan::Error&) {
+    }
   }
 
   if (failures) {
