@@ -19,6 +19,7 @@
  *   ss_detect_corners       replaces features::detect_corners  features.hpp:52, features.cpp:86-124
  *   ss_describe             replaces features::describe        features.hpp:57, features.cpp:126-166
  *   ss_match_features       replaces features::match_features  features.hpp:61, features.cpp:168-208
+ *   ss_fusion_*             the SPEC's fusion module (no reference source)
  *
  * Throughput entry (no reference analogue): ss_ctx_* run the
  * whole run_stereo_only chain for a batch of frames on one
@@ -161,6 +162,57 @@ ss_status ss_match_features(const double* pos_a, const uint64_t* desc_a, int32_t
                             const double* pos_b, const uint64_t* desc_b, int32_t nb,
                             int32_t max_hamming, int32_t* index_a, int32_t* index_b,
                             int32_t* hamming, double* displacement, int32_t* n);
+
+/* ---- fusion consumer (SPEC.md:440-476 [MODULE] fusion) ----
+ * The surfel model lives on the GPU; keyframe clouds are fused where they
+ * were produced. The reference has no source for this module: the rules are
+ * the SPEC's (DESIGN.md §12 lists the conventions), with the SPEC's defaults.
+ *   pose[12]: row-major [R | t] mapping world to camera (X_cam = R X_world + t).
+ *   rasterize: surfels with X_cam.z > 0 project to pixel (floor(fx x/z + cx +
+ *     0.5), floor(fy y/z + cy + 0.5)); the smallest depth wins, then the smaller
+ *     surfel id; ids -1 / depth 0 where empty.
+ *   fuse: every pixel with a point (raster order) associates with the raster's
+ *     surfel when |z - z_surfel| <= gate: increment clamped to trunc_mm, weight
+ *     average (new observation weight 1), weight <- min(weight + 1, cap), normal
+ *     re-normalised, colour averaged with omega(u,v) = clamp(1 - r/R, omega_min,
+ *     1) (r: distance to the image centre, R: half-diagonal); other pixels are
+ *     appended as new surfels (weight 1) in raster order. */
+typedef struct ss_fusion_params {
+  double trunc_mm;            /* 10 */
+  double weight_cap;          /* 50 */
+  double association_gate_mm; /* 5 */
+  double omega_min;           /* 0.1 */
+} ss_fusion_params;
+
+typedef struct ss_fusion ss_fusion;
+
+void ss_fusion_params_default(ss_fusion_params* p);
+ss_status ss_fusion_create(int32_t device, const ss_fusion_params* p, ss_fusion** out);
+ss_status ss_fusion_destroy(ss_fusion* f);
+ss_status ss_fusion_size(ss_fusion* f, int32_t* n);
+/* Replace / read the model: pos, normal, colour (3 doubles each), weight,
+ * colour weight per surfel (NULL outputs are skipped). */
+ss_status ss_fusion_upload(ss_fusion* f, int32_t n, const double* pos, const double* normal,
+                           const double* color, const double* weight,
+                           const double* color_weight);
+ss_status ss_fusion_download(ss_fusion* f, double* pos, double* normal, double* color,
+                             double* weight, double* color_weight);
+/* rasterize: ids / depth of rig->width * rig->height pixels. */
+ss_status ss_fusion_rasterize(ss_fusion* f, const double* pose, const ss_stereo_rig* rig,
+                              int32_t* ids, double* depth);
+/* fuse_frame from host arrays: a StereoCloud (index per
+ * pixel, points / normals as doubles in the camera frame, colours). */
+ss_status ss_fusion_fuse_frame(ss_fusion* f, const int32_t* index, int32_t n_points,
+                               const double* points, const double* normals,
+                               const uint8_t* colors, int32_t w, int32_t h, const double* pose,
+                               const ss_stereo_rig* rig);
+/* Same from DEVICE arrays of one frame as the batch API leaves them
+ * (ss_ctx_device_outputs / ss_stereo_batch_device: index, float points and
+ * normals, colours); `stream` (nullable) is the producer stream to wait on. */
+ss_status ss_fusion_fuse_device(ss_fusion* f, const int32_t* d_index, const float* d_points,
+                                const float* d_normals, const uint8_t* d_colors, int32_t w,
+                                int32_t h, const double* pose, const ss_stereo_rig* rig,
+                                void* stream);
 
 /* ---- throughput API: a batch of frames through the whole chain on one GPU ---- */
 

@@ -244,6 +244,45 @@ class Oracle:
                                                 _p(order, _I32)))
         return order[:len(ia)].copy()
 
+    # --- fusion consumer (restatement only: SPEC.md:440-476, no reference source) ---
+    def rasterize(self, pos, pose, rig):
+        pos = np.ascontiguousarray(pos, np.float64).reshape(-1, 3)
+        P = np.ascontiguousarray(np.asarray(pose, np.float64)[:3, :4]).reshape(12)
+        w, h = int(rig["width"]), int(rig["height"])
+        ids = np.zeros((h, w), np.int32)
+        dep = np.zeros((h, w), np.float64)
+        self._check(self.lib.orc_rasterize(_p(pos, _F64), len(pos), _p(P, _F64),
+                                           C.c_double(rig["fx"]), C.c_double(rig["fy"]),
+                                           C.c_double(rig["cx"]), C.c_double(rig["cy"]), w, h,
+                                           _p(ids, _I32), _p(dep, _F64)))
+        return ids, dep
+
+    def fuse_frame(self, model, index, points, normals, colors, pose, rig, trunc=10.0, cap=50.0,
+                   gate=5.0, omega_min=0.1):
+        """model: dict pos/normal/color (n x 3), weight/color_weight (n); returns the new one."""
+        n0 = len(model["weight"])
+        index = np.ascontiguousarray(index, np.int32)
+        pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        capn = n0 + int((index >= 0).sum()) + 1
+        arr = {}
+        for k, per in (("pos", 3), ("normal", 3), ("color", 3), ("weight", 1), ("color_weight", 1)):
+            a = np.zeros((capn, per) if per == 3 else capn, np.float64)
+            a[:n0] = model[k]
+            arr[k] = a
+        n = _I32(n0)
+        P = np.ascontiguousarray(np.asarray(pose, np.float64)[:3, :4]).reshape(12)
+        nrm = np.ascontiguousarray(normals, np.float64).reshape(-1, 3)
+        col = np.ascontiguousarray(colors, np.uint8).reshape(-1, 3)
+        w, h = int(rig["width"]), int(rig["height"])
+        self._check(self.lib.orc_fuse_frame(
+            _p(arr["pos"], _F64), _p(arr["normal"], _F64), _p(arr["color"], _F64),
+            _p(arr["weight"], _F64), _p(arr["color_weight"], _F64), C.byref(n), capn,
+            _p(index, _I32), _p(pts, _F64), _p(nrm, _F64), _p(col, _U8), w, h, _p(P, _F64),
+            C.c_double(rig["fx"]), C.c_double(rig["fy"]), C.c_double(rig["cx"]),
+            C.c_double(rig["cy"]), C.c_double(trunc), C.c_double(cap), C.c_double(gate),
+            C.c_double(omega_min)))
+        return {k: v[:n.value] for k, v in arr.items()}
+
     def remove_outliers(self, disp, valid, radius, threshold, naive=False):
         disp = np.ascontiguousarray(disp, np.float32)
         valid = np.ascontiguousarray(valid, np.uint8)

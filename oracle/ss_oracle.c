@@ -655,3 +655,129 @@ int orc_disparity_to_cloud(const float* disp, const uint8_t* valid, int32_t w, i
   }
   return 0;
 }
+
+/* ---- Fusion consumer (SPEC.md:440-476 [MODULE]
+ * fusion). No reference source exists (SPEC only): this is the restatement
+ * the GPU fusion is held to, with the SPEC's examples and properties as KATs
+ * ("parity unpinned" against reference code). Conventions (also
+ * include/ss_stereo.h):
+ *   pose[12]  row-major [R | t], world -> camera: X_cam = R X_world + t
+ *   surfels   SoA, pos/normal/color/weight/color_weight in double
+ *   rasterize: X_cam.z > 0; pixel = (floor(fx x/z + cx + 0.5),
+ *              floor(fy y/z + cy + 0.5)); smallest depth wins, then the
+ *              smaller surfel id
+ *   fuse     : per stereo pixel with a point (raster order), associate with
+ *              the raster's surfel when |z - z_s| <= gate, else append. */
+static void orc_apply(const double* P, const double x[3], double y[3]) {
+  for (int r = 0; r < 3; ++r)
+    y[r] = ((P[4 * r] * x[0] + P[4 * r + 1] * x[1]) + P[4 * r + 2] * x[2]) + P[4 * r + 3];
+}
+static void orc_apply_inv(const double* P, const double y[3], double x[3]) {
+  const double d0 = y[0] - P[3], d1 = y[1] - P[7], d2 = y[2] - P[11];
+  for (int c = 0; c < 3; ++c) x[c] = (P[c] * d0 + P[4 + c] * d1) + P[8 + c] * d2;
+}
+static void orc_rot_inv(const double* P, const double y[3], double x[3]) {
+  for (int c = 0; c < 3; ++c) x[c] = (P[c] * y[0] + P[4 + c] * y[1]) + P[8 + c] * y[2];
+}
+
+int orc_rasterize(const double* pos, int32_t n, const double* pose, double fx, double fy,
+                  double cx, double cy, int32_t w, int32_t h, int32_t* ids, double* depth) {
+  for (long i = 0; i < (long)w * h; ++i) {
+    ids[i] = -1;
+    depth[i] = 0.0;
+  }
+  for (int32_t s = 0; s < n; ++s) {
+    double q[3];
+    orc_apply(pose, pos + 3L * s, q);
+    if (!(q[2] > 0.0)) continue;
+    const double u = (fx * q[0]) / q[2] + cx, v = (fy * q[1]) / q[2] + cy;
+    const double fu = floor(u + 0.5), fv = floor(v + 0.5);
+    if (!(fu >= 0.0 && fu < (double)w && fv >= 0.0 && fv < (double)h)) continue;
+    const long k = (long)fv * w + (long)fu;
+    if (ids[k] < 0 || q[2] < depth[k] || (q[2] == depth[k] && s < ids[k])) {
+      ids[k] = s;
+      depth[k] = q[2];
+    }
+  }
+  return 0;
+}
+
+/* Colour weight of pixel (u, v): clamp(1 - r / R, omega_min, 1), r the
+ * distance to the image centre ((w-1)/2, (h-1)/2), R the half-diagonal. */
+static double orc_omega(int u, int v, int w, int h, double omega_min) {
+  const double cu = 0.5 * (double)(w - 1), cv = 0.5 * (double)(h - 1);
+  const double du = (double)u - cu, dv = (double)v - cv;
+  const double r = sqrt(du * du + dv * dv), R = sqrt(cu * cu + cv * cv);
+  double o = R > 0.0 ? 1.0 - r / R : 1.0;
+  if (o < omega_min) o = omega_min;
+  if (o > 1.0) o = 1.0;
+  return o;
+}
+
+/* One frame into the model (arrays of capacity cap; *n in/out). */
+int orc_fuse_frame(double* pos, double* nrm, double* col, double* wgt, double* cwgt, int32_t* n,
+                   int32_t cap, const int32_t* index, const double* pts, const double* nrms,
+                   const uint8_t* colors, int32_t w, int32_t h, const double* pose, double fx,
+                   double fy, double cx, double cy, double trunc, double weight_cap,
+                   double gate, double omega_min) {
+  const long N = (long)w * h;
+  int32_t* ids = (int32_t*)malloc(sizeof(int32_t) * (N > 0 ? N : 1));
+  double* dep = (double*)malloc(sizeof(double) * (N > 0 ? N : 1));
+  orc_rasterize(pos, *n, pose, fx, fy, cx, cy, w, h, ids, dep);
+  int32_t m = *n;
+  for (int v = 0; v < h; ++v)
+    for (int u = 0; u < w; ++u) {
+      const long k = (long)v * w + u;
+      const int32_t p = index[k];
+      if (p < 0) continue;
+      double xw[3], nw[3];
+      orc_apply_inv(pose, pts + 3L * p, xw);
+      orc_rot_inv(pose, nrms + 3L * p, nw);
+      const double om = orc_omega(u, v, w, h, omega_min);
+      const double c[3] = {(double)colors[3L * p], (double)colors[3L * p + 1],
+                           (double)colors[3L * p + 2]};
+      const int32_t s = ids[k];
+      if (s >= 0 && fabs(pts[3L * p + 2] - dep[k]) <= gate) {
+        double* P = pos + 3L * s;
+        double d[3] = {xw[0] - P[0], xw[1] - P[1], xw[2] - P[2]};
+        const double len = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+        if (len > trunc) {
+          const double f = trunc / len;
+          d[0] *= f;
+          d[1] *= f;
+          d[2] *= f;
+        }
+        const double wo = wgt[s], inv = 1.0 / (wo + 1.0);
+        for (int i = 0; i < 3; ++i) P[i] = P[i] + d[i] * inv;
+        double* Nn = nrm + 3L * s;
+        double a[3];
+        for (int i = 0; i < 3; ++i) a[i] = wo * Nn[i] + nw[i];
+        const double al = sqrt((a[0] * a[0] + a[1] * a[1]) + a[2] * a[2]);
+        if (al > 0.0)
+          for (int i = 0; i < 3; ++i) Nn[i] = a[i] / al;
+        double* C = col + 3L * s;
+        const double cw = cwgt[s], cs = cw + om;
+        for (int i = 0; i < 3; ++i) C[i] = (cw * C[i] + om * c[i]) / cs;
+        wgt[s] = wo + 1.0 < weight_cap ? wo + 1.0 : weight_cap;
+        cwgt[s] = cs < weight_cap ? cs : weight_cap;
+      } else {
+        if (m >= cap) {
+          free(ids);
+          free(dep);
+          return fail(2, "fuse_frame: surfel capacity exceeded");
+        }
+        for (int i = 0; i < 3; ++i) {
+          pos[3L * m + i] = xw[i];
+          nrm[3L * m + i] = nw[i];
+          col[3L * m + i] = c[i];
+        }
+        wgt[m] = 1.0;
+        cwgt[m] = om;
+        ++m;
+      }
+    }
+  *n = m;
+  free(ids);
+  free(dep);
+  return 0;
+}

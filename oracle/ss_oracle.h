@@ -123,6 +123,15 @@ int orc_compute_disparity_right(const orc_params* p, const uint8_t* left,
 int orc_lr_check(const float* disp, const uint8_t* valid, const float* disp_r,
                  const uint8_t* valid_r, int32_t w, int32_t h, int32_t max_diff,
                  float* out_disp, uint8_t* out_valid);
+/* Restatement-only: the fusion consumer (no reference
+ * source; conventions in ss_oracle.c). */
+int orc_rasterize(const double* pos, int32_t n, const double* pose, double fx, double fy,
+                  double cx, double cy, int32_t w, int32_t h, int32_t* ids, double* depth);
+int orc_fuse_frame(double* pos, double* nrm, double* col, double* wgt, double* cwgt, int32_t* n,
+                   int32_t cap, const int32_t* index, const double* pts, const double* nrms,
+                   const uint8_t* colors, int32_t w, int32_t h, const double* pose, double fx,
+                   double fy, double cx, double cy, double trunc, double weight_cap,
+                   double gate, double omega_min);
 int orc_params_validate(const orc_params* p);
 int orc_rig_validate(const orc_rig* rig);
 

@@ -26,5 +26,5 @@ from .stereo import (  # noqa: F401
     remove_outliers,
     to_gray,
 )
-from . import features  # noqa: F401
+from . import features, fusion  # noqa: F401
 from ._lib import SS_IN_GRAY, SS_IN_RGB, SS_OUT_CLOUD, SS_OUT_DISPARITY, SS_OUT_NORMALS  # noqa: F401

@@ -34,6 +34,11 @@ class SsRig(C.Structure):
                 ("width", C.c_int32), ("height", C.c_int32), ("baseline_mm", C.c_double)]
 
 
+class SsFusionParams(C.Structure):
+    _fields_ = [("trunc_mm", C.c_double), ("weight_cap", C.c_double),
+                ("association_gate_mm", C.c_double), ("omega_min", C.c_double)]
+
+
 class SsBatchOut(C.Structure):
     _fields_ = [("disparity", C.c_void_p), ("valid", C.c_void_p), ("index", C.c_void_p),
                 ("points", C.c_void_p), ("normals", C.c_void_p), ("colors", C.c_void_p),
@@ -76,6 +81,15 @@ def lib():
         "ss_detect_corners": (i32, [vp, i32, i32, i32, i32, vp, vp, vp, P(i32)]),
         "ss_describe": (i32, [vp, i32, i32, vp, vp, vp, i32, vp, vp, P(i32)]),
         "ss_match_features": (i32, [vp, vp, i32, vp, vp, i32, i32, vp, vp, vp, vp, P(i32)]),
+        "ss_fusion_params_default": (None, [P(SsFusionParams)]),
+        "ss_fusion_create": (i32, [i32, P(SsFusionParams), P(vp)]),
+        "ss_fusion_destroy": (i32, [vp]),
+        "ss_fusion_size": (i32, [vp, P(i32)]),
+        "ss_fusion_upload": (i32, [vp, i32, vp, vp, vp, vp, vp]),
+        "ss_fusion_download": (i32, [vp, vp, vp, vp, vp, vp]),
+        "ss_fusion_rasterize": (i32, [vp, vp, P(SsRig), vp, vp]),
+        "ss_fusion_fuse_frame": (i32, [vp, vp, i32, vp, vp, vp, i32, i32, vp, P(SsRig)]),
+        "ss_fusion_fuse_device": (i32, [vp, vp, vp, vp, vp, i32, i32, vp, P(SsRig), vp]),
         "ss_remove_outliers": (i32, [vp, vp, i32, i32, i32, f64, vp, vp]),
         "ss_fill_holes": (i32, [vp, vp, i32, i32, i32, i32, i32, vp, vp]),
         "ss_cleanup_pass": (i32, [P(SsParams), vp, vp, i32, i32, vp, vp]),

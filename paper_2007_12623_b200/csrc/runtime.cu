@@ -960,6 +960,219 @@ ss_status ss_match_features(const double* pos_a, const uint64_t* desc_a, int32_t
   });
 }
 
+// ---- fusion consumer ----
+
+}  // extern "C"
+
+struct ss_fusion {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  ss_fusion_params prm{};
+  int32_t n = 0, cap = 0;
+  DevBuf pos, nrm, col, w, cw;               // surfel model (SoA, FP64)
+  DevBuf zbits, ids, is_new, block_new, total, st_index, st_pd, st_nd, st_col, r_ids, r_depth;
+
+  ~ss_fusion() {
+    for (DevBuf* b : {&pos, &nrm, &col, &w, &cw, &zbits, &ids, &is_new, &block_new, &total,
+                      &st_index, &st_pd, &st_nd, &st_col, &r_ids, &r_depth})
+      b->release();
+    if (stream) cudaStreamDestroy(stream);
+  }
+  void activate() { ck(cudaSetDevice(device), "cudaSetDevice"); }
+  // capacity for `need` surfels, keeping the first n
+  void reserve(int64_t need) {
+    if (need <= cap) return;
+    const int64_t nc = std::max<int64_t>(need, std::max<int64_t>(2 * (int64_t)cap, 4096));
+    if (nc > INT32_MAX) raise(SS_EINVAL, "fusion: surfel count exceeds int32");
+    const std::pair<DevBuf*, int> fields[5] = {{&pos, 3}, {&nrm, 3}, {&col, 3}, {&w, 1}, {&cw, 1}};
+    for (auto [b, per] : fields) {
+      DevBuf nb;
+      nb.ensure(sizeof(double) * per * nc);
+      if (n > 0)
+        ck(cudaMemcpyAsync(nb.p, b->p, sizeof(double) * per * n, cudaMemcpyDeviceToDevice, stream),
+           "copy");
+      ck(cudaStreamSynchronize(stream), "sync");
+      b->release();
+      *b = nb;
+      nb.p = nullptr;
+    }
+    cap = (int32_t)nc;
+  }
+  void raster(const double* pose, const ss_stereo_rig* rig) {
+    const long npx = (long)rig->width * rig->height;
+    zbits.ensure(sizeof(unsigned long long) * npx);
+    ids.ensure(sizeof(int) * npx);
+    launch_rasterize(pos.as<double>(), n, pose, rig->fx, rig->fy, rig->cx, rig->cy, rig->width,
+                     rig->height, zbits.as<unsigned long long>(), ids.as<int>(), stream);
+  }
+  // fuse one frame's cloud (device pointers; pd/nd double or pf/nf float)
+  void fuse(const int* index, const double* pd, const double* nd, const float* pf,
+            const float* nf, const uint8_t* colors, int64_t max_new, const double* pose,
+            const ss_stereo_rig* rig) {
+    const long npx = (long)rig->width * rig->height;
+    reserve((int64_t)n + max_new);
+    raster(pose, rig);
+    is_new.ensure(npx);
+    block_new.ensure(sizeof(int) * ((npx + 255) / 256 + 1));
+    total.ensure(sizeof(int));
+    launch_fuse(pos.as<double>(), nrm.as<double>(), col.as<double>(), w.as<double>(),
+                cw.as<double>(), index, pd, nd, pf, nf, colors, pose, rig->fx, rig->fy, rig->cx,
+                rig->cy, rig->width, rig->height, zbits.as<unsigned long long>(), ids.as<int>(),
+                prm.trunc_mm, prm.weight_cap, prm.association_gate_mm, prm.omega_min,
+                is_new.as<uint8_t>(), block_new.as<int>(), total.as<int>(), n, stream);
+    int added = 0;
+    ck(cudaMemcpyAsync(&added, total.p, sizeof(int), cudaMemcpyDeviceToHost, stream), "D2H");
+    ck(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    n += added;
+  }
+};
+
+namespace {
+void check_rig_for_fusion(const ss_stereo_rig* rig) {
+  if (!rig) raise(SS_EINVAL, "fusion: null rig");
+  validate_rig(rig);
+}
+void check_pose(const double* pose) {
+  if (!pose) raise(SS_EINVAL, "fusion: null pose");
+}
+}  // namespace
+
+extern "C" {
+
+void ss_fusion_params_default(ss_fusion_params* p) {
+  p->trunc_mm = 10.0;
+  p->weight_cap = 50.0;
+  p->association_gate_mm = 5.0;
+  p->omega_min = 0.1;
+}
+
+ss_status ss_fusion_create(int32_t device, const ss_fusion_params* p, ss_fusion** out) {
+  return guarded([&] {
+    require_device();
+    if (!out) raise(SS_EINVAL, "ss_fusion_create: null out");
+    auto f = std::make_unique<ss_fusion>();
+    f->device = device;
+    f->activate();
+    if (p) f->prm = *p;
+    else ss_fusion_params_default(&f->prm);
+    if (!(f->prm.trunc_mm > 0.0) || !(f->prm.weight_cap >= 1.0) ||
+        !(f->prm.association_gate_mm >= 0.0) || !(f->prm.omega_min >= 0.0 && f->prm.omega_min <= 1.0))
+      raise(SS_EPARAM, "fusion: parameters out of range");
+    ck(cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    *out = f.release();
+  });
+}
+
+ss_status ss_fusion_destroy(ss_fusion* f) {
+  return guarded([&] {
+    if (f) {
+      f->activate();
+      delete f;
+    }
+  });
+}
+
+ss_status ss_fusion_size(ss_fusion* f, int32_t* n) {
+  return guarded([&] { *n = f->n; });
+}
+
+ss_status ss_fusion_upload(ss_fusion* f, int32_t n, const double* pos, const double* nrm,
+                           const double* col, const double* w, const double* cw) {
+  return guarded([&] {
+    f->activate();
+    if (n < 0) raise(SS_EINVAL, "ss_fusion_upload: negative count");
+    f->n = 0;
+    f->reserve(n);
+    const size_t s3 = sizeof(double) * 3 * n, s1 = sizeof(double) * n;
+    if (n) {
+      ck(cudaMemcpyAsync(f->pos.p, pos, s3, cudaMemcpyHostToDevice, f->stream), "H2D");
+      ck(cudaMemcpyAsync(f->nrm.p, nrm, s3, cudaMemcpyHostToDevice, f->stream), "H2D");
+      ck(cudaMemcpyAsync(f->col.p, col, s3, cudaMemcpyHostToDevice, f->stream), "H2D");
+      ck(cudaMemcpyAsync(f->w.p, w, s1, cudaMemcpyHostToDevice, f->stream), "H2D");
+      ck(cudaMemcpyAsync(f->cw.p, cw, s1, cudaMemcpyHostToDevice, f->stream), "H2D");
+    }
+    ck(cudaStreamSynchronize(f->stream), "sync");
+    f->n = n;
+  });
+}
+
+ss_status ss_fusion_download(ss_fusion* f, double* pos, double* nrm, double* col, double* w,
+                             double* cw) {
+  return guarded([&] {
+    f->activate();
+    const int n = f->n;
+    const size_t s3 = sizeof(double) * 3 * n, s1 = sizeof(double) * n;
+    if (n) {
+      if (pos) ck(cudaMemcpyAsync(pos, f->pos.p, s3, cudaMemcpyDeviceToHost, f->stream), "D2H");
+      if (nrm) ck(cudaMemcpyAsync(nrm, f->nrm.p, s3, cudaMemcpyDeviceToHost, f->stream), "D2H");
+      if (col) ck(cudaMemcpyAsync(col, f->col.p, s3, cudaMemcpyDeviceToHost, f->stream), "D2H");
+      if (w) ck(cudaMemcpyAsync(w, f->w.p, s1, cudaMemcpyDeviceToHost, f->stream), "D2H");
+      if (cw) ck(cudaMemcpyAsync(cw, f->cw.p, s1, cudaMemcpyDeviceToHost, f->stream), "D2H");
+    }
+    ck(cudaStreamSynchronize(f->stream), "sync");
+  });
+}
+
+ss_status ss_fusion_rasterize(ss_fusion* f, const double* pose, const ss_stereo_rig* rig,
+                              int32_t* ids, double* depth) {
+  return guarded([&] {
+    f->activate();
+    check_pose(pose);
+    check_rig_for_fusion(rig);
+    const long npx = (long)rig->width * rig->height;
+    f->raster(pose, rig);
+    f->r_ids.ensure(sizeof(int) * npx);
+    f->r_depth.ensure(sizeof(double) * npx);
+    launch_raster_out(f->zbits.as<unsigned long long>(), f->ids.as<int>(), f->r_ids.as<int>(),
+                      f->r_depth.as<double>(), npx, f->stream);
+    ck(cudaMemcpyAsync(ids, f->r_ids.p, sizeof(int) * npx, cudaMemcpyDeviceToHost, f->stream), "D2H");
+    ck(cudaMemcpyAsync(depth, f->r_depth.p, sizeof(double) * npx, cudaMemcpyDeviceToHost, f->stream),
+       "D2H");
+    ck(cudaStreamSynchronize(f->stream), "sync");
+  });
+}
+
+ss_status ss_fusion_fuse_frame(ss_fusion* f, const int32_t* index, int32_t n_points,
+                               const double* points, const double* normals,
+                               const uint8_t* colors, int32_t w, int32_t h, const double* pose,
+                               const ss_stereo_rig* rig) {
+  return guarded([&] {
+    f->activate();
+    check_pose(pose);
+    check_rig_for_fusion(rig);
+    if (w != rig->width || h != rig->height)
+      raise(SS_EINVAL, "fuse_frame: cloud size differs from the rig's image size");
+    const long npx = (long)w * h;
+    h2d(f->st_index, index, sizeof(int) * npx, f->stream);
+    h2d(f->st_pd, points, sizeof(double) * 3 * std::max(n_points, 0), f->stream);
+    h2d(f->st_nd, normals, sizeof(double) * 3 * std::max(n_points, 0), f->stream);
+    h2d(f->st_col, colors, 3 * std::max(n_points, 0), f->stream);
+    f->fuse(f->st_index.as<int>(), f->st_pd.as<double>(), f->st_nd.as<double>(), nullptr, nullptr,
+            f->st_col.as<uint8_t>(), n_points, pose, rig);
+  });
+}
+
+ss_status ss_fusion_fuse_device(ss_fusion* f, const int32_t* d_index, const float* d_points,
+                                const float* d_normals, const uint8_t* d_colors, int32_t w,
+                                int32_t h, const double* pose, const ss_stereo_rig* rig,
+                                void* stream) {
+  return guarded([&] {
+    f->activate();
+    check_pose(pose);
+    check_rig_for_fusion(rig);
+    if (w != rig->width || h != rig->height)
+      raise(SS_EINVAL, "fuse_frame: cloud size differs from the rig's image size");
+    if (stream) {  // the cloud's producer stream: order the fusion after it
+      cudaEvent_t e;
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      ck(cudaEventRecord(e, static_cast<cudaStream_t>(stream)), "event");
+      ck(cudaStreamWaitEvent(f->stream, e, 0), "event");
+      cudaEventDestroy(e);
+    }
+    f->fuse(d_index, nullptr, nullptr, d_points, d_normals, d_colors, (int64_t)w * h, pose, rig);
+  });
+}
+
 ss_status ss_remove_outliers(const float* disparity, const uint8_t* valid, int32_t w, int32_t h,
                              int32_t radius, double threshold, float* out_disparity,
                              uint8_t* out_valid) {

@@ -128,6 +128,19 @@ void launch_match(const unsigned long long* da, const double* pa, int na,
                   int* best_b, int* best_b_d, int* best_a, int* best_a_d, int* keep, int* ia,
                   int* ib, int* ham, double* disp, int* n_out, cudaStream_t s);
 
+// Fusion consumer (k_fusion.cu).
+void launch_rasterize(const double* pos, int n, const double* pose12, double fx, double fy,
+                      double cx, double cy, int w, int h, unsigned long long* zbits, int* ids,
+                      cudaStream_t s);
+void launch_raster_out(const unsigned long long* zbits, const int* ids, int* out_ids,
+                       double* out_depth, long npx, cudaStream_t s);
+void launch_fuse(double* pos, double* nrm, double* col, double* w, double* cw, const int* index,
+                 const double* pd, const double* nd, const float* pf, const float* nf,
+                 const uint8_t* colors, const double* pose12, double fx, double fy, double cx,
+                 double cy, int W, int H, const unsigned long long* zbits, const int* ids,
+                 double trunc, double cap, double gate, double omega_min, uint8_t* is_new,
+                 int* block_new, int* total, int n0, cudaStream_t s);
+
 // emap: scratch of edge_map_words(W, H) * frames words (smooth-edge bitmaps)
 inline long edge_map_words(int W, int H) {
   const long w32 = (W + 31) / 32 + 1, h32 = (H + 31) / 32 + 1;
