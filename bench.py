@@ -212,7 +212,7 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def extensions(ss, ctxs, step_device, barrier, stream, F, Lh_first, Rh_first):
+def extensions(ss, ctxs, step_device, barrier, stream, F, Lh_first, Rh_first, od=None):
     """Side measurements of the SURVEY §8f rows (not the headline metric):
     the chain with the opt-in LR check (device pairs/s, same workload), and
     the feature front end on one C1 frame pair through the per-stage C-ABI
@@ -239,6 +239,38 @@ def extensions(ss, ctxs, step_device, barrier, stream, F, Lh_first, Rh_first):
     for c in ctxs:
         c.set_lr_check(False)
     barrier()
+    if od is not None:
+        # fusion of the step's device-resident clouds into one surfel model
+        # (a slow pan: 1 mm and 0.1 mrad per frame), device events around it
+        from paper_2007_12623_b200.synth import default_rig
+        rig = default_rig(W, H)
+        model = ss.fusion.SurfelModel(torch.cuda.current_device())
+        nf = min(F, 32)
+        poses = []
+        for f in range(nf):
+            a_ = 1e-4 * f
+            poses.append(np.array([[np.cos(a_), 0, np.sin(a_), 1.0 * f], [0, 1, 0, 0],
+                                   [-np.sin(a_), 0, np.cos(a_), 0]]))
+        N = W * H
+
+        def fuse_all(m):
+            for f in range(nf):
+                m.fuse_device(od["index"][f].data_ptr(), od["points"][f].data_ptr(),
+                              od["normals"][f].data_ptr(), od["colors"][f].data_ptr(),
+                              poses[f], rig)
+
+        fuse_all(model)  # warm (allocations)
+        model.close()
+        model = ss.fusion.SurfelModel(torch.cuda.current_device())
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fuse_all(model)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out["fusion"] = {"frames_per_s": nf / dt, "frames": nf, "surfels": len(model),
+                         "note": "fuse_device of C1 clouds (~0.5 M points each) into one model; "
+                                 "host wall clock around synchronous calls"}
+        model.close()
     gl = ss.to_gray(Lh_first)
     gr = ss.to_gray(Rh_first)
 
@@ -452,7 +484,8 @@ def run_ours(args):
                          "(unmodified reference, OpenMP all cores) + restated cloud"}
     stage_ms_per_pair = {k: v[0] / frames_timed for k, v in stages.items()}
     ext = None if (args.no_extensions or world > 1) else extensions(ss, ctxs, step_device, barrier, stream, F,
-                                                     Lh_first=Lh[0].numpy(), Rh_first=Rh[0].numpy())
+                                                     Lh_first=Lh[0].numpy(), Rh_first=Rh[0].numpy(),
+                                                     od=od)
     line = {
         "metric": "stereo pairs/sec at 960x540 D=64", "value": value, "unit": "pairs/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
