@@ -67,7 +67,7 @@ def build(verbose: bool = True) -> str:
         objs = list(ex.map(_compile, srcs))
     if _newer(LIB, objs):
         cmd = [NVCC] + ARCH + ["-shared", "-cudart", "shared", "-o", LIB] + objs + \
-            ["-Xlinker", f"-rpath,{CUDA_LIB}"]
+            ["-Xlinker", f"-rpath,{CUDA_LIB}", "-lz"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
@@ -78,20 +78,21 @@ def build(verbose: bool = True) -> str:
 
 
 def _build_cpp_test(verbose):
-    src = os.path.join(ROOT, "tests", "cpp", "test_api.cpp")
-    if not os.path.exists(src):
-        return
     out_dir = os.path.join(ROOT, "tests", "cpp", "build")
     os.makedirs(out_dir, exist_ok=True)
-    exe = os.path.join(out_dir, "test_api")
-    if _newer(exe, [src, LIB] + _deps()):
-        cmd = ["g++", "-std=c++17", "-O1", f"-I{INC}", src, "-o", exe, f"-L{LIB_DIR}",
-               "-lstereoscan_b200", f"-Wl,-rpath,{LIB_DIR}", f"-Wl,-rpath,{CUDA_LIB}"]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            raise RuntimeError(f"C++ test build failed:\n{r.stdout}\n{r.stderr}")
-        if verbose:
-            print(f"built {exe}")
+    for name in ("test_api", "io_tool"):
+        src = os.path.join(ROOT, "tests", "cpp", name + ".cpp")
+        if not os.path.exists(src):
+            continue
+        exe = os.path.join(out_dir, name)
+        if _newer(exe, [src, LIB] + _deps()):
+            cmd = ["g++", "-std=c++17", "-O1", f"-I{INC}", src, "-o", exe, f"-L{LIB_DIR}",
+                   "-lstereoscan_b200", f"-Wl,-rpath,{LIB_DIR}", f"-Wl,-rpath,{CUDA_LIB}"]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError(f"C++ test build failed:\n{r.stdout}\n{r.stderr}")
+            if verbose:
+                print(f"built {exe}")
 
 
 if __name__ == "__main__":
