@@ -45,7 +45,7 @@ namespace ssb {
 
 namespace {
 
-constexpr int kRB = 2;  // output rows per shared-memory reduction chunk
+constexpr int kRB = 1;  // output rows per shared-memory reduction chunk
 constexpr int kTH = 64;  // rows per block strip (11-row warm-up amortised over 64)
 constexpr int kNoArg = INT_MIN;  // "no defined candidate" (disparities may be negative)
 
@@ -177,15 +177,19 @@ __global__ void __launch_bounds__(512) k_wta11(
     int do_argmax, long tap_stride, long copy_stride, long lstat_stride, long rstat_stride,
     long map_stride, long win_stride) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int lane = threadIdx.x, j = threadIdx.y, NB = blockDim.y;
+  // warps 0 .. NB-1 sweep (one block of kDB candidates each); warp NB merges
+  const int lane = threadIdx.x, j = threadIdx.y, NB = blockDim.y - 1;
+  const bool merger = j == NB;
   const int NCB = NB * kDB;  // staged candidates per pixel
   const RingGeom rg = ring_geom(NB);
   unsigned char* ring = smem_raw;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kNSlots * rg.slot_bytes);
-  float* s_best = reinterpret_cast<float*>(bars + kNSlots);
-  float* s_sec = s_best + kRB * NB * 32;
-  int* s_arg = reinterpret_cast<int*>(s_sec + kRB * NB * 32);
-  float* s_g = reinterpret_cast<float*>(s_arg + kRB * NB * 32);  // [kRB][NCB][32]
+  // staging, double-buffered by chunk parity: partials [2][kRB][NB][32],
+  // scores [2][kRB][NCB][32]
+  float* s_best0 = reinterpret_cast<float*>(bars + kNSlots);
+  float* s_sec0 = s_best0 + 2 * kRB * NB * 32;
+  int* s_arg0 = reinterpret_cast<int*>(s_sec0 + 2 * kRB * NB * 32);
+  float* s_g0 = reinterpret_cast<float*>(s_arg0 + 2 * kRB * NB * 32);
 
   const long fr = blockIdx.z;
   ltap += fr * tap_stride;
@@ -212,7 +216,7 @@ __global__ void __launch_bounds__(512) k_wta11(
   // outside it (the refinement's +-5 margin) come from k_window_build.
   const int ND = g.dmax - g.dmin + 1;
   const int c0 = g.dmin + j * kDB;
-  const int nact = min(kDB, ND - j * kDB);
+  const int nact = merger ? 0 : min(kDB, ND - j * kDB);
   const bool active = (u < W - h) && (nact > 0);
   unsigned amask = 0;
 #pragma unroll
@@ -282,6 +286,96 @@ __global__ void __launch_bounds__(512) k_wta11(
     return w;
   };
 
+  const int nrows = v_end - v_begin;
+  const int nchunks = (nrows + kRB - 1) / kRB;
+  // Named barriers: FULL(b) = 1 + b (sweep warps arrive, the merger waits),
+  // EMPTY(b) = 3 + b (the merger arrives, sweep warps wait before reusing
+  // staging buffer b two chunks later).
+  const int nthr = (NB + 1) * 32;
+
+  if (merger) {
+    for (int k = 0; k < nchunks; ++k) {
+      const int b = k & 1;
+      bar_sync(1 + b, nthr);
+      const int vk0 = v_begin + k * kRB, rows = min(kRB, v_end - vk0);
+      const int vlast = vk0 + rows - 1;
+      // every sweep warp is past step vlast: rows <= vlast - 6 are dead
+      if (lane == 0) {
+        const int hi = min(y_last, vlast - 6 + kNSlots);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int y = issued + 1; y <= hi; ++y) issue(y);
+      }
+      issued = min(y_last, max(issued, vlast - 6 + kNSlots));
+      const float* s_best = s_best0 + b * kRB * NB * 32;
+      const float* s_sec = s_sec0 + b * kRB * NB * 32;
+      const int* s_arg = s_arg0 + b * kRB * NB * 32;
+      const float* s_g = s_g0 + b * kRB * NCB * 32;
+      for (int r = 0; r < rows; ++r) {
+        float B = -INFINITY, S = -INFINITY;
+        int A = kNoArg;
+        for (int jj = 0; jj < NB; ++jj) {
+          const int o = (r * NB + jj) * 32 + lane;
+          const int a = s_arg[o];
+          if (a == kNoArg) continue;
+          const float bb = s_best[o], s2 = s_sec[o];
+          if (bb > B) {
+            S = fmaxf(B, s2);
+            B = bb;
+            A = a;
+          } else {
+            S = fmaxf(S, fmaxf(bb, s2));
+          }
+        }
+        if (u >= W - h) continue;
+        const int vv = vk0 + r;
+        const long idx = (long)vv * W + u;
+        const float rl = __int_as_float(__ldg(&lstat[idx].y));
+        if (do_argmax) {
+          float dout = 0.f;
+          uint8_t vout = 0;
+          if (A != kNoArg && !isnan(rl)) {
+            const bool near_tie = S >= B - 4e-6f * fabsf(B);
+            const float sc = B * rl;
+            const bool amb = fabsf(sc - min_zncc_f) <= thr_tol;
+            if (near_tie || amb) {
+              flag_list[atomicAdd(flag_count, 1u)] = (int)idx;
+            } else if (sc >= min_zncc_f) {
+              dout = (float)A;
+              vout = 1;
+            }
+          }
+          disp[idx] = dout;
+          valid[idx] = vout;
+        }
+        // Candidate window for the refinement: kWin consecutive scores
+        // s = g * rl around the pick (or the caller's base map).
+        if (!win) continue;  // argmax only (right view of the LR check)
+        const int anchor = base_map ? base_map[idx] : A;
+        int wb = kNoWin;
+        if (!isnan(rl) && anchor != kNoArg && anchor != kNoWin)
+          wb = window_base(anchor, g.cmin, g.NC);
+        // A window reaching past [d_min, d_max] is left for k_window_build
+        // (wbase kNoWin never matches the post-cleanup check's target).
+        if (wb != kNoWin && (wb < g.dmin || wb + kWin - 1 > g.dmax)) wb = kNoWin;
+        const long bi = bt_index(W, vv, u);
+        wbase[bi] = wb;
+        if (wb != kNoWin) {
+          const float* gr = s_g + (r * NCB + wb - g.dmin) * 32 + lane;
+          uint32_t w[kWin / 2];  // kWin fp16 match costs (m_code)
+#pragma unroll
+          for (int q = 0; q < kWin / 2; ++q)
+            w[q] = pack_m2(gr[(2 * q) * 32] * rl, gr[(2 * q + 1) * 32] * rl);
+          uint32_t* wq = reinterpret_cast<uint32_t*>(win) + win_word(W, vv, u, 0);
+#pragma unroll
+          for (int q = 0; q < kWin / 2; ++q) wq[(long)q * W * 32] = w[q];
+        }
+      }
+      __syncwarp();
+      bar_arrive(3 + b, nthr);
+    }
+    return;
+  }
+
   int X[kDB], Y[kDB];
 #pragma unroll
   for (int i = 0; i < kDB; ++i) X[i] = Y[i] = 0;
@@ -305,11 +399,10 @@ __global__ void __launch_bounds__(512) k_wta11(
         step_all(wo, wn, X, Y, std::make_integer_sequence<int, kDB>{});
       }
     }
-    const int slot = (v - v_begin) & (kRB - 1);
-    // Staging of a new chunk waits until the previous chunk's merges are done
-    // (the merges overlap the non-merging warps' step of this row).
-    if (slot == 0 && v > v_begin) bar_sync(2, NB * 32);
-    float* gs = s_g + (slot * NCB + j * kDB) * 32 + lane;  // staged g of this (row, block)
+    const int k = (v - v_begin) / kRB, slot = (v - v_begin) - k * kRB, b = k & 1;
+    // staging buffer b was merged (chunk k - 2) before it is rewritten
+    if (slot == 0 && k >= 2) bar_sync(3 + b, nthr);
+    float* gs = s_g0 + ((b * kRB + slot) * NCB + j * kDB) * 32 + lane;
     float best = -INFINITY, second = -INFINITY;
     int arg = kNoArg;
     if (active) {
@@ -325,88 +418,11 @@ __global__ void __launch_bounds__(512) k_wta11(
                         std::make_integer_sequence<int, kDB>{});
       arg = ai >= 0 ? c0 + ai : kNoArg;
     }
-    const int so = (slot * NB + j) * 32 + lane;
-    s_best[so] = best;
-    s_sec[so] = second;
-    s_arg[so] = arg;
-    if (slot == kRB - 1 || v == v_end - 1) {
-      // Barrier 1: the chunk's partials are staged. Warps j <= slot merge one
-      // row each (and wait for all partials); the others only arrive and go
-      // on with the next row's step.
-      if (j > slot) {
-        bar_arrive(1, NB * 32);
-        continue;
-      }
-      bar_sync(1, NB * 32);
-      // every warp is past step v: rows <= v - 6 are dead, their slots free
-      if (tid == 0) {
-        const int hi = min(y_last, v - 6 + kNSlots);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        for (int y = issued + 1; y <= hi; ++y) issue(y);
-      }
-      issued = min(y_last, max(issued, v - 6 + kNSlots));
-      for (int r = j; r <= slot; r += NB) {
-        float B = -INFINITY, S = -INFINITY;
-        int A = kNoArg;
-        for (int jj = 0; jj < NB; ++jj) {
-          const int o = (r * NB + jj) * 32 + lane;
-          const int a = s_arg[o];
-          if (a == kNoArg) continue;
-          const float b = s_best[o], s2 = s_sec[o];
-          if (b > B) {
-            S = fmaxf(B, s2);
-            B = b;
-            A = a;
-          } else {
-            S = fmaxf(S, fmaxf(b, s2));
-          }
-        }
-        if (u < W - h) {
-          const int vv = v - slot + r;
-          const long idx = (long)vv * W + u;
-          const float rl = __int_as_float(__ldg(&lstat[idx].y));
-          if (do_argmax) {
-            float dout = 0.f;
-            uint8_t vout = 0;
-            if (A != kNoArg && !isnan(rl)) {
-              const bool near_tie = S >= B - 4e-6f * fabsf(B);
-              const float sc = B * rl;
-              const bool amb = fabsf(sc - min_zncc_f) <= thr_tol;
-              if (near_tie || amb) {
-                flag_list[atomicAdd(flag_count, 1u)] = (int)idx;
-              } else if (sc >= min_zncc_f) {
-                dout = (float)A;
-                vout = 1;
-              }
-            }
-            disp[idx] = dout;
-            valid[idx] = vout;
-          }
-          // Candidate window for the refinement: kWin consecutive scores
-          // s = g * rl around the pick (or the caller's base map).
-          if (!win) continue;  // argmax only (right view of the LR check)
-          const int anchor = base_map ? base_map[idx] : A;
-          int wb = kNoWin;
-          if (!isnan(rl) && anchor != kNoArg && anchor != kNoWin)
-            wb = window_base(anchor, g.cmin, g.NC);
-          // A window reaching past [d_min, d_max] is left for k_window_build
-          // (wbase kNoWin never matches the post-cleanup check's target).
-          if (wb != kNoWin && (wb < g.dmin || wb + kWin - 1 > g.dmax)) wb = kNoWin;
-          const long bi = bt_index(W, vv, u);
-          wbase[bi] = wb;
-          if (wb != kNoWin) {
-            const float* gr = s_g + (r * NCB + wb - g.dmin) * 32 + lane;
-            uint32_t w[kWin / 2];  // kWin fp16 match costs (m_code)
-#pragma unroll
-            for (int q = 0; q < kWin / 2; ++q)
-              w[q] = pack_m2(gr[(2 * q) * 32] * rl, gr[(2 * q + 1) * 32] * rl);
-            uint32_t* wq = reinterpret_cast<uint32_t*>(win) + win_word(W, vv, u, 0);
-#pragma unroll
-            for (int q = 0; q < kWin / 2; ++q) wq[(long)q * W * 32] = w[q];
-          }
-        }
-      }
-    }
+    const int so = ((b * kRB + slot) * NB + j) * 32 + lane;
+    s_best0[so] = best;
+    s_sec0[so] = second;
+    s_arg0[so] = arg;
+    if (slot == kRB - 1 || v == v_end - 1) bar_arrive(1 + b, nthr);  // chunk k staged
   }
 }
 
@@ -420,10 +436,10 @@ void launch_wta11(const uint4* ltap, const uint32_t* rcopy, const int2* lstat, c
   if (g.W - 2 * h <= 0 || g.H - 2 * h <= 0 || frames <= 0) return;
   const int NB = (g.dmax - g.dmin + 1 + kDB - 1) / kDB;
   const RingGeom rg = ring_geom(NB);
-  dim3 block(32, NB);
+  dim3 block(32, NB + 1);
   dim3 grid((g.W - 2 * h + 31) / 32, (g.H - 2 * h + kTH - 1) / kTH, frames);
   const size_t smem = (size_t)kNSlots * rg.slot_bytes + 8 * kNSlots +
-                      (size_t)kRB * NB * 32 * 12 + (size_t)kRB * NB * kDB * 32 * 4;
+                      2 * ((size_t)kRB * NB * 32 * 12 + (size_t)kRB * NB * kDB * 32 * 4);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     cudaFuncSetAttribute(k_wta11, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
