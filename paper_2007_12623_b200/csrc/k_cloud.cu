@@ -271,7 +271,7 @@ constexpr int kNW = 3;              // kNormalWindowHalf (cloud.cpp:10)
 constexpr int kNTX = 32, kNTY = 8;  // output tile
 constexpr int kNIX = kNTX + 2 * kNW, kNIY = kNTY + 2 * kNW;  // input tile (38 x 14)
 constexpr int kNQ = 10;             // window moments: n, sx, sy, sz, sxx, sxy, sxz, syy, syz, szz
-constexpr int kNSeg = 4;            // output columns per horizontal running-sum task
+constexpr int kNSeg = 2;            // output columns per horizontal running-sum task
 
 struct NormalSmem {
   double p[4][kNIY][kNIX];    // per input pixel: point flag (1/0), x, y, z (0 where no point)
