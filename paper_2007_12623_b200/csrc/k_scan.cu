@@ -124,7 +124,7 @@ void launch_scan_bt_i(const int* xT, const uint8_t* mT, int* pT, int W, int H, i
 // which leaves a prefix bit-identical (it is never -0.0: it starts at +0.0 and
 // an exactly-zero round-to-nearest sum is +0.0).
 constexpr int kChunkB = 32;
-constexpr int kScanBWarps = 8;
+constexpr int kScanBWarps = 16;
 struct ScanBRaw {  // [column][row]
   int so[kChunkB][32], cnt[kChunkB][32], o[kChunkB][32];
   double d[kChunkB][32];
