@@ -133,18 +133,31 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// dout2/vout2 (optional): a second copy of the result (the radial fill's
+// output buffer, so that fill only writes the pixels it fills); list/count
+// (optional): per-frame list of the invalid output pixels.
+__device__ __forceinline__ void append_invalid(int* list, unsigned* count, long f, long stride,
+                                               int pix) {
+  list[f * stride + atomicAdd(count + f, 1u)] = pix;
+}
+
 __global__ void k_remove_outliers(const float* __restrict__ din, const uint8_t* __restrict__ vin,
                                   float* __restrict__ dout, uint8_t* __restrict__ vout, int W,
                                   int H, int r, const uint32_t* __restrict__ emap, long stride,
-                                  long fw) {
+                                  long fw, float* __restrict__ dout2, uint8_t* __restrict__ vout2,
+                                  int* __restrict__ list, unsigned* __restrict__ count) {
   const long f = blockIdx.z;
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = blockIdx.y * blockDim.y + threadIdx.y;
   if (u >= W || v >= H) return;
   const long i = f * stride + (long)v * W + u;
-  dout[i] = din[i];
+  const float d0 = din[i];
+  dout[i] = d0;
+  if (dout2) dout2[i] = d0;
   if (!vin[i]) {
     vout[i] = 0;
+    if (vout2) vout2[i] = 0;
+    if (list) append_invalid(list, count, f, stride, v * W + u);
     return;
   }
   const EdgeMaps M = edge_maps(const_cast<uint32_t*>(emap) + f * fw, W, H);
@@ -162,23 +175,19 @@ __global__ void k_remove_outliers(const float* __restrict__ din, const uint8_t* 
   if (!keep && u - r >= 0 && v + r < H) keep = run_ok(d2, v + 1, r);     // (-1, 1)
   if (!keep && u - r >= 0 && v - r >= 0) keep = run_ok(d1, v - r, r);   // (-1, -1)
   vout[i] = keep ? 1 : 0;
+  if (vout2) vout2[i] = keep ? 1 : 0;
+  if (list && !keep) append_invalid(list, count, f, stride, v * W + u);
 }
 
-__global__ void k_fill_radial(const float* __restrict__ din, const uint8_t* __restrict__ vin,
-                              float* __restrict__ dout, uint8_t* __restrict__ vout, int W, int H,
-                              int radius, int min_support, long stride) {
-  const long f = blockIdx.z;
-  din += f * stride;
-  vin += f * stride;
-  dout += f * stride;
-  vout += f * stride;
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  const int v = blockIdx.y * blockDim.y + threadIdx.y;
-  if (u >= W || v >= H) return;
+// Radial fill of one invalid pixel (cleanup.cpp:54-68): writes dout/vout
+// only when the pixel is filled.
+__device__ __forceinline__ void radial_fill_pixel(const float* __restrict__ din,
+                                                  const uint8_t* __restrict__ vin,
+                                                  float* __restrict__ dout,
+                                                  uint8_t* __restrict__ vout, int W, int H,
+                                                  int u, int v, int radius, int min_support) {
   const long i = (long)v * W + u;
-  float od = din[i];
-  uint8_t ov = vin[i];
-  if (!ov) {
+  {
     double wsum = 0.0, vsum = 0.0;
     int support = 0;
     for (int dir = 0; dir < 8; ++dir) {
@@ -197,12 +206,43 @@ __global__ void k_fill_radial(const float* __restrict__ din, const uint8_t* __re
       }
     }
     if (support >= min_support && wsum > 0.0) {
-      od = (float)__ddiv_rn(vsum, wsum);
-      ov = 1;
+      dout[i] = (float)__ddiv_rn(vsum, wsum);
+      vout[i] = 1;
     }
   }
-  dout[i] = od;
-  vout[i] = ov;
+}
+
+__global__ void k_fill_radial(const float* __restrict__ din, const uint8_t* __restrict__ vin,
+                              float* __restrict__ dout, uint8_t* __restrict__ vout, int W, int H,
+                              int radius, int min_support, long stride) {
+  const long f = blockIdx.z;
+  din += f * stride;
+  vin += f * stride;
+  dout += f * stride;
+  vout += f * stride;
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y * blockDim.y + threadIdx.y;
+  if (u >= W || v >= H) return;
+  const long i = (long)v * W + u;
+  dout[i] = din[i];
+  vout[i] = vin[i];
+  if (!vin[i]) radial_fill_pixel(din, vin, dout, vout, W, H, u, v, radius, min_support);
+}
+
+// Chain variant: dout/vout already hold the input map (k_remove_outliers'
+// second copy); one thread per listed invalid pixel, no idle lanes.
+__global__ void k_fill_radial_list(const float* __restrict__ din, const uint8_t* __restrict__ vin,
+                                   float* __restrict__ dout, uint8_t* __restrict__ vout, int W,
+                                   int H, int radius, int min_support, long stride,
+                                   const int* __restrict__ list,
+                                   const unsigned* __restrict__ count) {
+  const long f = blockIdx.y;
+  const unsigned n = count[f];
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int pix = list[f * stride + t];
+    radial_fill_pixel(din + f * stride, vin + f * stride, dout + f * stride, vout + f * stride,
+                      W, H, pix % W, pix / W, radius, min_support);
+  }
 }
 
 // Disc fill, pass 1: copy the map through and, for invalid pixels, count the
@@ -305,7 +345,8 @@ static dim3 map_grid(int W, int H, int frames, dim3 b) {
 
 void launch_remove_outliers(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
                             int W, int H, int radius, double thr, uint32_t* emap, int frames,
-                            long stride, cudaStream_t s) {
+                            long stride, cudaStream_t s, float* dout2, uint8_t* vout2, int* list,
+                            unsigned* count) {
   if (W <= 0 || H <= 0 || frames <= 0) return;
   const long fw = edge_map_words(W, H);
   if (radius > 0) {
@@ -315,7 +356,16 @@ void launch_remove_outliers(const float* din, const uint8_t* vin, float* dout, u
   }
   dim3 b(32, 8);
   k_remove_outliers<<<map_grid(W, H, frames, b), b, 0, s>>>(din, vin, dout, vout, W, H, radius,
-                                                            emap, stride, fw);
+                                                            emap, stride, fw, dout2, vout2, list,
+                                                            count);
+}
+
+void launch_fill_radial_list(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
+                             int W, int H, int radius, int min_support, const int* list,
+                             const unsigned* count, int frames, long stride, cudaStream_t s) {
+  if (W <= 0 || H <= 0 || frames <= 0) return;
+  k_fill_radial_list<<<dim3(96, frames), 128, 0, s>>>(din, vin, dout, vout, W, H, radius,
+                                                      min_support, stride, list, count);
 }
 
 void launch_fill_radial(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,

@@ -146,9 +146,18 @@ inline long edge_map_words(int W, int H) {
   const long w32 = (W + 31) / 32 + 1, h32 = (H + 31) / 32 + 1;
   return (long)H * w32 + (long)W * h32 + 2L * (W + H - 1) * h32;
 }
+// dout2/vout2/list/count (optional, nullptr = off): a second copy of the
+// result and the per-frame list of invalid output pixels (the chain's radial
+// fill then touches only those).
 void launch_remove_outliers(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
                             int W, int H, int radius, double thr, uint32_t* emap, int frames,
-                            long stride, cudaStream_t s);
+                            long stride, cudaStream_t s, float* dout2 = nullptr,
+                            uint8_t* vout2 = nullptr, int* list = nullptr,
+                            unsigned* count = nullptr);
+// dout/vout must already hold din/vin; fills the listed pixels only.
+void launch_fill_radial_list(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
+                             int W, int H, int radius, int min_support, const int* list,
+                             const unsigned* count, int frames, long stride, cudaStream_t s);
 void launch_fill_radial(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
                         int W, int H, int radius, int min_support, int frames, long stride,
                         cudaStream_t s);
