@@ -271,6 +271,40 @@ def extensions(ss, ctxs, step_device, barrier, stream, F, Lh_first, Rh_first, od
                          "note": "fuse_device of C1 clouds (~0.5 M points each) into one model; "
                                  "host wall clock around synchronous calls"}
         model.close()
+    # C3 / C5 geometry (BASELINE.json configs[2], [4]): 1920x1080, D = 128,
+    # device-resident throughput over 48 synthetic pairs (6 seeded, tiled)
+    try:
+        from paper_2007_12623_b200.synth import as_rgb, default_rig, params_for, stereo_pair
+        Wf, Hf, Df, nf, Bf = 1920, 1080, 128, 48, 8
+        uniq = [stereo_pair("textured", Wf, Hf, Df, seed=100 + i)[:2] for i in range(6)]
+        Lf = torch.from_numpy(np.stack([as_rgb(uniq[i % 6][0]) for i in range(nf)])).cuda()
+        Rf = torch.from_numpy(np.stack([as_rgb(uniq[i % 6][1]) for i in range(nf)])).cuda()
+        pf = ss.StereoParams(**params_for(Df))
+        rf = ss.StereoRig(**default_rig(Wf, Hf))
+        cf = [ss.StereoContext(torch.cuda.current_device(), Wf, Hf, Bf, pf, rf) for _ in range(2)]
+        flags = ss.SS_OUT_DISPARITY | ss.SS_OUT_CLOUD | ss.SS_OUT_NORMALS
+
+        def run_fhd():
+            for i, f0 in enumerate(range(0, nf, Bf)):
+                cf[i % 2].run_device(Bf, Wf, Hf, Lf[f0].data_ptr(), Rf[f0].data_ptr(), flags)
+            for c in cf:
+                c.sync()
+
+        run_fhd()  # warm (allocations)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        run_fhd()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out["fhd_d128"] = {"value": nf / dt, "unit": "pairs/s", "ms_per_pair": 1000 * dt / nf,
+                           "workload": "48 synthetic textured 1920x1080 pairs, D=128 (d 0..127), "
+                                       "full chain incl. normals, 2 contexts, inputs in HBM",
+                           "timing": "host wall clock around synchronous batches"}
+        for c in cf:
+            c.close()
+        del Lf, Rf
+    except Exception as e:  # informational side measurement
+        out["fhd_d128"] = {"error": str(e)[:200]}
     gl = ss.to_gray(Lh_first)
     gr = ss.to_gray(Rh_first)
 
