@@ -154,7 +154,9 @@ Geom make_geom(int W, int H, const ss_stereo_params* p) {
 }
 
 bool fast_path(const Geom& g, const ss_stereo_params* p) {
-  return p->window == 11 && g.NC >= 1 && (g.NC + kDB - 1) / kDB <= 16;
+  // one sweep warp per kDB candidates of [d_min, d_max] plus the merge warp,
+  // at most 512 threads per block
+  return p->window == 11 && g.NC >= 1 && (g.dmax - g.dmin + 1 + kDB - 1) / kDB <= 15;
 }
 
 }  // namespace
