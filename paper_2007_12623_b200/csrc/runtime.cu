@@ -169,7 +169,7 @@ struct ss_ctx {
   bool has_rig = false;
   int max_w = 0, max_h = 0, max_batch = 1;
 
-  DevBuf in_l, in_r, gray_l, gray_r, plane_l, plane_r, lstat, rstat, win, wbase;
+  DevBuf in_l, in_r, gray_l, gray_r, ltap_buf, rcopy_buf, lstat, rstat, win, wbase;
   // opt-in left-right consistency (k_lr.cu)
   DevBuf gray_fl, gray_fr, disp_r, valid_r;
   // feature front end scratch (k_features.cu)
@@ -222,7 +222,7 @@ struct ss_ctx {
   int last_frames = 0;
 
   ~ss_ctx() {
-    for (DevBuf* b : {&in_l, &in_r, &gray_l, &gray_r, &plane_l, &plane_r, &lstat, &rstat, &win, &wbase,
+    for (DevBuf* b : {&in_l, &in_r, &gray_l, &gray_r, &ltap_buf, &rcopy_buf, &lstat, &rstat, &win, &wbase,
                       &disp_a, &disp_b, &valid_a, &valid_b, &flags, &flag_count, &o, &d, &avg,
                       &b, &psum, &pcnt, &cnt, &span, &wtab, &fspan, &fx, &emap, &index, &block_sums, &npoints,
                       &pts_f, &nrm_f, &colors, &pts_d, &nrm_d, &pixels, &pts4, &counters, &oi, &trace_o,
@@ -338,8 +338,8 @@ struct ss_ctx {
     const long rstride = (long)g.H * g.SP;
     // (+ slack: the sweep's row copies are fixed-size and may run past the
     // last row of the last frame; those bytes feed only inactive lanes)
-    plane_l.ensure(sizeof(uint4) * tap_stride * n + 4096);
-    plane_r.ensure(sizeof(uint32_t) * copy_stride * n + 4096);
+    ltap_buf.ensure(sizeof(uint4) * tap_stride * n + 4096);
+    rcopy_buf.ensure(sizeof(uint32_t) * copy_stride * n + 4096);
     lstat.ensure(sizeof(int2) * N * n);
     rstat.ensure(sizeof(int2) * rstride * n);
     const long bs = bt_frame(g.W, g.H, 0);  // windows are BT-indexed
@@ -349,8 +349,8 @@ struct ss_ctx {
     flag_count.ensure(sizeof(unsigned) * n);
     {
     Stage st(this, 1);
-    launch_ltap(gl, plane_l.as<uint4>(), g, n, N, tap_stride, stream);
-    launch_rcopy(gr, plane_r.as<uint32_t>(), g, n, N, copy_stride, stream);
+    launch_ltap(gl, ltap_buf.as<uint4>(), g, n, N, tap_stride, stream);
+    launch_rcopy(gr, rcopy_buf.as<uint32_t>(), g, n, N, copy_stride, stream);
     launch_stats(gl, lstat.as<int2>(), nullptr, 0, g, n, N, N, stream);
     launch_stats(gr, nullptr, rstat.as<int2>(), 1, g, n, N, rstride, stream);
     stats.kernel_launches += 4;
@@ -361,7 +361,7 @@ struct ss_ctx {
       ck(cudaMemsetAsync(vld, 0, N * n, stream), "memset");
     }
     Stage st(this, 2);
-    launch_wta11(plane_l.as<uint4>(), plane_r.as<uint32_t>(), lstat.as<int2>(), rstat.as<int2>(),
+    launch_wta11(ltap_buf.as<uint4>(), rcopy_buf.as<uint32_t>(), lstat.as<int2>(), rstat.as<int2>(),
                  windows ? win.as<wscore_t>() : nullptr, wbase.as<int>(), nullptr, dsp, vld,
                  flags.as<int>(), flag_count.as<unsigned>(), g,
                  params.min_zncc, n, tap_stride, copy_stride, N, rstride, N, bs,
