@@ -163,6 +163,26 @@ def reference_chain(pairs):
     return time.perf_counter() - t0, kind
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def omp_threads(n):
+    """Set the OpenMP team size of this process (the reference library's)."""
+    import ctypes
+    try:
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(int(n))
+        return True
+    except OSError:
+        return False
+
+
 def cpu_pairs(n):
     from paper_2007_12623_b200.synth import as_rgb, stereo_pair
     out = []
@@ -513,9 +533,13 @@ def run_ours(args):
         pairs_cpu = cpu_pairs(args.cpu_pairs)
         tcpu, kind = reference_chain(pairs_cpu)
         cpu = {"value": len(pairs_cpu) / tcpu, "unit": "pairs/s", "cores": os.cpu_count(),
-               "kind": kind,
+               "kind": kind, "cpu_model": cpu_model(),
                "sample": f"{len(pairs_cpu)} C1 pairs (960x540 D=64) through oracle/_ref "
                          "(unmodified reference, OpenMP all cores) + restated cloud"}
+        if omp_threads(1):  # also one thread
+            t1, _ = reference_chain(pairs_cpu[:1])
+            cpu["single_thread_value"] = 1.0 / t1
+            omp_threads(os.cpu_count())
     stage_ms_per_pair = {k: v[0] / frames_timed for k, v in stages.items()}
     ext = None if (args.no_extensions or world > 1) else extensions(ss, ctxs, step_device, barrier, stream, F,
                                                      Lh_first=Lh[0].numpy(), Rh_first=Rh[0].numpy(),
