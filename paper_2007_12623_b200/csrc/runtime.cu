@@ -1,5 +1,7 @@
 // Runtime + C-ABI (include/ss_stereo.h): device context, buffer arena,
-// stage orchestration on one CUDA stream, and the per-stage drop-ins.
+// stage orchestration on one CUDA stream, the per-stage drop-ins, the
+// pipelined host batch API (H2D / chain / D2H on three streams, two slots),
+// the opt-in LR check, the feature front end and the fusion model.
 //
 // One ss_ctx per (host thread, GPU). All per-frame buffers are byte arenas that
 // grow on demand; strides are recomputed from each call's geometry, so one
