@@ -42,8 +42,16 @@ __device__ __forceinline__ unsigned short m_code(float s) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaxf(s, 1e-3f)));
   return __half_as_ushort(__float2half_rn(fminf(r, 999.5f)));
 }
+// Two m_codes in one packed conversion (bit-identical to m_code: 1000 and the
+// capped reciprocal convert exactly as there).
+__device__ __forceinline__ float m_value(float s) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaxf(s, 1e-3f)));
+  return s >= 0.99e-3f ? fminf(r, 999.5f) : 1000.f;
+}
 __device__ __forceinline__ uint32_t pack_m2(float s0, float s1) {
-  return (uint32_t)m_code(s0) | ((uint32_t)m_code(s1) << 16);
+  const __half2 h = __floats2half2_rn(m_value(s0), m_value(s1));
+  return *reinterpret_cast<const uint32_t*>(&h);
 }
 constexpr int kNoWin = -2147483647 - 1;  // INT_MIN: no window / no defined candidate
 
