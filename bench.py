@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=16, help="frames per device launch")
     ap.add_argument("--unique", type=int, default=32, help="distinct seeded frames (tiled)")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--streams", type=int, default=3,
+    ap.add_argument("--streams", type=int, default=4,
                     help="concurrent contexts (one CUDA stream each) sharing the frames")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extensions", action="store_true",
