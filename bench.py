@@ -525,6 +525,12 @@ def run_ours(args):
         "peak_source": f"{n_sm} SM x 128 lanes x sm_max_mhz {sm_max:.0f} (MEASURED_PEAKS.json); "
                        "ALU issue, not a bf16/HBM figure: the path is integer/FP64 ALU work",
         "ops_per_launch": ops_per_launch, "avg_launch_ms": wta_ms / launches,
+        "hbm_view": ({"achieved_gbs": traffic / (wta_ms / launches / 1000.0) / 1e9,
+                      "peak_gbs": hbm_peak,
+                      "frac": traffic / (wta_ms / launches / 1000.0) / 1e9 / hbm_peak,
+                      "note": "ncu DRAM bytes per launch over the live launch time: the "
+                              "sweep is not HBM-bound"}
+                     if traffic and wta_ms > 0 else None),
         "pipeline_census_frac": CENSUS["textured"] * value / world / alu_peak,
         "hbm_frac_pipeline": 21.8e6 * value / world / (hbm_peak * 1e9),
     }
