@@ -285,6 +285,26 @@ ss_status ss_stereo_batch_device(ss_ctx* ctx, int32_t n, int32_t w, int32_t h,
 /* Device pointers of the ctx-owned result buffers of the last batch. */
 ss_status ss_ctx_device_outputs(ss_ctx* ctx, ss_batch_out* d_out);
 
+/* ---- in-process frame sharding across GPUs ----
+ * One ctx and one host thread per device entry; a batch splits into
+ * contiguous frame blocks (sizes differ by <= 1) and each device writes its
+ * block straight into the caller's frame-ordered host outputs (the host-side
+ * gather; no collective). Entries may repeat a device. Results are identical
+ * to one ss_stereo_batch over all frames. On failure ss_multi_last_error()
+ * names the device. */
+typedef struct ss_multi ss_multi;
+ss_status ss_multi_create(int32_t n_devices, const int32_t* devices, int32_t max_w, int32_t max_h,
+                          int32_t max_batch, const ss_stereo_params* p, const ss_stereo_rig* rig,
+                          ss_multi** out);
+ss_status ss_multi_destroy(ss_multi* m);
+int32_t ss_multi_size(const ss_multi* m);
+ss_ctx* ss_multi_ctx(ss_multi* m, int32_t k);
+ss_status ss_multi_set_lr_check(ss_multi* m, int32_t enable, int32_t max_diff);
+ss_status ss_multi_stereo_batch(ss_multi* m, int32_t n, int32_t w, int32_t h, int32_t in_format,
+                                const uint8_t* left, const uint8_t* right, uint32_t out_flags,
+                                const ss_batch_out* out);
+const char* ss_multi_last_error(void);
+
 /* Pinned host memory helpers (cudaHostAlloc / cudaFreeHost). */
 void* ss_host_alloc(size_t bytes);
 void ss_host_free(void* p);

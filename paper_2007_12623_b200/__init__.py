@@ -10,6 +10,7 @@ from .stereo import (  # noqa: F401
     InvalidArgument,
     StereoCloud,
     StereoContext,
+    StereoMulti,
     StereoError,
     StereoParams,
     StereoRig,

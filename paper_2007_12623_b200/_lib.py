@@ -110,6 +110,13 @@ def lib():
         "ss_ctx_set_lr_check": (i32, [vp, i32, i32]),
         "ss_ctx_enable_timing": (i32, [vp, i32]),
         "ss_ctx_stage_times": (i32, [vp, P(C.c_double), P(C.c_int64)]),
+        "ss_multi_create": (i32, [i32, P(i32), i32, i32, i32, P(SsParams), P(SsRig), P(vp)]),
+        "ss_multi_destroy": (i32, [vp]),
+        "ss_multi_size": (i32, [vp]),
+        "ss_multi_set_lr_check": (i32, [vp, i32, i32]),
+        "ss_multi_stereo_batch": (i32, [vp, i32, i32, i32, i32, vp, vp, C.c_uint32,
+                                        P(SsBatchOut)]),
+        "ss_multi_last_error": (C.c_char_p, []),
         "ss_host_alloc": (vp, [C.c_size_t]),
         "ss_host_free": (None, [vp]),
     }

@@ -330,6 +330,53 @@ class StereoContext:
         return {k: getattr(bo, k) for k, _ in L.SsBatchOut._fields_}
 
 
+class StereoMulti:
+    """In-process frame sharding across GPUs (ss_multi_*): one context and one
+    host thread per device entry; each device writes its contiguous block of
+    frames into the shared, frame-ordered outputs (the host-side gather)."""
+
+    def __init__(self, devices, max_w=960, max_h=540, max_batch=8, params=None, rig=None,
+                 lr_check=False, lr_max_diff=1):
+        self._m = C.c_void_p()
+        dev = (C.c_int32 * len(devices))(*devices)
+        r = C.byref(_rig(rig)) if rig is not None else None
+        rc = L.lib().ss_multi_create(len(devices), dev, max_w, max_h, max_batch,
+                                     C.byref(_params(params)), r, C.byref(self._m))
+        _check(rc)
+        if lr_check:
+            _check(L.lib().ss_multi_set_lr_check(self._m, 1, int(lr_max_diff)))
+
+    def close(self):
+        if self._m:
+            L.lib().ss_multi_destroy(self._m)
+            self._m = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __len__(self):
+        return int(L.lib().ss_multi_size(self._m))
+
+    def run(self, left, right, out_flags=L.SS_OUT_DISPARITY, in_format=None, out=None):
+        left, right = np.ascontiguousarray(left), np.ascontiguousarray(right)
+        if in_format is None:
+            in_format = L.SS_IN_RGB if left.ndim == 4 else L.SS_IN_GRAY
+        n, h, w = left.shape[:3]
+        if out is None:
+            out = StereoContext.alloc_outputs(n, h, w, out_flags)
+        bo = L.SsBatchOut(*[_ptr(out.get(k)) if out.get(k) is not None else None
+                            for k, _ in L.SsBatchOut._fields_])
+        rc = L.lib().ss_multi_stereo_batch(self._m, n, w, h, in_format, _ptr(left), _ptr(right),
+                                           out_flags, C.byref(bo))
+        if rc != L.SS_OK:
+            raise (InvalidArgument if rc == L.SS_EINVAL else StereoError)(
+                rc, L.lib().ss_multi_last_error().decode())
+        return out
+
+
 def pinned_empty(shape, dtype):
     """numpy array backed by pinned (page-locked) host memory."""
     dtype = np.dtype(dtype)

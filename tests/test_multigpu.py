@@ -71,3 +71,34 @@ def test_sharded_gather_matches_single_rank(tmp_path, orc, world):
         L, R, _ = stereo_pair("textured", 48, 32, 8, seed=f)
         d, v = orc.compute_disparity(L, R, p)
         assert np.array_equal(g["disparity"][f], d) and np.array_equal(g["valid"][f], v)
+
+
+@pytest.mark.gpu
+def test_multi_device_api_matches_single_context():
+    """ss_multi_* with two contexts on the visible GPU(s): the sharded batch,
+    gathered into frame order on the host, equals one context over all frames
+    (bit for bit, clouds included)."""
+    import paper_2007_12623_b200 as ss
+    from paper_2007_12623_b200.synth import as_rgb, default_rig, params_for, stereo_pair
+    W, H, D = 192, 112, 24
+    p = ss.StereoParams(**params_for(D))
+    rig = ss.StereoRig(**default_rig(W, H))
+    frames = [stereo_pair("textured" if i % 2 else "lowtex", W, H, D, seed=i)[:2] for i in range(5)]
+    Ls = np.stack([as_rgb(f[0]) for f in frames])
+    Rs = np.stack([as_rgb(f[1]) for f in frames])
+    flags = ss.SS_OUT_DISPARITY | ss.SS_OUT_CLOUD | ss.SS_OUT_NORMALS
+    ctx = ss.StereoContext(0, W, H, 2, p, rig)
+    want = ctx.run(Ls, Rs, flags)
+    ctx.close()
+    n_dev = max(1, ss.device_count())
+    devices = [k % n_dev for k in range(3)]  # three entries: repeats on a one-GPU box
+    multi = ss.StereoMulti(devices, W, H, 2, p, rig)
+    assert len(multi) == 3
+    got = multi.run(Ls, Rs, flags)
+    multi.close()
+    for k in ("disparity", "valid", "index", "n_points"):
+        assert np.array_equal(got[k], want[k]), k
+    for f in range(len(frames)):
+        m = int(want["n_points"][f])
+        for k in ("points", "normals", "colors"):
+            assert np.array_equal(got[k][f][:m], want[k][f][:m]), (k, f)
