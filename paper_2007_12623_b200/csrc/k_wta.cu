@@ -294,8 +294,16 @@ __global__ void __launch_bounds__(512) k_wta11(
   const int nthr = (NB + 1) * 32;
 
   if (merger) {
+    static_assert(kRB == 1, "the merge warp prefetches one row's 1/sqrt(var_l) ahead");
+    // 1/sqrt(var_l) of the next row, loaded before waiting for its partials
+    // (a global load off the merge warp's critical path)
+    const bool in_img = u < W - h;
+    float rl_next = in_img ? __int_as_float(__ldg(&lstat[(long)v_begin * W + u].y)) : 0.f;
     for (int k = 0; k < nchunks; ++k) {
       const int b = k & 1;
+      const float rl_cur = rl_next;
+      if (in_img && k + 1 < nchunks)
+        rl_next = __int_as_float(__ldg(&lstat[(long)(v_begin + k + 1) * W + u].y));
       bar_sync(1 + b, nthr);
       const int vk0 = v_begin + k * kRB, rows = min(kRB, v_end - vk0);
       const int vlast = vk0 + rows - 1;
@@ -329,7 +337,7 @@ __global__ void __launch_bounds__(512) k_wta11(
         if (u >= W - h) continue;
         const int vv = vk0 + r;
         const long idx = (long)vv * W + u;
-        const float rl = __int_as_float(__ldg(&lstat[idx].y));
+        const float rl = rl_cur;
         if (do_argmax) {
           float dout = 0.f;
           uint8_t vout = 0;
