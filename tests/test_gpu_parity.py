@@ -191,6 +191,22 @@ def test_default_params_negative_disparities(ss, orc):
                      "default refine")
 
 
+@pytest.mark.parametrize("d_min,d_max", [(0, 199), (-40, 199), (0, 255), (3, 9)])
+def test_wide_and_narrow_disparity_ranges(ss, orc, d_min, d_max):
+    """Sweep geometry at the edges: 13-15 sweep warps (the fast path's limit is
+    15 + the merge warp), the generic exact path beyond, and fewer candidates
+    than one 16-wide warp block (masked lanes, windows rebuilt)."""
+    from paper_2007_12623_b200.synth import stereo_pair
+    L, R, _ = stereo_pair("textured", 400, 96, 48, seed=12)
+    R = np.roll(R, 30, axis=1)
+    p = dict(d_min=d_min, d_max=d_max)
+    want = orc.compute_disparity(L, R, p)
+    assert_map_equal(ss.compute_disparity(L, R, p), want, f"WTA {d_min}..{d_max}")
+    wc = orc.cleanup_pass(*want, p)
+    assert_map_equal(ss.refine_disparities(*wc, L, R, p), orc.refine_disparities(*wc, L, R, p),
+                     f"refine {d_min}..{d_max}")
+
+
 @pytest.mark.parametrize("window", [3, 7, 9, 13])
 def test_other_windows(ss, orc, window):
     from paper_2007_12623_b200.synth import params_for, stereo_pair
