@@ -328,3 +328,64 @@ def test_batch_api_matches_per_stage(ss, orc):
         assert k == len(cl.points)
         assert np.array_equal(outs[0]["points"][i][:k], cl.points.astype(np.float32))
         assert np.array_equal(outs[0]["colors"][i][:k], cl.colors)
+
+
+def _random_params(rng):
+    """One seeded draw over every StereoParams field the validator accepts,
+    including smoothing radii that take the generic gather (R != 15) and the
+    global-memory gather (tile too large for shared memory), eta <= 0,
+    min_zncc <= 0 and zero cleanup / refine iterations."""
+    d_min = int(rng.integers(-12, 6))
+    return dict(window=int(rng.choice([3, 5, 7, 9, 11, 13])), d_min=d_min,
+                d_max=d_min + int(rng.integers(3, 41)),
+                neighbor_jump_threshold=float(rng.choice([0.5, 1.0, 2.5, 6.0])),
+                outlier_radius_start=int(rng.integers(1, 16)),
+                outlier_radius_step=int(rng.integers(1, 13)),
+                cleanup_iterations=int(rng.integers(0, 5)),
+                fill_radius_radial=int(rng.integers(1, 61)),
+                fill_radius_disc=int(rng.integers(1, 26)),
+                smoothing_radius=int(rng.choice([1, 4, 15, 15, 16, 31, 33, 70, 120])),
+                alpha=float(rng.choice([0.0, 0.1, 0.35, 1.0])),
+                eta_smooth=float(rng.choice([-0.02, 0.0, 0.01, 0.05])),
+                refine_iterations=int(rng.integers(0, 5)),
+                min_zncc=float(rng.choice([-0.5, 0.0, 0.3, 0.5, 0.9])))
+
+
+@pytest.mark.parametrize("seed", range(36))
+def test_random_parameter_sets(ss, orc, seed):
+    """Every stage bit-exact to the oracle under a random parameter set
+    (params.hpp:7-24 fields) and a ragged image size, stage-isolated: WTA,
+    cleanup, refine."""
+    from paper_2007_12623_b200.synth import stereo_pair
+    rng = np.random.default_rng(1000 + seed)
+    p = _random_params(rng)
+    kind = "lowtex" if seed % 3 == 0 else "textured"
+    w, h = [(144, 88), (97, 61), (300, 40), (33, 150)][seed % 4]
+    L, R, _ = stereo_pair(kind, w, h, 24, seed=seed)
+    R = np.roll(R, -p["d_min"] // 2, axis=1)
+    want = orc.compute_disparity(L, R, p)
+    assert_map_equal(ss.compute_disparity(L, R, p), want, f"WTA {p}")
+    wc = orc.cleanup_pass(*want, p)
+    assert_map_equal(ss.cleanup_pass(*want, p), wc, f"cleanup {p}")
+    assert_map_equal(ss.refine_disparities(*wc, L, R, p), orc.refine_disparities(*wc, L, R, p),
+                     f"refine {p}")
+
+
+@pytest.mark.parametrize("seed", [3, 7])
+def test_batch_api_random_params(ss, orc, seed):
+    """The fused batch chain (one context, frames in one launch) under a
+    random parameter set equals the oracle's per-stage chain per frame."""
+    from paper_2007_12623_b200.synth import as_rgb, default_rig, stereo_pair
+    rng = np.random.default_rng(2000 + seed)
+    p = _random_params(rng)
+    W, H, n = 200, 120, 3
+    pairs = [stereo_pair("textured", W, H, 24, seed=seed * 10 + i) for i in range(n)]
+    Ls = np.stack([as_rgb(a) for a, _, _ in pairs])
+    Rs = np.stack([as_rgb(b) for _, b, _ in pairs])
+    ctx = ss.StereoContext(0, W, H, n, ss.StereoParams(**p), ss.StereoRig(**default_rig(W, H)))
+    out = ctx.run(Ls, Rs, ss.SS_OUT_DISPARITY)
+    ctx.close()
+    for i, (L, R, _) in enumerate(pairs):
+        d, v = orc.refine_disparities(*orc.cleanup_pass(*orc.compute_disparity(L, R, p), p),
+                                      L, R, p)
+        assert_map_equal((out["disparity"][i], out["valid"][i]), (d, v), f"frame {i} {p}")
