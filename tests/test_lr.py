@@ -137,3 +137,22 @@ def test_gpu_batch_chain_with_lr(ss, orc):
         d, v = orc.cleanup_pass(d, v, p)
         d, v = orc.refine_disparities(d, v, L, R, p)
         assert _eq(out["valid"][i], v) and _eq(out["disparity"][i], d), f"frame {i}"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(12))
+def test_gpu_lr_random_params(ss, orc, seed):
+    """Random window / disparity range (negative included) / min_zncc /
+    max_diff and ragged sizes: both views and the checked map bit-exact."""
+    rng = np.random.default_rng(300 + seed)
+    d_min = int(rng.integers(-10, 6))
+    p = params_for(24, window=int(rng.choice([3, 5, 7, 9, 11, 13])), d_min=d_min,
+                   d_max=d_min + int(rng.integers(3, 41)),
+                   min_zncc=float(rng.choice([-0.5, 0.0, 0.5, 0.9])))
+    W, H = [(150, 90), (97, 61), (40, 33)][seed % 3]
+    L, R, _ = stereo_pair("lowtex" if seed % 2 else "textured", W, H, 24, seed=seed)
+    md = int(rng.integers(0, 4))
+    got = ss.compute_disparity_lr(L, R, p, max_diff=md)
+    want = orc.compute_disparity_lr(L, R, p, max_diff=md)
+    for g, w, what in zip(got, want, ["disp", "valid", "right disp", "right valid"]):
+        assert _eq(g, w), f"{p} max_diff={md}: {what} differs"
