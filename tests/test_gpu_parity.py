@@ -389,3 +389,32 @@ def test_batch_api_random_params(ss, orc, seed):
         d, v = orc.refine_disparities(*orc.cleanup_pass(*orc.compute_disparity(L, R, p), p),
                                       L, R, p)
         assert_map_equal((out["disparity"][i], out["valid"][i]), (d, v), f"frame {i} {p}")
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_cloud_random_rigs(ss, orc, seed):
+    """Back-projection under random intrinsics / baselines and disparity
+    fields with negative, zero and tiny values (cloud.cpp:43-60 skips d <= 0):
+    index, points, colours bit-exact; normals within 1e-3 rad where the
+    oracle's eigen gap >= 1e-3."""
+    from paper_2007_12623_b200.synth import as_rgb, params_for, stereo_pair
+    rng = np.random.default_rng(600 + seed)
+    W, H = [(200, 120), (97, 61), (64, 150)][seed % 3]
+    L, R, _ = stereo_pair("textured", W, H, 24, seed=seed)
+    p = params_for(24, d_min=-4)
+    d, v = orc.refine_disparities(*orc.cleanup_pass(*orc.compute_disparity(L, R, p), p), L, R, p)
+    d = d.copy()
+    d[rng.random(d.shape) < 0.02] = 0.0
+    d[rng.random(d.shape) < 0.01] = 1e-6
+    rig = dict(fx=float(rng.uniform(200, 3000)), fy=float(rng.uniform(200, 3000)),
+               cx=float(rng.uniform(0, W - 1)), cy=float(rng.uniform(0, H - 1)),
+               width=W, height=H, baseline_mm=float(rng.uniform(0.5, 120)))
+    rgb = as_rgb(L)
+    want = orc.disparity_to_cloud(d, v, rgb, rig)
+    got = ss.disparity_to_cloud(d, v, rgb, rig)
+    assert np.array_equal(got.index, want.index)
+    assert np.array_equal(bits(got.points), bits(want.points))
+    assert np.array_equal(got.colors, want.colors) and np.array_equal(got.pixels, want.pixels)
+    ang = np.arccos(np.clip(np.abs(np.sum(got.normals * want.normals, axis=1)), 0, 1))
+    ok = want.eigen_gap >= 1e-3
+    assert np.all(ang[ok] <= 1e-3), f"max normal angle {ang[ok].max()}"
