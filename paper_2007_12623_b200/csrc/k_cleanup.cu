@@ -72,7 +72,7 @@ __device__ __forceinline__ bool run_ok(const uint32_t* __restrict__ line, int p,
 __global__ void __launch_bounds__(256)
     k_edge_bits(const float* __restrict__ din, const uint8_t* __restrict__ vin,
                 uint32_t* __restrict__ emap, int W, int H, double thr, long stride, long fw) {
-  __shared__ float td[34][33];     // rows v0-1 .. v0+32, columns u0 .. u0+32
+  __shared__ double td[34][33];    // rows v0-1 .. v0+32, columns u0 .. u0+32 (widened once)
   __shared__ uint32_t tv[34][33];  // validity (words: no byte bank conflicts)
   __shared__ uint32_t eb[32][34];  // per pixel: bit0 E_h, bit1 E_v, bit2 E_d1, bit3 E_d2
   const long f = blockIdx.z;
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256)
   for (int r = wy; r < 34; r += 8)
     for (int c = lane; c < 33; c += 32) {
       const int v = v0 - 1 + r, u = u0 + c;
-      float x = 0.f;
+      double x = 0.0;
       uint32_t m = 0;
       if (v >= 0 && v < H && u < W) {
         const long i = f * stride + (long)v * W + u;
@@ -95,8 +95,7 @@ __global__ void __launch_bounds__(256)
   // smooth edge from cell (r, c) to (r2, c2): both valid, |d2 - d| <= thr in
   // double (cleanup.cpp:29-30; NaN compares false, as there)
   auto E = [&](int r, int c, int r2, int c2) -> unsigned {
-    return (tv[r][c] & tv[r2][c2]) &&
-                   !(fabs((double)td[r2][c2] - (double)td[r][c]) > thr)
+    return (tv[r][c] & tv[r2][c2]) && !(fabs(td[r2][c2] - td[r][c]) > thr)
                ? 1u
                : 0u;
   };
