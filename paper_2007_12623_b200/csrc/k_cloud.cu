@@ -273,9 +273,12 @@ constexpr int kNIX = kNTX + 2 * kNW, kNIY = kNTY + 2 * kNW;  // input tile (38 x
 constexpr int kNQ = 10;             // window moments: n, sx, sy, sz, sxx, sxy, sxz, syy, syz, szz
 constexpr int kNSeg = 2;            // output columns per horizontal running-sum task
 
+constexpr int kNVSeg = 4;           // output rows per vertical running-sum task
+
 struct NormalSmem {
   double p[4][kNIY][kNIX];    // per input pixel: point flag (1/0), x, y, z (0 where no point)
   double h[kNQ][kNIY][kNTX];  // 7-wide horizontal window sums of the kNQ quantities
+  double m[kNQ][kNTY][kNTX];  // 7x7 window sums (vertical running sums of h)
 };
 
 // Normals from 7x7 window moments (cloud.cpp:41-90). The window's point count,
@@ -298,15 +301,27 @@ __global__ void __launch_bounds__(kNTX * kNTY, 2)
   pts4 += f * stride;
   const int bx = blockIdx.x * kNTX, by = blockIdx.y * kNTY;
   const int tid = threadIdx.y * kNTX + threadIdx.x;
-  for (int t = tid; t < kNIY * kNIX; t += kNTX * kNTY) {
+  // all of a thread's tile loads are issued before the first store
+  constexpr int kLoads = (kNIY * kNIX + kNTX * kNTY - 1) / (kNTX * kNTY);
+  float4 pl[kLoads];
+#pragma unroll
+  for (int j = 0; j < kLoads; ++j) {
+    const int t = tid + j * kNTX * kNTY;
     const int ty = t / kNIX, tx = t - ty * kNIX;
     const int gx = bx + tx - kNW, gy = by + ty - kNW;
-    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (gx >= 0 && gx < W && gy >= 0 && gy < H) p = pts4[(long)gy * W + gx];
-    S.p[0][ty][tx] = p.w != 0.f ? 1.0 : 0.0;
-    S.p[1][ty][tx] = p.x;
-    S.p[2][ty][tx] = p.y;
-    S.p[3][ty][tx] = p.z;
+    pl[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t < kNIY * kNIX && gx >= 0 && gx < W && gy >= 0 && gy < H)
+      pl[j] = pts4[(long)gy * W + gx];
+  }
+#pragma unroll
+  for (int j = 0; j < kLoads; ++j) {
+    const int t = tid + j * kNTX * kNTY;
+    if (t >= kNIY * kNIX) break;
+    const int ty = t / kNIX, tx = t - ty * kNIX;
+    S.p[0][ty][tx] = pl[j].w != 0.f ? 1.0 : 0.0;
+    S.p[1][ty][tx] = pl[j].x;
+    S.p[2][ty][tx] = pl[j].y;
+    S.p[3][ty][tx] = pl[j].z;
   }
   __syncthreads();
   // horizontal: task = (input row, kNSeg output columns); the 10 quantities of
@@ -352,19 +367,29 @@ __global__ void __launch_bounds__(kNTX * kNTY, 2)
     }
   }
   __syncthreads();
+  // vertical: task = (quantity, column, kNVSeg output rows), a 7-high running sum
+  constexpr int kVSegs = kNTY / kNVSeg;
+  for (int t = tid; t < kNQ * kNTX * kVSegs; t += kNTX * kNTY) {
+    const int col = t % kNTX, qs = t / kNTX, q = qs / kVSegs, r0 = (qs % kVSegs) * kNVSeg;
+    double acc = 0.0;
+#pragma unroll
+    for (int dv = 0; dv <= 2 * kNW; ++dv) acc += S.h[q][r0 + dv][col];
+    S.m[q][r0][col] = acc;
+#pragma unroll
+    for (int j = 1; j < kNVSeg; ++j) {
+      acc += S.h[q][r0 + j + 2 * kNW][col] - S.h[q][r0 + j - 1][col];
+      S.m[q][r0 + j][col] = acc;
+    }
+  }
+  __syncthreads();
   const int u = bx + threadIdx.x, v = by + threadIdx.y;
   if (u >= W || v >= H) return;
-  const float4 c = pts4[(long)v * W + u];
-  if (c.w == 0.f) return;
+  const int cy = threadIdx.y + kNW, cx = threadIdx.x + kNW;
+  if (S.p[0][cy][cx] == 0.0) return;
   const int k = index[f * stride + (long)v * W + u];
   double m[kNQ];
 #pragma unroll
-  for (int q = 0; q < kNQ; ++q) {
-    double acc = 0.0;
-#pragma unroll
-    for (int dv = 0; dv <= 2 * kNW; ++dv) acc += S.h[q][threadIdx.y + dv][threadIdx.x];
-    m[q] = acc;
-  }
+  for (int q = 0; q < kNQ; ++q) m[q] = S.m[q][threadIdx.y][threadIdx.x];
   const int count = (int)m[0];
   float n[3] = {0.f, 0.f, -1.f};
   bool fitted = false;
@@ -441,7 +466,7 @@ __global__ void __launch_bounds__(kNTX * kNTY, 2)
     }
   }
   double nd[3] = {n[0], n[1], n[2]};
-  const double pc[3] = {c.x, c.y, c.z};
+  const double pc[3] = {S.p[1][cy][cx], S.p[2][cy][cx], S.p[3][cy][cx]};
   if (!fitted) {
     const double len = sqrt(pc[0] * pc[0] + pc[1] * pc[1] + pc[2] * pc[2]);
     nd[0] = -pc[0] / len;
