@@ -204,6 +204,9 @@ void launch_cloud_points(const float* disp, const int* index, const uint8_t* rgb
 // trigonometric eigenvalues, eigenvector from the best-conditioned cross
 // product of two rows of (A - l0 I). T = float on the fast path, double for
 // the near-degenerate re-check.
+__device__ __forceinline__ void sincos_t(float x, float* s, float* c) { sincosf(x, s, c); }
+__device__ __forceinline__ void sincos_t(double x, double* s, double* c) { sincos(x, s, c); }
+
 template <typename T>
 __device__ void sym3_smallest(const T a[6], T ev[3], T n[3]) {
   const T a00 = a[0], a01 = a[1], a02 = a[2], a11 = a[3], a12 = a[4], a22 = a[5];
@@ -233,8 +236,11 @@ __device__ void sym3_smallest(const T a[6], T ev[3], T n[3]) {
   T r = det / (T(2) * p * p * p);
   r = r < T(-1) ? T(-1) : (r > T(1) ? T(1) : r);
   const T phi = acos(r) / T(3);
-  const T e2 = q + T(2) * p * cos(phi);
-  const T e0 = q + T(2) * p * cos(phi + T(2.0943951023931954923));  // + 2 pi / 3
+  T sp, cp;
+  sincos_t(phi, &sp, &cp);
+  const T e2 = q + T(2) * p * cp;
+  // cos(phi + 2 pi / 3) = -(cos phi + sqrt(3) sin phi) / 2
+  const T e0 = q - p * (cp + T(1.7320508075688772935) * sp);
   const T e1 = T(3) * q - e0 - e2;
   ev[0] = e0;
   ev[1] = e1;
@@ -416,11 +422,12 @@ __global__ void __launch_bounds__(kNTX * kNTY, 2)
       const double x0 = c00 * e[0] + c01 * e[1] + c02 * e[2];
       const double x1 = c01 * e[0] + c11 * e[1] + c12 * e[2];
       const double x2 = c02 * e[0] + c12 * e[1] + c22 * e[2];
-      const double len = sqrt(x0 * x0 + x1 * x1 + x2 * x2);
-      if (len > 0.0 && isfinite(len)) {
-        n[0] = (float)(x0 / len);
-        n[1] = (float)(x1 / len);
-        n[2] = (float)(x2 / len);
+      const double len2 = x0 * x0 + x1 * x1 + x2 * x2;
+      if (len2 > 0.0 && isfinite(len2)) {
+        const double rl = rsqrt(len2);  // the normal is stored in FP32
+        n[0] = (float)(x0 * rl);
+        n[1] = (float)(x1 * rl);
+        n[2] = (float)(x2 * rl);
       } else {
         n[0] = e[0];
         n[1] = e[1];
