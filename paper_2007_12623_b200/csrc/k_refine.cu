@@ -556,16 +556,38 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
     // rounds once where M16 + (eta df) df rounded twice, inside the same bar.
     float best_cost = INFINITY, second = INFINITY;
     const int nk = c_hi - c_lo;
+    // Candidate costs two at a time on the packed FP32 pipe (FADD2 / FMUL2 /
+    // FFMA2: per-lane IEEE ops, the same values as the scalar expressions
+    // (c - dv_f) and fma(eta df, df, M16)).
+    float cost[kMaxCand + 1];
+    const float cf = (float)c_lo;
+#pragma unroll
+    for (int k = 0; k < kMaxCand; k += 2) {
+      float mk[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kk = k + h;
+        if (kk >= kMaxCand) {
+          mk[h] = 0.f;
+          continue;
+        }
+        const uint32_t hw = (kk & 1) ? __byte_perm(wd[kk >> 1], wd[min(kk + 1, 11) >> 1], sel_o)
+                                     : __byte_perm(wd[kk >> 1], 0u, sel_e);
+        mk[h] = __half2float(__ushort_as_half((unsigned short)(hw & 0xFFFFu)));
+      }
+      const float2 c2 = __fadd2_rn(make_float2(cf, cf), make_float2((float)k, (float)(k + 1)));
+      const float2 df = __fadd2_rn(c2, make_float2(-dv_f, -dv_f));
+      const float2 e = __fmul2_rn(make_float2(a.eta_f, a.eta_f), df);
+      const float2 c = __ffma2_rn(e, df, make_float2(mk[0], mk[1]));
+      cost[k] = c.x;
+      cost[k + 1] = c.y;
+    }
 #pragma unroll
     for (int k = 0; k < kMaxCand; ++k) {
-      const uint32_t hw = (k & 1) ? __byte_perm(wd[k >> 1], wd[(k + 1) >> 1], sel_o)
-                                  : __byte_perm(wd[k >> 1], 0u, sel_e);
-      const float m = __half2float(__ushort_as_half((unsigned short)(hw & 0xFFFFu)));
-      const float df = (float)((float)c_lo + (float)k) - dv_f;
-      const float cost = k <= nk ? __fmaf_rn(__fmul_rn(a.eta_f, df), df, m) : INFINITY;
-      second = fminf(second, fmaxf(best_cost, cost));
-      best = cost < best_cost ? c_lo + k : best;
-      best_cost = fminf(best_cost, cost);
+      const float ck = k <= nk ? cost[k] : INFINITY;
+      second = fminf(second, fmaxf(best_cost, ck));
+      best = ck < best_cost ? c_lo + k : best;
+      best_cost = fminf(best_cost, ck);
     }
     if (second * (1.f - kEps) - errE > best_cost * (1.f + kEps) + errE) return best;
     // Ambiguous: FP64 costs (exact E, exact clamped/undefined M) with error
