@@ -45,12 +45,20 @@ def _newer(target, sources):
     return any(os.path.getmtime(s) > t for s in sources)
 
 
+# Translation units whose only FP32/FP64 arithmetic outside explicit rounding
+# intrinsics is tolerance-checked (the normal fit): FMA contraction allowed.
+FMAD_OK = {"k_cloud.cu"}
+
+
 def _compile(src):
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-    if _newer(obj, [src] + _deps()):
-        cmd = [NVCC] + COMMON + ["-c", src, "-o", obj]
+    if _newer(obj, [src] + _deps() + [__file__]):
+        flags = COMMON
+        if os.path.basename(src) in FMAD_OK:
+            flags = [f for f in COMMON if f != "--fmad=false"] + ["--fmad=true"]
+        cmd = [NVCC] + flags + ["-c", src, "-o", obj]
         if src.endswith(".cpp"):
-            cmd = [NVCC] + COMMON + ["-x", "cu", "-c", src, "-o", obj]
+            cmd = [NVCC] + flags + ["-x", "cu", "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
