@@ -274,6 +274,14 @@ ss_status ss_stereo_batch(ss_ctx* ctx, int32_t n, int32_t w, int32_t h, int32_t 
                           const uint8_t* left, const uint8_t* right, uint32_t out_flags,
                           const ss_batch_out* out);
 
+/* One pair through the whole chain (the fused per-frame entry of SURVEY.md
+ * §8b): host buffers in and out, on the calling thread's lazily created
+ * per-device context, synchronous. Equal to a one-frame ss_stereo_batch with
+ * the same params / rig (rig may be NULL without SS_OUT_CLOUD / _NORMALS). */
+ss_status ss_stereo_frame(const ss_stereo_params* p, const ss_stereo_rig* rig, int32_t w,
+                          int32_t h, int32_t in_format, const uint8_t* left,
+                          const uint8_t* right, uint32_t out_flags, const ss_batch_out* out);
+
 /* Same with DEVICE inputs/outputs; asynchronous on `stream` (NULL = ctx
  * stream). Output device pointers may be NULL to keep results in the ctx's
  * own buffers (see ss_ctx_device_outputs). */

@@ -25,6 +25,7 @@ from .stereo import (  # noqa: F401
     pinned_empty,
     refine_disparities,
     remove_outliers,
+    stereo_frame,
     to_gray,
 )
 from . import features, fusion  # noqa: F401

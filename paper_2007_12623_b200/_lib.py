@@ -104,6 +104,8 @@ def lib():
         "ss_ctx_get_stats": (i32, [vp, P(SsCtxStats)]),
         "ss_ctx_reset_stats": (i32, [vp]),
         "ss_stereo_batch": (i32, [vp, i32, i32, i32, i32, vp, vp, C.c_uint32, P(SsBatchOut)]),
+        "ss_stereo_frame": (i32, [P(SsParams), P(SsRig), i32, i32, i32, vp, vp,
+                                  C.c_uint32, P(SsBatchOut)]),
         "ss_stereo_batch_device": (i32, [vp, i32, i32, i32, i32, vp, vp, C.c_uint32,
                                          P(SsBatchOut), vp]),
         "ss_ctx_device_outputs": (i32, [vp, P(SsBatchOut)]),

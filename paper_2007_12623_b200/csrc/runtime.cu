@@ -1470,6 +1470,25 @@ ss_status ss_stereo_batch_device(ss_ctx* ctx, int32_t n, int32_t w, int32_t h,
   });
 }
 
+ss_status ss_stereo_frame(const ss_stereo_params* p, const ss_stereo_rig* rig, int32_t w,
+                          int32_t h, int32_t in_format, const uint8_t* left,
+                          const uint8_t* right, uint32_t out_flags, const ss_batch_out* out) {
+  ss_ctx* c = nullptr;
+  const ss_status st = guarded([&] {
+    if (!p || !out) raise(SS_EINVAL, "ss_stereo_frame: null params or outputs");
+    validate_params(p);
+    if (rig) validate_rig(rig);
+    c = thread_ctx();
+    c->params = *p;
+    c->has_rig = rig != nullptr;
+    if (rig) c->rig = *rig;
+    c->lr_check = false;
+    c->max_batch = 1;
+  });
+  if (st != SS_OK) return st;
+  return ss_stereo_batch(c, 1, w, h, in_format, left, right, out_flags, out);
+}
+
 ss_status ss_ctx_device_outputs(ss_ctx* ctx, ss_batch_out* o) {
   return guarded([&] {
     o->disparity = ctx->last_disp;

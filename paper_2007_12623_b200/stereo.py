@@ -377,6 +377,22 @@ class StereoMulti:
         return out
 
 
+def stereo_frame(left, right, params=None, rig=None, out_flags=L.SS_OUT_DISPARITY):
+    """One pair through the whole chain (ss_stereo_frame): host arrays in, a
+    dict of host arrays out (the keys of StereoContext.alloc_outputs, frame
+    axis of length 1)."""
+    left, right = np.ascontiguousarray(left), np.ascontiguousarray(right)
+    in_format = L.SS_IN_RGB if left.ndim == 3 else L.SS_IN_GRAY
+    h, w = left.shape[:2]
+    out = StereoContext.alloc_outputs(1, h, w, out_flags)
+    bo = L.SsBatchOut(*[_ptr(out.get(k)) if out.get(k) is not None else None
+                        for k, _ in L.SsBatchOut._fields_])
+    r = C.byref(_rig(rig)) if rig is not None else None
+    _check(L.lib().ss_stereo_frame(C.byref(_params(params)), r, w, h, in_format, _ptr(left),
+                                   _ptr(right), out_flags, C.byref(bo)))
+    return out
+
+
 def pinned_empty(shape, dtype):
     """numpy array backed by pinned (page-locked) host memory."""
     dtype = np.dtype(dtype)

@@ -418,3 +418,26 @@ def test_cloud_random_rigs(ss, orc, seed):
     ang = np.arccos(np.clip(np.abs(np.sum(got.normals * want.normals, axis=1)), 0, 1))
     ok = want.eigen_gap >= 1e-3
     assert np.all(ang[ok] <= 1e-3), f"max normal angle {ang[ok].max()}"
+
+
+def test_stereo_frame_entry(ss, orc):
+    """ss_stereo_frame (the fused per-frame entry): the
+    oracle's chain for one pair, with and without a rig; a cloud request
+    without a rig fails like the batch API."""
+    from paper_2007_12623_b200.synth import as_rgb, default_rig, params_for, stereo_pair
+    W, H, D = 200, 120, 24
+    L, R, _ = stereo_pair("textured", W, H, D, seed=31)
+    p = params_for(D)
+    d, v = orc.refine_disparities(*orc.cleanup_pass(*orc.compute_disparity(L, R, p), p), L, R, p)
+    out = ss.stereo_frame(as_rgb(L), as_rgb(R), ss.StereoParams(**p))
+    assert_map_equal((out["disparity"][0], out["valid"][0]), (d, v), "stereo_frame")
+    rig = default_rig(W, H)
+    flags = ss.SS_OUT_DISPARITY | ss.SS_OUT_CLOUD | ss.SS_OUT_NORMALS
+    out = ss.stereo_frame(L, R, ss.StereoParams(**p), ss.StereoRig(**rig), flags)
+    assert_map_equal((out["disparity"][0], out["valid"][0]), (d, v), "stereo_frame gray")
+    cl = orc.disparity_to_cloud(d, v, as_rgb(L), rig)
+    k = out["n_points"][0]
+    assert k == len(cl.points)
+    assert np.array_equal(out["points"][0][:k], cl.points.astype(np.float32))
+    with pytest.raises(ss.InvalidArgument):
+        ss.stereo_frame(L, R, ss.StereoParams(**p), None, flags)
