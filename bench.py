@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--no-extensions", action="store_true",
                     help="skip the LR-check / feature side measurements")
     ap.add_argument("--cpu-pairs", type=int, default=2)
+    ap.add_argument("--cpu-configs", action="store_true",
+                    help="also time the reference CPU chain on C1/C2/C3 (median of 3; minutes)")
     return ap.parse_args()
 
 
@@ -143,16 +145,17 @@ def make_frames(rank, world, frames, unique):
     return np.tile(Ls, (reps, 1, 1, 1))[:frames], np.tile(Rs, (reps, 1, 1, 1))[:frames]
 
 
-def reference_chain(pairs):
+def reference_chain(pairs, Wc=None, Hc=None, Dc=None):
     """The reference's own CPU path (oracle/_ref) on host pairs; cloud stage from
     the restatement (the reference's needs Eigen, absent). Returns seconds."""
+    Wc, Hc, Dc = Wc or W, Hc or H, Dc or D
     from oracle.oracle import Oracle
     from paper_2007_12623_b200.synth import default_rig, params_for
     kind = "reference" if Oracle.available("ref") else "port"
     ref = Oracle("ref" if kind == "reference" else "orc")
     orc = Oracle("orc")
-    p = params_for(D)
-    rig = default_rig(W, H)
+    p = params_for(Dc)
+    rig = default_rig(Wc, Hc)
     t0 = time.perf_counter()
     for L, R in pairs:
         lg, rg = ref.to_gray(L), ref.to_gray(R)
@@ -232,6 +235,60 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def geometry_throughput(ss, kind, Wf, Hf, Df, nf, Bf, nctx):
+    """Device-resident pairs/s of the full chain (incl. normals) for one
+    synthetic geometry: nf pairs (6 seeded, tiled) in HBM, batches of Bf
+    spread over nctx contexts; host wall clock around synchronous batches."""
+    import torch
+    from paper_2007_12623_b200.synth import as_rgb, default_rig, params_for, stereo_pair
+    uniq = [stereo_pair(kind, Wf, Hf, Df, seed=100 + i)[:2] for i in range(6)]
+    Lf = torch.from_numpy(np.stack([as_rgb(uniq[i % 6][0]) for i in range(nf)])).cuda()
+    Rf = torch.from_numpy(np.stack([as_rgb(uniq[i % 6][1]) for i in range(nf)])).cuda()
+    pf = ss.StereoParams(**params_for(Df))
+    rf = ss.StereoRig(**default_rig(Wf, Hf))
+    cf = [ss.StereoContext(torch.cuda.current_device(), Wf, Hf, Bf, pf, rf) for _ in range(nctx)]
+    flags = ss.SS_OUT_DISPARITY | ss.SS_OUT_CLOUD | ss.SS_OUT_NORMALS
+
+    def run():
+        for i, f0 in enumerate(range(0, nf, Bf)):
+            cf[i % nctx].run_device(Bf, Wf, Hf, Lf[f0].data_ptr(), Rf[f0].data_ptr(), flags)
+        for c in cf:
+            c.sync()
+
+    run()  # warm (allocations)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    run()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    for c in cf:
+        c.close()
+    return {"value": nf / dt, "unit": "pairs/s", "ms_per_pair": 1000 * dt / nf,
+            "workload": f"{nf} synthetic {kind} {Wf}x{Hf} pairs, D={Df} (d 0..{Df - 1}), "
+                        f"full chain incl. normals, {nctx} contexts, inputs in HBM",
+            "timing": "host wall clock around synchronous batches"}
+
+
+def cpu_side_by_side(runs=3):
+    """SURVEY.md §8d CPU side-by-side: the reference chain (oracle/_ref) on one
+    pair of each of C1, C2 and C3, median of `runs`, all host cores; C1 also
+    on one thread. Seconds of host time: opt-in (--cpu-configs)."""
+    from paper_2007_12623_b200.synth import as_rgb, stereo_pair
+    out = {"cores": os.cpu_count(), "cpu_model": cpu_model(), "runs": runs}
+    for key, kind, Wc, Hc, Dc in (("C1", "textured", 960, 540, 64), ("C2", "lowtex", 960, 540, 64),
+                                  ("C3", "textured", 1920, 1080, 128)):
+        L, R, _ = stereo_pair(kind, Wc, Hc, Dc, seed=1234)
+        pair = [(as_rgb(L), as_rgb(R))]
+        ts = [reference_chain(pair, Wc, Hc, Dc)[0] for _ in range(runs)]
+        out[key] = {"pairs_per_s": 1.0 / statistics.median(ts), "median_s": statistics.median(ts)}
+    L, R, _ = stereo_pair("textured", 960, 540, 64, seed=1234)
+    omp_threads(1)
+    ts = [reference_chain([(as_rgb(L), as_rgb(R))])[0] for _ in range(runs)]
+    omp_threads(os.cpu_count())
+    out["C1"]["pairs_per_s_1thread"] = 1.0 / statistics.median(ts)
+    return out
+
+
 def extensions(ss, ctxs, step_device, barrier, stream, F, Lh_first, Rh_first, od=None):
     """Side measurements of the SURVEY §8f rows (not the headline metric):
     the chain with the opt-in LR check (device pairs/s, same workload), and
@@ -291,40 +348,15 @@ def extensions(ss, ctxs, step_device, barrier, stream, F, Lh_first, Rh_first, od
                          "note": "fuse_device of C1 clouds (~0.5 M points each) into one model; "
                                  "host wall clock around synchronous calls"}
         model.close()
-    # C3 / C5 geometry (BASELINE.json configs[2], [4]): 1920x1080, D = 128,
-    # device-resident throughput over 48 synthetic pairs (6 seeded, tiled)
-    try:
-        from paper_2007_12623_b200.synth import as_rgb, default_rig, params_for, stereo_pair
-        Wf, Hf, Df, nf, Bf = 1920, 1080, 128, 48, 8
-        uniq = [stereo_pair("textured", Wf, Hf, Df, seed=100 + i)[:2] for i in range(6)]
-        Lf = torch.from_numpy(np.stack([as_rgb(uniq[i % 6][0]) for i in range(nf)])).cuda()
-        Rf = torch.from_numpy(np.stack([as_rgb(uniq[i % 6][1]) for i in range(nf)])).cuda()
-        pf = ss.StereoParams(**params_for(Df))
-        rf = ss.StereoRig(**default_rig(Wf, Hf))
-        cf = [ss.StereoContext(torch.cuda.current_device(), Wf, Hf, Bf, pf, rf) for _ in range(2)]
-        flags = ss.SS_OUT_DISPARITY | ss.SS_OUT_CLOUD | ss.SS_OUT_NORMALS
-
-        def run_fhd():
-            for i, f0 in enumerate(range(0, nf, Bf)):
-                cf[i % 2].run_device(Bf, Wf, Hf, Lf[f0].data_ptr(), Rf[f0].data_ptr(), flags)
-            for c in cf:
-                c.sync()
-
-        run_fhd()  # warm (allocations)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        run_fhd()
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        out["fhd_d128"] = {"value": nf / dt, "unit": "pairs/s", "ms_per_pair": 1000 * dt / nf,
-                           "workload": "48 synthetic textured 1920x1080 pairs, D=128 (d 0..127), "
-                                       "full chain incl. normals, 2 contexts, inputs in HBM",
-                           "timing": "host wall clock around synchronous batches"}
-        for c in cf:
-            c.close()
-        del Lf, Rf
-    except Exception as e:  # informational side measurement
-        out["fhd_d128"] = {"error": str(e)[:200]}
+    # C3 / C5 geometry (BASELINE.json configs[2], [4]): 1920x1080, D = 128; and
+    # C2 (960x540 low-texture, D = 64): device-resident throughput over
+    # synthetic pairs (6 seeded, tiled)
+    for key, kind, Wf, Hf, Df, nf, Bf, nctx in (("fhd_d128", "textured", 1920, 1080, 128, 48, 8, 2),
+                                                ("lowtex_c2", "lowtex", 960, 540, 64, 128, 16, 4)):
+        try:
+            out[key] = geometry_throughput(ss, kind, Wf, Hf, Df, nf, Bf, nctx)
+        except Exception as e:  # informational side measurement
+            out[key] = {"error": str(e)[:200]}
     gl = ss.to_gray(Lh_first)
     gr = ss.to_gray(Rh_first)
 
@@ -546,6 +578,8 @@ def run_ours(args):
             t1, _ = reference_chain(pairs_cpu[:1])
             cpu["single_thread_value"] = 1.0 / t1
             omp_threads(os.cpu_count())
+    if cpu is not None and args.cpu_configs:
+        cpu["side_by_side"] = cpu_side_by_side()
     stage_ms_per_pair = {k: v[0] / frames_timed for k, v in stages.items()}
     ext = None if (args.no_extensions or world > 1) else extensions(ss, ctxs, step_device, barrier, stream, F,
                                                      Lh_first=Lh[0].numpy(), Rh_first=Rh[0].numpy(),

@@ -297,7 +297,7 @@ struct NormalSmem {
 // entries) and solved in FP32 (closed-form eigenpairs); windows whose middle
 // eigenvalue is within 1e-4 of degenerate are re-fitted from FP64 points so
 // the reference's 1e-9 acceptance test (cloud.cpp:81) decides them.
-__global__ void __launch_bounds__(kNTX * kNTY, 2)
+__global__ void __launch_bounds__(kNTX * kNTY, 3)
     k_cloud_normals(const float4* __restrict__ pts4, const float* __restrict__ disp, int W,
                     int H, CloudArgs cargs, double* __restrict__ nrm_d,
                     float* __restrict__ nrm_f, const int* __restrict__ index, long stride) {
