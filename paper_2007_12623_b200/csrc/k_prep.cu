@@ -153,6 +153,99 @@ __global__ void k_stats(const uint8_t* __restrict__ gray, int2* __restrict__ out
   }
 }
 
+// Window 11 (the default): one thread walks one column down a strip of
+// kStatRows output rows with running sums, so each image row is read once per
+// column (11 byte loads) instead of once per output pixel (61). For output v
+// the chessboard taps are: rows v + odd k use the row's odd-offset taps
+// (du = +-1, +-3, +-5: "Ho"), rows v + even k its even-offset taps (du = 0,
+// +-2, +-4: "He"). With P(r) = Ho(r) | He(r) << 16 (each half <= 6 * 255, so
+// sums of 6 rows never carry) and
+//   PO(v) = sum_{k odd} P(v + k),   PE(v) = sum_{k even} P(v + k),
+// the window sum is lo16(PO) + hi16(PE), and one row down
+//   PO(v + 1) = PE(v) + P(v + 6),   PE(v + 1) = PO(v) - P(v - 5);
+// the squares run the same recurrences on separate Ho / He accumulators.
+// Integer sums: bit-identical to k_stats<5>.
+constexpr int kStatRows = 32;
+constexpr int kStatCols = 128;
+
+__global__ void __launch_bounds__(kStatCols)
+    k_stats_col(const uint8_t* __restrict__ gray, int2* __restrict__ out, int W, int H,
+                int pitch, int pad, long gray_stride, long stat_stride) {
+  constexpr int HALF = 5;
+  __shared__ int3 ring[12][kStatCols];  // P, Qo, Qe of the column's last 12 rows
+  const long f = blockIdx.z;
+  gray += f * gray_stride;
+  out += f * stat_stride;
+  const int x = blockIdx.x * kStatCols + threadIdx.x;
+  if (x >= pitch) return;
+  const int u = x - pad;
+  const int v0 = blockIdx.y * kStatRows, v1 = min(v0 + kStatRows, H);
+  const int2 undef = make_int2(0, 0x7fc00000);
+  const bool col_ok = u >= HALF && u < W - HALF;
+  const int vs = max(v0, HALF), ve = min(v1, H - HALF);  // rows with a fitting window
+  for (int v = v0; v < (col_ok ? min(vs, v1) : v1); ++v) out[(long)v * pitch + x] = undef;
+  if (!col_ok || vs >= ve) {
+    if (col_ok)
+      for (int v = max(vs, ve); v < v1; ++v) out[(long)v * pitch + x] = undef;
+    return;
+  }
+  int3* rc = &ring[0][threadIdx.x];
+  auto row_sums = [&](int r) {  // P, Qo, Qe of image row r at column u
+    const uint8_t* p = gray + (long)r * W + u;
+    int P = 0, qo = 0, qe = 0;
+#pragma unroll
+    for (int du = -HALF; du <= HALF; ++du) {
+      const int a = __ldg(p + du);
+      if (du & 1) {
+        P += a;
+        qo += a * a;
+      } else {
+        P += a << 16;
+        qe += a * a;
+      }
+    }
+    return make_int3(P, qo, qe);
+  };
+  // warm-up: rows vs - 5 .. vs + 5 by parity of k = r - vs
+  int PO = 0, PE = 0, QOo = 0, QEo = 0, QOe = 0, QEe = 0;
+#pragma unroll 1
+  for (int k = -HALF; k <= HALF; ++k) {
+    const int3 s = row_sums(vs + k);
+    rc[((vs + k) % 12) * kStatCols] = s;
+    if (k & 1) {
+      PO += s.x;
+      QOo += s.y;
+      QOe += s.z;
+    } else {
+      PE += s.x;
+      QEo += s.y;
+      QEe += s.z;
+    }
+  }
+#pragma unroll 1
+  for (int v = vs;; ++v) {
+    const int sum = (PO & 0xFFFF) + (int)((unsigned)PE >> 16);
+    const int sq = QOo + QEe;
+    // patch_stats stores int32 (matcher.cpp:132-133)
+    const int32_t var = 61 * sq - sum * sum;
+    int2 r = make_int2(sum, 0x7fc00000);
+    if (var != 0) r.y = __float_as_int((float)(1.0 / sqrt((double)var)));
+    out[(long)v * pitch + x] = r;
+    if (v + 1 >= ve) break;
+    const int3 nw = row_sums(v + HALF + 1);
+    const int3 od = rc[((v - HALF) % 12) * kStatCols];
+    rc[((v + HALF + 1) % 12) * kStatCols] = nw;
+    const int po = PO, qoo = QOo, qoe = QOe;
+    PO = PE + nw.x;
+    QOo = QEo + nw.y;
+    QOe = QEe + nw.z;
+    PE = po - od.x;
+    QEo = qoo - od.y;
+    QEe = qoe - od.z;
+  }
+  for (int v = ve; v < v1; ++v) out[(long)v * pitch + x] = undef;
+}
+
 void launch_stats(const uint8_t* gray, int2* lstat, int2* rstat, int is_right, const Geom& g,
                   int frames, long gray_stride, long stat_stride, cudaStream_t s) {
   if (g.W <= 0 || g.H <= 0 || frames <= 0) return;
@@ -160,10 +253,11 @@ void launch_stats(const uint8_t* gray, int2* lstat, int2* rstat, int is_right, c
   const int pad = is_right ? g.SPAD : 0;
   const int threads = 128;
   dim3 grid((pitch + threads - 1) / threads, g.H, frames);
-  if (g.half == 5)
-    k_stats<5><<<grid, threads, 0, s>>>(gray, is_right ? rstat : lstat, g.W, g.H, g.half, pitch,
-                                        pad, gray_stride, stat_stride);
-  else
+  if (g.half == 5) {
+    dim3 gc((pitch + kStatCols - 1) / kStatCols, (g.H + kStatRows - 1) / kStatRows, frames);
+    k_stats_col<<<gc, kStatCols, 0, s>>>(gray, is_right ? rstat : lstat, g.W, g.H, pitch, pad,
+                                         gray_stride, stat_stride);
+  } else
     k_stats<0><<<grid, threads, 0, s>>>(gray, is_right ? rstat : lstat, g.W, g.H, g.half, pitch,
                                         pad, gray_stride, stat_stride);
 }
