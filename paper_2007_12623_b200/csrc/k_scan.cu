@@ -24,8 +24,6 @@
 namespace ssb {
 
 namespace {
-constexpr int kScanWarps = 4;
-constexpr int kRowsPerWarp = 8;
 constexpr int kChunk = 64;  // columns per TMA chunk
 
 }  // namespace
@@ -232,57 +230,36 @@ void launch_scan_b(const int* soT, const int* cntT, const int* oT, const double*
 
 // ---------------- normal-layout count scan (cleanup disc support) ----------------
 
-__global__ void __launch_bounds__(32 * kScanWarps)
+// Per-row prefix counts of a u8 mask, psum[r][c + 1] = #nonzero in [0, c]
+// (integers, so any order): one warp per row, 32 columns per step by ballot.
+constexpr int kCountWarps = 8;
+
+__global__ void __launch_bounds__(32 * kCountWarps)
     k_row_count(const uint8_t* __restrict__ mask, int* __restrict__ psum, int W, int H,
                 long stride, long pstride) {
-  __shared__ uint8_t mtile[kScanWarps][kRowsPerWarp][33];
-  __shared__ int tile[kScanWarps][kRowsPerWarp][33];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long f = blockIdx.y;
-  const int r0 = (blockIdx.x * kScanWarps + warp) * kRowsPerWarp;
-  if (r0 >= H) return;  // warp-uniform
-  const int nrows = min(kRowsPerWarp, H - r0);
-  mask += f * stride + (long)r0 * W;
-  psum += f * pstride + (long)r0 * (W + 1);
-  uint8_t(*mt)[33] = mtile[warp];
-  int(*tl)[33] = tile[warp];
-  uint8_t nm[kRowsPerWarp];
-  auto load = [&](int c0) {
-    const int c = c0 + lane;
-#pragma unroll
-    for (int rr = 0; rr < kRowsPerWarp; ++rr)
-      nm[rr] = (rr < nrows && c < W) ? __ldg(mask + (long)rr * W + c) : 0;
-  };
-  if (lane < nrows) psum[(long)lane * (W + 1)] = 0;
+  const int r = blockIdx.x * kCountWarps + warp;
+  if (r >= H) return;  // warp-uniform
+  const uint8_t* m = mask + f * stride + (long)r * W;
+  int* ps = psum + f * pstride + (long)r * (W + 1);
+  if (lane == 0) ps[0] = 0;
+  const unsigned below = (1u << lane) - 1u;
   int s = 0;
-  load(0);
   for (int c0 = 0; c0 < W; c0 += 32) {
-    const int cols = min(32, W - c0);
-#pragma unroll
-    for (int rr = 0; rr < kRowsPerWarp; ++rr) mt[rr][lane] = nm[rr];
-    __syncwarp();
-    if (c0 + 32 < W) load(c0 + 32);
-    if (lane < nrows) {
-#pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        if (c >= cols) break;
-        s += mt[lane][c] ? 1 : 0;
-        tl[lane][c] = s;
-      }
-    }
-    __syncwarp();
-    if (lane < cols)
-      for (int rr = 0; rr < nrows; ++rr) psum[(long)rr * (W + 1) + c0 + lane + 1] = tl[rr][lane];
-    __syncwarp();
+    const int c = c0 + lane;
+    const bool on = c < W && __ldg(m + c) != 0;
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, on);
+    if (c < W) ps[c + 1] = s + __popc(b & below) + (on ? 1 : 0);
+    s += __popc(b);
   }
 }
 
 void launch_row_count(const uint8_t* valid, int* pcnt, int W, int H, int frames, long stride,
                       long pstride, cudaStream_t s) {
   if (W <= 0 || H <= 0 || frames <= 0) return;
-  const int rows_per_block = kRowsPerWarp * kScanWarps;
-  k_row_count<<<dim3((H + rows_per_block - 1) / rows_per_block, frames), 32 * kScanWarps, 0,
-                s>>>(valid, pcnt, W, H, stride, pstride);
+  k_row_count<<<dim3((H + kCountWarps - 1) / kCountWarps, frames), 32 * kCountWarps, 0, s>>>(
+      valid, pcnt, W, H, stride, pstride);
 }
 
 }  // namespace ssb
