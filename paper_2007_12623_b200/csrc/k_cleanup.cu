@@ -78,19 +78,33 @@ __global__ void __launch_bounds__(256)
   const long f = blockIdx.z;
   const int u0 = blockIdx.x * 32, v0 = blockIdx.y * 32;
   const int lane = threadIdx.x, wy = threadIdx.y;
-  for (int r = wy; r < 34; r += 8)
-    for (int c = lane; c < 33; c += 32) {
-      const int v = v0 - 1 + r, u = u0 + c;
-      double x = 0.0;
-      uint32_t m = 0;
-      if (v >= 0 && v < H && u < W) {
-        const long i = f * stride + (long)v * W + u;
-        m = vin[i] ? 1u : 0u;
-        x = din[i];
-      }
-      td[r][c] = x;
-      tv[r][c] = m;
+  // cells (r, c): c = lane for r = wy + 8k (k < 5), plus column 32 for the
+  // threads 0..33 — every load issued before the first store
+  constexpr int kCells = 6;
+  float xs[kCells];
+  uint8_t ms[kCells];
+#pragma unroll
+  for (int k = 0; k < kCells; ++k) {
+    const int tid = wy * 32 + lane;
+    const int r = k < 5 ? wy + 8 * k : tid, c = k < 5 ? lane : 32;
+    const int v = v0 - 1 + r, u = u0 + c;
+    xs[k] = 0.f;
+    ms[k] = 0;
+    if (r < 34 && v >= 0 && v < H && u < W) {
+      const long i = f * stride + (long)v * W + u;
+      ms[k] = vin[i];
+      xs[k] = din[i];
     }
+  }
+#pragma unroll
+  for (int k = 0; k < kCells; ++k) {
+    const int tid = wy * 32 + lane;
+    const int r = k < 5 ? wy + 8 * k : tid, c = k < 5 ? lane : 32;
+    if (r < 34) {
+      td[r][c] = (double)xs[k];
+      tv[r][c] = ms[k] ? 1u : 0u;
+    }
+  }
   __syncthreads();
   // smooth edge from cell (r, c) to (r2, c2): both valid, |d2 - d| <= thr in
   // double (cleanup.cpp:29-30; NaN compares false, as there)
@@ -192,16 +206,33 @@ __device__ __forceinline__ void radial_fill_pixel(const float* __restrict__ din,
     for (int dir = 0; dir < 8; ++dir) {
       const double len = dir < 4 ? 1.0 : 1.41421356237309504880;  // M_SQRT2
       const int du = c_dirU[dir], dv = c_dirV[dir];
-      for (int step = 1; step <= radius; ++step) {
-        const int nu = u + du * step, nv = v + dv * step;
-        if (nu < 0 || nu >= W || nv < 0 || nv >= H) break;
-        const long ni = (long)nv * W + nu;
-        if (!__ldg(vin + ni)) continue;
-        const double w = __ddiv_rn(1.0, __dmul_rn((double)step, len));
+      // first valid pixel at step 1..radius, stopping at the image border;
+      // four steps' validity loads in flight at a time
+      int hit = 0;
+      for (int s0 = 1; s0 <= radius && hit == 0; s0 += 4) {
+        uint8_t ok[4];
+        bool in[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int step = s0 + k, nu = u + du * step, nv = v + dv * step;
+          in[k] = step <= radius && nu >= 0 && nu < W && nv >= 0 && nv < H;
+          ok[k] = in[k] ? __ldg(vin + (long)nv * W + nu) : 0;
+        }
+        bool stop = false;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (stop || hit) continue;
+          if (!in[k]) stop = true;
+          else if (ok[k]) hit = s0 + k;
+        }
+        if (stop) break;
+      }
+      if (hit) {
+        const long ni = (long)(v + dv * hit) * W + (u + du * hit);
+        const double w = __ddiv_rn(1.0, __dmul_rn((double)hit, len));
         wsum = __dadd_rn(wsum, w);
         vsum = __dadd_rn(vsum, __dmul_rn(w, (double)__ldg(din + ni)));
         ++support;
-        break;
       }
     }
     if (support >= min_support && wsum > 0.0) {
