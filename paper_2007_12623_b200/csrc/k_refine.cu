@@ -845,10 +845,9 @@ __global__ void k_so_update(const int2* __restrict__ chg, const unsigned* __rest
       const long rowbase = rok ? f * bs + ((long)(y >> 5) * W) * 32 + (y & 31) : 0;
       for (int x = xlo; x <= xhi; ++x) {
         const int dx = x - u;
-        if ((dx < 0 ? -dx : dx) <= sy) {
-          const long bi = rowbase + (long)x * 32;
-          if (mT[bi]) atomicAdd(soT + bi, e.y);
-        }
+        // unmasked targets are updated too: their S_o is never read (k_scan_b
+        // and k_d_repick use it under the mask), which saves the mask loads
+        if ((dx < 0 ? -dx : dx) <= sy) atomicAdd(soT + rowbase + (long)x * 32, e.y);
       }
     }
   }
