@@ -237,9 +237,11 @@ bool make_psum_tmap(CUtensorMap* map, const void* base, bool is_double, int W, i
 __global__ void __launch_bounds__(256)
     k_refine_init(const float* __restrict__ disp, const uint8_t* __restrict__ valid,
                   uint8_t* __restrict__ mT, double* __restrict__ oT, double* __restrict__ dT,
-                  int W, int H, long stride, long bs) {
+                  int W, int H, long stride, long bs, const int2* __restrict__ lstat,
+                  int* __restrict__ wbase, int* __restrict__ list, unsigned* __restrict__ count,
+                  Geom g) {
   __shared__ float td[32][33];
-  __shared__ uint8_t tv[32][33];
+  __shared__ uint8_t tv[32][33];  // bit 0: valid, bit 1: var_l == 0 (no defined score)
   const long f = blockIdx.z;
   const int u0 = blockIdx.x * 32, rb = blockIdx.y, v0 = rb * 32;
   for (int r = threadIdx.y; r < 32; r += 8) {
@@ -250,6 +252,7 @@ __global__ void __launch_bounds__(256)
       const long i = f * stride + (long)v * W + c;
       m = valid[i] ? 1 : 0;
       x = disp[i];
+      if (wbase && m && isnan(__int_as_float(__ldg(&lstat[i].y)))) m |= 2;
     }
     td[r][threadIdx.x] = x;
     tv[r][threadIdx.x] = m;
@@ -260,19 +263,32 @@ __global__ void __launch_bounds__(256)
     if (c >= W) continue;
     const long bi = f * bs + ((long)rb * W + c) * 32 + threadIdx.x;
     const uint8_t m = tv[threadIdx.x][cc];
-    const double x = m ? (double)td[threadIdx.x][cc] : 0.0;  // rows past H: m = 0
-    mT[bi] = m;
+    const float xf = td[threadIdx.x][cc];
+    const double x = (m & 1) ? (double)xf : 0.0;  // rows past H: m = 0
+    mT[bi] = m & 1;
     oT[bi] = x;
     dT[bi] = x;
+    if (wbase && (m & 1)) {
+      // window check (the sweep's window vs one centred on the cleanup output)
+      const int v = v0 + threadIdx.x, h = g.half;
+      const bool fits = c >= h && c < W - h && v >= h && v < H - h;
+      if (!fits || (m & 2)) {
+        wbase[bi] = kNoWin;
+      } else {
+        const int want = window_base((int)floor((double)xf), g.cmin, g.NC);
+        if (wbase[bi] != want) list[f * stride + atomicAdd(count + f, 1u)] = v * W + c;
+      }
+    }
   }
 }
 
 void launch_refine_init(const float* disp, const uint8_t* valid, uint8_t* mT, double* oT,
                         double* dT, int W, int H, int frames, long stride, long bs,
+                        const int2* lstat, int* wbase, int* list, unsigned* count, const Geom& g,
                         cudaStream_t s) {
   if (W <= 0 || H <= 0 || frames <= 0) return;
   k_refine_init<<<dim3((W + 31) / 32, (H + 31) / 32, frames), dim3(32, 8), 0, s>>>(
-      disp, valid, mT, oT, dT, W, H, stride, bs);
+      disp, valid, mT, oT, dT, W, H, stride, bs, lstat, wbase, list, count, g);
 }
 
 __global__ void __launch_bounds__(256)

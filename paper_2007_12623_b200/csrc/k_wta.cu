@@ -553,31 +553,9 @@ void launch_wta_generic(const uint8_t* lgray, const uint8_t* rgray, float* disp,
 
 // ---- candidate windows for pixels the cleanup changed (post-cleanup) ----
 
-// Pass 1: a valid pixel needs a window centred on its (possibly filled)
-// disparity o0; if the sweep's window is centred elsewhere (the pixel was
-// removed/filled, or its WTA pick was resolved in FP64) queue it.
-__global__ void k_window_check(const float* __restrict__ disp, const uint8_t* __restrict__ valid,
-                               const int2* __restrict__ lstat, int* __restrict__ wbase,
-                               int* __restrict__ list, unsigned* __restrict__ count, Geom g,
-                               long stride, long win_stride) {
-  const long f = blockIdx.z;
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  const int v = blockIdx.y * blockDim.y + threadIdx.y;
-  if (u >= g.W || v >= g.H) return;
-  const long pix = (long)v * g.W + u, i = f * stride + pix;
-  if (!valid[i]) return;
-  const int h = g.half;
-  const bool fits = u >= h && u < g.W - h && v >= h && v < g.H - h;
-  int* wb = wbase + f * win_stride + bt_index(g.W, v, u);
-  if (!fits || isnan(__int_as_float(__ldg(&lstat[i].y)))) {
-    *wb = kNoWin;
-    return;
-  }
-  const int want = window_base((int)floor((double)disp[i]), g.cmin, g.NC);
-  if (*wb != want) list[f * stride + atomicAdd(count + f, 1u)] = (int)pix;
-}
-
-// Pass 2: half a warp per queued pixel, lane q computes candidate wbase + q
+// Pixels queued by the window check in k_refine_init (a valid pixel whose
+// sweep window is not centred on its possibly filled disparity): half a warp
+// per queued pixel, lane q computes candidate wbase + q
 // with the sweep's exact integer arithmetic (61-tap chessboard cross sum,
 // num = 61 slr - sl sr, g = float(num) / sqrt(var_r), s = g / sqrt(var_l)),
 // so the window is bit-identical to one the sweep would have written.
@@ -620,15 +598,11 @@ __global__ void k_window_build(const float* __restrict__ disp, const uint8_t* __
   }
 }
 
-void launch_window_fix(const float* disp, const uint8_t* valid, const uint8_t* lgray,
-                       const uint8_t* rgray, const int2* lstat, const int2* rstat, wscore_t* win,
-                       int* wbase, int* list, unsigned* count, const Geom& g, int frames,
-                       long stride, long rstat_stride, long win_stride, cudaStream_t s) {
+void launch_window_build(const float* disp, const uint8_t* lgray, const uint8_t* rgray,
+                         const int2* lstat, const int2* rstat, wscore_t* win, int* wbase,
+                         const int* list, const unsigned* count, const Geom& g, int frames,
+                         long stride, long rstat_stride, long win_stride, cudaStream_t s) {
   if (g.W <= 0 || g.H <= 0 || frames <= 0) return;
-  cudaMemsetAsync(count, 0, sizeof(unsigned) * frames, s);
-  dim3 b(32, 8);
-  k_window_check<<<dim3((g.W + 31) / 32, (g.H + 7) / 8, frames), b, 0, s>>>(
-      disp, valid, lstat, wbase, list, count, g, stride, win_stride);
   k_window_build<<<dim3(148, frames), 256, 0, s>>>(disp, lgray, rgray, lstat, rstat, win, wbase,
                                                    list, count, g, stride, rstat_stride,
                                                    win_stride);

@@ -544,22 +544,28 @@ struct ss_ctx {
     oi.ensure(sizeof(int) * bs * n);
     int* op = oi.as<int>();
     uint8_t* mT = mbt.as<uint8_t>();
+    // Score windows: re-centre the sweep's windows on the cleanup output (the
+    // check runs inside refine_init, the rebuild below).
+    const bool fix_windows = have_windows && iters > 0;
+    if (fix_windows)
+      ck(cudaMemsetAsync(flag_count.p, 0, sizeof(unsigned) * n, stream), "memset");
     launch_refine_init(disp_a.as<float>(), valid_a.as<uint8_t>(), mT, o.as<double>(),
-                       d.as<double>(), W, H, n, N, bs, stream);
+                       d.as<double>(), W, H, n, N, bs, fix_windows ? lstat.as<int2>() : nullptr,
+                       fix_windows ? wbase.as<int>() : nullptr, flags.as<int>(),
+                       flag_count.as<unsigned>(), g, stream);
     launch_scan_bt_i(nullptr, mT, pcnt.as<int>(), W, H, r, n, stream);  // per-row valid counts
     launch_disc_isum(mT, pcnt.as<int>(), cnt.as<int>(), a, n, stream);  // disc counts
     stats.kernel_launches += 3;
     so.ensure(sizeof(int) * bs * n);
     chg.ensure(sizeof(int2) * bs * n);
     chg_count.ensure(sizeof(unsigned) * n);
-    // Score windows: re-centre the sweep's windows on the cleanup output.
     const wscore_t* winp = nullptr;
-    if (have_windows && iters > 0) {
-      launch_window_fix(disp_a.as<float>(), valid_a.as<uint8_t>(), gray_l.as<uint8_t>(),
-                        gray_r.as<uint8_t>(), lstat.as<int2>(), rstat.as<int2>(),
-                        win.as<wscore_t>(), wbase.as<int>(), flags.as<int>(),
-                        flag_count.as<unsigned>(), g, n, N, (long)H * g.SP, bs, stream);
-      stats.kernel_launches += 2;
+    if (fix_windows) {
+      launch_window_build(disp_a.as<float>(), gray_l.as<uint8_t>(), gray_r.as<uint8_t>(),
+                          lstat.as<int2>(), rstat.as<int2>(), win.as<wscore_t>(),
+                          wbase.as<int>(), flags.as<int>(), flag_count.as<unsigned>(), g, n, N,
+                          (long)H * g.SP, bs, stream);
+      stats.kernel_launches += 1;
       winp = win.as<wscore_t>();
     }
     defer.ensure(sizeof(Deferred) * bs * n);

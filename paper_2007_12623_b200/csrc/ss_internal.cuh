@@ -98,11 +98,13 @@ void launch_wta11(const uint4* ltap, const uint32_t* rcopy, const int2* lstat,
                   long lstat_stride, long rstat_stride, long map_stride, long win_stride,
                   int do_argmax, cudaStream_t s);
 // After cleanup: every valid pixel whose window is not centred on its
-// (possibly filled) disparity gets a freshly computed window.
-void launch_window_fix(const float* disp, const uint8_t* valid, const uint8_t* lgray,
-                       const uint8_t* rgray, const int2* lstat, const int2* rstat, wscore_t* win,
-                       int* wbase, int* list, unsigned* count, const Geom& g, int frames,
-                       long stride, long rstat_stride, long win_stride, cudaStream_t s);
+// (possibly filled) disparity gets a freshly computed window. The pixels are
+// queued by launch_refine_init's window check (list / count, count zeroed
+// before it).
+void launch_window_build(const float* disp, const uint8_t* lgray, const uint8_t* rgray,
+                         const int2* lstat, const int2* rstat, wscore_t* win, int* wbase,
+                         const int* list, const unsigned* count, const Geom& g, int frames,
+                         long stride, long rstat_stride, long win_stride, cudaStream_t s);
 void launch_wta_resolve(const uint8_t* lgray, const uint8_t* rgray, const int* flag_list,
                         const unsigned int* flag_count, float* disp, uint8_t* valid,
                         const Geom& g, double min_zncc, int frames, long gray_stride,
@@ -212,9 +214,14 @@ __host__ __device__ inline void bt_decode(int W, long idx, int& v, int& u) {
   u = (int)(q % W);
   v = (int)(q / W) * 32 + (int)(idx & 31);
 }
-// normal (disp, valid) -> BT mask m, o = d = valid ? disp : 0 (double)
+// normal (disp, valid) -> BT mask m, o = d = valid ? disp : 0 (double).
+// wbase != NULL: also the post-cleanup window check — a valid pixel whose
+// sweep window (wbase, BT) is not centred on its disparity is queued on
+// list / count (per frame, stride `stride`); kNoWin where no window fits or
+// var_l == 0 (lstat).
 void launch_refine_init(const float* disp, const uint8_t* valid, uint8_t* mT, double* oT,
                         double* dT, int W, int H, int frames, long stride, long bs,
+                        const int2* lstat, int* wbase, int* list, unsigned* count, const Geom& g,
                         cudaStream_t s);
 // Row prefixes carry `ext` (= the smoothing radius) columns past psum[W]
 // that repeat the row total: a disc span clipped at the right edge,
