@@ -21,17 +21,43 @@ __device__ __forceinline__ ExactScore zncc_exact(const uint8_t* __restrict__ L,
                                                  int lv, int ru, int half,
                                                  bool wta_semantics) {
   int64_t n = 0, sl = 0, sr = 0, sll = 0, srr = 0, slr = 0;
-  for (int dv = -half; dv <= half; ++dv) {
-    const uint8_t* lr = L + (long)(lv + dv) * W + lu;
-    const uint8_t* rr = R + (long)(lv + dv) * W + ru;
-    for (int du = -half + ((dv + half) & 1); du <= half; du += 2) {
-      const int64_t a = __ldg(lr + du), b = __ldg(rr + du);
-      n += 1;
-      sl += a;
-      sr += b;
-      sll += a * a;
-      srr += b * b;
-      slr += a * b;
+  if (half == 5) {
+    // window 11, fully unrolled (all 122 loads in flight); the tap sums fit
+    // int32 (61 * 255^2 < 2^31), so they equal the int64 ones
+    int s_l = 0, s_r = 0, s_ll = 0, s_rr = 0, s_lr = 0;
+#pragma unroll
+    for (int dv = -5; dv <= 5; ++dv) {
+      const uint8_t* lr = L + (long)(lv + dv) * W + lu;
+      const uint8_t* rr = R + (long)(lv + dv) * W + ru;
+#pragma unroll
+      for (int du = -5 + ((dv + 5) & 1); du <= 5; du += 2) {
+        const int a = __ldg(lr + du), b = __ldg(rr + du);
+        s_l += a;
+        s_r += b;
+        s_ll += a * a;
+        s_rr += b * b;
+        s_lr += a * b;
+      }
+    }
+    n = 61;
+    sl = s_l;
+    sr = s_r;
+    sll = s_ll;
+    srr = s_rr;
+    slr = s_lr;
+  } else {
+    for (int dv = -half; dv <= half; ++dv) {
+      const uint8_t* lr = L + (long)(lv + dv) * W + lu;
+      const uint8_t* rr = R + (long)(lv + dv) * W + ru;
+      for (int du = -half + ((dv + half) & 1); du <= half; du += 2) {
+        const int64_t a = __ldg(lr + du), b = __ldg(rr + du);
+        n += 1;
+        sl += a;
+        sr += b;
+        sll += a * a;
+        srr += b * b;
+        slr += a * b;
+      }
     }
   }
   int64_t var_l = n * sll - sl * sl;
