@@ -82,23 +82,29 @@ __global__ void k_ltap(const uint8_t* __restrict__ gray, uint4* __restrict__ lta
 // One thread per output word.
 __global__ void k_rcopy(const uint8_t* __restrict__ gray, uint32_t* __restrict__ rcopy, int W,
                         int PB, int PP, long gray_stride, long copy_stride) {
+  // one thread: word wi of the four byte-shifted copies s = 0..3 of plane
+  // `par` of image row y (sub-rows (y * 2 + par) * 4 + s): plane bytes
+  // j0 .. j0 + 6, j0 = 4 wi - PB, loaded once and funnel-shifted per s
   const long f = blockIdx.z;
   const int words = PP / 4;
   const int wi = blockIdx.x * blockDim.x + threadIdx.x;
-  const int row = blockIdx.y;  // (y * 2 + par) * 4 + s
+  const int yp = blockIdx.y;  // y * 2 + par
   if (wi >= words) return;
-  const int s = row & 3, par = (row >> 2) & 1, y = row >> 3;
+  const int par = yp & 1, y = yp >> 1;
   const int half_w = (W + 1) / 2;
   const uint8_t* src = gray + f * gray_stride + (long)y * W;
-  uint32_t word = 0;
+  uint32_t lo = 0, hi = 0;
 #pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    const int j = wi * 4 + b + s - PB;  // plane index
+  for (int b = 0; b < 7; ++b) {
+    const int j = wi * 4 + b - PB;  // plane index
     const int x = 2 * j + par;
     const uint32_t val = (j >= 0 && j < half_w && x < W) ? (uint32_t)__ldg(src + x) : 0u;
-    word |= val << (8 * b);
+    if (b < 4) lo |= val << (8 * b);
+    else hi |= val << (8 * (b - 4));
   }
-  rcopy[f * copy_stride + (long)row * words + wi] = word;
+  uint32_t* dst = rcopy + f * copy_stride + (long)yp * 4 * words + wi;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) dst[(long)s * words] = __funnelshift_r(lo, hi, 8 * s);
 }
 
 void launch_ltap(const uint8_t* gray, uint4* ltap, const Geom& g, int frames, long gray_stride,
@@ -112,7 +118,7 @@ void launch_rcopy(const uint8_t* gray, uint32_t* rcopy, const Geom& g, int frame
                   long gray_stride, long copy_stride, cudaStream_t s) {
   if (g.W <= 0 || g.H <= 0 || frames <= 0) return;
   const int words = g.PP / 4;
-  k_rcopy<<<dim3((words + 127) / 128, 8 * g.H, frames), 128, 0, s>>>(
+  k_rcopy<<<dim3((words + 127) / 128, 2 * g.H, frames), 128, 0, s>>>(
       gray, rcopy, g.W, g.PB, g.PP, gray_stride, copy_stride);
 }
 
