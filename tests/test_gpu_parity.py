@@ -441,3 +441,23 @@ def test_stereo_frame_entry(ss, orc):
     assert np.array_equal(out["points"][0][:k], cl.points.astype(np.float32))
     with pytest.raises(ss.InvalidArgument):
         ss.stereo_frame(L, R, ss.StereoParams(**p), None, flags)
+
+
+def test_batch_api_odd_frame_size(ss, orc):
+    """Frames of an odd pixel count: every frame after the first starts
+    unaligned in the packed RGB / gray buffers (the luma kernel's scalar
+    path), ragged column strips in the window statistics and the planes."""
+    from paper_2007_12623_b200.synth import as_rgb, params_for, stereo_pair
+    W, H, D, n = 97, 61, 16, 3
+    p = params_for(D)
+    pairs = [stereo_pair("textured", W, H, D, seed=70 + i) for i in range(n)]
+    Ls = np.stack([as_rgb(a) for a, _, _ in pairs])
+    Rs = np.stack([as_rgb(b) for _, b, _ in pairs])
+    ctx = ss.StereoContext(0, W, H, n, ss.StereoParams(**p))
+    out = ctx.run(Ls, Rs, ss.SS_OUT_DISPARITY)
+    ctx.close()
+    for i, (L, R, _) in enumerate(pairs):
+        assert np.array_equal(orc.to_gray(as_rgb(L)), L)
+        d, v = orc.refine_disparities(*orc.cleanup_pass(*orc.compute_disparity(L, R, p), p),
+                                      L, R, p)
+        assert_map_equal((out["disparity"][i], out["valid"][i]), (d, v), f"frame {i}")
