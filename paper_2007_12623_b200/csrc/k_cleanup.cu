@@ -154,10 +154,12 @@ __device__ __forceinline__ void append_invalid(int* list, unsigned* count, long 
   list[f * stride + atomicAdd(count + f, 1u)] = pix;
 }
 
-__global__ void k_remove_outliers(const float* __restrict__ din, const uint8_t* __restrict__ vin,
-                                  float* __restrict__ dout, uint8_t* __restrict__ vout, int W,
-                                  int H, int r, const uint32_t* __restrict__ emap, long stride,
-                                  long fw, float* __restrict__ dout2, uint8_t* __restrict__ vout2,
+// In place allowed (vout == vin, dout == NULL: each thread reads only its own
+// pixel of din / vin, before writing it), hence no __restrict__ on those.
+__global__ void k_remove_outliers(const float* din, const uint8_t* vin, float* dout,
+                                  uint8_t* vout, int W, int H, int r,
+                                  const uint32_t* __restrict__ emap, long stride, long fw,
+                                  float* __restrict__ dout2, uint8_t* __restrict__ vout2,
                                   int* __restrict__ list, unsigned* __restrict__ count) {
   const long f = blockIdx.z;
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
@@ -165,7 +167,7 @@ __global__ void k_remove_outliers(const float* __restrict__ din, const uint8_t* 
   if (u >= W || v >= H) return;
   const long i = f * stride + (long)v * W + u;
   const float d0 = din[i];
-  dout[i] = d0;
+  if (dout) dout[i] = d0;
   if (dout2) dout2[i] = d0;
   if (!vin[i]) {
     vout[i] = 0;

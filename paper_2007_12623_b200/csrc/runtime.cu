@@ -482,22 +482,20 @@ struct ss_ctx {
     flag_count.ensure(sizeof(unsigned) * n);
     for (int k = 0; k < params.cleanup_iterations; ++k) {
       const int r = params.outlier_radius_start + k * params.outlier_radius_step;
-      // outliers: a -> b, and in place into a (each pixel reads only itself),
-      // listing the invalid pixels; the radial fill then writes only those
-      // into a, reading b (the reference's no-cascade input map)
+      // outliers: validity in place in a (each pixel reads only itself) plus
+      // a copy into b, listing the invalid pixels; the radial fill writes
+      // only those into b, reading a (the reference's no-cascade input map);
+      // the disc fill reads b and writes a — the round ends in a, no copies
       ck(cudaMemsetAsync(flag_count.p, 0, sizeof(unsigned) * n, stream), "memset");
-      launch_remove_outliers(disp_a.as<float>(), valid_a.as<uint8_t>(), disp_b.as<float>(),
-                             valid_b.as<uint8_t>(), W, H, r, params.neighbor_jump_threshold,
-                             emap.as<uint32_t>(), n, N, stream, disp_a.as<float>(),
-                             valid_a.as<uint8_t>(), flags.as<int>(), flag_count.as<unsigned>());
-      launch_fill_radial_list(disp_b.as<float>(), valid_b.as<uint8_t>(), disp_a.as<float>(),
-                              valid_a.as<uint8_t>(), W, H, params.fill_radius_radial, 4,
+      launch_remove_outliers(disp_a.as<float>(), valid_a.as<uint8_t>(), nullptr,
+                             valid_a.as<uint8_t>(), W, H, r, params.neighbor_jump_threshold,
+                             emap.as<uint32_t>(), n, N, stream, disp_b.as<float>(),
+                             valid_b.as<uint8_t>(), flags.as<int>(), flag_count.as<unsigned>());
+      launch_fill_radial_list(disp_a.as<float>(), valid_a.as<uint8_t>(), disp_b.as<float>(),
+                              valid_b.as<uint8_t>(), W, H, params.fill_radius_radial, 4,
                               flags.as<int>(), flag_count.as<unsigned>(), n, N, stream);
-      fill_disc(n, W, H, disp_a.as<float>(), valid_a.as<uint8_t>(), disp_b.as<float>(),
-                valid_b.as<uint8_t>(), params.fill_radius_disc, disc_support);
-      ck(cudaMemcpyAsync(disp_a.p, disp_b.p, sizeof(float) * N * n, cudaMemcpyDeviceToDevice,
-                         stream), "copy");
-      ck(cudaMemcpyAsync(valid_a.p, valid_b.p, N * n, cudaMemcpyDeviceToDevice, stream), "copy");
+      fill_disc(n, W, H, disp_b.as<float>(), valid_b.as<uint8_t>(), disp_a.as<float>(),
+                valid_a.as<uint8_t>(), params.fill_radius_disc, disc_support);
       stats.kernel_launches += 2;
     }
   }
