@@ -736,9 +736,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int best = repick(a, u, v, dv, L, Rg, win != nullptr, wv, wbk, px, defer + f * bs,
                             defer_count + f);
     if (best != INT_MIN) {
-      if (USE_SO && best != olk)
+      if (!USE_SO) {
+        oT[bi] = best;
+      } else if (best != olk) {  // o only changes for a few hundred pixels per frame
         chg[f * bs + atomicAdd(chg_count + f, 1u)] = make_int2((int)px, best - olk);
-      oT[bi] = best;
+        oT[bi] = best;
+      }
     }
   }
   // the window copies must land before the block's shared memory is released
