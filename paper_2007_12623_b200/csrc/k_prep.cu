@@ -125,13 +125,10 @@ void launch_rcopy(const uint8_t* gray, uint32_t* rcopy, const Geom& g, int frame
 // Chessboard window statistics of one image. out[i] = {sum, bits(1/sqrt(var))}
 // with NaN when the window leaves the image or var == 0 (undefined ZNCC).
 // Right-image rows are padded by SPAD entries each side ({0, NaN}).
-// HALF > 0: compile-time window (fully unrolled, int32 sums: exact for
-// window <= 19, where 181 * 255^2 < 2^31); HALF == 0: any window, int64.
-template <int HALF>
+// Any window (int64 sums); window 11 runs k_stats_col below.
 __global__ void k_stats(const uint8_t* __restrict__ gray, int2* __restrict__ out, int W,
-                        int H, int half_rt, int pitch, int pad, long gray_stride,
+                        int H, int half, int pitch, int pad, long gray_stride,
                         long stat_stride) {
-  const int half = HALF > 0 ? HALF : half_rt;
   const long f = blockIdx.z;
   gray += f * gray_stride;
   out += f * stat_stride;
@@ -142,31 +139,13 @@ __global__ void k_stats(const uint8_t* __restrict__ gray, int2* __restrict__ out
     int2 r = make_int2(0, __float_as_int(__int_as_float(0x7fc00000)));
     if (u >= half && u < W - half && v >= half && v < H - half) {
       int64_t n = 0, s = 0, sq = 0;
-      if constexpr (HALF > 0) {
-        int s32 = 0, q32 = 0, n32 = 0;
-#pragma unroll
-        for (int dv = -HALF; dv <= HALF; ++dv) {
-          const uint8_t* row = gray + (long)(v + dv) * W + u;
-#pragma unroll
-          for (int du = -HALF + ((dv + HALF) & 1); du <= HALF; du += 2) {
-            const int a = __ldg(row + du);
-            n32 += 1;
-            s32 += a;
-            q32 += a * a;
-          }
-        }
-        n = n32;
-        s = s32;
-        sq = q32;
-      } else {
-        for (int dv = -half; dv <= half; ++dv) {
-          const uint8_t* row = gray + (long)(v + dv) * W + u;
-          for (int du = -half + ((dv + half) & 1); du <= half; du += 2) {
-            const int64_t a = row[du];
-            n += 1;
-            s += a;
-            sq += a * a;
-          }
+      for (int dv = -half; dv <= half; ++dv) {
+        const uint8_t* row = gray + (long)(v + dv) * W + u;
+        for (int du = -half + ((dv + half) & 1); du <= half; du += 2) {
+          const int64_t a = row[du];
+          n += 1;
+          s += a;
+          sq += a * a;
         }
       }
       // patch_stats stores int32 (matcher.cpp:132-133); windows >= 27 wrap.
@@ -189,7 +168,7 @@ __global__ void k_stats(const uint8_t* __restrict__ gray, int2* __restrict__ out
 // the window sum is lo16(PO) + hi16(PE), and one row down
 //   PO(v + 1) = PE(v) + P(v + 6),   PE(v + 1) = PO(v) - P(v - 5);
 // the squares run the same recurrences on separate Ho / He accumulators.
-// Integer sums: bit-identical to k_stats<5>.
+// Integer sums: bit-identical to the direct 61-tap loop of k_stats.
 constexpr int kStatRows = 32;
 constexpr int kStatCols = 128;
 
@@ -283,7 +262,7 @@ void launch_stats(const uint8_t* gray, int2* lstat, int2* rstat, int is_right, c
     k_stats_col<<<gc, kStatCols, 0, s>>>(gray, is_right ? rstat : lstat, g.W, g.H, pitch, pad,
                                          gray_stride, stat_stride);
   } else
-    k_stats<0><<<grid, threads, 0, s>>>(gray, is_right ? rstat : lstat, g.W, g.H, g.half, pitch,
+    k_stats<<<grid, threads, 0, s>>>(gray, is_right ? rstat : lstat, g.W, g.H, g.half, pitch,
                                         pad, gray_stride, stat_stride);
 }
 

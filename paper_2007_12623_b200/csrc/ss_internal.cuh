@@ -87,7 +87,7 @@ void launch_stats(const uint8_t* gray, int2* lstat, int2* rstat, int is_right, c
 // window: kWin scores s(c) = g(c) / sqrt(var_l) for c = wbase .. wbase+kWin-1,
 // wbase centred on the WTA pick, or on base_map[pixel] when base_map != NULL
 // (per-stage refine). wbase = kNoWin when var_l == 0 (no defined score) or
-// when the window would reach past [d_min, d_max] (launch_window_fix then
+// when the window would reach past [d_min, d_max] (launch_window_build then
 // rebuilds it for the pixels the refinement uses).
 // win == NULL: argmax only (the right-view sweep of the LR check).
 // win / wbase are BT-indexed (bt_index, frame stride win_stride).
