@@ -60,26 +60,32 @@ void launch_to_gray(const uint8_t* rgb, uint8_t* gray, long n, int frames, long 
 //   x = L(u-4) L(u-2) L(u) L(u+2)   y = L(u+4) 0 0 0
 //   z = L(u-5) L(u-3) L(u-1) L(u+1) w = L(u+3) L(u+5) 0 0
 // byte 0 lowest; bytes outside the row are 0 (such pixels never score).
-__global__ void k_ltap(const uint8_t* __restrict__ gray, uint4* __restrict__ ltap, int W,
-                       long gray_stride, long tap_stride) {
+__global__ void __launch_bounds__(128)
+    k_ltap(const uint8_t* __restrict__ gray, uint4* __restrict__ ltap, int W, long gray_stride,
+           long tap_stride) {
+  // the block's row segment u0 - 5 .. u0 + 132 staged once (coalesced), each
+  // thread then packs its 11 taps from shared memory
+  __shared__ uint8_t seg[128 + 16];
   const long f = blockIdx.z;
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int u0 = blockIdx.x * 128;
+  const int u = u0 + threadIdx.x;
   const int y = blockIdx.y;
-  if (u >= W) return;
   const uint8_t* row = gray + f * gray_stride + (long)y * W;
-  auto at = [&](int x) -> uint32_t { return (x >= 0 && x < W) ? (uint32_t)__ldg(row + x) : 0u; };
+  for (int k = threadIdx.x; k < 128 + 10; k += 128) {
+    const int x = u0 - 5 + k;
+    seg[k] = (x >= 0 && x < W) ? __ldg(row + x) : 0;
+  }
+  __syncthreads();
+  if (u >= W) return;
+  auto at = [&](int dx) -> uint32_t { return seg[threadIdx.x + 5 + dx]; };
   uint4 t;
-  t.x = at(u - 4) | at(u - 2) << 8 | at(u) << 16 | at(u + 2) << 24;
-  t.y = at(u + 4);
-  t.z = at(u - 5) | at(u - 3) << 8 | at(u - 1) << 16 | at(u + 1) << 24;
-  t.w = at(u + 3) | at(u + 5) << 8;
+  t.x = at(-4) | at(-2) << 8 | at(0) << 16 | at(2) << 24;
+  t.y = at(4);
+  t.z = at(-5) | at(-3) << 8 | at(-1) << 16 | at(1) << 24;
+  t.w = at(3) | at(5) << 8;
   ltap[f * tap_stride + (long)y * W + u] = t;
 }
 
-// Right parity planes in 4 byte-shifted copies: rcopy[y][par][s] byte j =
-// plane byte j + s, plane byte i = R(2 (i - PB) + par) (0 in the padding), so
-// any byte offset of a plane row starts an aligned word in one of the copies.
-// One thread per output word.
 __global__ void k_rcopy(const uint8_t* __restrict__ gray, uint32_t* __restrict__ rcopy, int W,
                         int PB, int PP, long gray_stride, long copy_stride) {
   // one thread: word wi of the four byte-shifted copies s = 0..3 of plane
