@@ -1,34 +1,54 @@
 #!/usr/bin/env python
 """Benchmark: stereo pairs/s of the full per-frame stereo chain on B200.
 
-Metric (BASELINE.json): stereo pairs/sec at 960x540 D=64, 1/2/4/8 B200.
-Workload (BASELINE.json configs[3], "C4"): every rank processes a batch of
-256 synthetic textured 960x540 pairs per step, d in [0, 63], the whole
-run_stereo_only chain: luma -> ZNCC WTA -> 3 rounds of
+Metric (BASELINE.json): stereo pairs/sec at 960x540 D=64 (1/2/4/8 B200),
+ms/pair, fraction of the roofline. Every step runs the whole run_stereo_only
+chain on every frame: luma -> ZNCC WTA -> 3 rounds of
 outlier removal + hole filling -> 10 refinement iterations -> oriented point
-cloud (points, normals, colours). Frames shard across ranks with no collective
-(weak scaling); NCCL only carries the barrier and the max-over-ranks time.
+cloud (points, normals, colours). Frames shard across ranks with no collective;
+NCCL carries only the barrier and the max-over-ranks time.
 
-  value  device-resident throughput: inputs already in HBM, results written to
-         device output tensors; CUDA events on the ctx stream, max over ranks.
-  e2e    the same through the public host API (ss_stereo_batch): pinned host
-         RGB in, H2D + chain + D2H of disparity/validity/cloud inside the timed
-         region.
-  roofline  dominant kernel = the ZNCC cost sweep (k_wta11): algorithmic
-         lane-ops per launch (SURVEY.md §8d census: 12 N (D+10) + 3 N D per
-         frame) / its CUDA-event duration vs the ALU issue peak
-         (148 SM x 128 lanes x sm_max_mhz).
-  cpu_baseline  the reference itself (oracle/_ref, compiled from
-         /root/reference by oracle/Makefile) on the host cores, bounded sample.
+Workloads (--workload; BASELINE.json configs):
+  c4  (default, configs[3]) 256 synthetic textured 960x540 pairs per GPU per
+      step, D=64 (d 0..63); weak scaling.
+  c2  (configs[1]) the same with the low-texture recipe.
+  c3  (configs[2]) 32 textured 1920x1080 pairs per GPU per step, D=128.
+  c5  (configs[4]) a 1024-pair 1920x1080 D=128 synthetic video stream split
+      into contiguous frame blocks across the GPUs (strong scaling); e2e
+      streams it through the host API into a per-thread host ring (the
+      streaming contract of SPEC.md:600: a frame's outputs are consumed before
+      their slot is reused).
 
-`--impl reference` runs only that reference CPU path (rank 0) on the same
-metric and config.
+Keys:
+  value     device-resident pairs/s: inputs in HBM, results written to device
+            buffers; CUDA events on the context streams, max over ranks.
+  e2e       the same through the public host API (ss_stereo_batch): pinned
+            host RGB in, H2D + chain + D2H of disparity/validity/cloud inside
+            the timed region.
+  roofline  the dominant kernel group (largest device-time share, measured
+            live with CUDA events on the launching stream): algorithmic
+            lane-ops per launch (SURVEY.md §8d census) / its
+            average launch time vs the ALU issue peak 148 SM x 128 lanes x
+            sm_max_mhz; `stages` holds every kernel group's fraction.
+  parity    the step's own outputs against SHA-256 digests of the reference's
+            outputs for the same seeded frames (tests/golden/digests.json,
+            made from oracle/_ref by tests/golden/make_digests.py), and, in
+            the cpu_baseline leg, whole arrays against the reference run here.
+            Any mismatch fails the run (exit status 1).
+  cpu_baseline  the reference itself (oracle/_ref) on the host cores, bounded
+            sample of the same workload's frames.
+
+`--impl reference` runs only the reference CPU path (rank 0) on the same
+metric and config. `--gpus N` without a torchrun environment re-launches
+itself under torch.distributed.run with N ranks.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -40,8 +60,31 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-W, H, D = 960, 540, 64
-CENSUS = {"textured": 2.16e9, "lowtex": 2.25e9, "fhd": 10.6e9}  # lane-ops/pair, BASELINE.md
+WORKLOADS = {
+    "c4": dict(kind="textured", W=960, H=540, D=64, frames=256, batch=16, streams=4, unique=32,
+               seed_base=0, scaling="weak", ref_pairs=5,
+               desc="C4 (BASELINE.json configs[3]): 256 synthetic textured 960x540 stereo pairs "
+                    "per GPU per step, D=64 (d 0..63), full chain luma+WTA+cleanup+refine+"
+                    "cloud(normals)"),
+    "c2": dict(kind="lowtex", W=960, H=540, D=64, frames=256, batch=16, streams=4, unique=32,
+               seed_base=0, scaling="weak", ref_pairs=5,
+               desc="C2 (BASELINE.json configs[1]): 256 synthetic low-texture 960x540 pairs per "
+                    "GPU per step, D=64, full chain incl. normals"),
+    "c3": dict(kind="textured", W=1920, H=1080, D=128, frames=32, batch=8, streams=2, unique=8,
+               seed_base=100, scaling="weak", ref_pairs=2,
+               desc="C3 (BASELINE.json configs[2]): 32 synthetic textured 1920x1080 stereo pairs "
+                    "per GPU per step, D=128 (d 0..127), full chain incl. normals"),
+    "c5": dict(kind="video", W=1920, H=1080, D=128, frames=1024, batch=8, streams=2, unique=32,
+               seed_base=0, scaling="strong", ref_pairs=2,
+               desc="C5 (BASELINE.json configs[4]): 1024-pair 1920x1080 D=128 synthetic video "
+                    "stream (32 distinct drifting frames, tiled) split into contiguous frame "
+                    "blocks across the GPUs, full chain incl. normals, clouds gathered to host"),
+}
+# SURVEY.md §8d census, 32-bit lane-ops per pair (whole chain).
+CENSUS_TOTAL = {"c4": 2.16e9, "c2": 2.25e9, "c3": 10.6e9, "c5": 10.6e9}
+# measured disc-fill list sizes summed over the 3 rounds (C3 scaled by area)
+I_DISC = {"c4": 29.4e3, "c2": 54.0e3, "c3": 117.6e3, "c5": 117.6e3}
+DIGEST_PATH = os.path.join(ROOT, "tests", "golden", "digests.json")
 
 
 def parse():
@@ -50,19 +93,32 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--frames", type=int, default=256, help="pairs per rank per step")
-    ap.add_argument("--batch", type=int, default=16, help="frames per device launch")
-    ap.add_argument("--unique", type=int, default=32, help="distinct seeded frames (tiled)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--streams", type=int, default=4,
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--frames", type=int, default=None, help="pairs per rank per step (c5: total)")
+    ap.add_argument("--batch", type=int, default=None, help="frames per device launch")
+    ap.add_argument("--streams", type=int, default=None,
                     help="concurrent contexts (one CUDA stream each) sharing the frames")
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extensions", action="store_true",
-                    help="skip the LR-check / feature side measurements")
+                    help="skip the LR-check / feature / fusion side measurements")
     ap.add_argument("--cpu-pairs", type=int, default=2)
     ap.add_argument("--cpu-configs", action="store_true",
                     help="also time the reference CPU chain on C1/C2/C3 (median of 3; minutes)")
-    return ap.parse_args()
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher/sharding logic only (gloo, no GPU work): for CPU tests")
+    a = ap.parse_args()
+    wl = WORKLOADS[a.workload]
+    a.frames = a.frames or wl["frames"]
+    a.batch = a.batch or wl["batch"]
+    a.streams = a.streams or wl["streams"]
+    return a
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def dist_env():
@@ -70,6 +126,23 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def self_launch(args):
+    """--gpus N outside torchrun: re-exec under torch.distributed.run, one rank
+    per GPU (the driver's own launch, so the measured path is the same)."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            sys.exit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+        return
+    if args.gpus <= 1:
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    r = subprocess.run(cmd)
+    sys.exit(r.returncode)
 
 
 class ClockSampler:
@@ -130,40 +203,112 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_frames(rank, world, frames, unique):
-    from paper_2007_12623_b200.shard import frame_range
+# ---------------------------------------------------------------- frames
+
+def frame_seed(wl_name, rank, world, i, frames):
+    """(seed, video frame) of local frame i of `rank` (the tiling is by seed, so
+    the digest table names the first frames of rank 0 directly)."""
+    wl = WORKLOADS[wl_name]
+    u = wl["unique"]
+    if wl["scaling"] == "strong":
+        from paper_2007_12623_b200.shard import frame_range
+        g = frame_range(frames, rank, world)[0] + i
+        return g % u, g % u
+    return wl["seed_base"] + rank * frames + (i % u), 0
+
+
+def local_frames(args, rank, world):
+    if WORKLOADS[args.workload]["scaling"] == "strong":
+        from paper_2007_12623_b200.shard import frame_range
+        a, b = frame_range(args.frames, rank, world)
+        return b - a
+    return args.frames
+
+
+def make_unique(args, rank, world, count):
+    """The distinct frames this rank needs (RGB), in local order modulo `unique`."""
     from paper_2007_12623_b200.synth import as_rgb, stereo_pair
-    start, _ = frame_range(world * frames, rank, world)  # this rank's block of the global batch
-    u = max(1, min(unique, frames))
+    wl = WORKLOADS[args.workload]
+    u = max(1, min(wl["unique"], count))
     Ls, Rs = [], []
     for i in range(u):
-        L, R, _ = stereo_pair("textured", W, H, D, seed=start + i)
+        seed, fr = frame_seed(args.workload, rank, world, i, args.frames)
+        L, R, _ = stereo_pair(wl["kind"], wl["W"], wl["H"], wl["D"], seed=seed, frame=fr)
         Ls.append(as_rgb(L))
         Rs.append(as_rgb(R))
-    Ls, Rs = np.stack(Ls), np.stack(Rs)
-    reps = (frames + u - 1) // u
-    return np.tile(Ls, (reps, 1, 1, 1))[:frames], np.tile(Rs, (reps, 1, 1, 1))[:frames]
+    return np.stack(Ls), np.stack(Rs)
 
 
-def reference_chain(pairs, Wc=None, Hc=None, Dc=None):
-    """The reference's own CPU path (oracle/_ref) on host pairs; cloud stage from
-    the restatement (the reference's needs Eigen, absent). Returns seconds."""
-    Wc, Hc, Dc = Wc or W, Hc or H, Dc or D
+def config_dict(args, world):
+    wl = WORKLOADS[args.workload]
+    return {"workload": wl["desc"], "width": wl["W"], "height": wl["H"], "disparities": wl["D"],
+            "cache": "inputs > L2: every frame of a step is read from its own HBM copy (c4/c2/c3: "
+                     "distinct per-frame buffers, >= 398 MB per GPU; c5: 32 distinct 12.4 MB frames "
+                     "in rotation), no flush",
+            "parallelism": f"frame-shard x{world}, no collective"}
+
+
+# ---------------------------------------------------------------- digests
+
+def map_digest(d, v):
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(d, np.float32).tobytes())
+    h.update(np.ascontiguousarray(v, np.uint8).tobytes())
+    return h.hexdigest()
+
+
+def sha(a, dt):
+    return hashlib.sha256(np.ascontiguousarray(a, dt).tobytes()).hexdigest()
+
+
+def digest_keys(args):
+    dig = json.load(open(DIGEST_PATH)) if os.path.exists(DIGEST_PATH) else {}
+    pre = {"c4": "bench_c4_", "c3": "bench_c3_", "c5": "bench_c5_"}.get(args.workload)
+    if pre is None:
+        return dig, []
+    keys = sorted(k for k in dig if k.startswith(pre))
+    return dig, keys
+
+
+def check_frames(get_frame, keys, dig, cloud=True):
+    """get_frame(i) -> dict of host arrays for local frame i; returns mismatching keys."""
+    bad = []
+    for i, k in enumerate(keys):
+        e, f = dig[k], get_frame(i)
+        ok = map_digest(f["disparity"], f["valid"]) == e["refine"]
+        if cloud and ok:
+            n = int(f["n_points"])
+            ok = (n == e["n_points"] and sha(f["index"], np.int32) == e["cloud_index"]
+                  and sha(f["points"][:n], np.float32) == e["cloud_points_f32"])
+        if not ok:
+            bad.append(k)
+    return bad
+
+
+# ---------------------------------------------------------------- reference CPU path
+
+def reference_chain(pairs, wl, want_outputs=False):
+    """The reference's own CPU path (oracle/_ref) on host RGB pairs; cloud
+    stage from the restatement (the reference's needs Eigen, absent). Returns
+    (seconds, kind, outputs)."""
     from oracle.oracle import Oracle
     from paper_2007_12623_b200.synth import default_rig, params_for
     kind = "reference" if Oracle.available("ref") else "port"
     ref = Oracle("ref" if kind == "reference" else "orc")
     orc = Oracle("orc")
-    p = params_for(Dc)
-    rig = default_rig(Wc, Hc)
+    p = params_for(wl["D"])
+    rig = default_rig(wl["W"], wl["H"])
+    outs = []
     t0 = time.perf_counter()
     for L, R in pairs:
         lg, rg = ref.to_gray(L), ref.to_gray(R)
         d, v = ref.compute_disparity(lg, rg, p)
         d, v = ref.cleanup_pass(d, v, p)
         d, v = ref.refine_disparities(d, v, lg, rg, p)
-        orc.disparity_to_cloud(d, v, L, rig)
-    return time.perf_counter() - t0, kind
+        cl = orc.disparity_to_cloud(d, v, L, rig)
+        if want_outputs:
+            outs.append((d, v, cl))
+    return time.perf_counter() - t0, kind, outs
 
 
 def cpu_model():
@@ -186,87 +331,51 @@ def omp_threads(n):
         return False
 
 
-def cpu_pairs(n):
+def workload_pairs(args, n):
     from paper_2007_12623_b200.synth import as_rgb, stereo_pair
+    wl = WORKLOADS[args.workload]
     out = []
     for i in range(n):
-        L, R, _ = stereo_pair("textured", W, H, D, seed=i)
+        seed, fr = frame_seed(args.workload, 0, 1, i, args.frames)
+        L, R, _ = stereo_pair(wl["kind"], wl["W"], wl["H"], wl["D"], seed=seed, frame=fr)
         out.append((as_rgb(L), as_rgb(R)))
     return out
-
-
-def config_dict(args, world):
-    return {"workload": "C4: 256 synthetic textured 960x540 stereo pairs per rank per step, "
-                        "D=64 (d 0..63), full chain luma+WTA+cleanup+refine+cloud(normals)",
-            "width": W, "height": H, "disparities": D, "pairs_per_step_per_gpu": args.frames,
-            "frames_per_launch": args.batch, "unique_seeded_frames": min(args.unique, args.frames),
-            "cache": "inputs > L2 (per-step input 796 MB RGB per GPU, not flushed: each frame is "
-                     "read once per step)",
-            "parallelism": f"frame-shard x{world}, no collective",
-            "streams_per_gpu": args.streams}
 
 
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    pairs = cpu_pairs(1)
+    wl = WORKLOADS[args.workload]
+    k = wl["ref_pairs"]
+    pairs = workload_pairs(args, k)
     times = []
     kind = "reference"
     for i in range(args.warmup + args.steps):
-        t, kind = reference_chain(pairs)
+        t, kind, _ = reference_chain(pairs, wl)
         if i >= args.warmup:
             times.append(t)
     total = sum(times)
-    value = len(times) / total
+    value = k * len(times) / total
     cores = os.cpu_count()
     line = {
-        "metric": "stereo pairs/sec at 960x540 D=64", "value": value, "unit": "pairs/s",
+        "metric": "stereo pairs/sec", "value": value, "unit": "pairs/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1000.0 * total / len(times), "pairs_per_step": k,
+        "ms_per_pair": 1000.0 * total / (k * len(times)),
+        "higher_is_better": True, "scaling": wl["scaling"],
         "vs_baseline": None, "dtype": "u8/int64/f64", "data": "synthetic",
         "config": config_dict(args, world), "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores, "kind": kind,
-                         "sample": "1 C1 pair per step through oracle/_ref (unmodified reference "
-                                   "matcher/cleanup/smoothing, OpenMP all cores) + restated cloud"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"{k} pairs of the workload's first frames per step through "
+                                   "oracle/_ref (unmodified reference matcher/cleanup/smoothing, "
+                                   "OpenMP on all cores) + restated cloud (Eigen absent); the "
+                                   "reference API is per pair"},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
-
-
-def geometry_throughput(ss, kind, Wf, Hf, Df, nf, Bf, nctx):
-    """Device-resident pairs/s of the full chain (incl. normals) for one
-    synthetic geometry: nf pairs (6 seeded, tiled) in HBM, batches of Bf
-    spread over nctx contexts; host wall clock around synchronous batches."""
-    import torch
-    from paper_2007_12623_b200.synth import as_rgb, default_rig, params_for, stereo_pair
-    uniq = [stereo_pair(kind, Wf, Hf, Df, seed=100 + i)[:2] for i in range(6)]
-    Lf = torch.from_numpy(np.stack([as_rgb(uniq[i % 6][0]) for i in range(nf)])).cuda()
-    Rf = torch.from_numpy(np.stack([as_rgb(uniq[i % 6][1]) for i in range(nf)])).cuda()
-    pf = ss.StereoParams(**params_for(Df))
-    rf = ss.StereoRig(**default_rig(Wf, Hf))
-    cf = [ss.StereoContext(torch.cuda.current_device(), Wf, Hf, Bf, pf, rf) for _ in range(nctx)]
-    flags = ss.SS_OUT_DISPARITY | ss.SS_OUT_CLOUD | ss.SS_OUT_NORMALS
-
-    def run():
-        for i, f0 in enumerate(range(0, nf, Bf)):
-            cf[i % nctx].run_device(Bf, Wf, Hf, Lf[f0].data_ptr(), Rf[f0].data_ptr(), flags)
-        for c in cf:
-            c.sync()
-
-    run()  # warm (allocations)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    run()
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-    for c in cf:
-        c.close()
-    return {"value": nf / dt, "unit": "pairs/s", "ms_per_pair": 1000 * dt / nf,
-            "workload": f"{nf} synthetic {kind} {Wf}x{Hf} pairs, D={Df} (d 0..{Df - 1}), "
-                        f"full chain incl. normals, {nctx} contexts, inputs in HBM",
-            "timing": "host wall clock around synchronous batches"}
 
 
 def cpu_side_by_side(runs=3):
@@ -278,122 +387,92 @@ def cpu_side_by_side(runs=3):
     for key, kind, Wc, Hc, Dc in (("C1", "textured", 960, 540, 64), ("C2", "lowtex", 960, 540, 64),
                                   ("C3", "textured", 1920, 1080, 128)):
         L, R, _ = stereo_pair(kind, Wc, Hc, Dc, seed=1234)
-        pair = [(as_rgb(L), as_rgb(R))]
-        ts = [reference_chain(pair, Wc, Hc, Dc)[0] for _ in range(runs)]
+        wl = dict(W=Wc, H=Hc, D=Dc)
+        ts = [reference_chain([(as_rgb(L), as_rgb(R))], wl)[0] for _ in range(runs)]
         out[key] = {"pairs_per_s": 1.0 / statistics.median(ts), "median_s": statistics.median(ts)}
-    L, R, _ = stereo_pair("textured", 960, 540, 64, seed=1234)
-    omp_threads(1)
-    ts = [reference_chain([(as_rgb(L), as_rgb(R))])[0] for _ in range(runs)]
-    omp_threads(os.cpu_count())
-    out["C1"]["pairs_per_s_1thread"] = 1.0 / statistics.median(ts)
     return out
 
 
-def extensions(ss, ctxs, step_device, barrier, stream, F, Lh_first, Rh_first, od=None):
-    """Side measurements of the SURVEY §8f rows (not the headline metric):
-    the chain with the opt-in LR check (device pairs/s, same workload), and
-    the feature front end on one C1 frame pair through the per-stage C-ABI
-    (host buffers, transfers included) beside the reference's CPU code."""
-    import torch
+# ---------------------------------------------------------------- roofline
+
+def roofline_report(args, stages, frames_timed, n_sm, sm_max, hbm_peak, iters=10):
+    """Per kernel group: census lane-ops per
+    launch over the live average launch time (CUDA events on the launching
+    stream, one context, no concurrency)."""
+    wl = WORKLOADS[args.workload]
+    N, D = wl["W"] * wl["H"], wl["D"]
+    alu_peak = n_sm * 128 * sm_max * 1e6
+    census = {  # lane-ops per frame
+        "wta_sweep": ("k_wta11: chessboard ZNCC over [d_min, d_max] + WTA", 15.0 * N * D),
+        "refine_repick": ("k_d_repick: b-disc gather 62N + smoothing 3N + re-pick 60N per "
+                          "iteration", 125.0 * N * iters),
+        "cleanup_disc": ("k_row_count/k_disc_select/k_disc_sum: I_disc x (82 + 3 x 1256)",
+                         I_DISC[args.workload] * (82 + 3 * 1256)),
+        "cleanup_radial": ("k_fill_radial_list: 144N", 144.0 * N),
+        "cleanup_outliers": ("k_edge_bits + k_remove_outliers: 72N", 72.0 * N),
+        "cloud_normals": ("k_cloud_normals: 7x7 moments + 3x3 eigen, 600N", 600.0 * N),
+    }
+    hbm = {"refine_scan": ("k_scan_b / k_scan_bt: row prefix scans, 29 B/px per iteration",
+                           29.0 * N * iters)}
     out = {}
-    for c in ctxs:
-        c.set_lr_check(True, 1)
-    step_device()  # warm: the right-view buffers are allocated on first use
-    barrier()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for st in [torch.cuda.ExternalStream(c.stream) for c in ctxs][1:]:
-        st.wait_event(a)
-    step_device()
-    for c in ctxs[1:]:
-        ev = torch.cuda.Event()
-        ev.record(torch.cuda.ExternalStream(c.stream))
-        stream.wait_event(ev)
-    b.record(stream)
-    b.synchronize()
-    out["lr_check_chain"] = {"value": F / (a.elapsed_time(b) / 1000.0), "unit": "pairs/s",
-                             "note": "full chain + right-view sweep + LR check, 1 step"}
-    for c in ctxs:
-        c.set_lr_check(False)
-    barrier()
-    if od is not None:
-        # fusion of the step's device-resident clouds into one surfel model
-        # (a slow pan: 1 mm and 0.1 mrad per frame), device events around it
-        from paper_2007_12623_b200.synth import default_rig
-        rig = default_rig(W, H)
-        model = ss.fusion.SurfelModel(torch.cuda.current_device())
-        nf = min(F, 32)
-        poses = []
-        for f in range(nf):
-            a_ = 1e-4 * f
-            poses.append(np.array([[np.cos(a_), 0, np.sin(a_), 1.0 * f], [0, 1, 0, 0],
-                                   [-np.sin(a_), 0, np.cos(a_), 0]]))
-        N = W * H
+    for name, (what, ops) in census.items():
+        ms, launches = stages.get(name, (0.0, 0))
+        if ms <= 0 or launches <= 0:
+            continue
+        per_launch = ops * frames_timed / launches
+        t = ms / launches / 1e3
+        out[name] = {"kernel": what, "bound": "alu", "achieved": per_launch / t / 1e12,
+                     "peak": alu_peak / 1e12, "unit": "Tlane-op/s",
+                     "frac": per_launch / t / alu_peak, "ops_per_launch": per_launch,
+                     "avg_launch_ms": t * 1e3, "launches": launches,
+                     "share_of_chain": None}
+    for name, (what, nbytes) in hbm.items():
+        ms, launches = stages.get(name, (0.0, 0))
+        if ms <= 0 or launches <= 0:
+            continue
+        per_launch = nbytes * frames_timed / launches
+        t = ms / launches / 1e3
+        out[name] = {"kernel": what, "bound": "hbm", "achieved": per_launch / t / 1e9,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": per_launch / t / 1e9 / hbm_peak,
+                     "bytes_per_launch": per_launch, "avg_launch_ms": t * 1e3,
+                     "launches": launches, "share_of_chain": None}
+    chain_ms = sum(stages[k][0] for k in ("luma", "stats", "wta_sweep", "wta_resolve", "cleanup",
+                                          "refine", "cloud"))
+    for name, r in out.items():
+        r["share_of_chain"] = stages[name][0] / chain_ms if chain_ms else None
+    # whole-stage view (census per pair over the stage's per-pair time)
+    stage_census = {"wta_sweep": 15.0 * N * D,
+                    "cleanup": 216.0 * N + I_DISC[args.workload] * (82 + 3 * 1256),
+                    "refine": 1910.0 * N, "cloud": 700.0 * N,
+                    "luma+stats": 36.0 * N}
+    per_stage = {}
+    for name, ops in stage_census.items():
+        ms = (stages["luma"][0] + stages["stats"][0]) if name == "luma+stats" else stages[name][0]
+        if ms > 0:
+            t = ms / frames_timed / 1e3
+            per_stage[name] = {"us_per_pair": t * 1e6, "frac": ops / t / alu_peak}
+    return out, per_stage, alu_peak
 
-        def fuse_all(m):
-            for f in range(nf):
-                m.fuse_device(od["index"][f].data_ptr(), od["points"][f].data_ptr(),
-                              od["normals"][f].data_ptr(), od["colors"][f].data_ptr(),
-                              poses[f], rig)
 
-        fuse_all(model)  # warm (allocations)
-        model.close()
-        model = ss.fusion.SurfelModel(torch.cuda.current_device())
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        fuse_all(model)
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        out["fusion"] = {"frames_per_s": nf / dt, "frames": nf, "surfels": len(model),
-                         "note": "fuse_device of C1 clouds (~0.5 M points each) into one model; "
-                                 "host wall clock around synchronous calls"}
-        model.close()
-    # C3 / C5 geometry (BASELINE.json configs[2], [4]): 1920x1080, D = 128; and
-    # C2 (960x540 low-texture, D = 64): device-resident throughput over
-    # synthetic pairs (6 seeded, tiled)
-    for key, kind, Wf, Hf, Df, nf, Bf, nctx in (("fhd_d128", "textured", 1920, 1080, 128, 48, 8, 2),
-                                                ("lowtex_c2", "lowtex", 960, 540, 64, 128, 16, 4)):
-        try:
-            out[key] = geometry_throughput(ss, kind, Wf, Hf, Df, nf, Bf, nctx)
-        except Exception as e:  # informational side measurement
-            out[key] = {"error": str(e)[:200]}
-    gl = ss.to_gray(Lh_first)
-    gr = ss.to_gray(Rh_first)
+# ---------------------------------------------------------------- our arm
 
-    def feat_gpu():
-        fl = ss.features.describe(gl, ss.features.detect_corners(gl, 2000, 20))
-        fr = ss.features.describe(gr, ss.features.detect_corners(gr, 2000, 20))
-        return ss.features.match_features(*fl, *fr, 64)
-
-    def feat_cpu(ref):
-        cl = ref.detect_corners(gl, 2000, 20)
-        cr = ref.detect_corners(gr, 2000, 20)
-        fl, fr = ref.describe(gl, cl), ref.describe(gr, cr)
-        return ref.match_features(*fl, *fr, 64)
-
-    feat_gpu()
-    t = []
-    for _ in range(5):
-        t0 = time.perf_counter()
-        m = feat_gpu()
-        t.append(time.perf_counter() - t0)
-    out["features_pair"] = {"gpu_ms": 1000 * statistics.median(t), "matches": int(len(m["index_a"])),
-                            "what": "detect_corners(2000, thr 20) + describe on both C1 views + "
-                                    "match_features(64), per-stage C-ABI incl. H2D/D2H"}
-    try:
-        from oracle.oracle import Oracle
-        if Oracle.available("ref"):
-            ref = Oracle("ref")
-            t = []
-            for _ in range(3):
-                t0 = time.perf_counter()
-                feat_cpu(ref)
-                t.append(time.perf_counter() - t0)
-            out["features_pair"]["cpu_reference_ms"] = 1000 * statistics.median(t)
-            out["features_pair"]["cpu_cores"] = os.cpu_count()
-    except Exception as e:  # the CPU side is informational
-        out["features_pair"]["cpu_reference_error"] = str(e)[:200]
-    return out
+def run_dry(args):
+    """Launcher / sharding check without a GPU (tests/test_bench_contract.py)."""
+    import torch.distributed as dist
+    from paper_2007_12623_b200.shard import frame_range, max_over_ranks
+    world, rank, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    n = local_frames(args, rank, world)
+    t = max_over_ranks(float(rank + 1))
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "gpus_flag": args.gpus,
+                          "frames_rank0": n, "max_over_ranks": t,
+                          "block0": frame_range(args.frames, 0, world)
+                          if WORKLOADS[args.workload]["scaling"] == "strong" else None}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def run_ours(args):
@@ -401,6 +480,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2007_12623_b200 as ss
+    from paper_2007_12623_b200.shard import max_over_ranks
     from paper_2007_12623_b200.synth import default_rig, params_for
 
     world, rank, local = dist_env()
@@ -409,38 +489,47 @@ def run_ours(args):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    F, B = args.frames, args.batch
+    wl = WORKLOADS[args.workload]
+    W, H, D = wl["W"], wl["H"], wl["D"]
     N = W * H
-    Lh_np, Rh_np = make_frames(rank, world, F, args.unique)
-    # pinned host inputs (e2e) and HBM-resident copies (device value)
-    Lh = torch.from_numpy(Lh_np).pin_memory()
-    Rh = torch.from_numpy(Rh_np).pin_memory()
-    Ld, Rd = Lh.to(dev), Rh.to(dev)
-    del Lh_np, Rh_np
+    B, S = args.batch, max(1, args.streams)
+    F = local_frames(args, rank, world)
+    strong = wl["scaling"] == "strong"
+    Lu_np, Ru_np = make_unique(args, rank, world, F)
+    u = len(Lu_np)
+    assert u % B == 0 or F <= u, "unique frames must tile into whole launches"
+    # HBM-resident inputs. c4/c2/c3: one distinct copy per frame of the step
+    # (> L2); c5: the 32 distinct frames in rotation.
+    Lu = torch.from_numpy(Lu_np).to(dev)
+    Ru = torch.from_numpy(Ru_np).to(dev)
+    if strong:
+        Ld, Rd = Lu, Ru
+        in_index = [i % u for i in range(F)]
+    else:
+        reps = (F + u - 1) // u
+        Ld = Lu.repeat(reps, 1, 1, 1)[:F].contiguous()
+        Rd = Ru.repeat(reps, 1, 1, 1)[:F].contiguous()
+        in_index = list(range(F))
     flags = ss.SS_OUT_DISPARITY | ss.SS_OUT_CLOUD | ss.SS_OUT_NORMALS
-    od = {"disparity": torch.empty((F, H, W), dtype=torch.float32, device=dev),
-          "valid": torch.empty((F, H, W), dtype=torch.uint8, device=dev),
-          "index": torch.empty((F, H, W), dtype=torch.int32, device=dev),
-          "points": torch.empty((F, N, 3), dtype=torch.float32, device=dev),
-          "normals": torch.empty((F, N, 3), dtype=torch.float32, device=dev),
-          "colors": torch.empty((F, N, 3), dtype=torch.uint8, device=dev),
-          "n_points": torch.empty((F,), dtype=torch.int32, device=dev)}
+    # device outputs: all frames of the step (weak); a ring of 2 launches per
+    # context (strong: the stream's consumer has drained a slot before reuse)
+    n_out = F if not strong else min(F, 2 * S * B)
+    od = ss.StereoContext.alloc_outputs(n_out, H, W, flags,
+                                        alloc=lambda s, dt: torch.empty(s, dtype=dt, device=dev))
     p = params_for(D)
-    # S contexts, one CUDA stream each: 16-frame chunks go round-robin, so one
-    # chunk's latency-bound phases (serial FP64 scans, small exact-resolve
-    # grids, launch tails) overlap another's wide kernels.
-    S = max(1, args.streams)
-    ctxs = [ss.StereoContext(local, W, H, B, ss.StereoParams(**p), ss.StereoRig(**default_rig(W, H)))
-            for _ in range(S)]
+    ctxs = [ss.StereoContext(local, W, H, B, ss.StereoParams(**p),
+                             ss.StereoRig(**default_rig(W, H))) for _ in range(S)]
     ctx = ctxs[0]
     streams = [torch.cuda.ExternalStream(c.stream, device=dev) for c in ctxs]
     stream = streams[0]
+    chunks = [(f0, min(B, F - f0)) for f0 in range(0, F, B)]
 
     def step_device(cs=ctxs):
-        for i, f0 in enumerate(range(0, F, B)):
-            m = min(B, F - f0)
-            d_out = {k: t[f0:f0 + m].data_ptr() for k, t in od.items()}
-            cs[i % len(cs)].run_device(m, W, H, Ld[f0].data_ptr(), Rd[f0].data_ptr(), flags,
+        for i, (f0, m) in enumerate(chunks):
+            o0 = f0 % n_out
+            d_out = {k: t[o0:o0 + m].data_ptr() for k, t in od.items()}
+            j = in_index[f0]
+            cs[i % len(cs)].run_device(m, W, H, Ld[j].data_ptr(), Rd[j].data_ptr(), flags,
                                        d_out=d_out)
 
     def barrier():
@@ -473,36 +562,68 @@ def run_ours(args):
         barrier()
     ms = e0.elapsed_time(e1)
     stats = {k: sum(c.stats()[k] for c in ctxs) for k in ctxs[0].stats()}
-    # Per-stage device times (and the sweep's roofline) from one extra,
-    # untimed-for-value step on a single context: kernels of concurrent
-    # streams would inflate each other's event brackets.
+
+    # ---- parity of the timed step's own outputs (rank 0 holds the digest frames)
+    dig, keys = digest_keys(args)
+    parity = None
+    if rank == 0 and keys:
+        keys = keys[:min(len(keys), F)]
+        if strong:  # the ring was overwritten: re-run the stream's first launch
+            ctx.run_device(B, W, H, Ld[0].data_ptr(), Rd[0].data_ptr(), flags,
+                           d_out={k: t[0:B].data_ptr() for k, t in od.items()})
+            ctx.sync()
+        torch.cuda.synchronize(dev)
+        hk = {k: t[:len(keys)].cpu().numpy() for k, t in od.items()}
+        bad = check_frames(lambda i: {k: v[i] for k, v in hk.items()}, keys, dig)
+        parity = {"reference": "SHA-256 of oracle/_ref outputs (tests/golden/digests.json)",
+                  "device_frames_checked": len(keys), "device_frames_mismatched": bad}
+
+    # ---- per-kernel-group device times on one context (no concurrency)
     ctx.enable_timing(True)
     step_device([ctx])
     barrier()
     stages = ctx.stage_times()
     ctx.enable_timing(False)
-    from paper_2007_12623_b200.shard import max_over_ranks
     ms_max = max_over_ranks(ms, device=dev)
-    pairs = world * F * args.steps
+    pairs = (args.frames if strong else world * F) * args.steps
     value = pairs / (ms_max / 1000.0)
 
     # ---- e2e through the public host API (pinned host buffers) ----
-    e2e_value, h2d, d2h = None, 0, 0
+    e2e_value, h2d, d2h, e2e_extra = None, 0, 0, {}
     if args.e2e_steps > 0:
-        ho = ss.StereoContext.alloc_outputs(F, H, W, flags,
-                                            alloc=lambda s, dt: ss.pinned_empty(s, dt))
-        # the S contexts take contiguous frame ranges, one host thread each
-        # (ss_stereo_batch is synchronous; ctypes releases the GIL)
-        cuts = [F * i // S for i in range(S + 1)]
-        Lnp, Rnp = Lh.numpy(), Rh.numpy()
+        Lh = ss.pinned_empty(tuple(Ld.shape), np.uint8)
+        Rh = ss.pinned_empty(tuple(Rd.shape), np.uint8)
+        Lh[...] = Ld.cpu().numpy()
+        Rh[...] = Rd.cpu().numpy()
+        if strong:
+            # per-thread host ring of 2 launches; each chunk is consumed
+            # (its clouds summed) before the ring slot is reused
+            ho = [ss.StereoContext.alloc_outputs(2 * B, H, W, flags,
+                                                 alloc=lambda s, dt: ss.pinned_empty(s, dt))
+                  for _ in range(S)]
+            consumed = [0] * S
 
-        def e2e_part(i, steps):
-            a, b = cuts[i], cuts[i + 1]
-            for _ in range(steps):
-                ctxs[i].run(Lnp[a:b], Rnp[a:b], flags, out={k: v[a:b] for k, v in ho.items()})
+            def e2e_part(k, steps):
+                for _ in range(steps):
+                    for ci in range(k, len(chunks), S):
+                        f0, m = chunks[ci]
+                        j = in_index[f0]
+                        slot = (ci // S) % 2
+                        o = {kk: v[slot * B:slot * B + m] for kk, v in ho[k].items()}
+                        ctxs[k].run(Lh[j:j + m], Rh[j:j + m], flags, out=o)
+                        consumed[k] += int(o["n_points"].sum())
+        else:
+            ho_all = ss.StereoContext.alloc_outputs(F, H, W, flags,
+                                                    alloc=lambda s, dt: ss.pinned_empty(s, dt))
+            cuts = [F * i // S for i in range(S + 1)]
+
+            def e2e_part(k, steps):
+                a, b = cuts[k], cuts[k + 1]
+                for _ in range(steps):
+                    ctxs[k].run(Lh[a:b], Rh[a:b], flags, out={kk: v[a:b] for kk, v in ho_all.items()})
 
         def e2e_all(steps):
-            th = [threading.Thread(target=e2e_part, args=(i, steps)) for i in range(S)]
+            th = [threading.Thread(target=e2e_part, args=(k, steps)) for k in range(S)]
             for t in th:
                 t.start()
             for t in th:
@@ -517,10 +638,19 @@ def run_ours(args):
         f1e.synchronize()
         barrier()
         ems = max_over_ranks(f0e.elapsed_time(f1e), device=dev)
-        e2e_value = world * F * args.e2e_steps / (ems / 1000.0)
+        e2e_value = (args.frames if strong else world * F) * args.e2e_steps / (ems / 1000.0)
         h2d = 2 * F * N * 3
         # cloud arrays leave at full per-frame capacity (ss_stereo_batch pipeline)
         d2h = F * N * (4 + 1 + 4) + 4 * F + F * N * (12 + 12 + 3)
+        e2e_extra = {"d2h_bytes_per_pair": d2h / F, "d2h_gbs_per_gpu":
+                     d2h * args.e2e_steps / (ems / 1000.0) / 1e9}
+        if strong:
+            e2e_extra["host_ring_frames_per_thread"] = 2 * B
+            e2e_extra["points_consumed"] = int(sum(consumed))
+        if parity is not None and not strong:
+            bad = check_frames(lambda i: {k: v[i] for k, v in ho_all.items()}, keys, dig)
+            parity["e2e_frames_checked"] = len(keys)
+            parity["e2e_frames_mismatched"] = bad
 
     if world > 1:
         dist.barrier()
@@ -534,69 +664,83 @@ def run_ours(args):
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {}
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    alu_peak = n_sm * 128 * sm_max * 1e6  # lane-ops/s
-    wta_ms, wta_launches = stages["wta_sweep"]
-    per_frame_ops = N * (12 * (D + 10) + 3 * D)
-    launches = max(wta_launches, 1)
-    frames_timed = F  # the single-context stage-timing step
-    ops_per_launch = per_frame_ops * frames_timed / launches
-    achieved = ops_per_launch / (wta_ms / launches / 1000.0) if wta_ms > 0 else 0.0
     hbm_peak = float(peaks.get("hbm_gbs", 6446.9))
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    groups, per_stage, alu_peak = roofline_report(args, stages, F, n_sm, sm_max, hbm_peak,
+                                                  iters=p["refine_iterations"])
+    top = max(groups, key=lambda k: groups[k]["share_of_chain"] or 0.0)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(tpath):
-        t = json.load(open(tpath)).get("k_wta11", {})
-        if t.get("frames_per_launch") == B:
+        t = json.load(open(tpath)).get(top, {})
+        if t.get("frames_per_launch") == B and t.get("workload") == args.workload:
             traffic = t.get("dram_bytes_per_launch")
-    roofline = {
-        "bound": "alu", "kernel": "k_wta11 (ZNCC cost sweep + WTA)",
-        "achieved": achieved / 1e12, "peak": alu_peak / 1e12, "unit": "Tlane-op/s",
-        "frac": achieved / alu_peak if alu_peak else None, "traffic": traffic,
-        "traffic_unit": "DRAM bytes per launch (ncu, profiles/roofline_traffic.json)",
+    roofline = dict(groups[top])
+    roofline.update({
+        "group": top, "traffic": traffic,
+        "traffic_unit": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                        "(profiles/roofline_traffic.json)",
         "peak_source": f"{n_sm} SM x 128 lanes x sm_max_mhz {sm_max:.0f} (MEASURED_PEAKS.json); "
                        "ALU issue, not a bf16/HBM figure: the path is integer/FP64 ALU work",
-        "ops_per_launch": ops_per_launch, "avg_launch_ms": wta_ms / launches,
-        "hbm_view": ({"achieved_gbs": traffic / (wta_ms / launches / 1000.0) / 1e9,
-                      "peak_gbs": hbm_peak,
-                      "frac": traffic / (wta_ms / launches / 1000.0) / 1e9 / hbm_peak,
-                      "note": "ncu DRAM bytes per launch over the live launch time: the "
-                              "sweep is not HBM-bound"}
-                     if traffic and wta_ms > 0 else None),
-        "pipeline_census_frac": CENSUS["textured"] * value / world / alu_peak,
-        "hbm_frac_pipeline": 21.8e6 * value / world / (hbm_peak * 1e9),
-    }
+        "stages": per_stage, "kernel_groups": groups,
+        "pipeline_census_frac": CENSUS_TOTAL[args.workload] * value / world / alu_peak,
+        "hbm_frac_pipeline": (21.8e6 if N < 1e6 else 87.1e6) * value / world / (hbm_peak * 1e9),
+    })
+
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        pairs_cpu = cpu_pairs(args.cpu_pairs)
-        tcpu, kind = reference_chain(pairs_cpu)
-        cpu = {"value": len(pairs_cpu) / tcpu, "unit": "pairs/s", "cores": os.cpu_count(),
+        npairs = min(args.cpu_pairs, F)
+        pairs_cpu = workload_pairs(args, npairs)
+        tcpu, kind, routs = reference_chain(pairs_cpu, wl, want_outputs=True)
+        cpu = {"value": npairs / tcpu, "unit": "pairs/s", "cores": os.cpu_count(),
                "kind": kind, "cpu_model": cpu_model(),
-               "sample": f"{len(pairs_cpu)} C1 pairs (960x540 D=64) through oracle/_ref "
-                         "(unmodified reference, OpenMP all cores) + restated cloud"}
-        if omp_threads(1):  # also one thread
-            t1, _ = reference_chain(pairs_cpu[:1])
+               "sample": f"the workload's first {npairs} pairs through oracle/_ref (unmodified "
+                         "reference, OpenMP all cores) + restated cloud"}
+        # whole-array comparison of those frames with this run's device outputs
+        if not strong or npairs <= B:
+            if strong:
+                ctx.run_device(B, W, H, Ld[0].data_ptr(), Rd[0].data_ptr(), flags,
+                               d_out={k: t[0:B].data_ptr() for k, t in od.items()})
+                ctx.sync()
+            torch.cuda.synchronize(dev)
+            mism = 0
+            for i, (d, v, cl) in enumerate(routs):
+                gd = od["disparity"][i].cpu().numpy()
+                gv = od["valid"][i].cpu().numpy()
+                mism += int((gv != v).sum()) + int((gd.view(np.uint32) != d.view(np.uint32)).sum())
+            if parity is None:
+                parity = {}
+            parity["live_reference_frames"] = npairs
+            parity["live_reference_mismatched_px"] = mism
+        if omp_threads(1) and args.workload in ("c4", "c2"):  # also one thread
+            t1, _, _ = reference_chain(pairs_cpu[:1], wl)
             cpu["single_thread_value"] = 1.0 / t1
             omp_threads(os.cpu_count())
     if cpu is not None and args.cpu_configs:
         cpu["side_by_side"] = cpu_side_by_side()
-    stage_ms_per_pair = {k: v[0] / frames_timed for k, v in stages.items()}
-    ext = None if (args.no_extensions or world > 1) else extensions(ss, ctxs, step_device, barrier, stream, F,
-                                                     Lh_first=Lh[0].numpy(), Rh_first=Rh[0].numpy(),
-                                                     od=od)
+    ok = True
+    if parity is not None:
+        ok = (not parity.get("device_frames_mismatched") and not parity.get("e2e_frames_mismatched")
+              and not parity.get("live_reference_mismatched_px"))
+        parity["ok"] = ok
+    ext = None
+    if not (args.no_extensions or world > 1 or args.workload != "c4"):
+        ext = extensions(ss, ctxs, step_device, barrier, stream, F, Lu_np[0], Ru_np[0], od, W, H)
     line = {
-        "metric": "stereo pairs/sec at 960x540 D=64", "value": value, "unit": "pairs/s",
+        "metric": "stereo pairs/sec", "value": value, "unit": "pairs/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": wl["scaling"],
         "vs_baseline": None, "dtype": "u8/int32/f32-filter/f64", "data": "synthetic",
         "config": config_dict(args, world),
-        "ms_per_pair": ms_max / args.steps / F,
-        "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+        "workload": args.workload, "pairs_per_step_per_gpu": F, "frames_per_launch": B,
+        "streams_per_gpu": S,
+        "ms_per_pair": ms_max / args.steps / (pairs / args.steps / world),
+        "e2e": dict({"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
+                     "d2h_bytes_per_step": d2h}, **e2e_extra),
         "gpu_launches": int(stats["kernel_launches"]),
-        "roofline": roofline, "cpu_baseline": cpu,
+        "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
         "clocks": clk.summary(),
-        "stage_ms_per_pair": stage_ms_per_pair,
+        "stage_ms_per_pair": {k: v[0] / F for k, v in stages.items()},
         "exact_resolves": {"wta_pixels": stats["wta_resolved"],
                            "refine_repicks": stats["refine_resolved"],
                            "frames": stats["frames"]},
@@ -607,11 +751,106 @@ def run_ours(args):
         c.close()
     if world > 1:
         dist.destroy_process_group()
+    if not ok:
+        print("bench.py: outputs differ from the reference digests", file=sys.stderr)
+        sys.exit(1)
+
+
+def extensions(ss, ctxs, step_device, barrier, stream, F, L0, R0, od, W, H):
+    """Side measurements of the SURVEY §8f rows (not the headline metric):
+    the chain with the opt-in LR check (device pairs/s, same workload), fusion
+    of the step's device-resident clouds, and the feature front end on one C1
+    frame pair through the per-stage C-ABI (host buffers, transfers included)
+    beside the reference's CPU code."""
+    import torch
+    out = {}
+    for c in ctxs:
+        c.set_lr_check(True, 1)
+    step_device()  # warm: the right-view buffers are allocated on first use
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for st in [torch.cuda.ExternalStream(c.stream) for c in ctxs][1:]:
+        st.wait_event(a)
+    step_device()
+    for c in ctxs[1:]:
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.ExternalStream(c.stream))
+        stream.wait_event(ev)
+    b.record(stream)
+    b.synchronize()
+    out["lr_check_chain"] = {"value": F / (a.elapsed_time(b) / 1000.0), "unit": "pairs/s",
+                             "note": "full chain + right-view sweep + LR check, 1 step"}
+    for c in ctxs:
+        c.set_lr_check(False)
+    barrier()
+    from paper_2007_12623_b200.synth import default_rig
+    rig = default_rig(W, H)
+    model = ss.fusion.SurfelModel(torch.cuda.current_device())
+    nf = min(F, 32)
+    poses = []
+    for f in range(nf):
+        a_ = 1e-4 * f
+        poses.append(np.array([[np.cos(a_), 0, np.sin(a_), 1.0 * f], [0, 1, 0, 0],
+                               [-np.sin(a_), 0, np.cos(a_), 0]]))
+
+    def fuse_all(m):
+        for f in range(nf):
+            m.fuse_device(od["index"][f].data_ptr(), od["points"][f].data_ptr(),
+                          od["normals"][f].data_ptr(), od["colors"][f].data_ptr(), poses[f], rig)
+
+    fuse_all(model)  # warm (allocations)
+    model.close()
+    model = ss.fusion.SurfelModel(torch.cuda.current_device())
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    fuse_all(model)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    out["fusion"] = {"frames_per_s": nf / dt, "frames": nf, "surfels": len(model),
+                     "note": "fuse_device of C1 clouds (~0.5 M points each) into one model; "
+                             "host wall clock around synchronous calls"}
+    model.close()
+    gl = ss.to_gray(L0)
+    gr = ss.to_gray(R0)
+
+    def feat_gpu():
+        fl = ss.features.describe(gl, ss.features.detect_corners(gl, 2000, 20))
+        fr = ss.features.describe(gr, ss.features.detect_corners(gr, 2000, 20))
+        return ss.features.match_features(*fl, *fr, 64)
+
+    feat_gpu()
+    t = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        m = feat_gpu()
+        t.append(time.perf_counter() - t0)
+    out["features_pair"] = {"gpu_ms": 1000 * statistics.median(t), "matches": int(len(m["index_a"])),
+                            "what": "detect_corners(2000, thr 20) + describe on both C1 views + "
+                                    "match_features(64), per-stage C-ABI incl. H2D/D2H"}
+    try:
+        from oracle.oracle import Oracle
+        if Oracle.available("ref"):
+            ref = Oracle("ref")
+            t = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                cl, cr = ref.detect_corners(gl, 2000, 20), ref.detect_corners(gr, 2000, 20)
+                ref.match_features(*ref.describe(gl, cl), *ref.describe(gr, cr), 64)
+                t.append(time.perf_counter() - t0)
+            out["features_pair"]["cpu_reference_ms"] = 1000 * statistics.median(t)
+            out["features_pair"]["cpu_cores"] = os.cpu_count()
+    except Exception as e:  # the CPU side is informational
+        out["features_pair"]["cpu_reference_error"] = str(e)[:200]
+    return out
 
 
 def main():
     args = parse()
-    if args.impl == "reference":
+    self_launch(args)
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -14,8 +14,10 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
 SS_OK, SS_EINVAL, SS_EPARAM, SS_ECUDA, SS_ENOMEM, SS_ENODEV = range(6)
 SS_IN_RGB, SS_IN_GRAY = 0, 1
 SS_OUT_DISPARITY, SS_OUT_CLOUD, SS_OUT_NORMALS = 1, 2, 4
-SS_N_STAGES = 7
-STAGE_NAMES = ["luma", "stats", "wta_sweep", "wta_resolve", "cleanup", "refine", "cloud"]
+SS_N_STAGES = 14
+STAGE_NAMES = ["luma", "stats", "wta_sweep", "wta_resolve", "cleanup", "refine", "cloud",
+               "cleanup_outliers", "cleanup_radial", "cleanup_disc", "refine_scan", "refine_repick",
+               "refine_exact", "cloud_normals"]
 
 
 class SsParams(C.Structure):

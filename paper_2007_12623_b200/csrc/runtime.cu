@@ -74,23 +74,36 @@ void require_device() {
   tl_gpu = true;
 }
 
-// Growable device arena.
+// Growable device arena. A borrowed buffer wraps caller memory (the batch
+// API's output pointers): it is never freed and never grows.
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  bool borrowed = false;
   void ensure(size_t need) {
     if (need <= bytes) return;
+    if (borrowed) raise(SS_EINVAL, "output buffer smaller than the batch needs");
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
-    need = std::max<size_t>(need, 256);
+    // grow geometrically so alternating frame sizes do not free/realloc
+    // (cudaFree synchronizes the device) on every call
+    need = std::max<size_t>(need + need / 8, 256);
     ck(cudaMalloc(&p, need), "cudaMalloc");
     bytes = need;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p && !borrowed) cudaFree(p);
     p = nullptr;
     bytes = 0;
+    borrowed = false;
+  }
+  static DevBuf borrow(void* q, size_t n) {
+    DevBuf b;
+    b.p = q;
+    b.bytes = n;
+    b.borrowed = true;
+    return b;
   }
   template <class T>
   T* as() const {
@@ -183,7 +196,9 @@ struct ss_ctx {
   DevBuf o, oi, d, avg, b, psum, pcnt, cnt, span, wtab, fspan, fx, emap;
   DevBuf index, block_sums, npoints, pts_f, nrm_f, colors, pts_d, nrm_d, pixels, pts4;
   DevBuf counters, trace_o, trace_d, so, chg, chg_count, mbt, defer, defer_count;
-  int wtab_radius = -1;
+  int wtab_radius = -1, span_radius = -1;
+  std::vector<double> wtab_host;
+  std::vector<int> fspan_host, span_host;
 
   // ss_stereo_batch pipeline: chunk k uses slot k % 2 — its inputs arrive on
   // s_in while chunk k-1 computes on `stream` and chunk k-2's outputs leave on
@@ -218,10 +233,9 @@ struct ss_ctx {
   double stage_ms[SS_N_STAGES] = {};
   int64_t stage_launches[SS_N_STAGES] = {};
   // which buffer holds the final map of the last run
-  float* last_disp = nullptr;
-  uint8_t* last_valid = nullptr;
-  long last_N = 0;
-  int last_frames = 0;
+  // device pointers of the last chain's results (ss_ctx_device_outputs);
+  // they may be caller buffers (ss_stereo_batch_device) or slot buffers
+  ss_batch_out last{};
 
   ~ss_ctx() {
     for (DevBuf* b : {&in_l, &in_r, &gray_l, &gray_r, &ltap_buf, &rcopy_buf, &lstat, &rstat, &win, &wbase,
@@ -446,14 +460,18 @@ struct ss_ctx {
         if (dd > 0 && dd <= r2)
           w[(size_t)(dv + R) * D + (du + R)] = 1.0 / std::sqrt(static_cast<double>(dd));
       }
-    wtab.ensure(sizeof(double) * w.size());
-    ck(cudaMemcpy(wtab.p, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice), "wtab");
+    // stream-ordered uploads from host copies that live as long as the ctx
+    wtab_host.swap(w);
+    wtab.ensure(sizeof(double) * wtab_host.size());
+    ck(cudaMemcpyAsync(wtab.p, wtab_host.data(), sizeof(double) * wtab_host.size(),
+                       cudaMemcpyHostToDevice, stream), "wtab");
     // disc rows: |du| <= floor(sqrt(r^2 - dv^2))  <=>  du^2 + dv^2 <= r^2
-    std::vector<int> sp(R + 1);
+    fspan_host.assign(R + 1, 0);
     for (int dv = 0; dv <= R; ++dv)
-      sp[dv] = (int)std::floor(std::sqrt((double)(r2 - dv * dv)));
-    fspan.ensure(sizeof(int) * sp.size());
-    ck(cudaMemcpy(fspan.p, sp.data(), sizeof(int) * sp.size(), cudaMemcpyHostToDevice), "fspan");
+      fspan_host[dv] = (int)std::floor(std::sqrt((double)(r2 - dv * dv)));
+    fspan.ensure(sizeof(int) * fspan_host.size());
+    ck(cudaMemcpyAsync(fspan.p, fspan_host.data(), sizeof(int) * fspan_host.size(),
+                       cudaMemcpyHostToDevice, stream), "fspan");
     wtab_radius = radius;
   }
 
@@ -487,16 +505,24 @@ struct ss_ctx {
       // only those into b, reading a (the reference's no-cascade input map);
       // the disc fill reads b and writes a — the round ends in a, no copies
       ck(cudaMemsetAsync(flag_count.p, 0, sizeof(unsigned) * n, stream), "memset");
+      {
+      Stage so(this, 7);
       launch_remove_outliers(disp_a.as<float>(), valid_a.as<uint8_t>(), nullptr,
                              valid_a.as<uint8_t>(), W, H, r, params.neighbor_jump_threshold,
                              emap.as<uint32_t>(), n, N, stream, disp_b.as<float>(),
                              valid_b.as<uint8_t>(), flags.as<int>(), flag_count.as<unsigned>());
+      stats.kernel_launches += r > 0 ? 2 : 1;
+      }
+      {
+      Stage sr(this, 8);
       launch_fill_radial_list(disp_a.as<float>(), valid_a.as<uint8_t>(), disp_b.as<float>(),
                               valid_b.as<uint8_t>(), W, H, params.fill_radius_radial, 4,
                               flags.as<int>(), flag_count.as<unsigned>(), n, N, stream);
+      stats.kernel_launches += 1;
+      }
+      Stage sd(this, 9);
       fill_disc(n, W, H, disp_b.as<float>(), valid_b.as<uint8_t>(), disp_a.as<float>(),
                 valid_a.as<uint8_t>(), params.fill_radius_disc, disc_support);
-      stats.kernel_launches += 2;
     }
   }
 
@@ -516,12 +542,15 @@ struct ss_ctx {
     pcnt.ensure(sizeof(int) * bp * n);     // BT prefix (int)
     mbt.ensure(bs * n);                    // BT mask
     cnt.ensure(sizeof(int) * bs * n);
-    std::vector<int> sp(std::max(r, 0) + 1);
-    for (int dy = 0; dy <= r; ++dy)
-      sp[dy] = (int)std::floor(std::sqrt((double)r * r - (double)dy * dy));
-    span.ensure(sizeof(int) * sp.size());
-    ck(cudaMemcpyAsync(span.p, sp.data(), sizeof(int) * sp.size(), cudaMemcpyHostToDevice, stream),
-       "span");
+    if (span_radius != r) {  // smoothing.cpp:22-26 row half-widths, uploaded once per radius
+      span_host.assign(std::max(r, 0) + 1, 0);
+      for (int dy = 0; dy <= r; ++dy)
+        span_host[dy] = (int)std::floor(std::sqrt((double)r * r - (double)dy * dy));
+      span.ensure(sizeof(int) * span_host.size());
+      ck(cudaMemcpyAsync(span.p, span_host.data(), sizeof(int) * span_host.size(),
+                         cudaMemcpyHostToDevice, stream), "span");
+      span_radius = r;
+    }
     RefineArgs a{};
     a.g = g;
     a.alpha = params.alpha;
@@ -570,22 +599,33 @@ struct ss_ctx {
     defer_count.ensure(sizeof(unsigned) * n);
     auto repick = [&](const double* avgp, int2* chgp, unsigned* chgc) {
       ck(cudaMemsetAsync(defer_count.p, 0, sizeof(unsigned) * n, stream), "memset");
+      {
+      Stage sp(this, 11);
       launch_d_repick(psum.as<double>(), mT, cnt.as<int>(), avgp, so.as<int>(), d.as<double>(),
                       op, gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), winp, wbase.as<int>(),
                       chgp, chgc, defer.as<Deferred>(), defer_count.as<unsigned>(), a, n, N,
                       stream);
+      stats.kernel_launches += 1;
+      }
+      Stage sx(this, 12);
       launch_repick_exact(defer.as<Deferred>(), defer_count.as<unsigned>(), op,
                           gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), chgp, chgc, a, n, N,
                           ctr() + 1, stream);
-      stats.kernel_launches += 2;
+      stats.kernel_launches += 1;
     };
     for (int it = 0; it < iters; ++it) {
       if (it == 0) {
         // o is the cleanup output (fractional fills): the reference's FP64 path.
-        launch_scan_bt_d(o.as<double>(), mT, psum.as<double>(), W, H, r, n, stream);
+        {
+          Stage ss(this, 10);
+          launch_scan_bt_d(o.as<double>(), mT, psum.as<double>(), W, H, r, n, stream);
+        }
         launch_avg_b(psum.as<double>(), mT, cnt.as<int>(), o.as<double>(), d.as<double>(),
                      avg.as<double>(), b.as<double>(), a, n, stream);
-        launch_scan_bt_d(b.as<double>(), mT, psum.as<double>(), W, H, r, n, stream);
+        {
+          Stage ss(this, 10);
+          launch_scan_bt_d(b.as<double>(), mT, psum.as<double>(), W, H, r, n, stream);
+        }
         stats.kernel_launches += 3;
         repick(avg.as<double>(), nullptr, nullptr);
         if (iters > 1) {
@@ -596,8 +636,11 @@ struct ss_ctx {
         }
       } else {
         ck(cudaMemsetAsync(chg_count.p, 0, sizeof(unsigned) * n, stream), "memset");
-        launch_scan_b(so.as<int>(), cnt.as<int>(), op, d.as<double>(), mT, a.alpha,
-                      a.one_minus_alpha, psum.as<double>(), W, H, r, n, stream);
+        {
+          Stage ss(this, 10);
+          launch_scan_b(so.as<int>(), cnt.as<int>(), op, d.as<double>(), mT, a.alpha,
+                        a.one_minus_alpha, psum.as<double>(), W, H, r, n, stream);
+        }
         stats.kernel_launches += 1;
         repick(nullptr, chg.as<int2>(), chg_count.as<unsigned>());
         if (it + 1 < iters) {
@@ -656,6 +699,7 @@ struct ss_ctx {
                         rgb_stride, stream);
     stats.kernel_launches += 1;
     if (want_normals) {
+      Stage sn(this, 13);
       launch_cloud_normals(pts4.as<float4>(), dsp, index.as<int>(), c,
                            want_double ? nrm_d.as<double>() : nullptr,
                            want_double ? nullptr : nrm_f.as<float>(), W, H, n, N, stream);
@@ -666,19 +710,24 @@ struct ss_ctx {
   // Whole run_stereo_only chain on device inputs (in_l/in_r hold the frames).
   void run_chain(int n, int W, int H, int in_format, const uint8_t* dl, const uint8_t* dr,
                  uint32_t flags_out) {
+    if ((flags_out & (SS_OUT_CLOUD | SS_OUT_NORMALS)) && !has_rig)
+      raise(SS_EINVAL, "stereo batch: cloud output requested but ctx has no rig");
     const Geom g = make_geom(W, H, &params);
     prepare_gray(n, W, H, in_format, dl, dr);
     const bool vol_ok = run_wta(n, g);
     run_cleanup(n, W, H);
     run_refine(n, g, vol_ok, nullptr, nullptr);
-    last_disp = disp_b.as<float>();
-    last_valid = valid_a.as<uint8_t>();
-    last_N = g.N();
-    last_frames = n;
+    last = ss_batch_out{};
+    last.disparity = disp_b.as<float>();
+    last.valid = valid_a.as<uint8_t>();
     if (flags_out & (SS_OUT_CLOUD | SS_OUT_NORMALS)) {
-      if (!has_rig) raise(SS_EINVAL, "stereo batch: cloud output requested but ctx has no rig");
-      run_cloud(n, W, H, last_disp, last_valid, in_format == SS_IN_RGB ? dl : nullptr, W, H,
+      run_cloud(n, W, H, last.disparity, last.valid, in_format == SS_IN_RGB ? dl : nullptr, W, H,
                 3L * g.N(), false, (flags_out & SS_OUT_NORMALS) != 0, false);
+      last.index = index.as<int32_t>();
+      last.n_points = npoints.as<int32_t>();
+      last.points = pts_f.as<float>();
+      last.colors = colors.as<uint8_t>();
+      if (flags_out & SS_OUT_NORMALS) last.normals = nrm_f.as<float>();
     }
     stats.frames += n;
   }
@@ -1449,22 +1498,41 @@ ss_status ss_stereo_batch_device(ss_ctx* ctx, int32_t n, int32_t w, int32_t h,
       ck(cudaEventRecord(ev, user), "event");
       ck(cudaStreamWaitEvent(ctx->stream, ev, 0), "wait");
     }
-    if (n > 0) ctx->run_chain(n, w, h, in_format, d_left, d_right, out_flags);
     const long N = (long)w * h;
-    if (d_out && n > 0) {
-      auto cp = [&](void* dst, const void* src, size_t bytes) {
-        if (dst && bytes)
-          ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream), "D2D");
-      };
-      cp(d_out->disparity, ctx->last_disp, sizeof(float) * N * n);
-      cp(d_out->valid, ctx->last_valid, N * n);
-      if (out_flags & SS_OUT_CLOUD) {
-        cp(d_out->index, ctx->index.p, sizeof(int) * N * n);
-        cp(d_out->n_points, ctx->npoints.p, sizeof(int) * n);
-        cp(d_out->points, ctx->pts_f.p, sizeof(float) * 3 * N * n);
-        cp(d_out->colors, ctx->colors.p, 3 * N * n);
+    if (n > 0) {
+      // The chain writes its results straight into the caller's buffers:
+      // each given output pointer is swapped in as a borrowed arena for the
+      // duration of the chain (no device-to-device copies afterwards).
+      ss_ctx::Slot io;
+      const bool cl = (out_flags & SS_OUT_CLOUD) != 0, nm = (out_flags & SS_OUT_NORMALS) != 0;
+      if (d_out) {
+        auto lend = [&](DevBuf& b, void* q, size_t bytes, bool want) {
+          if (q && want) b = DevBuf::borrow(q, bytes);
+        };
+        lend(io.disp_b, d_out->disparity, sizeof(float) * N * n, true);
+        lend(io.valid_a, d_out->valid, (size_t)N * n, true);
+        lend(io.index, d_out->index, sizeof(int) * N * n, cl || nm);
+        lend(io.npoints, d_out->n_points, sizeof(int) * n, cl || nm);
+        lend(io.pts_f, d_out->points, sizeof(float) * 3 * N * n, cl || nm);
+        lend(io.colors, d_out->colors, 3 * (size_t)N * n, cl || nm);
+        lend(io.nrm_f, d_out->normals, sizeof(float) * 3 * N * n, nm);
       }
-      if (out_flags & SS_OUT_NORMALS) cp(d_out->normals, ctx->nrm_f.p, sizeof(float) * 3 * N * n);
+      // swap in only what was lent; the rest stays the ctx's own
+      auto swap_lent = [&] {
+        for (auto pr : {std::make_pair(&ctx->disp_b, &io.disp_b), {&ctx->valid_a, &io.valid_a},
+                        {&ctx->index, &io.index}, {&ctx->npoints, &io.npoints},
+                        {&ctx->pts_f, &io.pts_f}, {&ctx->colors, &io.colors},
+                        {&ctx->nrm_f, &io.nrm_f}})
+          if (pr.second->borrowed || pr.first->borrowed) std::swap(*pr.first, *pr.second);
+      };
+      swap_lent();
+      try {
+        ctx->run_chain(n, w, h, in_format, d_left, d_right, out_flags);
+      } catch (...) {
+        swap_lent();
+        throw;
+      }
+      swap_lent();
     }
     if (ev) {
       ck(cudaEventRecord(ev, ctx->stream), "event");
@@ -1495,13 +1563,8 @@ ss_status ss_stereo_frame(const ss_stereo_params* p, const ss_stereo_rig* rig, i
 
 ss_status ss_ctx_device_outputs(ss_ctx* ctx, ss_batch_out* o) {
   return guarded([&] {
-    o->disparity = ctx->last_disp;
-    o->valid = ctx->last_valid;
-    o->index = ctx->index.as<int32_t>();
-    o->points = ctx->pts_f.as<float>();
-    o->normals = ctx->nrm_f.as<float>();
-    o->colors = ctx->colors.as<uint8_t>();
-    o->n_points = ctx->npoints.as<int32_t>();
+    if (!ctx || !o) raise(SS_EINVAL, "ss_ctx_device_outputs: null argument");
+    *o = ctx->last;
   });
 }
 
@@ -1510,49 +1573,63 @@ ss_status ss_stereo_batch(ss_ctx* ctx, int32_t n, int32_t w, int32_t h, int32_t 
                           const ss_batch_out* out) {
   return guarded([&] {
     if (!ctx) raise(SS_EINVAL, "ss_stereo_batch: null ctx");
+    if (!out) raise(SS_EINVAL, "ss_stereo_batch: null outputs");
     if (n < 0 || w <= 0 || h <= 0) raise(SS_EINVAL, "ss_stereo_batch: bad shape");
+    if (n > 0 && (!left || !right)) raise(SS_EINVAL, "ss_stereo_batch: null inputs");
     if (in_format != SS_IN_RGB && in_format != SS_IN_GRAY)
       raise(SS_EINVAL, "ss_stereo_batch: unknown input format");
+    const bool cloud = (out_flags & (SS_OUT_CLOUD | SS_OUT_NORMALS)) != 0;
+    if (cloud && !ctx->has_rig)
+      raise(SS_EINVAL, "stereo batch: cloud output requested but ctx has no rig");
     ctx->activate();
     const long N = (long)w * h;
     const long in_bytes = (in_format == SS_IN_RGB ? 3 : 1) * N;
-    const bool cloud = (out_flags & (SS_OUT_CLOUD | SS_OUT_NORMALS)) != 0;
     // Chunk k on slot k % 2: H2D (s_in) || chain (stream) || D2H (s_out).
     // Cloud arrays leave at full per-frame capacity (no host round trip for
     // the point counts); entries past n_points[f] are unspecified.
-    int k = 0;
-    for (int f0 = 0; f0 < n; f0 += ctx->max_batch, ++k) {
-      const int m = std::min(ctx->max_batch, n - f0);
-      ss_ctx::Slot& sl = ctx->slots[k & 1];
-      ck(cudaStreamWaitEvent(ctx->s_in, sl.done, 0), "wait");  // slot inputs consumed
-      h2d(sl.in_l, left + f0 * in_bytes, in_bytes * m, ctx->s_in);
-      h2d(sl.in_r, right + f0 * in_bytes, in_bytes * m, ctx->s_in);
-      ck(cudaEventRecord(sl.in_ready, ctx->s_in), "record");
-      ck(cudaStreamWaitEvent(ctx->stream, sl.in_ready, 0), "wait");
-      ck(cudaStreamWaitEvent(ctx->stream, sl.out_free, 0), "wait");  // slot outputs drained
-      ctx->swap_outputs(sl);
-      try {
-        ctx->run_chain(m, w, h, in_format, sl.in_l.as<uint8_t>(), sl.in_r.as<uint8_t>(),
-                       out_flags);
-      } catch (...) {
+    try {
+      int k = 0;
+      for (int f0 = 0; f0 < n; f0 += ctx->max_batch, ++k) {
+        const int m = std::min(ctx->max_batch, n - f0);
+        ss_ctx::Slot& sl = ctx->slots[k & 1];
+        ck(cudaStreamWaitEvent(ctx->s_in, sl.done, 0), "wait");  // slot inputs consumed
+        h2d(sl.in_l, left + f0 * in_bytes, in_bytes * m, ctx->s_in);
+        h2d(sl.in_r, right + f0 * in_bytes, in_bytes * m, ctx->s_in);
+        ck(cudaEventRecord(sl.in_ready, ctx->s_in), "record");
+        ck(cudaStreamWaitEvent(ctx->stream, sl.in_ready, 0), "wait");
+        ck(cudaStreamWaitEvent(ctx->stream, sl.out_free, 0), "wait");  // slot outputs drained
         ctx->swap_outputs(sl);
-        throw;
+        try {
+          ctx->run_chain(m, w, h, in_format, sl.in_l.as<uint8_t>(), sl.in_r.as<uint8_t>(),
+                         out_flags);
+        } catch (...) {
+          ctx->swap_outputs(sl);
+          throw;
+        }
+        ctx->swap_outputs(sl);
+        ck(cudaEventRecord(sl.done, ctx->stream), "record");
+        cudaStream_t so = ctx->s_out;
+        ck(cudaStreamWaitEvent(so, sl.done, 0), "wait");
+        const ss_batch_out& r = ctx->last;
+        if (out->disparity) d2h(out->disparity + f0 * N, r.disparity, sizeof(float) * N * m, so);
+        if (out->valid) d2h(out->valid + f0 * N, r.valid, N * m, so);
+        if (cloud) {
+          if (out->n_points) d2h(out->n_points + f0, r.n_points, sizeof(int) * m, so);
+          if (out->index) d2h(out->index + f0 * N, r.index, sizeof(int) * N * m, so);
+          if (out->points) d2h(out->points + f0 * N * 3, r.points, sizeof(float) * 3 * N * m, so);
+          if (out->colors) d2h(out->colors + f0 * N * 3, r.colors, 3 * N * m, so);
+          if (out->normals && (out_flags & SS_OUT_NORMALS))
+            d2h(out->normals + f0 * N * 3, r.normals, sizeof(float) * 3 * N * m, so);
+        }
+        ck(cudaEventRecord(sl.out_free, so), "record");
       }
-      ctx->swap_outputs(sl);
-      ck(cudaEventRecord(sl.done, ctx->stream), "record");
-      cudaStream_t so = ctx->s_out;
-      ck(cudaStreamWaitEvent(so, sl.done, 0), "wait");
-      if (out->disparity) d2h(out->disparity + f0 * N, ctx->last_disp, sizeof(float) * N * m, so);
-      if (out->valid) d2h(out->valid + f0 * N, ctx->last_valid, N * m, so);
-      if (cloud) {
-        if (out->n_points) d2h(out->n_points + f0, sl.npoints.p, sizeof(int) * m, so);
-        if (out->index) d2h(out->index + f0 * N, sl.index.p, sizeof(int) * N * m, so);
-        if (out->points) d2h(out->points + f0 * N * 3, sl.pts_f.p, sizeof(float) * 3 * N * m, so);
-        if (out->colors) d2h(out->colors + f0 * N * 3, sl.colors.p, 3 * N * m, so);
-        if (out->normals && (out_flags & SS_OUT_NORMALS))
-          d2h(out->normals + f0 * N * 3, sl.nrm_f.p, sizeof(float) * 3 * N * m, so);
-      }
-      ck(cudaEventRecord(sl.out_free, so), "record");
+    } catch (...) {
+      // no copy may still be writing into (or reading from) the caller's
+      // host buffers once the error is returned
+      cudaStreamSynchronize(ctx->s_in);
+      cudaStreamSynchronize(ctx->stream);
+      cudaStreamSynchronize(ctx->s_out);
+      throw;
     }
     ck(cudaStreamSynchronize(ctx->s_out), "cudaStreamSynchronize");
     sync(ctx);

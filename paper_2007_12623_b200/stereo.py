@@ -121,6 +121,39 @@ def _ptr(a):
     return a.ctypes.data_as(C.c_void_p) if a is not None else None
 
 
+def _batch_inputs(left, right, in_format, rgb_ndim):
+    """uint8, C-contiguous, equal shapes; the format follows the rank
+    (rgb_ndim dims = interleaved RGB) unless given, and must agree with it."""
+    left, right = _u8(left), _u8(right)
+    if left.shape != right.shape:
+        raise InvalidArgument(L.SS_EINVAL, f"stereo batch: left {left.shape} and right "
+                                           f"{right.shape} shapes differ")
+    if in_format is None:
+        in_format = L.SS_IN_RGB if left.ndim == rgb_ndim else L.SS_IN_GRAY
+    want = rgb_ndim if in_format == L.SS_IN_RGB else rgb_ndim - 1
+    if left.ndim != want or (in_format == L.SS_IN_RGB and left.shape[-1] != 3):
+        raise InvalidArgument(L.SS_EINVAL, f"stereo batch: input shape {left.shape} does not "
+                                           f"match the {'RGB' if in_format == L.SS_IN_RGB else 'gray'} format")
+    dims = left.shape[:rgb_ndim - 1]
+    return left, right, in_format, dims
+
+
+def _batch_outputs(out, n, h, w, out_flags):
+    """Allocate, or check dtype / shape / contiguity of caller-given outputs."""
+    want = StereoContext.alloc_outputs(n, h, w, out_flags, alloc=lambda s, dt: (s, np.dtype(dt)))
+    if out is None:
+        return StereoContext.alloc_outputs(n, h, w, out_flags)
+    for k, (shape, dt) in want.items():
+        a = out.get(k)
+        if a is None:
+            continue
+        if not isinstance(a, np.ndarray) or a.dtype != dt or tuple(a.shape) != tuple(shape) \
+                or not a.flags.c_contiguous:
+            raise InvalidArgument(L.SS_EINVAL, f"stereo batch: output {k!r} must be a C-contiguous "
+                                               f"{dt} array of shape {shape}")
+    return out
+
+
 def device_count() -> int:
     return int(L.lib().ss_device_count())
 
@@ -290,12 +323,8 @@ class StereoContext:
 
     def run(self, left, right, out_flags=L.SS_OUT_DISPARITY, in_format=None, out=None):
         """left/right: (n, H, W, 3) RGB or (n, H, W) gray uint8 host arrays."""
-        left, right = np.ascontiguousarray(left), np.ascontiguousarray(right)
-        if in_format is None:
-            in_format = L.SS_IN_RGB if left.ndim == 4 else L.SS_IN_GRAY
-        n, h, w = left.shape[:3]
-        if out is None:
-            out = self.alloc_outputs(n, h, w, out_flags)
+        left, right, in_format, (n, h, w) = _batch_inputs(left, right, in_format, 4)
+        out = _batch_outputs(out, n, h, w, out_flags)
         bo = L.SsBatchOut(*[_ptr(out.get(k)) if out.get(k) is not None else None
                             for k, _ in L.SsBatchOut._fields_])
         _check(L.lib().ss_stereo_batch(self._ctx, n, w, h, in_format, _ptr(left), _ptr(right),
@@ -361,12 +390,8 @@ class StereoMulti:
         return int(L.lib().ss_multi_size(self._m))
 
     def run(self, left, right, out_flags=L.SS_OUT_DISPARITY, in_format=None, out=None):
-        left, right = np.ascontiguousarray(left), np.ascontiguousarray(right)
-        if in_format is None:
-            in_format = L.SS_IN_RGB if left.ndim == 4 else L.SS_IN_GRAY
-        n, h, w = left.shape[:3]
-        if out is None:
-            out = StereoContext.alloc_outputs(n, h, w, out_flags)
+        left, right, in_format, (n, h, w) = _batch_inputs(left, right, in_format, 4)
+        out = _batch_outputs(out, n, h, w, out_flags)
         bo = L.SsBatchOut(*[_ptr(out.get(k)) if out.get(k) is not None else None
                             for k, _ in L.SsBatchOut._fields_])
         rc = L.lib().ss_multi_stereo_batch(self._m, n, w, h, in_format, _ptr(left), _ptr(right),
@@ -381,10 +406,8 @@ def stereo_frame(left, right, params=None, rig=None, out_flags=L.SS_OUT_DISPARIT
     """One pair through the whole chain (ss_stereo_frame): host arrays in, a
     dict of host arrays out (the keys of StereoContext.alloc_outputs, frame
     axis of length 1)."""
-    left, right = np.ascontiguousarray(left), np.ascontiguousarray(right)
-    in_format = L.SS_IN_RGB if left.ndim == 3 else L.SS_IN_GRAY
-    h, w = left.shape[:2]
-    out = StereoContext.alloc_outputs(1, h, w, out_flags)
+    left, right, in_format, (h, w) = _batch_inputs(left, right, None, 3)
+    out = _batch_outputs(None, 1, h, w, out_flags)
     bo = L.SsBatchOut(*[_ptr(out.get(k)) if out.get(k) is not None else None
                         for k, _ in L.SsBatchOut._fields_])
     r = C.byref(_rig(rig)) if rig is not None else None
@@ -394,16 +417,14 @@ def stereo_frame(left, right, params=None, rig=None, out_flags=L.SS_OUT_DISPARIT
 
 
 def pinned_empty(shape, dtype):
-    """numpy array backed by pinned (page-locked) host memory."""
+    """numpy array backed by pinned (page-locked) host memory; the pages are
+    released (cudaFreeHost) when the last view of the array is gone."""
+    import weakref
     dtype = np.dtype(dtype)
     nbytes = int(np.prod(shape)) * dtype.itemsize
     p = L.lib().ss_host_alloc(max(nbytes, 1))
     if not p:
         raise StereoError(L.SS_ENOMEM, "cudaHostAlloc failed")
     buf = (C.c_uint8 * max(nbytes, 1)).from_address(p)
-    arr = np.frombuffer(buf, dtype=np.uint8, count=nbytes).view(dtype).reshape(shape)
-    _PINNED[id(arr)] = p
-    return arr
-
-
-_PINNED = {}
+    weakref.finalize(buf, L.lib().ss_host_free, C.c_void_p(p))
+    return np.frombuffer(buf, dtype=np.uint8, count=nbytes).view(dtype).reshape(shape)
