@@ -515,7 +515,8 @@ def run_ours(args):
     # context (strong: the stream's consumer has drained a slot before reuse)
     n_out = F if not strong else min(F, 2 * S * B)
     od = ss.StereoContext.alloc_outputs(n_out, H, W, flags,
-                                        alloc=lambda s, dt: torch.empty(s, dtype=dt, device=dev))
+                                        alloc=lambda s, dt: torch.empty(
+                                            s, dtype=torch.from_numpy(np.empty(0, dt)).dtype, device=dev))
     p = params_for(D)
     ctxs = [ss.StereoContext(local, W, H, B, ss.StereoParams(**p),
                              ss.StereoRig(**default_rig(W, H))) for _ in range(S)]

@@ -619,14 +619,16 @@ struct ss_ctx {
         {
           Stage ss(this, 10);
           launch_scan_bt_d(o.as<double>(), mT, psum.as<double>(), W, H, r, n, stream);
+          stats.kernel_launches += 1;
         }
         launch_avg_b(psum.as<double>(), mT, cnt.as<int>(), o.as<double>(), d.as<double>(),
                      avg.as<double>(), b.as<double>(), a, n, stream);
+        stats.kernel_launches += 1;
         {
           Stage ss(this, 10);
           launch_scan_bt_d(b.as<double>(), mT, psum.as<double>(), W, H, r, n, stream);
+          stats.kernel_launches += 1;
         }
-        stats.kernel_launches += 3;
         repick(avg.as<double>(), nullptr, nullptr);
         if (iters > 1) {
           // o is integer-valued from here on: exact integer disc sums S_o.
@@ -640,8 +642,8 @@ struct ss_ctx {
           Stage ss(this, 10);
           launch_scan_b(so.as<int>(), cnt.as<int>(), op, d.as<double>(), mT, a.alpha,
                         a.one_minus_alpha, psum.as<double>(), W, H, r, n, stream);
+          stats.kernel_launches += 1;
         }
-        stats.kernel_launches += 1;
         repick(nullptr, chg.as<int2>(), chg_count.as<unsigned>());
         if (it + 1 < iters) {
           launch_so_update(chg.as<int2>(), chg_count.as<unsigned>(), mT, so.as<int>(), a, n,
