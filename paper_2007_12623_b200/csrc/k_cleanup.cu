@@ -10,23 +10,22 @@
 //                      IDW w = 1/(step * {1, sqrt2}), double sums in direction
 //                      order 0..7 (the reference's order, so bit-exact).
 //   k_disc_select /    cleanup.cpp:69-84 — support of every invalid pixel from
-//   k_disc_sum         per-row prefix counts (exact integers); only pixels that
-//                      will be filled enter a compacted list, and one thread
-//                      per listed pixel accumulates all valid pixels of the
-//                      radius-R disc in raster order in FP64, w = 1/sqrt(dd)
-//                      from a table built with the same IEEE ops on the host.
+//   k_disc_sum_cert    per-row prefix counts (exact integers); only pixels that
+//                      will be filled enter a compacted list; 8 lanes per
+//                      listed pixel sum the radius-R disc in FP64 (w = 1/sqrt(dd)
+//                      from a table built with the same IEEE ops on the host)
+//                      and certify that the result rounds to the reference's
+//                      float, else recompute it in the reference's raster order.
 // All maps of a frame stay L2-resident (5 B/pixel); these passes are a few
 // percent of the frame and latency-, not bandwidth-bound.
 #include <math.h>
+
+#include <algorithm>
 
 #include "ss_internal.cuh"
 
 namespace ssb {
 
-// Invalid-neighbour marker in fx: the smallest denormal (low word 1) — a double
-// converted from a float always has its low 29 mantissa bits zero, so no
-// disparity (not even NaN/inf) carries it, and 0 * marker = +0.
-constexpr int kInvalidLo = 1;
 
 __constant__ int c_dirU[8] = {1, -1, 0, 0, 1, 1, -1, -1};
 __constant__ int c_dirV[8] = {0, 0, 1, -1, 1, -1, 1, -1};
@@ -148,12 +147,8 @@ __global__ void __launch_bounds__(256)
 
 // dout2/vout2 (optional): a second copy of the result (the radial fill's
 // output buffer, so that fill only writes the pixels it fills); list/count
-// (optional): per-frame list of the invalid output pixels.
-__device__ __forceinline__ void append_invalid(int* list, unsigned* count, long f, long stride,
-                                               int pix) {
-  list[f * stride + atomicAdd(count + f, 1u)] = pix;
-}
-
+// (optional): per-frame list of the invalid output pixels (warp-aggregated
+// appends: ~5% of the pixels, one counter per frame).
 // In place allowed (vout == vin, dout == NULL: each thread reads only its own
 // pixel of din / vin, before writing it), hence no __restrict__ on those.
 __global__ void k_remove_outliers(const float* din, const uint8_t* vin, float* dout,
@@ -169,29 +164,26 @@ __global__ void k_remove_outliers(const float* din, const uint8_t* vin, float* d
   const float d0 = din[i];
   if (dout) dout[i] = d0;
   if (dout2) dout2[i] = d0;
-  if (!vin[i]) {
-    vout[i] = 0;
-    if (vout2) vout2[i] = 0;
-    if (list) append_invalid(list, count, f, stride, v * W + u);
-    return;
+  bool keep = false;
+  if (vin[i]) {
+    const EdgeMaps M = edge_maps(const_cast<uint32_t*>(emap) + f * fw, W, H);
+    keep = r <= 0;  // no steps: every ray is smooth (cleanup.cpp:21-33)
+    const uint32_t* row = M.bh + (long)v * M.lw;
+    const uint32_t* col = M.bv + (long)u * M.lh;
+    const uint32_t* d1 = M.bd1 + ((long)u - v + H - 1) * M.lh;
+    const uint32_t* d2 = M.bd2 + ((long)u + v) * M.lh;
+    if (!keep && u + r < W) keep = run_ok(row, u, r);                      // (1, 0)
+    if (!keep && u - r >= 0) keep = run_ok(row, u - r, r);                 // (-1, 0)
+    if (!keep && v + r < H) keep = run_ok(col, v, r);                      // (0, 1)
+    if (!keep && v - r >= 0) keep = run_ok(col, v - r, r);                 // (0, -1)
+    if (!keep && u + r < W && v + r < H) keep = run_ok(d1, v, r);          // (1, 1)
+    if (!keep && u + r < W && v - r >= 0) keep = run_ok(d2, v - r + 1, r); // (1, -1)
+    if (!keep && u - r >= 0 && v + r < H) keep = run_ok(d2, v + 1, r);     // (-1, 1)
+    if (!keep && u - r >= 0 && v - r >= 0) keep = run_ok(d1, v - r, r);   // (-1, -1)
   }
-  const EdgeMaps M = edge_maps(const_cast<uint32_t*>(emap) + f * fw, W, H);
-  bool keep = r <= 0;  // no steps: every ray is smooth (cleanup.cpp:21-33)
-  const uint32_t* row = M.bh + (long)v * M.lw;
-  const uint32_t* col = M.bv + (long)u * M.lh;
-  const uint32_t* d1 = M.bd1 + ((long)u - v + H - 1) * M.lh;
-  const uint32_t* d2 = M.bd2 + ((long)u + v) * M.lh;
-  if (!keep && u + r < W) keep = run_ok(row, u, r);                      // (1, 0)
-  if (!keep && u - r >= 0) keep = run_ok(row, u - r, r);                 // (-1, 0)
-  if (!keep && v + r < H) keep = run_ok(col, v, r);                      // (0, 1)
-  if (!keep && v - r >= 0) keep = run_ok(col, v - r, r);                 // (0, -1)
-  if (!keep && u + r < W && v + r < H) keep = run_ok(d1, v, r);          // (1, 1)
-  if (!keep && u + r < W && v - r >= 0) keep = run_ok(d2, v - r + 1, r); // (1, -1)
-  if (!keep && u - r >= 0 && v + r < H) keep = run_ok(d2, v + 1, r);     // (-1, 1)
-  if (!keep && u - r >= 0 && v - r >= 0) keep = run_ok(d1, v - r, r);   // (-1, -1)
   vout[i] = keep ? 1 : 0;
   if (vout2) vout2[i] = keep ? 1 : 0;
-  if (list && !keep) append_invalid(list, count, f, stride, v * W + u);
+  if (list) warp_append(list + f * stride, count + f, !keep, v * W + u);
 }
 
 // Radial fill of one invalid pixel (cleanup.cpp:54-68): writes dout/vout
@@ -279,93 +271,208 @@ __global__ void k_fill_radial_list(const float* __restrict__ din, const uint8_t*
 
 // Disc fill, pass 1: copy the map through and, for invalid pixels, count the
 // valid disc neighbours from per-row prefix counts (exact integers, 2 loads
-// per disc row). Pixels that will be filled go to a per-frame list.
-__global__ void k_disc_select(const float* __restrict__ din, const uint8_t* __restrict__ vin,
-                              float* __restrict__ dout, uint8_t* __restrict__ vout,
-                              const int* __restrict__ pcnt, const int* __restrict__ span,
-                              int* __restrict__ list, unsigned* __restrict__ count,
-                              double* __restrict__ fx, int W, int H, int radius, int min_support,
-                              long stride, long pstride) {
+// per disc row). Pixels that will be filled go to a per-frame list. fx gets
+// the map as floats with invalid pixels replaced by the marker -0.0f (so
+// w * x adds -0.0, which leaves a sum unchanged); meta[f] = {max |d| over
+// valid pixels (float bits), 1 if a valid pixel holds -0.0f (that frame then
+// takes the exact path throughout; the chain never produces one)}.
+constexpr uint32_t kMarkF = 0x80000000u;  // -0.0f
+
+__global__ void __launch_bounds__(256)
+    k_disc_select(const float* __restrict__ din, const uint8_t* __restrict__ vin,
+                  float* __restrict__ dout, uint8_t* __restrict__ vout,
+                  const int* __restrict__ pcnt, const int* __restrict__ span,
+                  int* __restrict__ list, unsigned* __restrict__ count, float* __restrict__ fx,
+                  unsigned* __restrict__ meta, int W, int H, int radius, int min_support,
+                  long stride, long pstride) {
   const long f = blockIdx.z;
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = blockIdx.y * blockDim.y + threadIdx.y;
-  if (u >= W || v >= H) return;
-  const long i = f * stride + (long)v * W + u;
-  const float od = din[i];
-  const uint8_t ov = vin[i];
-  dout[i] = od;
-  vout[i] = ov;
-  fx[i] = ov ? (double)od : __hiloint2double(0, kInvalidLo);  // invalid neighbour
-  if (ov || radius <= 0) return;
-  const int* pc = pcnt + f * pstride;
+  unsigned amax = 0, clash = 0;
+  bool listed = false;
+  if (u < W && v < H) {
+    const long i = f * stride + (long)v * W + u;
+    const float od = din[i];
+    const uint8_t ov = vin[i];
+    dout[i] = od;
+    vout[i] = ov;
+    fx[i] = ov ? od : __uint_as_float(kMarkF);
+    if (ov) {
+      amax = __float_as_uint(fabsf(od));  // NaN sorts above every finite value
+      clash = __float_as_uint(od) == kMarkF;
+    } else if (radius > 0) {
+      const int* pc = pcnt + f * pstride;
+      const int v0 = max(-radius, -v), v1 = min(radius, H - 1 - v);
+      int support = 0;
+      for (int dv = v0; dv <= v1; ++dv) {
+        const int sx = __ldg(span + (dv < 0 ? -dv : dv));
+        const int* row = pc + (long)(v + dv) * (W + 1);
+        support += __ldg(row + min(W - 1, u + sx) + 1) - __ldg(row + max(0, u - sx));
+      }
+      // The centre is invalid, so it never contributes (cleanup.cpp:74 skips dd == 0).
+      listed = support >= min_support && support > 0;
+    }
+  }
+  warp_append(list + f * stride, count + f, listed, v * W + u);
+  amax = __reduce_max_sync(0xFFFFFFFFu, amax);
+  clash = __reduce_or_sync(0xFFFFFFFFu, clash);
+  if ((threadIdx.x & 31) == 0) {
+    if (amax) atomicMax(meta + 2 * f, amax);
+    if (clash) atomicOr(meta + 2 * f + 1, 1u);
+  }
+}
+
+// The reference's raster-order double accumulation (cleanup.cpp:71-83) for
+// one pixel, from the input map itself: the exact path.
+__device__ double disc_fill_exact(const float* __restrict__ din, const uint8_t* __restrict__ vin,
+                                  const int* __restrict__ span, const double* w_tab, int W, int H,
+                                  int u, int v, int radius, double& wsum) {
+  const int D = 2 * radius + 1;
   const int v0 = max(-radius, -v), v1 = min(radius, H - 1 - v);
-  int support = 0;
+  double vsum = 0.0;
+  wsum = 0.0;
   for (int dv = v0; dv <= v1; ++dv) {
     const int sx = __ldg(span + (dv < 0 ? -dv : dv));
-    const int* row = pc + (long)(v + dv) * (W + 1);
-    support += __ldg(row + min(W - 1, u + sx) + 1) - __ldg(row + max(0, u - sx));
+    const int a = max(-sx, -u), b = min(sx, W - 1 - u);
+    const long r = (long)(v + dv) * W + u;
+    const double* wr = w_tab + (dv + radius) * D + radius;
+    for (int du = a; du <= b; ++du) {
+      if (du == 0 && dv == 0) continue;
+      if (!__ldg(vin + r + du)) continue;
+      const double w = wr[du];
+      wsum = __dadd_rn(wsum, w);
+      vsum = __dadd_rn(vsum, __dmul_rn(w, (double)__ldg(din + r + du)));
+    }
   }
-  // The centre is invalid, so it never contributes (cleanup.cpp:74 skips dd == 0).
-  if (support >= min_support && support > 0)
-    list[f * stride + atomicAdd(count + f, 1u)] = (int)((long)v * W + u);
+  return vsum;
 }
 
-// Disc fill, pass 2: one thread per listed pixel, the reference's raster-order
-// double accumulation (cleanup.cpp:71-83) with w = 1/sqrt(dd) from a host
-// table ((2R+1)^2 doubles, staged in shared memory). The neighbours come from
-// fx = valid ? double(d) : marker (written by pass 1): one load per disc pixel
-// gives both, an invalid one adds +0.0 to both sums, the loads
-// of a row are issued together and only the two FP64 add chains are serial.
-__device__ __forceinline__ void disc_acc(double& wsum, double& vsum, double w, double x) {
-  // invalid: w_eff = 0 adds +0.0 to both sums, which leaves them bit-identical
-  // (neither is ever -0.0: both start at +0.0 and an exactly-zero
-  // round-to-nearest sum is +0.0)
-  const double we = __double2loint(x) != kInvalidLo ? w : 0.0;
-  wsum = __dadd_rn(wsum, we);
-  vsum = __dadd_rn(vsum, __dmul_rn(we, x));
-}
-
-template <bool SMEM>
+// Disc fill, pass 2 (certified, parallel): G lanes per listed pixel. Lane g
+// sums disc rows dv = v0 + g, v0 + g + G, ... (each row left to right), so the
+// partial sums reassociate the reference's raster-order sums
+// (cleanup.cpp:71-83); the G partials are combined by shuffles. Both the
+// reference's serial sums and these add the SAME terms (table weights w and
+// products fl(w x)), so each is within gamma_{n-1} sum|term| of the exact sum
+// and they differ by at most 4 n u sum|term| <= 4 n u wsum max|d| (n = disc
+// taps, u = 2^-53). The reference's fl(vsum / wsum) therefore lies in
+// [q_lo, q_hi], computed with directed rounding; when both ends round to the
+// same float — the output type — that float is the reference's result.
+// Otherwise (and in a frame where a valid pixel holds the marker) lane 0
+// recomputes the pixel in the reference's exact order. The weight sum uses
+// fma(w, m, wsum) with m in {0, 1}: w m is exact, so it equals the masked add.
+template <int G>
 __global__ void __launch_bounds__(256)
-    k_disc_sum(const double* __restrict__ fx, float* __restrict__ dout, uint8_t* __restrict__ vout,
-               const int* __restrict__ list, const unsigned* __restrict__ count,
-               const int* __restrict__ span, const double* __restrict__ wtab, int W, int H,
-               int radius, long stride) {
+    k_disc_sum_cert(const float* __restrict__ fx, const float* __restrict__ din,
+                    const uint8_t* __restrict__ vin, float* __restrict__ dout,
+                    uint8_t* __restrict__ vout, const int* __restrict__ list,
+                    const unsigned* __restrict__ count, const unsigned* __restrict__ meta,
+                    const int* __restrict__ span, const double* __restrict__ wtab, int W, int H,
+                    int radius, long stride, unsigned long long* __restrict__ ctr) {
   extern __shared__ double s_w[];
   const int D = 2 * radius + 1;
-  if (SMEM) {
-    for (int k = threadIdx.x; k < D * D; k += blockDim.x) s_w[k] = __ldg(wtab + k);
-    __syncthreads();
-  }
+  for (int k = threadIdx.x; k < D * D; k += blockDim.x) s_w[k] = __ldg(wtab + k);
+  __syncthreads();
   const long f = blockIdx.y;
   const unsigned n = count[f];
-  const double* xf = fx + f * stride;
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && ctr) atomicAdd(ctr + 4, (unsigned long long)n);
+  const bool exact_all = meta[2 * f + 1] != 0;
+  const double xmax = (double)__uint_as_float(meta[2 * f]);
+  const int lane = threadIdx.x & 31, g = lane & (G - 1);
+  const unsigned gmask = ((1u << G) - 1u) << (lane & ~(G - 1));
+  const unsigned gpb = blockDim.x / G;
+  // 4 n u with n = (2R+1)^2 >= the taps of any clipped disc
+  const double c4nu = 4.0 * (double)(D * D) * 0x1p-53;
+  const float* xf = fx + f * stride;
+  const float* df = din + f * stride;
+  const uint8_t* vf = vin + f * stride;
+  for (unsigned t = blockIdx.x * gpb + threadIdx.x / G; t < n; t += gridDim.x * gpb) {
     const int idx = list[f * stride + t];
     const int v = idx / W, u = idx % W;
-    const int v0 = max(-radius, -v), v1 = min(radius, H - 1 - v);
-    double wsum = 0.0, vsum = 0.0;
-    for (int dv = v0; dv <= v1; ++dv) {
-      const int sx = __ldg(span + (dv < 0 ? -dv : dv));
-      const int a = max(-sx, -u), b = min(sx, W - 1 - u);
-      const double* xr = xf + (long)(v + dv) * W + u;
-      const int wo = (dv + radius) * D + radius;
-      int du = a;
-      for (; du + 3 <= b; du += 4) {
-        double x[4], w[4];
+    bool done = false;
+    float out = 0.f;
+    if (!exact_all) {
+      const int v0 = max(-radius, -v), v1 = min(radius, H - 1 - v);
+      double ws = 0.0, vs = 0.0;
+      for (int dv = v0 + g; dv <= v1; dv += G) {
+        const int sx = __ldg(span + (dv < 0 ? -dv : dv));
+        const int a = max(-sx, -u), b = min(sx, W - 1 - u);
+        const float* xr = xf + (long)(v + dv) * W + u;
+        const double* wr = s_w + (dv + radius) * D + radius;
+        int du = a;
+        for (; du + 3 <= b; du += 4) {
+          float x[4];
+          double w[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          x[k] = __ldg(xr + du + k);
-          w[k] = SMEM ? s_w[wo + du + k] : __ldg(wtab + wo + du + k);
+          for (int k = 0; k < 4; ++k) {
+            x[k] = __ldg(xr + du + k);
+            w[k] = wr[du + k];
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const double m = __float_as_uint(x[k]) != kMarkF ? 1.0 : 0.0;
+            ws = __fma_rn(w[k], m, ws);
+            vs = __dadd_rn(vs, __dmul_rn(w[k], (double)x[k]));
+          }
         }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) disc_acc(wsum, vsum, w[k], x[k]);
+        for (; du <= b; ++du) {
+          const float x = __ldg(xr + du);
+          const double w = wr[du];
+          ws = __fma_rn(w, __float_as_uint(x) != kMarkF ? 1.0 : 0.0, ws);
+          vs = __dadd_rn(vs, __dmul_rn(w, (double)x));
+        }
       }
-      for (; du <= b; ++du)
-        disc_acc(wsum, vsum, SMEM ? s_w[wo + du] : __ldg(wtab + wo + du), __ldg(xr + du));
+#pragma unroll
+      for (int off = G / 2; off > 0; off >>= 1) {
+        ws = __dadd_rn(ws, __shfl_xor_sync(gmask, ws, off));
+        vs = __dadd_rn(vs, __shfl_xor_sync(gmask, vs, off));
+      }
+      const double ev = __dmul_ru(__dmul_ru(c4nu, ws), xmax);
+      const double ew = __dmul_ru(c4nu, ws);
+      const double nlo = __dsub_rd(vs, ev), nhi = __dadd_ru(vs, ev);
+      const double dlo = __dsub_rd(ws, ew), dhi = __dadd_ru(ws, ew);
+      if (dlo > 0.0) {
+        const double qlo = __ddiv_rd(nlo, nlo >= 0.0 ? dhi : dlo);
+        const double qhi = __ddiv_ru(nhi, nhi >= 0.0 ? dlo : dhi);
+        const float flo = __double2float_rn(qlo), fhi = __double2float_rn(qhi);
+        if (__float_as_uint(flo) == __float_as_uint(fhi) && !isnan(flo)) {
+          done = true;
+          out = flo;
+        }
+      }
     }
-    if (wsum > 0.0) {
-      dout[f * stride + idx] = (float)__ddiv_rn(vsum, wsum);
+    if (g == 0) {
+      if (!done) {
+        double ws;
+        const double vs = disc_fill_exact(df, vf, span, s_w, W, H, u, v, radius, ws);
+        if (ctr) atomicAdd(ctr + 3, 1ull);
+        done = ws > 0.0;
+        out = (float)__ddiv_rn(vs, ws);
+      }
+      if (done) {
+        dout[f * stride + idx] = out;
+        vout[f * stride + idx] = 1;
+      }
+    }
+  }
+}
+
+// Generic disc fill pass 2 (weights table too large for shared memory): one
+// thread per listed pixel in the exact order.
+__global__ void __launch_bounds__(256)
+    k_disc_sum_serial(const float* __restrict__ din, const uint8_t* __restrict__ vin,
+                      float* __restrict__ dout, uint8_t* __restrict__ vout,
+                      const int* __restrict__ list, const unsigned* __restrict__ count,
+                      const int* __restrict__ span, const double* __restrict__ wtab, int W, int H,
+                      int radius, long stride) {
+  const long f = blockIdx.y;
+  const unsigned n = count[f];
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int idx = list[f * stride + t];
+    double ws;
+    const double vs = disc_fill_exact(din + f * stride, vin + f * stride, span, wtab, W, H,
+                                      idx % W, idx / W, radius, ws);
+    if (ws > 0.0) {
+      dout[f * stride + idx] = (float)__ddiv_rn(vs, ws);
       vout[f * stride + idx] = 1;
     }
   }
@@ -411,23 +518,29 @@ void launch_fill_radial(const float* din, const uint8_t* vin, float* dout, uint8
 
 void launch_fill_disc(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
                       int W, int H, int radius, int min_support, const double* wtab,
-                      const int* span, int* pcnt, int* list, unsigned* count, double* fx,
-                      int frames, long stride, cudaStream_t s) {
+                      const int* span, int* pcnt, int* list, unsigned* count, float* fx,
+                      unsigned* meta, unsigned long long* ctr, int frames, long stride,
+                      int n_sm, cudaStream_t s) {
   if (W <= 0 || H <= 0 || frames <= 0) return;
   const long pstride = (long)H * (W + 1);
   launch_row_count(vin, pcnt, W, H, frames, stride, pstride, s);
   cudaMemsetAsync(count, 0, sizeof(unsigned) * frames, s);
+  cudaMemsetAsync(meta, 0, sizeof(unsigned) * 2 * frames, s);
   dim3 b(32, 8);
   k_disc_select<<<map_grid(W, H, frames, b), b, 0, s>>>(din, vin, dout, vout, pcnt, span, list,
-                                                        count, fx, W, H, radius, min_support,
-                                                        stride, pstride);
+                                                        count, fx, meta, W, H, radius,
+                                                        min_support, stride, pstride);
+  // persistent grid: ~8 blocks per SM over all frames, each block's groups
+  // stride through its frame's device-side list
+  const int gx = std::max(1, 8 * n_sm / frames);
   const size_t wbytes = sizeof(double) * (2 * (size_t)radius + 1) * (2 * (size_t)radius + 1);
-  if (wbytes <= 40 * 1024)
-    k_disc_sum<true><<<dim3(96, frames), 256, wbytes, s>>>(fx, dout, vout, list, count, span, wtab,
-                                                         W, H, radius, stride);
+  if (wbytes <= 48 * 1024)
+    k_disc_sum_cert<8><<<dim3(gx, frames), 256, wbytes, s>>>(fx, din, vin, dout, vout, list, count,
+                                                             meta, span, wtab, W, H, radius,
+                                                             stride, ctr);
   else
-    k_disc_sum<false><<<dim3(96, frames), 256, 0, s>>>(fx, dout, vout, list, count, span, wtab, W,
-                                                     H, radius, stride);
+    k_disc_sum_serial<<<dim3(gx, frames), 256, 0, s>>>(din, vin, dout, vout, list, count, span,
+                                                       wtab, W, H, radius, stride);
 }
 
 }  // namespace ssb

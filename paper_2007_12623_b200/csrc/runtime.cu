@@ -113,6 +113,10 @@ struct DevBuf {
 
 long round_up(long x, long m) { return (x + m - 1) / m * m; }
 
+// device counters: 0 WTA exact resolves, 1 refine exact re-picks, 2 refine
+// fallbacks, 3 disc-fill exact recomputes, 4 disc-filled pixels
+constexpr int kNumCounters = 8;
+
 void validate_params(const ss_stereo_params* p) {
   // StereoParams::validate, matcher.cpp:9-19 — same checks, order, messages.
   if (p->window < 3 || p->window % 2 == 0) raise(SS_EPARAM, "stereo: window must be odd and >= 3");
@@ -195,7 +199,8 @@ struct ss_ctx {
   DevBuf disp_a, disp_b, valid_a, valid_b, flags, flag_count;
   DevBuf o, oi, d, avg, b, psum, pcnt, cnt, span, wtab, fspan, fx, emap;
   DevBuf index, block_sums, npoints, pts_f, nrm_f, colors, pts_d, nrm_d, pixels, pts4;
-  DevBuf counters, trace_o, trace_d, so, chg, chg_count, mbt, defer, defer_count;
+  DevBuf counters, trace_o, trace_d, so, chg, chg_count, mbt, defer, defer_count, fmeta;
+  int n_sm = 148;
   int wtab_radius = -1, span_radius = -1;
   std::vector<double> wtab_host;
   std::vector<int> fspan_host, span_host;
@@ -242,7 +247,7 @@ struct ss_ctx {
                       &disp_a, &disp_b, &valid_a, &valid_b, &flags, &flag_count, &o, &d, &avg,
                       &b, &psum, &pcnt, &cnt, &span, &wtab, &fspan, &fx, &emap, &index, &block_sums, &npoints,
                       &pts_f, &nrm_f, &colors, &pts_d, &nrm_d, &pixels, &pts4, &counters, &oi, &trace_o,
-                      &trace_d, &so, &chg, &chg_count, &mbt, &defer, &defer_count, &gray_fl,
+                      &trace_d, &so, &chg, &chg_count, &mbt, &defer, &defer_count, &fmeta, &gray_fl,
                       &gray_fr, &disp_r, &valid_r})
       b->release();
     for (DevBuf& b : fe) b.release();
@@ -320,8 +325,9 @@ struct ss_ctx {
     for (Slot& sl : slots)
       for (cudaEvent_t* e : {&sl.in_ready, &sl.done, &sl.out_free})
         ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
-    counters.ensure(4 * sizeof(unsigned long long));
-    ck(cudaMemsetAsync(counters.p, 0, 4 * sizeof(unsigned long long), stream), "memset");
+    counters.ensure(kNumCounters * sizeof(unsigned long long));
+    ck(cudaMemsetAsync(counters.p, 0, kNumCounters * sizeof(unsigned long long), stream), "memset");
+    ck(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device), "attribute");
   }
 
   unsigned long long* ctr() { return counters.as<unsigned long long>(); }
@@ -482,10 +488,11 @@ struct ss_ctx {
     pcnt.ensure(sizeof(int) * (long)H * (W + 1) * n);
     flags.ensure(sizeof(int) * N * n);
     flag_count.ensure(sizeof(unsigned) * n);
-    fx.ensure(sizeof(double) * N * n);
+    fx.ensure(sizeof(float) * N * n);
+    fmeta.ensure(sizeof(unsigned) * 2 * n);
     launch_fill_disc(din, vin, dout, vout, W, H, radius, min_support, wtab.as<double>(),
                      fspan.as<int>(), pcnt.as<int>(), flags.as<int>(), flag_count.as<unsigned>(),
-                     fx.as<double>(), n, N, stream);
+                     fx.as<float>(), fmeta.as<unsigned>(), ctr(), n, N, n_sm, stream);
     stats.kernel_launches += 3;
   }
 
@@ -1458,20 +1465,23 @@ ss_status ss_ctx_sync(ss_ctx* ctx) {
 ss_status ss_ctx_get_stats(ss_ctx* ctx, ss_ctx_stats* st) {
   return guarded([&] {
     ctx->activate();
-    unsigned long long c[4];
+    unsigned long long c[kNumCounters];
     ck(cudaMemcpyAsync(c, ctx->counters.p, sizeof c, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
     sync(ctx);
     *st = ctx->stats;
     st->wta_resolved = (int64_t)c[0];
     st->refine_resolved = (int64_t)c[1];
     st->refine_fallback = (int64_t)c[2];
+    st->disc_fill_exact = (int64_t)c[3];
+    st->disc_fill_pixels = (int64_t)c[4];
   });
 }
 
 ss_status ss_ctx_reset_stats(ss_ctx* ctx) {
   return guarded([&] {
     ctx->activate();
-    ck(cudaMemsetAsync(ctx->counters.p, 0, 4 * sizeof(unsigned long long), ctx->stream), "memset");
+    ck(cudaMemsetAsync(ctx->counters.p, 0, kNumCounters * sizeof(unsigned long long), ctx->stream),
+       "memset");
     sync(ctx);
     ctx->collect_times();
     ctx->stats = ss_ctx_stats{};

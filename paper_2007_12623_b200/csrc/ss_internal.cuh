@@ -174,11 +174,13 @@ void launch_fill_radial(const float* din, const uint8_t* vin, float* dout, uint8
                         int W, int H, int radius, int min_support, int frames, long stride,
                         cudaStream_t s);
 // pcnt: scratch [frames][H][W+1] ints; list: scratch [frames][W*H]; count: [frames];
-// fx: scratch [frames][W*H] doubles; wtab: [(2R+1)^2] disc weights (dv-major)
+// fx: scratch [frames][W*H] floats; meta: [frames][2] scratch; wtab: [(2R+1)^2]
+// disc weights (dv-major); ctr[3] += certification fallbacks, ctr[4] += fills
 void launch_fill_disc(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
                       int W, int H, int radius, int min_support, const double* wtab,
-                      const int* span, int* pcnt, int* list, unsigned* count, double* fx,
-                      int frames, long stride, cudaStream_t s);
+                      const int* span, int* pcnt, int* list, unsigned* count, float* fx,
+                      unsigned* meta, unsigned long long* ctr, int frames, long stride,
+                      int n_sm, cudaStream_t s);
 
 struct RefineArgs {
   Geom g;
@@ -196,6 +198,22 @@ void launch_row_count(const uint8_t* valid, int* pcnt, int W, int H, int frames,
 // refinement field is BT with CW = W (pixel fields, incl. the score windows
 // and wbase) or CW = W + 1 (row prefixes). A warp owns 32 consecutive rows of
 // one column: its loads and stores are single 128/256-byte lines. ----
+// Warp-aggregated list append: the lanes with `pred` write `val` to
+// consecutive slots of list[] reserved by ONE atomic per (converged part of a)
+// warp, instead of one atomic per lane on the same counter.
+__device__ __forceinline__ void warp_append(int* list, unsigned* count, bool pred, int val) {
+  const unsigned active = __activemask();
+  const unsigned m = __ballot_sync(active, pred);
+  if (!m) return;
+  unsigned lane;
+  asm("mov.u32 %0, %%laneid;" : "=r"(lane));
+  const int leader = __ffs(m) - 1;
+  unsigned base = 0;
+  if ((int)lane == leader) base = atomicAdd(count, (unsigned)__popc(m));
+  base = __shfl_sync(active, base, leader);
+  if (pred) list[base + __popc(m & ((1u << lane) - 1u))] = val;
+}
+
 __host__ __device__ inline long bt_frame(int W, int H, int extra_col) {
   return (long)((H + 31) / 32) * (W + extra_col) * 32;
 }

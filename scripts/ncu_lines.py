@@ -1,32 +1,41 @@
-"""Per-source-line stall samples / executed instructions from
-`ncu -i REP --page source --csv --print-source cuda,sass` output (stdin)."""
+#!/usr/bin/env python
+"""Per-source-line instruction counts and stall samples of one ncu report
+(ncu --page source --print-source cuda,sass), normalised per `unit` warps.
+
+    python scripts/ncu_lines.py gpurun_out/prof_x.ncu-rep [units] [top]
+"""
 import csv
+import io
+import subprocess
 import sys
 
-rows = list(csv.reader(sys.stdin))
-agg, src, cur = {}, {}, None
-fname = ""
-for r in rows:
-    if len(r) == 2 and r[0] == "File Path":
-        fname = r[1].split("/")[-1]
+rep = sys.argv[1]
+units = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
+top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                     capture_output=True, text=True).stdout
+agg, cur, line = {}, None, None
+for r in csv.reader(io.StringIO(txt)):
+    if not r:
         continue
-    if len(r) < 8 or r[0] == "Line No":
+    if r[0] == "File Path":
+        cur = r[1].split("/")[-1]
         continue
-    if r[0]:
-        cur = (fname, int(r[0]))
-        src[cur] = r[1]
+    if r[0] in ("Function Name", "Line No"):
         continue
-    if cur is None:
+    if r[0] != "":
+        line = (cur, r[0], r[1].strip()[:90])
         continue
     try:
-        s, ie = float(r[4] or 0), float(r[7] or 0)
-    except ValueError:
+        n = int(r[7]) if r[7] not in ("", "-") else 0
+        s = int(r[4]) if r[4] not in ("", "-") else 0
+    except (ValueError, IndexError):
         continue
-    a = agg.setdefault(cur, [0.0, 0.0])
-    a[0] += s
-    a[1] += ie
-tot = sum(a[0] for a in agg.values()) or 1
-ti = sum(a[1] for a in agg.values()) or 1
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 30
-for k, a in sorted(agg.items(), key=lambda x: -x[1][0])[:n]:
-    print(f"{k[0][:14]:14s}:{k[1]:<4d} {100*a[0]/tot:5.1f}% stall {100*a[1]/ti:5.1f}% inst  {src[k][:80]}")
+    a = agg.setdefault(line, [0, 0])
+    a[0] += n
+    a[1] += s
+tot = sum(v[0] for v in agg.values())
+st = sum(v[1] for v in agg.values()) or 1
+print(f"total warp instructions {tot} ({tot / units:.1f} per unit)")
+for k, (n, s) in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
+    print(f"{n / units:8.1f} {100 * s / st:5.1f}%  {k[0]}:{k[1]}  {k[2]}")
