@@ -272,22 +272,31 @@ __global__ void k_fill_radial_list(const float* __restrict__ din, const uint8_t*
 // Disc fill, pass 1: copy the map through and, for invalid pixels, count the
 // valid disc neighbours from per-row prefix counts (exact integers, 2 loads
 // per disc row). Pixels that will be filled go to a per-frame list. fx gets
-// the map as floats with invalid pixels replaced by the marker -0.0f (so
-// w * x adds -0.0, which leaves a sum unchanged); meta[f] = {max |d| over
-// valid pixels (float bits), 1 if a valid pixel holds -0.0f (that frame then
-// takes the exact path throughout; the chain never produces one)}.
-constexpr uint32_t kMarkF = 0x80000000u;  // -0.0f
+// the map as doubles in a layout padded by R on every side, invalid pixels
+// and the padding holding the marker -0.0 (so w * x adds -0.0, which leaves a
+// sum unchanged, and every disc tap of every pixel is in bounds); meta[f] =
+// {max |d| over valid pixels (float bits), 1 if a valid pixel holds a value
+// whose high word is the marker's (only -0.0 and negative denormals: that
+// frame then takes the exact path throughout; the chain never produces one)}.
+constexpr int kMarkHi = (int)0x80000000;  // high word of -0.0
+
+__host__ __device__ inline long disc_pitch(int W, int R) { return (long)W + 2 * R; }
+__host__ __device__ inline long disc_frame(int W, int H, int R) {
+  return disc_pitch(W, R) * ((long)H + 2 * R);
+}
 
 __global__ void __launch_bounds__(256)
     k_disc_select(const float* __restrict__ din, const uint8_t* __restrict__ vin,
                   float* __restrict__ dout, uint8_t* __restrict__ vout,
                   const int* __restrict__ pcnt, const int* __restrict__ span,
-                  int* __restrict__ list, unsigned* __restrict__ count, float* __restrict__ fx,
+                  int* __restrict__ list, unsigned* __restrict__ count, double* __restrict__ fx,
                   unsigned* __restrict__ meta, int W, int H, int radius, int min_support,
                   long stride, long pstride) {
   const long f = blockIdx.z;
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = blockIdx.y * blockDim.y + threadIdx.y;
+  const long P = disc_pitch(W, radius);
+  double* xf = fx + f * disc_frame(W, H, radius) + (long)radius * P + radius;
   unsigned amax = 0, clash = 0;
   bool listed = false;
   if (u < W && v < H) {
@@ -296,10 +305,11 @@ __global__ void __launch_bounds__(256)
     const uint8_t ov = vin[i];
     dout[i] = od;
     vout[i] = ov;
-    fx[i] = ov ? od : __uint_as_float(kMarkF);
+    const double xd = (double)od;
+    xf[(long)v * P + u] = ov ? xd : -0.0;
     if (ov) {
       amax = __float_as_uint(fabsf(od));  // NaN sorts above every finite value
-      clash = __float_as_uint(od) == kMarkF;
+      clash = __double2hiint(xd) == kMarkHi;
     } else if (radius > 0) {
       const int* pc = pcnt + f * pstride;
       const int v0 = max(-radius, -v), v1 = min(radius, H - 1 - v);
@@ -317,7 +327,9 @@ __global__ void __launch_bounds__(256)
   amax = __reduce_max_sync(0xFFFFFFFFu, amax);
   clash = __reduce_or_sync(0xFFFFFFFFu, clash);
   if ((threadIdx.x & 31) == 0) {
-    if (amax) atomicMax(meta + 2 * f, amax);
+    // one frame-wide maximum: read first, so only the few warps that raise
+    // it touch the counter atomically
+    if (amax > __ldcg(meta + 2 * f)) atomicMax(meta + 2 * f, amax);
     if (clash) atomicOr(meta + 2 * f + 1, 1u);
   }
 }
@@ -325,8 +337,8 @@ __global__ void __launch_bounds__(256)
 // The reference's raster-order double accumulation (cleanup.cpp:71-83) for
 // one pixel, from the input map itself: the exact path.
 __device__ double disc_fill_exact(const float* __restrict__ din, const uint8_t* __restrict__ vin,
-                                  const int* __restrict__ span, const double* w_tab, int W, int H,
-                                  int u, int v, int radius, double& wsum) {
+                                  const int* __restrict__ span, const double* __restrict__ wtab,
+                                  int W, int H, int u, int v, int radius, double& wsum) {
   const int D = 2 * radius + 1;
   const int v0 = max(-radius, -v), v1 = min(radius, H - 1 - v);
   double vsum = 0.0;
@@ -335,11 +347,11 @@ __device__ double disc_fill_exact(const float* __restrict__ din, const uint8_t* 
     const int sx = __ldg(span + (dv < 0 ? -dv : dv));
     const int a = max(-sx, -u), b = min(sx, W - 1 - u);
     const long r = (long)(v + dv) * W + u;
-    const double* wr = w_tab + (dv + radius) * D + radius;
+    const double* wr = wtab + (dv + radius) * D + radius;
     for (int du = a; du <= b; ++du) {
       if (du == 0 && dv == 0) continue;
       if (!__ldg(vin + r + du)) continue;
-      const double w = wr[du];
+      const double w = __ldg(wr + du);
       wsum = __dadd_rn(wsum, w);
       vsum = __dadd_rn(vsum, __dmul_rn(w, (double)__ldg(din + r + du)));
     }
@@ -347,84 +359,83 @@ __device__ double disc_fill_exact(const float* __restrict__ din, const uint8_t* 
   return vsum;
 }
 
-// Disc fill, pass 2 (certified, parallel): G lanes per listed pixel. Lane g
-// sums disc rows dv = v0 + g, v0 + g + G, ... (each row left to right), so the
-// partial sums reassociate the reference's raster-order sums
-// (cleanup.cpp:71-83); the G partials are combined by shuffles. Both the
-// reference's serial sums and these add the SAME terms (table weights w and
-// products fl(w x)), so each is within gamma_{n-1} sum|term| of the exact sum
-// and they differ by at most 4 n u sum|term| <= 4 n u wsum max|d| (n = disc
-// taps, u = 2^-53). The reference's fl(vsum / wsum) therefore lies in
+// Disc fill, pass 2 (certified, parallel): one warp per listed pixel. The
+// disc's taps (centre excluded) are a table in raster order in shared memory
+// (padded-layout offset, weight); lane l sums taps l, l + 32, ..., so a warp
+// load reads consecutive pixels of one or two rows, and the 32 partial sums
+// are combined by shuffles. This reassociates the reference's raster-order
+// sums (cleanup.cpp:71-83). Both add the SAME terms — table weights w and
+// products fl(w x) — so each is within gamma_{n-1} sum|term| of the exact
+// sum and they differ by at most 4 n u sum|term| <= 4 n u wsum max|d|
+// (n = taps, u = 2^-53). The reference's fl(vsum / wsum) therefore lies in
 // [q_lo, q_hi], computed with directed rounding; when both ends round to the
 // same float — the output type — that float is the reference's result.
-// Otherwise (and in a frame where a valid pixel holds the marker) lane 0
-// recomputes the pixel in the reference's exact order. The weight sum uses
-// fma(w, m, wsum) with m in {0, 1}: w m is exact, so it equals the masked add.
-template <int G>
+// Otherwise (~1 pixel per frame), and in a frame where a valid pixel holds
+// the marker, lane 0 recomputes the pixel in the reference's exact order. The
+// weight sum is fma(w, m, wsum) with m in {0, 1}: w m is exact, so it equals
+// the masked add.
+constexpr int kDiscMaxR = 31;  // (2R+1)^2 <= 3969 taps in shared memory
+
 __global__ void __launch_bounds__(256)
-    k_disc_sum_cert(const float* __restrict__ fx, const float* __restrict__ din,
+    k_disc_sum_cert(const double* __restrict__ fx, const float* __restrict__ din,
                     const uint8_t* __restrict__ vin, float* __restrict__ dout,
                     uint8_t* __restrict__ vout, const int* __restrict__ list,
                     const unsigned* __restrict__ count, const unsigned* __restrict__ meta,
                     const int* __restrict__ span, const double* __restrict__ wtab, int W, int H,
                     int radius, long stride, unsigned long long* __restrict__ ctr) {
-  extern __shared__ double s_w[];
+  extern __shared__ double s_tw[];  // [taps] weights, then [taps] int offsets
   const int D = 2 * radius + 1;
-  for (int k = threadIdx.x; k < D * D; k += blockDim.x) s_w[k] = __ldg(wtab + k);
+  const long P = disc_pitch(W, radius);
+  int* s_off = reinterpret_cast<int*>(s_tw + D * D);
+  __shared__ int s_row0[2 * kDiscMaxR + 2];  // raster index of each disc row's first tap
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int dv = -radius; dv <= radius; ++dv) {
+      s_row0[dv + radius] = n;
+      n += 2 * __ldg(span + (dv < 0 ? -dv : dv)) + 1 - (dv == 0 ? 1 : 0);
+    }
+    s_row0[D] = n;
+  }
   __syncthreads();
+  // raster-order tap table (dv, then du ascending), centre excluded
+  for (int k = threadIdx.x; k < D * D; k += blockDim.x) {
+    const int dv = k / D - radius, du = k % D - radius;
+    const int sx = __ldg(span + (dv < 0 ? -dv : dv));
+    if ((du < 0 ? -du : du) > sx || (du == 0 && dv == 0)) continue;
+    const int t = s_row0[dv + radius] + du + sx - (dv == 0 && du > 0 ? 1 : 0);
+    s_tw[t] = __ldg(wtab + k);
+    s_off[t] = (int)(dv * P + du);
+  }
+  __syncthreads();
+  const int taps = s_row0[D];
   const long f = blockIdx.y;
   const unsigned n = count[f];
   if (blockIdx.x == 0 && threadIdx.x == 0 && ctr) atomicAdd(ctr + 4, (unsigned long long)n);
   const bool exact_all = meta[2 * f + 1] != 0;
   const double xmax = (double)__uint_as_float(meta[2 * f]);
-  const int lane = threadIdx.x & 31, g = lane & (G - 1);
-  const unsigned gmask = ((1u << G) - 1u) << (lane & ~(G - 1));
-  const unsigned gpb = blockDim.x / G;
-  // 4 n u with n = (2R+1)^2 >= the taps of any clipped disc
-  const double c4nu = 4.0 * (double)(D * D) * 0x1p-53;
-  const float* xf = fx + f * stride;
-  const float* df = din + f * stride;
-  const uint8_t* vf = vin + f * stride;
-  for (unsigned t = blockIdx.x * gpb + threadIdx.x / G; t < n; t += gridDim.x * gpb) {
+  const int lane = threadIdx.x & 31;
+  const unsigned wpb = blockDim.x >> 5;
+  const double c4nu = 4.0 * (double)taps * 0x1p-53;
+  const double* xf = fx + f * disc_frame(W, H, radius) + (long)radius * P + radius;
+  for (unsigned t = blockIdx.x * wpb + (threadIdx.x >> 5); t < n; t += gridDim.x * wpb) {
     const int idx = list[f * stride + t];
     const int v = idx / W, u = idx % W;
     bool done = false;
     float out = 0.f;
     if (!exact_all) {
-      const int v0 = max(-radius, -v), v1 = min(radius, H - 1 - v);
+      const double* xc = xf + (long)v * P + u;
       double ws = 0.0, vs = 0.0;
-      for (int dv = v0 + g; dv <= v1; dv += G) {
-        const int sx = __ldg(span + (dv < 0 ? -dv : dv));
-        const int a = max(-sx, -u), b = min(sx, W - 1 - u);
-        const float* xr = xf + (long)(v + dv) * W + u;
-        const double* wr = s_w + (dv + radius) * D + radius;
-        int du = a;
-        for (; du + 3 <= b; du += 4) {
-          float x[4];
-          double w[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            x[k] = __ldg(xr + du + k);
-            w[k] = wr[du + k];
-          }
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const double m = __float_as_uint(x[k]) != kMarkF ? 1.0 : 0.0;
-            ws = __fma_rn(w[k], m, ws);
-            vs = __dadd_rn(vs, __dmul_rn(w[k], (double)x[k]));
-          }
-        }
-        for (; du <= b; ++du) {
-          const float x = __ldg(xr + du);
-          const double w = wr[du];
-          ws = __fma_rn(w, __float_as_uint(x) != kMarkF ? 1.0 : 0.0, ws);
-          vs = __dadd_rn(vs, __dmul_rn(w, (double)x));
-        }
+#pragma unroll 4
+      for (int k = lane; k < taps; k += 32) {
+        const double w = s_tw[k];
+        const double x = __ldg(xc + s_off[k]);
+        ws = __fma_rn(w, __double2hiint(x) != kMarkHi ? 1.0 : 0.0, ws);
+        vs = __dadd_rn(vs, __dmul_rn(w, x));
       }
 #pragma unroll
-      for (int off = G / 2; off > 0; off >>= 1) {
-        ws = __dadd_rn(ws, __shfl_xor_sync(gmask, ws, off));
-        vs = __dadd_rn(vs, __shfl_xor_sync(gmask, vs, off));
+      for (int off = 16; off > 0; off >>= 1) {
+        ws = __dadd_rn(ws, __shfl_xor_sync(0xFFFFFFFFu, ws, off));
+        vs = __dadd_rn(vs, __shfl_xor_sync(0xFFFFFFFFu, vs, off));
       }
       const double ev = __dmul_ru(__dmul_ru(c4nu, ws), xmax);
       const double ew = __dmul_ru(c4nu, ws);
@@ -440,10 +451,11 @@ __global__ void __launch_bounds__(256)
         }
       }
     }
-    if (g == 0) {
+    if (lane == 0) {
       if (!done) {
         double ws;
-        const double vs = disc_fill_exact(df, vf, span, s_w, W, H, u, v, radius, ws);
+        const double vs = disc_fill_exact(din + f * stride, vin + f * stride, span, wtab, W, H,
+                                          u, v, radius, ws);
         if (ctr) atomicAdd(ctr + 3, 1ull);
         done = ws > 0.0;
         out = (float)__ddiv_rn(vs, ws);
@@ -516,9 +528,36 @@ void launch_fill_radial(const float* din, const uint8_t* vin, float* dout, uint8
                                                         min_support, stride);
 }
 
+// The R-wide frame of fx around the image: the marker (a disc tap there adds
+// nothing), written per call (fx is shared by every geometry of the ctx).
+__global__ void __launch_bounds__(256) k_disc_pad(double* __restrict__ fx, int W, int H, int R) {
+  const long P = disc_pitch(W, R);
+  const long top = (long)R * P;                 // rows -R..-1 (and H..H+R-1 below)
+  const long side = (long)H * 2 * R;            // R columns left and right of each row
+  long k = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  double* xf = fx + blockIdx.y * disc_frame(W, H, R);
+  long y, x;
+  if (k < top) {
+    y = k / P;
+    x = k % P;
+  } else if ((k -= top) < top) {
+    y = R + H + k / P;
+    x = k % P;
+  } else if ((k -= top) < side) {
+    y = R + k / (2 * R);
+    x = k % (2 * R);
+    if (x >= R) x += W;
+  } else {
+    return;
+  }
+  xf[y * P + x] = -0.0;
+}
+
+long disc_fx_elems(int W, int H, int radius) { return disc_frame(W, H, std::max(radius, 0)); }
+
 void launch_fill_disc(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
                       int W, int H, int radius, int min_support, const double* wtab,
-                      const int* span, int* pcnt, int* list, unsigned* count, float* fx,
+                      const int* span, int* pcnt, int* list, unsigned* count, double* fx,
                       unsigned* meta, unsigned long long* ctr, int frames, long stride,
                       int n_sm, cudaStream_t s) {
   if (W <= 0 || H <= 0 || frames <= 0) return;
@@ -528,19 +567,25 @@ void launch_fill_disc(const float* din, const uint8_t* vin, float* dout, uint8_t
   cudaMemsetAsync(meta, 0, sizeof(unsigned) * 2 * frames, s);
   dim3 b(32, 8);
   k_disc_select<<<map_grid(W, H, frames, b), b, 0, s>>>(din, vin, dout, vout, pcnt, span, list,
-                                                        count, fx, meta, W, H, radius,
+                                                        count, fx, meta, W, H, std::max(radius, 0),
                                                         min_support, stride, pstride);
-  // persistent grid: ~8 blocks per SM over all frames, each block's groups
-  // stride through its frame's device-side list
+  // persistent grid: ~8 blocks per SM over all frames; each block's warps
+  // stride through their frame's device-side list
   const int gx = std::max(1, 8 * n_sm / frames);
-  const size_t wbytes = sizeof(double) * (2 * (size_t)radius + 1) * (2 * (size_t)radius + 1);
-  if (wbytes <= 48 * 1024)
-    k_disc_sum_cert<8><<<dim3(gx, frames), 256, wbytes, s>>>(fx, din, vin, dout, vout, list, count,
-                                                             meta, span, wtab, W, H, radius,
-                                                             stride, ctr);
-  else
+  const long D = 2L * std::max(radius, 0) + 1;
+  if (radius <= kDiscMaxR) {
+    k_disc_pad<<<dim3((unsigned)((disc_frame(W, H, radius) - (long)W * H + 255) / 256), frames), 256,
+                 0, s>>>(fx, W, H, std::max(radius, 0));
+    const size_t smem = D * D * (sizeof(double) + sizeof(int));
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_disc_sum_cert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_disc_sum_cert<<<dim3(gx, frames), 256, smem, s>>>(fx, din, vin, dout, vout, list, count,
+                                                         meta, span, wtab, W, H,
+                                                         std::max(radius, 0), stride, ctr);
+  } else {
     k_disc_sum_serial<<<dim3(gx, frames), 256, 0, s>>>(din, vin, dout, vout, list, count, span,
                                                        wtab, W, H, radius, stride);
+  }
 }
 
 }  // namespace ssb

@@ -488,11 +488,11 @@ struct ss_ctx {
     pcnt.ensure(sizeof(int) * (long)H * (W + 1) * n);
     flags.ensure(sizeof(int) * N * n);
     flag_count.ensure(sizeof(unsigned) * n);
-    fx.ensure(sizeof(float) * N * n);
+    fx.ensure(sizeof(double) * disc_fx_elems(W, H, radius) * n);
     fmeta.ensure(sizeof(unsigned) * 2 * n);
     launch_fill_disc(din, vin, dout, vout, W, H, radius, min_support, wtab.as<double>(),
                      fspan.as<int>(), pcnt.as<int>(), flags.as<int>(), flag_count.as<unsigned>(),
-                     fx.as<float>(), fmeta.as<unsigned>(), ctr(), n, N, n_sm, stream);
+                     fx.as<double>(), fmeta.as<unsigned>(), ctr(), n, N, n_sm, stream);
     stats.kernel_launches += 3;
   }
 
