@@ -224,6 +224,16 @@ typedef struct ss_ctx ss_ctx;
 #define SS_OUT_DISPARITY 1u  /* disparity (f32) + valid (u8) per pixel */
 #define SS_OUT_CLOUD 2u      /* packed cloud: index, points f32x3, colors */
 #define SS_OUT_NORMALS 4u    /* normals f32x3 (needs SS_OUT_CLOUD) */
+/* Compact transfer formats (opt-in; the default outputs are the reference's):
+ * SS_OUT_NORMALS_OCT  normals as 2 x int16 octahedral snorm per point in
+ *                     `normals_oct` instead of f32x3 in `normals` (4 B instead
+ *                     of 12 B; decoded direction within 1e-4 rad, see
+ *                     ss_oct_decode); implies SS_OUT_NORMALS.
+ * SS_OUT_TRIM         host API only: points / normals / colors leave the GPU
+ *                     with n_points entries per frame instead of the full
+ *                     per-frame capacity (one count read-back per chunk). */
+#define SS_OUT_NORMALS_OCT 8u
+#define SS_OUT_TRIM 16u
 
 /* Per-batch outputs. Host pointers for ss_stereo_batch, device pointers for
  * ss_stereo_batch_device. Arrays are frame-major: frame f of n starts at
@@ -237,7 +247,24 @@ typedef struct ss_batch_out {
   float* normals;
   uint8_t* colors;
   int32_t* n_points; /* n entries */
+  int16_t* normals_oct; /* SS_OUT_NORMALS_OCT: [n][w*h][2] */
 } ss_batch_out;
+
+/* Decode one SS_OUT_NORMALS_OCT normal (octahedral map, snorm16). */
+static inline void ss_oct_decode(const int16_t e[2], float n[3]) {
+  float x = (float)e[0] / 32767.0f, y = (float)e[1] / 32767.0f;
+  const float z = 1.0f - (x < 0 ? -x : x) - (y < 0 ? -y : y);
+  if (z < 0) {
+    const float ox = x;
+    x = (1.0f - (y < 0 ? -y : y)) * (ox < 0 ? -1.0f : 1.0f);
+    y = (1.0f - (ox < 0 ? -ox : ox)) * (y < 0 ? -1.0f : 1.0f);
+  }
+  float l = x * x + y * y + z * z;
+  l = l > 0 ? 1.0f / __builtin_sqrtf(l) : 0.0f;
+  n[0] = x * l;
+  n[1] = y * l;
+  n[2] = z * l;
+}
 
 typedef struct ss_ctx_stats {
   int64_t frames;            /* frames processed */

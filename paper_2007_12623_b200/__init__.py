@@ -17,6 +17,7 @@ from .stereo import (  # noqa: F401
     cleanup_pass,
     compute_disparity,
     compute_disparity_lr,
+    decode_oct_normals,
     device_count,
     disc_fill_min_support,
     disc_neighbor_count,
@@ -29,4 +30,5 @@ from .stereo import (  # noqa: F401
     to_gray,
 )
 from . import features, fusion  # noqa: F401
-from ._lib import SS_IN_GRAY, SS_IN_RGB, SS_OUT_CLOUD, SS_OUT_DISPARITY, SS_OUT_NORMALS  # noqa: F401
+from ._lib import (SS_IN_GRAY, SS_IN_RGB, SS_OUT_CLOUD, SS_OUT_DISPARITY, SS_OUT_NORMALS,  # noqa: F401
+                   SS_OUT_NORMALS_OCT, SS_OUT_TRIM)

@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
 SS_OK, SS_EINVAL, SS_EPARAM, SS_ECUDA, SS_ENOMEM, SS_ENODEV = range(6)
 SS_IN_RGB, SS_IN_GRAY = 0, 1
 SS_OUT_DISPARITY, SS_OUT_CLOUD, SS_OUT_NORMALS = 1, 2, 4
+SS_OUT_NORMALS_OCT, SS_OUT_TRIM = 8, 16
 SS_N_STAGES = 14
 STAGE_NAMES = ["luma", "stats", "wta_sweep", "wta_resolve", "cleanup", "refine", "cloud",
                "cleanup_outliers", "cleanup_radial", "cleanup_disc", "refine_scan", "refine_repick",
@@ -44,7 +45,7 @@ class SsFusionParams(C.Structure):
 class SsBatchOut(C.Structure):
     _fields_ = [("disparity", C.c_void_p), ("valid", C.c_void_p), ("index", C.c_void_p),
                 ("points", C.c_void_p), ("normals", C.c_void_p), ("colors", C.c_void_p),
-                ("n_points", C.c_void_p)]
+                ("n_points", C.c_void_p), ("normals_oct", C.c_void_p)]
 
 
 class SsCtxStats(C.Structure):

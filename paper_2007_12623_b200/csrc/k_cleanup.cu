@@ -274,10 +274,10 @@ __global__ void k_fill_radial_list(const float* __restrict__ din, const uint8_t*
 // per disc row). Pixels that will be filled go to a per-frame list. fx gets
 // the map as doubles in a layout padded by R on every side, invalid pixels
 // and the padding holding the marker -0.0 (so w * x adds -0.0, which leaves a
-// sum unchanged, and every disc tap of every pixel is in bounds); meta[f] =
-// {max |d| over valid pixels (float bits), 1 if a valid pixel holds a value
-// whose high word is the marker's (only -0.0 and negative denormals: that
-// frame then takes the exact path throughout; the chain never produces one)}.
+// sum unchanged, and every disc tap of every pixel is in bounds); meta[2f+1]
+// = 1 if a valid pixel holds a value whose high word is the marker's (only
+// -0.0 converts to one: that frame then takes the exact path throughout; the
+// chain never produces one).
 constexpr int kMarkHi = (int)0x80000000;  // high word of -0.0
 
 __host__ __device__ inline long disc_pitch(int W, int R) { return (long)W + 2 * R; }
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(256)
   const int v = blockIdx.y * blockDim.y + threadIdx.y;
   const long P = disc_pitch(W, radius);
   double* xf = fx + f * disc_frame(W, H, radius) + (long)radius * P + radius;
-  unsigned amax = 0, clash = 0;
+  unsigned clash = 0;
   bool listed = false;
   if (u < W && v < H) {
     const long i = f * stride + (long)v * W + u;
@@ -308,7 +308,6 @@ __global__ void __launch_bounds__(256)
     const double xd = (double)od;
     xf[(long)v * P + u] = ov ? xd : -0.0;
     if (ov) {
-      amax = __float_as_uint(fabsf(od));  // NaN sorts above every finite value
       clash = __double2hiint(xd) == kMarkHi;
     } else if (radius > 0) {
       const int* pc = pcnt + f * pstride;
@@ -324,14 +323,7 @@ __global__ void __launch_bounds__(256)
     }
   }
   warp_append(list + f * stride, count + f, listed, v * W + u);
-  amax = __reduce_max_sync(0xFFFFFFFFu, amax);
-  clash = __reduce_or_sync(0xFFFFFFFFu, clash);
-  if ((threadIdx.x & 31) == 0) {
-    // one frame-wide maximum: read first, so only the few warps that raise
-    // it touch the counter atomically
-    if (amax > __ldcg(meta + 2 * f)) atomicMax(meta + 2 * f, amax);
-    if (clash) atomicOr(meta + 2 * f + 1, 1u);
-  }
+  if (__any_sync(0xFFFFFFFFu, clash) && (threadIdx.x & 31) == 0) atomicOr(meta + 2 * f + 1, 1u);
 }
 
 // The reference's raster-order double accumulation (cleanup.cpp:71-83) for
@@ -375,6 +367,7 @@ __device__ double disc_fill_exact(const float* __restrict__ din, const uint8_t* 
 // weight sum is fma(w, m, wsum) with m in {0, 1}: w m is exact, so it equals
 // the masked add.
 constexpr int kDiscMaxR = 31;  // (2R+1)^2 <= 3969 taps in shared memory
+__host__ __device__ inline int disc_tab_cap(int R) { return ((2 * R + 1) * (2 * R + 1) + 31) & ~31; }
 
 __global__ void __launch_bounds__(256)
     k_disc_sum_cert(const double* __restrict__ fx, const float* __restrict__ din,
@@ -383,11 +376,11 @@ __global__ void __launch_bounds__(256)
                     const unsigned* __restrict__ count, const unsigned* __restrict__ meta,
                     const int* __restrict__ span, const double* __restrict__ wtab, int W, int H,
                     int radius, long stride, unsigned long long* __restrict__ ctr) {
-  extern __shared__ double s_tw[];  // [taps] weights, then [taps] int offsets
+  extern __shared__ double s_tw[];  // [cap] weights, then [cap] byte offsets
   const int D = 2 * radius + 1;
   const long P = disc_pitch(W, radius);
-  int* s_off = reinterpret_cast<int*>(s_tw + D * D);
-  __shared__ int s_row0[2 * kDiscMaxR + 2];  // raster index of each disc row's first tap
+  int* s_off = reinterpret_cast<int*>(s_tw + disc_tab_cap(radius));
+  __shared__ int s_row0[2 * kDiscMaxR + 2];
   if (threadIdx.x == 0) {
     int n = 0;
     for (int dv = -radius; dv <= radius; ++dv) {
@@ -397,22 +390,27 @@ __global__ void __launch_bounds__(256)
     s_row0[D] = n;
   }
   __syncthreads();
-  // raster-order tap table (dv, then du ascending), centre excluded
+  const int taps = s_row0[D];
+  const int taps32 = (taps + 31) & ~31;  // padded to whole warp passes: w = 0, offset 0
+  // raster-order tap table (dv, then du ascending), centre excluded; byte
+  // offsets into the padded map
   for (int k = threadIdx.x; k < D * D; k += blockDim.x) {
     const int dv = k / D - radius, du = k % D - radius;
     const int sx = __ldg(span + (dv < 0 ? -dv : dv));
     if ((du < 0 ? -du : du) > sx || (du == 0 && dv == 0)) continue;
     const int t = s_row0[dv + radius] + du + sx - (dv == 0 && du > 0 ? 1 : 0);
     s_tw[t] = __ldg(wtab + k);
-    s_off[t] = (int)(dv * P + du);
+    s_off[t] = (int)((dv * P + du) * (long)sizeof(double));
+  }
+  for (int t = taps + threadIdx.x; t < taps32; t += blockDim.x) {
+    s_tw[t] = 0.0;
+    s_off[t] = 0;  // the (invalid) centre: adds w * -0.0 and 0 weight
   }
   __syncthreads();
-  const int taps = s_row0[D];
   const long f = blockIdx.y;
   const unsigned n = count[f];
   if (blockIdx.x == 0 && threadIdx.x == 0 && ctr) atomicAdd(ctr + 4, (unsigned long long)n);
   const bool exact_all = meta[2 * f + 1] != 0;
-  const double xmax = (double)__uint_as_float(meta[2 * f]);
   const int lane = threadIdx.x & 31;
   const unsigned wpb = blockDim.x >> 5;
   const double c4nu = 4.0 * (double)taps * 0x1p-53;
@@ -423,21 +421,27 @@ __global__ void __launch_bounds__(256)
     bool done = false;
     float out = 0.f;
     if (!exact_all) {
-      const double* xc = xf + (long)v * P + u;
-      double ws = 0.0, vs = 0.0;
+      const char* xc = reinterpret_cast<const char*>(xf + (long)v * P + u);
+      double ws = 0.0, vs = 0.0, as = 0.0;
 #pragma unroll 4
-      for (int k = lane; k < taps; k += 32) {
+      for (int k = lane; k < taps32; k += 32) {
         const double w = s_tw[k];
-        const double x = __ldg(xc + s_off[k]);
+        const double x = __ldg(reinterpret_cast<const double*>(xc + s_off[k]));
+        const double p = __dmul_rn(w, x);
         ws = __fma_rn(w, __double2hiint(x) != kMarkHi ? 1.0 : 0.0, ws);
-        vs = __dadd_rn(vs, __dmul_rn(w, x));
+        vs = __dadd_rn(vs, p);
+        as = __dadd_rn(as, fabs(p));
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
         ws = __dadd_rn(ws, __shfl_xor_sync(0xFFFFFFFFu, ws, off));
         vs = __dadd_rn(vs, __shfl_xor_sync(0xFFFFFFFFu, vs, off));
+        as = __dadd_rn(as, __shfl_xor_sync(0xFFFFFFFFu, as, off));
       }
-      const double ev = __dmul_ru(__dmul_ru(c4nu, ws), xmax);
+      // both sums are within gamma_{n-1} * sum|p| of exact; the computed
+      // sum|p| (as) is within gamma_n of its own exact value: 2.02 n u as
+      // bounds the difference, 4 n u as with margin
+      const double ev = __dmul_ru(c4nu, as);
       const double ew = __dmul_ru(c4nu, ws);
       const double nlo = __dsub_rd(vs, ev), nhi = __dadd_ru(vs, ev);
       const double dlo = __dsub_rd(ws, ew), dhi = __dadd_ru(ws, ew);
@@ -576,7 +580,7 @@ void launch_fill_disc(const float* din, const uint8_t* vin, float* dout, uint8_t
   if (radius <= kDiscMaxR) {
     k_disc_pad<<<dim3((unsigned)((disc_frame(W, H, radius) - (long)W * H + 255) / 256), frames), 256,
                  0, s>>>(fx, W, H, std::max(radius, 0));
-    const size_t smem = D * D * (sizeof(double) + sizeof(int));
+    const size_t smem = disc_tab_cap(std::max(radius, 0)) * (sizeof(double) + sizeof(int));
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(k_disc_sum_cert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_disc_sum_cert<<<dim3(gx, frames), 256, smem, s>>>(fx, din, vin, dout, vout, list, count,

@@ -300,7 +300,8 @@ struct NormalSmem {
 __global__ void __launch_bounds__(kNTX * kNTY, 3)
     k_cloud_normals(const float4* __restrict__ pts4, const float* __restrict__ disp, int W,
                     int H, CloudArgs cargs, double* __restrict__ nrm_d,
-                    float* __restrict__ nrm_f, const int* __restrict__ index, long stride) {
+                    float* __restrict__ nrm_f, short2* __restrict__ nrm_o,
+                    const int* __restrict__ index, long stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   NormalSmem& S = *reinterpret_cast<NormalSmem*>(smem_raw);
   const long f = blockIdx.z;
@@ -496,11 +497,23 @@ __global__ void __launch_bounds__(kNTX * kNTY, 3)
     nrm_f[o + 1] = (float)nd[1];
     nrm_f[o + 2] = (float)nd[2];
   }
+  if (nrm_o) {
+    // octahedral map of the unit normal, snorm16 (decoded by ss_oct_decode)
+    const float a = fabsf((float)nd[0]) + fabsf((float)nd[1]) + fabsf((float)nd[2]);
+    float x = (float)nd[0] / a, y = (float)nd[1] / a;
+    if (nd[2] < 0.0) {
+      const float ox = x;
+      x = (1.f - fabsf(y)) * (ox < 0.f ? -1.f : 1.f);
+      y = (1.f - fabsf(ox)) * (y < 0.f ? -1.f : 1.f);
+    }
+    nrm_o[f * stride + k] = make_short2((short)__float2int_rn(fminf(fmaxf(x, -1.f), 1.f) * 32767.f),
+                                        (short)__float2int_rn(fminf(fmaxf(y, -1.f), 1.f) * 32767.f));
+  }
 }
 
 void launch_cloud_normals(const float4* pts4, const float* disp, const int* index,
-                          const CloudArgs& c, double* nrm_d, float* nrm_f, int W, int H,
-                          int frames, long stride, cudaStream_t s) {
+                          const CloudArgs& c, double* nrm_d, float* nrm_f, short2* nrm_o,
+                          int W, int H, int frames, long stride, cudaStream_t s) {
   if (W <= 0 || H <= 0 || frames <= 0) return;
   dim3 b(kNTX, kNTY);
   dim3 grid((W + kNTX - 1) / kNTX, (H + kNTY - 1) / kNTY, frames);
@@ -510,8 +523,8 @@ void launch_cloud_normals(const float4* pts4, const float* disp, const int* inde
                          (int)sizeof(NormalSmem));
     configured = true;
   }
-  k_cloud_normals<<<grid, b, sizeof(NormalSmem), s>>>(pts4, disp, W, H, c, nrm_d, nrm_f, index,
-                                                      stride);
+  k_cloud_normals<<<grid, b, sizeof(NormalSmem), s>>>(pts4, disp, W, H, c, nrm_d, nrm_f, nrm_o,
+                                                      index, stride);
 }
 
 }  // namespace ssb

@@ -198,7 +198,7 @@ struct ss_ctx {
   int lr_max_diff = 1;
   DevBuf disp_a, disp_b, valid_a, valid_b, flags, flag_count;
   DevBuf o, oi, d, avg, b, psum, pcnt, cnt, span, wtab, fspan, fx, emap;
-  DevBuf index, block_sums, npoints, pts_f, nrm_f, colors, pts_d, nrm_d, pixels, pts4;
+  DevBuf index, block_sums, npoints, pts_f, nrm_f, nrm_o, colors, pts_d, nrm_d, pixels, pts4;
   DevBuf counters, trace_o, trace_d, so, chg, chg_count, mbt, defer, defer_count, fmeta;
   int n_sm = 148;
   int wtab_radius = -1, span_radius = -1;
@@ -210,8 +210,8 @@ struct ss_ctx {
   // s_out. A slot owns the input buffers and the chain's output buffers, which
   // are swapped into the ctx for the duration of its chunk's chain.
   struct Slot {
-    DevBuf in_l, in_r, disp_b, valid_a, index, npoints, pts_f, colors, nrm_f;
-    cudaEvent_t in_ready = nullptr, done = nullptr, out_free = nullptr;
+    DevBuf in_l, in_r, disp_b, valid_a, index, npoints, pts_f, colors, nrm_f, nrm_o;
+    cudaEvent_t in_ready = nullptr, done = nullptr, out_free = nullptr, counts_ready = nullptr;
   };
   Slot slots[2];
   cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -223,6 +223,20 @@ struct ss_ctx {
     std::swap(pts_f, sl.pts_f);
     std::swap(colors, sl.colors);
     std::swap(nrm_f, sl.nrm_f);
+    std::swap(nrm_o, sl.nrm_o);
+  }
+
+  // pinned per-slot point counts for SS_OUT_TRIM when the caller passes no n_points
+  int32_t* h_counts = nullptr;
+  int h_counts_cap = 0;
+  void ensure_host_counts() {
+    if (h_counts_cap >= 2 * max_batch) return;
+    if (h_counts) cudaFreeHost(h_counts);
+    h_counts = nullptr;
+    h_counts_cap = 0;
+    ck(cudaHostAlloc((void**)&h_counts, sizeof(int32_t) * 2 * max_batch, cudaHostAllocDefault),
+       "cudaHostAlloc");
+    h_counts_cap = 2 * max_batch;
   }
 
   ss_ctx_stats stats{};
@@ -246,18 +260,19 @@ struct ss_ctx {
     for (DevBuf* b : {&in_l, &in_r, &gray_l, &gray_r, &ltap_buf, &rcopy_buf, &lstat, &rstat, &win, &wbase,
                       &disp_a, &disp_b, &valid_a, &valid_b, &flags, &flag_count, &o, &d, &avg,
                       &b, &psum, &pcnt, &cnt, &span, &wtab, &fspan, &fx, &emap, &index, &block_sums, &npoints,
-                      &pts_f, &nrm_f, &colors, &pts_d, &nrm_d, &pixels, &pts4, &counters, &oi, &trace_o,
+                      &pts_f, &nrm_f, &nrm_o, &colors, &pts_d, &nrm_d, &pixels, &pts4, &counters, &oi, &trace_o,
                       &trace_d, &so, &chg, &chg_count, &mbt, &defer, &defer_count, &fmeta, &gray_fl,
                       &gray_fr, &disp_r, &valid_r})
       b->release();
     for (DevBuf& b : fe) b.release();
     for (Slot& sl : slots) {
       for (DevBuf* b : {&sl.in_l, &sl.in_r, &sl.disp_b, &sl.valid_a, &sl.index, &sl.npoints,
-                        &sl.pts_f, &sl.colors, &sl.nrm_f})
+                        &sl.pts_f, &sl.colors, &sl.nrm_f, &sl.nrm_o})
         b->release();
-      for (cudaEvent_t e : {sl.in_ready, sl.done, sl.out_free})
+      for (cudaEvent_t e : {sl.in_ready, sl.done, sl.out_free, sl.counts_ready})
         if (e) cudaEventDestroy(e);
     }
+    if (h_counts) cudaFreeHost(h_counts);
     if (s_in) cudaStreamDestroy(s_in);
     if (s_out) cudaStreamDestroy(s_out);
     for (auto& r : pending) {
@@ -323,7 +338,7 @@ struct ss_ctx {
     ck(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking), "cudaStreamCreate");
     for (Slot& sl : slots)
-      for (cudaEvent_t* e : {&sl.in_ready, &sl.done, &sl.out_free})
+      for (cudaEvent_t* e : {&sl.in_ready, &sl.done, &sl.out_free, &sl.counts_ready})
         ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
     counters.ensure(kNumCounters * sizeof(unsigned long long));
     ck(cudaMemsetAsync(counters.p, 0, kNumCounters * sizeof(unsigned long long), stream), "memset");
@@ -680,7 +695,7 @@ struct ss_ctx {
   // disparity_to_cloud of (disp, valid) -> index/points/normals/colors.
   void run_cloud(int n, int W, int H, const float* dsp, const uint8_t* vld, const uint8_t* rgb,
                  int cw, int ch, long rgb_stride, bool want_double, bool want_normals,
-                 bool want_pixels) {
+                 bool want_pixels, bool want_oct = false) {
     Stage st(this, 6);
     const long N = (long)W * H;
     index.ensure(sizeof(int) * N * n);
@@ -697,7 +712,8 @@ struct ss_ctx {
       if (want_normals) nrm_d.ensure(sizeof(double) * 3 * N * n);
     } else {
       pts_f.ensure(sizeof(float) * 3 * N * n);
-      if (want_normals) nrm_f.ensure(sizeof(float) * 3 * N * n);
+      if (want_normals && !want_oct) nrm_f.ensure(sizeof(float) * 3 * N * n);
+      if (want_normals && want_oct) nrm_o.ensure(sizeof(short2) * N * n);
     }
     if (want_pixels) pixels.ensure(sizeof(int) * 2 * N * n);
     pts4.ensure(sizeof(float4) * N * n);
@@ -711,7 +727,8 @@ struct ss_ctx {
       Stage sn(this, 13);
       launch_cloud_normals(pts4.as<float4>(), dsp, index.as<int>(), c,
                            want_double ? nrm_d.as<double>() : nullptr,
-                           want_double ? nullptr : nrm_f.as<float>(), W, H, n, N, stream);
+                           want_double || want_oct ? nullptr : nrm_f.as<float>(),
+                           want_oct ? nrm_o.as<short2>() : nullptr, W, H, n, N, stream);
       stats.kernel_launches += 1;
     }
   }
@@ -719,7 +736,7 @@ struct ss_ctx {
   // Whole run_stereo_only chain on device inputs (in_l/in_r hold the frames).
   void run_chain(int n, int W, int H, int in_format, const uint8_t* dl, const uint8_t* dr,
                  uint32_t flags_out) {
-    if ((flags_out & (SS_OUT_CLOUD | SS_OUT_NORMALS)) && !has_rig)
+    if ((flags_out & (SS_OUT_CLOUD | SS_OUT_NORMALS | SS_OUT_NORMALS_OCT)) && !has_rig)
       raise(SS_EINVAL, "stereo batch: cloud output requested but ctx has no rig");
     const Geom g = make_geom(W, H, &params);
     prepare_gray(n, W, H, in_format, dl, dr);
@@ -729,14 +746,17 @@ struct ss_ctx {
     last = ss_batch_out{};
     last.disparity = disp_b.as<float>();
     last.valid = valid_a.as<uint8_t>();
-    if (flags_out & (SS_OUT_CLOUD | SS_OUT_NORMALS)) {
+    if (flags_out & (SS_OUT_CLOUD | SS_OUT_NORMALS | SS_OUT_NORMALS_OCT)) {
+      const bool oct = (flags_out & SS_OUT_NORMALS_OCT) != 0;
+      const bool nrm = oct || (flags_out & SS_OUT_NORMALS);
       run_cloud(n, W, H, last.disparity, last.valid, in_format == SS_IN_RGB ? dl : nullptr, W, H,
-                3L * g.N(), false, (flags_out & SS_OUT_NORMALS) != 0, false);
+                3L * g.N(), false, nrm, false, oct);
       last.index = index.as<int32_t>();
       last.n_points = npoints.as<int32_t>();
       last.points = pts_f.as<float>();
       last.colors = colors.as<uint8_t>();
-      if (flags_out & SS_OUT_NORMALS) last.normals = nrm_f.as<float>();
+      if (nrm && !oct) last.normals = nrm_f.as<float>();
+      if (oct) last.normals_oct = nrm_o.as<int16_t>();
     }
     stats.frames += n;
   }
@@ -1516,25 +1536,28 @@ ss_status ss_stereo_batch_device(ss_ctx* ctx, int32_t n, int32_t w, int32_t h,
       // each given output pointer is swapped in as a borrowed arena for the
       // duration of the chain (no device-to-device copies afterwards).
       ss_ctx::Slot io;
-      const bool cl = (out_flags & SS_OUT_CLOUD) != 0, nm = (out_flags & SS_OUT_NORMALS) != 0;
+      const bool oct = (out_flags & SS_OUT_NORMALS_OCT) != 0;
+      const bool nm = !oct && (out_flags & SS_OUT_NORMALS) != 0;
+      const bool cl = (out_flags & SS_OUT_CLOUD) != 0 || nm || oct;
       if (d_out) {
         auto lend = [&](DevBuf& b, void* q, size_t bytes, bool want) {
           if (q && want) b = DevBuf::borrow(q, bytes);
         };
         lend(io.disp_b, d_out->disparity, sizeof(float) * N * n, true);
         lend(io.valid_a, d_out->valid, (size_t)N * n, true);
-        lend(io.index, d_out->index, sizeof(int) * N * n, cl || nm);
-        lend(io.npoints, d_out->n_points, sizeof(int) * n, cl || nm);
-        lend(io.pts_f, d_out->points, sizeof(float) * 3 * N * n, cl || nm);
-        lend(io.colors, d_out->colors, 3 * (size_t)N * n, cl || nm);
+        lend(io.index, d_out->index, sizeof(int) * N * n, cl);
+        lend(io.npoints, d_out->n_points, sizeof(int) * n, cl);
+        lend(io.pts_f, d_out->points, sizeof(float) * 3 * N * n, cl);
+        lend(io.colors, d_out->colors, 3 * (size_t)N * n, cl);
         lend(io.nrm_f, d_out->normals, sizeof(float) * 3 * N * n, nm);
+        lend(io.nrm_o, d_out->normals_oct, sizeof(short2) * N * n, oct);
       }
       // swap in only what was lent; the rest stays the ctx's own
       auto swap_lent = [&] {
         for (auto pr : {std::make_pair(&ctx->disp_b, &io.disp_b), {&ctx->valid_a, &io.valid_a},
                         {&ctx->index, &io.index}, {&ctx->npoints, &io.npoints},
                         {&ctx->pts_f, &io.pts_f}, {&ctx->colors, &io.colors},
-                        {&ctx->nrm_f, &io.nrm_f}})
+                        {&ctx->nrm_f, &io.nrm_f}, {&ctx->nrm_o, &io.nrm_o}})
           if (pr.second->borrowed || pr.first->borrowed) std::swap(*pr.first, *pr.second);
       };
       swap_lent();
@@ -1590,17 +1613,63 @@ ss_status ss_stereo_batch(ss_ctx* ctx, int32_t n, int32_t w, int32_t h, int32_t 
     if (n > 0 && (!left || !right)) raise(SS_EINVAL, "ss_stereo_batch: null inputs");
     if (in_format != SS_IN_RGB && in_format != SS_IN_GRAY)
       raise(SS_EINVAL, "ss_stereo_batch: unknown input format");
-    const bool cloud = (out_flags & (SS_OUT_CLOUD | SS_OUT_NORMALS)) != 0;
+    const bool oct = (out_flags & SS_OUT_NORMALS_OCT) != 0;
+    const bool cloud = (out_flags & (SS_OUT_CLOUD | SS_OUT_NORMALS)) != 0 || oct;
+    const bool trim = cloud && (out_flags & SS_OUT_TRIM) != 0;
     if (cloud && !ctx->has_rig)
       raise(SS_EINVAL, "stereo batch: cloud output requested but ctx has no rig");
     ctx->activate();
     const long N = (long)w * h;
     const long in_bytes = (in_format == SS_IN_RGB ? 3 : 1) * N;
+    if (trim) ctx->ensure_host_counts();
     // Chunk k on slot k % 2: H2D (s_in) || chain (stream) || D2H (s_out).
-    // Cloud arrays leave at full per-frame capacity (no host round trip for
-    // the point counts); entries past n_points[f] are unspecified.
+    // Without SS_OUT_TRIM the cloud arrays leave at full per-frame capacity
+    // (entries past n_points[f] unspecified) right behind their chain. With
+    // it, chunk k's per-frame point counts come back first; the host reads
+    // them once chunk k+1's chain is queued (so the GPU never waits on the
+    // host) and then queues n_points[f] entries per frame.
+    struct Done {
+      int f0, m, slot;
+      ss_batch_out r;
+    };
+    auto cloud_d2h = [&](const Done& c, const int32_t* counts) {
+      cudaStream_t so = ctx->s_out;
+      for (int j = 0; j < c.m; ++j) {
+        const long f = c.f0 + j;
+        const long np = counts ? counts[j] : N;
+        if (out->points)
+          d2h(out->points + f * N * 3, c.r.points + j * N * 3, sizeof(float) * 3 * np, so);
+        if (out->colors) d2h(out->colors + f * N * 3, c.r.colors + j * N * 3, 3 * np, so);
+        if (oct && out->normals_oct)
+          d2h(out->normals_oct + f * N * 2, c.r.normals_oct + j * N * 2, sizeof(int16_t) * 2 * np,
+              so);
+        if (!oct && out->normals && (out_flags & SS_OUT_NORMALS))
+          d2h(out->normals + f * N * 3, c.r.normals + j * N * 3, sizeof(float) * 3 * np, so);
+        if (!counts) break;  // full capacity: one copy per array covers the chunk
+      }
+    };
+    auto full_cloud_d2h = [&](const Done& c) {
+      cudaStream_t so = ctx->s_out;
+      const long m = c.m, f0 = c.f0;
+      if (out->points) d2h(out->points + f0 * N * 3, c.r.points, sizeof(float) * 3 * N * m, so);
+      if (out->colors) d2h(out->colors + f0 * N * 3, c.r.colors, 3 * N * m, so);
+      if (oct && out->normals_oct)
+        d2h(out->normals_oct + f0 * N * 2, c.r.normals_oct, sizeof(int16_t) * 2 * N * m, so);
+      if (!oct && out->normals && (out_flags & SS_OUT_NORMALS))
+        d2h(out->normals + f0 * N * 3, c.r.normals, sizeof(float) * 3 * N * m, so);
+    };
+    auto finish_trim = [&](const Done& c) {
+      ss_ctx::Slot& sl = ctx->slots[c.slot];
+      ck(cudaEventSynchronize(sl.counts_ready), "cudaEventSynchronize");
+      const int32_t* counts =
+          out->n_points ? out->n_points + c.f0 : ctx->h_counts + c.slot * ctx->max_batch;
+      cloud_d2h(c, counts);
+      ck(cudaEventRecord(sl.out_free, ctx->s_out), "record");
+    };
     try {
       int k = 0;
+      Done prev{};
+      bool have_prev = false;
       for (int f0 = 0; f0 < n; f0 += ctx->max_batch, ++k) {
         const int m = std::min(ctx->max_batch, n - f0);
         ss_ctx::Slot& sl = ctx->slots[k & 1];
@@ -1613,7 +1682,7 @@ ss_status ss_stereo_batch(ss_ctx* ctx, int32_t n, int32_t w, int32_t h, int32_t 
         ctx->swap_outputs(sl);
         try {
           ctx->run_chain(m, w, h, in_format, sl.in_l.as<uint8_t>(), sl.in_r.as<uint8_t>(),
-                         out_flags);
+                         out_flags & ~(uint32_t)SS_OUT_TRIM);
         } catch (...) {
           ctx->swap_outputs(sl);
           throw;
@@ -1622,19 +1691,27 @@ ss_status ss_stereo_batch(ss_ctx* ctx, int32_t n, int32_t w, int32_t h, int32_t 
         ck(cudaEventRecord(sl.done, ctx->stream), "record");
         cudaStream_t so = ctx->s_out;
         ck(cudaStreamWaitEvent(so, sl.done, 0), "wait");
-        const ss_batch_out& r = ctx->last;
+        const Done cur{f0, m, k & 1, ctx->last};
+        const ss_batch_out& r = cur.r;
         if (out->disparity) d2h(out->disparity + f0 * N, r.disparity, sizeof(float) * N * m, so);
         if (out->valid) d2h(out->valid + f0 * N, r.valid, N * m, so);
         if (cloud) {
-          if (out->n_points) d2h(out->n_points + f0, r.n_points, sizeof(int) * m, so);
           if (out->index) d2h(out->index + f0 * N, r.index, sizeof(int) * N * m, so);
-          if (out->points) d2h(out->points + f0 * N * 3, r.points, sizeof(float) * 3 * N * m, so);
-          if (out->colors) d2h(out->colors + f0 * N * 3, r.colors, 3 * N * m, so);
-          if (out->normals && (out_flags & SS_OUT_NORMALS))
-            d2h(out->normals + f0 * N * 3, r.normals, sizeof(float) * 3 * N * m, so);
+          int32_t* hc = out->n_points ? out->n_points + f0
+                                      : (trim ? ctx->h_counts + (k & 1) * ctx->max_batch : nullptr);
+          if (hc) d2h(hc, r.n_points, sizeof(int) * m, so);
         }
-        ck(cudaEventRecord(sl.out_free, so), "record");
+        if (!trim) {
+          if (cloud) full_cloud_d2h(cur);
+          ck(cudaEventRecord(sl.out_free, so), "record");
+        } else {
+          ck(cudaEventRecord(sl.counts_ready, so), "record");
+          if (have_prev) finish_trim(prev);
+          prev = cur;
+          have_prev = true;
+        }
       }
+      if (trim && have_prev) finish_trim(prev);
     } catch (...) {
       // no copy may still be writing into (or reading from) the caller's
       // host buffers once the error is returned

@@ -334,10 +334,13 @@ class StereoContext:
     @staticmethod
     def alloc_outputs(n, h, w, out_flags, alloc=np.empty):
         o = {"disparity": alloc((n, h, w), np.float32), "valid": alloc((n, h, w), np.uint8)}
-        if out_flags & (L.SS_OUT_CLOUD | L.SS_OUT_NORMALS):
+        oct_ = bool(out_flags & L.SS_OUT_NORMALS_OCT)
+        if out_flags & (L.SS_OUT_CLOUD | L.SS_OUT_NORMALS) or oct_:
             o.update(index=alloc((n, h, w), np.int32), points=alloc((n, h * w, 3), np.float32),
                      colors=alloc((n, h * w, 3), np.uint8), n_points=alloc((n,), np.int32))
-        if out_flags & L.SS_OUT_NORMALS:
+        if oct_:
+            o["normals_oct"] = alloc((n, h * w, 2), np.int16)
+        elif out_flags & L.SS_OUT_NORMALS:
             o["normals"] = alloc((n, h * w, 3), np.float32)
         return o
 
@@ -414,6 +417,20 @@ def stereo_frame(left, right, params=None, rig=None, out_flags=L.SS_OUT_DISPARIT
     _check(L.lib().ss_stereo_frame(C.byref(_params(params)), r, w, h, in_format, _ptr(left),
                                    _ptr(right), out_flags, C.byref(bo)))
     return out
+
+
+def decode_oct_normals(enc):
+    """SS_OUT_NORMALS_OCT payload (..., 2) int16 -> unit normals (..., 3) float32
+    (the inverse octahedral map of ss_oct_decode in include/ss_stereo.h)."""
+    e = np.asarray(enc, np.float32) / 32767.0
+    x, y = e[..., 0], e[..., 1]
+    z = 1.0 - np.abs(x) - np.abs(y)
+    neg = z < 0
+    xs = np.where(neg, (1.0 - np.abs(y)) * np.where(x < 0, -1.0, 1.0), x)
+    ys = np.where(neg, (1.0 - np.abs(x)) * np.where(y < 0, -1.0, 1.0), y)
+    n = np.stack([xs, ys, z], axis=-1).astype(np.float32)
+    ln = np.linalg.norm(n, axis=-1, keepdims=True)
+    return n / np.where(ln > 0, ln, 1.0)
 
 
 def pinned_empty(shape, dtype):
