@@ -369,7 +369,7 @@ __device__ double disc_fill_exact(const float* __restrict__ din, const uint8_t* 
 constexpr int kDiscMaxR = 31;  // (2R+1)^2 <= 3969 taps in shared memory
 __host__ __device__ inline int disc_tab_cap(int R) { return ((2 * R + 1) * (2 * R + 1) + 31) & ~31; }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
     k_disc_sum_cert(const double* __restrict__ fx, const float* __restrict__ din,
                     const uint8_t* __restrict__ vin, float* __restrict__ dout,
                     uint8_t* __restrict__ vout, const int* __restrict__ list,
@@ -423,14 +423,23 @@ __global__ void __launch_bounds__(256)
     if (!exact_all) {
       const char* xc = reinterpret_cast<const char*>(xf + (long)v * P + u);
       double ws = 0.0, vs = 0.0, as = 0.0;
-#pragma unroll 4
-      for (int k = lane; k < taps32; k += 32) {
-        const double w = s_tw[k];
-        const double x = __ldg(reinterpret_cast<const double*>(xc + s_off[k]));
-        const double p = __dmul_rn(w, x);
-        ws = __fma_rn(w, __double2hiint(x) != kMarkHi ? 1.0 : 0.0, ws);
-        vs = __dadd_rn(vs, p);
-        as = __dadd_rn(as, fabs(p));
+      // batches of 8 taps per lane: all 8 loads in flight before the first use
+      for (int k0 = lane; k0 < taps32; k0 += 8 * 32) {
+        double xs[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = k0 + 32 * j;
+          xs[j] = k < taps32 ? __ldg(reinterpret_cast<const double*>(xc + s_off[k])) : -0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = k0 + 32 * j;
+          const double w = k < taps32 ? s_tw[k] : 0.0;
+          const double p = __dmul_rn(w, xs[j]);
+          ws = __fma_rn(w, __double2hiint(xs[j]) != kMarkHi ? 1.0 : 0.0, ws);
+          vs = __dadd_rn(vs, p);
+          as = __dadd_rn(as, fabs(p));
+        }
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
@@ -573,9 +582,9 @@ void launch_fill_disc(const float* din, const uint8_t* vin, float* dout, uint8_t
   k_disc_select<<<map_grid(W, H, frames, b), b, 0, s>>>(din, vin, dout, vout, pcnt, span, list,
                                                         count, fx, meta, W, H, std::max(radius, 0),
                                                         min_support, stride, pstride);
-  // persistent grid: ~8 blocks per SM over all frames; each block's warps
+  // persistent grid: ~4 blocks per SM over all frames; each block's warps
   // stride through their frame's device-side list
-  const int gx = std::max(1, 8 * n_sm / frames);
+  const int gx = std::max(1, 4 * n_sm / frames);
   const long D = 2L * std::max(radius, 0) + 1;
   if (radius <= kDiscMaxR) {
     k_disc_pad<<<dim3((unsigned)((disc_frame(W, H, radius) - (long)W * H + 255) / 256), frames), 256,

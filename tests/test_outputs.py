@@ -44,7 +44,7 @@ def test_trim_and_oct_match_full_outputs():
     flags = ss.SS_OUT_DISPARITY | ss.SS_OUT_CLOUD | ss.SS_OUT_NORMALS_OCT | ss.SS_OUT_TRIM
     out = ss.StereoContext.alloc_outputs(n, H, W, flags)
     for k in ("points", "colors", "normals_oct"):
-        out[k].fill(0x55)  # sentinel: trimmed entries past n_points must stay untouched
+        out[k].view(np.uint8).fill(0x55)  # sentinel: trimmed entries past n_points must stay untouched
     ctx.run(Ls, Rs, flags, out=out)
     ctx.close()
     for k in ("disparity", "valid", "index", "n_points"):
