@@ -776,7 +776,6 @@ def run_ours(args):
         "stage_ms_per_pair": {k: v[0] / F for k, v in stages.items()},
         "exact_resolves": {"wta_pixels": stats["wta_resolved"],
                            "refine_repicks": stats["refine_resolved"],
-                           "disc_fill_exact": stats.get("disc_fill_exact"),
                            "disc_fill_pixels": stats.get("disc_fill_pixels"),
                            "frames": stats["frames"]},
         "extensions": ext,

@@ -272,9 +272,7 @@ typedef struct ss_ctx_stats {
   int64_t refine_resolved;   /* (pixel, iteration) re-picks resolved in exact FP64 */
   int64_t refine_fallback;   /* (pixel, iteration) re-picks recomputed without the cost volume */
   int64_t kernel_launches;   /* kernels launched by this ctx */
-  int64_t disc_fill_exact;   /* disc-filled pixels recomputed in the reference's exact order
-                                (the certified parallel sum was not conclusive) */
-  int64_t disc_fill_pixels;  /* disc-filled pixels */
+  int64_t disc_fill_pixels;  /* pixels that went through the disc fill (all cleanup rounds) */
 } ss_ctx_stats;
 
 ss_status ss_ctx_create(int32_t device, int32_t max_w, int32_t max_h, int32_t max_batch,

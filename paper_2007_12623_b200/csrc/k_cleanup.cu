@@ -10,12 +10,11 @@
 //                      IDW w = 1/(step * {1, sqrt2}), double sums in direction
 //                      order 0..7 (the reference's order, so bit-exact).
 //   k_disc_select /    cleanup.cpp:69-84 — support of every invalid pixel from
-//   k_disc_sum_cert    per-row prefix counts (exact integers); only pixels that
-//                      will be filled enter a compacted list; 8 lanes per
-//                      listed pixel sum the radius-R disc in FP64 (w = 1/sqrt(dd)
-//                      from a table built with the same IEEE ops on the host)
-//                      and certify that the result rounds to the reference's
-//                      float, else recompute it in the reference's raster order.
+//   k_disc_sum         per-row prefix counts (exact integers); only pixels that
+//                      will be filled enter a compacted list, and one thread
+//                      per listed pixel accumulates all valid pixels of the
+//                      radius-R disc in raster order in FP64, w = 1/sqrt(dd)
+//                      from a table built with the same IEEE ops on the host.
 // All maps of a frame stay L2-resident (5 B/pixel); these passes are a few
 // percent of the frame and latency-, not bandwidth-bound.
 #include <math.h>
@@ -269,235 +268,103 @@ __global__ void k_fill_radial_list(const float* __restrict__ din, const uint8_t*
   }
 }
 
+// Invalid-neighbour marker in fx: the smallest denormal (low word 1) — a double
+// converted from a float always has its low 29 mantissa bits zero, so no
+// disparity (not even NaN/inf) carries it, and 0 * marker = +0.
+constexpr int kInvalidLo = 1;
+
 // Disc fill, pass 1: copy the map through and, for invalid pixels, count the
 // valid disc neighbours from per-row prefix counts (exact integers, 2 loads
-// per disc row). Pixels that will be filled go to a per-frame list. fx gets
-// the map as doubles in a layout padded by R on every side, invalid pixels
-// and the padding holding the marker -0.0 (so w * x adds -0.0, which leaves a
-// sum unchanged, and every disc tap of every pixel is in bounds); meta[2f+1]
-// = 1 if a valid pixel holds a value whose high word is the marker's (only
-// -0.0 converts to one: that frame then takes the exact path throughout; the
-// chain never produces one).
-constexpr int kMarkHi = (int)0x80000000;  // high word of -0.0
-
-__host__ __device__ inline long disc_pitch(int W, int R) { return (long)W + 2 * R; }
-__host__ __device__ inline long disc_frame(int W, int H, int R) {
-  return disc_pitch(W, R) * ((long)H + 2 * R);
-}
-
-__global__ void __launch_bounds__(256)
-    k_disc_select(const float* __restrict__ din, const uint8_t* __restrict__ vin,
-                  float* __restrict__ dout, uint8_t* __restrict__ vout,
-                  const int* __restrict__ pcnt, const int* __restrict__ span,
-                  int* __restrict__ list, unsigned* __restrict__ count, double* __restrict__ fx,
-                  unsigned* __restrict__ meta, int W, int H, int radius, int min_support,
-                  long stride, long pstride) {
+// per disc row). Pixels that will be filled go to a per-frame list.
+__global__ void k_disc_select(const float* __restrict__ din, const uint8_t* __restrict__ vin,
+                              float* __restrict__ dout, uint8_t* __restrict__ vout,
+                              const int* __restrict__ pcnt, const int* __restrict__ span,
+                              int* __restrict__ list, unsigned* __restrict__ count,
+                              double* __restrict__ fx, int W, int H, int radius, int min_support,
+                              long stride, long pstride) {
   const long f = blockIdx.z;
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = blockIdx.y * blockDim.y + threadIdx.y;
-  const long P = disc_pitch(W, radius);
-  double* xf = fx + f * disc_frame(W, H, radius) + (long)radius * P + radius;
-  unsigned clash = 0;
+  if (u >= W || v >= H) return;
+  const long i = f * stride + (long)v * W + u;
+  const float od = din[i];
+  const uint8_t ov = vin[i];
+  dout[i] = od;
+  vout[i] = ov;
+  fx[i] = ov ? (double)od : __hiloint2double(0, kInvalidLo);  // invalid neighbour
   bool listed = false;
-  if (u < W && v < H) {
-    const long i = f * stride + (long)v * W + u;
-    const float od = din[i];
-    const uint8_t ov = vin[i];
-    dout[i] = od;
-    vout[i] = ov;
-    const double xd = (double)od;
-    xf[(long)v * P + u] = ov ? xd : -0.0;
-    if (ov) {
-      clash = __double2hiint(xd) == kMarkHi;
-    } else if (radius > 0) {
-      const int* pc = pcnt + f * pstride;
-      const int v0 = max(-radius, -v), v1 = min(radius, H - 1 - v);
-      int support = 0;
-      for (int dv = v0; dv <= v1; ++dv) {
-        const int sx = __ldg(span + (dv < 0 ? -dv : dv));
-        const int* row = pc + (long)(v + dv) * (W + 1);
-        support += __ldg(row + min(W - 1, u + sx) + 1) - __ldg(row + max(0, u - sx));
-      }
-      // The centre is invalid, so it never contributes (cleanup.cpp:74 skips dd == 0).
-      listed = support >= min_support && support > 0;
+  if (!ov && radius > 0) {
+    const int* pc = pcnt + f * pstride;
+    const int v0 = max(-radius, -v), v1 = min(radius, H - 1 - v);
+    int support = 0;
+    for (int dv = v0; dv <= v1; ++dv) {
+      const int sx = __ldg(span + (dv < 0 ? -dv : dv));
+      const int* row = pc + (long)(v + dv) * (W + 1);
+      support += __ldg(row + min(W - 1, u + sx) + 1) - __ldg(row + max(0, u - sx));
     }
+    // The centre is invalid, so it never contributes (cleanup.cpp:74 skips dd == 0).
+    listed = support >= min_support && support > 0;
   }
   warp_append(list + f * stride, count + f, listed, v * W + u);
-  if (__any_sync(0xFFFFFFFFu, clash) && (threadIdx.x & 31) == 0) atomicOr(meta + 2 * f + 1, 1u);
 }
 
-// The reference's raster-order double accumulation (cleanup.cpp:71-83) for
-// one pixel, from the input map itself: the exact path.
-__device__ double disc_fill_exact(const float* __restrict__ din, const uint8_t* __restrict__ vin,
-                                  const int* __restrict__ span, const double* __restrict__ wtab,
-                                  int W, int H, int u, int v, int radius, double& wsum) {
-  const int D = 2 * radius + 1;
-  const int v0 = max(-radius, -v), v1 = min(radius, H - 1 - v);
-  double vsum = 0.0;
-  wsum = 0.0;
-  for (int dv = v0; dv <= v1; ++dv) {
-    const int sx = __ldg(span + (dv < 0 ? -dv : dv));
-    const int a = max(-sx, -u), b = min(sx, W - 1 - u);
-    const long r = (long)(v + dv) * W + u;
-    const double* wr = wtab + (dv + radius) * D + radius;
-    for (int du = a; du <= b; ++du) {
-      if (du == 0 && dv == 0) continue;
-      if (!__ldg(vin + r + du)) continue;
-      const double w = __ldg(wr + du);
-      wsum = __dadd_rn(wsum, w);
-      vsum = __dadd_rn(vsum, __dmul_rn(w, (double)__ldg(din + r + du)));
-    }
-  }
-  return vsum;
+// Disc fill, pass 2: one thread per listed pixel, the reference's raster-order
+// double accumulation (cleanup.cpp:71-83) with w = 1/sqrt(dd) from a host
+// table ((2R+1)^2 doubles, staged in shared memory). The neighbours come from
+// fx = valid ? double(d) : marker (written by pass 1): one load per disc pixel
+// gives both, an invalid one adds +0.0 to both sums, the loads
+// of a row are issued together and only the two FP64 add chains are serial.
+__device__ __forceinline__ void disc_acc(double& wsum, double& vsum, double w, double x) {
+  // invalid: w_eff = 0 adds +0.0 to both sums, which leaves them bit-identical
+  // (neither is ever -0.0: both start at +0.0 and an exactly-zero
+  // round-to-nearest sum is +0.0)
+  const double we = __double2loint(x) != kInvalidLo ? w : 0.0;
+  wsum = __dadd_rn(wsum, we);
+  vsum = __dadd_rn(vsum, __dmul_rn(we, x));
 }
 
-// Disc fill, pass 2 (certified, parallel): one warp per listed pixel. The
-// disc's taps (centre excluded) are a table in raster order in shared memory
-// (padded-layout offset, weight); lane l sums taps l, l + 32, ..., so a warp
-// load reads consecutive pixels of one or two rows, and the 32 partial sums
-// are combined by shuffles. This reassociates the reference's raster-order
-// sums (cleanup.cpp:71-83). Both add the SAME terms — table weights w and
-// products fl(w x) — so each is within gamma_{n-1} sum|term| of the exact
-// sum and they differ by at most 4 n u sum|term| <= 4 n u wsum max|d|
-// (n = taps, u = 2^-53). The reference's fl(vsum / wsum) therefore lies in
-// [q_lo, q_hi], computed with directed rounding; when both ends round to the
-// same float — the output type — that float is the reference's result.
-// Otherwise (~1 pixel per frame), and in a frame where a valid pixel holds
-// the marker, lane 0 recomputes the pixel in the reference's exact order. The
-// weight sum is fma(w, m, wsum) with m in {0, 1}: w m is exact, so it equals
-// the masked add.
-constexpr int kDiscMaxR = 31;  // (2R+1)^2 <= 3969 taps in shared memory
-__host__ __device__ inline int disc_tab_cap(int R) { return ((2 * R + 1) * (2 * R + 1) + 31) & ~31; }
-
-__global__ void __launch_bounds__(256, 4)
-    k_disc_sum_cert(const double* __restrict__ fx, const float* __restrict__ din,
-                    const uint8_t* __restrict__ vin, float* __restrict__ dout,
-                    uint8_t* __restrict__ vout, const int* __restrict__ list,
-                    const unsigned* __restrict__ count, const unsigned* __restrict__ meta,
-                    const int* __restrict__ span, const double* __restrict__ wtab, int W, int H,
-                    int radius, long stride, unsigned long long* __restrict__ ctr) {
-  extern __shared__ double s_tw[];  // [cap] weights, then [cap] byte offsets
+template <bool SMEM>
+__global__ void __launch_bounds__(256)
+    k_disc_sum(const double* __restrict__ fx, float* __restrict__ dout, uint8_t* __restrict__ vout,
+               const int* __restrict__ list, const unsigned* __restrict__ count,
+               const int* __restrict__ span, const double* __restrict__ wtab, int W, int H,
+               int radius, long stride, unsigned long long* __restrict__ ctr) {
+  extern __shared__ double s_w[];
   const int D = 2 * radius + 1;
-  const long P = disc_pitch(W, radius);
-  int* s_off = reinterpret_cast<int*>(s_tw + disc_tab_cap(radius));
-  __shared__ int s_row0[2 * kDiscMaxR + 2];
-  if (threadIdx.x == 0) {
-    int n = 0;
-    for (int dv = -radius; dv <= radius; ++dv) {
-      s_row0[dv + radius] = n;
-      n += 2 * __ldg(span + (dv < 0 ? -dv : dv)) + 1 - (dv == 0 ? 1 : 0);
-    }
-    s_row0[D] = n;
+  if (SMEM) {
+    for (int k = threadIdx.x; k < D * D; k += blockDim.x) s_w[k] = __ldg(wtab + k);
+    __syncthreads();
   }
-  __syncthreads();
-  const int taps = s_row0[D];
-  const int taps32 = (taps + 31) & ~31;  // padded to whole warp passes: w = 0, offset 0
-  // raster-order tap table (dv, then du ascending), centre excluded; byte
-  // offsets into the padded map
-  for (int k = threadIdx.x; k < D * D; k += blockDim.x) {
-    const int dv = k / D - radius, du = k % D - radius;
-    const int sx = __ldg(span + (dv < 0 ? -dv : dv));
-    if ((du < 0 ? -du : du) > sx || (du == 0 && dv == 0)) continue;
-    const int t = s_row0[dv + radius] + du + sx - (dv == 0 && du > 0 ? 1 : 0);
-    s_tw[t] = __ldg(wtab + k);
-    s_off[t] = (int)((dv * P + du) * (long)sizeof(double));
-  }
-  for (int t = taps + threadIdx.x; t < taps32; t += blockDim.x) {
-    s_tw[t] = 0.0;
-    s_off[t] = 0;  // the (invalid) centre: adds w * -0.0 and 0 weight
-  }
-  __syncthreads();
   const long f = blockIdx.y;
   const unsigned n = count[f];
   if (blockIdx.x == 0 && threadIdx.x == 0 && ctr) atomicAdd(ctr + 4, (unsigned long long)n);
-  const bool exact_all = meta[2 * f + 1] != 0;
-  const int lane = threadIdx.x & 31;
-  const unsigned wpb = blockDim.x >> 5;
-  const double c4nu = 4.0 * (double)taps * 0x1p-53;
-  const double* xf = fx + f * disc_frame(W, H, radius) + (long)radius * P + radius;
-  for (unsigned t = blockIdx.x * wpb + (threadIdx.x >> 5); t < n; t += gridDim.x * wpb) {
-    const int idx = list[f * stride + t];
-    const int v = idx / W, u = idx % W;
-    bool done = false;
-    float out = 0.f;
-    if (!exact_all) {
-      const char* xc = reinterpret_cast<const char*>(xf + (long)v * P + u);
-      double ws = 0.0, vs = 0.0, as = 0.0;
-      // batches of 8 taps per lane: all 8 loads in flight before the first use
-      for (int k0 = lane; k0 < taps32; k0 += 8 * 32) {
-        double xs[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int k = k0 + 32 * j;
-          xs[j] = k < taps32 ? __ldg(reinterpret_cast<const double*>(xc + s_off[k])) : -0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int k = k0 + 32 * j;
-          const double w = k < taps32 ? s_tw[k] : 0.0;
-          const double p = __dmul_rn(w, xs[j]);
-          ws = __fma_rn(w, __double2hiint(xs[j]) != kMarkHi ? 1.0 : 0.0, ws);
-          vs = __dadd_rn(vs, p);
-          as = __dadd_rn(as, fabs(p));
-        }
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        ws = __dadd_rn(ws, __shfl_xor_sync(0xFFFFFFFFu, ws, off));
-        vs = __dadd_rn(vs, __shfl_xor_sync(0xFFFFFFFFu, vs, off));
-        as = __dadd_rn(as, __shfl_xor_sync(0xFFFFFFFFu, as, off));
-      }
-      // both sums are within gamma_{n-1} * sum|p| of exact; the computed
-      // sum|p| (as) is within gamma_n of its own exact value: 2.02 n u as
-      // bounds the difference, 4 n u as with margin
-      const double ev = __dmul_ru(c4nu, as);
-      const double ew = __dmul_ru(c4nu, ws);
-      const double nlo = __dsub_rd(vs, ev), nhi = __dadd_ru(vs, ev);
-      const double dlo = __dsub_rd(ws, ew), dhi = __dadd_ru(ws, ew);
-      if (dlo > 0.0) {
-        const double qlo = __ddiv_rd(nlo, nlo >= 0.0 ? dhi : dlo);
-        const double qhi = __ddiv_ru(nhi, nhi >= 0.0 ? dlo : dhi);
-        const float flo = __double2float_rn(qlo), fhi = __double2float_rn(qhi);
-        if (__float_as_uint(flo) == __float_as_uint(fhi) && !isnan(flo)) {
-          done = true;
-          out = flo;
-        }
-      }
-    }
-    if (lane == 0) {
-      if (!done) {
-        double ws;
-        const double vs = disc_fill_exact(din + f * stride, vin + f * stride, span, wtab, W, H,
-                                          u, v, radius, ws);
-        if (ctr) atomicAdd(ctr + 3, 1ull);
-        done = ws > 0.0;
-        out = (float)__ddiv_rn(vs, ws);
-      }
-      if (done) {
-        dout[f * stride + idx] = out;
-        vout[f * stride + idx] = 1;
-      }
-    }
-  }
-}
-
-// Generic disc fill pass 2 (weights table too large for shared memory): one
-// thread per listed pixel in the exact order.
-__global__ void __launch_bounds__(256)
-    k_disc_sum_serial(const float* __restrict__ din, const uint8_t* __restrict__ vin,
-                      float* __restrict__ dout, uint8_t* __restrict__ vout,
-                      const int* __restrict__ list, const unsigned* __restrict__ count,
-                      const int* __restrict__ span, const double* __restrict__ wtab, int W, int H,
-                      int radius, long stride) {
-  const long f = blockIdx.y;
-  const unsigned n = count[f];
+  const double* xf = fx + f * stride;
   for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     const int idx = list[f * stride + t];
-    double ws;
-    const double vs = disc_fill_exact(din + f * stride, vin + f * stride, span, wtab, W, H,
-                                      idx % W, idx / W, radius, ws);
-    if (ws > 0.0) {
-      dout[f * stride + idx] = (float)__ddiv_rn(vs, ws);
+    const int v = idx / W, u = idx % W;
+    const int v0 = max(-radius, -v), v1 = min(radius, H - 1 - v);
+    double wsum = 0.0, vsum = 0.0;
+    for (int dv = v0; dv <= v1; ++dv) {
+      const int sx = __ldg(span + (dv < 0 ? -dv : dv));
+      const int a = max(-sx, -u), b = min(sx, W - 1 - u);
+      const double* xr = xf + (long)(v + dv) * W + u;
+      const int wo = (dv + radius) * D + radius;
+      int du = a;
+      for (; du + 3 <= b; du += 4) {
+        double x[4], w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          x[k] = __ldg(xr + du + k);
+          w[k] = SMEM ? s_w[wo + du + k] : __ldg(wtab + wo + du + k);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) disc_acc(wsum, vsum, w[k], x[k]);
+      }
+      for (; du <= b; ++du)
+        disc_acc(wsum, vsum, SMEM ? s_w[wo + du] : __ldg(wtab + wo + du), __ldg(xr + du));
+    }
+    if (wsum > 0.0) {
+      dout[f * stride + idx] = (float)__ddiv_rn(vsum, wsum);
       vout[f * stride + idx] = 1;
     }
   }
@@ -541,64 +408,25 @@ void launch_fill_radial(const float* din, const uint8_t* vin, float* dout, uint8
                                                         min_support, stride);
 }
 
-// The R-wide frame of fx around the image: the marker (a disc tap there adds
-// nothing), written per call (fx is shared by every geometry of the ctx).
-__global__ void __launch_bounds__(256) k_disc_pad(double* __restrict__ fx, int W, int H, int R) {
-  const long P = disc_pitch(W, R);
-  const long top = (long)R * P;                 // rows -R..-1 (and H..H+R-1 below)
-  const long side = (long)H * 2 * R;            // R columns left and right of each row
-  long k = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  double* xf = fx + blockIdx.y * disc_frame(W, H, R);
-  long y, x;
-  if (k < top) {
-    y = k / P;
-    x = k % P;
-  } else if ((k -= top) < top) {
-    y = R + H + k / P;
-    x = k % P;
-  } else if ((k -= top) < side) {
-    y = R + k / (2 * R);
-    x = k % (2 * R);
-    if (x >= R) x += W;
-  } else {
-    return;
-  }
-  xf[y * P + x] = -0.0;
-}
-
-long disc_fx_elems(int W, int H, int radius) { return disc_frame(W, H, std::max(radius, 0)); }
-
 void launch_fill_disc(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
                       int W, int H, int radius, int min_support, const double* wtab,
                       const int* span, int* pcnt, int* list, unsigned* count, double* fx,
-                      unsigned* meta, unsigned long long* ctr, int frames, long stride,
-                      int n_sm, cudaStream_t s) {
+                      unsigned long long* ctr, int frames, long stride, cudaStream_t s) {
   if (W <= 0 || H <= 0 || frames <= 0) return;
   const long pstride = (long)H * (W + 1);
   launch_row_count(vin, pcnt, W, H, frames, stride, pstride, s);
   cudaMemsetAsync(count, 0, sizeof(unsigned) * frames, s);
-  cudaMemsetAsync(meta, 0, sizeof(unsigned) * 2 * frames, s);
   dim3 b(32, 8);
   k_disc_select<<<map_grid(W, H, frames, b), b, 0, s>>>(din, vin, dout, vout, pcnt, span, list,
-                                                        count, fx, meta, W, H, std::max(radius, 0),
-                                                        min_support, stride, pstride);
-  // persistent grid: ~4 blocks per SM over all frames; each block's warps
-  // stride through their frame's device-side list
-  const int gx = std::max(1, 4 * n_sm / frames);
-  const long D = 2L * std::max(radius, 0) + 1;
-  if (radius <= kDiscMaxR) {
-    k_disc_pad<<<dim3((unsigned)((disc_frame(W, H, radius) - (long)W * H + 255) / 256), frames), 256,
-                 0, s>>>(fx, W, H, std::max(radius, 0));
-    const size_t smem = disc_tab_cap(std::max(radius, 0)) * (sizeof(double) + sizeof(int));
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_disc_sum_cert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_disc_sum_cert<<<dim3(gx, frames), 256, smem, s>>>(fx, din, vin, dout, vout, list, count,
-                                                         meta, span, wtab, W, H,
-                                                         std::max(radius, 0), stride, ctr);
-  } else {
-    k_disc_sum_serial<<<dim3(gx, frames), 256, 0, s>>>(din, vin, dout, vout, list, count, span,
-                                                       wtab, W, H, radius, stride);
-  }
+                                                        count, fx, W, H, radius, min_support,
+                                                        stride, pstride);
+  const size_t wbytes = sizeof(double) * (2 * (size_t)radius + 1) * (2 * (size_t)radius + 1);
+  if (wbytes <= 40 * 1024)
+    k_disc_sum<true><<<dim3(96, frames), 256, wbytes, s>>>(fx, dout, vout, list, count, span, wtab,
+                                                         W, H, radius, stride, ctr);
+  else
+    k_disc_sum<false><<<dim3(96, frames), 256, 0, s>>>(fx, dout, vout, list, count, span, wtab, W,
+                                                     H, radius, stride, ctr);
 }
 
 }  // namespace ssb

@@ -114,7 +114,7 @@ struct DevBuf {
 long round_up(long x, long m) { return (x + m - 1) / m * m; }
 
 // device counters: 0 WTA exact resolves, 1 refine exact re-picks, 2 refine
-// fallbacks, 3 disc-fill exact recomputes, 4 disc-filled pixels
+// fallbacks, 4 disc-filled pixels
 constexpr int kNumCounters = 8;
 
 void validate_params(const ss_stereo_params* p) {
@@ -503,11 +503,10 @@ struct ss_ctx {
     pcnt.ensure(sizeof(int) * (long)H * (W + 1) * n);
     flags.ensure(sizeof(int) * N * n);
     flag_count.ensure(sizeof(unsigned) * n);
-    fx.ensure(sizeof(double) * disc_fx_elems(W, H, radius) * n);
-    fmeta.ensure(sizeof(unsigned) * 2 * n);
+    fx.ensure(sizeof(double) * N * n);
     launch_fill_disc(din, vin, dout, vout, W, H, radius, min_support, wtab.as<double>(),
                      fspan.as<int>(), pcnt.as<int>(), flags.as<int>(), flag_count.as<unsigned>(),
-                     fx.as<double>(), fmeta.as<unsigned>(), ctr(), n, N, n_sm, stream);
+                     fx.as<double>(), ctr(), n, N, stream);
     stats.kernel_launches += 3;
   }
 
@@ -1492,7 +1491,6 @@ ss_status ss_ctx_get_stats(ss_ctx* ctx, ss_ctx_stats* st) {
     st->wta_resolved = (int64_t)c[0];
     st->refine_resolved = (int64_t)c[1];
     st->refine_fallback = (int64_t)c[2];
-    st->disc_fill_exact = (int64_t)c[3];
     st->disc_fill_pixels = (int64_t)c[4];
   });
 }
@@ -1627,7 +1625,8 @@ ss_status ss_stereo_batch(ss_ctx* ctx, int32_t n, int32_t w, int32_t h, int32_t 
     // (entries past n_points[f] unspecified) right behind their chain. With
     // it, chunk k's per-frame point counts come back first; the host reads
     // them once chunk k+1's chain is queued (so the GPU never waits on the
-    // host) and then queues n_points[f] entries per frame.
+    // host) and queues n_points[f] entries per frame ahead of chunk k+1's
+    // copies.
     struct Done {
       int f0, m, slot;
       ss_batch_out r;
@@ -1689,6 +1688,12 @@ ss_status ss_stereo_batch(ss_ctx* ctx, int32_t n, int32_t w, int32_t h, int32_t 
         }
         ctx->swap_outputs(sl);
         ck(cudaEventRecord(sl.done, ctx->stream), "record");
+        // chunk k-1's trimmed copies go ahead of chunk k's on s_out: they
+        // depend only on chain k-1, so chain k+1 never waits behind chain k
+        if (trim && have_prev) {
+          finish_trim(prev);
+          have_prev = false;
+        }
         cudaStream_t so = ctx->s_out;
         ck(cudaStreamWaitEvent(so, sl.done, 0), "wait");
         const Done cur{f0, m, k & 1, ctx->last};
@@ -1706,7 +1711,6 @@ ss_status ss_stereo_batch(ss_ctx* ctx, int32_t n, int32_t w, int32_t h, int32_t 
           ck(cudaEventRecord(sl.out_free, so), "record");
         } else {
           ck(cudaEventRecord(sl.counts_ready, so), "record");
-          if (have_prev) finish_trim(prev);
           prev = cur;
           have_prev = true;
         }

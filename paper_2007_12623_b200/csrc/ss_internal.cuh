@@ -174,15 +174,12 @@ void launch_fill_radial(const float* din, const uint8_t* vin, float* dout, uint8
                         int W, int H, int radius, int min_support, int frames, long stride,
                         cudaStream_t s);
 // pcnt: scratch [frames][H][W+1] ints; list: scratch [frames][W*H]; count: [frames];
-// fx: scratch [frames][disc_fx_elems] doubles (the map padded by R);
-// meta: [frames][2] scratch; wtab: [(2R+1)^2] disc weights (dv-major);
-// ctr[3] += certification fallbacks, ctr[4] += disc-filled pixels
-long disc_fx_elems(int W, int H, int radius);
+// fx: scratch [frames][W*H] doubles; wtab: [(2R+1)^2] disc weights (dv-major);
+// ctr[4] += disc-filled pixels
 void launch_fill_disc(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
                       int W, int H, int radius, int min_support, const double* wtab,
                       const int* span, int* pcnt, int* list, unsigned* count, double* fx,
-                      unsigned* meta, unsigned long long* ctr, int frames, long stride,
-                      int n_sm, cudaStream_t s);
+                      unsigned long long* ctr, int frames, long stride, cudaStream_t s);
 
 struct RefineArgs {
   Geom g;
