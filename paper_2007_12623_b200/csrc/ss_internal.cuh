@@ -248,6 +248,18 @@ void launch_refine_init(const float* disp, const uint8_t* valid, uint8_t* mT, do
 // the reference's double sum unchanged), every pixel takes the unclipped
 // compile-time disc gather.
 __host__ __device__ inline int psum_cw(int W, int ext) { return W + 1 + ext; }
+// Row-major FP64 row prefixes (the refinement's disc gathers at radius kRmR):
+// element (v, c) at v * rm_pitch + c, c in [0, W + ext] (columns past W repeat
+// the row total), frame stride rm_frame; the pitch is even (16-byte rows for
+// the TMA tensor map).
+constexpr int kRmR = 15;
+__host__ __device__ inline int rm_pitch(int W, int ext) { return (W + 1 + ext + 1) & ~1; }
+__host__ __device__ inline long rm_frame(int W, int H, int ext) { return (long)H * rm_pitch(W, ext); }
+void launch_scan_rm(const double* xT, const uint8_t* mT, double* pR, int W, int H, int ext,
+                    int frames, cudaStream_t s);
+void launch_scan_b_rm(const int* soT, const int* cntT, const int* oT, const double* dT,
+                      const uint8_t* mT, double alpha, double one_minus_alpha, double* pR, int W,
+                      int H, int ext, int frames, cudaStream_t s);
 // masked serial row prefix (psum[.][0] = 0, psum_cw(W, ext) columns, BT
 // layout); xT == nullptr for the int scan means x = 1 (disc counts)
 void launch_scan_bt_d(const double* xT, const uint8_t* mT, double* pT, int W, int H, int ext,
