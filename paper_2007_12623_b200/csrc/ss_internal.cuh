@@ -293,6 +293,18 @@ void launch_d_repick(const double* psumT, const uint8_t* mT, const int* cntT,
                      const int* wbase, int2* chg, unsigned* chg_count, Deferred* defer,
                      unsigned* defer_count, const RefineArgs& a, int frames, long gray_stride,
                      cudaStream_t s);
+// Row-major variants at radius kRmR (psumR from launch_scan_rm / _b_rm);
+// rm_ready: the radius fits and the driver accepts the tensor map.
+bool rm_ready(const double* psumR, const RefineArgs& a, int frames);
+void launch_avg_b_rm(const double* psumR, const uint8_t* mT, const int* cntT, const double* oT,
+                     const double* dT, double* avgT, double* bT, const RefineArgs& a, int frames,
+                     cudaStream_t s);
+void launch_d_repick_rm(const double* psumR, const uint8_t* mT, const int* cntT,
+                        const double* avgT, const int* soT, double* dT, int* oT,
+                        const uint8_t* lgray, const uint8_t* rgray, const wscore_t* win,
+                        const int* wbase, int2* chg, unsigned* chg_count, Deferred* defer,
+                        unsigned* defer_count, const RefineArgs& a, int frames, long gray_stride,
+                        cudaStream_t s);
 void launch_repick_exact(const Deferred* defer, const unsigned* defer_count, int* oT,
                          const uint8_t* lgray, const uint8_t* rgray, int2* chg,
                          unsigned* chg_count, const RefineArgs& a, int frames, long gray_stride,
