@@ -787,7 +787,7 @@ void launch_d_repick(const double* psumT, const uint8_t* mT, const int* cntT,
 // The refinement's b-disc gather at the default radius (R = kRmR = 15),
 // restructured around the row-major FP64 prefixes (k_scan_rm / k_scan_b_rm).
 // A block owns a 32 x 32 pixel tile; one TMA tensor copy brings the 62-row,
-// 64-column prefix box (psum columns u0 - R .. u0 + 48, rows v0 - R ..
+// 64-column prefix box (psum columns u0 - R - 1 .. u0 + 47, rows v0 - R ..
 // v0 + 46, out-of-image entries zero-filled) into shared memory.
 //
 // Gather phase — lane = column, each thread a strip of kRmK = 4 vertically
@@ -868,13 +868,15 @@ __device__ __forceinline__ void rm_gather(unsigned char* smem, uint64_t* bar,
     mbar_init(bar, 1);
     mbar_fence_init();
     mbar_expect_tx(bar, (unsigned)kRmTileBytes);
-    tma_load_3d(tile, map, u0 - kRmR, v0 - kRmR, (int)blockIdx.z, bar);
+    // the box starts one column early: the innermost start coordinate must
+    // be 16-byte aligned (an odd double index faults)
+    tma_load_3d(tile, map, u0 - kRmR - 1, v0 - kRmR, (int)blockIdx.z, bar);
   }
   __syncthreads();
   mbar_wait(bar, 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double acc[kRmK] = {0.0, 0.0, 0.0, 0.0};
-  rm_rows<kRmR>(tile + (kRmK * warp) * kRmTP + lane + kRmR, acc,
+  rm_rows<kRmR>(tile + (kRmK * warp) * kRmTP + lane + kRmR + 1, acc,
                 std::make_integer_sequence<int, 2 * kRmR + kRmK>{});
 #pragma unroll
   for (int j = 0; j < kRmK; ++j) sT[kRmK * warp + j][lane] = acc[j];

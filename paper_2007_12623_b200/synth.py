@@ -11,6 +11,8 @@ CUDA path consume the identical bytes.
   variance), amplitude sigma 1.75 elsewhere, and a band of period-16 stripes
   (period < D) that produces wrong matches and outliers for cleanup.
 * ``video``       — C5: textured with a per-frame drift of the disparity field.
+* ``plane`` / ``sphere`` — SPEC.md:610 (acceptance #2): a textured slanted
+  plane, and a sphere in front of a slanted plane, with +-0.5 gray-level noise.
 
 Images are returned as (H, W) uint8 gray planes; ``as_rgb`` replicates them
 into interleaved RGB (luma of (g, g, g) is g, so to_gray is the identity).
@@ -20,9 +22,20 @@ from __future__ import annotations
 import numpy as np
 
 
-def _disparity_field(w, h, D, phase=0.0):
+def _disparity_field(w, h, D, phase=0.0, shape="wave"):
+    """Disparity in RIGHT-image coordinates (x, y): the recipes' smooth field
+    ("wave"), the SPEC acceptance #2 slanted plane, or a sphere in front of a
+    slanted background plane."""
     x = np.arange(w, dtype=np.float64)[None, :]
     y = np.arange(h, dtype=np.float64)[:, None]
+    if shape == "plane":
+        return 0.2 * D + 0.45 * D * x / w + 0.15 * D * y / h + 0.0 * y
+    if shape == "sphere":
+        base = 0.2 * D + 0.25 * D * x / w + 0.1 * D * y / h
+        cx, cy, rad = 0.5 * w, 0.5 * h, 0.35 * min(w, h)
+        r2 = (x - cx) ** 2 + (y - cy) ** 2
+        cap = np.sqrt(np.maximum(rad * rad - r2, 0.0)) / rad  # unit hemisphere height
+        return base + 0.3 * D * cap
     return 0.25 * D + 0.5 * D * x / w + 0.1 * D * np.sin(0.01 * y + phase)
 
 
@@ -45,7 +58,7 @@ def stereo_pair(kind: str = "textured", width: int = 960, height: int = 540, D: 
     rng = np.random.default_rng(seed)
     w, h = width, height
     margin = D + 8
-    if kind in ("textured", "video"):
+    if kind in ("textured", "video", "plane", "sphere"):
         tex = 128.0 + 40.0 * rng.standard_normal((h, w + margin))
     elif kind == "lowtex":
         tex = 100.0 + 1.75 * rng.standard_normal((h, w + margin))
@@ -61,11 +74,15 @@ def stereo_pair(kind: str = "textured", width: int = 960, height: int = 540, D: 
     else:
         raise ValueError(f"unknown synthetic kind {kind!r}")
     phase = 0.05 * frame if kind == "video" else 0.0
-    dtrue = _disparity_field(w, h, D, phase)
+    shape = kind if kind in ("plane", "sphere") else "wave"
+    dtrue = _disparity_field(w, h, D, phase, shape)
     xs = np.arange(w, dtype=np.float64)[None, :] + dtrue
     left = tex[:, :w].copy()
     right = _sample(tex, xs)
-    if kind != "lowtex":
+    if kind in ("plane", "sphere"):  # +-0.5 gray-level noise
+        left = left + rng.uniform(-0.5, 0.5, (h, w))
+        right = right + rng.uniform(-0.5, 0.5, (h, w))
+    elif kind != "lowtex":
         left = left + rng.standard_normal((h, w))
         right = right + rng.standard_normal((h, w))
     else:
@@ -77,9 +94,17 @@ def stereo_pair(kind: str = "textured", width: int = 960, height: int = 540, D: 
     # Ground truth in LEFT coordinates: left u sees the point right x sees when
     # x + d(x) = u; solve x = u - d(x) by fixed-point iteration (|d'| << 1).
     u = np.arange(w, dtype=np.float64)[None, :]
+    rows = np.arange(h)[:, None]
     xr = u - dtrue
-    for _ in range(6):
-        xr = u - (0.25 * D + 0.5 * D * xr / w + 0.1 * D * np.sin(0.01 * np.arange(h)[:, None] + phase))
+    for _ in range(30 if shape == "sphere" else 6):
+        # field value at the fractional right-image positions xr (linear
+        # interpolation of the per-column field; exact for the linear ones)
+        xi = np.clip(xr, 0, w - 1)
+        x0 = np.floor(xi).astype(np.int64)
+        x1 = np.minimum(x0 + 1, w - 1)
+        t = xi - x0
+        dr = dtrue[rows, x0] * (1 - t) + dtrue[rows, x1] * t
+        xr = u - dr
     dleft = u - xr
     return _to_u8(left), _to_u8(right), dleft
 
