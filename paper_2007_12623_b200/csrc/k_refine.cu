@@ -813,6 +813,7 @@ constexpr int kRmTP = 64;                  // tile pitch (63 prefix columns used
 constexpr int kRmTR = 32 + 2 * kRmR;       // tile rows
 constexpr size_t kRmTileBytes = sizeof(double) * kRmTP * kRmTR;
 constexpr size_t kRmSmem = kRmTileBytes + sizeof(double) * 32 * 33;
+constexpr size_t kRmSmemWin = kRmSmem + kWinSmem;  // + the tile's score windows
 
 // strip pixel J reads prefix row T as its disc row dy = T - J, span s
 __host__ __device__ constexpr bool rm_in(int R, int T, int J) { return T - J >= -R && T - J <= R; }
@@ -913,7 +914,7 @@ __global__ void __launch_bounds__(kRmThreads, 4)
 }
 
 template <bool USE_SO>
-__global__ void __launch_bounds__(kRmThreads, 4)
+__global__ void __launch_bounds__(kRmThreads, 3)
     k_d_repick_rm(const uint8_t* __restrict__ mT, const int* __restrict__ cntT,
                   const double* __restrict__ avgT, const int* __restrict__ soT,
                   double* __restrict__ dT, int* __restrict__ oT, const uint8_t* __restrict__ lgray,
@@ -923,47 +924,87 @@ __global__ void __launch_bounds__(kRmThreads, 4)
                   unsigned* __restrict__ defer_count, RefineArgs a, long gray_stride,
                   const __grid_constant__ CUtensorMap map) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar;
-  rm_gather(smem, &bar, &map);
-  const double(*sT)[33] = reinterpret_cast<const double(*)[33]>(smem + kRmTileBytes);
+  __shared__ __align__(8) uint64_t bar, bar_win;
   const long f = blockIdx.z;
   const int W = a.g.W, H = a.g.H, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long bs = bt_frame(W, H, 0);
-  const int rb = blockIdx.y, v = rb * 32 + lane;
+  const int rb = blockIdx.y, v = rb * 32 + lane, u0 = blockIdx.x * 32;
+  const int ncols = min(32, W - u0);
+  // The tile's score windows go to shared memory on their own barrier, and
+  // every re-pick-phase field is loaded into registers, before the gather:
+  // both arrive while the disc sums are computed.
+  uint32_t* planes = reinterpret_cast<uint32_t*>(smem + kRmSmem);
+  if (threadIdx.x == 0 && win) {
+    mbar_init(&bar_win, 1);
+    mbar_fence_init();
+    const unsigned npx = ncols * 32;
+    mbar_expect_tx(&bar_win, (kWin / 2) * npx * 4);
+    const uint32_t* wsrc = reinterpret_cast<const uint32_t*>(win) + f * bs * (kWin / 2);
+#pragma unroll 1
+    for (int j = 0; j < kWin / 2; ++j)
+      bulk_g2s(planes + j * kWinPlane, wsrc + (((long)rb * (kWin / 2) + j) * W + u0) * 32,
+               npx * 4, &bar_win);
+  }
+  constexpr int kP = 32 / kRmWarps;  // re-pick pixels per thread
+  uint32_t mk = 0;                   // mask bits of the thread's pixels
+  int cnk[kP], sok[kP], olk[kP], wbk[kP];
+  double avk[kP];
+#pragma unroll
+  for (int k = 0; k < kP; ++k) {
+    const int t = warp + kRmWarps * k;
+    cnk[k] = sok[k] = olk[k] = 0;
+    wbk[k] = kNoWin;
+    avk[k] = 0.0;
+    if (t < ncols && v < H) {
+      const long bi = f * bs + ((long)rb * W + u0 + t) * 32 + lane;
+      if (mT[bi]) {
+        mk |= 1u << k;
+        cnk[k] = cntT[bi];
+        if (USE_SO) {
+          sok[k] = soT[bi];
+          olk[k] = oT[bi];
+        } else {
+          avk[k] = avgT[bi];
+        }
+        if (win) wbk[k] = wbase[bi];
+      }
+    }
+  }
+  rm_gather(smem, &bar, &map);
+  const double(*sT)[33] = reinterpret_cast<const double(*)[33]>(smem + kRmTileBytes);
   const uint8_t* L = lgray + f * gray_stride;
   const uint8_t* Rg = rgray + f * gray_stride;
-  const uint32_t* wplanes =
-      win ? reinterpret_cast<const uint32_t*>(win) + f * bs * (kWin / 2) : nullptr;
-#pragma unroll 1
-  for (int k = 0; k < 32 / kRmWarps; ++k) {
-    const int t = warp + kRmWarps * k, u = blockIdx.x * 32 + t;
-    if (u >= W || v >= H) continue;
+  bool win_ready = win == nullptr;
+#pragma unroll
+  for (int k = 0; k < kP; ++k) {
+    if (!((mk >> k) & 1u)) continue;
+    const int t = warp + kRmWarps * k, u = u0 + t;
     const long px = ((long)rb * W + u) * 32 + lane;  // frame-local BT index
     const long bi = f * bs + px;
-    if (!mT[bi]) continue;
-    const double c = (double)cntT[bi];
+    const double c = (double)cnk[k];
     const double bav = __ddiv_rn(sT[lane][t], c);
-    const double a_o = USE_SO ? __ddiv_rn((double)soT[bi], c) : avgT[bi];
+    const double a_o = USE_SO ? __ddiv_rn((double)sok[k], c) : avk[k];
     const double x = __dsub_rn(a_o, bav);
     const double dv = x < a.lo ? a.lo : (a.hi < x ? a.hi : x);  // std::clamp
     dT[bi] = dv;
-    const int wbk = win ? wbase[bi] : kNoWin;
-    const WinView wv{wplanes ? wplanes + ((long)rb * (kWin / 2) * W + u) * 32 + lane : nullptr,
-                     (long)W * 32};
-    const int best = repick(a, u, v, dv, L, Rg, win != nullptr, wv, wbk, px, defer + f * bs,
+    if (!win_ready) {
+      mbar_wait(&bar_win, 0);
+      win_ready = true;
+    }
+    const WinView wv{planes + t * 32 + lane, kWinPlane};
+    const int best = repick(a, u, v, dv, L, Rg, win != nullptr, wv, wbk[k], px, defer + f * bs,
                             defer_count + f);
     if (best != INT_MIN) {
       if (!USE_SO) {
         oT[bi] = best;
-      } else {
-        const int olk = oT[bi];
-        if (best != olk) {  // o only changes for a few hundred pixels per frame
-          chg[f * bs + atomicAdd(chg_count + f, 1u)] = make_int2((int)px, best - olk);
-          oT[bi] = best;
-        }
+      } else if (best != olk[k]) {  // o only changes for a few hundred pixels per frame
+        chg[f * bs + atomicAdd(chg_count + f, 1u)] = make_int2((int)px, best - olk[k]);
+        oT[bi] = best;
       }
     }
   }
+  // the window copies must land before the block's shared memory is released
+  if (!win_ready) mbar_wait(&bar_win, 0);
 }
 
 bool make_psum_rm_tmap(CUtensorMap* map, const double* base, int W, int H, int frames) {
@@ -1010,12 +1051,18 @@ void launch_d_repick_rm(const double* psumR, const uint8_t* mT, const int* cntT,
   CUtensorMap map;
   if (!make_psum_rm_tmap(&map, psumR, a.g.W, a.g.H, frames)) return;
   dim3 grid((a.g.W + 31) / 32, (a.g.H + 31) / 32, frames);
+  static bool configured = false;
+  if (!configured) {
+    set_smem(k_d_repick_rm<false>, kRmSmemWin);
+    set_smem(k_d_repick_rm<true>, kRmSmemWin);
+    configured = true;
+  }
   if (avgT)
-    k_d_repick_rm<false><<<grid, kRmThreads, kRmSmem, s>>>(
+    k_d_repick_rm<false><<<grid, kRmThreads, kRmSmemWin, s>>>(
         mT, cntT, avgT, soT, dT, oT, lgray, rgray, win, wbase, chg, chg_count, defer,
         defer_count, a, gray_stride, map);
   else
-    k_d_repick_rm<true><<<grid, kRmThreads, kRmSmem, s>>>(
+    k_d_repick_rm<true><<<grid, kRmThreads, kRmSmemWin, s>>>(
         mT, cntT, avgT, soT, dT, oT, lgray, rgray, win, wbase, chg, chg_count, defer,
         defer_count, a, gray_stride, map);
 }
