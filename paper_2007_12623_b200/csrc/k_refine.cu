@@ -448,10 +448,9 @@ namespace {
 
 // A thread's window: 16 fp16 match costs (m_code) in 8 u32 planes of shared memory.
 struct WinView {
-  const uint32_t* p;  // plane 0 word of this pixel; plane j at p[j * stride]
-  long stride;        // kWinPlane (shared-memory stash) or W * 32 (global BT planes)
+  const uint32_t* p;  // plane 0 word of this pixel; plane j at p[j * kWinPlane]
   __device__ __forceinline__ float mcost(int k) const {  // k in [0, kWin)
-    const uint32_t w = p[(k >> 1) * stride];
+    const uint32_t w = p[(k >> 1) * kWinPlane];
     return __half2float(__ushort_as_half((unsigned short)((k & 1) ? (w >> 16) : (w & 0xFFFFu))));
   }
 };
@@ -567,7 +566,7 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
     const int off = c_lo - wb, par = off & 1, w0 = off >> 1;
     uint32_t wd[6];
 #pragma unroll
-    for (int i = 0; i < 6; ++i) wd[i] = wv.p[min(w0 + i, kWin / 2 - 1) * wv.stride];
+    for (int i = 0; i < 6; ++i) wd[i] = wv.p[min(w0 + i, kWin / 2 - 1) * kWinPlane];
     const unsigned sel_e = par ? 0x3232u : 0x1010u, sel_o = par ? 0x5454u : 0x3232u;
     // Branch-free over the 11 slots: slots past c_hi cost +inf. The FMA
     // rounds once where M16 + (eta df) df rounded twice, inside the same bar.
@@ -720,7 +719,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int cnk = s_cnt[slot];
     const int olk = USE_SO ? s_o[slot] : 0;
     const int wbk = win ? s_wb[slot] : kNoWin;
-    const WinView wv{planes + slot, kWinPlane};
+    const WinView wv{planes + slot};
     const double s = disc_sum_any<RF>(P, a.span, W, H, u, v, R);
     const double c = (double)cnk;
     const double bav = __ddiv_rn(s, c);
@@ -780,298 +779,6 @@ void launch_d_repick(const double* psumT, const uint8_t* mT, const int* cntT,
     else k_d_repick<0, true><<<grid, bl, smem, s>>>(SS_REPICK_ARGS, map, tile ? 0 : 1);
   }
 #undef SS_REPICK_ARGS
-}
-
-// ---------------- row-major disc gathers (radius kRmR) ----------------
-//
-// The refinement's b-disc gather at the default radius (R = kRmR = 15),
-// restructured around the row-major FP64 prefixes (k_scan_rm / k_scan_b_rm).
-// A block owns a 32 x 32 pixel tile; one TMA tensor copy brings the 62-row,
-// 64-column prefix box (psum columns u0 - R - 1 .. u0 + 47, rows v0 - R ..
-// v0 + 46, out-of-image entries zero-filled) into shared memory.
-//
-// Gather phase — lane = column, each thread a strip of kRmK = 4 vertically
-// adjacent pixels. Every span difference D_s(r) = P[r][c + s + 1] - P[r][c - s]
-// (the reference's operands, smoothing.cpp:52-58) is computed once per prefix
-// row r and distinct span s, and added to each of the strip's pixels whose disc
-// row r is (a row serves pixels above and below it with the same span): 43
-// shared loads per pixel instead of 62. Each pixel still adds its 31 terms in
-// dy-ascending order, so the sums are bit-identical. Lanes read 32
-// consecutive doubles of one row: conflict-free. The sums are transposed
-// through a padded shared array.
-//
-// Re-pick phase — lane = row (BT order, so the per-pixel fields and score
-// windows are single coalesced lines read straight from global memory), as in
-// k_d_repick. 256 threads and 40 KB of shared memory per block: four blocks
-// per SM, so one block's TMA wait overlaps three others' work.
-namespace {
-
-constexpr int kRmK = 4;                    // pixels per gather strip
-constexpr int kRmWarps = 32 / kRmK;        // 8 warps cover the tile's 32 rows
-constexpr int kRmThreads = 32 * kRmWarps;  // 256
-constexpr int kRmTP = 64;                  // tile pitch (63 prefix columns used)
-constexpr int kRmTR = 32 + 2 * kRmR;       // tile rows
-constexpr size_t kRmTileBytes = sizeof(double) * kRmTP * kRmTR;
-constexpr size_t kRmSmem = kRmTileBytes + sizeof(double) * 32 * 33;
-constexpr size_t kRmSmemWin = kRmSmem + kWinSmem;  // + the tile's score windows
-
-// strip pixel J reads prefix row T as its disc row dy = T - J, span s
-__host__ __device__ constexpr bool rm_in(int R, int T, int J) { return T - J >= -R && T - J <= R; }
-__host__ __device__ constexpr int rm_span(int R, int T, int J) {
-  return rm_in(R, T, J) ? isqrt_floor(R * R - (T - J) * (T - J)) : -1;
-}
-// an earlier strip pixel with the same span on this row (its D is reused)
-template <int R, int T, int J, int I = 0>
-__host__ __device__ constexpr int rm_dup() {
-  if constexpr (I >= J) {
-    return -1;
-  } else if constexpr (rm_in(R, T, I) && rm_span(R, T, I) == rm_span(R, T, J)) {
-    return I;
-  } else {
-    return rm_dup<R, T, J, I + 1>();
-  }
-}
-template <int R, int T, int J>
-__device__ __forceinline__ void rm_step(const double* rp, double (&D)[kRmK],
-                                        double (&acc)[kRmK]) {
-  if constexpr (rm_in(R, T, J)) {
-    constexpr int sx = rm_span(R, T, J);
-    constexpr int dup = rm_dup<R, T, J>();
-    if constexpr (dup >= 0) D[J] = D[dup];
-    else D[J] = __dsub_rn(rp[sx + 1], rp[-sx]);
-    acc[J] = __dadd_rn(acc[J], D[J]);
-  }
-}
-template <int R, int T>
-__device__ __forceinline__ void rm_row(const double* base, double (&acc)[kRmK]) {
-  const double* rp = base + (T + R) * kRmTP;
-  double D[kRmK];
-  rm_step<R, T, 0>(rp, D, acc);
-  rm_step<R, T, 1>(rp, D, acc);
-  rm_step<R, T, 2>(rp, D, acc);
-  rm_step<R, T, 3>(rp, D, acc);
-}
-template <int R, int... I>
-__device__ __forceinline__ void rm_rows(const double* base, double (&acc)[kRmK],
-                                        std::integer_sequence<int, I...>) {
-  (rm_row<R, I - R>(base, acc), ...);  // prefix rows ascending = dy ascending per pixel
-}
-
-// Issue the block's prefix box, gather, and leave the 32 x 32 disc sums in
-// sT[row][col] (rows and columns relative to the tile).
-__device__ __forceinline__ void rm_gather(unsigned char* smem, uint64_t* bar,
-                                          const CUtensorMap* map) {
-  static_assert(kRmK == 4, "rm_row unrolls four strip pixels");
-  double* tile = reinterpret_cast<double*>(smem);
-  double(*sT)[33] = reinterpret_cast<double(*)[33]>(smem + kRmTileBytes);
-  const int u0 = blockIdx.x * 32, v0 = blockIdx.y * 32;
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    mbar_fence_init();
-    mbar_expect_tx(bar, (unsigned)kRmTileBytes);
-    // the box starts one column early: the innermost start coordinate must
-    // be 16-byte aligned (an odd double index faults)
-    tma_load_3d(tile, map, u0 - kRmR - 1, v0 - kRmR, (int)blockIdx.z, bar);
-  }
-  __syncthreads();
-  mbar_wait(bar, 0);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double acc[kRmK] = {0.0, 0.0, 0.0, 0.0};
-  rm_rows<kRmR>(tile + (kRmK * warp) * kRmTP + lane + kRmR + 1, acc,
-                std::make_integer_sequence<int, 2 * kRmR + kRmK>{});
-#pragma unroll
-  for (int j = 0; j < kRmK; ++j) sT[kRmK * warp + j][lane] = acc[j];
-  __syncthreads();
-}
-
-}  // namespace
-
-// Iteration 0: avg = disc mean of o, b = (avg - a o) - (1 - a) d (k_avg_b).
-__global__ void __launch_bounds__(kRmThreads, 4)
-    k_avg_b_rm(const uint8_t* __restrict__ mT, const int* __restrict__ cntT,
-               const double* __restrict__ oT, const double* __restrict__ dT,
-               double* __restrict__ avgT, double* __restrict__ bT, RefineArgs a,
-               const __grid_constant__ CUtensorMap map) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar;
-  rm_gather(smem, &bar, &map);
-  const double(*sT)[33] = reinterpret_cast<const double(*)[33]>(smem + kRmTileBytes);
-  const long f = blockIdx.z;
-  const int W = a.g.W, H = a.g.H, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long bs = bt_frame(W, H, 0);
-  const int v = blockIdx.y * 32 + lane;
-#pragma unroll
-  for (int k = 0; k < 32 / kRmWarps; ++k) {
-    const int t = warp + kRmWarps * k, u = blockIdx.x * 32 + t;
-    if (u >= W || v >= H) continue;
-    const long bi = f * bs + bt_index(W, v, u);
-    if (!mT[bi]) continue;
-    const double av = __ddiv_rn(sT[lane][t], (double)cntT[bi]);
-    avgT[bi] = av;
-    bT[bi] = __dsub_rn(__dsub_rn(av, __dmul_rn(a.alpha, oT[bi])),
-                       __dmul_rn(a.one_minus_alpha, dT[bi]));
-  }
-}
-
-template <bool USE_SO>
-__global__ void __launch_bounds__(kRmThreads, 3)
-    k_d_repick_rm(const uint8_t* __restrict__ mT, const int* __restrict__ cntT,
-                  const double* __restrict__ avgT, const int* __restrict__ soT,
-                  double* __restrict__ dT, int* __restrict__ oT, const uint8_t* __restrict__ lgray,
-                  const uint8_t* __restrict__ rgray, const wscore_t* __restrict__ win,
-                  const int* __restrict__ wbase, int2* __restrict__ chg,
-                  unsigned* __restrict__ chg_count, Deferred* __restrict__ defer,
-                  unsigned* __restrict__ defer_count, RefineArgs a, long gray_stride,
-                  const __grid_constant__ CUtensorMap map) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar, bar_win;
-  const long f = blockIdx.z;
-  const int W = a.g.W, H = a.g.H, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long bs = bt_frame(W, H, 0);
-  const int rb = blockIdx.y, v = rb * 32 + lane, u0 = blockIdx.x * 32;
-  const int ncols = min(32, W - u0);
-  // The tile's score windows go to shared memory on their own barrier, and
-  // every re-pick-phase field is loaded into registers, before the gather:
-  // both arrive while the disc sums are computed.
-  uint32_t* planes = reinterpret_cast<uint32_t*>(smem + kRmSmem);
-  if (threadIdx.x == 0 && win) {
-    mbar_init(&bar_win, 1);
-    mbar_fence_init();
-    const unsigned npx = ncols * 32;
-    mbar_expect_tx(&bar_win, (kWin / 2) * npx * 4);
-    const uint32_t* wsrc = reinterpret_cast<const uint32_t*>(win) + f * bs * (kWin / 2);
-#pragma unroll 1
-    for (int j = 0; j < kWin / 2; ++j)
-      bulk_g2s(planes + j * kWinPlane, wsrc + (((long)rb * (kWin / 2) + j) * W + u0) * 32,
-               npx * 4, &bar_win);
-  }
-  constexpr int kP = 32 / kRmWarps;  // re-pick pixels per thread
-  uint32_t mk = 0;                   // mask bits of the thread's pixels
-  int cnk[kP], sok[kP], olk[kP], wbk[kP];
-  double avk[kP];
-#pragma unroll
-  for (int k = 0; k < kP; ++k) {
-    const int t = warp + kRmWarps * k;
-    cnk[k] = sok[k] = olk[k] = 0;
-    wbk[k] = kNoWin;
-    avk[k] = 0.0;
-    if (t < ncols && v < H) {
-      const long bi = f * bs + ((long)rb * W + u0 + t) * 32 + lane;
-      if (mT[bi]) {
-        mk |= 1u << k;
-        cnk[k] = cntT[bi];
-        if (USE_SO) {
-          sok[k] = soT[bi];
-          olk[k] = oT[bi];
-        } else {
-          avk[k] = avgT[bi];
-        }
-        if (win) wbk[k] = wbase[bi];
-      }
-    }
-  }
-  rm_gather(smem, &bar, &map);
-  const double(*sT)[33] = reinterpret_cast<const double(*)[33]>(smem + kRmTileBytes);
-  const uint8_t* L = lgray + f * gray_stride;
-  const uint8_t* Rg = rgray + f * gray_stride;
-  bool win_ready = win == nullptr;
-#pragma unroll
-  for (int k = 0; k < kP; ++k) {
-    if (!((mk >> k) & 1u)) continue;
-    const int t = warp + kRmWarps * k, u = u0 + t;
-    const long px = ((long)rb * W + u) * 32 + lane;  // frame-local BT index
-    const long bi = f * bs + px;
-    const double c = (double)cnk[k];
-    const double bav = __ddiv_rn(sT[lane][t], c);
-    const double a_o = USE_SO ? __ddiv_rn((double)sok[k], c) : avk[k];
-    const double x = __dsub_rn(a_o, bav);
-    const double dv = x < a.lo ? a.lo : (a.hi < x ? a.hi : x);  // std::clamp
-    dT[bi] = dv;
-    if (!win_ready) {
-      mbar_wait(&bar_win, 0);
-      win_ready = true;
-    }
-    const WinView wv{planes + t * 32 + lane, kWinPlane};
-    const int best = repick(a, u, v, dv, L, Rg, win != nullptr, wv, wbk[k], px, defer + f * bs,
-                            defer_count + f);
-    if (best != INT_MIN) {
-      if (!USE_SO) {
-        oT[bi] = best;
-      } else if (best != olk[k]) {  // o only changes for a few hundred pixels per frame
-        chg[f * bs + atomicAdd(chg_count + f, 1u)] = make_int2((int)px, best - olk[k]);
-        oT[bi] = best;
-      }
-    }
-  }
-  // the window copies must land before the block's shared memory is released
-  if (!win_ready) mbar_wait(&bar_win, 0);
-}
-
-bool make_psum_rm_tmap(CUtensorMap* map, const double* base, int W, int H, int frames) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !fn)
-      return false;
-    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
-  const cuuint64_t PW = rm_pitch(W, kRmR);
-  const cuuint64_t dims[3] = {PW, (cuuint64_t)H, (cuuint64_t)frames};
-  const cuuint64_t strides[2] = {PW * 8, PW * 8 * (cuuint64_t)H};
-  const cuuint32_t box[3] = {kRmTP, kRmTR, 1};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
-                strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-bool rm_supported(const RefineArgs& a) { return a.radius == kRmR; }
-
-void launch_avg_b_rm(const double* psumR, const uint8_t* mT, const int* cntT, const double* oT,
-                     const double* dT, double* avgT, double* bT, const RefineArgs& a, int frames,
-                     cudaStream_t s) {
-  if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
-  CUtensorMap map;
-  if (!make_psum_rm_tmap(&map, psumR, a.g.W, a.g.H, frames)) return;  // checked by rm_ready
-  dim3 grid((a.g.W + 31) / 32, (a.g.H + 31) / 32, frames);
-  k_avg_b_rm<<<grid, kRmThreads, kRmSmem, s>>>(mT, cntT, oT, dT, avgT, bT, a, map);
-}
-
-void launch_d_repick_rm(const double* psumR, const uint8_t* mT, const int* cntT,
-                        const double* avgT, const int* soT, double* dT, int* oT,
-                        const uint8_t* lgray, const uint8_t* rgray, const wscore_t* win,
-                        const int* wbase, int2* chg, unsigned* chg_count, Deferred* defer,
-                        unsigned* defer_count, const RefineArgs& a, int frames, long gray_stride,
-                        cudaStream_t s) {
-  if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
-  CUtensorMap map;
-  if (!make_psum_rm_tmap(&map, psumR, a.g.W, a.g.H, frames)) return;
-  dim3 grid((a.g.W + 31) / 32, (a.g.H + 31) / 32, frames);
-  static bool configured = false;
-  if (!configured) {
-    set_smem(k_d_repick_rm<false>, kRmSmemWin);
-    set_smem(k_d_repick_rm<true>, kRmSmemWin);
-    configured = true;
-  }
-  if (avgT)
-    k_d_repick_rm<false><<<grid, kRmThreads, kRmSmemWin, s>>>(
-        mT, cntT, avgT, soT, dT, oT, lgray, rgray, win, wbase, chg, chg_count, defer,
-        defer_count, a, gray_stride, map);
-  else
-    k_d_repick_rm<true><<<grid, kRmThreads, kRmSmemWin, s>>>(
-        mT, cntT, avgT, soT, dT, oT, lgray, rgray, win, wbase, chg, chg_count, defer,
-        defer_count, a, gray_stride, map);
-}
-
-// Whether the row-major path can run (radius and a tensor map the driver accepts).
-bool rm_ready(const double* psumR, const RefineArgs& a, int frames) {
-  if (!rm_supported(a)) return false;
-  CUtensorMap map;
-  return make_psum_rm_tmap(&map, psumR, a.g.W, a.g.H, frames);
 }
 
 // Deferred re-picks: one warp per pixel, lane k scores candidate c_lo + k in

@@ -228,203 +228,6 @@ void launch_scan_b(const int* soT, const int* cntT, const int* oT, const double*
       soT, cntT, oT, dT, mT, alpha, one_minus_alpha, pT, W, RB, ext);
 }
 
-// ---------------- row-major FP64 prefixes (refinement, radius kRmR) ----------------
-// The same serial add chains (lane = row, left to right); the results are
-// staged per 32-column chunk in a padded shared transpose and written out
-// row-major (a warp stores 32 consecutive columns of one row), the layout the
-// row-major disc gathers read with lanes = columns (k_refine.cu).
-
-constexpr int kChunkR = 32;
-
-// psum[v][0] = 0, psum[v][c + 1] = masked prefix of x through column c,
-// psum[v][W + 1 .. W + ext] = the row total.
-__global__ void __launch_bounds__(32)
-    k_scan_rm(const double* __restrict__ xT, const uint8_t* __restrict__ mT,
-              double* __restrict__ pR, int W, int H, int RB, int ext) {
-  __shared__ alignas(128) double xb[2][kChunkR][32];
-  __shared__ alignas(128) uint8_t mb[2][kChunkR][32];
-  __shared__ double tr[kChunkR][33];
-  __shared__ alignas(8) uint64_t bar[2];
-  const int lane = threadIdx.x;
-  const long f = blockIdx.y;
-  const int rb = blockIdx.x;
-  const double* xs = xT + (f * RB + rb) * (long)W * 32;
-  const uint8_t* ms = mT + (f * RB + rb) * (long)W * 32;
-  const int PW = rm_pitch(W, ext);
-  double* dst = pR + f * rm_frame(W, H, ext) + (long)rb * 32 * PW;
-  const int rows = min(32, H - rb * 32);
-  const int nchunks = (W + kChunkR - 1) / kChunkR;
-  if (lane == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  auto issue = [&](int k) {
-    const int c0 = k * kChunkR, cols = min(kChunkR, W - c0);
-    uint64_t* b = &bar[k & 1];
-    mbar_expect_tx(b, cols * 32 * (sizeof(double) + 1));
-    bulk_g2s(&xb[k & 1][0][0], xs + (long)c0 * 32, cols * 32 * sizeof(double), b);
-    bulk_g2s(&mb[k & 1][0][0], ms + (long)c0 * 32, cols * 32, b);
-  };
-  if (lane == 0 && nchunks > 0) issue(0);
-  double s = 0.0;
-  if (lane < rows) dst[(long)lane * PW] = 0.0;  // psum[.][0]
-  for (int k = 0; k < nchunks; ++k) {
-    if (lane == 0 && k + 1 < nchunks) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(k + 1);
-    }
-    mbar_wait(&bar[k & 1], (k >> 1) & 1);
-    const int c0 = k * kChunkR, cols = min(kChunkR, W - c0);
-#pragma unroll 8
-    for (int c = 0; c < cols; ++c) {
-      if (mb[k & 1][c][lane]) s = __dadd_rn(s, xb[k & 1][c][lane]);
-      tr[c][lane] = s;
-    }
-    __syncwarp();
-    // row r's columns c0 + 1 .. c0 + cols, lanes = columns
-    for (int r = 0; r < rows; ++r)
-      if (lane < cols) dst[(long)r * PW + c0 + 1 + lane] = tr[lane][r];
-    __syncwarp();
-  }
-  // row totals past psum[W] (clipped spans read them unclipped)
-  tr[0][lane] = s;
-  __syncwarp();
-  for (int r = 0; r < rows; ++r)
-    for (int c = lane; c < ext; c += 32) dst[(long)r * PW + W + 1 + c] = tr[0][r];
-}
-
-void launch_scan_rm(const double* xT, const uint8_t* mT, double* pR, int W, int H, int ext,
-                    int frames, cudaStream_t s) {
-  if (W <= 0 || H <= 0 || frames <= 0) return;
-  const int RB = (H + 31) / 32;
-  k_scan_rm<<<dim3(RB, frames), 32, 0, s>>>(xT, mT, pR, W, H, RB, ext);
-}
-
-// k_scan_b with the row-major output: warp 0 runs the chains of chunk k-1
-// into the transpose buffer tr[(k-1)&1] while warps 1.. form b for chunk k
-// and store chunk k-2 (tr[k&1]) row-major.
-struct ScanBRmSmem {
-  ScanBRaw raw[2];
-  double b[2][kChunkB][32];
-  double tr[2][kChunkB][33];
-  uint64_t bar[2];
-};
-
-__global__ void __launch_bounds__(32 * kScanBWarps)
-    k_scan_b_rm(const int* __restrict__ soT, const int* __restrict__ cntT,
-                const int* __restrict__ oT, const double* __restrict__ dT,
-                const uint8_t* __restrict__ mT, double alpha, double one_minus_alpha,
-                double* __restrict__ pR, int W, int H, int RB, int ext) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  ScanBRmSmem& S = *reinterpret_cast<ScanBRmSmem*>(smem_raw);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long f = blockIdx.y;
-  const int rb = blockIdx.x;
-  const long base = (f * RB + rb) * (long)W * 32;
-  const int PW = rm_pitch(W, ext);
-  double* dst = pR + f * rm_frame(W, H, ext) + (long)rb * 32 * PW;
-  const int rows = min(32, H - rb * 32);
-  const int nchunks = (W + kChunkB - 1) / kChunkB;
-  auto issue = [&](int k) {
-    const int c0 = k * kChunkB, cols = min(kChunkB, W - c0);
-    const long e0 = base + (long)c0 * 32;
-    const unsigned n = cols * 32;
-    ScanBRaw& B = S.raw[k & 1];
-    uint64_t* bar = &S.bar[k & 1];
-    mbar_expect_tx(bar, n * (3 * sizeof(int) + sizeof(double) + 1));
-    bulk_g2s(&B.so[0][0], soT + e0, n * sizeof(int), bar);
-    bulk_g2s(&B.cnt[0][0], cntT + e0, n * sizeof(int), bar);
-    bulk_g2s(&B.o[0][0], oT + e0, n * sizeof(int), bar);
-    bulk_g2s(&B.d[0][0], dT + e0, n * sizeof(double), bar);
-    bulk_g2s(&B.m[0][0], mT + e0, n, bar);
-  };
-  // copy chunk kk (its chains are in tr[kk & 1]) to rows of dst, warps
-  // [w0, w0 + nw) sharing the rows
-  auto store = [&](int kk, int w0, int nw) {
-    const int c0 = kk * kChunkB, cols = min(kChunkB, W - c0);
-    const double(*t)[33] = S.tr[kk & 1];
-    for (int r = warp - w0; r < rows; r += nw)
-      if (lane < cols) dst[(long)r * PW + c0 + 1 + lane] = t[lane][r];
-  };
-  if (threadIdx.x == 0) {
-    mbar_init(&S.bar[0], 1);
-    mbar_init(&S.bar[1], 1);
-    mbar_fence_init();
-    if (nchunks > 0) issue(0);
-    if (nchunks > 1) issue(1);
-  }
-  __syncthreads();
-  double s = 0.0;
-  for (int r = warp; r < rows; r += kScanBWarps)
-    if (lane == 0) dst[(long)r * PW] = 0.0;
-  for (int k = 0; k <= nchunks; ++k) {
-    if (warp == 0) {
-      if (k >= 1) {  // add chains over chunk k-1
-        const int c0 = (k - 1) * kChunkB, cols = min(kChunkB, W - c0);
-        const double(*bk)[32] = S.b[(k - 1) & 1];
-        double(*t)[33] = S.tr[(k - 1) & 1];
-        if (cols == kChunkB) {
-#pragma unroll 8
-          for (int c = 0; c < kChunkB; ++c) {
-            s = __dadd_rn(s, bk[c][lane]);
-            t[c][lane] = s;
-          }
-        } else {
-          for (int c = 0; c < cols; ++c) {
-            s = __dadd_rn(s, bk[c][lane]);
-            t[c][lane] = s;
-          }
-        }
-      }
-    } else {
-      if (k < nchunks) {  // form b for chunk k
-        mbar_wait(&S.bar[k & 1], (k >> 1) & 1);
-        const int cols = min(kChunkB, W - k * kChunkB);
-        const ScanBRaw& B = S.raw[k & 1];
-        double(*bk)[32] = S.b[k & 1];
-        for (int c = warp - 1; c < cols; c += kScanBWarps - 1) {
-          double b = 0.0;
-          if (B.m[c][lane]) {
-            const double avg = __ddiv_rn((double)B.so[c][lane], (double)B.cnt[c][lane]);
-            b = __dsub_rn(__dsub_rn(avg, __dmul_rn(alpha, (double)B.o[c][lane])),
-                          __dmul_rn(one_minus_alpha, B.d[c][lane]));
-          }
-          bk[c][lane] = b;
-        }
-      }
-      if (k >= 2) store(k - 2, 1, kScanBWarps - 1);  // written by warp 0 in step k-1
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && k + 2 < nchunks) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(k + 2);  // raw[k & 1] was last read in step k
-    }
-  }
-  if (nchunks >= 1) store(nchunks - 1, 0, kScanBWarps);
-  // row totals past psum[W] (the b buffers are free after the last barrier)
-  if (warp == 0) S.b[0][0][lane] = s;
-  __syncthreads();
-  for (int r = warp; r < rows; r += kScanBWarps)
-    for (int c = lane; c < ext; c += 32) dst[(long)r * PW + W + 1 + c] = S.b[0][0][r];
-}
-
-void launch_scan_b_rm(const int* soT, const int* cntT, const int* oT, const double* dT,
-                      const uint8_t* mT, double alpha, double one_minus_alpha, double* pR, int W,
-                      int H, int ext, int frames, cudaStream_t s) {
-  if (W <= 0 || H <= 0 || frames <= 0) return;
-  const int RB = (H + 31) / 32;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_scan_b_rm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(ScanBRmSmem));
-    configured = true;
-  }
-  k_scan_b_rm<<<dim3(RB, frames), 32 * kScanBWarps, sizeof(ScanBRmSmem), s>>>(
-      soT, cntT, oT, dT, mT, alpha, one_minus_alpha, pR, W, H, RB, ext);
-}
-
 // ---------------- normal-layout count scan (cleanup disc support) ----------------
 
 // Per-row prefix counts of a u8 mask, psum[r][c + 1] = #nonzero in [0, c]

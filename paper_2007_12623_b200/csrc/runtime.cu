@@ -559,8 +559,7 @@ struct ss_ctx {
     d.ensure(sizeof(double) * bs * n);
     avg.ensure(sizeof(double) * bs * n);
     b.ensure(sizeof(double) * bs * n);
-    // FP64 row prefix: BT, or row-major for the default radius (rm path)
-    psum.ensure(sizeof(double) * std::max(bp, rm_frame(W, H, std::max(r, 0))) * n);
+    psum.ensure(sizeof(double) * bp * n);  // BT prefix (double)
     pcnt.ensure(sizeof(int) * bp * n);     // BT prefix (int)
     mbt.ensure(bs * n);                    // BT mask
     cnt.ensure(sizeof(int) * bs * n);
@@ -619,21 +618,14 @@ struct ss_ctx {
     }
     defer.ensure(sizeof(Deferred) * bs * n);
     defer_count.ensure(sizeof(unsigned) * n);
-    const bool rm = iters > 0 && rm_ready(psum.as<double>(), a, n);
     auto repick = [&](const double* avgp, int2* chgp, unsigned* chgc) {
       ck(cudaMemsetAsync(defer_count.p, 0, sizeof(unsigned) * n, stream), "memset");
       {
       Stage sp(this, 11);
-      if (rm)
-        launch_d_repick_rm(psum.as<double>(), mT, cnt.as<int>(), avgp, so.as<int>(),
-                           d.as<double>(), op, gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), winp,
-                           wbase.as<int>(), chgp, chgc, defer.as<Deferred>(),
-                           defer_count.as<unsigned>(), a, n, N, stream);
-      else
-        launch_d_repick(psum.as<double>(), mT, cnt.as<int>(), avgp, so.as<int>(),
-                        d.as<double>(), op, gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), winp,
-                        wbase.as<int>(), chgp, chgc, defer.as<Deferred>(),
-                        defer_count.as<unsigned>(), a, n, N, stream);
+      launch_d_repick(psum.as<double>(), mT, cnt.as<int>(), avgp, so.as<int>(), d.as<double>(),
+                      op, gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), winp, wbase.as<int>(),
+                      chgp, chgc, defer.as<Deferred>(), defer_count.as<unsigned>(), a, n, N,
+                      stream);
       stats.kernel_launches += 1;
       }
       Stage sx(this, 12);
@@ -647,21 +639,15 @@ struct ss_ctx {
         // o is the cleanup output (fractional fills): the reference's FP64 path.
         {
           Stage ss(this, 10);
-          if (rm) launch_scan_rm(o.as<double>(), mT, psum.as<double>(), W, H, r, n, stream);
-          else launch_scan_bt_d(o.as<double>(), mT, psum.as<double>(), W, H, r, n, stream);
+          launch_scan_bt_d(o.as<double>(), mT, psum.as<double>(), W, H, r, n, stream);
           stats.kernel_launches += 1;
         }
-        if (rm)
-          launch_avg_b_rm(psum.as<double>(), mT, cnt.as<int>(), o.as<double>(), d.as<double>(),
-                          avg.as<double>(), b.as<double>(), a, n, stream);
-        else
-          launch_avg_b(psum.as<double>(), mT, cnt.as<int>(), o.as<double>(), d.as<double>(),
-                       avg.as<double>(), b.as<double>(), a, n, stream);
+        launch_avg_b(psum.as<double>(), mT, cnt.as<int>(), o.as<double>(), d.as<double>(),
+                     avg.as<double>(), b.as<double>(), a, n, stream);
         stats.kernel_launches += 1;
         {
           Stage ss(this, 10);
-          if (rm) launch_scan_rm(b.as<double>(), mT, psum.as<double>(), W, H, r, n, stream);
-          else launch_scan_bt_d(b.as<double>(), mT, psum.as<double>(), W, H, r, n, stream);
+          launch_scan_bt_d(b.as<double>(), mT, psum.as<double>(), W, H, r, n, stream);
           stats.kernel_launches += 1;
         }
         repick(avg.as<double>(), nullptr, nullptr);
@@ -675,12 +661,8 @@ struct ss_ctx {
         ck(cudaMemsetAsync(chg_count.p, 0, sizeof(unsigned) * n, stream), "memset");
         {
           Stage ss(this, 10);
-          if (rm)
-            launch_scan_b_rm(so.as<int>(), cnt.as<int>(), op, d.as<double>(), mT, a.alpha,
-                             a.one_minus_alpha, psum.as<double>(), W, H, r, n, stream);
-          else
-            launch_scan_b(so.as<int>(), cnt.as<int>(), op, d.as<double>(), mT, a.alpha,
-                          a.one_minus_alpha, psum.as<double>(), W, H, r, n, stream);
+          launch_scan_b(so.as<int>(), cnt.as<int>(), op, d.as<double>(), mT, a.alpha,
+                        a.one_minus_alpha, psum.as<double>(), W, H, r, n, stream);
           stats.kernel_launches += 1;
         }
         repick(nullptr, chg.as<int2>(), chg_count.as<unsigned>());

@@ -248,18 +248,6 @@ void launch_refine_init(const float* disp, const uint8_t* valid, uint8_t* mT, do
 // the reference's double sum unchanged), every pixel takes the unclipped
 // compile-time disc gather.
 __host__ __device__ inline int psum_cw(int W, int ext) { return W + 1 + ext; }
-// Row-major FP64 row prefixes (the refinement's disc gathers at radius kRmR):
-// element (v, c) at v * rm_pitch + c, c in [0, W + ext] (columns past W repeat
-// the row total), frame stride rm_frame; the pitch is even (16-byte rows for
-// the TMA tensor map).
-constexpr int kRmR = 15;
-__host__ __device__ inline int rm_pitch(int W, int ext) { return (W + 1 + ext + 1) & ~1; }
-__host__ __device__ inline long rm_frame(int W, int H, int ext) { return (long)H * rm_pitch(W, ext); }
-void launch_scan_rm(const double* xT, const uint8_t* mT, double* pR, int W, int H, int ext,
-                    int frames, cudaStream_t s);
-void launch_scan_b_rm(const int* soT, const int* cntT, const int* oT, const double* dT,
-                      const uint8_t* mT, double alpha, double one_minus_alpha, double* pR, int W,
-                      int H, int ext, int frames, cudaStream_t s);
 // masked serial row prefix (psum[.][0] = 0, psum_cw(W, ext) columns, BT
 // layout); xT == nullptr for the int scan means x = 1 (disc counts)
 void launch_scan_bt_d(const double* xT, const uint8_t* mT, double* pT, int W, int H, int ext,
@@ -293,18 +281,6 @@ void launch_d_repick(const double* psumT, const uint8_t* mT, const int* cntT,
                      const int* wbase, int2* chg, unsigned* chg_count, Deferred* defer,
                      unsigned* defer_count, const RefineArgs& a, int frames, long gray_stride,
                      cudaStream_t s);
-// Row-major variants at radius kRmR (psumR from launch_scan_rm / _b_rm);
-// rm_ready: the radius fits and the driver accepts the tensor map.
-bool rm_ready(const double* psumR, const RefineArgs& a, int frames);
-void launch_avg_b_rm(const double* psumR, const uint8_t* mT, const int* cntT, const double* oT,
-                     const double* dT, double* avgT, double* bT, const RefineArgs& a, int frames,
-                     cudaStream_t s);
-void launch_d_repick_rm(const double* psumR, const uint8_t* mT, const int* cntT,
-                        const double* avgT, const int* soT, double* dT, int* oT,
-                        const uint8_t* lgray, const uint8_t* rgray, const wscore_t* win,
-                        const int* wbase, int2* chg, unsigned* chg_count, Deferred* defer,
-                        unsigned* defer_count, const RefineArgs& a, int frames, long gray_stride,
-                        cudaStream_t s);
 void launch_repick_exact(const Deferred* defer, const unsigned* defer_count, int* oT,
                          const uint8_t* lgray, const uint8_t* rgray, int2* chg,
                          unsigned* chg_count, const RefineArgs& a, int frames, long gray_stride,
