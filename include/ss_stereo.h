@@ -129,12 +129,14 @@ ss_status ss_refine_disparities(const ss_stereo_params* p, const float* disparit
                                 double* trace_discrete, double* trace_smooth);
 
 /* StereoCloud (cloud.hpp:14-29): index[w*h]; per point (capacity w*h):
- * points xyz, normals xyz (double), colors rgb, pixels (u,v). */
+ * points xyz, normals xyz (double), colors rgb, pixels (u,v). fitted
+ * (optional, may be NULL): 1 where the normal is the plane fit, 0 where the
+ * fit/fallback test of cloud.cpp:81 chose the sight-ray fallback. */
 ss_status ss_disparity_to_cloud(const float* disparity, const uint8_t* valid, int32_t w,
                                 int32_t h, const uint8_t* rgb, int32_t cw, int32_t ch,
                                 const ss_stereo_rig* rig, int32_t* index, double* points,
                                 double* normals, uint8_t* colors, int32_t* pixels,
-                                int32_t* n_points);
+                                int32_t* n_points, uint8_t* fitted);
 
 /* ---- feature front end (features.hpp:45-66) ----
  * Same results as the reference (integer work, bit-exact). */
@@ -250,21 +252,9 @@ typedef struct ss_batch_out {
   int16_t* normals_oct; /* SS_OUT_NORMALS_OCT: [n][w*h][2] */
 } ss_batch_out;
 
-/* Decode one SS_OUT_NORMALS_OCT normal (octahedral map, snorm16). */
-static inline void ss_oct_decode(const int16_t e[2], float n[3]) {
-  float x = (float)e[0] / 32767.0f, y = (float)e[1] / 32767.0f;
-  const float z = 1.0f - (x < 0 ? -x : x) - (y < 0 ? -y : y);
-  if (z < 0) {
-    const float ox = x;
-    x = (1.0f - (y < 0 ? -y : y)) * (ox < 0 ? -1.0f : 1.0f);
-    y = (1.0f - (ox < 0 ? -ox : ox)) * (y < 0 ? -1.0f : 1.0f);
-  }
-  float l = x * x + y * y + z * z;
-  l = l > 0 ? 1.0f / __builtin_sqrtf(l) : 0.0f;
-  n[0] = x * l;
-  n[1] = y * l;
-  n[2] = z * l;
-}
+/* Decode n SS_OUT_NORMALS_OCT normals (octahedral map, snorm16) on the host:
+ * enc[2k], enc[2k+1] -> unit xyz in out[3k..3k+2]. */
+void ss_oct_decode(const int16_t* enc, int64_t n, float* out);
 
 typedef struct ss_ctx_stats {
   int64_t frames;            /* frames processed */

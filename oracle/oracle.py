@@ -93,6 +93,7 @@ class CloudResult:
     colors: np.ndarray
     pixels: np.ndarray
     eigen_gap: np.ndarray
+    decision: np.ndarray = None  # (l1 - t) / t, t = 1e-9 max(1, l2) (cloud.cpp:81)
 
 
 def _p(a, t):
@@ -357,15 +358,25 @@ class Oracle:
         col = np.empty((n, 3), np.uint8)
         pix = np.empty((n, 2), np.int32)
         gap = np.empty((n,), np.float64)
+        dec = np.empty((n,), np.float64)
         npts = _I32(0)
         r = rig if isinstance(rig, OrcRig) else OrcRig(**rig)
         self._check(self.lib.orc_disparity_to_cloud(
             _p(disp, _F32), _p(valid, _U8), w, h, _p(rgb, _U8), cw, ch, C.byref(r),
             _p(index, _I32), _p(pts, _F64), _p(nrm, _F64), _p(col, _U8), _p(pix, _I32),
-            C.byref(npts), _p(gap, _F64)))
+            C.byref(npts), _p(gap, _F64), _p(dec, _F64)))
         k = npts.value
         return CloudResult(index, pts[:k].copy(), nrm[:k].copy(), col[:k].copy(),
-                           pix[:k].copy(), gap[:k].copy())
+                           pix[:k].copy(), gap[:k].copy(), dec[:k].copy())
+
+    def eigen3_sym(self, a):
+        """Eigen 3.4.0 SelfAdjointEigenSolver<Matrix3d> restatement: (evals
+        ascending, evecs as columns, converged)."""
+        a = np.ascontiguousarray(a, np.float64).reshape(3, 3)
+        ev = np.empty(3, np.float64)
+        vec = np.empty((3, 3), np.float64)
+        rc = self.lib.orc_eigen3_sym(_p(a, _F64), _p(ev, _F64), _p(vec, _F64))
+        return ev, vec, rc == 0
 
     def stereo_frame(self, left_rgb, right_rgb, rig, params=None):
         """run_stereo_only order: to_gray -> compute_disparity

@@ -9,9 +9,12 @@
  * the committed golden vectors in tests/golden/ (generated from oracle/_ref by
  * tests/golden/make_golden.py). disparity_to_cloud cannot be pinned that way:
  * the reference needs Eigen, which is absent. Its points follow
- * cloud.cpp:23-39 operation for operation; its normals use a cyclic Jacobi
- * 3x3 eigensolver and are pinned only by the SPEC examples
- * -> "normals parity unpinned".
+ * cloud.cpp:23-39 operation for operation; its normals restate, operation for
+ * operation, the eigensolver the reference calls (cloud.cpp:78:
+ * Eigen::SelfAdjointEigenSolver<Matrix3d>, Eigen 3.4.0 — the version is not
+ * pinned by the reference, whose vendored Eigen is git-ignored): see
+ * eigen3_sym below. Pinned to the SPEC examples and, as an
+ * eigensolver, to LAPACK (numpy.linalg.eigh) in tests/test_oracle.py.
  *
  * Floating point: build with -ffp-contract=off and no -ffast-math/-march
  * (SURVEY.md fact 7). Every double expression below keeps the reference's
@@ -19,6 +22,7 @@
  */
 #include "ss_oracle.h"
 
+#include <float.h>
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -506,56 +510,186 @@ int orc_refine_disparities(const orc_params* p, const float* disp, const uint8_t
 
 /* ---- disparity_to_cloud restatement (cloud.cpp:14-94), Eigen-free ---- */
 
-/* Cyclic Jacobi eigen-decomposition of a symmetric 3x3 matrix. On return
- * evals are ascending and evec[:, k] (column k, row-major a[r][k]) is the
- * unit eigenvector of evals[k]. */
-static void jacobi3(const double a_in[3][3], double evals[3], double evec[3][3]) {
-  double a[3][3], v[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
-  memcpy(a, a_in, sizeof a);
-  for (int sweep = 0; sweep < 50; ++sweep) {
-    const double off = fabs(a[0][1]) + fabs(a[0][2]) + fabs(a[1][2]);
-    const double diag = fabs(a[0][0]) + fabs(a[1][1]) + fabs(a[2][2]);
-    if (off == 0.0 || off <= 1e-300 || off < 1e-18 * diag) break;
-    for (int pq = 0; pq < 3; ++pq) {
-      const int P = pq == 2 ? 1 : 0, Q = pq == 0 ? 1 : 2;
-      const double apq = a[P][Q];
-      if (apq == 0.0) continue;
-      const double theta = (a[Q][Q] - a[P][P]) / (2.0 * apq);
-      const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-      const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
-      for (int k = 0; k < 3; ++k) {
-        const double akp = a[k][P], akq = a[k][Q];
-        a[k][P] = c * akp - s * akq;
-        a[k][Q] = s * akp + c * akq;
+/* Restatement of Eigen 3.4.0 SelfAdjointEigenSolver<Matrix3d>::compute(A,
+ * ComputeEigenvectors) — the call at cloud.cpp:78 — in the same operations
+ * and order (Eigen/src/Eigenvalues/SelfAdjointEigenSolver.h,
+ * Tridiagonalization.h, Jacobi/Jacobi.h, scalar double, no FMA):
+ *  1. mat = lower triangle of A; scale = max |mat_ij| (1 if 0); mat /= scale;
+ *  2. tridiagonalization_inplace_selector<Matrix3d, 3, false>::run: one
+ *     Householder reflection, Q returned in mat;
+ *  3. computeFromTridiagonal_impl: deflate (|e_i| < DBL_MIN, or
+ *     (e_i / eps)^2 <= |d_i| + |d_i+1|), implicit symmetric QR steps with a
+ *     Wilkinson shift (tridiagonal_qr_step), Givens rotations from
+ *     JacobiRotation::makeGivens applied to Q on the right; at most 30 n
+ *     iterations;
+ *  4. eigenvalues sorted ascending with their columns (first minimum),
+ *     then multiplied by scale.
+ * evec[r][k] = component r of the eigenvector of evals[k]. Returns 0, or 1
+ * when the QR iteration did not converge (Eigen's NoConvergence). */
+static double eg_hypot(double x, double y) { /* Eigen positive_real_hypot(|x|, |y|) */
+  x = fabs(x);
+  y = fabs(y);
+  if (isinf(x) || isinf(y)) return INFINITY;
+  if (isnan(x) || isnan(y)) return NAN;
+  const double p = x > y ? x : y; /* numext::maxi(x, y) */
+  if (p == 0.0) return 0.0;
+  const double qp = (y < x ? y : x) / p; /* numext::mini(y, x) / p */
+  return p * sqrt(1.0 + qp * qp);
+}
+
+static void eg_givens(double p, double q, double* c, double* s) { /* makeGivens(p, q) */
+  if (q == 0.0) {
+    *c = p < 0.0 ? -1.0 : 1.0;
+    *s = 0.0;
+  } else if (p == 0.0) {
+    *c = 0.0;
+    *s = q < 0.0 ? 1.0 : -1.0;
+  } else if (fabs(p) > fabs(q)) {
+    const double t = q / p;
+    double u = sqrt(1.0 + t * t);
+    if (p < 0.0) u = -u;
+    *c = 1.0 / u;
+    *s = -t * *c;
+  } else {
+    const double t = p / q;
+    double u = sqrt(1.0 + t * t);
+    if (q < 0.0) u = -u;
+    *s = -1.0 / u;
+    *c = -t * *s;
+  }
+}
+
+/* tridiagonal_qr_step<ColMajor>(diag, subdiag, start, end, Q, 3) */
+static void eg_qr_step(double* diag, double* sub, int start, int end, double Q[3][3]) {
+  const double td = (diag[end - 1] - diag[end]) * 0.5;
+  const double e = sub[end - 1];
+  double mu = diag[end];
+  if (td == 0.0) {
+    mu -= fabs(e);
+  } else if (e != 0.0) {
+    const double e2 = e * e;
+    const double h = eg_hypot(td, e);
+    if (e2 == 0.0)
+      mu -= e / ((td + (td > 0.0 ? h : -h)) / e);
+    else
+      mu -= e2 / (td + (td > 0.0 ? h : -h));
+  }
+  double x = diag[start] - mu;
+  double z = sub[start];
+  for (int k = start; k < end && z != 0.0; ++k) {
+    double c, s;
+    eg_givens(x, z, &c, &s);
+    const double sdk = s * diag[k] + c * sub[k];
+    const double dkp1 = s * sub[k] + c * diag[k + 1];
+    diag[k] = c * (c * diag[k] - s * sub[k]) - s * (c * sub[k] - s * diag[k + 1]);
+    diag[k + 1] = s * sdk + c * dkp1;
+    sub[k] = c * sdk - s * dkp1;
+    if (k > start) sub[k - 1] = c * sub[k - 1] - s * z;
+    x = sub[k];
+    if (k < end - 1) {
+      z = -s * sub[k + 1];
+      sub[k + 1] = c * sub[k + 1];
+    }
+    /* Q = Q * G: columns k, k+1 rotated by G' = (c, -s) (applyOnTheRight) */
+    for (int i = 0; i < 3; ++i) {
+      const double xi = Q[i][k], yi = Q[i][k + 1];
+      Q[i][k] = c * xi + (-s) * yi;
+      Q[i][k + 1] = -(-s) * xi + c * yi;
+    }
+  }
+}
+
+static int eigen3_sym(const double A[3][3], double evals[3], double evec[3][3]) {
+  double m[3][3] = {{0}};
+  double scale = 0.0;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c <= r; ++c) {
+      m[r][c] = A[r][c];
+      if (fabs(m[r][c]) > scale) scale = fabs(m[r][c]);
+    }
+  if (scale == 0.0) scale = 1.0;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c <= r; ++c) m[r][c] /= scale;
+  double diag[3], sub[2];
+  /* tridiagonalization_inplace_selector<MatrixType, 3, false>::run */
+  diag[0] = m[0][0];
+  const double v1norm2 = m[2][0] * m[2][0];
+  if (v1norm2 <= DBL_MIN) {
+    diag[1] = m[1][1];
+    diag[2] = m[2][2];
+    sub[0] = m[1][0];
+    sub[1] = m[2][1];
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) evec[r][c] = r == c ? 1.0 : 0.0;
+  } else {
+    const double beta = sqrt(m[1][0] * m[1][0] + v1norm2);
+    const double invBeta = 1.0 / beta;
+    const double m01 = m[1][0] * invBeta;
+    const double m02 = m[2][0] * invBeta;
+    const double q = 2.0 * m01 * m[2][1] + m02 * (m[2][2] - m[1][1]);
+    diag[1] = m[1][1] + m02 * q;
+    diag[2] = m[2][2] - m02 * q;
+    sub[0] = beta;
+    sub[1] = m[2][1] - m01 * q;
+    const double Q[3][3] = {{1, 0, 0}, {0, m01, m02}, {0, m02, -m01}};
+    memcpy(evec, Q, sizeof Q);
+  }
+  /* computeFromTridiagonal_impl(diag, subdiag, 30, true, evec) */
+  const int n = 3, max_iter = 30;
+  const double precision_inv = 1.0 / DBL_EPSILON;
+  int end = n - 1, start = 0, iter = 0;
+  while (end > 0) {
+    for (int i = start; i < end; ++i) {
+      if (fabs(sub[i]) < DBL_MIN) {
+        sub[i] = 0.0;
+      } else {
+        const double scaled = precision_inv * sub[i];
+        if (scaled * scaled <= (fabs(diag[i]) + fabs(diag[i + 1]))) sub[i] = 0.0;
       }
-      for (int k = 0; k < 3; ++k) {
-        const double apk = a[P][k], aqk = a[Q][k];
-        a[P][k] = c * apk - s * aqk;
-        a[Q][k] = s * apk + c * aqk;
-      }
-      for (int k = 0; k < 3; ++k) {
-        const double vkp = v[k][P], vkq = v[k][Q];
-        v[k][P] = c * vkp - s * vkq;
-        v[k][Q] = s * vkp + c * vkq;
+    }
+    while (end > 0 && sub[end - 1] == 0.0) end--;
+    if (end <= 0) break;
+    iter++;
+    if (iter > max_iter * n) break;
+    start = end - 1;
+    while (start > 0 && sub[start - 1] != 0.0) start--;
+    eg_qr_step(diag, sub, start, end, evec);
+  }
+  const int ok = iter <= max_iter * n;
+  if (ok) {
+    for (int i = 0; i < n - 1; ++i) {
+      int k = 0; /* minCoeff over diag[i..n): first minimum */
+      for (int j = 1; j < n - i; ++j)
+        if (diag[i + j] < diag[i + k]) k = j;
+      if (k > 0) {
+        const double t = diag[i];
+        diag[i] = diag[k + i];
+        diag[k + i] = t;
+        for (int r = 0; r < 3; ++r) {
+          const double tv = evec[r][i];
+          evec[r][i] = evec[r][k + i];
+          evec[r][k + i] = tv;
+        }
       }
     }
   }
-  int idx[3] = {0, 1, 2};
-  for (int i = 0; i < 3; ++i)
-    for (int j = i + 1; j < 3; ++j)
-      if (a[idx[j]][idx[j]] < a[idx[i]][idx[i]]) {
-        const int t = idx[i]; idx[i] = idx[j]; idx[j] = t;
-      }
-  for (int k = 0; k < 3; ++k) {
-    evals[k] = a[idx[k]][idx[k]];
-    for (int r = 0; r < 3; ++r) evec[r][k] = v[r][idx[k]];
-  }
+  for (int k = 0; k < 3; ++k) evals[k] = diag[k] * scale;
+  return ok ? 0 : 1;
+}
+
+int orc_eigen3_sym(const double* a9, double* evals, double* evec9) {
+  double A[3][3], V[3][3];
+  memcpy(A, a9, sizeof A);
+  const int rc = eigen3_sym(A, evals, V);
+  memcpy(evec9, V, sizeof V);
+  return rc;
 }
 
 int orc_disparity_to_cloud(const float* disp, const uint8_t* valid, int32_t w, int32_t h,
                            const uint8_t* rgb, int32_t cw, int32_t ch, const orc_rig* rig,
                            int32_t* index, double* points, double* normals, uint8_t* colors,
-                           int32_t* pixels, int32_t* n_points, double* eigen_gap) {
+                           int32_t* pixels, int32_t* n_points, double* eigen_gap,
+                           double* decision) {
   const int rc = orc_rig_validate(rig);
   if (rc) return rc;
   const long n = (long)w * h;
@@ -608,7 +742,7 @@ int orc_disparity_to_cloud(const float* disp, const uint8_t* valid, int32_t w, i
         }
       double nrm[3] = {0.0, 0.0, -1.0};
       int fitted = 0;
-      double gap = -1.0;
+      double gap = -1.0, margin = -INFINITY;
       if (count >= 3) {
         mean[0] /= count;
         mean[1] /= count;
@@ -626,9 +760,10 @@ int orc_disparity_to_cloud(const float* disp, const uint8_t* valid, int32_t w, i
               for (int c = 0; c < 3; ++c) cov[r][c] += q[r] * q[c];
           }
         double ev[3], vec[3][3];
-        jacobi3(cov, ev, vec);
-        const double m = ev[2] > 1.0 ? ev[2] : 1.0;
-        if (ev[1] > 1e-9 * m) {
+        eigen3_sym(cov, ev, vec);
+        const double m = ev[2] > 1.0 ? ev[2] : 1.0; /* std::max(1.0, ev(2)) */
+        margin = (ev[1] - 1e-9 * m) / (1e-9 * m);
+        if (ev[1] > 1e-9 * m) { /* cloud.cpp:81 */
           nrm[0] = vec[0][0];
           nrm[1] = vec[1][0];
           nrm[2] = vec[2][0];
@@ -651,6 +786,7 @@ int orc_disparity_to_cloud(const float* disp, const uint8_t* valid, int32_t w, i
       normals[3 * pi + 1] = nrm[1];
       normals[3 * pi + 2] = nrm[2];
       if (eigen_gap) eigen_gap[pi] = gap;
+      if (decision) decision[pi] = margin;
     }
   }
   return 0;

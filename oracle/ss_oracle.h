@@ -106,15 +106,24 @@ int ref_match_features(const double* pos_a, const uint64_t* desc_a, int32_t na,
 int ref_histogram_vote(const int32_t* ia, const int32_t* ib, const int32_t* ham,
                        const double* disp, int32_t n, double bin_size, int32_t* order);
 
-/* Restatement-only: disparity_to_cloud (cloud.cpp:14-94), Eigen-free.
+/* Restatement-only: disparity_to_cloud (cloud.cpp:14-94); the normals'
+ * eigensolver restates Eigen 3.4.0 SelfAdjointEigenSolver (orc_eigen3_sym).
  * Outputs are sized for w*h points; *n_points receives the count.
- * points/normals are xyz doubles per point, colors rgb bytes, pixels (u,v). */
+ * points/normals are xyz doubles per point, colors rgb bytes, pixels (u,v).
+ * eigen_gap (optional): (l1 - l0) / l2 of fitted points, -1 otherwise;
+ * decision (optional): (l1 - t) / t with t = 1e-9 max(1, l2), the relative
+ * margin of the fit/fallback test of cloud.cpp:81 (> 0: fitted; -inf: fewer
+ * than 3 neighbours). */
 int orc_disparity_to_cloud(const float* disp, const uint8_t* valid, int32_t w,
                            int32_t h, const uint8_t* rgb, int32_t cw,
                            int32_t ch, const orc_rig* rig, int32_t* index,
                            double* points, double* normals, uint8_t* colors,
                            int32_t* pixels, int32_t* n_points,
-                           double* eigen_gap);
+                           double* eigen_gap, double* decision);
+/* Eigen 3.4.0 SelfAdjointEigenSolver<Matrix3d> restatement on a row-major
+ * 3x3 (lower triangle read): ascending evals, evec9[r*3+k] = component r of
+ * eigenvector k. Returns 1 on NoConvergence. */
+int orc_eigen3_sym(const double* a9, double* evals, double* evec9);
 /* Restatement-only: opt-in left-right consistency (extension, no reference
  * analogue): right-view WTA and the check (ss_compute_disparity_lr). */
 int orc_compute_disparity_right(const orc_params* p, const uint8_t* left,

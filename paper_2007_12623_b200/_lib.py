@@ -99,7 +99,7 @@ def lib():
         "ss_refine_disparities": (i32, [P(SsParams), vp, vp, i32, i32, vp, i32, i32, vp, i32,
                                         i32, vp, vp, vp, vp]),
         "ss_disparity_to_cloud": (i32, [vp, vp, i32, i32, vp, i32, i32, P(SsRig), vp, vp, vp,
-                                        vp, vp, P(i32)]),
+                                        vp, vp, P(i32), vp]),
         "ss_ctx_create": (i32, [i32, i32, i32, i32, P(SsParams), P(SsRig), P(vp)]),
         "ss_ctx_destroy": (i32, [vp]),
         "ss_ctx_stream": (vp, [vp]),
@@ -124,6 +124,7 @@ def lib():
         "ss_multi_last_error": (C.c_char_p, []),
         "ss_host_alloc": (vp, [C.c_size_t]),
         "ss_host_free": (None, [vp]),
+        "ss_oct_decode": (None, [vp, C.c_int64, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -301,7 +301,8 @@ __global__ void __launch_bounds__(kNTX * kNTY, 3)
     k_cloud_normals(const float4* __restrict__ pts4, const float* __restrict__ disp, int W,
                     int H, CloudArgs cargs, double* __restrict__ nrm_d,
                     float* __restrict__ nrm_f, short2* __restrict__ nrm_o,
-                    const int* __restrict__ index, long stride) {
+                    uint8_t* __restrict__ fitted_out, const int* __restrict__ index,
+                    long stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   NormalSmem& S = *reinterpret_cast<NormalSmem*>(smem_raw);
   const long f = blockIdx.z;
@@ -497,6 +498,7 @@ __global__ void __launch_bounds__(kNTX * kNTY, 3)
     nrm_f[o + 1] = (float)nd[1];
     nrm_f[o + 2] = (float)nd[2];
   }
+  if (fitted_out) fitted_out[f * stride + k] = fitted ? 1 : 0;
   if (nrm_o) {
     // octahedral map of the unit normal, snorm16 (decoded by ss_oct_decode)
     const float a = fabsf((float)nd[0]) + fabsf((float)nd[1]) + fabsf((float)nd[2]);
@@ -513,7 +515,8 @@ __global__ void __launch_bounds__(kNTX * kNTY, 3)
 
 void launch_cloud_normals(const float4* pts4, const float* disp, const int* index,
                           const CloudArgs& c, double* nrm_d, float* nrm_f, short2* nrm_o,
-                          int W, int H, int frames, long stride, cudaStream_t s) {
+                          uint8_t* fitted, int W, int H, int frames, long stride,
+                          cudaStream_t s) {
   if (W <= 0 || H <= 0 || frames <= 0) return;
   dim3 b(kNTX, kNTY);
   dim3 grid((W + kNTX - 1) / kNTX, (H + kNTY - 1) / kNTY, frames);
@@ -524,7 +527,7 @@ void launch_cloud_normals(const float4* pts4, const float* disp, const int* inde
     configured = true;
   }
   k_cloud_normals<<<grid, b, sizeof(NormalSmem), s>>>(pts4, disp, W, H, c, nrm_d, nrm_f, nrm_o,
-                                                      index, stride);
+                                                      fitted, index, stride);
 }
 
 }  // namespace ssb

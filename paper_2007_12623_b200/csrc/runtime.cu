@@ -198,7 +198,8 @@ struct ss_ctx {
   int lr_max_diff = 1;
   DevBuf disp_a, disp_b, valid_a, valid_b, flags, flag_count;
   DevBuf o, oi, d, avg, b, psum, pcnt, cnt, span, wtab, fspan, fx, emap;
-  DevBuf index, block_sums, npoints, pts_f, nrm_f, nrm_o, colors, pts_d, nrm_d, pixels, pts4;
+  DevBuf index, block_sums, npoints, pts_f, nrm_f, nrm_o, colors, pts_d, nrm_d, pixels, pts4,
+      fitted;
   DevBuf counters, trace_o, trace_d, so, chg, chg_count, mbt, defer, defer_count, fmeta;
   int n_sm = 148;
   int wtab_radius = -1, span_radius = -1;
@@ -260,7 +261,7 @@ struct ss_ctx {
     for (DevBuf* b : {&in_l, &in_r, &gray_l, &gray_r, &ltap_buf, &rcopy_buf, &lstat, &rstat, &win, &wbase,
                       &disp_a, &disp_b, &valid_a, &valid_b, &flags, &flag_count, &o, &d, &avg,
                       &b, &psum, &pcnt, &cnt, &span, &wtab, &fspan, &fx, &emap, &index, &block_sums, &npoints,
-                      &pts_f, &nrm_f, &nrm_o, &colors, &pts_d, &nrm_d, &pixels, &pts4, &counters, &oi, &trace_o,
+                      &pts_f, &nrm_f, &nrm_o, &colors, &pts_d, &nrm_d, &pixels, &pts4, &fitted, &counters, &oi, &trace_o,
                       &trace_d, &so, &chg, &chg_count, &mbt, &defer, &defer_count, &fmeta, &gray_fl,
                       &gray_fr, &disp_r, &valid_r})
       b->release();
@@ -694,7 +695,7 @@ struct ss_ctx {
   // disparity_to_cloud of (disp, valid) -> index/points/normals/colors.
   void run_cloud(int n, int W, int H, const float* dsp, const uint8_t* vld, const uint8_t* rgb,
                  int cw, int ch, long rgb_stride, bool want_double, bool want_normals,
-                 bool want_pixels, bool want_oct = false) {
+                 bool want_pixels, bool want_oct = false, bool want_fitted = false) {
     Stage st(this, 6);
     const long N = (long)W * H;
     index.ensure(sizeof(int) * N * n);
@@ -715,6 +716,7 @@ struct ss_ctx {
       if (want_normals && want_oct) nrm_o.ensure(sizeof(short2) * N * n);
     }
     if (want_pixels) pixels.ensure(sizeof(int) * 2 * N * n);
+    if (want_fitted) fitted.ensure(N * n);
     pts4.ensure(sizeof(float4) * N * n);
     launch_cloud_points(dsp, index.as<int>(), rgb, cw, ch, W, H, c,
                         want_double ? pts_d.as<double>() : nullptr,
@@ -727,7 +729,8 @@ struct ss_ctx {
       launch_cloud_normals(pts4.as<float4>(), dsp, index.as<int>(), c,
                            want_double ? nrm_d.as<double>() : nullptr,
                            want_double || want_oct ? nullptr : nrm_f.as<float>(),
-                           want_oct ? nrm_o.as<short2>() : nullptr, W, H, n, N, stream);
+                           want_oct ? nrm_o.as<short2>() : nullptr,
+                           want_fitted ? fitted.as<uint8_t>() : nullptr, W, H, n, N, stream);
       stats.kernel_launches += 1;
     }
   }
@@ -1375,7 +1378,7 @@ ss_status ss_disparity_to_cloud(const float* disparity, const uint8_t* valid, in
                                 int32_t h, const uint8_t* rgb, int32_t cw, int32_t ch,
                                 const ss_stereo_rig* rig, int32_t* index, double* points,
                                 double* normals, uint8_t* colors, int32_t* pixels,
-                                int32_t* n_points) {
+                                int32_t* n_points, uint8_t* fitted) {
   return guarded([&] {
     validate_rig(rig);
     check_dims(w, h, "disparity_to_cloud");
@@ -1396,7 +1399,7 @@ ss_status ss_disparity_to_cloud(const float* disparity, const uint8_t* valid, in
       drgb = c->in_l.as<uint8_t>();
     }
     c->run_cloud(1, w, h, c->disp_a.as<float>(), c->valid_a.as<uint8_t>(), drgb, cw, ch, 0,
-                 true, true, true);
+                 true, true, true, false, fitted != nullptr);
     int np = 0;
     d2h(&np, c->npoints.p, sizeof(int), c->stream);
     sync(c);
@@ -1406,6 +1409,7 @@ ss_status ss_disparity_to_cloud(const float* disparity, const uint8_t* valid, in
     d2h(normals, c->nrm_d.p, sizeof(double) * 3 * np, c->stream);
     d2h(colors, c->colors.p, 3L * np, c->stream);
     d2h(pixels, c->pixels.p, sizeof(int) * 2 * np, c->stream);
+    if (fitted) d2h(fitted, c->fitted.p, np, c->stream);
     sync(c);
   });
 }
@@ -1727,6 +1731,23 @@ ss_status ss_stereo_batch(ss_ctx* ctx, int32_t n, int32_t w, int32_t h, int32_t 
     ck(cudaStreamSynchronize(ctx->s_out), "cudaStreamSynchronize");
     sync(ctx);
   });
+}
+
+void ss_oct_decode(const int16_t* enc, int64_t n, float* out) {
+  for (int64_t k = 0; k < n; ++k) {
+    float x = (float)enc[2 * k] / 32767.0f, y = (float)enc[2 * k + 1] / 32767.0f;
+    const float z = 1.0f - std::fabs(x) - std::fabs(y);
+    if (z < 0.0f) {
+      const float ox = x;
+      x = (1.0f - std::fabs(y)) * (ox < 0.0f ? -1.0f : 1.0f);
+      y = (1.0f - std::fabs(ox)) * (y < 0.0f ? -1.0f : 1.0f);
+    }
+    const float l2 = x * x + y * y + z * z;
+    const float l = l2 > 0.0f ? 1.0f / std::sqrt(l2) : 0.0f;
+    out[3 * k + 0] = x * l;
+    out[3 * k + 1] = y * l;
+    out[3 * k + 2] = z * l;
+  }
 }
 
 void* ss_host_alloc(size_t bytes) {

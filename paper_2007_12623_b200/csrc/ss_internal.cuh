@@ -303,9 +303,11 @@ void launch_cloud_points(const float* disp, const int* index, const uint8_t* rgb
                          int ch, int W, int H, const CloudArgs& c, double* pts_d,
                          float* pts_f, float4* pts4, uint8_t* colors, int* pixels, int frames,
                          long stride, long rgb_stride, cudaStream_t s);
-// nrm_o (optional): octahedral snorm16 normals (SS_OUT_NORMALS_OCT)
+// nrm_o (optional): octahedral snorm16 normals (SS_OUT_NORMALS_OCT);
+// fitted (optional): per point, 1 = plane fit, 0 = sight-ray fallback
 void launch_cloud_normals(const float4* pts4, const float* disp, const int* index,
                           const CloudArgs& c, double* nrm_d, float* nrm_f, short2* nrm_o,
-                          int W, int H, int frames, long stride, cudaStream_t s);
+                          uint8_t* fitted, int W, int H, int frames, long stride,
+                          cudaStream_t s);
 
 }  // namespace ssb

@@ -252,7 +252,7 @@ StereoCloud disparity_to_cloud(const DisparityMap& map, const ColorImage& color,
                                  color.width, color.height, &c, cloud.index.data(),
                                  reinterpret_cast<double*>(pts.data()),
                                  reinterpret_cast<double*>(nrm.data()), col.data(), pix.data(),
-                                 &np));
+                                 &np, nullptr));
   cloud.points.assign(pts.begin(), pts.begin() + np);
   cloud.normals.assign(nrm.begin(), nrm.begin() + np);
   cloud.colors.resize(np);

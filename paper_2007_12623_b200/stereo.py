@@ -90,6 +90,7 @@ class StereoCloud:
     normals: np.ndarray
     colors: np.ndarray
     pixels: np.ndarray = field(default=None)
+    fitted: np.ndarray = field(default=None)  # 1: plane fit, 0: sight-ray fallback (cloud.cpp:81)
 
 
 def _params(p) -> L.SsParams:
@@ -256,13 +257,14 @@ def disparity_to_cloud(disp, valid, rgb, rig) -> StereoCloud:
     nrm = np.empty((n, 3), np.float64)
     col = np.empty((n, 3), np.uint8)
     pix = np.empty((n, 2), np.int32)
+    fit = np.empty((n,), np.uint8)
     np_ = C.c_int32(0)
     _check(L.lib().ss_disparity_to_cloud(_ptr(disp), _ptr(valid), w, h, _ptr(rgb), cw, ch,
                                          C.byref(_rig(rig)), _ptr(index), _ptr(pts), _ptr(nrm),
-                                         _ptr(col), _ptr(pix), C.byref(np_)))
+                                         _ptr(col), _ptr(pix), C.byref(np_), _ptr(fit)))
     k = np_.value
     return StereoCloud(w, h, index, pts[:k].copy(), nrm[:k].copy(), col[:k].copy(),
-                       pix[:k].copy())
+                       pix[:k].copy(), fit[:k].copy())
 
 
 class StereoContext:

@@ -98,3 +98,18 @@ def test_device_outputs_written_in_place_with_oct():
         r = want["normals"][f][:m].astype(np.float64)
         ang = np.arctan2(np.linalg.norm(np.cross(d, r), axis=1), (d * r).sum(1))
         assert ang.max() < 1e-4
+
+
+def test_oct_decode_c_abi_matches_python():
+    """ss_oct_decode (host C-ABI helper) equals decode_oct_normals."""
+    import ctypes as C
+
+    from paper_2007_12623_b200 import _lib as L
+    from paper_2007_12623_b200 import decode_oct_normals
+    rng = np.random.default_rng(1)
+    n = rng.standard_normal((5000, 3))
+    n /= np.linalg.norm(n, axis=1, keepdims=True)
+    enc = np.ascontiguousarray(_oct_encode(n))
+    out = np.empty((len(enc), 3), np.float32)
+    L.lib().ss_oct_decode(enc.ctypes.data_as(C.c_void_p), len(enc), out.ctypes.data_as(C.c_void_p))
+    assert np.allclose(out, decode_oct_normals(enc), atol=2e-7)
