@@ -23,7 +23,9 @@ CSRC = os.path.join(PKG, "csrc")
 INC = os.path.join(ROOT, "include")
 OBJ = os.path.join(PKG, "build")
 LIB_DIR = os.path.join(PKG, "lib")
-LIB = os.path.join(LIB_DIR, "libstereoscan_b200.so")
+LIB = os.path.join(LIB_DIR, "libstereoscan_b200.so")          # C-ABI (include/ss_stereo.h)
+LIB_CXX = os.path.join(LIB_DIR, "libstereoscan_b200_cxx.so")  # C++ drop-in API + io on it
+CXX_SRCS = ("stereoscan_api.cpp", "io.cpp")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CUDA_LIB = "/usr/local/cuda/lib64"
 
@@ -73,14 +75,24 @@ def build(verbose: bool = True) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(_compile, srcs))
-    if _newer(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "shared", "-o", LIB] + objs + \
-            ["-Xlinker", f"-rpath,{CUDA_LIB}", "-lz"]
+    core = [o for o, s in zip(objs, srcs) if os.path.basename(s) not in CXX_SRCS]
+    cxx = [o for o, s in zip(objs, srcs) if os.path.basename(s) in CXX_SRCS]
+    if _newer(LIB, core):
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "shared", "-o", LIB] + core + \
+            ["-Xlinker", f"-rpath,{CUDA_LIB}"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
         if verbose:
             print(f"built {LIB}")
+    if _newer(LIB_CXX, cxx + [LIB]):
+        cmd = ["g++", "-shared", "-o", LIB_CXX] + cxx + [f"-L{LIB_DIR}", "-lstereoscan_b200",
+                                                          f"-Wl,-rpath,{LIB_DIR}", "-lz"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"C++ API link failed:\n{r.stdout}\n{r.stderr}")
+        if verbose:
+            print(f"built {LIB_CXX}")
     _build_cpp_test(verbose)
     return LIB
 
@@ -93,9 +105,10 @@ def _build_cpp_test(verbose):
         if not os.path.exists(src):
             continue
         exe = os.path.join(out_dir, name)
-        if _newer(exe, [src, LIB] + _deps()):
+        if _newer(exe, [src, LIB, LIB_CXX] + _deps()):
             cmd = ["g++", "-std=c++17", "-O1", f"-I{INC}", src, "-o", exe, f"-L{LIB_DIR}",
-                   "-lstereoscan_b200", f"-Wl,-rpath,{LIB_DIR}", f"-Wl,-rpath,{CUDA_LIB}"]
+                   "-lstereoscan_b200_cxx", "-lstereoscan_b200", f"-Wl,-rpath,{LIB_DIR}",
+                   f"-Wl,-rpath,{CUDA_LIB}"]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:
                 raise RuntimeError(f"C++ test build failed:\n{r.stdout}\n{r.stderr}")

@@ -72,6 +72,9 @@ void StereoParams::validate() const {
   throw_on(ss_params_validate(&c));
 }
 
+#ifndef SSB_USE_REFERENCE_GEOMETRY
+// Compiled into the reference's build, geometry.cpp keeps these definitions
+// (INTEGRATION.md): -DSSB_USE_REFERENCE_GEOMETRY drops ours.
 void CameraIntrinsics::validate() const {
   StereoRig r;
   r.intrinsics = *this;
@@ -84,6 +87,7 @@ void StereoRig::validate() const {
   const ss_stereo_rig c = to_c(*this);
   throw_on(ss_rig_validate(&c));
 }
+#endif
 
 size_t DisparityMap::valid_count() const {
   size_t n = 0;
@@ -268,6 +272,8 @@ StereoCloud disparity_to_cloud(const DisparityMap& map, const ColorImage& color,
 
 // ---------------- feature front end (features.hpp) ----------------
 
+#ifndef SSB_USE_REFERENCE_FEATURES
+// -DSSB_USE_REFERENCE_FEATURES: the reference keeps its own features.cpp.
 namespace stereoscan::features {
 
 int Descriptor256::hamming(const Descriptor256& other) const {
@@ -391,3 +397,4 @@ std::vector<std::pair<Vec2, Vec2>> read_match_file(const std::string& path) {
 }
 
 }  // namespace stereoscan::features
+#endif
