@@ -114,6 +114,22 @@ def _build_cpp_test(verbose):
                 raise RuntimeError(f"C++ test build failed:\n{r.stdout}\n{r.stderr}")
             if verbose:
                 print(f"built {exe}")
+    # source-compatibility probe: the reference's unmodified reference.cpp
+    # against this repository's headers (only where /root/reference exists;
+    # the binary travels to the GPU box with the snapshot)
+    ref_src = "/root/reference/proj/src/stereo/reference.cpp"
+    ref_inc = "/root/reference/proj/include"
+    src = os.path.join(ROOT, "tests", "cpp", "ref_compat.cpp")
+    exe = os.path.join(out_dir, "ref_compat")
+    if os.path.exists(ref_src) and _newer(exe, [src, ref_src, LIB, LIB_CXX] + _deps()):
+        cmd = ["g++", "-std=c++20", "-O1", f"-I{INC}", f"-idirafter{ref_inc}", src, ref_src,
+               "-o", exe, f"-L{LIB_DIR}", "-lstereoscan_b200_cxx", "-lstereoscan_b200",
+               f"-Wl,-rpath,{LIB_DIR}", f"-Wl,-rpath,{CUDA_LIB}"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"reference.cpp against include/ failed:\n{r.stdout}\n{r.stderr}")
+        if verbose:
+            print(f"built {exe}")
 
 
 if __name__ == "__main__":

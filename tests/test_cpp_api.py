@@ -22,3 +22,26 @@ def test_cpp_api_on_gpu():
     r = subprocess.run([EXE], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "test_api OK" in r.stdout
+
+
+REF_COMPAT = os.path.join(ROOT, "tests", "cpp", "build", "ref_compat")
+
+
+def test_reference_source_compiles_against_our_headers():
+    """The reference's unmodified reference.cpp builds against include/ and
+    links with the drop-in libraries (build() does it where /root/reference
+    exists)."""
+    if not os.path.exists("/root/reference/proj/src/stereo/reference.cpp"):
+        pytest.skip("/root/reference absent (GPU box): the prebuilt binary is used there")
+    from paper_2007_12623_b200.build import build
+    build(verbose=False)
+    assert os.path.exists(REF_COMPAT)
+
+
+@pytest.mark.gpu
+def test_reference_source_vs_gpu_dropins():
+    if not os.path.exists(REF_COMPAT):
+        pytest.skip("ref_compat not built (needs /root/reference at build time)")
+    r = subprocess.run([REF_COMPAT], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "ref_compat OK" in r.stdout
