@@ -94,20 +94,18 @@ __device__ __forceinline__ uint32_t term_o(const RowWords& w) {
 
 // One row step of the running sums for candidate I (center v-1 -> v):
 //   X' = Y - He(v-6) + Ho(v+5),  Y' = X + He(v+5) - Ho(v-6)
-// X' goes to T and Y' back into Y: with the caller alternating the X and T
-// arrays between consecutive rows no register moves are needed.
 template <int I>
-__device__ __forceinline__ void step_i(const RowWords& wo, const RowWords& wn,
-                                       const int (&X)[kDB], int (&Y)[kDB], int (&T)[kDB]) {
+__device__ __forceinline__ void step_i(const RowWords& wo, const RowWords& wn, int (&X)[kDB],
+                                       int (&Y)[kDB]) {
+  const int xn = Y[I] - (int)term_e<I>(wo) + (int)term_o<I>(wn);
   const int yn = X[I] + (int)term_e<I>(wn) - (int)term_o<I>(wo);
-  T[I] = Y[I] - (int)term_e<I>(wo) + (int)term_o<I>(wn);
+  X[I] = xn;
   Y[I] = yn;
 }
 template <int... Is>
-__device__ __forceinline__ void step_all(const RowWords& wo, const RowWords& wn,
-                                         const int (&X)[kDB], int (&Y)[kDB], int (&T)[kDB],
-                                         std::integer_sequence<int, Is...>) {
-  (step_i<Is>(wo, wn, X, Y, T), ...);
+__device__ __forceinline__ void step_all(const RowWords& wo, const RowWords& wn, int (&X)[kDB],
+                                         int (&Y)[kDB], std::integer_sequence<int, Is...>) {
+  (step_i<Is>(wo, wn, X, Y), ...);
 }
 
 // Warm-up accumulation of one row: dy even -> X += He, Y += Ho; odd swaps.
@@ -170,7 +168,6 @@ __host__ __device__ inline RingGeom ring_geom(int NB) {
   return r;
 }
 
-template <int NBT>  // sweep warps per block (0: blockDim.y - 1 at run time)
 __global__ void __launch_bounds__(512) k_wta11(
     const uint4* __restrict__ ltap, const uint32_t* __restrict__ rcopy,
     const int2* __restrict__ lstat, const int2* __restrict__ rstat, wscore_t* __restrict__ win,
@@ -181,7 +178,7 @@ __global__ void __launch_bounds__(512) k_wta11(
     long map_stride, long win_stride) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // warps 0 .. NB-1 sweep (one block of kDB candidates each); warp NB merges
-  const int lane = threadIdx.x, j = threadIdx.y, NB = NBT > 0 ? NBT : (int)blockDim.y - 1;
+  const int lane = threadIdx.x, j = threadIdx.y, NB = blockDim.y - 1;
   const bool merger = j == NB;
   const int NCB = NB * kDB;  // staged candidates per pixel
   const RingGeom rg = ring_geom(NB);
@@ -387,9 +384,9 @@ __global__ void __launch_bounds__(512) k_wta11(
     return;
   }
 
-  int X[kDB], Y[kDB], T[kDB];
+  int X[kDB], Y[kDB];
 #pragma unroll
-  for (int i = 0; i < kDB; ++i) X[i] = Y[i] = T[i] = 0;
+  for (int i = 0; i < kDB; ++i) X[i] = Y[i] = 0;
 
 #pragma unroll 1
   for (int dy = -h; dy <= h; ++dy) {
@@ -401,8 +398,15 @@ __global__ void __launch_bounds__(512) k_wta11(
     }
   }
 
-  // score row v from its cross sums S and stage the partials for the merge warp
-  auto finish = [&](int v, const int (&S)[kDB]) {
+  for (int v = v_begin; v < v_end; ++v) {
+    if (v > v_begin) {
+      wait_row(v + 5);
+      if (active) {
+        const RowWords wo = words(v - 6);
+        const RowWords wn = words(v + 5);
+        step_all(wo, wn, X, Y, std::make_integer_sequence<int, kDB>{});
+      }
+    }
     const int k = (v - v_begin) / kRB, slot = (v - v_begin) - k * kRB, b = k & 1;
     // staging buffer b was merged (chunk k - 2) before it is rewritten
     if (slot == 0 && k >= 2) bar_sync(3 + b, nthr);
@@ -415,10 +419,10 @@ __global__ void __launch_bounds__(512) k_wta11(
                          (int)((rs_base + (long)v * g.SP) & 1);
       int ai = -1;
       if (full)
-        score_all<false>(S, rrow, sl, amask, gs, best, second, ai,
+        score_all<false>(X, rrow, sl, amask, gs, best, second, ai,
                          std::make_integer_sequence<int, kDB>{});
       else
-        score_all<true>(S, rrow, sl, amask, gs, best, second, ai,
+        score_all<true>(X, rrow, sl, amask, gs, best, second, ai,
                         std::make_integer_sequence<int, kDB>{});
       arg = ai >= 0 ? c0 + ai : kNoArg;
     }
@@ -427,28 +431,6 @@ __global__ void __launch_bounds__(512) k_wta11(
     s_sec0[so] = second;
     s_arg0[so] = arg;
     if (slot == kRB - 1 || v == v_end - 1) bar_arrive(1 + b, nthr);  // chunk k staged
-  };
-  // advance the window to center v: new X into Tn, new Y into Y
-  auto advance = [&](int v, const int (&Xo)[kDB], int (&Tn)[kDB]) {
-    wait_row(v + 5);
-    if (active) {
-      const RowWords wo = words(v - 6);
-      const RowWords wn = words(v + 5);
-      step_all(wo, wn, Xo, Y, Tn, std::make_integer_sequence<int, kDB>{});
-    }
-  };
-  finish(v_begin, X);
-  int v = v_begin + 1;
-  // two rows per trip, the X and T arrays trading places (no register moves)
-  for (; v + 1 < v_end; v += 2) {
-    advance(v, X, T);
-    finish(v, T);
-    advance(v + 1, T, X);
-    finish(v + 1, X);
-  }
-  if (v < v_end) {
-    advance(v, X, T);
-    finish(v, T);
   }
 }
 
@@ -468,21 +450,15 @@ void launch_wta11(const uint4* ltap, const uint32_t* rcopy, const int2* lstat, c
                       2 * ((size_t)kRB * NB * 32 * 12 + (size_t)kRB * NB * kDB * 32 * 4);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    cudaFuncSetAttribute(k_wta11<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_wta11<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_wta11<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_wta11, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = smem;
   }
   const float mz = (float)min_zncc;
   const float tol = 4e-6f * fmaxf(1.f, fabsf(mz));
-#define SS_WTA_ARGS                                                                           \
-  ltap, rcopy, lstat, rstat, win, wbase, base_map, disp, valid, flag_list, flag_count, g, mz, tol, \
-      do_argmax, tap_stride, copy_stride, lstat_stride, rstat_stride, map_stride, win_stride
-  // D = 64 and D = 128 (the benchmark ranges) get compile-time ring geometry
-  if (NB == 4) k_wta11<4><<<grid, block, smem, s>>>(SS_WTA_ARGS);
-  else if (NB == 8) k_wta11<8><<<grid, block, smem, s>>>(SS_WTA_ARGS);
-  else k_wta11<0><<<grid, block, smem, s>>>(SS_WTA_ARGS);
-#undef SS_WTA_ARGS
+  k_wta11<<<grid, block, smem, s>>>(ltap, rcopy, lstat, rstat, win, wbase, base_map, disp, valid,
+                                    flag_list, flag_count, g, mz, tol, do_argmax, tap_stride,
+                                    copy_stride, lstat_stride, rstat_stride, map_stride,
+                                    win_stride);
 }
 
 // ---- exact FP64 path: warp per pixel, lanes over d ----
