@@ -609,6 +609,19 @@ def run_ours(args):
             pts = int(np.sum(npts)) if fl & ss.SS_OUT_TRIM else len(npts) * N
             return len(npts) * (N * per_px + 4) + pts * per_pt
 
+        # one set of pinned host outputs serves both formats (the compact one
+        # adds only the octahedral normals): ~4.8 GB per rank at C4, not 2x
+        pool = {}
+
+        def host_outputs(n, fl):
+            want = ss.StereoContext.alloc_outputs(n, H, W, fl, alloc=lambda s_, dt: (s_, dt))
+            out = {}
+            for k, (shape, dt) in want.items():
+                if k not in pool or pool[k].shape != shape:
+                    pool[k] = ss.pinned_empty(shape, dt)
+                out[k] = pool[k]
+            return out
+
         def measure_e2e(fl):
             consumed = [0] * S
             if strong:
@@ -616,7 +629,7 @@ def run_ours(args):
                 # (its point count read) before the ring slot is reused
                 ho = [ss.StereoContext.alloc_outputs(2 * B, H, W, fl,
                                                      alloc=lambda s_, dt: ss.pinned_empty(s_, dt))
-                      for _ in range(S)]
+                      for _ in range(S)]  # a ring of 2 launches per thread: small
                 nbytes = [0] * S
 
                 def part(k, steps):
@@ -631,8 +644,7 @@ def run_ours(args):
                             nbytes[k] += d2h_bytes(fl, o["n_points"])
                 outs = None
             else:
-                outs = ss.StereoContext.alloc_outputs(F, H, W, fl,
-                                                      alloc=lambda s_, dt: ss.pinned_empty(s_, dt))
+                outs = host_outputs(F, fl)
                 cuts = [F * i // S for i in range(S + 1)]
 
                 def part(k, steps):
@@ -669,6 +681,8 @@ def run_ours(args):
             return val, db, ext, outs
 
         e2e_value, d2h, e2e_extra, ho_c = measure_e2e(compact)
+        if parity is not None and not strong:  # checked before the buffers are reused
+            bad_c = check_frames(lambda i: {k: v[i] for k, v in ho_c.items()}, keys, dig)
         h2d = 2 * F * N * 3
         e2e_extra["format"] = ("compact (SS_OUT_NORMALS_OCT | SS_OUT_TRIM): disparity f32, valid, "
                                "index, n_points, points f32 + colours for n_points entries, "
@@ -679,11 +693,11 @@ def run_ours(args):
                                     "format": "reference outputs at full per-frame capacity: "
                                               "normals f32x3, untrimmed cloud arrays"}
         if parity is not None and not strong:
-            bad = check_frames(lambda i: {k: v[i] for k, v in ho_c.items()}, keys, dig)
-            bad += check_frames(lambda i: {k: v[i] for k, v in ho_f.items()}, keys, dig)
+            bad = bad_c + check_frames(lambda i: {k: v[i] for k, v in ho_f.items()}, keys, dig)
             parity["e2e_frames_checked"] = 2 * len(keys)
             parity["e2e_frames_mismatched"] = bad
         del ho_c, ho_f
+        pool.clear()
 
     if world > 1:
         dist.barrier()
