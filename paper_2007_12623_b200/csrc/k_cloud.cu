@@ -573,9 +573,10 @@ __global__ void __launch_bounds__(kNTX * kNTY, 3)
     sym3_smallest<float>(a, ev, e);
     const float scale = fmaxf(1.f, ev[2]);
     // the closed-form FP32 eigenvalues of a near-degenerate neighbourhood
-    // are only sqrt(eps) accurate: above 1e-2 l2 the reference's 1e-9 test
+    // are only ~sqrt(eps) accurate (|l1 error| <= 2e-4 max(1, l2) measured
+    // over rank-1 neighbourhoods): above 2e-3 the reference's 1e-9 test
     // certainly passes; below, the reference's own solver decides (refit)
-    if (ev[1] > 1e-2f * scale) {
+    if (ev[1] > 2e-3f * scale) {
       // One FP64 inverse-iteration step, x = adj(A - mu I) e: the FP32
       // eigenvector's error shrinks by |lambda0 - mu| / |lambda1 - mu|, so
       // small eigen gaps (1e-3 of lambda2) still give ~1e-7 rad normals.
