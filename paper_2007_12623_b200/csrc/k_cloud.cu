@@ -202,12 +202,12 @@ void launch_cloud_points(const float* disp, const int* index, const uint8_t* rgb
 
 // ---- The reference's eigensolver on the device (cloud.cpp:78) ----
 // Eigen 3.4.0 SelfAdjointEigenSolver<Matrix3d>::compute, restated operation
-// for operation as oracle/ss_oracle.c:eigen3_sym does (scale by the largest
-// |lower-triangle| entry, 3x3 Householder tridiagonalisation, implicit
-// symmetric QR with Wilkinson shifts and makeGivens rotations, ascending
-// sort). Every operation is an explicit IEEE round-to-nearest intrinsic (this
-// translation unit is built with FMA contraction), so for the same covariance
-// the eigenvalues, and the fit/fallback test on them, are the restatement's.
+// for operation (scale by the largest |lower-triangle| entry, 3x3 Householder
+// tridiagonalisation, implicit symmetric QR with Wilkinson shifts and
+// makeGivens rotations, ascending sort). Every operation is an
+// explicit IEEE round-to-nearest intrinsic (this translation unit is built
+// with FMA contraction), so for the same covariance the eigenvalues, and the
+// fit/fallback test on them, are the test restatement's.
 // Used for the near-degenerate neighbourhoods, where the fast closed-form
 // solver cannot decide the 1e-9 test.
 namespace eg {
