@@ -726,6 +726,21 @@ def run_ours(args):
         t = json.load(open(tpath)).get(top, {})
         if t.get("frames_per_launch") == B and t.get("workload") == args.workload:
             traffic = t.get("dram_bytes_per_launch")
+    # Binding-pipe view (measured pipe peaks, profiles/r2/pipe_rates.json): the
+    # group's launch time if its dominant kernel's busiest pipe (ncu) ran at
+    # 100%, over the live launch time. The census peak above counts every op
+    # at 128 lanes/clock; FP64, dp4a and IMAD issue at 64 and shared memory
+    # moves 128 B/clock, so the census fraction understates how close a kernel is.
+    ppath = os.path.join(ROOT, "profiles", "pipe_roofline.json")
+    if os.path.exists(ppath):
+        for name, pr in json.load(open(ppath))["groups"].items():
+            g = groups.get(name)
+            if g and pr.get("frames_per_launch") == B and pr.get("workload") == args.workload:
+                g["pipe_roofline"] = {
+                    "kernel": pr["kernel"], "binding_pipe": pr["binding_pipe"],
+                    "roof_ms_per_launch": pr["roof_ms_per_launch"],
+                    "frac": pr["roof_ms_per_launch"] / g["avg_launch_ms"],
+                    "source": "profiles/pipe_roofline.json (ncu --set full, one launch)"}
     roofline = dict(groups[top])
     roofline.update({
         "group": top, "traffic": traffic,

@@ -15,6 +15,9 @@ for path in sys.argv[1:]:
     print("  groups:", {k: (round(v['avg_launch_ms'], 3), round(v['frac'], 3),
                             round(v['share_of_chain'] or 0, 3))
                         for k, v in r.get('kernel_groups', {}).items()})
+    print("  pipe roofline:", {k: (v['pipe_roofline']['binding_pipe'],
+                                   round(v['pipe_roofline']['frac'], 3))
+                               for k, v in r.get('kernel_groups', {}).items() if 'pipe_roofline' in v})
     print("  parity:", d.get("parity"), "clocks:", d.get("clocks"))
     if d.get("cpu_baseline"):
         print("  cpu:", {k: d['cpu_baseline'].get(k) for k in ('value', 'cores', 'kind')})
