@@ -415,7 +415,7 @@ def roofline_report(args, stages, frames_timed, n_sm, sm_max, hbm_peak, iters=10
         "cleanup_disc": ("k_row_count/k_disc_select/k_disc_sum: I_disc x (82 + 3 x 1256)",
                          I_DISC[args.workload] * (82 + 3 * 1256)),
         "cleanup_radial": ("k_fill_radial_list: 144N", 144.0 * N),
-        "cleanup_outliers": ("k_edge_bits + k_remove_outliers: 72N", 72.0 * N),
+        "cleanup_outliers": ("k_edge_words + k_outlier_words: 72N", 72.0 * N),
         "cloud_normals": ("k_cloud_normals: 7x7 moments + 3x3 eigen, 600N", 600.0 * N),
     }
     hbm = {"refine_scan": ("k_scan_b / k_scan_bt: row prefix scans, 29 B/px per iteration",

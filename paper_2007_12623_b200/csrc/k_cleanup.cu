@@ -29,162 +29,241 @@ namespace ssb {
 __constant__ int c_dirU[8] = {1, -1, 0, 0, 1, 1, -1, -1};
 __constant__ int c_dirV[8] = {0, 0, 1, -1, 1, -1, 1, -1};
 
-// Outlier rays via smooth-edge bitmaps. A ray from a valid pixel p in
-// direction e passes iff its far end is inside the image and every step q ->
-// q + e (q = p, p + e, ...) joins two valid pixels with |d(q+e) - d(q)| <= thr
-// (the reference's double comparison). That edge predicate is symmetric, so
-// four bitmaps hold it for all eight directions — E_h (q -> q+(1,0)) by rows,
-// E_v ((0,1)) by columns, E_d1 ((1,1)) and E_d2 ((1,-1)) by diagonals — laid
-// out so that every ray is a run of consecutive bits, and the ray test is
-// "r consecutive ones" on one or two words.
+// Outlier rays as bit-parallel runs over smooth-edge bitmaps. A ray from a
+// valid pixel p in direction e passes iff its far end is inside the image and
+// every step q -> q + e (q = p, p + e, ...) joins two valid pixels with
+// |d(q+e) - d(q)| <= thr (the reference's double comparison). That edge
+// predicate is symmetric, so four edge maps hold it for all eight directions:
+// E_h (q -> q+(1,0)), E_v ((0,1)), E_d1 ((1,1)) and E_d2 ((1,-1)), each
+// row-major with bit u of word u/32 for pixel (u, v), plus the validity map.
+// k_edge_words builds them (a warp walks a strip of rows of one 32-pixel word
+// column: one coalesced load per pixel, neighbours by shuffles, one ballot per
+// map and row); k_outlier_words decides 32 pixels per thread: a ray test is
+// an AND over its r edges of one shifted word per step, horizontal runs by
+// shift doubling, and a word stops as soon as all its valid pixels passed.
 namespace {
-struct EdgeMaps {
-  uint32_t *bh, *bv, *bd1, *bd2;
-  int lw, lh;  // words per row line (E_h) / per column or diagonal line
-};
-__host__ __device__ inline EdgeMaps edge_maps(uint32_t* base, int W, int H) {
-  EdgeMaps m;
-  m.lw = (W + 31) / 32 + 1;  // +1: a two-word read never leaves the line
-  m.lh = (H + 31) / 32 + 1;
-  m.bh = base;
-  m.bv = m.bh + (long)H * m.lw;
-  m.bd1 = m.bv + (long)W * m.lh;
-  m.bd2 = m.bd1 + (long)(W + H - 1) * m.lh;
-  return m;
-}
-// bits [p, p + r) of a line all set
-__device__ __forceinline__ bool run_ok(const uint32_t* __restrict__ line, int p, int r) {
-  while (r > 0) {
-    const int wi = p >> 5, b = p & 31;
-    const uint32_t x = __funnelshift_r(__ldg(line + wi), __ldg(line + wi + 1), b);
-    const int n = r < 32 ? r : 32;
-    const uint32_t m = n == 32 ? 0xFFFFFFFFu : (1u << n) - 1u;
-    if ((x & m) != m) return false;
-    p += n;
-    r -= n;
+constexpr int kEdgeMaps = 5;  // V, E_h, E_v, E_d1, E_d2
+constexpr int kEdgeStrip = 16;  // rows per warp in k_edge_words
+struct EdgeWords {
+  const uint32_t* m[kEdgeMaps];
+  int ww;  // words per row
+  __device__ __forceinline__ uint32_t word(int map, int v, int q) const {
+    return (q >= 0 && q < ww) ? __ldg(m[map] + (long)v * ww + q) : 0u;
   }
-  return true;
-}
+  // the 32 bits of row v of `map` starting at bit position `pos` (zero outside the row)
+  __device__ __forceinline__ uint32_t bits(int map, int v, int pos) const {
+    const int q = pos >> 5;  // floor (arithmetic shift)
+    return __funnelshift_r(word(map, v, q), word(map, v, q + 1), pos & 31);
+  }
+};
+__host__ __device__ inline int edge_ww(int W) { return (W + 31) / 32; }
 }  // namespace
 
-__global__ void __launch_bounds__(256)
-    k_edge_bits(const float* __restrict__ din, const uint8_t* __restrict__ vin,
-                uint32_t* __restrict__ emap, int W, int H, double thr, long stride, long fw) {
-  __shared__ double td[34][33];    // rows v0-1 .. v0+32, columns u0 .. u0+32 (widened once)
-  __shared__ uint32_t tv[34][33];  // validity (words: no byte bank conflicts)
-  __shared__ uint32_t eb[32][34];  // per pixel: bit0 E_h, bit1 E_v, bit2 E_d1, bit3 E_d2
+__global__ void __launch_bounds__(128)
+    k_edge_words(const float* __restrict__ din, const uint8_t* __restrict__ vin,
+                 uint32_t* __restrict__ emap, int W, int H, double thr, long stride, long fw,
+                 float* __restrict__ dcopy, float* __restrict__ dcopy2) {
   const long f = blockIdx.z;
-  const int u0 = blockIdx.x * 32, v0 = blockIdx.y * 32;
-  const int lane = threadIdx.x, wy = threadIdx.y;
-  // cells (r, c): c = lane for r = wy + 8k (k < 5), plus column 32 for the
-  // threads 0..33 — every load issued before the first store
-  constexpr int kCells = 6;
-  float xs[kCells];
-  uint8_t ms[kCells];
-#pragma unroll
-  for (int k = 0; k < kCells; ++k) {
-    const int tid = wy * 32 + lane;
-    const int r = k < 5 ? wy + 8 * k : tid, c = k < 5 ? lane : 32;
-    const int v = v0 - 1 + r, u = u0 + c;
-    xs[k] = 0.f;
-    ms[k] = 0;
-    if (r < 34 && v >= 0 && v < H && u < W) {
-      const long i = f * stride + (long)v * W + u;
-      ms[k] = vin[i];
-      xs[k] = din[i];
+  const int lane = threadIdx.x;
+  const int w = blockIdx.x * 4 + threadIdx.y, ww = edge_ww(W);
+  if (w >= ww) return;
+  const int v0 = blockIdx.y * kEdgeStrip, v1 = min(H, v0 + kEdgeStrip);
+  const int u = w * 32 + lane;
+  const float* dr = din + f * stride;
+  const uint8_t* vr = vin + f * stride;
+  // pixel (u, v) and its right neighbour (u + 1, v): lane 31 loads the latter
+  auto load = [&](int v, double& d, bool& ok, double& dn, bool& okn) {
+    float x = 0.f, xn = 0.f;
+    ok = false;
+    okn = false;
+    if (v >= 0 && v < H) {
+      const long i = (long)v * W + u;
+      if (u < W) {
+        x = dr[i];
+        ok = vr[i] != 0;
+        if (v >= v0 && v < v1) {
+          if (dcopy) dcopy[f * stride + i] = x;
+          if (dcopy2) dcopy2[f * stride + i] = x;
+        }
+      }
+      if (lane == 31 && u + 1 < W) {
+        xn = dr[i + 1];
+        okn = vr[i + 1] != 0;
+      }
     }
-  }
-#pragma unroll
-  for (int k = 0; k < kCells; ++k) {
-    const int tid = wy * 32 + lane;
-    const int r = k < 5 ? wy + 8 * k : tid, c = k < 5 ? lane : 32;
-    if (r < 34) {
-      td[r][c] = (double)xs[k];
-      tv[r][c] = ms[k] ? 1u : 0u;
+    const float sx = __shfl_down_sync(0xFFFFFFFFu, x, 1);
+    const bool sok = __shfl_down_sync(0xFFFFFFFFu, ok ? 1 : 0, 1) != 0;
+    if (lane != 31) {
+      xn = sx;
+      okn = sok;
     }
-  }
-  __syncthreads();
-  // smooth edge from cell (r, c) to (r2, c2): both valid, |d2 - d| <= thr in
-  // double (cleanup.cpp:29-30; NaN compares false, as there)
-  auto E = [&](int r, int c, int r2, int c2) -> unsigned {
-    return (tv[r][c] & tv[r2][c2]) && !(fabs(td[r2][c2] - td[r][c]) > thr)
-               ? 1u
-               : 0u;
+    d = (double)x;
+    dn = (double)xn;
   };
-  for (int l = wy; l < 32; l += 8) {
-    const int r = l + 1, c = lane;
-    eb[l][lane] = E(r, c, r, c + 1) | (E(r, c, r + 1, c) << 1) | (E(r, c, r + 1, c + 1) << 2) |
-                  (E(r, c, r - 1, c + 1) << 3);
-  }
-  __syncthreads();
-  const EdgeMaps M = edge_maps(emap + f * fw, W, H);
-  for (int l = wy; l < 32; l += 8) {  // E_h: lanes = columns, one word per row
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, eb[l][lane] & 1u);
-    if (lane == 0 && v0 + l < H) M.bh[(long)(v0 + l) * M.lw + (u0 >> 5)] = m;
-  }
-  for (int c = wy; c < 32; c += 8) {  // E_v: lanes = rows, one word per column
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, (eb[lane][c] >> 1) & 1u);
-    if (lane == 0 && u0 + c < W) M.bv[(long)(u0 + c) * M.lh + (v0 >> 5)] = m;
-  }
-  // diagonals: lanes = rows; a tile holds a partial word of 63 diagonals of
-  // each kind, OR-ed into the (zeroed) maps.
-  for (int dd = wy; dd < 63; dd += 8) {
-    {  // E_d1 (1,1): diagonal u - v = const, column c = lane + delta
-      const int delta = dd - 31, c = lane + delta;
-      const bool e = c >= 0 && c < 32 && ((eb[lane][c] >> 2) & 1u);
-      const unsigned m = __ballot_sync(0xFFFFFFFFu, e);
-      if (lane == 0 && m) atomicOr(M.bd1 + ((long)(u0 - v0 + delta) + H - 1) * M.lh + (v0 >> 5), m);
+  // smooth edge between values a (valid oa) and b (valid ob): cleanup.cpp:25-31
+  auto edge = [&](bool oa, double a, bool ob, double b) {
+    return oa && ob && !(fabs(b - a) > thr);
+  };
+  double dp, dpn, dc, dcn, dn, dnn;
+  bool op, opn, oc, ocn, on, onn;
+  load(v0 - 1, dp, op, dpn, opn);
+  load(v0, dc, oc, dcn, ocn);
+  uint32_t* out = emap + f * fw;
+  const long plane = (long)H * ww;
+#pragma unroll 1
+  for (int v = v0; v < v1; ++v) {
+    load(v + 1, dn, on, dnn, onn);
+    const unsigned bv = __ballot_sync(0xFFFFFFFFu, oc);
+    const unsigned bh = __ballot_sync(0xFFFFFFFFu, edge(oc, dc, ocn, dcn));
+    const unsigned bvv = __ballot_sync(0xFFFFFFFFu, edge(oc, dc, on, dn));
+    const unsigned bd1 = __ballot_sync(0xFFFFFFFFu, edge(oc, dc, onn, dnn));
+    const unsigned bd2 = __ballot_sync(0xFFFFFFFFu, edge(oc, dc, opn, dpn));
+    if (lane < kEdgeMaps) {
+      const unsigned x = lane == 0 ? bv : lane == 1 ? bh : lane == 2 ? bvv : lane == 3 ? bd1 : bd2;
+      out[lane * plane + (long)v * ww + w] = x;
     }
-    {  // E_d2 (1,-1): diagonal u + v = const, column c = dd - lane
-      const int c = dd - lane;
-      const bool e = c >= 0 && c < 32 && ((eb[lane][c] >> 3) & 1u);
-      const unsigned m = __ballot_sync(0xFFFFFFFFu, e);
-      if (lane == 0 && m) atomicOr(M.bd2 + ((long)u0 + v0 + dd) * M.lh + (v0 >> 5), m);
-    }
+    dpn = dcn;
+    opn = ocn;
+    dc = dn;
+    oc = on;
+    dcn = dnn;
+    ocn = onn;
   }
+}
+
+// keep bits of the 32 pixels of word w of row v, for rays of r steps
+// (r > 0). The early exit only skips rays whose pixels already passed.
+__device__ __forceinline__ uint32_t outlier_keep(const EdgeWords& E, int W, int H, int v, int w,
+                                                 int r) {
+  const uint32_t valid = E.word(0, v, w);
+  if (!valid) return 0u;
+  uint32_t keep = 0u;
+  const int u0 = w * 32;
+  // horizontal: runs of r set bits of E_h, starting at u (1,0) or ending at u - 1 (-1,0)
+  if (r <= 32) {
+    // 64-bit windows over columns u0 - 32 .. u0 + 31 (lo) and u0 .. u0 + 63 (hi)
+    const uint64_t a = ((uint64_t)E.word(1, v, w + 1) << 32) | E.word(1, v, w);
+    const uint64_t b = ((uint64_t)E.word(1, v, w) << 32) | E.word(1, v, w - 1);
+    // run-of-r masks by doubling: bit j of R set iff bits j .. j + r - 1 all set
+    auto runs = [r](uint64_t x) {
+      uint64_t acc = ~0ull, p = x;
+      int off = 0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {  // p = runs of 2^k
+        if ((r >> k) & 1) {
+          acc &= p >> off;
+          off += 1 << k;
+        }
+        if ((2 << k) > r) break;
+        p &= p >> (1 << k);
+      }
+      return acc;
+    };
+    keep |= (uint32_t)runs(a);                 // bits u .. u + r - 1
+    keep |= (uint32_t)(runs(b) >> (32 - r));   // bits u - r .. u - 1
+  } else {
+    uint32_t p = ~0u, m = ~0u;
+    for (int k = 0; k < r && (p | m); ++k) {
+      p &= E.bits(1, v, u0 + k);
+      m &= E.bits(1, v, u0 - 1 - k);
+    }
+    keep |= p | m;
+  }
+  keep &= valid;
+  if (keep == valid) return keep;
+  // vertical and diagonal rays: one word per step; the far end must be in the image
+  if (v + r <= H - 1) {
+    uint32_t a = ~0u, d1 = ~0u, d2 = ~0u;
+#pragma unroll 4
+    for (int k = 0; k < r; ++k) {
+      a &= E.word(2, v + k, w);                   // (0, 1): E_v rows v .. v + r - 1
+      d1 &= E.bits(3, v + k, u0 + k);             // (1, 1): E_d1 row v + k, bit u + k
+      d2 &= E.bits(4, v + k + 1, u0 - 1 - k);     // (-1, 1): E_d2 row v + k + 1, bit u - k - 1
+      if (!((a | d1 | d2) & valid & ~keep)) break;
+    }
+    keep |= (a | d1 | d2) & valid;
+    if (keep == valid) return keep;
+  }
+  if (v - r >= 0) {
+    uint32_t a = ~0u, d1 = ~0u, d2 = ~0u;
+#pragma unroll 4
+    for (int k = 0; k < r; ++k) {
+      a &= E.word(2, v - 1 - k, w);               // (0, -1): E_v rows v - 1 .. v - r
+      d1 &= E.bits(3, v - 1 - k, u0 - 1 - k);     // (-1, -1): E_d1 row v - k - 1, bit u - k - 1
+      d2 &= E.bits(4, v - k, u0 + k);             // (1, -1): E_d2 row v - k, bit u + k
+      if (!((a | d1 | d2) & valid & ~keep)) break;
+    }
+    keep |= (a | d1 | d2) & valid;
+  }
+  (void)W;
+  return keep;
 }
 
 // dout2/vout2 (optional): a second copy of the result (the radial fill's
-// output buffer, so that fill only writes the pixels it fills); list/count
-// (optional): per-frame list of the invalid output pixels (warp-aggregated
-// appends: ~5% of the pixels, one counter per frame).
-// In place allowed (vout == vin, dout == NULL: each thread reads only its own
-// pixel of din / vin, before writing it), hence no __restrict__ on those.
-__global__ void k_remove_outliers(const float* din, const uint8_t* vin, float* dout,
-                                  uint8_t* vout, int W, int H, int r,
-                                  const uint32_t* __restrict__ emap, long stride, long fw,
-                                  float* __restrict__ dout2, uint8_t* __restrict__ vout2,
-                                  int* __restrict__ list, unsigned* __restrict__ count) {
+// output buffer, so that fill only writes the pixels it fills; the disparity
+// copies are written by k_edge_words); list/count (optional): per-frame list
+// of the invalid output pixels (one atomic per warp, ~5% of the pixels).
+// vout may alias the input validity (the maps hold it).
+__global__ void __launch_bounds__(128)
+    k_outlier_words(const uint32_t* __restrict__ emap, uint8_t* vout, uint8_t* __restrict__ vout2,
+                    int W, int H, int r, long stride, long fw, int* __restrict__ list,
+                    unsigned* __restrict__ count) {
   const long f = blockIdx.z;
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ww = edge_ww(W);
+  const int w = blockIdx.x * 32 + threadIdx.x;
   const int v = blockIdx.y * blockDim.y + threadIdx.y;
-  if (u >= W || v >= H) return;
-  const long i = f * stride + (long)v * W + u;
-  const float d0 = din[i];
-  if (dout) dout[i] = d0;
-  if (dout2) dout2[i] = d0;
-  bool keep = false;
-  if (vin[i]) {
-    const EdgeMaps M = edge_maps(const_cast<uint32_t*>(emap) + f * fw, W, H);
-    keep = r <= 0;  // no steps: every ray is smooth (cleanup.cpp:21-33)
-    const uint32_t* row = M.bh + (long)v * M.lw;
-    const uint32_t* col = M.bv + (long)u * M.lh;
-    const uint32_t* d1 = M.bd1 + ((long)u - v + H - 1) * M.lh;
-    const uint32_t* d2 = M.bd2 + ((long)u + v) * M.lh;
-    if (!keep && u + r < W) keep = run_ok(row, u, r);                      // (1, 0)
-    if (!keep && u - r >= 0) keep = run_ok(row, u - r, r);                 // (-1, 0)
-    if (!keep && v + r < H) keep = run_ok(col, v, r);                      // (0, 1)
-    if (!keep && v - r >= 0) keep = run_ok(col, v - r, r);                 // (0, -1)
-    if (!keep && u + r < W && v + r < H) keep = run_ok(d1, v, r);          // (1, 1)
-    if (!keep && u + r < W && v - r >= 0) keep = run_ok(d2, v - r + 1, r); // (1, -1)
-    if (!keep && u - r >= 0 && v + r < H) keep = run_ok(d2, v + 1, r);     // (-1, 1)
-    if (!keep && u - r >= 0 && v - r >= 0) keep = run_ok(d1, v - r, r);   // (-1, -1)
+  const bool act = w < ww && v < H;
+  EdgeWords E;
+  const long plane = (long)H * ww;
+#pragma unroll
+  for (int k = 0; k < kEdgeMaps; ++k) E.m[k] = emap + f * fw + k * plane;
+  E.ww = ww;
+  uint32_t keep = 0u, inimg = 0u;
+  if (act) {
+    keep = r > 0 ? outlier_keep(E, W, H, v, w, r) : E.word(0, v, w);  // r <= 0: no steps
+    const int n = min(32, W - w * 32);
+    inimg = n == 32 ? ~0u : (1u << n) - 1u;
+    const long i0 = f * stride + (long)v * W + w * 32;
+    if (n == 32 && ((i0 & 15) == 0)) {
+      uint4 q[2];
+      uint32_t* qw = reinterpret_cast<uint32_t*>(q);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)  // 4 bits -> 4 bytes of 0/1
+        qw[k] = (((keep >> (4 * k)) & 0xFu) * 0x00204081u) & 0x01010101u;
+      reinterpret_cast<uint4*>(vout + i0)[0] = q[0];
+      reinterpret_cast<uint4*>(vout + i0)[1] = q[1];
+      if (vout2) {
+        reinterpret_cast<uint4*>(vout2 + i0)[0] = q[0];
+        reinterpret_cast<uint4*>(vout2 + i0)[1] = q[1];
+      }
+    } else {
+      for (int k = 0; k < n; ++k) {
+        const uint8_t b = (keep >> k) & 1u;
+        vout[i0 + k] = b;
+        if (vout2) vout2[i0 + k] = b;
+      }
+    }
   }
-  vout[i] = keep ? 1 : 0;
-  if (vout2) vout2[i] = keep ? 1 : 0;
-  if (list) warp_append(list + f * stride, count + f, !keep, v * W + u);
+  if (list) {
+    // invalid output pixels, raster order within a thread's word
+    const uint32_t bad = inimg & ~keep;
+    const int c = __popc(bad);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if ((int)threadIdx.x >= o) incl += t;
+    }
+    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (total) {
+      unsigned base = 0;
+      if (threadIdx.x == 31) base = atomicAdd(count + f, (unsigned)total);
+      base = __shfl_sync(0xFFFFFFFFu, base, 31) + (unsigned)(incl - c);
+      int* lf = list + f * stride;
+      for (uint32_t m = bad; m; m &= m - 1) lf[base++] = v * W + w * 32 + (__ffs(m) - 1);
+    }
+  }
 }
-
 // Radial fill of one invalid pixel (cleanup.cpp:54-68): writes dout/vout
 // only when the pixel is filled.
 __device__ __forceinline__ void radial_fill_pixel(const float* __restrict__ din,
@@ -380,15 +459,11 @@ void launch_remove_outliers(const float* din, const uint8_t* vin, float* dout, u
                             unsigned* count) {
   if (W <= 0 || H <= 0 || frames <= 0) return;
   const long fw = edge_map_words(W, H);
-  if (radius > 0) {
-    cudaMemsetAsync(emap, 0, sizeof(uint32_t) * fw * frames, s);
-    k_edge_bits<<<dim3((W + 31) / 32, (H + 31) / 32, frames), dim3(32, 8), 0, s>>>(
-        din, vin, emap, W, H, thr, stride, fw);
-  }
-  dim3 b(32, 8);
-  k_remove_outliers<<<map_grid(W, H, frames, b), b, 0, s>>>(din, vin, dout, vout, W, H, radius,
-                                                            emap, stride, fw, dout2, vout2, list,
-                                                            count);
+  const int ww = edge_ww(W);
+  k_edge_words<<<dim3((ww + 3) / 4, (H + kEdgeStrip - 1) / kEdgeStrip, frames), dim3(32, 4), 0,
+                 s>>>(din, vin, emap, W, H, thr, stride, fw, dout, dout2);
+  k_outlier_words<<<dim3((ww + 31) / 32, (H + 3) / 4, frames), dim3(32, 4), 0, s>>>(
+      emap, vout, vout2, W, H, radius, stride, fw, list, count);
 }
 
 void launch_fill_radial_list(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,

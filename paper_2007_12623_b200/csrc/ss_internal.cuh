@@ -153,11 +153,9 @@ void launch_fuse(double* pos, double* nrm, double* col, double* w, double* cw, c
                  double trunc, double cap, double gate, double omega_min, uint8_t* is_new,
                  int* block_new, int* total, int n0, cudaStream_t s);
 
-// emap: scratch of edge_map_words(W, H) * frames words (smooth-edge bitmaps)
-inline long edge_map_words(int W, int H) {
-  const long w32 = (W + 31) / 32 + 1, h32 = (H + 31) / 32 + 1;
-  return (long)H * w32 + (long)W * h32 + 2L * (W + H - 1) * h32;
-}
+// emap: scratch of edge_map_words(W, H) * frames words (validity and
+// smooth-edge bitmaps, five row-major planes of ceil(W/32) words per row)
+inline long edge_map_words(int W, int H) { return 5L * H * ((W + 31) / 32); }
 // dout2/vout2/list/count (optional, nullptr = off): a second copy of the
 // result and the per-frame list of invalid output pixels (the chain's radial
 // fill then touches only those).
