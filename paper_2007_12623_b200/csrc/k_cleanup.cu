@@ -43,7 +43,7 @@ __constant__ int c_dirV[8] = {0, 0, 1, -1, 1, -1, 1, -1};
 // shift doubling, and a word stops as soon as all its valid pixels passed.
 namespace {
 constexpr int kEdgeMaps = 5;  // V, E_h, E_v, E_d1, E_d2
-constexpr int kEdgeStrip = 16;  // rows per warp in k_edge_words
+constexpr int kEdgeStrip = 8;  // rows per warp in k_edge_words (all loads in flight)
 struct EdgeWords {
   const uint32_t* m[kEdgeMaps];
   int ww;  // words per row
@@ -63,71 +63,72 @@ __global__ void __launch_bounds__(128)
     k_edge_words(const float* __restrict__ din, const uint8_t* __restrict__ vin,
                  uint32_t* __restrict__ emap, int W, int H, double thr, long stride, long fw,
                  float* __restrict__ dcopy, float* __restrict__ dcopy2) {
+  constexpr int KS = kEdgeStrip, NR = KS + 2;  // rows v0 - 1 .. v0 + KS
   const long f = blockIdx.z;
   const int lane = threadIdx.x;
   const int w = blockIdx.x * 4 + threadIdx.y, ww = edge_ww(W);
   if (w >= ww) return;
-  const int v0 = blockIdx.y * kEdgeStrip, v1 = min(H, v0 + kEdgeStrip);
+  const int v0 = blockIdx.y * KS;
   const int u = w * 32 + lane;
-  const float* dr = din + f * stride;
-  const uint8_t* vr = vin + f * stride;
-  // pixel (u, v) and its right neighbour (u + 1, v): lane 31 loads the latter
-  auto load = [&](int v, double& d, bool& ok, double& dn, bool& okn) {
-    float x = 0.f, xn = 0.f;
-    ok = false;
-    okn = false;
+  const bool inx = u < W, inx1 = lane == 31 && u + 1 < W;
+  // every load of the strip in flight at once: pixel (u, v) per lane, and
+  // lane 31 also the right neighbour (u + 1, v)
+  float x[NR], x1[NR];
+  uint32_t ok = 0u, ok1 = 0u;  // bit j: row v0 - 1 + j valid at u / at u + 1 (lane 31)
+  const long base = f * stride + (long)(v0 - 1) * W + u;
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    const int v = v0 - 1 + j;
+    x[j] = 0.f;
+    x1[j] = 0.f;
     if (v >= 0 && v < H) {
-      const long i = (long)v * W + u;
-      if (u < W) {
-        x = dr[i];
-        ok = vr[i] != 0;
-        if (v >= v0 && v < v1) {
-          if (dcopy) dcopy[f * stride + i] = x;
-          if (dcopy2) dcopy2[f * stride + i] = x;
-        }
+      const long i = base + (long)j * W;
+      if (inx) {
+        x[j] = din[i];
+        ok |= (vin[i] != 0 ? 1u : 0u) << j;
       }
-      if (lane == 31 && u + 1 < W) {
-        xn = dr[i + 1];
-        okn = vr[i + 1] != 0;
+      if (inx1) {
+        x1[j] = din[i + 1];
+        ok1 |= (vin[i + 1] != 0 ? 1u : 0u) << j;
       }
     }
-    const float sx = __shfl_down_sync(0xFFFFFFFFu, x, 1);
-    const bool sok = __shfl_down_sync(0xFFFFFFFFu, ok ? 1 : 0, 1) != 0;
-    if (lane != 31) {
-      xn = sx;
-      okn = sok;
+  }
+  if (inx) {
+#pragma unroll
+    for (int j = 1; j <= KS; ++j) {
+      if (v0 - 1 + j < H) {
+        if (dcopy) dcopy[base + (long)j * W] = x[j];
+        if (dcopy2) dcopy2[base + (long)j * W] = x[j];
+      }
     }
-    d = (double)x;
-    dn = (double)xn;
-  };
-  // smooth edge between values a (valid oa) and b (valid ob): cleanup.cpp:25-31
-  auto edge = [&](bool oa, double a, bool ob, double b) {
-    return oa && ob && !(fabs(b - a) > thr);
-  };
-  double dp, dpn, dc, dcn, dn, dnn;
-  bool op, opn, oc, ocn, on, onn;
-  load(v0 - 1, dp, op, dpn, opn);
-  load(v0, dc, oc, dcn, ocn);
-  uint32_t* out = emap + f * fw;
+  }
+  // right neighbours: from lane + 1, lane 31 from its own extra loads
+  const uint32_t okn_all = __shfl_down_sync(0xFFFFFFFFu, ok, 1);
+  const uint32_t okn = lane == 31 ? ok1 : okn_all;
+  double d[NR], dn[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    const float s = __shfl_down_sync(0xFFFFFFFFu, x[j], 1);
+    d[j] = (double)x[j];
+    dn[j] = (double)(lane == 31 ? x1[j] : s);
+  }
+  // smooth edge: both ends valid and |b - a| <= thr in double (cleanup.cpp:25-31)
+  auto sm = [thr](double a, double b) { return !(fabs(b - a) > thr); };
   const long plane = (long)H * ww;
-#pragma unroll 1
-  for (int v = v0; v < v1; ++v) {
-    load(v + 1, dn, on, dnn, onn);
+  uint32_t* out = emap + f * fw + (long)lane * plane + (long)v0 * ww + w;
+#pragma unroll
+  for (int j = 1; j <= KS; ++j) {
+    if (v0 - 1 + j >= H) break;
+    const bool oc = (ok >> j) & 1u;
     const unsigned bv = __ballot_sync(0xFFFFFFFFu, oc);
-    const unsigned bh = __ballot_sync(0xFFFFFFFFu, edge(oc, dc, ocn, dcn));
-    const unsigned bvv = __ballot_sync(0xFFFFFFFFu, edge(oc, dc, on, dn));
-    const unsigned bd1 = __ballot_sync(0xFFFFFFFFu, edge(oc, dc, onn, dnn));
-    const unsigned bd2 = __ballot_sync(0xFFFFFFFFu, edge(oc, dc, opn, dpn));
-    if (lane < kEdgeMaps) {
-      const unsigned x = lane == 0 ? bv : lane == 1 ? bh : lane == 2 ? bvv : lane == 3 ? bd1 : bd2;
-      out[lane * plane + (long)v * ww + w] = x;
-    }
-    dpn = dcn;
-    opn = ocn;
-    dc = dn;
-    oc = on;
-    dcn = dnn;
-    ocn = onn;
+    const unsigned bh = __ballot_sync(0xFFFFFFFFu, oc && ((okn >> j) & 1u) && sm(d[j], dn[j]));
+    const unsigned bvv = __ballot_sync(0xFFFFFFFFu, oc && ((ok >> (j + 1)) & 1u) && sm(d[j], d[j + 1]));
+    const unsigned bd1 =
+        __ballot_sync(0xFFFFFFFFu, oc && ((okn >> (j + 1)) & 1u) && sm(d[j], dn[j + 1]));
+    const unsigned bd2 =
+        __ballot_sync(0xFFFFFFFFu, oc && ((okn >> (j - 1)) & 1u) && sm(d[j], dn[j - 1]));
+    if (lane < kEdgeMaps)
+      out[(long)(j - 1) * ww] = lane == 0 ? bv : lane == 1 ? bh : lane == 2 ? bvv : lane == 3 ? bd1 : bd2;
   }
 }
 

@@ -163,6 +163,47 @@ __global__ void k_lds(int* out, int seed, Clk* c) {
   if (acc == 0x12345678u) out[0] = (int)acc;
 }
 
+// Warp shuffles (32-bit, index from a register): lane-ops per clock.
+__global__ void k_shfl(int* out, int seed, Clk* c) {
+  uint32_t a[kChains];
+  for (int k = 0; k < kChains; ++k) a[k] = seed + threadIdx.x + k;
+  const int src = (threadIdx.x + 1) & 31;
+  clk_begin(c);
+#pragma unroll 16
+  for (int i = 0; i < kIters; ++i)
+#pragma unroll
+    for (int k = 0; k < kChains; ++k)
+      asm volatile("shfl.sync.idx.b32 %0, %0, %1, 31, -1;" : "+r"(a[k]) : "r"(src));
+  clk_end(c);
+  uint32_t s = 0;
+  for (int k = 0; k < kChains; ++k) s ^= a[k];
+  if (s == 0x7fffffffu) out[0] = (int)s;
+}
+
+// LDS.64 and 64-bit shuffles interleaved one to one: if the two share the
+// shared-memory data path, the byte rate of the pair stays at the LDS rate.
+__global__ void k_lds_shfl(int* out, int seed, Clk* c) {
+  __shared__ __align__(16) uint32_t sm[8192];
+  for (int i = threadIdx.x; i < 8192; i += blockDim.x) sm[i] = i * 2654435761u + seed;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  uint32_t acc = 0, b0 = seed, b1 = seed + 1;
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(sm) + lane * 8;
+  const int src = (lane + 1) & 31;
+  clk_begin(c);
+#pragma unroll 16
+  for (int i = 0; i < kIters; ++i) {
+    const uint32_t a = base + (i & 15) * 256;
+    uint32_t x, y;
+    asm volatile("ld.volatile.shared.v2.u32 {%0, %1}, [%2];" : "=r"(x), "=r"(y) : "r"(a));
+    asm volatile("shfl.sync.idx.b32 %0, %0, %2, 31, -1;\n\tshfl.sync.idx.b32 %1, %1, %2, 31, -1;"
+                 : "+r"(b0), "+r"(b1) : "r"(src));
+    acc ^= x ^ y;
+  }
+  clk_end(c);
+  if ((acc ^ b0 ^ b1) == 0x12345678u) out[0] = (int)acc;
+}
+
 typedef void (*Kern)(int*, int, Clk*);
 
 // lane-ops (or bytes) per clock per SM: a block's work over its cycle count
@@ -217,7 +258,11 @@ int main() {
   rc |= run("dfma_f64", k_dfma, ops, "lane-ops", nsm, d_out, d_clk, h_clk, false);
   rc |= run("lds_32", k_lds<4>, (double)kIters * 4, "bytes", nsm, d_out, d_clk, h_clk, false);
   rc |= run("lds_64", k_lds<8>, (double)kIters * 8, "bytes", nsm, d_out, d_clk, h_clk, false);
-  rc |= run("lds_128", k_lds<16>, (double)kIters * 16, "bytes", nsm, d_out, d_clk, h_clk, true);
+  rc |= run("lds_128", k_lds<16>, (double)kIters * 16, "bytes", nsm, d_out, d_clk, h_clk, false);
+  rc |= run("shfl_32", k_shfl, ops, "lane-ops", nsm, d_out, d_clk, h_clk, false);
+  // pair rate: LDS.64 bytes per clock with two 32-bit shuffles beside each load
+  rc |= run("lds_64_with_2_shfl", k_lds_shfl, (double)kIters * 8, "LDS bytes", nsm, d_out, d_clk,
+            h_clk, true);
   printf("  }\n}\n");
   return rc;
 }
