@@ -206,7 +206,7 @@ __device__ __forceinline__ uint32_t outlier_keep(const EdgeWords& E, int W, int 
 // of the invalid output pixels (one atomic per warp, ~5% of the pixels).
 // vout may alias the input validity (the maps hold it).
 __global__ void __launch_bounds__(128)
-    k_outlier_words(const uint32_t* __restrict__ emap, uint8_t* vout, uint8_t* __restrict__ vout2,
+    k_outlier_words(uint32_t* __restrict__ emap, uint8_t* vout, uint8_t* __restrict__ vout2,
                     int W, int H, int r, long stride, long fw, int* __restrict__ list,
                     unsigned* __restrict__ count) {
   const long f = blockIdx.z;
@@ -217,11 +217,12 @@ __global__ void __launch_bounds__(128)
   EdgeWords E;
   const long plane = (long)H * ww;
 #pragma unroll
-  for (int k = 0; k < kEdgeMaps; ++k) E.m[k] = emap + f * fw + k * plane;
+  for (int k = 0; k < kEdgeMaps; ++k) E.m[k] = emap + f * fw + k * plane;  // read only
   E.ww = ww;
   uint32_t keep = 0u, inimg = 0u;
   if (act) {
     keep = r > 0 ? outlier_keep(E, W, H, v, w, r) : E.word(0, v, w);  // r <= 0: no steps
+    emap[f * fw + kEdgeMaps * plane + (long)v * ww + w] = keep;  // result plane (radial fill)
     const int n = min(32, W - w * 32);
     inimg = n == 32 ? ~0u : (1u << n) - 1u;
     const long i0 = f * stride + (long)v * W + w * 32;
@@ -332,19 +333,151 @@ __global__ void k_fill_radial(const float* __restrict__ din, const uint8_t* __re
   if (!vin[i]) radial_fill_pixel(din, vin, dout, vout, W, H, u, v, radius, min_support);
 }
 
-// Chain variant: dout/vout already hold the input map (k_remove_outliers'
-// second copy); one thread per listed invalid pixel, no idle lanes.
-__global__ void k_fill_radial_list(const float* __restrict__ din, const uint8_t* __restrict__ vin,
-                                   float* __restrict__ dout, uint8_t* __restrict__ vout, int W,
-                                   int H, int radius, int min_support, long stride,
-                                   const int* __restrict__ list,
-                                   const unsigned* __restrict__ count) {
+// The outlier pass's result by columns and by diagonals (for the radial
+// fill's ray searches): one warp per (32-row block, word column w), lane =
+// row; each transposed word is one ballot over the lanes' row words. Lines:
+// column u (position v); d1 = u - v + H - 1 (position v); d2 = u + v
+// (position v); ceil(H/32) words per line. Word columns -1 .. ww cover the
+// diagonals that cross a row block's first row outside the image.
+namespace {
+struct ValidLines {
+  uint32_t *col, *d1, *d2;
+  int hw;
+};
+__host__ __device__ inline ValidLines valid_lines(uint32_t* frame, int W, int H) {
+  const int ww = edge_ww(W), hw = (H + 31) / 32;
+  ValidLines L;
+  L.col = frame + 6L * H * ww;
+  L.d1 = L.col + (long)W * hw;
+  L.d2 = L.d1 + (long)(W + H - 1) * hw;
+  L.hw = hw;
+  return L;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(128)
+    k_valid_bits(uint32_t* __restrict__ emap, int W, int H, long fw) {
+  const long f = blockIdx.z;
+  const int lane = threadIdx.x;
+  const int w = (int)(blockIdx.x * blockDim.y + threadIdx.y) - 1;  // -1 .. ww
+  const int ww = edge_ww(W);
+  if (w > ww) return;
+  const int rb = blockIdx.y, v = rb * 32 + lane;
+  uint32_t* fr = emap + f * fw;
+  const uint32_t* K = fr + kEdgeMaps * (long)H * ww;
+  auto kw = [&](int q) { return (v < H && q >= 0 && q < ww) ? K[(long)v * ww + q] : 0u; };
+  const uint32_t km = kw(w - 1), k0 = kw(w), kp = kw(w + 1);
+  const uint64_t a1 = ((uint64_t)kp << 32) | k0;  // columns 32w .. 32w + 63
+  const uint64_t a2 = ((uint64_t)k0 << 32) | km;  // columns 32w - 32 .. 32w + 31
+  const ValidLines L = valid_lines(fr, W, H);
+  uint32_t mc = 0, m1 = 0, m2 = 0;
+#pragma unroll 4
+  for (int d = 0; d < 32; ++d) {
+    // column 32w + d; d1 line through (32w + d, 32 rb); d2 line through it
+    const uint32_t c = __ballot_sync(0xFFFFFFFFu, (k0 >> d) & 1u);
+    const uint32_t x1 = __ballot_sync(0xFFFFFFFFu, (uint32_t)(a1 >> (d + lane)) & 1u);
+    const uint32_t x2 = __ballot_sync(0xFFFFFFFFu, (uint32_t)(a2 >> (32 + d - lane)) & 1u);
+    if (lane == d) {
+      mc = c;
+      m1 = x1;
+      m2 = x2;
+    }
+  }
+  const int u = 32 * w + lane;
+  if (w >= 0 && u < W) L.col[(long)u * L.hw + rb] = mc;
+  const long i1 = (long)u - rb * 32 + H - 1, i2 = (long)u + rb * 32;
+  if (w < ww && i1 >= 0 && i1 < W + H - 1) L.d1[i1 * L.hw + rb] = m1;
+  if (w >= 0 && i2 >= 0 && i2 < W + H - 1) L.d2[i2 * L.hw + rb] = m2;
+}
+
+namespace {
+// first / last set position of a bit line in [a, b] (a <= b), or -1
+__device__ __forceinline__ int first_set(const uint32_t* __restrict__ line, int a, int b) {
+  for (int q = a >> 5; q <= (b >> 5); ++q) {
+    uint32_t x = __ldg(line + q);
+    if (q == (a >> 5)) x &= ~0u << (a & 31);
+    if (q == (b >> 5)) x &= ~0u >> (31 - (b & 31));
+    if (x) return q * 32 + __ffs(x) - 1;
+  }
+  return -1;
+}
+__device__ __forceinline__ int last_set(const uint32_t* __restrict__ line, int a, int b) {
+  for (int q = b >> 5; q >= (a >> 5); --q) {
+    uint32_t x = __ldg(line + q);
+    if (q == (a >> 5)) x &= ~0u << (a & 31);
+    if (q == (b >> 5)) x &= ~0u >> (31 - (b & 31));
+    if (x) return q * 32 + 31 - __clz(x);
+  }
+  return -1;
+}
+}  // namespace
+
+// Chain variant: dout/vout already hold the input map (the outlier pass's
+// second copy); one thread per listed invalid pixel. The nearest valid pixel
+// of each ray is a bit search on the outlier result's row, column or
+// diagonal line (the reference's per-step walk, cleanup.cpp:57-66, stops at
+// the first valid pixel within the radius and at the image border; the
+// search range is clipped to both). Sums in direction order 0..7, as there.
+__global__ void k_fill_radial_list(const float* __restrict__ din, float* __restrict__ dout,
+                                   uint8_t* __restrict__ vout, int W, int H, int radius,
+                                   int min_support, long stride, const int* __restrict__ list,
+                                   const unsigned* __restrict__ count,
+                                   const uint32_t* __restrict__ emap, long fw) {
   const long f = blockIdx.y;
   const unsigned n = count[f];
+  const int ww = edge_ww(W);
+  const uint32_t* fr = emap + f * fw;
+  const uint32_t* K = fr + kEdgeMaps * (long)H * ww;
+  const ValidLines L = valid_lines(const_cast<uint32_t*>(fr), W, H);
+  const float* dr = din + f * stride;
   for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     const int pix = list[f * stride + t];
-    radial_fill_pixel(din + f * stride, vin + f * stride, dout + f * stride, vout + f * stride,
-                      W, H, pix % W, pix / W, radius, min_support);
+    const int u = pix % W, v = pix / W;
+    const int r = radius;
+    const int rr = min(r, W - 1 - u), rl = min(r, u), rd = min(r, H - 1 - v), ru = min(r, v);
+    const uint32_t* row = K + (long)v * ww;
+    const uint32_t* col = L.col + (long)u * L.hw;
+    const uint32_t* d1 = L.d1 + ((long)u - v + H - 1) * L.hw;
+    const uint32_t* d2 = L.d2 + ((long)u + v) * L.hw;
+    int step[8];
+    int p;
+    p = rr > 0 ? first_set(row, u + 1, u + rr) : -1;
+    step[0] = p < 0 ? 0 : p - u;                                          // (1, 0)
+    p = rl > 0 ? last_set(row, u - rl, u - 1) : -1;
+    step[1] = p < 0 ? 0 : u - p;                                          // (-1, 0)
+    p = rd > 0 ? first_set(col, v + 1, v + rd) : -1;
+    step[2] = p < 0 ? 0 : p - v;                                          // (0, 1)
+    p = ru > 0 ? last_set(col, v - ru, v - 1) : -1;
+    step[3] = p < 0 ? 0 : v - p;                                          // (0, -1)
+    int m = min(rr, rd);
+    p = m > 0 ? first_set(d1, v + 1, v + m) : -1;
+    step[4] = p < 0 ? 0 : p - v;                                          // (1, 1)
+    m = min(rr, ru);
+    p = m > 0 ? last_set(d2, v - m, v - 1) : -1;
+    step[5] = p < 0 ? 0 : v - p;                                          // (1, -1)
+    m = min(rl, rd);
+    p = m > 0 ? first_set(d2, v + 1, v + m) : -1;
+    step[6] = p < 0 ? 0 : p - v;                                          // (-1, 1)
+    m = min(rl, ru);
+    p = m > 0 ? last_set(d1, v - m, v - 1) : -1;
+    step[7] = p < 0 ? 0 : v - p;                                          // (-1, -1)
+    double wsum = 0.0, vsum = 0.0;
+    int support = 0;
+#pragma unroll
+    for (int dir = 0; dir < 8; ++dir) {
+      const int hit = step[dir];
+      if (!hit) continue;
+      const double len = dir < 4 ? 1.0 : 1.41421356237309504880;  // M_SQRT2
+      const long ni = (long)(v + c_dirV[dir] * hit) * W + (u + c_dirU[dir] * hit);
+      const double w = __ddiv_rn(1.0, __dmul_rn((double)hit, len));
+      wsum = __dadd_rn(wsum, w);
+      vsum = __dadd_rn(vsum, __dmul_rn(w, (double)__ldg(dr + ni)));
+      ++support;
+    }
+    if (support >= min_support && wsum > 0.0) {
+      dout[f * stride + pix] = (float)__ddiv_rn(vsum, wsum);
+      vout[f * stride + pix] = 1;
+    }
   }
 }
 
@@ -469,10 +602,16 @@ void launch_remove_outliers(const float* din, const uint8_t* vin, float* dout, u
 
 void launch_fill_radial_list(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
                              int W, int H, int radius, int min_support, const int* list,
-                             const unsigned* count, int frames, long stride, cudaStream_t s) {
+                             const unsigned* count, const uint32_t* emap, int frames, long stride,
+                             cudaStream_t s) {
+  (void)vin;  // the validity comes from the outlier pass's bit planes in emap
   if (W <= 0 || H <= 0 || frames <= 0) return;
-  k_fill_radial_list<<<dim3(96, frames), 128, 0, s>>>(din, vin, dout, vout, W, H, radius,
-                                                      min_support, stride, list, count);
+  const long fw = edge_map_words(W, H);
+  const int ww = edge_ww(W);
+  k_valid_bits<<<dim3((ww + 2 + 3) / 4, (H + 31) / 32, frames), dim3(32, 4), 0, s>>>(
+      const_cast<uint32_t*>(emap), W, H, fw);
+  k_fill_radial_list<<<dim3(96, frames), 128, 0, s>>>(din, dout, vout, W, H, radius, min_support,
+                                                      stride, list, count, emap, fw);
 }
 
 void launch_fill_radial(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,

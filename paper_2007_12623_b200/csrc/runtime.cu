@@ -533,14 +533,15 @@ struct ss_ctx {
                              valid_a.as<uint8_t>(), W, H, r, params.neighbor_jump_threshold,
                              emap.as<uint32_t>(), n, N, stream, disp_b.as<float>(),
                              valid_b.as<uint8_t>(), flags.as<int>(), flag_count.as<unsigned>());
-      stats.kernel_launches += r > 0 ? 2 : 1;
+      stats.kernel_launches += 2;
       }
       {
       Stage sr(this, 8);
       launch_fill_radial_list(disp_a.as<float>(), valid_a.as<uint8_t>(), disp_b.as<float>(),
                               valid_b.as<uint8_t>(), W, H, params.fill_radius_radial, 4,
-                              flags.as<int>(), flag_count.as<unsigned>(), n, N, stream);
-      stats.kernel_launches += 1;
+                              flags.as<int>(), flag_count.as<unsigned>(), emap.as<uint32_t>(), n,
+                              N, stream);
+      stats.kernel_launches += 2;
       }
       Stage sd(this, 9);
       fill_disc(n, W, H, disp_b.as<float>(), valid_b.as<uint8_t>(), disp_a.as<float>(),

@@ -153,9 +153,14 @@ void launch_fuse(double* pos, double* nrm, double* col, double* w, double* cw, c
                  double trunc, double cap, double gate, double omega_min, uint8_t* is_new,
                  int* block_new, int* total, int n0, cudaStream_t s);
 
-// emap: scratch of edge_map_words(W, H) * frames words (validity and
-// smooth-edge bitmaps, five row-major planes of ceil(W/32) words per row)
-inline long edge_map_words(int W, int H) { return 5L * H * ((W + 31) / 32); }
+// emap: scratch of edge_map_words(W, H) * frames words: the outlier pass's
+// validity and smooth-edge bitmaps (five row-major planes of ceil(W/32) words
+// per row), its result (a sixth row-major plane) and that result by columns
+// and by both diagonals (lines of ceil(H/32) words) for the radial fill
+inline long edge_map_words(int W, int H) {
+  const long ww = (W + 31) / 32, hw = (H + 31) / 32;
+  return 6L * H * ww + (long)W * hw + 2L * (W + H - 1) * hw;
+}
 // dout2/vout2/list/count (optional, nullptr = off): a second copy of the
 // result and the per-frame list of invalid output pixels (the chain's radial
 // fill then touches only those).
@@ -164,10 +169,12 @@ void launch_remove_outliers(const float* din, const uint8_t* vin, float* dout, u
                             long stride, cudaStream_t s, float* dout2 = nullptr,
                             uint8_t* vout2 = nullptr, int* list = nullptr,
                             unsigned* count = nullptr);
-// dout/vout must already hold din/vin; fills the listed pixels only.
+// dout/vout must already hold din/vin; fills the listed pixels only. emap:
+// the maps launch_remove_outliers left (its result is vin), searched by bits.
 void launch_fill_radial_list(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
                              int W, int H, int radius, int min_support, const int* list,
-                             const unsigned* count, int frames, long stride, cudaStream_t s);
+                             const unsigned* count, const uint32_t* emap, int frames, long stride,
+                             cudaStream_t s);
 void launch_fill_radial(const float* din, const uint8_t* vin, float* dout, uint8_t* vout,
                         int W, int H, int radius, int min_support, int frames, long stride,
                         cudaStream_t s);
