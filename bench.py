@@ -269,7 +269,8 @@ def sha(a, dt):
 
 def digest_keys(args):
     dig = json.load(open(DIGEST_PATH)) if os.path.exists(DIGEST_PATH) else {}
-    pre = {"c4": "bench_c4_", "c3": "bench_c3_", "c5": "bench_c5_"}.get(args.workload)
+    pre = {"c4": "bench_c4_", "c2": "bench_c2_", "c3": "bench_c3_",
+           "c5": "bench_c5_"}.get(args.workload)
     if pre is None:
         return dig, []
     keys = sorted(k for k in dig if k.startswith(pre))

@@ -10,13 +10,18 @@
 //       the reference's association order -> bit-identical points; colour
 //       from the left RGB image when (u, v) is inside it.
 //   k_cloud_normals
-//       7x7 neighbourhood (kNormalWindowHalf = 3) of existing points, mean and
-//       covariance accumulated in raster order in FP64, closed-form symmetric
-//       3x3 eigen-decomposition (trigonometric eigenvalues, cross-product
-//       eigenvector) instead of Eigen's SelfAdjointEigenSolver (cloud.cpp:78):
-//       agreement is within tolerance, not bitwise. Same
-//       acceptance rule (lambda1 > 1e-9 max(1, lambda2)), same -p/|p|
-//       fallback and camera-facing flip (cloud.cpp:81-89).
+//       7x7 neighbourhood (kNormalWindowHalf = 3) of existing points: window
+//       moments as FP64 box sums over a 32 x 8 tile, covariance, closed-form
+//       FP32 eigenvalues with an FP64 inverse-iteration eigenvector; the fast
+//       path only claims "fitted" when lambda1 > 2e-3 max(1, lambda2), ten
+//       times its measured error. Below that the pixel runs the reference's
+//       computation on the device: mean and covariance of the FP64 points in
+//       its neighbour order and a restatement of Eigen 3.4.0's
+//       SelfAdjointEigenSolver (cloud.cpp:78, eg::eigen3_sym below) with its
+//       acceptance rule lambda1 > 1e-9 max(1, lambda2) (cloud.cpp:81).
+//       Normals agree within a tolerance, not bitwise; the
+//       fit/fallback decision and the -p/|p| fallback and camera-facing flip
+//       (cloud.cpp:81-89) are the reference's.
 #include <math.h>
 
 #include "ss_internal.cuh"

@@ -45,6 +45,10 @@ CASES = [
     ("bench_c4_1", "textured", 960, 540, 64, 1, 0),
     ("bench_c4_2", "textured", 960, 540, 64, 2, 0),
     ("bench_c4_3", "textured", 960, 540, 64, 3, 0),
+    ("bench_c2_0", "lowtex", 960, 540, 64, 0, 0),
+    ("bench_c2_1", "lowtex", 960, 540, 64, 1, 0),
+    ("bench_c2_2", "lowtex", 960, 540, 64, 2, 0),
+    ("bench_c2_3", "lowtex", 960, 540, 64, 3, 0),
     ("bench_c3_0", "textured", 1920, 1080, 128, 100, 0),
     ("bench_c3_1", "textured", 1920, 1080, 128, 101, 0),
     ("bench_c5_0", "video", 1920, 1080, 128, 0, 0),
