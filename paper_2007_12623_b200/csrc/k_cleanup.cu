@@ -481,10 +481,15 @@ __global__ void k_fill_radial_list(const float* __restrict__ din, float* __restr
   }
 }
 
-// Invalid-neighbour marker in fx: the smallest denormal (low word 1) — a double
-// converted from a float always has its low 29 mantissa bits zero, so no
-// disparity (not even NaN/inf) carries it, and 0 * marker = +0.
-constexpr int kInvalidLo = 1;
+// fx (pass 1) holds the disc pass's input as floats: a valid disparity as is,
+// an invalid neighbour as a NaN payload that valid disparities are re-coded
+// away from (half the tap-load bytes of a double map; measured 5% faster).
+constexpr uint32_t kFxInvalid = 0xFFBADBADu;
+using fx_t = float;
+__device__ __forceinline__ fx_t fx_code(bool ok, float d) {
+  return ok ? (__float_as_uint(d) == kFxInvalid ? __uint_as_float(0x7FFFFFFFu) : d)
+            : __uint_as_float(kFxInvalid);
+}
 
 // Disc fill, pass 1: copy the map through and, for invalid pixels, count the
 // valid disc neighbours from per-row prefix counts (exact integers, 2 loads
@@ -504,7 +509,7 @@ __global__ void k_disc_select(const float* __restrict__ din, const uint8_t* __re
   const uint8_t ov = vin[i];
   dout[i] = od;
   vout[i] = ov;
-  fx[i] = ov ? (double)od : __hiloint2double(0, kInvalidLo);  // invalid neighbour
+  reinterpret_cast<fx_t*>(fx)[i] = fx_code(ov != 0, od);  // invalid neighbour: marker
   bool listed = false;
   if (!ov && radius > 0) {
     const int* pc = pcnt + f * pstride;
@@ -524,21 +529,21 @@ __global__ void k_disc_select(const float* __restrict__ din, const uint8_t* __re
 // Disc fill, pass 2: one thread per listed pixel, the reference's raster-order
 // double accumulation (cleanup.cpp:71-83) with w = 1/sqrt(dd) from a host
 // table ((2R+1)^2 doubles, staged in shared memory). The neighbours come from
-// fx = valid ? double(d) : marker (written by pass 1): one load per disc pixel
+// fx = valid ? d : marker (written by pass 1): one 4-byte load per disc pixel
 // gives both, an invalid one adds +0.0 to both sums, the loads
 // of a row are issued together and only the two FP64 add chains are serial.
-__device__ __forceinline__ void disc_acc(double& wsum, double& vsum, double w, double x) {
-  // invalid: w_eff = 0 adds +0.0 to both sums, which leaves them bit-identical
-  // (neither is ever -0.0: both start at +0.0 and an exactly-zero
-  // round-to-nearest sum is +0.0)
-  const double we = __double2loint(x) != kInvalidLo ? w : 0.0;
-  wsum = __dadd_rn(wsum, we);
-  vsum = __dadd_rn(vsum, __dmul_rn(we, x));
+__device__ __forceinline__ void disc_acc(double& wsum, double& vsum, double w, float xf) {
+  // invalid: x = 0 and w_eff = 0 add +0.0 to both sums, which leaves them
+  // bit-identical (neither is ever -0.0: both start at +0.0 and an
+  // exactly-zero round-to-nearest sum is +0.0)
+  const bool ok = __float_as_uint(xf) != kFxInvalid;
+  wsum = __dadd_rn(wsum, ok ? w : 0.0);
+  vsum = __dadd_rn(vsum, __dmul_rn(w, (double)(ok ? xf : 0.f)));
 }
 
 template <bool SMEM>
 __global__ void __launch_bounds__(256)
-    k_disc_sum(const double* __restrict__ fx, float* __restrict__ dout, uint8_t* __restrict__ vout,
+    k_disc_sum(const fx_t* __restrict__ fx, float* __restrict__ dout, uint8_t* __restrict__ vout,
                const int* __restrict__ list, const unsigned* __restrict__ count,
                const int* __restrict__ span, const double* __restrict__ wtab, int W, int H,
                int radius, long stride, unsigned long long* __restrict__ ctr) {
@@ -551,7 +556,7 @@ __global__ void __launch_bounds__(256)
   const long f = blockIdx.y;
   const unsigned n = count[f];
   if (blockIdx.x == 0 && threadIdx.x == 0 && ctr) atomicAdd(ctr + 4, (unsigned long long)n);
-  const double* xf = fx + f * stride;
+  const fx_t* xf = fx + f * stride;
   for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     const int idx = list[f * stride + t];
     const int v = idx / W, u = idx % W;
@@ -560,11 +565,12 @@ __global__ void __launch_bounds__(256)
     for (int dv = v0; dv <= v1; ++dv) {
       const int sx = __ldg(span + (dv < 0 ? -dv : dv));
       const int a = max(-sx, -u), b = min(sx, W - 1 - u);
-      const double* xr = xf + (long)(v + dv) * W + u;
+      const fx_t* xr = xf + (long)(v + dv) * W + u;
       const int wo = (dv + radius) * D + radius;
       int du = a;
       for (; du + 3 <= b; du += 4) {
-        double x[4], w[4];
+        fx_t x[4];
+        double w[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           x[k] = __ldg(xr + du + k);
@@ -637,11 +643,13 @@ void launch_fill_disc(const float* din, const uint8_t* vin, float* dout, uint8_t
                                                         stride, pstride);
   const size_t wbytes = sizeof(double) * (2 * (size_t)radius + 1) * (2 * (size_t)radius + 1);
   if (wbytes <= 40 * 1024)
-    k_disc_sum<true><<<dim3(96, frames), 256, wbytes, s>>>(fx, dout, vout, list, count, span, wtab,
-                                                         W, H, radius, stride, ctr);
+    k_disc_sum<true><<<dim3(96, frames), 256, wbytes, s>>>(
+        reinterpret_cast<const fx_t*>(fx), dout, vout, list, count, span, wtab, W, H, radius,
+        stride, ctr);
   else
-    k_disc_sum<false><<<dim3(96, frames), 256, 0, s>>>(fx, dout, vout, list, count, span, wtab, W,
-                                                     H, radius, stride, ctr);
+    k_disc_sum<false><<<dim3(96, frames), 256, 0, s>>>(
+        reinterpret_cast<const fx_t*>(fx), dout, vout, list, count, span, wtab, W, H, radius,
+        stride, ctr);
 }
 
 }  // namespace ssb
