@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(128)
   // smooth edge: both ends valid and |b - a| <= thr in double (cleanup.cpp:25-31)
   auto sm = [thr](double a, double b) { return !(fabs(b - a) > thr); };
   const long plane = (long)H * ww;
-  uint32_t* out = emap + f * fw + (long)lane * plane + (long)v0 * ww + w;
+  uint32_t* out = emap + f * fw + (long)v0 * ww + w;
 #pragma unroll
   for (int j = 1; j <= KS; ++j) {
     if (v0 - 1 + j >= H) break;
@@ -127,8 +127,14 @@ __global__ void __launch_bounds__(128)
         __ballot_sync(0xFFFFFFFFu, oc && ((okn >> (j + 1)) & 1u) && sm(d[j], dn[j + 1]));
     const unsigned bd2 =
         __ballot_sync(0xFFFFFFFFu, oc && ((okn >> (j - 1)) & 1u) && sm(d[j], dn[j - 1]));
-    if (lane < kEdgeMaps)
-      out[(long)(j - 1) * ww] = lane == 0 ? bv : lane == 1 ? bh : lane == 2 ? bvv : lane == 3 ? bd1 : bd2;
+    if (lane == 0) {
+      uint32_t* o = out + (long)(j - 1) * ww;
+      o[0] = bv;
+      o[plane] = bh;
+      o[2 * plane] = bvv;
+      o[3 * plane] = bd1;
+      o[4 * plane] = bd2;
+    }
   }
 }
 
