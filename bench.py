@@ -811,6 +811,7 @@ def run_ours(args):
         "exact_resolves": {"wta_pixels": stats["wta_resolved"],
                            "refine_repicks": stats["refine_resolved"],
                            "disc_fill_pixels": stats.get("disc_fill_pixels"),
+                           "refine_scored": stats.get("refine_scored"),
                            "frames": stats["frames"]},
         "extensions": ext,
     }

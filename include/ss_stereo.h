@@ -260,7 +260,8 @@ typedef struct ss_ctx_stats {
   int64_t frames;            /* frames processed */
   int64_t wta_resolved;      /* pixels whose WTA pick went through the exact FP64 resolve */
   int64_t refine_resolved;   /* (pixel, iteration) re-picks resolved in exact FP64 */
-  int64_t refine_fallback;   /* (pixel, iteration) re-picks recomputed without the cost volume */
+  int64_t refine_scored;     /* (pixel, iteration) re-picks scored; the others were certified
+                                unchanged (window 11, smoothing radius 15) */
   int64_t kernel_launches;   /* kernels launched by this ctx */
   int64_t disc_fill_pixels;  /* pixels that went through the disc fill (all cleanup rounds) */
 } ss_ctx_stats;

@@ -31,6 +31,7 @@
 #include <limits.h>
 #include <math.h>
 
+#include <stdexcept>
 #include <type_traits>
 #include <utility>
 
@@ -448,9 +449,10 @@ namespace {
 
 // A thread's window: 16 fp16 match costs (m_code) in 8 u32 planes of shared memory.
 struct WinView {
-  const uint32_t* p;  // plane 0 word of this pixel; plane j at p[j * kWinPlane]
+  const uint32_t* p;  // plane 0 word of this pixel; plane j at p[j * stride]
+  long stride;        // kWinPlane (shared-memory planes) or W * 32 (global BT planes)
   __device__ __forceinline__ float mcost(int k) const {  // k in [0, kWin)
-    const uint32_t w = p[(k >> 1) * kWinPlane];
+    const uint32_t w = p[(k >> 1) * stride];
     return __half2float(__ushort_as_half((unsigned short)((k & 1) ? (w >> 16) : (w & 0xFFFFu))));
   }
 };
@@ -501,8 +503,46 @@ __device__ __forceinline__ int defer_pixel(Deferred* defer, unsigned* defer_coun
   return INT_MIN;
 }
 
+// ---- re-pick certificates ----
+// A re-pick that proves its pick b the strict first minimum also proves it for
+// every later smoothed d' in an interval around its d: the candidate set is
+// fixed while ceil(d' - 5) and floor(d' + 5) (with the [lo, hi] clamps) are,
+// and a candidate c's cost gap to b is linear in d',
+//   gap_c(d') = gap_c(d) - 2 eta (c - b) (d' - d)     (real arithmetic),
+// because the match costs M_c do not depend on d. With a rigorous lower bound
+// on every gap_c(d) (the filter's error bars, a safety term that covers the
+// FP32 evaluation and the reference's own double roundings) the interval on
+// which every gap stays positive is stored per pixel (float, rounded inward);
+// a later iteration whose d' falls inside it keeps o = b without re-scoring.
+// An empty interval (lo > hi) means "always re-pick".
+__device__ __forceinline__ float2 iv_empty() { return make_float2(INFINITY, -INFINITY); }
+
+// [dv + dn, dv + up] intersected with the candidate-set cells, rounded inward.
+__device__ __forceinline__ float2 iv_finish(const RefineArgs& a, double dv, double dn, double up,
+                                            int c_lo, int c_hi) {
+  constexpr double m = 1e-9;  // >> ulp(|d| <= 2^10) / 2: RN(d' -+ 5) stays in the cell
+  double lo = dv + dn, hi = dv + up;
+  const double cl = ceil(a.lo), fh = floor(a.hi);
+  if ((double)c_lo > cl) {  // c_lo = ceil(RN(d - 5)): c_lo - 1 < d' - 5 <= c_lo
+    lo = fmax(lo, (double)c_lo + 4.0 + m);
+    hi = fmin(hi, (double)c_lo + 5.0);
+  } else {  // clamped at ceil(lo): d' - 5 <= ceil(lo)
+    hi = fmin(hi, cl + 5.0);
+  }
+  if ((double)c_hi < fh) {  // c_hi = floor(RN(d + 5)): c_hi <= d' + 5 < c_hi + 1
+    lo = fmax(lo, (double)c_hi - 5.0);
+    hi = fmin(hi, (double)c_hi - 4.0 - m);
+  } else {  // clamped at floor(hi): d' + 5 >= floor(hi)
+    lo = fmax(lo, fh - 5.0);
+  }
+  if (!(lo <= hi)) return iv_empty();
+  return make_float2(__double2float_ru(lo), __double2float_rd(hi));
+}
+
 // Re-pick of one pixel (smoothing.cpp:119-144) given its smoothed d.
-// Returns the new o, or INT_MIN when the pixel is deferred to the exact kernel.
+// Returns the new o, or INT_MIN: not found (dmask = 0, unreachable for a
+// clamped d) or to be settled exactly (dmask = the candidates c_lo + k to
+// score, dclo = c_lo). iv (optional) receives the pick's certificate interval.
 //
 // Filter error budget: window entries are fp16 match
 // costs M16 from the FP32 sweep score s_f (|s_f - s| <= 5 ulp_f32) with
@@ -512,11 +552,14 @@ __device__ __forceinline__ int defer_pixel(Deferred* defer, unsigned* defer_coun
 // reference's argmin.
 __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double dv,
                                       const uint8_t* L, const uint8_t* R, bool has_win,
-                                      const WinView& wv, int wb, long pix, Deferred* defer,
-                                      unsigned* defer_count) {
+                                      const WinView& wv, int wb, int& dclo, int& dmask,
+                                      float2* iv) {
   const int W = a.g.W, H = a.g.H, half = a.g.half;
   const int c_lo = max((int)ceil(__dsub_rn(dv, (double)kRefineR)), (int)ceil(a.lo));
   const int c_hi = min((int)floor(__dadd_rn(dv, (double)kRefineR)), (int)floor(a.hi));
+  dclo = c_lo;
+  dmask = 0;
+  if (iv) *iv = iv_empty();
   if (c_lo > c_hi) return INT_MIN;  // unreachable for a clamped d; mirrors `found`
   const bool fits = u >= half && u < W - half && v >= half && v < H - half;
 
@@ -547,6 +590,23 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
         best = c;
       }
     }
+    if (iv) {
+      // exact reference costs: the gaps are known up to the reference's
+      // roundings (~1e-13 at cost 1000)
+      double dn = -INFINITY, up = INFINITY;
+      bool ok = true;
+      for (int c = c_lo; c <= c_hi; ++c) {
+        if (c == best) continue;
+        const double diff = __dsub_rn((double)c, dv);
+        const double cost = __dadd_rn(m, __dmul_rn(__dmul_rn(a.eta, diff), diff));
+        const double gap = cost - best_cost - 1e-9 * (1.0 + fabs(best_cost));
+        ok = ok && gap > 0.0;
+        const double sl = 2.0 * a.eta * (double)(c - best);
+        if (sl > 0.0) up = fmin(up, gap / sl * (1.0 - 1e-9));
+        else if (sl < 0.0) dn = fmax(dn, gap / sl * (1.0 - 1e-9));
+      }
+      if (ok) *iv = iv_finish(a, dv, dn, up, c_lo, c_hi);
+    }
     return best;
   }
   int best = c_lo;
@@ -566,7 +626,7 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
     const int off = c_lo - wb, par = off & 1, w0 = off >> 1;
     uint32_t wd[6];
 #pragma unroll
-    for (int i = 0; i < 6; ++i) wd[i] = wv.p[min(w0 + i, kWin / 2 - 1) * kWinPlane];
+    for (int i = 0; i < 6; ++i) wd[i] = wv.p[min(w0 + i, kWin / 2 - 1) * wv.stride];
     const unsigned sel_e = par ? 0x3232u : 0x1010u, sel_o = par ? 0x5454u : 0x3232u;
     // Branch-free over the 11 slots: slots past c_hi cost +inf. The FMA
     // rounds once where M16 + (eta df) df rounded twice, inside the same bar.
@@ -605,7 +665,29 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
       best = ck < best_cost ? c_lo + k : best;
       best_cost = fminf(best_cost, ck);
     }
-    if (second * (1.f - kEps) - errE > best_cost * (1.f + kEps) + errE) return best;
+    const float ub = best_cost * (1.f + kEps) + errE;
+    if (second * (1.f - kEps) - errE > ub) {
+      if (iv) {
+        // gap_c(d) >= (cost_c (1 - eps) - errE) - ub, less 4e-6 (cost_c +
+        // cost_b) for the FP32 evaluation of that bound and the reference's
+        // double roundings; slopes from eta_f shrunk by 1e-4 relative.
+        const int kb = best - c_lo;
+        float dn = -INFINITY, up = INFINITY;
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < kMaxCand; ++k) {
+          if (k > nk || k == kb) continue;
+          const float gap = (cost[k] * (1.f - kEps) - errE) - ub - 4e-6f * (cost[k] + best_cost);
+          ok = ok && gap > 0.f;
+          const float sl = 2.f * a.eta_f * (float)(k - kb);
+          const float t = __fdiv_rn(gap, sl) * 0.9999f;
+          if (sl > 0.f) up = fminf(up, t);
+          else if (sl < 0.f) dn = fmaxf(dn, t);
+        }
+        if (ok) *iv = iv_finish(a, dv, (double)dn, (double)up, c_lo, c_hi);
+      }
+      return best;
+    }
     // Ambiguous: FP64 costs (exact E, exact clamped/undefined M) with error
     // bars on the fp16-derived M only.
     double bc = INFINITY, up = INFINITY;
@@ -630,10 +712,12 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
     // A single survivor, or survivors whose costs are all reference-exact
     // doubles (first minimum already taken), is the reference's pick.
     if (__popc(mask) == 1 || approx == 0) return best;
-    return defer_pixel(defer, defer_count, pix, c_lo, mask, dv);
+    dmask = mask;
+    return INT_MIN;
   }
   // Window miss: score every candidate exactly.
-  return defer_pixel(defer, defer_count, pix, c_lo, (1 << (c_hi - c_lo + 1)) - 1, dv);
+  dmask = (1 << (c_hi - c_lo + 1)) - 1;
+  return INT_MIN;
 }
 
 }  // namespace
@@ -719,7 +803,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int cnk = s_cnt[slot];
     const int olk = USE_SO ? s_o[slot] : 0;
     const int wbk = win ? s_wb[slot] : kNoWin;
-    const WinView wv{planes + slot};
+    const WinView wv{planes + slot, kWinPlane};
     const double s = disc_sum_any<RF>(P, a.span, W, H, u, v, R);
     const double c = (double)cnk;
     const double bav = __ddiv_rn(s, c);
@@ -733,8 +817,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_wait(&bar_win, 0);
       win_ready = true;
     }
-    const int best = repick(a, u, v, dv, L, Rg, win != nullptr, wv, wbk, px, defer + f * bs,
-                            defer_count + f);
+    int dclo, dmask;
+    int best = repick(a, u, v, dv, L, Rg, win != nullptr, wv, wbk, dclo, dmask, nullptr);
+    if (best == INT_MIN && dmask)
+      best = defer_pixel(defer + f * bs, defer_count + f, px, dclo, dmask, dv);
     if (best != INT_MIN) {
       if (!USE_SO) {
         oT[bi] = best;
@@ -779,6 +865,246 @@ void launch_d_repick(const double* psumT, const uint8_t* mT, const int* cntT,
     else k_d_repick<0, true><<<grid, bl, smem, s>>>(SS_REPICK_ARGS, map, tile ? 0 : 1);
   }
 #undef SS_REPICK_ARGS
+}
+
+// ---- certified path (window 11, radius 15 tile): gather + listed re-picks ----
+//
+// k_d_gather: the b-disc gather, d = clamp(avg - avg(b)) stored for every
+// masked pixel, and the pixel listed for a re-pick unless d falls inside its
+// certificate interval (iteration 0: every masked pixel). k_repick_list: one
+// thread per listed pixel (score window read from the global BT planes), the
+// interval of the new pick stored, exact settles done by the whole warp
+// in place (no deferred list, no extra launch).
+template <bool USE_SO>
+__global__ void __launch_bounds__(kThreads, 3)
+    k_d_gather(const double* __restrict__ psumT, const uint8_t* __restrict__ mT,
+               const int* __restrict__ cntT, const double* __restrict__ avgT,
+               const int* __restrict__ soT, const float2* __restrict__ ivT,
+               double* __restrict__ dT, int* __restrict__ list, unsigned* __restrict__ list_count,
+               RefineArgs a, const __grid_constant__ CUtensorMap map) {
+  constexpr int RF = 15;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar;
+  const long f = blockIdx.z;
+  const int W = a.g.W, H = a.g.H;
+  const long bs = bt_frame(W, H, 0);
+  const int lane = threadIdx.x, warp = threadIdx.y;
+  const int v = blockIdx.y * 32 + lane;
+  const int u0 = blockIdx.x * kTC, rb = blockIdx.y;
+  const int ncols = min(kTC, W - u0);
+  const unsigned npx = ncols * 32;
+  const long e0 = f * bs + ((long)rb * W + u0) * 32;
+  const size_t tb = tile_bytes<double>(RF);
+  double* s_av = reinterpret_cast<double*>(smem + tb);
+  int* s_so = reinterpret_cast<int*>(s_av);
+  float2* s_iv = reinterpret_cast<float2*>(s_av + kTilePx);
+  int* s_cnt = reinterpret_cast<int*>(s_iv + kTilePx);
+  uint8_t* s_m = reinterpret_cast<uint8_t*>(s_cnt + kTilePx);
+  const unsigned extra = npx * (USE_SO ? 4 + 8 : 8) + npx * 4 + npx;
+  const Tile<double> P = tile_issue<RF>(reinterpret_cast<double*>(smem),
+                                        psumT + f * bt_frame(W, H, 1 + RF), &map, W, RF, false,
+                                        &bar, extra);
+  if (lane == 0 && warp == 0) {
+    if (USE_SO) {
+      bulk_g2s(s_so, soT + e0, npx * 4, &bar);
+      bulk_g2s(s_iv, ivT + e0, npx * 8, &bar);
+    } else {
+      bulk_g2s(s_av, avgT + e0, npx * 8, &bar);
+    }
+    bulk_g2s(s_cnt, cntT + e0, npx * 4, &bar);
+    bulk_g2s(s_m, mT + e0, npx, &bar);
+  }
+  tile_wait(&bar);
+#pragma unroll 1
+  for (int k = 0; k < kPX; ++k) {
+    const int t = warp + kTWarps * k;  // tile column (warp-uniform)
+    if (t >= ncols) break;
+    const int slot = t * 32 + lane;
+    const int u = u0 + t;
+    const long px = ((long)rb * W + u) * 32 + lane;
+    bool need = false;
+    if (v < H && s_m[slot]) {
+      const double s = disc_sum_any<RF>(P, a.span, W, H, u, v, RF);
+      const double c = (double)s_cnt[slot];
+      const double bav = __ddiv_rn(s, c);
+      const double a_o = USE_SO ? __ddiv_rn((double)s_so[slot], c) : s_av[slot];
+      const double x = __dsub_rn(a_o, bav);
+      const double dv = x < a.lo ? a.lo : (a.hi < x ? a.hi : x);  // std::clamp
+      dT[f * bs + px] = dv;
+      if (USE_SO) {
+        const float2 iv = s_iv[slot];
+        need = !((double)iv.x <= dv && dv <= (double)iv.y);
+      }
+    }
+    // iteration 0 re-picks every masked pixel: the list kernel walks the mask
+    if (USE_SO) warp_append(list + f * bs, list_count + f, need, (int)px);
+  }
+}
+
+template <bool USE_SO>
+__global__ void __launch_bounds__(256)
+    k_repick_list(const int* __restrict__ list, const unsigned* __restrict__ list_count,
+                  const uint8_t* __restrict__ mT, const double* __restrict__ dT,
+                  int* __restrict__ oT,
+                  const uint8_t* __restrict__ lgray, const uint8_t* __restrict__ rgray,
+                  const wscore_t* __restrict__ win, const int* __restrict__ wbase,
+                  float2* __restrict__ ivT, int2* __restrict__ chg, unsigned* __restrict__ chg_count,
+                  RefineArgs a, long gray_stride, unsigned long long* __restrict__ counters) {
+  const long f = blockIdx.y;
+  const int W = a.g.W, H = a.g.H, half = a.g.half;
+  const long bs = bt_frame(W, H, 0);
+  // list == nullptr (iteration 0): every masked pixel, in BT order
+  const unsigned n = list ? list_count[f] : (unsigned)bs;
+  const int lane = threadIdx.x & 31;
+  const uint8_t* L = lgray + f * gray_stride;
+  const uint8_t* R = rgray + f * gray_stride;
+  const uint32_t* wplanes = reinterpret_cast<const uint32_t*>(win) + f * bs * (kWin / 2);
+  const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
+  unsigned n_exact = 0, n_scored = 0;
+  for (unsigned w0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; w0 < n;
+       w0 += nwarps * 32) {
+    const unsigned i = w0 + lane;
+    bool act = i < n;
+    int px = 0;
+    if (list) {
+      if (act) px = list[f * bs + i];
+    } else {
+      px = (int)i;
+      act = act && mT[f * bs + i];
+    }
+    n_scored += __popc(__ballot_sync(0xffffffffu, act));
+    int v, u;
+    bt_decode(W, px, v, u);
+    const long bi = f * bs + px;
+    int best = INT_MIN, dclo = 0, dmask = 0, old = 0;
+    float2 iv = iv_empty();
+    double dv = 0.0;
+    if (act) {
+      dv = dT[bi];
+      if (USE_SO) old = oT[bi];
+      const WinView wv{wplanes + win_word(W, v, u, 0), (long)W * 32};
+      best = repick(a, u, v, dv, L, R, true, wv, wbase[bi], dclo, dmask, &iv);
+    }
+    // exact settles: the whole warp scores one pixel's candidates (lane k:
+    // c_lo + k) and takes the first minimum, as smoothing.cpp:138 does
+    unsigned pend = __ballot_sync(0xffffffffu, act && best == INT_MIN && dmask != 0);
+    n_exact += __popc(pend);
+    while (pend) {
+      const int src = __ffs(pend) - 1;
+      pend &= pend - 1;
+      const int pu = __shfl_sync(0xffffffffu, u, src), pv = __shfl_sync(0xffffffffu, v, src);
+      const int pc = __shfl_sync(0xffffffffu, dclo, src);
+      const double pd = __shfl_sync(0xffffffffu, dv, src);
+      // every candidate is scored (the lanes run in parallel anyway), so the
+      // pick's certificate comes out of the same costs
+      const int pch = min((int)floor(__dadd_rn(pd, (double)kRefineR)), (int)floor(a.hi));
+      const int pm = (1 << (pch - pc + 1)) - 1;
+      const bool fits = pu >= half && pu < W - half && pv >= half && pv < H - half;
+      const bool mine = lane < kMaxCand && ((pm >> lane) & 1);
+      double mycost = INFINITY;
+      if (mine) mycost = exact_cost(L, R, W, pu, pv, pc + lane, fits, half, pd, a.eta);
+      double cost = mycost;
+      int k = mine ? lane : 64;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double oc = __shfl_down_sync(0xffffffffu, cost, o);
+        const int ok = __shfl_down_sync(0xffffffffu, k, o);
+        if (oc < cost || (oc == cost && ok < k)) {
+          cost = oc;
+          k = ok;
+        }
+      }
+      k = __shfl_sync(0xffffffffu, k, 0);
+      // The reference's own costs of every candidate: the pick's certificate
+      // interval follows as on the exact no-window path (gaps known to the
+      // reference's roundings).
+      float2 piv = iv_empty();
+      if (k < 64) {
+        const double cb = __shfl_sync(0xffffffffu, mycost, k);
+        double up = INFINITY, dn = -INFINITY;
+        bool ok = true;
+        if (mine && lane != k) {
+          const double gap = mycost - cb - 1e-9 * (1.0 + fabs(cb));
+          ok = gap > 0.0;
+          const double sl = 2.0 * a.eta * (double)(lane - k);
+          if (sl > 0.0) up = gap / sl * (1.0 - 1e-9);
+          else if (sl < 0.0) dn = gap / sl * (1.0 - 1e-9);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          up = fmin(up, __shfl_xor_sync(0xffffffffu, up, o));
+          dn = fmax(dn, __shfl_xor_sync(0xffffffffu, dn, o));
+        }
+        if (__all_sync(0xffffffffu, ok)) piv = iv_finish(a, pd, dn, up, pc, pch);
+      }
+      if (lane == src && k < 64) {
+        best = pc + k;
+        iv = piv;
+      }
+    }
+    if (act) {
+      ivT[bi] = iv;
+      if (best != INT_MIN) {
+        if (!USE_SO) {
+          oT[bi] = best;
+        } else if (best != old) {
+          chg[f * bs + atomicAdd(chg_count + f, 1u)] = make_int2(px, best - old);
+          oT[bi] = best;
+        }
+      }
+    }
+  }
+  if (counters && lane == 0 && n_exact) atomicAdd(counters, (unsigned long long)n_exact);
+  // counters[1] (ctx counter 2): (pixel, iteration) re-picks scored (the rest were certified)
+  if (counters && lane == 0 && n_scored) atomicAdd(counters + 1, (unsigned long long)n_scored);
+}
+
+bool certified_repick_ok(const RefineArgs& a, bool has_win) {
+  return has_win && a.radius == 15 &&
+         use_tile<double>(15, (size_t)kTilePx * (8 + 8 + 4 + 1));
+}
+
+void launch_d_gather(const double* psumT, const uint8_t* mT, const int* cntT, const double* avgT,
+                     const int* soT, const float2* ivT, double* dT, int* list,
+                     unsigned* list_count, const RefineArgs& a, int frames, cudaStream_t s) {
+  if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
+  CUtensorMap map;
+  if (!psum_map(&map, psumT, a, frames, true))
+    throw std::runtime_error("k_d_gather: TMA tensor map rejected");
+  const size_t smem = tile_bytes<double>(15) + (size_t)kTilePx * (8 + 8 + 4 + 1);
+  static bool configured = false;
+  if (!configured) {
+    set_smem(k_d_gather<false>, smem);
+    set_smem(k_d_gather<true>, smem);
+    configured = true;
+  }
+  dim3 grid((a.g.W + kTC - 1) / kTC, (a.g.H + 31) / 32, frames);
+  dim3 bl(32, kTWarps);
+  if (avgT) k_d_gather<false><<<grid, bl, smem, s>>>(psumT, mT, cntT, avgT, soT, ivT, dT, list,
+                                                    list_count, a, map);
+  else k_d_gather<true><<<grid, bl, smem, s>>>(psumT, mT, cntT, avgT, soT, ivT, dT, list,
+                                              list_count, a, map);
+}
+
+void launch_repick_list(const int* list, const unsigned* list_count, const uint8_t* mT,
+                        const double* dT, int* oT,
+                        const uint8_t* lgray, const uint8_t* rgray, const wscore_t* win,
+                        const int* wbase, float2* ivT, int2* chg, unsigned* chg_count,
+                        const RefineArgs& a, int frames, long gray_stride, bool all_pixels,
+                        unsigned long long* counters, cudaStream_t s) {
+  if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
+  // all_pixels (iteration 0, list == nullptr): the whole mask; later lists
+  // hold a few percent of it
+  const int blocks = all_pixels ? 4 * 148 : 148;
+  if (all_pixels) list = nullptr;
+  if (chg)
+    k_repick_list<true><<<dim3(blocks, frames), 256, 0, s>>>(list, list_count, mT, dT, oT,
+                                                             lgray, rgray, win, wbase, ivT, chg,
+                                                             chg_count, a, gray_stride, counters);
+  else
+    k_repick_list<false><<<dim3(blocks, frames), 256, 0, s>>>(list, list_count, mT, dT, oT,
+                                                              lgray, rgray, win, wbase, ivT, chg,
+                                                              chg_count, a, gray_stride, counters);
 }
 
 // Deferred re-picks: one warp per pixel, lane k scores candidate c_lo + k in

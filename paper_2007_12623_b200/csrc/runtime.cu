@@ -114,7 +114,8 @@ struct DevBuf {
 long round_up(long x, long m) { return (x + m - 1) / m * m; }
 
 // device counters: 0 WTA exact resolves, 1 refine exact re-picks, 2 refine
-// fallbacks, 4 disc-filled pixels
+// re-picks scored (certified path; the others kept their certified pick),
+// 4 disc-filled pixels
 constexpr int kNumCounters = 8;
 
 void validate_params(const ss_stereo_params* p) {
@@ -201,6 +202,7 @@ struct ss_ctx {
   DevBuf index, block_sums, npoints, pts_f, nrm_f, nrm_o, colors, pts_d, nrm_d, pixels, pts4,
       fitted;
   DevBuf counters, trace_o, trace_d, so, chg, chg_count, mbt, defer, defer_count, fmeta;
+  DevBuf ivb, rlist;  // certified re-picks: per-pixel intervals (float2 BT), re-pick list
   int n_sm = 148;
   int wtab_radius = -1, span_radius = -1;
   std::vector<double> wtab_host;
@@ -262,7 +264,7 @@ struct ss_ctx {
                       &disp_a, &disp_b, &valid_a, &valid_b, &flags, &flag_count, &o, &d, &avg,
                       &b, &psum, &pcnt, &cnt, &span, &wtab, &fspan, &fx, &emap, &index, &block_sums, &npoints,
                       &pts_f, &nrm_f, &nrm_o, &colors, &pts_d, &nrm_d, &pixels, &pts4, &fitted, &counters, &oi, &trace_o,
-                      &trace_d, &so, &chg, &chg_count, &mbt, &defer, &defer_count, &fmeta, &gray_fl,
+                      &trace_d, &so, &chg, &chg_count, &ivb, &rlist, &mbt, &defer, &defer_count, &fmeta, &gray_fl,
                       &gray_fr, &disp_r, &valid_r})
       b->release();
     for (DevBuf& b : fe) b.release();
@@ -608,7 +610,6 @@ struct ss_ctx {
     stats.kernel_launches += 3;
     so.ensure(sizeof(int) * bs * n);
     chg.ensure(sizeof(int2) * bs * n);
-    chg_count.ensure(sizeof(unsigned) * n);
     const wscore_t* winp = nullptr;
     if (fix_windows) {
       launch_window_build(disp_a.as<float>(), gray_l.as<uint8_t>(), gray_r.as<uint8_t>(),
@@ -620,7 +621,26 @@ struct ss_ctx {
     }
     defer.ensure(sizeof(Deferred) * bs * n);
     defer_count.ensure(sizeof(unsigned) * n);
+    // Certified path (window 11, radius 15): gather + listed re-picks, each
+    // pick's certificate interval kept in ivb across iterations.
+    const bool cert = winp != nullptr && certified_repick_ok(a, true);
+    if (cert) {
+      ivb.ensure(sizeof(float2) * bs * n);
+      rlist.ensure(sizeof(int) * bs * n);
+    }
+    chg_count.ensure(sizeof(unsigned) * 2 * n);  // [chg counts][re-pick list counts]
+    unsigned* lcount = chg_count.as<unsigned>() + n;
     auto repick = [&](const double* avgp, int2* chgp, unsigned* chgc) {
+      if (cert) {
+        Stage sp(this, 11);
+        launch_d_gather(psum.as<double>(), mT, cnt.as<int>(), avgp, so.as<int>(),
+                        ivb.as<float2>(), d.as<double>(), rlist.as<int>(), lcount, a, n, stream);
+        launch_repick_list(rlist.as<int>(), lcount, mT, d.as<double>(), op, gray_l.as<uint8_t>(),
+                           gray_r.as<uint8_t>(), winp, wbase.as<int>(), ivb.as<float2>(), chgp,
+                           chgc, a, n, N, avgp != nullptr, ctr() + 1, stream);
+        stats.kernel_launches += 2;
+        return;
+      }
       ck(cudaMemsetAsync(defer_count.p, 0, sizeof(unsigned) * n, stream), "memset");
       {
       Stage sp(this, 11);
@@ -660,7 +680,8 @@ struct ss_ctx {
           stats.kernel_launches += 2;
         }
       } else {
-        ck(cudaMemsetAsync(chg_count.p, 0, sizeof(unsigned) * n, stream), "memset");
+        ck(cudaMemsetAsync(chg_count.p, 0, sizeof(unsigned) * (cert ? 2 : 1) * n, stream),
+           "memset");
         {
           Stage ss(this, 10);
           launch_scan_b(so.as<int>(), cnt.as<int>(), op, d.as<double>(), mT, a.alpha,
@@ -1495,7 +1516,7 @@ ss_status ss_ctx_get_stats(ss_ctx* ctx, ss_ctx_stats* st) {
     *st = ctx->stats;
     st->wta_resolved = (int64_t)c[0];
     st->refine_resolved = (int64_t)c[1];
-    st->refine_fallback = (int64_t)c[2];
+    st->refine_scored = (int64_t)c[2];
     st->disc_fill_pixels = (int64_t)c[4];
   });
 }
