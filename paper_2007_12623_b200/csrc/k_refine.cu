@@ -670,7 +670,9 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
       if (iv) {
         // gap_c(d) >= (cost_c (1 - eps) - errE) - ub, less 4e-6 (cost_c +
         // cost_b) for the FP32 evaluation of that bound and the reference's
-        // double roundings; slopes from eta_f shrunk by 1e-4 relative.
+        // double roundings. gap_c reaches 0 at d' - d = gap_c / (2 eta (c - b)),
+        // formed with approximate reciprocals (rel. error < 1e-6) and shrunk
+        // by 1e-4 relative.
         const int kb = best - c_lo;
         float dn = -INFINITY, up = INFINITY;
         bool ok = true;
@@ -679,10 +681,11 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
           if (k > nk || k == kb) continue;
           const float gap = (cost[k] * (1.f - kEps) - errE) - ub - 4e-6f * (cost[k] + best_cost);
           ok = ok && gap > 0.f;
-          const float sl = 2.f * a.eta_f * (float)(k - kb);
-          const float t = __fdiv_rn(gap, sl) * 0.9999f;
-          if (sl > 0.f) up = fminf(up, t);
-          else if (sl < 0.f) dn = fmaxf(dn, t);
+          float r;
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)(k - kb)));
+          const float t = gap * a.inv2eta_f * r * 0.9999f;
+          if (t > 0.f) up = fminf(up, t);
+          else if (t < 0.f) dn = fmaxf(dn, t);
         }
         if (ok) *iv = iv_finish(a, dv, (double)dn, (double)up, c_lo, c_hi);
       }
@@ -734,7 +737,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                const uint8_t* __restrict__ lgray, const uint8_t* __restrict__ rgray,
                const wscore_t* __restrict__ win, const int* __restrict__ wbase,
                int2* __restrict__ chg, unsigned* __restrict__ chg_count,
-               Deferred* __restrict__ defer, unsigned* __restrict__ defer_count, RefineArgs a,
+               Deferred* __restrict__ defer, unsigned* __restrict__ defer_count,
+               float2* __restrict__ ivT, RefineArgs a,
                long gray_stride, const __grid_constant__ CUtensorMap map, int glob) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar, bar_win;
@@ -818,7 +822,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       win_ready = true;
     }
     int dclo, dmask;
-    int best = repick(a, u, v, dv, L, Rg, win != nullptr, wv, wbk, dclo, dmask, nullptr);
+    float2 iv;
+    int best = repick(a, u, v, dv, L, Rg, win != nullptr, wv, wbk, dclo, dmask,
+                      ivT ? &iv : nullptr);
+    if (ivT) ivT[bi] = iv;  // empty when the pick is deferred
     if (best == INT_MIN && dmask)
       best = defer_pixel(defer + f * bs, defer_count + f, px, dclo, dmask, dv);
     if (best != INT_MIN) {
@@ -838,8 +845,8 @@ void launch_d_repick(const double* psumT, const uint8_t* mT, const int* cntT,
                      const double* avgT, const int* soT, double* dT, int* oT,
                      const uint8_t* lgray, const uint8_t* rgray, const wscore_t* win,
                      const int* wbase, int2* chg, unsigned* chg_count, Deferred* defer,
-                     unsigned* defer_count, const RefineArgs& a, int frames, long gray_stride,
-                     cudaStream_t s) {
+                     unsigned* defer_count, float2* ivT, const RefineArgs& a, int frames,
+                     long gray_stride, cudaStream_t s) {
   if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
   CUtensorMap map;
   const bool tile = psum_map(&map, psumT, a, frames, use_tile<double>(a.radius, kWinSmem + kPxSmem));
@@ -848,7 +855,7 @@ void launch_d_repick(const double* psumT, const uint8_t* mT, const int* cntT,
   dim3 bl(32, kTWarps);
 #define SS_REPICK_ARGS                                                                        \
   psumT, mT, cntT, avgT, soT, dT, oT, lgray, rgray, win, wbase, chg, chg_count, defer,        \
-      defer_count, a, gray_stride
+      defer_count, ivT, a, gray_stride
   if (a.radius == 15 && tile) {
     static bool configured = false;
     if (!configured) {

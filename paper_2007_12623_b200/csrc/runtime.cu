@@ -582,6 +582,7 @@ struct ss_ctx {
     a.one_minus_alpha = 1.0 - params.alpha;
     a.eta = params.eta_smooth;
     a.eta_f = (float)params.eta_smooth;
+    a.inv2eta_f = (float)(1.0 / (2.0 * params.eta_smooth));
     a.lo = params.d_min - kRefineR;
     a.hi = params.d_max + kRefineR;
     a.radius = r;
@@ -631,7 +632,9 @@ struct ss_ctx {
     chg_count.ensure(sizeof(unsigned) * 2 * n);  // [chg counts][re-pick list counts]
     unsigned* lcount = chg_count.as<unsigned>() + n;
     auto repick = [&](const double* avgp, int2* chgp, unsigned* chgc) {
-      if (cert) {
+      // iteration 0 (avgp != nullptr) re-picks every pixel: the fused
+      // gather + re-pick kernel, which also stores the certificates
+      if (cert && !avgp) {
         Stage sp(this, 11);
         launch_d_gather(psum.as<double>(), mT, cnt.as<int>(), avgp, so.as<int>(),
                         ivb.as<float2>(), d.as<double>(), rlist.as<int>(), lcount, a, n, stream);
@@ -646,8 +649,8 @@ struct ss_ctx {
       Stage sp(this, 11);
       launch_d_repick(psum.as<double>(), mT, cnt.as<int>(), avgp, so.as<int>(), d.as<double>(),
                       op, gray_l.as<uint8_t>(), gray_r.as<uint8_t>(), winp, wbase.as<int>(),
-                      chgp, chgc, defer.as<Deferred>(), defer_count.as<unsigned>(), a, n, N,
-                      stream);
+                      chgp, chgc, defer.as<Deferred>(), defer_count.as<unsigned>(),
+                      cert ? ivb.as<float2>() : nullptr, a, n, N, stream);
       stats.kernel_launches += 1;
       }
       Stage sx(this, 12);

@@ -190,6 +190,7 @@ struct RefineArgs {
   Geom g;
   double alpha, one_minus_alpha, eta, lo, hi;
   float eta_f;
+  float inv2eta_f;  // 1 / (2 eta) (+-inf for eta == 0): the certificate slopes
   int radius;       // smoothing_radius
   const int* span;  // [radius + 1]
 };
@@ -284,7 +285,8 @@ void launch_d_repick(const double* psumT, const uint8_t* mT, const int* cntT,
                      const double* avgT, const int* soT, double* dT, int* oT,
                      const uint8_t* lgray, const uint8_t* rgray, const wscore_t* win,
                      const int* wbase, int2* chg, unsigned* chg_count, Deferred* defer,
-                     unsigned* defer_count, const RefineArgs& a, int frames, long gray_stride,
+                     unsigned* defer_count, float2* ivT, const RefineArgs& a, int frames,
+                     long gray_stride,
                      cudaStream_t s);
 void launch_repick_exact(const Deferred* defer, const unsigned* defer_count, int* oT,
                          const uint8_t* lgray, const uint8_t* rgray, int2* chg,
