@@ -553,13 +553,13 @@ __device__ __forceinline__ float2 iv_finish(const RefineArgs& a, double dv, doub
 __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double dv,
                                       const uint8_t* L, const uint8_t* R, bool has_win,
                                       const WinView& wv, int wb, int& dclo, int& dmask,
-                                      float2* iv) {
+                                      float2& iv, bool want_iv) {
   const int W = a.g.W, H = a.g.H, half = a.g.half;
   const int c_lo = max((int)ceil(__dsub_rn(dv, (double)kRefineR)), (int)ceil(a.lo));
   const int c_hi = min((int)floor(__dadd_rn(dv, (double)kRefineR)), (int)floor(a.hi));
   dclo = c_lo;
   dmask = 0;
-  if (iv) *iv = iv_empty();
+  iv = iv_empty();
   if (c_lo > c_hi) return INT_MIN;  // unreachable for a clamped d; mirrors `found`
   const bool fits = u >= half && u < W - half && v >= half && v < H - half;
 
@@ -590,7 +590,7 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
         best = c;
       }
     }
-    if (iv) {
+    if (want_iv) {
       // exact reference costs: the gaps are known up to the reference's
       // roundings (~1e-13 at cost 1000)
       double dn = -INFINITY, up = INFINITY;
@@ -605,7 +605,7 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
         if (sl > 0.0) up = fmin(up, gap / sl * (1.0 - 1e-9));
         else if (sl < 0.0) dn = fmax(dn, gap / sl * (1.0 - 1e-9));
       }
-      if (ok) *iv = iv_finish(a, dv, dn, up, c_lo, c_hi);
+      if (ok) iv = iv_finish(a, dv, dn, up, c_lo, c_hi);
     }
     return best;
   }
@@ -667,7 +667,7 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
     }
     const float ub = best_cost * (1.f + kEps) + errE;
     if (second * (1.f - kEps) - errE > ub) {
-      if (iv) {
+      if (want_iv) {
         // gap_c(d) >= (cost_c (1 - eps) - errE) - ub, less 4e-6 (cost_c +
         // cost_b) for the FP32 evaluation of that bound and the reference's
         // double roundings. gap_c reaches 0 at d' - d = gap_c / (2 eta (c - b)),
@@ -687,7 +687,7 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
           if (t > 0.f) up = fminf(up, t);
           else if (t < 0.f) dn = fmaxf(dn, t);
         }
-        if (ok) *iv = iv_finish(a, dv, (double)dn, (double)up, c_lo, c_hi);
+        if (ok) iv = iv_finish(a, dv, (double)dn, (double)up, c_lo, c_hi);
       }
       return best;
     }
@@ -714,7 +714,29 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
     }
     // A single survivor, or survivors whose costs are all reference-exact
     // doubles (first minimum already taken), is the reference's pick.
-    if (__popc(mask) == 1 || approx == 0) return best;
+    if (__popc(mask) == 1 || approx == 0) {
+      if (want_iv) {
+        // certificate from the same bounds: gap_c >= (cost_c - err_c) -
+        // (cost_b + err_b), less a safety for the double roundings
+        double cb, eb;
+        repick_cost_d(a, u, best, dv, wv, wb, W, half, cb, eb);
+        const double ub = cb + eb;
+        double dn = -INFINITY, upv = INFINITY;
+        bool ok = true;
+        for (int c = c_lo; c <= c_hi; ++c) {
+          if (c == best) continue;
+          double cost, err;
+          repick_cost_d(a, u, c, dv, wv, wb, W, half, cost, err);
+          const double gap = (cost - err) - ub - 1e-9 * (1.0 + fabs(ub));
+          ok = ok && gap > 0.0;
+          const double sl = 2.0 * a.eta * (double)(c - best);
+          if (sl > 0.0) upv = fmin(upv, gap / sl * (1.0 - 1e-9));
+          else if (sl < 0.0) dn = fmax(dn, gap / sl * (1.0 - 1e-9));
+        }
+        if (ok) iv = iv_finish(a, dv, dn, upv, c_lo, c_hi);
+      }
+      return best;
+    }
     dmask = mask;
     return INT_MIN;
   }
@@ -823,8 +845,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     int dclo, dmask;
     float2 iv;
-    int best = repick(a, u, v, dv, L, Rg, win != nullptr, wv, wbk, dclo, dmask,
-                      ivT ? &iv : nullptr);
+    int best = repick(a, u, v, dv, L, Rg, win != nullptr, wv, wbk, dclo, dmask, iv,
+                      ivT != nullptr);
     if (ivT) ivT[bi] = iv;  // empty when the pick is deferred
     if (best == INT_MIN && dmask)
       best = defer_pixel(defer + f * bs, defer_count + f, px, dclo, dmask, dv);
@@ -990,7 +1012,7 @@ __global__ void __launch_bounds__(256)
       dv = dT[bi];
       if (USE_SO) old = oT[bi];
       const WinView wv{wplanes + win_word(W, v, u, 0), (long)W * 32};
-      best = repick(a, u, v, dv, L, R, true, wv, wbase[bi], dclo, dmask, &iv);
+      best = repick(a, u, v, dv, L, R, true, wv, wbase[bi], dclo, dmask, iv, true);
     }
     // exact settles: the whole warp scores one pixel's candidates (lane k:
     // c_lo + k) and takes the first minimum, as smoothing.cpp:138 does
