@@ -411,8 +411,10 @@ def roofline_report(args, stages, frames_timed, n_sm, sm_max, hbm_peak, iters=10
     alu_peak = n_sm * 128 * sm_max * 1e6
     census = {  # lane-ops per frame
         "wta_sweep": ("k_wta11: chessboard ZNCC over [d_min, d_max] + WTA", 15.0 * N * D),
-        "refine_repick": ("k_d_repick: b-disc gather 62N + smoothing 3N + re-pick 60N per "
-                          "iteration", 125.0 * N * iters),
+        "refine_repick": ("k_d_gather + k_repick_list (iteration 0: k_d_repick): b-disc "
+                          "gather 62N + smoothing 3N + re-pick 60N per iteration (re-picks "
+                          "certified unchanged are skipped, their census still counted)",
+                          125.0 * N * iters),
         "cleanup_disc": ("k_row_count/k_disc_select/k_disc_sum: I_disc x (82 + 3 x 1256)",
                          I_DISC[args.workload] * (82 + 3 * 1256)),
         "cleanup_radial": ("k_fill_radial_list: 144N", 144.0 * N),
