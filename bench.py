@@ -72,11 +72,11 @@ WORKLOADS = {
                seed_base=0, scaling="weak", ref_pairs=5,
                desc="C2 (BASELINE.json configs[1]): 256 synthetic low-texture 960x540 pairs per "
                     "GPU per step, D=64, full chain incl. normals"),
-    "c3": dict(kind="textured", W=1920, H=1080, D=128, frames=32, batch=8, streams=2, unique=8,
+    "c3": dict(kind="textured", W=1920, H=1080, D=128, frames=32, batch=4, streams=4, unique=8,
                seed_base=100, scaling="weak", ref_pairs=2,
                desc="C3 (BASELINE.json configs[2]): 32 synthetic textured 1920x1080 stereo pairs "
                     "per GPU per step, D=128 (d 0..127), full chain incl. normals"),
-    "c5": dict(kind="video", W=1920, H=1080, D=128, frames=1024, batch=8, streams=2, unique=32,
+    "c5": dict(kind="video", W=1920, H=1080, D=128, frames=1024, batch=4, streams=4, unique=32,
                seed_base=0, scaling="strong", ref_pairs=2,
                desc="C5 (BASELINE.json configs[4]): 1024-pair 1920x1080 D=128 synthetic video "
                     "stream (32 distinct drifting frames, tiled) split into contiguous frame "
