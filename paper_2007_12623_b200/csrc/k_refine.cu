@@ -373,9 +373,11 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
   for (int k = 0; k < kPX; ++k) {
     const int u = blockIdx.x * kTC + threadIdx.y + kTWarps * k;
-    if (u >= W || v >= H) continue;
+    if (u >= W) continue;
     const long bi = f * bs + bt_index(W, v, u);
-    outT[bi] = mT[bi] ? disc_sum_any<RF>(P, a.span, W, H, u, v, R) : 0;
+    // 0 off the mask and on the padding rows past H: the b scan takes its mask
+    // from the disc counts (cnt > 0)
+    outT[bi] = (v < H && mT[bi]) ? disc_sum_any<RF>(P, a.span, W, H, u, v, R) : 0;
   }
 }
 

@@ -123,10 +123,9 @@ void launch_scan_bt_i(const int* xT, const uint8_t* mT, int* pT, int W, int H, i
 // an exactly-zero round-to-nearest sum is +0.0).
 constexpr int kChunkB = 32;
 constexpr int kScanBWarps = 16;
-struct ScanBRaw {  // [column][row]
+struct ScanBRaw {  // [column][row]; the mask is cnt > 0 (disc counts are 0 off the mask)
   int so[kChunkB][32], cnt[kChunkB][32], o[kChunkB][32];
   double d[kChunkB][32];
-  uint8_t m[kChunkB][32];
 };
 struct ScanBSmem {
   ScanBRaw raw[2];
@@ -152,12 +151,11 @@ __global__ void __launch_bounds__(32 * kScanBWarps)
     const unsigned n = cols * 32;
     ScanBRaw& B = S.raw[k & 1];
     uint64_t* bar = &S.bar[k & 1];
-    mbar_expect_tx(bar, n * (3 * sizeof(int) + sizeof(double) + 1));
+    mbar_expect_tx(bar, n * (3 * sizeof(int) + sizeof(double)));
     bulk_g2s(&B.so[0][0], soT + e0, n * sizeof(int), bar);
     bulk_g2s(&B.cnt[0][0], cntT + e0, n * sizeof(int), bar);
     bulk_g2s(&B.o[0][0], oT + e0, n * sizeof(int), bar);
     bulk_g2s(&B.d[0][0], dT + e0, n * sizeof(double), bar);
-    bulk_g2s(&B.m[0][0], mT + e0, n, bar);
   };
   if (threadIdx.x == 0) {
     mbar_init(&S.bar[0], 1);
@@ -195,7 +193,7 @@ __global__ void __launch_bounds__(32 * kScanBWarps)
       double(*bk)[32] = S.b[k & 1];
       for (int c = warp - 1; c < cols; c += kScanBWarps - 1) {
         double b = 0.0;
-        if (B.m[c][lane]) {
+        if (B.cnt[c][lane] > 0) {
           const double avg = __ddiv_rn((double)B.so[c][lane], (double)B.cnt[c][lane]);
           b = __dsub_rn(__dsub_rn(avg, __dmul_rn(alpha, (double)B.o[c][lane])),
                         __dmul_rn(one_minus_alpha, B.d[c][lane]));
