@@ -990,11 +990,29 @@ __global__ void __launch_bounds__(256)
   const uint8_t* L = lgray + f * gray_stride;
   const uint8_t* R = rgray + f * gray_stride;
   const uint32_t* wplanes = reinterpret_cast<const uint32_t*>(win) + f * bs * (kWin / 2);
-  const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
-  unsigned n_exact = 0, n_scored = 0;
-  for (unsigned w0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; w0 < n;
-       w0 += nwarps * 32) {
-    const unsigned i = w0 + lane;
+  constexpr int kQ = 256;  // block size: one queue entry per thread at most
+  __shared__ int q_px[kQ], q_clo[kQ], q_old[kQ];
+  __shared__ double q_d[kQ];
+  __shared__ unsigned q_n;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned n_scored = 0;
+  auto finalize = [&](long bi, int px, int best, int old, float2 iv) {
+    ivT[bi] = iv;
+    if (best != INT_MIN) {
+      if (!USE_SO) {
+        oT[bi] = best;
+      } else if (best != old) {
+        chg[f * bs + atomicAdd(chg_count + f, 1u)] = make_int2(px, best - old);
+        oT[bi] = best;
+      }
+    }
+  };
+  // block-uniform rounds of blockDim.x entries: the filter per thread, then
+  // the round's exact settles spread over the block's warps
+  for (unsigned b0 = blockIdx.x * blockDim.x; b0 < n; b0 += gridDim.x * blockDim.x) {
+    if (threadIdx.x == 0) q_n = 0;
+    __syncthreads();
+    const unsigned i = b0 + threadIdx.x;
     bool act = i < n;
     int px = 0;
     if (list) {
@@ -1007,27 +1025,35 @@ __global__ void __launch_bounds__(256)
     int v, u;
     bt_decode(W, px, v, u);
     const long bi = f * bs + px;
-    int best = INT_MIN, dclo = 0, dmask = 0, old = 0;
-    float2 iv = iv_empty();
-    double dv = 0.0;
     if (act) {
-      dv = dT[bi];
-      if (USE_SO) old = oT[bi];
+      const double dv = dT[bi];
+      const int old = USE_SO ? oT[bi] : 0;
       const WinView wv{wplanes + win_word(W, v, u, 0), (long)W * 32};
-      best = repick(a, u, v, dv, L, R, true, wv, wbase[bi], dclo, dmask, iv, true);
+      int dclo = 0, dmask = 0;
+      float2 iv;
+      const int best = repick(a, u, v, dv, L, R, true, wv, wbase[bi], dclo, dmask, iv, true);
+      if (best == INT_MIN && dmask != 0) {
+        const unsigned k = atomicAdd(&q_n, 1u);
+        q_px[k] = px;
+        q_clo[k] = dclo;
+        q_old[k] = old;
+        q_d[k] = dv;
+      } else {
+        finalize(bi, px, best, old, iv);
+      }
     }
-    // exact settles: the whole warp scores one pixel's candidates (lane k:
-    // c_lo + k) and takes the first minimum, as smoothing.cpp:138 does
-    unsigned pend = __ballot_sync(0xffffffffu, act && best == INT_MIN && dmask != 0);
-    n_exact += __popc(pend);
-    while (pend) {
-      const int src = __ffs(pend) - 1;
-      pend &= pend - 1;
-      const int pu = __shfl_sync(0xffffffffu, u, src), pv = __shfl_sync(0xffffffffu, v, src);
-      const int pc = __shfl_sync(0xffffffffu, dclo, src);
-      const double pd = __shfl_sync(0xffffffffu, dv, src);
-      // every candidate is scored (the lanes run in parallel anyway), so the
-      // pick's certificate comes out of the same costs
+    __syncthreads();
+    // exact settles: a warp scores one queued pixel's candidates (lane k:
+    // c_lo + k) and takes the first minimum, as smoothing.cpp:138 does;
+    // every candidate is scored (the lanes run in parallel anyway), so the
+    // pick's certificate comes out of the same costs
+    const unsigned nq = q_n;
+    if (counters && threadIdx.x == 0 && nq) atomicAdd(counters, (unsigned long long)nq);
+    for (unsigned q = warp; q < nq; q += nw) {
+      const int qpx = q_px[q], pc = q_clo[q];
+      const double pd = q_d[q];
+      int pv, pu;
+      bt_decode(W, qpx, pv, pu);
       const int pch = min((int)floor(__dadd_rn(pd, (double)kRefineR)), (int)floor(a.hi));
       const int pm = (1 << (pch - pc + 1)) - 1;
       const bool fits = pu >= half && pu < W - half && pv >= half && pv < H - half;
@@ -1068,24 +1094,10 @@ __global__ void __launch_bounds__(256)
         }
         if (__all_sync(0xffffffffu, ok)) piv = iv_finish(a, pd, dn, up, pc, pch);
       }
-      if (lane == src && k < 64) {
-        best = pc + k;
-        iv = piv;
-      }
+      if (lane == 0) finalize(f * bs + qpx, qpx, k < 64 ? pc + k : INT_MIN, q_old[q], piv);
     }
-    if (act) {
-      ivT[bi] = iv;
-      if (best != INT_MIN) {
-        if (!USE_SO) {
-          oT[bi] = best;
-        } else if (best != old) {
-          chg[f * bs + atomicAdd(chg_count + f, 1u)] = make_int2(px, best - old);
-          oT[bi] = best;
-        }
-      }
-    }
+    __syncthreads();  // the queue is reset by the next round
   }
-  if (counters && lane == 0 && n_exact) atomicAdd(counters, (unsigned long long)n_exact);
   // counters[1] (ctx counter 2): (pixel, iteration) re-picks scored (the rest were certified)
   if (counters && lane == 0 && n_scored) atomicAdd(counters + 1, (unsigned long long)n_scored);
 }
