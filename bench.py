@@ -807,6 +807,7 @@ def run_ours(args):
         "e2e": dict({"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                      "d2h_bytes_per_step": d2h, "steps": args.e2e_steps}, **e2e_extra),
         "gpu_launches": int(stats["kernel_launches"]),
+        "graph_launches": int(stats.get("graph_launches", 0)),
         "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
         "clocks": clk.summary(),
         "stage_ms_per_pair": {k: v[0] / F for k, v in stages.items()},

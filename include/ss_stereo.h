@@ -264,6 +264,7 @@ typedef struct ss_ctx_stats {
                                 unchanged (window 11, smoothing radius 15) */
   int64_t kernel_launches;   /* kernels launched by this ctx */
   int64_t disc_fill_pixels;  /* pixels that went through the disc fill (all cleanup rounds) */
+  int64_t graph_launches;    /* batch chains launched as one captured CUDA graph */
 } ss_ctx_stats;
 
 ss_status ss_ctx_create(int32_t device, int32_t max_w, int32_t max_h, int32_t max_batch,

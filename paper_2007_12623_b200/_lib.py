@@ -51,7 +51,8 @@ class SsBatchOut(C.Structure):
 class SsCtxStats(C.Structure):
     _fields_ = [("frames", C.c_int64), ("wta_resolved", C.c_int64),
                 ("refine_resolved", C.c_int64), ("refine_scored", C.c_int64),
-                ("kernel_launches", C.c_int64), ("disc_fill_pixels", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("disc_fill_pixels", C.c_int64),
+                ("graph_launches", C.c_int64)]
 
 
 _lib = None

@@ -16,6 +16,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <cstdlib>
 #include <vector>
 
 #include "ss_internal.cuh"
@@ -260,6 +261,7 @@ struct ss_ctx {
   ss_batch_out last{};
 
   ~ss_ctx() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
     for (DevBuf* b : {&in_l, &in_r, &gray_l, &gray_r, &ltap_buf, &rcopy_buf, &lstat, &rstat, &win, &wbase,
                       &disp_a, &disp_b, &valid_a, &valid_b, &flags, &flag_count, &o, &d, &avg,
                       &b, &psum, &pcnt, &cnt, &span, &wtab, &fspan, &fx, &emap, &index, &block_sums, &npoints,
@@ -761,8 +763,82 @@ struct ss_ctx {
   }
 
   // Whole run_stereo_only chain on device inputs (in_l/in_r hold the frames).
+  // The batch chain (~80 launches) as one CUDA graph: the first call of a
+  // configuration runs directly (buffers sized, tables uploaded); later calls
+  // capture the same launch sequence on the ctx stream, update the cached
+  // executable graph in place (same topology, new pointers / parameters) and
+  // launch it. Stage timing (events) and any capture failure run directly.
+  struct ChainKey {
+    int n, W, H, in_format;
+    uint32_t flags;
+    bool lr;
+    bool operator==(const ChainKey& o) const {
+      return n == o.n && W == o.W && H == o.H && in_format == o.in_format && flags == o.flags &&
+             lr == o.lr;
+    }
+  };
+  bool use_graphs = getenv("SS_NO_GRAPHS") == nullptr;  // SS_NO_GRAPHS=1: direct launches
+  ChainKey graph_key{-1, 0, 0, 0, 0u, false};
+  int graph_key_runs = 0;
+  cudaGraphExec_t graph_exec = nullptr;
+
   void run_chain(int n, int W, int H, int in_format, const uint8_t* dl, const uint8_t* dr,
                  uint32_t flags_out) {
+    const ChainKey key{n, W, H, in_format, flags_out, lr_check};
+    if (!(key == graph_key)) {
+      graph_key = key;
+      graph_key_runs = 0;
+      if (graph_exec) cudaGraphExecDestroy(graph_exec);
+      graph_exec = nullptr;
+    }
+    if (!use_graphs || timing || graph_key_runs++ == 0) {
+      run_chain_direct(n, W, H, in_format, dl, dr, flags_out);
+      return;
+    }
+    ck(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
+    try {
+      run_chain_direct(n, W, H, in_format, dl, dr, flags_out);
+    } catch (...) {
+      // something in the chain does not capture: end the capture, give up on
+      // graphs for this ctx and run the chain directly (which re-raises any
+      // genuine error)
+      cudaGraph_t gr = nullptr;
+      cudaStreamEndCapture(stream, &gr);
+      if (gr) cudaGraphDestroy(gr);
+      cudaGetLastError();
+      use_graphs = false;
+      run_chain_direct(n, W, H, in_format, dl, dr, flags_out);
+      return;
+    }
+    cudaGraph_t gr = nullptr;
+    ck(cudaStreamEndCapture(stream, &gr), "capture");
+    if (graph_exec) {
+      cudaGraphExecUpdateResultInfo info;
+      if (cudaGraphExecUpdate(graph_exec, gr, &info) != cudaSuccess) {
+        cudaGetLastError();
+        cudaGraphExecDestroy(graph_exec);
+        graph_exec = nullptr;
+      }
+    }
+    if (!graph_exec) {
+      const cudaError_t e = cudaGraphInstantiate(&graph_exec, gr, 0);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        graph_exec = nullptr;
+      }
+    }
+    cudaGraphDestroy(gr);
+    if (graph_exec) {
+      ck(cudaGraphLaunch(graph_exec, stream), "graph launch");
+      stats.graph_launches += 1;
+    } else {  // the launches were only recorded: run them now
+      use_graphs = false;
+      run_chain_direct(n, W, H, in_format, dl, dr, flags_out);
+    }
+  }
+
+  void run_chain_direct(int n, int W, int H, int in_format, const uint8_t* dl, const uint8_t* dr,
+                        uint32_t flags_out) {
     if ((flags_out & (SS_OUT_CLOUD | SS_OUT_NORMALS | SS_OUT_NORMALS_OCT)) && !has_rig)
       raise(SS_EINVAL, "stereo batch: cloud output requested but ctx has no rig");
     const Geom g = make_geom(W, H, &params);
