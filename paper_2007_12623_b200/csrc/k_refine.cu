@@ -449,13 +449,14 @@ void launch_avg_b(const double* psumT, const uint8_t* mT, const int* cntT, const
 
 namespace {
 
-// A thread's window: 16 fp16 match costs (m_code) in 8 u32 planes of shared memory.
+// A thread's window: 16 fp16 match costs (m_code: M - 1) in 8 u32 planes.
 struct WinView {
   const uint32_t* p;  // plane 0 word of this pixel; plane j at p[j * stride]
   long stride;        // kWinPlane (shared-memory planes) or W * 32 (global BT planes)
-  __device__ __forceinline__ float mcost(int k) const {  // k in [0, kWin)
+  __device__ __forceinline__ float mcost(int k) const {  // M16 of entry k in [0, kWin)
     const uint32_t w = p[(k >> 1) * stride];
-    return __half2float(__ushort_as_half((unsigned short)((k & 1) ? (w >> 16) : (w & 0xFFFFu))));
+    return 1.f +
+           __half2float(__ushort_as_half((unsigned short)((k & 1) ? (w >> 16) : (w & 0xFFFFu))));
   }
 };
 
@@ -475,12 +476,11 @@ __device__ __forceinline__ double exact_cost(const uint8_t* L, const uint8_t* R,
 constexpr int kMaxCand = 2 * kRefineR + 1;
 
 // FP64 version for the rare paths: exact E (reference expression) and exact M
-// when the score is undefined/clamped (code 1000); err is the fp16 M's
-// uncertainty.
+// when the score is undefined/clamped (code 1000); err bounds the window M16's
+// error (kMA |M16 - 1| + kMB M16, ss_internal.cuh).
 __device__ __forceinline__ void repick_cost_d(const RefineArgs& a, int u, int c, double dv,
                                               const WinView& wv, int wb, int W, int half,
                                               double& cost, double& err) {
-  constexpr double kErrM = 6e-4;
   double m = 1000.0;
   err = 0.0;
   const int ru = u - c;
@@ -488,7 +488,7 @@ __device__ __forceinline__ void repick_cost_d(const RefineArgs& a, int u, int c,
     const float mf = wv.mcost(c - wb);
     if (mf != 1000.f) {
       m = (double)mf;
-      err = kErrM * mf;
+      err = (double)kMA * fabs((double)mf - 1.0) + (double)kMB * (double)mf;
     }
   }
   const double diff = __dsub_rn((double)c, dv);
@@ -614,15 +614,13 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
   int best = c_lo;
   if (c_lo >= wb && c_hi <= wb + kWin - 1) {
     // Common path, FP32. cost_f(c) = M16 + E_f with |cost_f - cost| <=
-    // eps cost + errE, eps = 6e-4 (fp16 M) + 1.2e-7 (FP32 sum),
-    // errE from the FP32 copy of d. The first minimum is certified when the
-    // runner-up's lower bound stays above the minimum's upper bound.
+    // err_c = kMA |M16 - 1| + kMB M16 (the window's M, ss_internal.cuh) +
+    // 2.4e-7 |cost_f| (the FMA's rounding and that of the bounds) + errE (the
+    // FP32 copy of d and E's roundings). The first minimum b is certified
+    // when every other candidate's lower bound stays above b's upper bound.
     const float dv_f = (float)dv;
     const float delta = fabsf(dv_f) * 1.2e-7f;  // |dv_f - d|, and FP32 rounding of c - dv_f
-    constexpr float kEps = 6e-4f + 1.2e-7f;
-    // (with eta < 0, E < 0 and the M error, relative to M, is bounded via |E| <= 25|eta|)
-    const float errE =
-        fabsf(a.eta_f) * (11.f * delta + 25.f * 4e-7f + (a.eta_f < 0.f ? 25.f * kEps : 0.f));
+    const float errE = fabsf(a.eta_f) * (11.f * delta + 25.f * 4e-7f);
     // The <= 11 candidates are entries off .. off+10 of the window: 6 words
     // from the planes, then one byte-permute per candidate.
     const int off = c_lo - wb, par = off & 1, w0 = off >> 1;
@@ -632,56 +630,65 @@ __device__ __forceinline__ int repick(const RefineArgs& a, int u, int v, double 
     const unsigned sel_e = par ? 0x3232u : 0x1010u, sel_o = par ? 0x5454u : 0x3232u;
     // Branch-free over the 11 slots: slots past c_hi cost +inf. The FMA
     // rounds once where M16 + (eta df) df rounded twice, inside the same bar.
-    float best_cost = INFINITY, second = INFINITY;
     const int nk = c_hi - c_lo;
     // Candidate costs two at a time on the packed FP32 pipe (FADD2 / FMUL2 /
     // FFMA2: per-lane IEEE ops, the same values as the scalar expressions
-    // (c - dv_f) and fma(eta df, df, M16)).
-    float cost[kMaxCand + 1];
+    // 1 + h, (c - dv_f) and fma(eta df, df, M16)).
+    float cost[kMaxCand + 1], errk[kMaxCand + 1];
     const float cf = (float)c_lo;
 #pragma unroll
     for (int k = 0; k < kMaxCand; k += 2) {
-      float mk[2];
+      float hk[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int kk = k + h;
         if (kk >= kMaxCand) {
-          mk[h] = 0.f;
+          hk[h] = 0.f;
           continue;
         }
         const uint32_t hw = (kk & 1) ? __byte_perm(wd[kk >> 1], wd[min(kk + 1, 11) >> 1], sel_o)
                                      : __byte_perm(wd[kk >> 1], 0u, sel_e);
-        mk[h] = __half2float(__ushort_as_half((unsigned short)(hw & 0xFFFFu)));
+        hk[h] = __half2float(__ushort_as_half((unsigned short)(hw & 0xFFFFu)));
       }
+      const float2 m16 = __fadd2_rn(make_float2(hk[0], hk[1]), make_float2(1.f, 1.f));  // exact
       const float2 c2 = __fadd2_rn(make_float2(cf, cf), make_float2((float)k, (float)(k + 1)));
       const float2 df = __fadd2_rn(c2, make_float2(-dv_f, -dv_f));
       const float2 e = __fmul2_rn(make_float2(a.eta_f, a.eta_f), df);
-      const float2 c = __ffma2_rn(e, df, make_float2(mk[0], mk[1]));
+      const float2 c = __ffma2_rn(e, df, m16);
       cost[k] = c.x;
       cost[k + 1] = c.y;
+      errk[k] = kMA * fabsf(hk[0]) + kMB * m16.x + 2.4e-7f * fabsf(c.x) + errE;
+      errk[k + 1] = kMA * fabsf(hk[1]) + kMB * m16.y + 2.4e-7f * fabsf(c.y) + errE;
     }
+    float best_cost = INFINITY, best_err = 0.f;
 #pragma unroll
     for (int k = 0; k < kMaxCand; ++k) {
       const float ck = k <= nk ? cost[k] : INFINITY;
-      second = fminf(second, fmaxf(best_cost, ck));
-      best = ck < best_cost ? c_lo + k : best;
+      const bool take = ck < best_cost;
+      best = take ? c_lo + k : best;
+      best_err = take ? errk[k] : best_err;
       best_cost = fminf(best_cost, ck);
     }
-    const float ub = best_cost * (1.f + kEps) + errE;
-    if (second * (1.f - kEps) - errE > ub) {
+    const int kb = best - c_lo;
+    const float ub = best_cost + best_err;
+    float lo_min = INFINITY;
+#pragma unroll
+    for (int k = 0; k < kMaxCand; ++k)
+      if (k <= nk && k != kb) lo_min = fminf(lo_min, cost[k] - errk[k]);
+    if (lo_min > ub) {
       if (want_iv) {
-        // gap_c(d) >= (cost_c (1 - eps) - errE) - ub, less 4e-6 (cost_c +
-        // cost_b) for the FP32 evaluation of that bound and the reference's
-        // double roundings. gap_c reaches 0 at d' - d = gap_c / (2 eta (c - b)),
+        // gap_c(d) >= (cost_c - err_c) - ub, less 4e-6 (|cost_c| + |cost_b|)
+        // for the FP32 evaluation of that bound and the reference's double
+        // roundings. gap_c reaches 0 at d' - d = gap_c / (2 eta (c - b)),
         // formed with approximate reciprocals (rel. error < 1e-6) and shrunk
         // by 1e-4 relative.
-        const int kb = best - c_lo;
         float dn = -INFINITY, up = INFINITY;
         bool ok = true;
 #pragma unroll
         for (int k = 0; k < kMaxCand; ++k) {
           if (k > nk || k == kb) continue;
-          const float gap = (cost[k] * (1.f - kEps) - errE) - ub - 4e-6f * (cost[k] + best_cost);
+          const float gap =
+              (cost[k] - errk[k]) - ub - 4e-6f * (fabsf(cost[k]) + fabsf(best_cost));
           ok = ok && gap > 0.f;
           float r;
           asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)(k - kb)));

@@ -30,24 +30,29 @@ constexpr int kRefineR = 5;    // kRefineSearchRadius (params.hpp:38)
 constexpr double kZnccEps = 1e-3;  // kZnccCostEpsilon (params.hpp:34)
 constexpr int kWin = 16;           // candidate window per pixel for the refinement
 // Window entries hold the re-pick's match cost M = 1/max(s, kZnccCostEpsilon)
-// as fp16 (32 B per pixel): exactly 1000 (= 1/1e-3 in double) when the score
-// is undefined or certainly clamped (s_f < 0.99e-3), otherwise
-// fp16(1/max(s_f, 1e-3)) capped at 999.5, so the code 1000 always means
-// "exact". |M16 - M| <= 5.01e-4 M (fp16 rounding, the cap, the FP32 score's
-// 5-ulp error): the re-pick filter's budget uses 6e-4.
+// (>= 1) as fp16 of M - 1 (32 B per pixel), so the good matches, M near 1,
+// keep 3-4 more bits than fp16(M) would: exactly 999 (M16 = 1000 = 1/1e-3 in
+// double) when the score is undefined or certainly clamped (s_f < 0.99e-3),
+// otherwise fp16(min(1/max(s_f, 1e-3), 999.5) - 1), so M16 = 1000 always
+// means "exact". With M16 = 1 + h (exact in FP32):
+//   |M16 - M| <= kMA |M16 - 1| + kMB M16
+// (fp16 rounding of M - 1 and the 999.5 cap: 5.02e-4; the FP32 score's 5 ulp,
+// the 1-ulp reciprocal and the FP32 subtraction: < 1e-6 M), used by the
+// re-pick filter's error bars.
+constexpr float kMA = 5.1e-4f, kMB = 2e-6f;
 typedef __half wscore_t;
 __device__ __forceinline__ unsigned short m_code(float s) {
-  if (!(s >= 0.99e-3f)) return __half_as_ushort(__float2half_rn(1000.f));
-  float r;  // 1 ulp reciprocal of a normal number: negligible next to fp16 rounding
+  if (!(s >= 0.99e-3f)) return __half_as_ushort(__float2half_rn(999.f));
+  float r;  // 1 ulp reciprocal of a normal number
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaxf(s, 1e-3f)));
-  return __half_as_ushort(__float2half_rn(fminf(r, 999.5f)));
+  return __half_as_ushort(__float2half_rn(fminf(r, 999.5f) - 1.f));
 }
-// Two m_codes in one packed conversion (bit-identical to m_code: 1000 and the
-// capped reciprocal convert exactly as there).
+// Two m_codes in one packed conversion (bit-identical to m_code: 999 and the
+// capped reciprocal minus 1 convert exactly as there).
 __device__ __forceinline__ float m_value(float s) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaxf(s, 1e-3f)));
-  return s >= 0.99e-3f ? fminf(r, 999.5f) : 1000.f;
+  return s >= 0.99e-3f ? fminf(r, 999.5f) - 1.f : 999.f;
 }
 __device__ __forceinline__ uint32_t pack_m2(float s0, float s1) {
   const __half2 h = __floats2half2_rn(m_value(s0), m_value(s1));
