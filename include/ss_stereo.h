@@ -284,8 +284,10 @@ ss_status ss_ctx_set_lr_check(ss_ctx* ctx, int32_t enable, int32_t max_diff);
  * 0 luma, 1 stats+planes, 2 cost sweep/WTA (k_wta11), 3 FP64 resolve,
  * 4 cleanup, 5 refine, 6 cloud; kernel groups nested inside them:
  * 7 outlier removal, 8 radial fill, 9 disc fill (inside 4), 10 refine row
- * prefix scans, 11 gather + re-pick (k_d_repick), 12 exact re-picks (inside
- * 5), 13 normals (inside 6). Timing is off by default. */
+ * prefix scans, 11 gather + re-picks (k_d_gather + k_repick_list; iteration 0:
+ * k_d_repick), 12 exact re-picks of iteration 0 (inside 5), 13 normals
+ * (inside 6). Timing is off by default; with timing on the batch chain is
+ * launched kernel by kernel instead of as one CUDA graph. */
 #define SS_N_STAGES 14
 ss_status ss_ctx_enable_timing(ss_ctx* ctx, int32_t on);
 /* Sums (ms) and launch counts per stage since the last reset; synchronizes. */

@@ -14,6 +14,6 @@ python scripts/bench_summary.py gpurun_out/bench_${TAG}*.json
 [ -x scripts/pipe_rates ] && scripts/pipe_rates > gpurun_out/pipe_rates_${TAG}.json
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
     python bench.py --frames 16 --batch 16 --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 0 --streams 1 --no-extensions > /dev/null 2>&1; echo "ncu list rc=$?"
-bash scripts/profile_k.sh ${TAG} k_d_gather:3 k_repick_list:3 k_d_repick:0 k_wta11:1 k_disc_sum:3 \
-    k_cloud_normals:1 k_scan_b:3 k_edge_words:3 k_outlier_words:3 k_fill_radial_list:3
+bash scripts/profile_k.sh ${TAG} k_d_gather:3 k_repick_list:3 k_d_repick:0 k_wta11:1 k_disc_sum:3 "^k_scan_b$":3 \
+    k_cloud_normals:1 k_edge_words:3 k_outlier_words:3 k_fill_radial_list:3
 python scripts/launch_shares.py gpurun_out/launches_${TAG}.csv > gpurun_out/launch_shares_${TAG}.md
