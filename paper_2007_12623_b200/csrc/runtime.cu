@@ -763,8 +763,8 @@ struct ss_ctx {
   }
 
   // Whole run_stereo_only chain on device inputs (in_l/in_r hold the frames).
-  // The batch chain (~80 launches) as one CUDA graph: the first call of a
-  // configuration runs directly (buffers sized, tables uploaded); later calls
+  // The batch chain (~80 launches) as one CUDA graph: the first calls of a
+  // configuration run directly (buffers sized, tables uploaded); later calls
   // capture the same launch sequence on the ctx stream, update the cached
   // executable graph in place (same topology, new pointers / parameters) and
   // launch it. Stage timing (events) and any capture failure run directly.
@@ -791,7 +791,9 @@ struct ss_ctx {
       if (graph_exec) cudaGraphExecDestroy(graph_exec);
       graph_exec = nullptr;
     }
-    if (!use_graphs || timing || graph_key_runs++ == 0) {
+    // the first two calls of a configuration run directly: the host batch API
+    // alternates two slot buffer sets, each sized on its first use
+    if (!use_graphs || timing || graph_key_runs++ < 2) {
       run_chain_direct(n, W, H, in_format, dl, dr, flags_out);
       return;
     }
