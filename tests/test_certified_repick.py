@@ -65,3 +65,34 @@ def test_certificates_skip_most_repicks(ss):
     valid = int(out["valid"].sum())
     later = valid * (p["refine_iterations"] - 1)  # (pixel, iteration) pairs after iteration 0
     assert 0 < st["refine_scored"] < 0.05 * later, (st, later)
+
+
+def test_graph_chain_matches_direct_launches(ss, monkeypatch):
+    """The batch chain launched as a captured CUDA graph (from the third call
+    of a configuration) returns what the kernel-by-kernel launches return."""
+    from paper_2007_12623_b200.synth import as_rgb, default_rig, params_for, stereo_pair
+    frames = [stereo_pair("textured", 320, 192, 32, seed=s)[:2] for s in (5, 6)]
+    left = np.stack([as_rgb(l) for l, _ in frames])
+    right = np.stack([as_rgb(r) for _, r in frames])
+    p = params_for(32)
+    rig = default_rig(320, 192)
+    flags = ss.SS_OUT_DISPARITY | ss.SS_OUT_CLOUD
+
+    def run(no_graphs):
+        if no_graphs:
+            monkeypatch.setenv("SS_NO_GRAPHS", "1")
+        else:
+            monkeypatch.delenv("SS_NO_GRAPHS", raising=False)
+        ctx = ss.StereoContext(max_w=320, max_h=192, max_batch=2, params=p, rig=rig)
+        try:
+            outs = [ctx.run(left, right, out_flags=flags) for _ in range(4)]
+            return outs, ctx.stats()["graph_launches"]
+        finally:
+            ctx.close()
+
+    direct, g0 = run(True)
+    graphed, g1 = run(False)
+    assert g0 == 0 and g1 >= 1, (g0, g1)
+    for o in direct + graphed:
+        for k in direct[0]:
+            assert np.array_equal(o[k], direct[0][k]), k
