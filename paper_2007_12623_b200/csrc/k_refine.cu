@@ -907,17 +907,17 @@ void launch_d_repick(const double* psumT, const uint8_t* mT, const int* cntT,
 
 // ---- certified path (window 11, radius 15 tile): gather + listed re-picks ----
 //
-// k_d_gather: the b-disc gather, d = clamp(avg - avg(b)) stored for every
-// masked pixel, and the pixel listed for a re-pick unless d falls inside its
-// certificate interval (iteration 0: every masked pixel). k_repick_list: one
-// thread per listed pixel (score window read from the global BT planes), the
-// interval of the new pick stored, exact settles done by the whole warp
-// in place (no deferred list, no extra launch).
-template <bool USE_SO>
+// Iterations >= 1 (iteration 0 is k_d_repick, which stores the first
+// certificates). k_d_gather: the b-disc gather, d = clamp(S_o / cnt -
+// avg(b)) stored for every masked pixel, and the pixel listed for a re-pick
+// unless d falls inside its certificate interval. k_repick_list: one thread
+// per listed pixel (score window read from the global BT planes), the
+// interval of the new pick stored, the block's exact settles spread over its
+// warps (no deferred list, no extra launch).
 __global__ void __launch_bounds__(kThreads, 3)
     k_d_gather(const double* __restrict__ psumT, const uint8_t* __restrict__ mT,
-               const int* __restrict__ cntT, const double* __restrict__ avgT,
-               const int* __restrict__ soT, const float2* __restrict__ ivT,
+               const int* __restrict__ cntT, const int* __restrict__ soT,
+               const float2* __restrict__ ivT,
                double* __restrict__ dT, int* __restrict__ list, unsigned* __restrict__ list_count,
                RefineArgs a, const __grid_constant__ CUtensorMap map) {
   constexpr int RF = 15;
@@ -933,22 +933,17 @@ __global__ void __launch_bounds__(kThreads, 3)
   const unsigned npx = ncols * 32;
   const long e0 = f * bs + ((long)rb * W + u0) * 32;
   const size_t tb = tile_bytes<double>(RF);
-  double* s_av = reinterpret_cast<double*>(smem + tb);
-  int* s_so = reinterpret_cast<int*>(s_av);
-  float2* s_iv = reinterpret_cast<float2*>(s_av + kTilePx);
-  int* s_cnt = reinterpret_cast<int*>(s_iv + kTilePx);
+  float2* s_iv = reinterpret_cast<float2*>(smem + tb);
+  int* s_so = reinterpret_cast<int*>(s_iv + kTilePx);
+  int* s_cnt = s_so + kTilePx;
   uint8_t* s_m = reinterpret_cast<uint8_t*>(s_cnt + kTilePx);
-  const unsigned extra = npx * (USE_SO ? 4 + 8 : 8) + npx * 4 + npx;
+  const unsigned extra = npx * (4 + 8 + 4 + 1);
   const Tile<double> P = tile_issue<RF>(reinterpret_cast<double*>(smem),
                                         psumT + f * bt_frame(W, H, 1 + RF), &map, W, RF, false,
                                         &bar, extra);
   if (lane == 0 && warp == 0) {
-    if (USE_SO) {
-      bulk_g2s(s_so, soT + e0, npx * 4, &bar);
-      bulk_g2s(s_iv, ivT + e0, npx * 8, &bar);
-    } else {
-      bulk_g2s(s_av, avgT + e0, npx * 8, &bar);
-    }
+    bulk_g2s(s_iv, ivT + e0, npx * 8, &bar);
+    bulk_g2s(s_so, soT + e0, npx * 4, &bar);
     bulk_g2s(s_cnt, cntT + e0, npx * 4, &bar);
     bulk_g2s(s_m, mT + e0, npx, &bar);
   }
@@ -965,24 +960,23 @@ __global__ void __launch_bounds__(kThreads, 3)
       const double s = disc_sum_any<RF>(P, a.span, W, H, u, v, RF);
       const double c = (double)s_cnt[slot];
       const double bav = __ddiv_rn(s, c);
-      const double a_o = USE_SO ? __ddiv_rn((double)s_so[slot], c) : s_av[slot];
+      // avg = S_o / c: with integer o the reference's double disc sum is
+      // exact, so the integer sum reproduces it bit for bit
+      const double a_o = __ddiv_rn((double)s_so[slot], c);
       const double x = __dsub_rn(a_o, bav);
       const double dv = x < a.lo ? a.lo : (a.hi < x ? a.hi : x);  // std::clamp
       dT[f * bs + px] = dv;
-      if (USE_SO) {
-        const float2 iv = s_iv[slot];
-        need = !((double)iv.x <= dv && dv <= (double)iv.y);
-      }
+      const float2 iv = s_iv[slot];
+      need = !((double)iv.x <= dv && dv <= (double)iv.y);
     }
-    // iteration 0 re-picks every masked pixel: the list kernel walks the mask
-    if (USE_SO) warp_append(list + f * bs, list_count + f, need, (int)px);
+    warp_append(list + f * bs, list_count + f, need, (int)px);
   }
 }
 
 template <bool USE_SO>
 __global__ void __launch_bounds__(256)
     k_repick_list(const int* __restrict__ list, const unsigned* __restrict__ list_count,
-                  const uint8_t* __restrict__ mT, const double* __restrict__ dT,
+                  const double* __restrict__ dT,
                   int* __restrict__ oT,
                   const uint8_t* __restrict__ lgray, const uint8_t* __restrict__ rgray,
                   const wscore_t* __restrict__ win, const int* __restrict__ wbase,
@@ -991,8 +985,7 @@ __global__ void __launch_bounds__(256)
   const long f = blockIdx.y;
   const int W = a.g.W, H = a.g.H, half = a.g.half;
   const long bs = bt_frame(W, H, 0);
-  // list == nullptr (iteration 0): every masked pixel, in BT order
-  const unsigned n = list ? list_count[f] : (unsigned)bs;
+  const unsigned n = list_count[f];
   const int lane = threadIdx.x & 31;
   const uint8_t* L = lgray + f * gray_stride;
   const uint8_t* R = rgray + f * gray_stride;
@@ -1020,14 +1013,8 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) q_n = 0;
     __syncthreads();
     const unsigned i = b0 + threadIdx.x;
-    bool act = i < n;
-    int px = 0;
-    if (list) {
-      if (act) px = list[f * bs + i];
-    } else {
-      px = (int)i;
-      act = act && mT[f * bs + i];
-    }
+    const bool act = i < n;
+    const int px = act ? list[f * bs + i] : 0;
     n_scored += __popc(__ballot_sync(0xffffffffu, act));
     int v, u;
     bt_decode(W, px, v, u);
@@ -1114,47 +1101,34 @@ bool certified_repick_ok(const RefineArgs& a, bool has_win) {
          use_tile<double>(15, (size_t)kTilePx * (8 + 8 + 4 + 1));
 }
 
-void launch_d_gather(const double* psumT, const uint8_t* mT, const int* cntT, const double* avgT,
-                     const int* soT, const float2* ivT, double* dT, int* list,
-                     unsigned* list_count, const RefineArgs& a, int frames, cudaStream_t s) {
+void launch_d_gather(const double* psumT, const uint8_t* mT, const int* cntT, const int* soT,
+                     const float2* ivT, double* dT, int* list, unsigned* list_count,
+                     const RefineArgs& a, int frames, cudaStream_t s) {
   if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
   CUtensorMap map;
   if (!psum_map(&map, psumT, a, frames, true))
     throw std::runtime_error("k_d_gather: TMA tensor map rejected");
-  const size_t smem = tile_bytes<double>(15) + (size_t)kTilePx * (8 + 8 + 4 + 1);
+  const size_t smem = tile_bytes<double>(15) + (size_t)kTilePx * (8 + 4 + 4 + 1);
   static bool configured = false;
   if (!configured) {
-    set_smem(k_d_gather<false>, smem);
-    set_smem(k_d_gather<true>, smem);
+    set_smem(k_d_gather, smem);
     configured = true;
   }
   dim3 grid((a.g.W + kTC - 1) / kTC, (a.g.H + 31) / 32, frames);
-  dim3 bl(32, kTWarps);
-  if (avgT) k_d_gather<false><<<grid, bl, smem, s>>>(psumT, mT, cntT, avgT, soT, ivT, dT, list,
-                                                    list_count, a, map);
-  else k_d_gather<true><<<grid, bl, smem, s>>>(psumT, mT, cntT, avgT, soT, ivT, dT, list,
-                                              list_count, a, map);
+  k_d_gather<<<grid, dim3(32, kTWarps), smem, s>>>(psumT, mT, cntT, soT, ivT, dT, list,
+                                                   list_count, a, map);
 }
 
-void launch_repick_list(const int* list, const unsigned* list_count, const uint8_t* mT,
-                        const double* dT, int* oT,
+void launch_repick_list(const int* list, const unsigned* list_count, const double* dT, int* oT,
                         const uint8_t* lgray, const uint8_t* rgray, const wscore_t* win,
                         const int* wbase, float2* ivT, int2* chg, unsigned* chg_count,
-                        const RefineArgs& a, int frames, long gray_stride, bool all_pixels,
+                        const RefineArgs& a, int frames, long gray_stride,
                         unsigned long long* counters, cudaStream_t s) {
   if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
-  // all_pixels (iteration 0, list == nullptr): the whole mask; later lists
-  // hold a few percent of it
-  const int blocks = all_pixels ? 4 * 148 : 148;
-  if (all_pixels) list = nullptr;
-  if (chg)
-    k_repick_list<true><<<dim3(blocks, frames), 256, 0, s>>>(list, list_count, mT, dT, oT,
-                                                             lgray, rgray, win, wbase, ivT, chg,
-                                                             chg_count, a, gray_stride, counters);
-  else
-    k_repick_list<false><<<dim3(blocks, frames), 256, 0, s>>>(list, list_count, mT, dT, oT,
-                                                              lgray, rgray, win, wbase, ivT, chg,
-                                                              chg_count, a, gray_stride, counters);
+  // the lists hold a few percent of the pixels
+  k_repick_list<true><<<dim3(148, frames), 256, 0, s>>>(list, list_count, dT, oT, lgray, rgray,
+                                                        win, wbase, ivT, chg, chg_count, a,
+                                                        gray_stride, counters);
 }
 
 // Deferred re-picks: one warp per pixel, lane k scores candidate c_lo + k in

@@ -638,11 +638,11 @@ struct ss_ctx {
       // gather + re-pick kernel, which also stores the certificates
       if (cert && !avgp) {
         Stage sp(this, 11);
-        launch_d_gather(psum.as<double>(), mT, cnt.as<int>(), avgp, so.as<int>(),
-                        ivb.as<float2>(), d.as<double>(), rlist.as<int>(), lcount, a, n, stream);
-        launch_repick_list(rlist.as<int>(), lcount, mT, d.as<double>(), op, gray_l.as<uint8_t>(),
+        launch_d_gather(psum.as<double>(), mT, cnt.as<int>(), so.as<int>(), ivb.as<float2>(),
+                        d.as<double>(), rlist.as<int>(), lcount, a, n, stream);
+        launch_repick_list(rlist.as<int>(), lcount, d.as<double>(), op, gray_l.as<uint8_t>(),
                            gray_r.as<uint8_t>(), winp, wbase.as<int>(), ivb.as<float2>(), chgp,
-                           chgc, a, n, N, avgp != nullptr, ctr() + 1, stream);
+                           chgc, a, n, N, ctr() + 1, stream);
         stats.kernel_launches += 2;
         return;
       }

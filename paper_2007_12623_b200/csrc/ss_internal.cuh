@@ -299,18 +299,17 @@ void launch_repick_exact(const Deferred* defer, const unsigned* defer_count, int
                          unsigned long long* counters, cudaStream_t s);
 // Certified re-pick path (window 11, smoothing radius 15, TMA tile): the
 // gather stores d and lists the pixels whose d left their certificate
-// interval ivT (float2 BT; iteration 0, avgT != nullptr: every masked pixel);
+// interval ivT (float2 BT; iteration 0's k_d_repick stores the first ones);
 // the list kernel re-picks them, stores their new intervals and settles
-// ambiguous ones exactly inside the warp.
+// ambiguous ones exactly inside the block.
 bool certified_repick_ok(const RefineArgs& a, bool has_win);
-void launch_d_gather(const double* psumT, const uint8_t* mT, const int* cntT, const double* avgT,
-                     const int* soT, const float2* ivT, double* dT, int* list,
-                     unsigned* list_count, const RefineArgs& a, int frames, cudaStream_t s);
-void launch_repick_list(const int* list, const unsigned* list_count, const uint8_t* mT,
-                        const double* dT, int* oT,
+void launch_d_gather(const double* psumT, const uint8_t* mT, const int* cntT, const int* soT,
+                     const float2* ivT, double* dT, int* list, unsigned* list_count,
+                     const RefineArgs& a, int frames, cudaStream_t s);
+void launch_repick_list(const int* list, const unsigned* list_count, const double* dT, int* oT,
                         const uint8_t* lgray, const uint8_t* rgray, const wscore_t* win,
                         const int* wbase, float2* ivT, int2* chg, unsigned* chg_count,
-                        const RefineArgs& a, int frames, long gray_stride, bool all_pixels,
+                        const RefineArgs& a, int frames, long gray_stride,
                         unsigned long long* counters, cudaStream_t s);
 // S_o += delta over the disc of every changed pixel (exact integers).
 void launch_so_update(const int2* chg, const unsigned* chg_count, const uint8_t* mT, int* soT,
