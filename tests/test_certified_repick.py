@@ -33,6 +33,9 @@ def bits(a):
     ("lowtex", -0.02, 0.3, 0, 31),      # negative eta: E < 0, slopes reversed
     ("textured", 0.05, 0.0, 0, 31),
     ("textured", 0.01, 0.1, 4, 20),     # clamps at d_min - 5 / d_max + 5 bind
+    ("lowtex", 0.5, 1.0, 0, 31),        # steep smoothness term, alpha = 1
+    ("textured", -0.5, 0.0, 0, 31),     # steep negative eta: costs can turn negative
+    ("lowtex", 1e-6, 0.1, -8, 23),      # near-flat slopes, negative disparities
 ])
 def test_certified_trace_bit_exact(ss, orc, kind, eta, alpha, dmin, dmax):
     from paper_2007_12623_b200.synth import params_for, stereo_pair
