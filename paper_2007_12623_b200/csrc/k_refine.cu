@@ -1126,7 +1126,7 @@ void launch_repick_list(const int* list, const unsigned* list_count, const doubl
                         unsigned long long* counters, cudaStream_t s) {
   if (a.g.W <= 0 || a.g.H <= 0 || frames <= 0) return;
   // the lists hold a few percent of the pixels
-  k_repick_list<true><<<dim3(148, frames), 256, 0, s>>>(list, list_count, dT, oT, lgray, rgray,
+  k_repick_list<true><<<dim3(48, frames), 256, 0, s>>>(list, list_count, dT, oT, lgray, rgray,
                                                         win, wbase, ivT, chg, chg_count, a,
                                                         gray_stride, counters);
 }
